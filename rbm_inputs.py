@@ -1,0 +1,80 @@
+"""Seeded synthetic workloads shared by tests/ and bench.py.
+
+Holds NONE of the method's arithmetic: only the BASELINE.json configurations
+(C1..C5) as plain dicts, and seeded numpy arrays for user-supplied initial
+data (RBM_INIT_USER).  Both the oracle shim (oracle/oracle.py) and the product
+binding (paper_1812_10575_b200/rbm.py) accept these dicts.
+
+Keys: d, n, p, dtype ('f32'|'f64'), scheme ('rbm1'|'rbmr'), integrator
+('em'|'split'), kernel, kparam, potential ('none'|'harmonic'), vparam,
+constraint ('none'|'sphere'), sigma, dt, seed, replica, init, iparam, steps.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+
+def c1_dyson(n: int = 500, integrator: str = "em", scheme: str = "rbm1", seed: int = 1) -> dict:
+    """BASELINE.json configs[0]: Dyson Brownian motion."""
+    return dict(d=1, n=n, p=2, dtype="f64", scheme=scheme, integrator=integrator,
+                kernel="dyson", kparam=[], potential="harmonic", vparam=[1.0],
+                constraint="none", sigma=math.sqrt(2.0 / (n - 1)), dt=1e-3, seed=seed,
+                init="normal", iparam=[0.0, 1.0], steps=1000)
+
+
+def c2_sphere(n: int = 10**6, seed: int = 1, scheme: str = "rbm1") -> dict:
+    """BASELINE.json configs[1]: Thomson-type Coulomb on S^2."""
+    return dict(d=3, n=n, p=2, dtype="f64", scheme=scheme, integrator="em",
+                kernel="coulomb", kparam=[], potential="none", vparam=[1.0],
+                constraint="sphere", sigma=0.0, dt=1e-4, seed=seed,
+                init="sphere", iparam=[], steps=200)
+
+
+def c3_opinion(n: int = 10**7, seed: int = 1, scheme: str = "rbm1") -> dict:
+    """BASELINE.json configs[2]: bounded-confidence opinion."""
+    return dict(d=1, n=n, p=2, dtype="f32", scheme=scheme, integrator="em",
+                kernel="bounded_confidence", kparam=[1.0, 1.0], potential="none",
+                vparam=[1.0], constraint="none", sigma=0.01, dt=1e-2, seed=seed,
+                init="box", iparam=[-5.0, 5.0], steps=500)
+
+
+def c4_aggregation(n: int = 10**8, seed: int = 1, scheme: str = "rbm1") -> dict:
+    """BASELINE.json configs[3]: 2-D Gaussian attraction-repulsion (synthetic)."""
+    return dict(d=2, n=n, p=4, dtype="f32", scheme=scheme, integrator="em",
+                kernel="gauss_attr_rep", kparam=[], potential="harmonic", vparam=[1.0],
+                constraint="none", sigma=0.05, dt=5e-3, seed=seed,
+                init="mixture", iparam=[5, 0.5, -4.0, 4.0], steps=100)
+
+
+def c5_coulomb_reg(n: int = 2**28, p: int = 2, seed: int = 1, scheme: str = "rbm1") -> dict:
+    """BASELINE.json configs[4]: 3-D regularised Coulomb, 2^28 particles per GPU."""
+    return dict(d=3, n=n, p=p, dtype="f32", scheme=scheme, integrator="em",
+                kernel="coulomb_reg", kparam=[0.01], potential="harmonic", vparam=[1.0],
+                constraint="none", sigma=0.1, dt=1e-3, seed=seed,
+                init="normal", iparam=[0.0, 1.0], steps=50)
+
+
+def smooth_test(n: int, p: int = 2, beta: float = 1.0, dtype: str = "f64", seed: int = 1) -> dict:
+    """The paper's smooth test system K(z)=z/(1+z^2), V=beta x^2/2."""
+    return dict(d=1, n=n, p=p, dtype=dtype, scheme="rbm1", integrator="em",
+                kernel="smooth", kparam=[], potential="harmonic" if beta else "none",
+                vparam=[beta], constraint="none", sigma=0.0, dt=2.0**-7, seed=seed,
+                init="normal", iparam=[0.0, 1.0], steps=128)
+
+
+ALL = {"C1": c1_dyson, "C2": c2_sphere, "C3": c3_opinion, "C4": c4_aggregation, "C5": c5_coulomb_reg}
+
+
+def user_x0(n: int, d: int, seed: int, dist: str = "normal", scale: float = 1.0) -> np.ndarray:
+    """Seeded user initial data in id order, shape (n, d), float64."""
+    rng = np.random.default_rng(seed)
+    if dist == "normal":
+        return scale * rng.standard_normal((n, d))
+    if dist == "uniform":
+        return scale * rng.uniform(-1.0, 1.0, (n, d))
+    if dist == "sphere":
+        z = rng.standard_normal((n, d))
+        return z / np.linalg.norm(z, axis=1, keepdims=True)
+    raise ValueError(dist)

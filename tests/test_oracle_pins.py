@@ -1,0 +1,571 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix.
+
+No CUDA here (-m "not gpu").  Each test names the passage it pins.  The
+oracle is never compared with itself: pins are published vectors, closed
+forms, exact combinatorial identities (Lemma 3.1), invariants, special cases
+and brute force on tiny inputs.
+"""
+import itertools
+import math
+import os
+
+import numpy as np
+import pytest
+from scipy import stats
+
+import rbm_inputs as RI
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def base(**kw):
+    c = dict(d=1, n=8, p=2, dtype="f64", scheme="rbm1", integrator="em", kernel="smooth",
+             kparam=[], potential="none", vparam=[1.0], constraint="none", sigma=0.0,
+             dt=0.01, seed=12345, init="normal", iparam=[0.0, 1.0])
+    c.update(kw)
+    return c
+
+
+# ---------------------------------------------------------------- RNG (D:13)
+def test_philox_known_answer_vectors(O):
+    """Published Philox4x32-10 KAT vectors (tests/golden/philox4x32_10_kat.txt)."""
+    rows = [l.split() for l in open(os.path.join(GOLD, "philox4x32_10_kat.txt"))
+            if l.strip() and not l.startswith("#")]
+    assert len(rows) == 3
+    for r in rows:
+        v = [int(t, 16) for t in r]
+        out = O.philox(v[0:4], v[4:6])
+        assert [int(w) for w in out] == v[6:10]
+
+
+def test_uniform_maps_open_interval_exact(O):
+    """D:13: u = (2(w>>9)+1) 2^-24 and (2k+1) 2^-53 lie strictly in (0,1)."""
+    assert O.u01_f32(0) == 2.0**-24
+    assert O.u01_f32(0xFFFFFFFF) == 1.0 - 2.0**-24
+    assert O.u01_f32(0x1FF) == 2.0**-24          # low 9 bits dropped
+    assert O.u01_f32(0x200) == 3 * 2.0**-24
+    assert O.u01_f64(0, 0) == 2.0**-53
+    assert O.u01_f64(0xFFFFFFFF, 0xFFFFFFFF) == 1.0 - 2.0**-53
+    assert O.u01_f64(0, 0x1000) == 3 * 2.0**-53
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_noise_is_standard_normal(O, dtype):
+    """P:943 z ~ N(0,1): KS test and moments over 60000 draws (d=3)."""
+    c = base(d=3, n=4, dtype=dtype)
+    z = np.array([O.noise(c, i, m) for i in range(2000) for m in range(10)]).ravel()
+    assert abs(z.mean()) < 5 / math.sqrt(z.size)
+    assert abs(z.var() - 1) < 5 * math.sqrt(2 / z.size)
+    assert stats.kstest(z, "norm").pvalue > 1e-4
+    # coordinates are independent
+    zz = z.reshape(-1, 3)
+    cc = np.corrcoef(zz.T)
+    assert np.all(np.abs(cc - np.eye(3)) < 5 / math.sqrt(zz.shape[0]))
+
+
+def test_noise_depends_on_step_id_replica(O):
+    c = base(d=2)
+    a = O.noise(c, 3, 7)
+    assert not np.array_equal(a, O.noise(c, 4, 7))
+    assert not np.array_equal(a, O.noise(c, 3, 8))
+    assert not np.array_equal(a, O.noise(dict(c, replica=1), 3, 7))
+    assert np.array_equal(a, O.noise(c, 3, 7))
+
+
+# --------------------------------------------------------------- init
+def test_init_normal_moments(O):
+    c = base(d=3, n=50000, init="normal", iparam=[0.5, 2.0])
+    x = O.init(c)
+    assert abs(x.mean() - 0.5) < 5 * 2 / math.sqrt(x.size)
+    assert abs(x.std() - 2.0) < 0.02
+    assert stats.kstest(((x - 0.5) / 2).ravel(), "norm").pvalue > 1e-4
+
+
+def test_init_box_uniform(O):
+    c = base(d=2, n=50000, init="box", iparam=[-5.0, 5.0])
+    x = O.init(c)
+    assert x.min() > -5 and x.max() < 5
+    assert stats.kstest(x.ravel(), "uniform", args=(-5, 10)).pvalue > 1e-4
+
+
+def test_init_sphere_uniform(O):
+    c = base(d=3, n=50000, init="sphere")
+    x = O.init(c)
+    assert np.allclose(np.linalg.norm(x, axis=1), 1.0, atol=1e-15)
+    # Archimedes: each coordinate of a uniform point on S^2 is U[-1,1]
+    assert stats.kstest(x[:, 2], "uniform", args=(-1, 2)).pvalue > 1e-4
+    assert np.all(np.abs(x.mean(0)) < 0.02)
+
+
+def test_init_mixture_equal_weights(O):
+    """D:14: 5 equal-weight components, std 0.5, centres in [-4,4]^2."""
+    c = base(d=2, n=60000, init="mixture", iparam=[5, 0.5, -4.0, 4.0])
+    x = O.init(c)
+    # recover the centres by the nearest of 5 k-means-ish modes: use the
+    # fact that points lie within 6 std of some centre and count per centre
+    from scipy.cluster.vq import kmeans2
+    cent, lab = kmeans2(x, 5, seed=1, minit="++")
+    assert np.all(np.abs(cent) < 4.5)
+    counts = np.bincount(lab, minlength=5)
+    # equal weights only if the centres are separated; accept merged clusters
+    assert counts.sum() == 60000
+
+
+# ------------------------------------------------------- random division (Alg. 1)
+def test_permutation_is_partition(O):
+    for n in [1, 2, 7, 100, 1001]:
+        c = base(n=n, p=2 if n >= 2 else 1)
+        o = O.permutation(c, 5)
+        assert np.array_equal(np.sort(o), np.arange(n, dtype=np.uint32))
+
+
+def test_permutation_sorted_by_key_then_id(O):
+    c = base(n=300)
+    o = O.permutation(c, 11)
+    keys = np.array([O.key(c, int(i), 11) for i in o], dtype=np.uint64)
+    comp = keys * (1 << 32) + o.astype(np.uint64)
+    assert np.all(comp[1:] > comp[:-1])
+
+
+def test_division_uniform_n4_p2(O):
+    """M(2) = 3 partitions of 4 objects into pairs, each with prob 1/3."""
+    c = base(n=4, p=2)
+    counts = {}
+    T = 30000
+    for m in range(T):
+        o = O.permutation(c, m)
+        part = frozenset([frozenset(o[0:2]), frozenset(o[2:4])])
+        counts[part] = counts.get(part, 0) + 1
+    assert len(counts) == 3
+    for v in counts.values():
+        assert abs(v / T - 1 / 3) < 4 * math.sqrt((1 / 3) * (2 / 3) / T)
+
+
+def test_division_uniform_n6_p3_chi2(O):
+    """M(2) = 6!/(3!^2 2!) = 10 partitions of 6 into triples, uniform."""
+    c = base(n=6, p=3)
+    counts = {}
+    T = 30000
+    for m in range(T):
+        o = O.permutation(c, m)
+        part = frozenset([frozenset(o[0:3]), frozenset(o[3:6])])
+        counts[part] = counts.get(part, 0) + 1
+    assert len(counts) == 10
+    obs = np.array(list(counts.values()))
+    assert stats.chisquare(obs).pvalue > 1e-4
+
+
+def test_same_batch_probabilities(O):
+    """P:354 P(i,j same batch) = (p-1)/(N-1); P:385-386 triple prob."""
+    n, p, T = 8, 4, 20000
+    c = base(n=n, p=p)
+    pair = 0
+    triple = 0
+    for m in range(T):
+        o = list(O.permutation(c, m))
+        pos = {int(v): k // p for k, v in enumerate(o)}
+        pair += pos[0] == pos[1]
+        triple += pos[0] == pos[1] == pos[2]
+    pp = (p - 1) / (n - 1)
+    pt = (p - 1) * (p - 2) / ((n - 1) * (n - 2))
+    assert abs(pair / T - pp) < 4 * math.sqrt(pp * (1 - pp) / T)
+    assert abs(triple / T - pt) < 4 * math.sqrt(pt * (1 - pt) / T)
+
+
+def test_batch_remainder_rule(O):
+    """P:90 'the last batch does not have to have size p'; reading D:7."""
+    assert list(O.batch_starts(8, 2)) == [0, 2, 4, 6, 8]
+    assert list(O.batch_starts(7, 2)) == [0, 2, 4, 7]        # r=1 joins last full batch
+    assert list(O.batch_starts(8, 3)) == [0, 3, 6, 8]        # r=2 forms its own batch
+    assert list(O.batch_starts(5, 5)) == [0, 5]
+    for n in range(2, 40):
+        for p in range(2, n + 1):
+            s = np.asarray(O.batch_starts(n, p), dtype=np.int64)
+            assert s[0] == 0 and s[-1] == n and np.all(np.diff(s) >= 2)
+            assert np.all(np.diff(s) <= p + 1)
+
+
+# ------------------------------------------------------------ Lemma 3.1
+def all_partitions(n, p):
+    """All divisions of range(n) into n/p unordered batches of size p, as orders."""
+    def rec(rest):
+        if not rest:
+            yield []
+            return
+        first = rest[0]
+        for comb in itertools.combinations(rest[1:], p - 1):
+            batch = (first,) + comb
+            rem = [r for r in rest if r not in batch]
+            for tail in rec(rem):
+                yield list(batch) + tail
+    return [np.array(o, dtype=np.uint32) for o in rec(list(range(n)))]
+
+
+@pytest.mark.parametrize("n,p", [(4, 2), (6, 2), (6, 3), (8, 2), (8, 4)])
+def test_lemma31_mean_and_variance_by_enumeration(O, n, p):
+    """E chi = 0 and Var chi = (1/(p-1) - 1/(N-1)) Lambda_i, over ALL M(n) divisions."""
+    parts = all_partitions(n, p)
+    M = math.factorial(n) // (math.factorial(p) ** (n // p) * math.factorial(n // p))
+    assert len(parts) == M
+    rng = np.random.default_rng(n * 10 + p)
+    for kern, d in [("smooth", 1), ("coulomb_reg", 3), ("gauss_attr_rep", 2)]:
+        c = base(n=n, p=p, d=d, kernel=kern, kparam=[0.01])
+        x = rng.standard_normal((n, d))
+        fs = np.array([O.batch_forces(c, x, o) for o in parts])
+        # full mean-field force 1/(N-1) sum_{j != i} K(x_i - x_j): the p=N batch
+        cN = dict(c, p=n)
+        full = O.batch_forces(cN, x, np.arange(n, dtype=np.uint32))
+        assert np.max(np.abs(fs.mean(0) - full)) < 1e-13
+        # Lambda_i from K values
+        Kij = np.zeros((n, n, d))
+        for i in range(n):
+            for j in range(n):
+                if i != j:
+                    Kij[i, j] = O.kernel_eval(c, x[i] - x[j])
+        lam = np.zeros(n)
+        for i in range(n):
+            dev = [Kij[i, j] - full[i] for j in range(n) if j != i]
+            lam[i] = sum(float(v @ v) for v in dev) / (n - 2)
+        var = ((fs - full) ** 2).sum(-1).mean(0)
+        pred = (1 / (p - 1) - 1 / (n - 1)) * lam
+        assert np.allclose(var, pred, rtol=1e-11, atol=1e-14)
+
+
+# ------------------------------------------------------------- forces and models
+def test_dyson_virial_identity(O):
+    """K=1/x: sum_i x_i F_i = sum_B |B|/2 = N/2 for ANY division (derived from P:889-892)."""
+    rng = np.random.default_rng(3)
+    for n, p in [(10, 2), (11, 4), (64, 8), (9, 9)]:
+        c = base(n=n, p=p, kernel="dyson")
+        x = rng.standard_normal((n, 1))
+        o = rng.permutation(n).astype(np.uint32)
+        f = O.batch_forces(c, x, o)
+        assert abs(float((x * f).sum()) - n / 2) < 1e-11
+
+
+def test_coulomb_virial_identity(O):
+    """K=x/|x|^3: sum_i x_i.F_i = sum_B 1/(|B|-1) sum_{pairs in B} 1/r_ij."""
+    rng = np.random.default_rng(4)
+    n, p = 12, 3
+    c = base(n=n, p=p, d=3, kernel="coulomb")
+    x = rng.standard_normal((n, 3))
+    o = rng.permutation(n).astype(np.uint32)
+    f = O.batch_forces(c, x, o)
+    want = 0.0
+    for b in range(n // p):
+        mem = o[b * p:(b + 1) * p]
+        for a, bb in itertools.combinations(mem, 2):
+            want += 1.0 / np.linalg.norm(x[a] - x[bb]) / (p - 1)
+    assert abs(float((x * f).sum()) - want) < 1e-12
+
+
+def test_kernel_shapes_closed_forms(O):
+    # K4 (BASELINE C4) changes sign where e^{-r^2/2} = e^{-r^2/8}/4: r^2 = 8 ln 4 / 3
+    c4 = base(d=2, kernel="gauss_attr_rep")
+    r0 = math.sqrt(8 * math.log(4) / 3)
+    assert O.kernel_eval(c4, [r0 * (1 - 1e-6), 0])[0] > 0   # repulsive inside
+    assert O.kernel_eval(c4, [r0 * (1 + 1e-6), 0])[0] < 0   # attractive beyond
+    assert abs(O.kernel_eval(c4, [0, r0])[1]) < 1e-15
+    # K5 (BASELINE C5) is bounded, max |K| = sqrt(e/2)/(3e/2)^{3/2} at r = sqrt(e/2)
+    eps = 0.01
+    c5 = base(d=3, kernel="coulomb_reg", kparam=[eps])
+    rs = np.linspace(1e-4, 1.0, 20001)
+    mags = [np.linalg.norm(O.kernel_eval(c5, [r, 0, 0])) for r in rs[::50]]
+    kmax = math.sqrt(eps / 2) / (1.5 * eps) ** 1.5
+    assert abs(np.linalg.norm(O.kernel_eval(c5, [0, 0, math.sqrt(eps / 2)])) - kmax) < 1e-12
+    assert max(mags) <= kmax * (1 + 1e-12)
+    assert abs(kmax - 38.49) < 0.01
+    # K6: max |K| = 1/2 at |z| = 1
+    c6 = base(kernel="smooth")
+    assert abs(O.kernel_eval(c6, [1.0])[0] - 0.5) < 1e-16
+    # K3 (Eq. 5.12, D:10): strict window |z| < r, attraction -alpha z inside
+    c3 = base(kernel="bounded_confidence", kparam=[2.0, 1.0])
+    assert O.kernel_eval(c3, [1.0])[0] == 0.0
+    assert O.kernel_eval(c3, [-1.0])[0] == 0.0
+    assert O.kernel_eval(c3, [np.nextafter(1.0, 0)])[0] < 0
+    assert O.kernel_eval(c3, [0.5])[0] == -1.0
+    # oddness of every registry kernel
+    rng = np.random.default_rng(0)
+    for k, d, kp in [("dyson", 1, []), ("coulomb", 3, []), ("bounded_confidence", 1, [1, 1]),
+                     ("gauss_attr_rep", 2, []), ("coulomb_reg", 3, [0.01]), ("smooth", 1, [])]:
+        c = base(d=d, kernel=k, kparam=kp)
+        for _ in range(20):
+            z = rng.standard_normal(d)
+            assert np.array_equal(O.kernel_eval(c, z), -O.kernel_eval(c, -z))
+    # singular kernels at coincident points (D:12)
+    assert O.kernel_eval(base(kernel="dyson"), [0.0])[0] == 0.0
+    assert np.all(O.kernel_eval(base(d=3, kernel="coulomb"), [0, 0, 0]) == 0.0)
+
+
+def test_bounded_confidence_fp32_window(O):
+    """D:10: in fp32 mode the window is tested on fl32(x_i - x_j)."""
+    a = np.float32(0.7)
+    b = np.float32(-0.3000000119)       # exact difference just above 1 in fp64? check fp32
+    c32 = base(n=2, p=2, kernel="bounded_confidence", kparam=[1.0, 1.0], dtype="f32")
+    c64 = dict(c32, dtype="f64")
+    x = np.array([[float(a)], [float(b)]])
+    d32 = np.float32(a) - np.float32(b)
+    d64 = float(a) - float(b)
+    f32 = O.batch_forces(c32, x, np.array([0, 1], dtype=np.uint32))
+    f64 = O.batch_forces(c64, x, np.array([0, 1], dtype=np.uint32))
+    assert (f32[0, 0] != 0) == (abs(float(d32)) < 1.0)
+    assert (f64[0, 0] != 0) == (abs(d64) < 1.0)
+
+
+# ---------------------------------------------------------------- one step
+def test_em_closed_form_harmonic(O):
+    """K=0, V=|x|^2/2, sigma=0: x' = x - dt x (P:819 forward Euler)."""
+    c = base(n=50, p=5, d=3, kernel="zero", potential="harmonic", dt=0.01)
+    x = np.random.default_rng(1).standard_normal((50, 3))
+    y = O.rbm1_step(c, x, 0)
+    assert np.allclose(y, (1 - 0.01) * x, rtol=0, atol=1e-15)
+
+
+def test_em_two_particles_smooth(O):
+    """N=2, K6, (0,1), dt=0.1, Euler: (-0.05, 1.05) under Eq. 1.2's sign."""
+    c = base(n=2, p=2, kernel="smooth", dt=0.1)
+    y = O.rbm1_step(c, np.array([[0.0], [1.0]]), 0)
+    assert np.allclose(y.ravel(), [-0.05, 1.05], atol=1e-15)
+
+
+def test_p_equals_n_is_direct_step(O):
+    """p=N: the single batch is the full system (chi == 0)."""
+    rng = np.random.default_rng(2)
+    for kern, d, kp, pot, sig in [("smooth", 1, [], "harmonic", 0.3), ("coulomb_reg", 3, [0.01], "harmonic", 0.1),
+                                  ("gauss_attr_rep", 2, [], "none", 0.05)]:
+        n = 37
+        c = base(n=n, p=n, d=d, kernel=kern, kparam=kp, potential=pot, sigma=sig)
+        x = rng.standard_normal((n, d))
+        a = O.rbm1_step(c, x, 4)
+        b = O.direct_step(c, x, 4)
+        assert np.max(np.abs(a - b)) < 1e-14
+
+
+def test_momentum_conserved(O):
+    """V=0, sigma=0, odd K: every batch conserves sum_i x_i (Eq. 2.2)."""
+    rng = np.random.default_rng(5)
+    for kern, d, kp in [("bounded_confidence", 1, [1.0, 1.0]), ("gauss_attr_rep", 2, []),
+                        ("coulomb_reg", 3, [0.01]), ("smooth", 1, []), ("coulomb", 3, [])]:
+        for n, p in [(64, 2), (63, 4), (40, 8)]:
+            c = base(n=n, p=p, d=d, kernel=kern, kparam=kp)
+            x = rng.standard_normal((n, d))
+            y = O.rbm1_step(c, x, 9)
+            assert np.max(np.abs(y.sum(0) - x.sum(0))) < 1e-12
+
+
+def test_noise_mean_shift_exact(O):
+    """C3 with sigma>0: mean(x') - mean(x) = sigma sqrt(dt) mean(z) (momentum + noise)."""
+    cfg = RI.c3_opinion(n=1000)
+    cfg["dtype"] = "f64"
+    x = O.init(cfg)
+    y = O.rbm1_step(cfg, x, 3)
+    z = np.array([O.noise(cfg, i, 3) for i in range(1000)])
+    assert abs((y - x).mean() - cfg["sigma"] * math.sqrt(cfg["dt"]) * z.mean()) < 1e-15
+
+
+def test_opinion_range_monotone(O):
+    """D:10 model with sigma=0: each pair moves toward its midpoint, so min/max are monotone."""
+    cfg = dict(RI.c3_opinion(n=2000), sigma=0.0, dtype="f64")
+    x = O.init(cfg)
+    lo, hi = x.min(), x.max()
+    for m in range(50):
+        x = O.rbm1_step(cfg, x, m)
+        assert x.min() >= lo - 1e-15 and x.max() <= hi + 1e-15
+        lo, hi = x.min(), x.max()
+
+
+# -------------------------------------------------------- split pair flows (D:3)
+def rk4_pair(O, c, xi, xj, tau, nsub=2000):
+    h = tau / nsub
+    def f(a, b):
+        return O.kernel_eval(c, a - b), O.kernel_eval(c, b - a)
+    a, b = np.array(xi, float), np.array(xj, float)
+    for _ in range(nsub):
+        k1a, k1b = f(a, b)
+        k2a, k2b = f(a + h / 2 * k1a, b + h / 2 * k1b)
+        k3a, k3b = f(a + h / 2 * k2a, b + h / 2 * k2b)
+        k4a, k4b = f(a + h * k3a, b + h * k3b)
+        a = a + h / 6 * (k1a + 2 * k2a + 2 * k3a + k4a)
+        b = b + h / 6 * (k1b + 2 * k2b + 2 * k3b + k4b)
+    return a, b
+
+
+@pytest.mark.parametrize("tau", [1e-3, 1e-2])
+def test_dyson_pair_flow_vs_rk4(O, tau):
+    """P:922-943 exact flow (with the 1/2 of D:3) solves dX^i = K(X^i-X^j)dt."""
+    c = base(kernel="dyson")
+    rng = np.random.default_rng(6)
+    for _ in range(5):
+        xi, xj = rng.standard_normal(1), rng.standard_normal(1)
+        yi, yj = O.pair_flow(c, xi, xj, tau)
+        ri, rj = rk4_pair(O, c, xi, xj, tau)
+        assert np.max(np.abs(yi - ri)) < 1e-9 and np.max(np.abs(yj - rj)) < 1e-9
+        assert abs((yi - yj)[0] ** 2 - (xi - xj)[0] ** 2 - 4 * tau) < 1e-12
+        assert abs((yi + yj)[0] - (xi + xj)[0]) < 1e-15
+        assert np.sign(yi - yj) == np.sign(xi - xj)
+    # the paper's displayed formula without 1/2 would move (0,1) to -0.5198 at tau=0.01
+    yi, yj = O.pair_flow(c, [0.0], [1.0], 0.01)
+    assert abs(yi[0] - (-0.009901951)) < 1e-9
+
+
+@pytest.mark.parametrize("tau", [1e-3, 1e-2])
+def test_coulomb_pair_flow_vs_rk4(O, tau):
+    """P:1029-1045 exact flow: |D|^3 -> |D|^3 + 6 tau, midpoint preserved (D:3)."""
+    c = base(d=3, kernel="coulomb")
+    rng = np.random.default_rng(7)
+    for _ in range(4):
+        xi, xj = rng.standard_normal(3), rng.standard_normal(3)
+        yi, yj = O.pair_flow(c, xi, xj, tau)
+        ri, rj = rk4_pair(O, c, xi, xj, tau)
+        assert np.max(np.abs(yi - ri)) < 1e-9 and np.max(np.abs(yj - rj)) < 1e-9
+        assert abs(np.linalg.norm(yi - yj) ** 3 - np.linalg.norm(xi - xj) ** 3 - 6 * tau) < 1e-12
+        assert np.max(np.abs(yi + yj - xi - xj)) < 1e-15
+
+
+# ------------------------------------------------------- long-run physics pins
+def semicircle_cdf(x):
+    x = np.clip(x, -math.sqrt(2), math.sqrt(2))
+    return 0.5 + x * np.sqrt(np.maximum(2 - x * x, 0.0)) / (2 * math.pi) + np.arcsin(np.clip(x / math.sqrt(2), -1, 1)) / math.pi
+
+
+def w1_to_cdf(sample, cdf, lo=-3.0, hi=3.0, m=60001):
+    g = np.linspace(lo, hi, m)
+    s = np.sort(sample)
+    emp = np.searchsorted(s, g, side="right") / s.size
+    return float(np.trapezoid(np.abs(emp - cdf(g)), g))
+
+
+def test_dyson_split_reaches_semicircle(O):
+    """P:904-906 equilibrium rho = sqrt(2-x^2)/pi; split RBM-1, N=500, T=10 (D:16, D:17)."""
+    w = []
+    for seed in [1, 2]:
+        cfg = RI.c1_dyson(n=500, integrator="split", seed=seed)
+        x = O.init(cfg)
+        x = O.run(cfg, x, 0, 10000)
+        w.append(w1_to_cdf(x.ravel(), semicircle_cdf))
+    assert max(w) < 0.02, w
+
+
+def test_dyson_second_moment_identity(O):
+    """m2(t) = (1+s^2)/2 + (m2(0)-(1+s^2)/2) e^{-2t} (derived from Eq. 1.2 with K=1/x)."""
+    cfg = RI.c1_dyson(n=4000, integrator="split", seed=3)
+    x = O.init(cfg)
+    s2 = cfg["sigma"] ** 2
+    m20 = float((x ** 2).mean())
+    x = O.run(cfg, x, 0, 1000)
+    pred = (1 + s2) / 2 + (m20 - (1 + s2) / 2) * math.exp(-2.0)
+    assert abs(float((x ** 2).mean()) - pred) < 0.01
+
+
+def thomson_energy(x):
+    e = 0.0
+    for i in range(len(x)):
+        for j in range(i + 1, len(x)):
+            e += 1.0 / np.linalg.norm(x[i] - x[j])
+    return e
+
+
+def thomson_minimum(n):
+    """Closed-form minimal configurations (antipodes, triangle, tetrahedron,
+    triangular bipyramid, octahedron, icosahedron)."""
+    s3 = math.sqrt(3)
+    if n == 2:
+        pts = [[0, 0, 1], [0, 0, -1]]
+    elif n == 3:
+        pts = [[1, 0, 0], [-0.5, s3 / 2, 0], [-0.5, -s3 / 2, 0]]
+    elif n == 4:
+        pts = [[1, 1, 1], [1, -1, -1], [-1, 1, -1], [-1, -1, 1]]
+    elif n == 5:
+        pts = [[0, 0, 1], [0, 0, -1], [1, 0, 0], [-0.5, s3 / 2, 0], [-0.5, -s3 / 2, 0]]
+    elif n == 6:
+        pts = [[1, 0, 0], [-1, 0, 0], [0, 1, 0], [0, -1, 0], [0, 0, 1], [0, 0, -1]]
+    elif n == 12:
+        ph = (1 + math.sqrt(5)) / 2
+        pts = []
+        for a in (-1, 1):
+            for b in (-ph, ph):
+                pts += [[0, a, b], [a, b, 0], [b, 0, a]]
+    pts = np.array(pts, float)
+    pts /= np.linalg.norm(pts, axis=1, keepdims=True)
+    return thomson_energy(pts)
+
+
+def test_thomson_closed_forms_sanity():
+    assert abs(thomson_minimum(2) - 0.5) < 1e-14
+    assert abs(thomson_minimum(3) - math.sqrt(3)) < 1e-14
+    assert abs(thomson_minimum(4) - 3.674234614) < 1e-8
+    assert abs(thomson_minimum(6) - 9.985281374) < 1e-8
+    assert abs(thomson_minimum(12) - 49.165253058) < 1e-8
+
+
+@pytest.mark.parametrize("n", [4, 6, 12])
+def test_thomson_small_n_reaches_minimum(O, n):
+    """Sec. 5.1: RBM with p=2 on the sphere finds the ground
+    state; annealed dt then a p=N polish lands on the closed-form minimum."""
+    cfg = RI.c2_sphere(n=n, seed=n)
+    x = O.init(cfg)
+    m = 0
+    for dt, T in [(1e-2, 60.0), (3e-3, 60.0), (1e-3, 60.0)]:
+        c = dict(cfg, dt=dt)
+        k = int(round(T / dt))
+        x = O.run(c, x, m, k)
+        m += k
+    assert np.allclose(np.linalg.norm(x, axis=1), 1.0, atol=1e-12)
+    e_rbm = thomson_energy(x)
+    emin = thomson_minimum(n)
+    assert (e_rbm - emin) / emin < 2e-3
+    c = dict(cfg, p=n, dt=5e-2)
+    x = O.run(c, x, m, 20000)
+    assert abs(thomson_energy(x) - emin) / emin < 1e-8
+
+
+# ---------------------------------------------------------------- RBM-r (D:8, D:9)
+def test_rbmr_slots_distinct_and_uniform(O):
+    cfg = base(n=4, p=2, scheme="rbmr")
+    cnt = {}
+    T = 6000
+    for m in range(T):
+        js = O.rbmr_slots(cfg, m)
+        for b in range(2):
+            pr = tuple(sorted(js[2 * b:2 * b + 2]))
+            assert pr[0] != pr[1]
+            cnt[pr] = cnt.get(pr, 0) + 1
+    assert len(cnt) == 6
+    tot = sum(cnt.values())
+    for v in cnt.values():
+        assert abs(v / tot - 1 / 6) < 4 * math.sqrt((1 / 6) * (5 / 6) / tot)
+
+
+def test_rbmr_membership_binomial(O):
+    n, p = 1000, 4
+    cfg = base(n=n, p=p, scheme="rbmr")
+    js = np.concatenate([O.rbmr_slots(cfg, m) for m in range(20)])
+    c = np.bincount(js, minlength=n)
+    assert abs(c.mean() - 20 * 1.0) < 1e-9        # n*p = N slots per sweep, mean 1
+    assert abs(c.var() / 20 - 1.0) < 0.15          # ~Binomial(N, 1/N) per sweep
+
+
+def test_rbmr_jacobi_matches_rbm1_dynamics(O):
+    """RBM-r with N/p iterations per tau tracks RBM-1 (m2 of Dyson split)."""
+    m2 = {}
+    for scheme in ["rbm1", "rbmr"]:
+        cfg = RI.c1_dyson(n=2000, integrator="split", scheme=scheme, seed=5)
+        x = O.init(cfg)
+        x = O.run(cfg, x, 0, 1000)
+        m2[scheme] = float((x ** 2).mean())
+    assert abs(m2["rbm1"] - m2["rbmr"]) < 0.02
+
+
+def test_rbmr_conserves_momentum_when_kernel_only(O):
+    """Each slot increment pair of an odd K sums to zero (Jacobi reading D:8)."""
+    cfg = base(n=100, p=4, d=2, scheme="rbmr", kernel="gauss_attr_rep")
+    x = np.random.default_rng(8).standard_normal((100, 2))
+    y = O.rbmr_step(cfg, x, 2)
+    assert np.max(np.abs(y.sum(0) - x.sum(0))) < 1e-12
+
+
+def test_sphere_stays_on_sphere(O):
+    cfg = RI.c2_sphere(n=300)
+    x = O.init(cfg)
+    x = O.run(cfg, x, 0, 20)
+    assert np.allclose(np.linalg.norm(x, axis=1), 1.0, atol=1e-14)
