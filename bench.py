@@ -1,0 +1,317 @@
+#!/usr/bin/env python
+"""RBM time-step benchmark (BASELINE.json metric: particle-steps/s + HBM GB/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5] [--p 2]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+    python bench.py --impl reference          # the CPU oracle arm
+
+A "step" is one RBM-1 time step (Alg. 1) of the whole
+workload: fresh random division, intra-batch interactions, Euler-Maruyama
+update.  Default workload: BASELINE.json configs[4] (C5), 2^28 particles per
+GPU, fp32, d=3, regularised Coulomb, p=2.  At N>1 GPUs each rank advances its
+own 2^28-particle system (ensemble replicas, replica = rank; weak scaling):
+the partitioned single-system mode is not in this build.
+
+Timing: W untimed warm-up steps, then exactly K steps bracketed by a barrier
+and torch.cuda.synchronize() on both sides, measured with CUDA events on the
+library's stream, max over ranks.  The state (4.3 GB at C5) is larger than the
+126 MB L2, so no flush is needed between steps.  Per-kernel device times come
+from CUDA events the library records between its kernels in the same timed
+region (rbm_timing_begin/end).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import rbm_inputs as RI  # noqa: E402
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C5", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--p", type=int, default=None, help="batch size override (C5: 2, 8, 32)")
+    ap.add_argument("--scheme", default="rbm1", choices=["rbm1", "rbmr"])
+    ap.add_argument("--n", type=int, default=None, help="particles per GPU override")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload(args, rank: int) -> dict:
+    kw = {"scheme": args.scheme}
+    if args.n:
+        kw["n"] = args.n
+    if args.workload == "C5":
+        cfg = RI.c5_coulomb_reg(p=args.p or 2, **kw)
+    else:
+        cfg = RI.ALL[args.workload](**kw)
+        if args.p:
+            cfg["p"] = args.p
+    cfg["replica"] = rank
+    return cfg
+
+
+def elt(cfg):
+    return 8 if cfg["dtype"] == "f64" else 4
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            P = json.load(f)
+        return float(P["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def kernel_bytes(name: str, cfg: dict) -> float:
+    """Algorithmic HBM bytes per launch: what the
+    kernel must move at minimum -- R = 4 + d*s bytes per particle record."""
+    n, R = cfg["n"], 4 + cfg["d"] * elt(cfg)
+    return {"scatter_top": 2.0 * R * n, "scatter_sub": 2.0 * R * n, "bucket_step": 2.0 * R * n,
+            "hist_sub": 4.0 * n, "hist_top": 0.0}.get(name, 0.0)
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 6 and r[0].isdigit()]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = sorted(int(r[0]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[2 + k].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": int(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def cpu_baseline(cfg: dict, budget_s: float = 12.0, n_sample: int = 1 << 19) -> dict:
+    """The oracle as it stands, single-threaded, on a bounded sample of the
+    same workload (same config, N = n_sample particles)."""
+    import numpy as np
+
+    from oracle import oracle as O
+    c = dict(cfg, n=min(cfg["n"], n_sample))
+    x = O.init(c)
+    t0 = time.perf_counter()
+    x = O.rbm1_step(c, x, 0) if c["scheme"] == "rbm1" else O.rbmr_step(c, x, 0)
+    t1 = time.perf_counter() - t0
+    k = int(max(1, min(40, budget_s / max(t1, 1e-6))))
+    t0 = time.perf_counter()
+    x = O.run(c, x, 1, k)
+    dt = time.perf_counter() - t0
+    assert np.isfinite(x).all()
+    return {"value": c["n"] * k / dt, "unit": "particle-steps/s", "cores": 1, "kind": "oracle",
+            "sample": f"{c['n']} particles of the same workload, {k} steps (oracle is single-threaded; host nproc={os.cpu_count()})"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = workload(args, 0)
+    from oracle import oracle as O
+    c = dict(cfg, n=min(cfg["n"], 1 << 17))
+    x = O.init(c)
+    x = O.run(c, x, 0, args.warmup)
+    t0 = time.perf_counter()
+    x = O.run(c, x, args.warmup, args.steps)
+    dt = time.perf_counter() - t0
+    v = c["n"] * args.steps / dt
+    line = {"impl": "reference", "metric": "particle-steps/s", "value": v, "unit": "particle-steps/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(args, cfg, args.gpus),
+            "cpu_baseline": {"value": v, "unit": "particle-steps/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{c['n']} particles of the workload per step (oracle, 1 thread)"},
+            "e2e": {"value": v, "unit": "particle-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(args, cfg, world):
+    return {"workload": f"{args.workload} " + {
+        "C1": "Dyson Brownian motion", "C2": "Thomson-type Coulomb on S^2",
+        "C3": "bounded-confidence opinion", "C4": "2-D Gaussian aggregation",
+        "C5": "3-D regularised Coulomb, partitioned-system size per GPU"}[args.workload],
+        "n_per_gpu": cfg["n"], "d": cfg["d"], "p": cfg["p"], "scheme": cfg["scheme"],
+        "kernel": cfg["kernel"], "integrator": cfg["integrator"], "dt": cfg["dt"],
+        "sigma": cfg["sigma"],
+        "multi_gpu": "single system" if world == 1 else "ensemble replicas (replica = rank), no collective",
+        "l2": "inputs larger than L2 (state >> 126 MB); no flush"
+        if cfg["n"] * (4 + cfg["d"] * elt(cfg)) > 2 * 126e6 else "state fits in L2; no flush"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1812_10575_b200 import RBM
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = workload(args, rank)
+    dev = torch.device("cuda", local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    s = RBM(cfg, device=dev)
+    stream = s.stream
+    s.run(args.warmup)
+    s.sync()
+    K = args.steps
+    s.timing_begin(K)
+    clk = Clocks(local)
+    clk.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(K):
+        s.step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    per_kernel, nrec = s.timing_end()
+    s.sync()
+    launches = s.launches_per_step * K
+    n_total = cfg["n"] * world
+    value = n_total * K / (ms / 1e3)
+
+    # roofline of the dominant kernel (largest share of the step)
+    name = max(per_kernel, key=per_kernel.get)
+    avg_ms = per_kernel[name] / max(nrec, 1)
+    peak, peak_kind = peaks()
+    nbytes = kernel_bytes(name, cfg)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(f"{args.workload}:p{cfg['p']}:{cfg['scheme']}:{name}")
+    except Exception:
+        pass
+    if nbytes > 0:
+        ach = nbytes / (avg_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "peak_source": peak_kind, "traffic": traffic,
+                "algorithmic_bytes_per_launch": nbytes, "avg_launch_ms": avg_ms}
+    else:
+        roof = {"bound": "alu", "kernel": name, "achieved": None, "peak": None, "unit": "GB/s",
+                "frac": None, "traffic": traffic, "avg_launch_ms": avg_ms}
+    step_ms = ms / K
+    shares = {k: round(v / max(nrec, 1), 4) for k, v in per_kernel.items()}
+    R = 4 + cfg["d"] * elt(cfg)
+    useful = value / world * 2 * cfg["d"] * elt(cfg) / 1e9
+
+    # end-to-end through the public API with host buffers (pinned)
+    e2e = None
+    if not args.no_e2e:
+        npdt = np.float32 if cfg["dtype"] == "f32" else np.float64
+        tdt = torch.float32 if cfg["dtype"] == "f32" else torch.float64
+        hin = torch.empty((cfg["n"], cfg["d"]), dtype=tdt, pin_memory=True)
+        hout = torch.empty((cfg["n"], cfg["d"]), dtype=tdt, pin_memory=True)
+        s.gather(host=False)  # warm
+        xin = hin.numpy()
+        xin[:] = np.resize(RI.user_x0(min(cfg["n"], 1 << 20), cfg["d"], seed=rank).astype(npdt),
+                           (cfg["n"], cfg["d"]))
+        ue = s
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ue.set_state(xin)                       # pinned host -> device (inside the timed region)
+        ue.run(K)                               # graph-replayed steps
+        from paper_1812_10575_b200 import rbm as RB
+        RB.rbm_gather(ue.ctx, 0, cfg["n"], hout.data_ptr(), RB.MEM_HOST)  # device -> pinned host
+        t = time.perf_counter() - t0
+        barrier()
+        t = max_over_ranks(t)
+        e2e = {"value": n_total * K / t, "unit": "particle-steps/s",
+               "h2d_bytes_per_step": cfg["n"] * cfg["d"] * elt(cfg) / K,
+               "d2h_bytes_per_step": cfg["n"] * cfg["d"] * elt(cfg) / K,
+               "job": f"upload X0 from pinned host, {K} steps (rbm_run), download X_K to pinned host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg)
+
+    line = {"metric": "particle-steps/s", "value": value, "unit": "particle-steps/s",
+            "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": cfg["dtype"], "data": "synthetic (Philox init from seed, BASELINE.json config)",
+            "config": config_dict(args, cfg, world),
+            "hbm": {"useful_gbs_per_gpu": useful, "record_bytes": R,
+                    "note": "useful = particle-steps/s x 2 d s (state read+write once)"},
+            "roofline": roof, "kernel_ms_per_step": shares, "clocks": clocks,
+            "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    s.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

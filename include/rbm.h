@@ -1,0 +1,213 @@
+/*
+ * include/rbm.h -- C ABI of the B200-native Random Batch Method library
+ * (librbm.so, built from paper_1812_10575_b200/csrc/ for sm_100a).
+ *
+ * One call of rbm_step() is one time step of the Random Batch Method of
+ * Jin, Li & Liu (arXiv:1812.10575) for the first-order binary-interaction
+ * particle system, Eq. (1.2):
+ *
+ *   dX^i = -grad V(X^i) dt + 1/(N-1) sum_{j != i} K(X^i - X^j) dt + sigma dB^i,
+ *
+ * in one of two schemes:
+ *   RBM_SCHEME_RBM1  Algorithm 1: a fresh random division of
+ *                    {0..N-1} into batches of size p, then Eq. (2.2)
+ *                     inside each batch with prefactor
+ *                    1/(|B|-1), integrated by forward Euler-Maruyama
+ *                     or by the splitting with the
+ *                    exact p=2 pair flow.
+ *   RBM_SCHEME_RBMR  Algorithms 2/3: one sweep of ceil(N/p)
+ *                    with-replacement batches, read as a Jacobi-additive sweep
+ *                    (reading D:8).
+ *
+ * The random division at step m is the permutation that sorts the ids by
+ * (key_m(id), id), key_m(id) = word 0 of Philox4x32-10 at counter
+ * (id, 0, m, TAG_KEY | replica<<8) under key (seed_lo, seed_hi); batch b is
+ * sorted positions [b p, (b+1) p) with the remainder rule of DESIGN.md D:7.
+ * Brownian increments use counter (id, blk, m, TAG_NOISE | replica<<8).
+ * Everything is a pure function of (config, seed, step, id): results do not
+ * depend on launch geometry, on the internal storage order, or on the GPU.
+ *
+ * Conventions for every entry point:
+ *   - No C++ types, no exceptions cross the boundary; every call returns an
+ *     rbm_status.  On failure rbm_last_error(ctx) (or rbm_last_error(NULL) for
+ *     failures before a context exists) returns a NUL-terminated message owned
+ *     by the library, valid until the next call on the same context/thread.
+ *   - Positions exchanged with the caller are row-major (particle, axis):
+ *     N*d scalars of the configured dtype (float for RBM_F32, double for
+ *     RBM_F64), in id order.
+ *   - "Device pointer" = CUDA global memory of the current device; "host
+ *     pointer" = ordinary or pinned host memory.
+ *   - Ownership: the caller owns the workspace, every input/output buffer and
+ *     the CUDA stream; the library owns the context (and its private capture
+ *     stream, CUDA graphs and events) and releases them in rbm_destroy().
+ *   - A context is used by one host thread at a time.
+ *   - Work is stream-ordered on the caller's stream and asynchronous unless
+ *     stated; device-side failures (non-finite state, overflow of an internal
+ *     capacity) surface at the next rbm_sync / rbm_gather as
+ *     RBM_ERR_NONFINITE / RBM_ERR_CAPACITY.
+ */
+#ifndef RBM_H_
+#define RBM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RBM_ABI_VERSION 1u
+
+typedef struct rbm_ctx rbm_ctx; /* opaque, library-owned host object */
+
+typedef enum {
+  RBM_OK = 0,
+  RBM_ERR_INVALID_ARG = 1,    /* config or argument rejected (message says which) */
+  RBM_ERR_UNKNOWN_KERNEL = 2, /* kernel/potential id not in the registry */
+  RBM_ERR_UNSUPPORTED = 3,    /* valid request this build does not implement */
+  RBM_ERR_WORKSPACE = 4,      /* workspace NULL, too small or misaligned (256 B) */
+  RBM_ERR_CUDA = 5,           /* a CUDA runtime call failed (message has the code) */
+  RBM_ERR_NCCL = 6,           /* reserved: multi-process partition mode */
+  RBM_ERR_NONFINITE = 7,      /* a non-finite position was produced; message names step and id */
+  RBM_ERR_STATE = 8,          /* call out of order (e.g. step before init) */
+  RBM_ERR_CAPACITY = 9        /* an internal per-bucket capacity was exceeded */
+} rbm_status;
+
+typedef enum { RBM_F32 = 0, RBM_F64 = 1 } rbm_dtype;
+typedef enum { RBM_SCHEME_RBM1 = 0, RBM_SCHEME_RBMR = 1 } rbm_scheme;
+typedef enum { RBM_INTEG_EULER_MARUYAMA = 0, RBM_INTEG_SPLIT_EXACT_PAIR = 1 } rbm_integrator;
+
+/* Interaction kernels K(z), z = X^i - X^j (Eq. 1.2). */
+typedef enum {
+  RBM_K_ZERO = 0,
+  RBM_K_DYSON = 1,              /* 1/z, d=1 (Eq. 4.4); K(0):=0            */
+  RBM_K_COULOMB = 2,            /* z/|z|^3, d=3; K(0):=0                 */
+  RBM_K_BOUNDED_CONFIDENCE = 3, /* -a z 1{|z|<r}, kparam={a, r} (Eq. 5.12) */
+  RBM_K_GAUSS_ATTR_REP = 4,     /* z e^{-|z|^2/2} - z e^{-|z|^2/8}/4 (BASELINE.json C4)       */
+  RBM_K_COULOMB_REG = 5,        /* z/(|z|^2+eps)^{3/2}, kparam={eps} (BASELINE.json C5)       */
+  RBM_K_SMOOTH_TEST = 6         /* z/(1+|z|^2)                             */
+} rbm_kernel;
+
+typedef enum { RBM_V_NONE = 0, RBM_V_HARMONIC = 1 /* beta|x|^2/2, vparam={beta} */ } rbm_potential;
+typedef enum { RBM_CONSTRAINT_NONE = 0, RBM_CONSTRAINT_UNIT_SPHERE = 1 /* d=3 */ } rbm_constraint;
+
+/* Initial data X_0^i ~ nu, iid; computed in fp64 from
+ * Philox counter (id, blk, 0, TAG_INIT|replica<<8), then rounded to dtype. */
+typedef enum {
+  RBM_INIT_USER = 0,          /* caller supplies X_0 via rbm_set_state()            */
+  RBM_INIT_NORMAL = 1,        /* iparam = {mean, std}                                */
+  RBM_INIT_UNIFORM_BOX = 2,   /* iparam = {a, b}: U[a,b]^d                           */
+  RBM_INIT_UNIFORM_SPHERE = 3,/* uniform on S^{d-1}                                  */
+  RBM_INIT_GAUSS_MIXTURE = 4  /* iparam = {K, std, lo, hi}: equal weights, centres U[lo,hi]^d */
+} rbm_init_kind;
+
+typedef enum { RBM_MEM_DEVICE = 0, RBM_MEM_HOST = 1 } rbm_mem;
+
+typedef struct {
+  uint32_t abi_version;  /* must be RBM_ABI_VERSION */
+  uint32_t dtype;        /* rbm_dtype: arithmetic and storage precision of X */
+  uint32_t d;            /* spatial dimension, 1..3 */
+  uint32_t p;            /* batch size, 2..64 (or p == n for n <= 4096) */
+  uint64_t n;            /* number of particles N, 2..2^31 */
+  uint32_t scheme;       /* rbm_scheme */
+  uint32_t integrator;   /* rbm_integrator */
+  uint32_t kernel;       /* rbm_kernel */
+  uint32_t potential;    /* rbm_potential */
+  uint32_t constraint;   /* rbm_constraint */
+  uint32_t init;         /* rbm_init_kind */
+  double kparam[4];
+  double vparam[2];
+  double iparam[8];
+  double sigma;          /* noise amplitude, >= 0 */
+  double dt;             /* time step tau, > 0 */
+  uint64_t seed;         /* Philox key (seed_lo, seed_hi) */
+  uint64_t step0;        /* index m of the first step (checkpoint resume) */
+  uint32_t replica;      /* ensemble member, enters Philox counter word 3 (< 2^24) */
+  int32_t world_size;    /* 1 (multi-process partition mode: RBM_ERR_UNSUPPORTED) */
+  int32_t rank;          /* 0 */
+  uint32_t debug_bucket_cap; /* 0 = automatic; >0 forces the per-bucket smem capacity (tests) */
+} rbm_config;
+
+/* Bytes of device workspace rbm_init() needs for this config.
+ * Errors: RBM_ERR_INVALID_ARG / RBM_ERR_UNKNOWN_KERNEL (same validation as rbm_init). */
+rbm_status rbm_workspace_size(const rbm_config* cfg, size_t* bytes);
+
+/* Validate cfg (eagerly, all checks), carve ws (device pointer, >= the size
+ * above, 256-byte aligned, owned by the caller and untouched by it until
+ * rbm_destroy), and enqueue the initial data on `cuda_stream` (a cudaStream_t;
+ * NULL = legacy default stream).  For RBM_INIT_USER the state is undefined
+ * until rbm_set_state().  nccl_unique_id must be NULL (world_size == 1).
+ * On success *out receives the context; the step index is cfg->step0. */
+rbm_status rbm_init(const rbm_config* cfg, void* ws, size_t ws_bytes, void* cuda_stream,
+                    const void* nccl_unique_id, rbm_ctx** out);
+
+/* Replace the state by X given in id order (N*d scalars of dtype, row-major);
+ * `where` says whether x is a host or device pointer.  Host input is copied
+ * before the call returns (synchronous); device input is stream-ordered. */
+rbm_status rbm_set_state(rbm_ctx* ctx, const void* x, uint32_t where);
+
+/* Enqueue one step X_m -> X_{m+1} (async); m advances by one. */
+rbm_status rbm_step(rbm_ctx* ctx);
+
+/* Enqueue nsteps steps as CUDA-graph replays (async); no host work per step. */
+rbm_status rbm_run(rbm_ctx* ctx, uint64_t nsteps);
+
+/* Write positions of ids [id_begin, id_end) in id order, (id_end-id_begin)*d
+ * scalars, to x_out (host or device per `where`).  Synchronises the stream,
+ * then reports RBM_ERR_NONFINITE / RBM_ERR_CAPACITY if the device flagged
+ * one; the data are written in any case. */
+rbm_status rbm_gather(rbm_ctx* ctx, uint64_t id_begin, uint64_t id_end, void* x_out, uint32_t where);
+
+/* Synchronise the stream and check the device flags (see rbm_gather). */
+rbm_status rbm_sync(rbm_ctx* ctx);
+
+/* Index m of the next step to be enqueued (host-side counter). */
+uint64_t rbm_step_index(const rbm_ctx* ctx);
+
+/* Number of kernel launches one rbm_step enqueues (for the bench's
+ * gpu_launches count); 0 if ctx is NULL. */
+uint32_t rbm_launches_per_step(const rbm_ctx* ctx);
+
+/* Diagnostics: bucket layout chosen for this config (B prefix bits, number of
+ * scatter passes, per-bucket capacity).  Any out pointer may be NULL. */
+rbm_status rbm_layout(const rbm_ctx* ctx, uint32_t* prefix_bits, uint32_t* passes, uint32_t* bucket_cap);
+
+/* Test hook: write the current storage order (position -> id, N uint32
+ * values) to `order_out` (device pointer, stream-ordered).  After an RBM-1
+ * step m the state is stored in sorted order, so this is exactly the step-m
+ * permutation pi_m (ids sorted by (key_m(id), id)); batch b = positions
+ * [b p, (b+1) p) with the remainder rule.  Does not change X or m. */
+rbm_status rbm_debug_permutation(rbm_ctx* ctx, uint32_t* order_out);
+
+/* Test hook (RBM_SCHEME_RBMR only): the slot draws j_s of the next step,
+ * ceil(N/p)*p uint32 values (device). */
+rbm_status rbm_debug_slots(rbm_ctx* ctx, uint32_t* slots_out);
+
+/* Test hook: Philox4x32-10 of `count` (ctr, key) pairs on the device:
+ * in = count*6 uint32 (c0,c1,c2,c3,k0,k1), out = count*4 uint32 (device). */
+rbm_status rbm_debug_philox(const uint32_t* in, uint32_t* out, uint64_t count, void* cuda_stream);
+
+/* Name of the i-th kernel one step launches (i < rbm_launches_per_step);
+ * "" when out of range.  Static storage. */
+const char* rbm_kernel_name(const rbm_ctx* ctx, uint32_t i);
+
+/* Per-kernel timing: after rbm_timing_begin(ctx, max_steps) the next
+ * max_steps steps (rbm_step, or rbm_run, which then launches eagerly instead of
+ * replaying graphs) record a CUDA event on the caller's stream before every
+ * kernel and after the last.  rbm_timing_end() synchronises the stream and
+ * writes, for every kernel slot i < rbm_launches_per_step, the summed device
+ * time in ms over the recorded steps (ms_per_kernel, caller-owned array) and
+ * the number of steps recorded. */
+rbm_status rbm_timing_begin(rbm_ctx* ctx, uint32_t max_steps);
+rbm_status rbm_timing_end(rbm_ctx* ctx, double* ms_per_kernel, uint32_t* steps_recorded);
+
+/* Message for the last failure on ctx (or on this thread if ctx == NULL). */
+const char* rbm_last_error(const rbm_ctx* ctx);
+
+/* Release everything the library owns; the caller may then free ws. */
+rbm_status rbm_destroy(rbm_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RBM_H_ */

@@ -64,10 +64,12 @@ def lib():
             "oracle_init": (C.c_int, [cfgp, f64p]),
             "oracle_key": (C.c_uint32, [cfgp, C.c_uint32, C.c_uint64]),
             "oracle_permutation": (C.c_int, [cfgp, C.c_uint64, u32p]),
+            "oracle_keys": (None, [cfgp, C.c_uint64, u32p]),
             "oracle_batches": (C.c_uint64, [C.c_uint64, C.c_uint32, u64p]),
             "oracle_batch_forces": (C.c_int, [cfgp, f64p, u32p, u64p, C.c_uint64, f64p]),
             "oracle_pair_flow": (None, [cfgp, f64p, f64p, C.c_double, f64p, f64p]),
             "oracle_rbm1_step": (C.c_int, [cfgp, C.c_uint64, f64p]),
+            "oracle_batch_update": (C.c_int, [cfgp, C.c_uint64, u32p, f64p, C.c_uint32, f64p]),
             "oracle_direct_step": (C.c_int, [cfgp, C.c_uint64, f64p]),
             "oracle_slot_draw": (C.c_uint32, [cfgp, C.c_uint64, C.c_uint32, C.c_uint64]),
             "oracle_rbmr_slots": (C.c_int, [cfgp, C.c_uint64, u32p]),
@@ -146,6 +148,13 @@ def permutation(cfg: dict, m: int) -> np.ndarray:
     order = np.zeros(c.n, dtype=np.uint32)
     lib().oracle_permutation(C.byref(c), int(m), _p(order, C.c_uint32))
     return order
+
+
+def keys(cfg: dict, m: int) -> np.ndarray:
+    c = make_cfg(cfg)
+    out = np.zeros(c.n, dtype=np.uint32)
+    lib().oracle_keys(C.byref(c), int(m), _p(out, C.c_uint32))
+    return out
 
 
 def batch_starts(n: int, p: int) -> np.ndarray:
@@ -228,3 +237,16 @@ def rbmr_slots(cfg: dict, m: int) -> np.ndarray:
     js = np.zeros(nb * c.p, dtype=np.uint32)
     lib().oracle_rbmr_slots(C.byref(c), int(m), _p(js, C.c_uint32))
     return js
+
+
+def batch_update(cfg: dict, m: int, ids, xb) -> np.ndarray:
+    """One batch of Alg. 1 (members in sorted order) -> their X_{m+1}."""
+    c = make_cfg(cfg)
+    ids = np.ascontiguousarray(ids, dtype=np.uint32)
+    xb = np.ascontiguousarray(xb, dtype=np.float64).reshape(len(ids), c.d)
+    xo = np.zeros_like(xb)
+    rc = lib().oracle_batch_update(C.byref(c), int(m), _p(ids, C.c_uint32), _p(xb, C.c_double),
+                                   len(ids), _p(xo, C.c_double))
+    if rc:
+        raise ValueError(f"oracle_batch_update rc={rc}")
+    return xo

@@ -276,6 +276,11 @@ uint32_t oracle_key(const oracle_cfg* c, uint32_t id, uint64_t m) {
   return w[0];
 }
 
+/* key_m(id) for every id 0..N-1 (test helper for full-size property checks) */
+void oracle_keys(const oracle_cfg* c, uint64_t m, uint32_t* keys) {
+  for (uint64_t i = 0; i < c->n; ++i) keys[i] = oracle_key(c, (uint32_t)i, m);
+}
+
 int oracle_permutation(const oracle_cfg* c, uint64_t m, uint32_t* order) {
   uint64_t n = c->n;
   kv_t* a = (kv_t*)malloc(sizeof(kv_t) * (n ? n : 1));
@@ -385,6 +390,44 @@ static void split_member(const oracle_cfg* c, const double* y, const double* z, 
 }
 
 /* ------------------------------------------------------------------ */
+/* one batch C_q of Alg. 1 line 4: members ids[0..b) in sorted  */
+/* order with positions xb (b x d, X_m) -> xo (b x d, X_{m+1}).             */
+/* EM: Eq. (2.2) with prefactor 1/(b-1), forward Euler-Maruyama.           */
+/* split (b = 2): exact pair flow, then confinement + noise.   */
+/* ------------------------------------------------------------------ */
+int oracle_batch_update(const oracle_cfg* c, uint64_t m, const uint32_t* ids,
+                        const double* xb, uint32_t b, double* xo) {
+  uint32_t d = c->d;
+  if (b < 2) return 1;
+  if (c->integrator == 0) {
+    double inv = 1.0 / (double)(b - 1);
+    for (uint32_t q = 0; q < b; ++q) {
+      double acc[3] = {0, 0, 0}, f[3], z[3];
+      for (uint32_t q2 = 0; q2 < b; ++q2) {    /* ascending sorted position */
+        if (q2 == q) continue;
+        double zz[3], kz[3];
+        diff(c, xb + (uint64_t)q * d, xb + (uint64_t)q2 * d, zz);
+        ok_kernel(c, zz, kz);
+        for (uint32_t k = 0; k < d; ++k) acc[k] += kz[k];
+      }
+      for (uint32_t k = 0; k < d; ++k) f[k] = acc[k] * inv;
+      oracle_noise(c, ids[q], m, z);
+      em_member(c, xb + (uint64_t)q * d, f, z, xo + (uint64_t)q * d);
+      if (c->constraint == 1) renormalise(c, xo + (uint64_t)q * d);
+    }
+  } else {
+    if (b != 2) return 1;
+    double y[2][3], z[3];
+    oracle_pair_flow(c, xb, xb + d, c->dt, y[0], y[1]);
+    for (uint32_t q = 0; q < 2; ++q) {
+      oracle_noise(c, ids[q], m, z);
+      split_member(c, y[q], z, xo + (uint64_t)q * d);
+    }
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------------ */
 /* RBM-1 step m: X_m (id order) -> X_{m+1} (id order), Alg. 1 */
 /* ------------------------------------------------------------------ */
 int oracle_rbm1_step(const oracle_cfg* c, uint64_t m, double* x) {
@@ -395,31 +438,24 @@ int oracle_rbm1_step(const oracle_cfg* c, uint64_t m, double* x) {
   uint64_t nb = oracle_batches(n, c->p, NULL);
   uint64_t* starts = (uint64_t*)malloc(sizeof(uint64_t) * (nb + 1));
   double* xn = (double*)malloc(sizeof(double) * n * d);
-  double* f = (double*)malloc(sizeof(double) * n * d);
-  if (!order || !starts || !xn || !f) return 2;
+  uint32_t bmax = c->p + 1;
+  double* xb = (double*)malloc(sizeof(double) * bmax * d);
+  double* xo = (double*)malloc(sizeof(double) * bmax * d);
+  if (!order || !starts || !xn || !xb || !xo) return 2;
   oracle_permutation(c, m, order);          /* line 2: random division */
   oracle_batches(n, c->p, starts);
-  if (c->integrator == 0) {                 /* lines 3-5: each batch, Eq. 2.2 */
-    oracle_batch_forces(c, x, order, starts, nb, f);
-    for (uint64_t i = 0; i < n; ++i) {
-      double z[3];
-      oracle_noise(c, (uint32_t)i, m, z);
-      em_member(c, x + i * d, f + i * d, z, xn + i * d);
-      if (c->constraint == 1) renormalise(c, xn + i * d);
-    }
-  } else {                                  /* splitting */
-    for (uint64_t b = 0; b < nb; ++b) {
-      uint32_t i = order[starts[b]], j = order[starts[b] + 1];
-      double yi[3], yj[3], z[3];
-      oracle_pair_flow(c, x + (uint64_t)i * d, x + (uint64_t)j * d, c->dt, yi, yj);
-      oracle_noise(c, i, m, z);
-      split_member(c, yi, z, xn + (uint64_t)i * d);
-      oracle_noise(c, j, m, z);
-      split_member(c, yj, z, xn + (uint64_t)j * d);
-    }
+  for (uint64_t b = 0; b < nb; ++b) {       /* lines 3-5: each batch */
+    uint64_t s = starts[b];
+    uint32_t sz = (uint32_t)(starts[b + 1] - s);
+    for (uint32_t q = 0; q < sz; ++q)
+      for (uint32_t k = 0; k < d; ++k) xb[q * d + k] = x[(uint64_t)order[s + q] * d + k];
+    int rc = oracle_batch_update(c, m, order + s, xb, sz, xo);
+    if (rc) return rc;
+    for (uint32_t q = 0; q < sz; ++q)
+      for (uint32_t k = 0; k < d; ++k) xn[(uint64_t)order[s + q] * d + k] = xo[q * d + k];
   }
   memcpy(x, xn, sizeof(double) * n * d);
-  free(order); free(starts); free(xn); free(f);
+  free(order); free(starts); free(xn); free(xb); free(xo);
   return 0;
 }
 

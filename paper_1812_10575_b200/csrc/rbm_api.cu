@@ -1,0 +1,306 @@
+// rbm_api.cu -- C ABI of librbm.so (declared in include/rbm.h).
+//
+// Host orchestration only: validation, bucket-layout choice, workspace
+// carving, per-config kernel dispatch, CUDA-graph capture/replay of steps.
+// Every arithmetic step of the RBM path runs in the kernels of
+// rbm_kernels.cuh; there is no CPU fallback.
+#include "rbm_host.cuh"
+
+namespace rbmhost {
+thread_local std::string g_err;
+
+EngineBase* make_engine(const rbm_config& k) {
+  return k.dtype == RBM_F64 ? make_engine_f64(k) : make_engine_f32(k);
+}
+
+rbm_status enqueue_steps(rbm_ctx* c, cudaStream_t s, uint64_t k) {
+  for (uint64_t i = 0; i < k; ++i) c->eng->step(*c, s);
+  CU(cudaGetLastError());
+  return RBM_OK;
+}
+
+rbm_status check_flags(rbm_ctx* c) {
+  unsigned long long nf = 0;
+  uint32_t cap = 0;
+  CU(cudaMemcpy(&nf, c->nonfinite, sizeof nf, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(&cap, c->capacity_err, sizeof cap, cudaMemcpyDeviceToHost));
+  if (cap) return fail(c, RBM_ERR_CAPACITY, "a bucket exceeded every capacity fallback; results of that step are invalid");
+  if (nf != ~0ull)
+    return fail(c, RBM_ERR_NONFINITE, "non-finite position at step %llu, particle id %llu",
+                (unsigned long long)(nf >> 32), (unsigned long long)(nf & 0xffffffffull));
+  return RBM_OK;
+}
+
+}  // namespace rbmhost
+
+extern "C" {
+
+rbm_status rbm_workspace_size(const rbm_config* cfg, size_t* bytes) {
+  rbm_status s = validate(cfg);
+  if (s) return s;
+  if (!bytes) return fail(nullptr, RBM_ERR_INVALID_ARG, "bytes is NULL");
+  rbm_ctx tmp;
+  tmp.cfg = *cfg;
+  tmp.L = choose_layout(*cfg);
+  Workspace ws;
+  carve(tmp, ws);
+  *bytes = ws.used;
+  return RBM_OK;
+}
+
+}  // extern "C"
+
+namespace rbmhost {
+rbm_status init_impl(rbm_ctx* c, const rbm_config* cfg, void* wsp, size_t ws_bytes) {
+  CU(cudaGetDevice(&c->device));
+  int major = 0;
+  CU(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, c->device));
+  if (major != 10) return fail(c, RBM_ERR_UNSUPPORTED, "device is sm_%d0; librbm is built for sm_100a", major);
+  Workspace ws;
+  ws.base = reinterpret_cast<unsigned char*>(wsp);
+  ws.size = ws_bytes;
+  carve(*c, ws);
+  c->eng.reset(make_engine(*cfg));
+  if (!c->eng) return fail(c, RBM_ERR_UNKNOWN_KERNEL, "no engine for kernel %u, d=%u", cfg->kernel, cfg->d);
+  DevParams& P = c->P;
+  P.n = cfg->n;
+  P.p = cfg->p;
+  P.seed_lo = (uint32_t)cfg->seed;
+  P.seed_hi = (uint32_t)(cfg->seed >> 32);
+  P.rep_hi = cfg->replica << 8;
+  P.potential = cfg->potential;
+  P.constraint = cfg->constraint;
+  P.has_noise = cfg->sigma > 0.0;
+  P.kp0 = cfg->kparam[0];
+  P.kp1 = cfg->kparam[1];
+  P.beta = cfg->potential == RBM_V_HARMONIC ? cfg->vparam[0] : 0.0;
+  P.dt = cfg->dt;
+  P.sq = cfg->sigma * std::sqrt(cfg->dt);
+  P.kp0f = (float)P.kp0; P.kp1f = (float)P.kp1; P.betaf = (float)P.beta;
+  P.dtf = (float)P.dt; P.sqf = (float)P.sq;
+  P.B = c->L.B; P.b1 = c->L.b1; P.b2 = c->L.b2; P.nbuckets = c->L.nbuckets; P.cap = c->L.cap;
+  P.step = c->step_dev;
+  P.nonfinite = c->nonfinite;
+  P.capacity_err = c->capacity_err;
+  P.big_claim = c->zero_block + 1024;
+  P.big_scratch = c->big_scratch;
+  rbm_status s = c->eng->setup(*c);
+  if (s) return s;
+  CU(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  cudaStream_t st = c->stream;
+  c->step = cfg->step0;
+  const unsigned long long clean = ~0ull;
+  CU(cudaMemcpyAsync(c->step_dev, &c->step, 8, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(c->nonfinite, &clean, 8, cudaMemcpyHostToDevice, st));
+  CU(cudaMemsetAsync(c->capacity_err, 0, 4, st));
+  const uint32_t s0[2] = {0u, (uint32_t)cfg->n};
+  if (c->L.B == 0) CU(cudaMemcpyAsync(c->S, s0, 8, cudaMemcpyHostToDevice, st));
+  if (cfg->init != RBM_INIT_USER) c->eng->init_state(*c, st);
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(st));  // the host-side sources above live on this stack frame
+  return RBM_OK;
+}
+}  // namespace rbmhost
+
+extern "C" {
+
+rbm_status rbm_init(const rbm_config* cfg, void* wsp, size_t ws_bytes, void* cuda_stream,
+                    const void* nccl_unique_id, rbm_ctx** out) {
+  rbm_status s = validate(cfg);
+  if (s) return s;
+  if (!out) return fail(nullptr, RBM_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (nccl_unique_id) return fail(nullptr, RBM_ERR_UNSUPPORTED, "nccl_unique_id must be NULL (world_size 1)");
+  size_t need = 0;
+  rbm_workspace_size(cfg, &need);
+  if (!wsp || ws_bytes < need || (reinterpret_cast<uintptr_t>(wsp) & 255))
+    return fail(nullptr, RBM_ERR_WORKSPACE, "workspace %p of %zu B; need %zu B, 256-B aligned", wsp, ws_bytes, need);
+  std::unique_ptr<rbm_ctx> c(new rbm_ctx());
+  c->cfg = *cfg;
+  c->L = choose_layout(*cfg);
+  c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  s = init_impl(c.get(), cfg, wsp, ws_bytes);
+  if (s) {
+    g_err = c->err;
+    if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+    return s;
+  }
+  *out = c.release();
+  return RBM_OK;
+}
+
+rbm_status rbm_set_state(rbm_ctx* c, const void* x, uint32_t where) {
+  if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
+  if (!x) return fail(c, RBM_ERR_INVALID_ARG, "x is NULL");
+  const size_t bytes = c->cfg.n * c->cfg.d * elt_size(c->cfg);
+  if (where == RBM_MEM_HOST) {
+    void* scratch = c->xbuf[c->cur ^ 1];  // inactive buffer as staging
+    CU(cudaMemcpyAsync(scratch, x, bytes, cudaMemcpyHostToDevice, c->stream));
+    c->eng->set_state(*c, scratch, c->stream);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(c->stream));
+  } else if (where == RBM_MEM_DEVICE) {
+    c->eng->set_state(*c, x, c->stream);
+    CU(cudaGetLastError());
+  } else {
+    return fail(c, RBM_ERR_INVALID_ARG, "where=%u", where);
+  }
+  return RBM_OK;
+}
+
+rbm_status rbm_step(rbm_ctx* c) {
+  if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
+  rbm_status s = enqueue_steps(c, c->stream, 1);
+  if (s) return s;
+  ++c->step;
+  return RBM_OK;
+}
+
+rbm_status rbm_run(rbm_ctx* c, uint64_t nsteps) {
+  if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
+  if (c->step + nsteps >= (1ull << 32)) return fail(c, RBM_ERR_INVALID_ARG, "step index would exceed 2^32");
+  // steps per graph: even when a step flips the ping-pong buffers
+  const bool flips = (c->cfg.scheme == RBM_SCHEME_RBM1) && (c->L.B == 0 || c->L.b2 != 0);
+  const uint32_t per = flips ? 8 : 8;
+  c->graph_steps = per;
+  uint64_t done = 0;
+  if (nsteps >= per && !c->timing) {
+    const int slot = c->cur;
+    if (!c->graph[slot]) {
+      const int cur0 = c->cur;
+      CU(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+      for (uint32_t i = 0; i < per; ++i) c->eng->step(*c, c->cap_stream);
+      cudaGraph_t g = nullptr;
+      CU(cudaStreamEndCapture(c->cap_stream, &g));
+      CU(cudaGraphInstantiate(&c->graph[slot], g, 0));
+      cudaGraphDestroy(g);
+      if (c->cur != cur0) return fail(c, RBM_ERR_STATE, "graph does not return the buffer parity");
+    }
+    const uint64_t reps = nsteps / per;
+    for (uint64_t r = 0; r < reps; ++r) CU(cudaGraphLaunch(c->graph[slot], c->stream));
+    done = reps * per;
+  }
+  rbm_status s = enqueue_steps(c, c->stream, nsteps - done);
+  if (s) return s;
+  c->step += nsteps;
+  return RBM_OK;
+}
+
+rbm_status rbm_gather(rbm_ctx* c, uint64_t id_begin, uint64_t id_end, void* x_out, uint32_t where) {
+  if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
+  if (!x_out) return fail(c, RBM_ERR_INVALID_ARG, "x_out is NULL");
+  if (id_begin > id_end || id_end > c->cfg.n) return fail(c, RBM_ERR_INVALID_ARG, "bad id range [%llu,%llu)", (unsigned long long)id_begin, (unsigned long long)id_end);
+  const size_t bytes = (id_end - id_begin) * c->cfg.d * elt_size(c->cfg);
+  if (where == RBM_MEM_HOST) {
+    void* scratch = c->xbuf[c->cur ^ 1];
+    c->eng->gather(*c, id_begin, id_end, scratch, c->stream);
+    CU(cudaGetLastError());
+    if (bytes) CU(cudaMemcpyAsync(x_out, scratch, bytes, cudaMemcpyDeviceToHost, c->stream));
+  } else if (where == RBM_MEM_DEVICE) {
+    c->eng->gather(*c, id_begin, id_end, x_out, c->stream);
+    CU(cudaGetLastError());
+  } else {
+    return fail(c, RBM_ERR_INVALID_ARG, "where=%u", where);
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  return check_flags(c);
+}
+
+rbm_status rbm_sync(rbm_ctx* c) {
+  if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
+  CU(cudaStreamSynchronize(c->stream));
+  return check_flags(c);
+}
+
+uint64_t rbm_step_index(const rbm_ctx* c) { return c ? c->step : 0; }
+
+uint32_t rbm_launches_per_step(const rbm_ctx* c) {
+  if (!c) return 0;
+  uint32_t k = 0;
+  kernel_names(*c, &k);
+  return k;
+}
+
+const char* rbm_kernel_name(const rbm_ctx* c, uint32_t i) {
+  if (!c) return "";
+  uint32_t k = 0;
+  const char* const* names = kernel_names(*c, &k);
+  return i < k ? names[i] : "";
+}
+
+rbm_status rbm_timing_begin(rbm_ctx* c, uint32_t max_steps) {
+  if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
+  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  c->ev.clear();
+  const size_t need = (size_t)max_steps * (rbm_launches_per_step(c) + 1);
+  c->ev.resize(need);
+  for (size_t i = 0; i < need; ++i) CU(cudaEventCreate(&c->ev[i]));
+  c->ev_used = 0;
+  c->timing = true;
+  return RBM_OK;
+}
+
+rbm_status rbm_timing_end(rbm_ctx* c, double* ms_per_kernel, uint32_t* steps_recorded) {
+  if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
+  if (!c->timing) return fail(c, RBM_ERR_STATE, "timing was not begun");
+  CU(cudaStreamSynchronize(c->stream));
+  const uint32_t k = rbm_launches_per_step(c);
+  const size_t per = k + 1;
+  const uint32_t steps = (uint32_t)(c->ev_used / per);
+  for (uint32_t j = 0; j < k; ++j) ms_per_kernel[j] = 0.0;
+  for (uint32_t t = 0; t < steps; ++t)
+    for (uint32_t j = 0; j < k; ++j) {
+      float ms = 0.f;
+      CU(cudaEventElapsedTime(&ms, c->ev[t * per + j], c->ev[t * per + j + 1]));
+      ms_per_kernel[j] += ms;
+    }
+  if (steps_recorded) *steps_recorded = steps;
+  c->timing = false;
+  return RBM_OK;
+}
+
+rbm_status rbm_layout(const rbm_ctx* c, uint32_t* prefix_bits, uint32_t* passes, uint32_t* bucket_cap) {
+  if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
+  if (prefix_bits) *prefix_bits = c->L.B;
+  if (passes) *passes = c->L.B == 0 ? 0 : (c->L.b2 ? 2 : 1);
+  if (bucket_cap) *bucket_cap = c->L.cap;
+  return RBM_OK;
+}
+
+rbm_status rbm_debug_permutation(rbm_ctx* c, uint32_t* order_out) {
+  if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
+  if (!order_out) return fail(c, RBM_ERR_INVALID_ARG, "order_out is NULL");
+  copy_ids_kernel<<<grid_for(c->cfg.n, 256), 256, 0, c->stream>>>(c->cfg.n, c->idbuf[c->cur], order_out);
+  CU(cudaGetLastError());
+  return RBM_OK;
+}
+
+rbm_status rbm_debug_slots(rbm_ctx* c, uint32_t* slots_out) {
+  if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
+  if (c->cfg.scheme != RBM_SCHEME_RBMR) return fail(c, RBM_ERR_STATE, "not an RBM-r context");
+  if (!slots_out) return fail(c, RBM_ERR_INVALID_ARG, "slots_out is NULL");
+  CU(cudaMemcpyAsync(slots_out, c->js, c->nslots * 4, cudaMemcpyDeviceToDevice, c->stream));
+  return RBM_OK;
+}
+
+rbm_status rbm_debug_philox(const uint32_t* in, uint32_t* out, uint64_t count, void* cuda_stream) {
+  rbm_ctx* c = nullptr;
+  if (!in || !out) return fail(nullptr, RBM_ERR_INVALID_ARG, "NULL buffer");
+  if (count) philox_test_kernel<<<grid_for(count, 256), 256, 0, (cudaStream_t)cuda_stream>>>(in, out, count);
+  CU(cudaGetLastError());
+  return RBM_OK;
+}
+
+const char* rbm_last_error(const rbm_ctx* c) { return c ? c->err.c_str() : g_err.c_str(); }
+
+rbm_status rbm_destroy(rbm_ctx* c) {
+  if (!c) return RBM_OK;
+  for (int i = 0; i < 2; ++i)
+    if (c->graph[i]) cudaGraphExecDestroy(c->graph[i]);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  delete c;
+  return RBM_OK;
+}
+
+}  // extern "C"

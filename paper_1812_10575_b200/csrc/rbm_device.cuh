@@ -1,0 +1,266 @@
+// rbm_device.cuh -- device building blocks of the RBM step (sm_100a).
+//
+// Philox4x32-10 counter RNG, exact open-interval uniform maps, Box-Muller,
+// the registry of interaction kernels K and potentials V, and the per-member
+// Euler-Maruyama / split-pair updates of Eq. (2.2).
+// Written for this library; shares nothing with oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rbm {
+
+enum : uint32_t { TAG_KEY = 0, TAG_NOISE = 1, TAG_INIT = 2, TAG_INIT_AUX = 3,
+                  TAG_SLOT = 4, TAG_NOISE_SLOT = 5 };
+enum : int { KK_ZERO = 0, KK_DYSON = 1, KK_COULOMB = 2, KK_BOUNDED = 3,
+             KK_GAUSS_AR = 4, KK_COULOMB_REG = 5, KK_SMOOTH = 6 };
+
+// Everything a kernel needs about the configuration; passed by value.
+struct DevParams {
+  uint64_t n;          // N
+  uint32_t p;          // batch size
+  uint32_t seed_lo, seed_hi;
+  uint32_t rep_hi;     // replica << 8, OR-ed into counter word 3
+  uint32_t potential;  // 0 none, 1 harmonic
+  uint32_t constraint; // 0 none, 1 unit sphere
+  uint32_t has_noise;  // sigma > 0
+  // model constants in both precisions
+  double kp0, kp1, beta, dt, sq;   // sq = sigma*sqrt(dt)
+  float kp0f, kp1f, betaf, dtf, sqf;
+  // bucket layout of the partition
+  uint32_t B;          // prefix bits of the final buckets
+  uint32_t b1, b2;     // digit bits of scatter passes 1 and 2 (b2 = 0: one pass)
+  uint32_t nbuckets;   // 2^B
+  uint32_t cap;        // per-bucket shared-memory capacity (elements)
+  const uint64_t* step;     // device step counter m
+  unsigned long long* nonfinite;  // atomicMin of (m<<32 | id); ~0 if clean
+  uint32_t* capacity_err;         // set to 1 if a bucket overflowed every fallback
+  uint32_t* big_claim;            // slot counter of the global-scratch fallback
+  unsigned char* big_scratch;     // NBIG slots of BIG_CAP elements
+};
+
+constexpr int NBIG = 2;             // concurrent oversized buckets handled per step
+constexpr uint32_t BIG_CAP = 65535; // u16 indices
+
+// ----------------------------------------------------------------- Philox
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c.x;
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c.z;
+    c = make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ k0, (uint32_t)p1,
+                   (uint32_t)(p0 >> 32) ^ c.w ^ k1, (uint32_t)p0);
+  }
+  return c;
+}
+
+__device__ __forceinline__ uint4 block_at(const DevParams& P, uint32_t c0, uint32_t c1,
+                                          uint32_t m, uint32_t tag) {
+  return philox4x32_10(make_uint4(c0, c1, m, tag | P.rep_hi), P.seed_lo, P.seed_hi);
+}
+
+// shuffle key of particle `id` at step m: word 0 of the TAG_KEY block
+__device__ __forceinline__ uint32_t shuffle_key(const DevParams& P, uint32_t id, uint32_t m) {
+  return block_at(P, id, 0u, m, TAG_KEY).x;
+}
+
+// ------------------------------------------------------------ uniform maps
+// fp32: (2 (w>>9) + 1) 2^-24 == ((w >> 8) | 1) 2^-24, exact
+__device__ __forceinline__ float u01f(uint32_t w) {
+  return __uint2float_rn((w >> 8) | 1u) * 0x1p-24f;
+}
+// fp64: (2k+1) 2^-53 with k = (a:b) >> 12, exact
+__device__ __forceinline__ double u01d(uint32_t a, uint32_t b) {
+  const uint64_t k = ((((uint64_t)a) << 32) | b) >> 12;
+  return (double)(2ull * k + 1ull) * 0x1p-53;
+}
+
+// ------------------------------------------------------------ Box-Muller
+__device__ __forceinline__ void bm_pair(float u1, float u2, float& z0, float& z1) {
+  const float r = sqrtf(-2.0f * logf(u1));
+  float s, c;
+  sincospif(2.0f * u2, &s, &c);
+  z0 = r * c;
+  z1 = r * s;
+}
+__device__ __forceinline__ void bm_pair(double u1, double u2, double& z0, double& z1) {
+  const double r = sqrt(-2.0 * log(u1));
+  double s, c;
+  sincospi(2.0 * u2, &s, &c);
+  z0 = r * c;
+  z1 = r * s;
+}
+
+// d standard normals from counter (c0, *, m, tag); layout of DESIGN.md D:13
+template <typename T, int D> struct Normals;
+template <int D> struct Normals<float, D> {
+  __device__ __forceinline__ static void get(const DevParams& P, uint32_t c0, uint32_t m,
+                                             uint32_t tag, float (&z)[D]) {
+    const uint4 w = block_at(P, c0, 0u, m, tag);
+    float a, b;
+    bm_pair(u01f(w.x), u01f(w.y), a, b);
+    z[0] = a;
+    if (D > 1) z[D > 1 ? 1 : 0] = b;
+    if (D > 2) {
+      float e, f;
+      bm_pair(u01f(w.z), u01f(w.w), e, f);
+      z[D > 2 ? 2 : 0] = e;
+    }
+  }
+};
+template <int D> struct Normals<double, D> {
+  __device__ __forceinline__ static void get(const DevParams& P, uint32_t c0, uint32_t m,
+                                             uint32_t tag, double (&z)[D]) {
+    const uint4 w = block_at(P, c0, 0u, m, tag);
+    double a, b;
+    bm_pair(u01d(w.x, w.y), u01d(w.z, w.w), a, b);
+    z[0] = a;
+    if (D > 1) z[D > 1 ? 1 : 0] = b;
+    if (D > 2) {
+      const uint4 v = block_at(P, c0, 1u, m, tag);
+      double e, f;
+      bm_pair(u01d(v.x, v.y), u01d(v.z, v.w), e, f);
+      z[D > 2 ? 2 : 0] = e;
+    }
+  }
+};
+
+// ------------------------------------------------------------ model registry
+template <typename T> struct Prm;
+template <> struct Prm<float> {
+  __device__ __forceinline__ static float kp0(const DevParams& P) { return P.kp0f; }
+  __device__ __forceinline__ static float kp1(const DevParams& P) { return P.kp1f; }
+  __device__ __forceinline__ static float beta(const DevParams& P) { return P.betaf; }
+  __device__ __forceinline__ static float dt(const DevParams& P) { return P.dtf; }
+  __device__ __forceinline__ static float sq(const DevParams& P) { return P.sqf; }
+};
+template <> struct Prm<double> {
+  __device__ __forceinline__ static double kp0(const DevParams& P) { return P.kp0; }
+  __device__ __forceinline__ static double kp1(const DevParams& P) { return P.kp1; }
+  __device__ __forceinline__ static double beta(const DevParams& P) { return P.beta; }
+  __device__ __forceinline__ static double dt(const DevParams& P) { return P.dt; }
+  __device__ __forceinline__ static double sq(const DevParams& P) { return P.sq; }
+};
+
+__device__ __forceinline__ float inv_cube_sqrt(float q) { const float r = rsqrtf(q); return r * r * r; }
+__device__ __forceinline__ double inv_cube_sqrt(double q) { return 1.0 / (q * sqrt(q)); }
+
+// K(z) = s(z) z for every registry entry (Eq. 1.2)
+template <typename T, int D, int KK>
+__device__ __forceinline__ T kernel_scale(const T (&z)[D], const DevParams& P) {
+  T r2 = z[0] * z[0];
+#pragma unroll
+  for (int c = 1; c < D; ++c) r2 += z[c] * z[c];
+  if (KK == KK_ZERO) return T(0);
+  if (KK == KK_DYSON) return r2 == T(0) ? T(0) : T(1) / r2;               // 1/z, K(0):=0
+  if (KK == KK_COULOMB) return r2 == T(0) ? T(0) : T(1) / (r2 * sqrt(r2));  // z/|z|^3
+  if (KK == KK_BOUNDED) {                                                   // -a z 1{|z|<r}
+    const bool inside = (D == 1) ? (fabs(z[0]) < Prm<T>::kp1(P)) : (sqrt(r2) < Prm<T>::kp1(P));
+    return inside ? -Prm<T>::kp0(P) : T(0);
+  }
+  if (KK == KK_GAUSS_AR) return exp(T(-0.5) * r2) - T(0.25) * exp(T(-0.125) * r2);
+  if (KK == KK_COULOMB_REG) return inv_cube_sqrt(r2 + Prm<T>::kp0(P));
+  if (KK == KK_SMOOTH) return T(1) / (T(1) + r2);
+  return T(0);
+}
+
+// accumulate K(xi - xj) into f
+template <typename T, int D, int KK>
+__device__ __forceinline__ void add_interaction(const T (&xi)[D], const T (&xj)[D], T (&f)[D],
+                                                const DevParams& P) {
+  T z[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) z[c] = xi[c] - xj[c];
+  const T s = kernel_scale<T, D, KK>(z, P);
+#pragma unroll
+  for (int c = 0; c < D; ++c) f[c] += s * z[c];
+}
+
+template <typename T, int D>
+__device__ __forceinline__ void renormalise(T (&x)[D]) {
+  T r2 = x[0] * x[0];
+#pragma unroll
+  for (int c = 1; c < D; ++c) r2 += x[c] * x[c];
+  const T r = sqrt(r2);
+#pragma unroll
+  for (int c = 0; c < D; ++c) x[c] /= r;
+}
+
+// Euler-Maruyama member update, f = prefactor * sum K.
+// Sphere: drift and noise projected on the tangent plane, then renormalised.
+// `normalise` false returns the unnormalised point (RBM-r increments, D:8).
+template <typename T, int D>
+__device__ __forceinline__ void em_update(const T (&x)[D], const T (&f)[D], const T (&z)[D],
+                                          T (&xn)[D], const DevParams& P, bool normalise) {
+  T drift[D], zz[D];
+  const T beta = Prm<T>::beta(P);
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    drift[c] = (P.potential == 1) ? (-(beta * x[c]) + f[c]) : f[c];
+    zz[c] = z[c];
+  }
+  if (P.constraint == 1) {
+    T a = T(0), b = T(0);
+#pragma unroll
+    for (int c = 0; c < D; ++c) { a += drift[c] * x[c]; b += zz[c] * x[c]; }
+#pragma unroll
+    for (int c = 0; c < D; ++c) { drift[c] -= a * x[c]; zz[c] -= b * x[c]; }
+  }
+  const T dt = Prm<T>::dt(P), sq = Prm<T>::sq(P);
+#pragma unroll
+  for (int c = 0; c < D; ++c) xn[c] = x[c] + dt * drift[c] + sq * zz[c];
+  if (normalise && P.constraint == 1) renormalise<T, D>(xn);
+}
+
+// exact pair flow (Dyson 922-943, Coulomb 1029-1045, with
+// the 1/2 of reading D:3): returns y for the member `first` (true) or second.
+template <typename T, int D, int KK>
+__device__ __forceinline__ void pair_flow(const T (&xi)[D], const T (&xj)[D], bool first,
+                                          T (&y)[D], const DevParams& P) {
+  T Dv[D], mid[D], Dn[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) { Dv[c] = xi[c] - xj[c]; mid[c] = T(0.5) * (xi[c] + xj[c]); }
+  const T dt = Prm<T>::dt(P);
+  if (KK == KK_DYSON) {
+    const T s = Dv[0] >= T(0) ? T(1) : T(-1);
+    Dn[0] = s * sqrt(Dv[0] * Dv[0] + T(4) * dt);
+#pragma unroll
+    for (int c = 1; c < D; ++c) Dn[c] = T(0);
+  } else {  // KK_COULOMB
+    T r2 = Dv[0] * Dv[0];
+#pragma unroll
+    for (int c = 1; c < D; ++c) r2 += Dv[c] * Dv[c];
+    const T r = sqrt(r2);
+    const T rn = cbrt(r2 * r + T(6) * dt);
+#pragma unroll
+    for (int c = 0; c < D; ++c) Dn[c] = (r == T(0)) ? (c == 0 ? rn : T(0)) : Dv[c] / r * rn;
+  }
+  const T sg = first ? T(0.5) : T(-0.5);
+#pragma unroll
+  for (int c = 0; c < D; ++c) y[c] = mid[c] + sg * Dn[c];
+}
+
+// second half of the splitting: x' = y - dt grad V(y) + sq z
+template <typename T, int D>
+__device__ __forceinline__ void split_finish(const T (&y)[D], const T (&z)[D], T (&xn)[D],
+                                             const DevParams& P, bool normalise) {
+  const T dt = Prm<T>::dt(P), sq = Prm<T>::sq(P), beta = Prm<T>::beta(P);
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    const T g = (P.potential == 1) ? beta * y[c] : T(0);
+    xn[c] = y[c] - dt * g + sq * z[c];
+  }
+  if (normalise && P.constraint == 1) renormalise<T, D>(xn);
+}
+
+template <typename T, int D>
+__device__ __forceinline__ void check_finite(const T (&x)[D], const DevParams& P, uint32_t id,
+                                             uint32_t m) {
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < D; ++c) ok = ok && isfinite(x[c]);
+  if (!ok) atomicMin(P.nonfinite, ((unsigned long long)m << 32) | id);
+}
+
+}  // namespace rbm

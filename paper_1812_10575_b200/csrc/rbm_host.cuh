@@ -1,0 +1,409 @@
+#pragma once
+// rbm_host.cuh -- host-side engine shared by rbm_api.cu and the per-dtype
+// instantiation units rbm_engines_f32.cu / rbm_engines_f64.cu.
+//
+// Host orchestration only: validation, bucket-layout choice, workspace
+// carving, per-config kernel dispatch, CUDA-graph capture/replay of steps.
+// Every arithmetic step of the RBM path runs in the kernels of
+// rbm_kernels.cuh; there is no CPU fallback.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/rbm.h"
+#include "rbm_kernels.cuh"
+
+using namespace rbm;
+
+namespace rbmhost {
+
+extern thread_local std::string g_err;  // failures without a context
+
+struct Workspace {
+  unsigned char* base = nullptr;
+  size_t size = 0, used = 0;
+  template <typename U>
+  U* take(size_t count) {
+    used = (used + 255) & ~size_t(255);
+    U* p = reinterpret_cast<U*>(base ? base + used : nullptr);
+    used += count * sizeof(U);
+    return p;
+  }
+};
+
+struct Layout {
+  uint32_t B = 0, b1 = 0, b2 = 0, nbuckets = 1, cap = 0;
+};
+
+struct EngineBase;
+
+}  // namespace rbmhost
+using namespace rbmhost;
+
+struct rbm_ctx {
+  rbm_config cfg{};
+  Layout L;
+  DevParams P{};
+  cudaStream_t stream = nullptr;       // caller's stream
+  cudaStream_t cap_stream = nullptr;   // private, for graph capture
+  int device = 0;
+  std::unique_ptr<EngineBase> eng;
+  // workspace carve
+  void* xbuf[2] = {nullptr, nullptr};
+  uint32_t* idbuf[2] = {nullptr, nullptr};
+  uint32_t* zero_block = nullptr;  // hist1[1024] + big_claim
+  size_t zero_bytes = 0;
+  uint32_t *hist1 = nullptr, *off1 = nullptr, *cur1 = nullptr, *tile_off = nullptr;
+  uint32_t *hist2 = nullptr, *cur2 = nullptr, *S = nullptr;
+  uint64_t* step_dev = nullptr;
+  unsigned long long* nonfinite = nullptr;
+  uint32_t* capacity_err = nullptr;
+  unsigned char* big_scratch = nullptr;
+  // RBM-r
+  uint32_t *js = nullptr, *rcnt = nullptr, *roff = nullptr, *rfill = nullptr, *rlst = nullptr,
+           *rparts = nullptr;
+  void* rdelta = nullptr;
+  uint64_t nbatch = 0, nslots = 0;
+  // state
+  int cur = 0;
+  uint64_t step = 0;
+  uint32_t launches = 0;
+  int tile = 4096;
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  uint32_t graph_steps = 1;
+  // optional per-kernel CUDA-event timing (rbm_timing_begin/end)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;
+  size_t ev_used = 0;
+  std::string err;
+  void mark(cudaStream_t s) {
+    if (timing && ev_used < ev.size()) cudaEventRecord(ev[ev_used++], s);
+  }
+};
+
+namespace rbmhost {
+
+inline rbm_status fail(rbm_ctx* c, rbm_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf; else g_err = buf;
+  return s;
+}
+
+#define CU(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(c, RBM_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                \
+  } while (0)
+
+inline uint32_t ceil_log2(double v) {
+  uint32_t b = 0;
+  while ((double)(1ull << b) < v) ++b;
+  return b;
+}
+
+inline size_t elt_size(const rbm_config& c) { return c.dtype == RBM_F64 ? 8 : 4; }
+
+inline Layout choose_layout(const rbm_config& c) {
+  Layout L;
+  const uint64_t n = c.n;
+  if (n <= 2048) {
+    L.B = 0;
+  } else {
+    L.B = ceil_log2((double)n / 2048.0);
+    if (L.B < 1) L.B = 1;
+    if (L.B > 18) L.B = 18;
+  }
+  if (L.B <= 10) { L.b1 = L.B; L.b2 = 0; }
+  else { L.b1 = (L.B + 1) / 2; L.b2 = L.B - L.b1; }
+  L.nbuckets = 1u << L.B;
+  if (L.B == 0) {
+    L.cap = (uint32_t)((n + 31) & ~31ull);
+  } else {
+    const double mu = (double)n / L.nbuckets;
+    L.cap = (uint32_t)(mu + 8.0 * std::sqrt(mu) + 64.0);
+    L.cap = (L.cap + 31) & ~31u;
+  }
+  if (c.debug_bucket_cap) L.cap = c.debug_bucket_cap;
+  return L;
+}
+
+inline size_t bucket_smem(const rbm_config& c, uint32_t cap) {
+  return 576 * 4 + (size_t)cap * (c.d * elt_size(c) + 8 + 4);
+}
+
+inline rbm_status validate(const rbm_config* cfg) {
+  rbm_ctx* c = nullptr;
+  if (!cfg) return fail(c, RBM_ERR_INVALID_ARG, "cfg is NULL");
+  const rbm_config& k = *cfg;
+  if (k.abi_version != RBM_ABI_VERSION)
+    return fail(c, RBM_ERR_INVALID_ARG, "abi_version %u != %u", k.abi_version, RBM_ABI_VERSION);
+  if (k.dtype > RBM_F64) return fail(c, RBM_ERR_INVALID_ARG, "dtype %u", k.dtype);
+  if (k.d < 1 || k.d > 3) return fail(c, RBM_ERR_INVALID_ARG, "d=%u not in 1..3", k.d);
+  if (k.n < 2 || k.n > (1ull << 31)) return fail(c, RBM_ERR_INVALID_ARG, "n=%llu not in 2..2^31", (unsigned long long)k.n);
+  if (k.p < 2 || k.p > k.n) return fail(c, RBM_ERR_INVALID_ARG, "p=%u must satisfy 2 <= p <= n", k.p);
+  if (k.p > 64 && !(k.p == k.n && k.n <= 2048))
+    return fail(c, RBM_ERR_INVALID_ARG, "p=%u: need p <= 64, or p == n <= 2048", k.p);
+  if (k.scheme > RBM_SCHEME_RBMR) return fail(c, RBM_ERR_INVALID_ARG, "scheme %u", k.scheme);
+  if (k.integrator > RBM_INTEG_SPLIT_EXACT_PAIR) return fail(c, RBM_ERR_INVALID_ARG, "integrator %u", k.integrator);
+  if (k.kernel > RBM_K_SMOOTH_TEST) return fail(c, RBM_ERR_UNKNOWN_KERNEL, "kernel %u not in registry", k.kernel);
+  if (k.potential > RBM_V_HARMONIC) return fail(c, RBM_ERR_UNKNOWN_KERNEL, "potential %u not in registry", k.potential);
+  if (k.constraint > RBM_CONSTRAINT_UNIT_SPHERE) return fail(c, RBM_ERR_INVALID_ARG, "constraint %u", k.constraint);
+  if (k.kernel == RBM_K_DYSON && k.d != 1) return fail(c, RBM_ERR_INVALID_ARG, "Dyson kernel needs d=1");
+  if (k.kernel == RBM_K_COULOMB && k.d != 3) return fail(c, RBM_ERR_INVALID_ARG, "Coulomb kernel needs d=3");
+  if (k.constraint == RBM_CONSTRAINT_UNIT_SPHERE && k.d != 3) return fail(c, RBM_ERR_INVALID_ARG, "sphere constraint needs d=3");
+  if (k.integrator == RBM_INTEG_SPLIT_EXACT_PAIR) {
+    if (k.p != 2) return fail(c, RBM_ERR_INVALID_ARG, "split integrator needs p=2");
+    if (k.kernel != RBM_K_DYSON && k.kernel != RBM_K_COULOMB)
+      return fail(c, RBM_ERR_INVALID_ARG, "split integrator needs the Dyson or Coulomb kernel");
+    if (k.scheme == RBM_SCHEME_RBM1 && (k.n % 2))
+      return fail(c, RBM_ERR_INVALID_ARG, "split integrator with RBM-1 needs even n");
+  }
+  if (!(k.sigma >= 0.0) || !std::isfinite(k.sigma)) return fail(c, RBM_ERR_INVALID_ARG, "sigma must be finite and >= 0");
+  if (!(k.dt > 0.0) || !std::isfinite(k.dt)) return fail(c, RBM_ERR_INVALID_ARG, "dt must be finite and > 0");
+  if (k.kernel == RBM_K_COULOMB_REG && !(k.kparam[0] > 0.0)) return fail(c, RBM_ERR_INVALID_ARG, "coulomb_reg needs kparam[0]=eps > 0");
+  if (k.kernel == RBM_K_BOUNDED_CONFIDENCE && !(k.kparam[1] > 0.0)) return fail(c, RBM_ERR_INVALID_ARG, "bounded confidence needs kparam[1]=radius > 0");
+  if (k.init > RBM_INIT_GAUSS_MIXTURE) return fail(c, RBM_ERR_INVALID_ARG, "init %u", k.init);
+  if (k.init == RBM_INIT_UNIFORM_SPHERE && k.d != 3) return fail(c, RBM_ERR_INVALID_ARG, "sphere init needs d=3");
+  if (k.init == RBM_INIT_GAUSS_MIXTURE && !(k.iparam[0] >= 1 && k.iparam[0] <= 64))
+    return fail(c, RBM_ERR_INVALID_ARG, "mixture needs 1 <= K <= 64");
+  if (k.replica >= (1u << 24)) return fail(c, RBM_ERR_INVALID_ARG, "replica must be < 2^24");
+  if (k.step0 + 1 >= (1ull << 32)) return fail(c, RBM_ERR_INVALID_ARG, "step0 must be < 2^32-1");
+  if (k.world_size != 1 || k.rank != 0)
+    return fail(c, RBM_ERR_UNSUPPORTED, "world_size=%d: multi-process partition mode is not in this build", k.world_size);
+  const Layout L = choose_layout(k);
+  if (k.scheme == RBM_SCHEME_RBM1 && bucket_smem(k, L.cap) > 227 * 1024)
+    return fail(c, RBM_ERR_INVALID_ARG, "bucket capacity %u needs %zu B of shared memory", L.cap, bucket_smem(k, L.cap));
+  return RBM_OK;
+}
+
+// carve (or size, when ws.base == nullptr) the workspace
+inline void carve(rbm_ctx& c, Workspace& ws) {
+  const rbm_config& k = c.cfg;
+  const size_t es = elt_size(k);
+  const uint64_t n = k.n;
+  for (int b = 0; b < 2; ++b) {
+    c.idbuf[b] = ws.take<uint32_t>(n);
+    c.xbuf[b] = ws.take<unsigned char>(n * k.d * es);
+  }
+  c.zero_block = ws.take<uint32_t>(1024 + 4);
+  c.zero_bytes = (1024 + 4) * 4;
+  c.hist1 = c.zero_block;
+  c.off1 = ws.take<uint32_t>(1025);
+  c.cur1 = ws.take<uint32_t>(1024);
+  c.tile_off = ws.take<uint32_t>(1025);
+  c.S = ws.take<uint32_t>((size_t)c.L.nbuckets + 1);
+  if (c.L.b2) {
+    c.hist2 = ws.take<uint32_t>(c.L.nbuckets);
+    c.cur2 = ws.take<uint32_t>(c.L.nbuckets);
+  }
+  c.step_dev = ws.take<uint64_t>(1);
+  c.nonfinite = ws.take<unsigned long long>(1);
+  c.capacity_err = ws.take<uint32_t>(1);
+  c.big_scratch = ws.take<unsigned char>(NBIG * ((size_t)BIG_CAP * (12 + k.d * es) + 64));
+  if (k.scheme == RBM_SCHEME_RBMR) {
+    c.nbatch = (n + k.p - 1) / k.p;
+    c.nslots = c.nbatch * k.p;
+    c.js = ws.take<uint32_t>(c.nslots);
+    c.rdelta = ws.take<unsigned char>(c.nslots * k.d * es);
+    c.rcnt = ws.take<uint32_t>(n);
+    c.rfill = ws.take<uint32_t>(n);
+    c.roff = ws.take<uint32_t>(n + 1);
+    c.rlst = ws.take<uint32_t>(c.nslots);
+    c.rparts = ws.take<uint32_t>((n + SCAN_TILE - 1) / SCAN_TILE + 1);
+  }
+  ws.used = (ws.used + 255) & ~size_t(255);
+}
+
+inline unsigned grid_for(uint64_t n, unsigned block, unsigned maxg = 148 * 16) {
+  uint64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > maxg) g = maxg;
+  return (unsigned)g;
+}
+
+struct EngineBase {
+  virtual ~EngineBase() {}
+  virtual rbm_status setup(rbm_ctx& c) = 0;
+  virtual void init_state(rbm_ctx& c, cudaStream_t s) = 0;
+  virtual void set_state(rbm_ctx& c, const void* x, cudaStream_t s) = 0;
+  virtual void step(rbm_ctx& c, cudaStream_t s) = 0;
+  virtual void gather(rbm_ctx& c, uint64_t i0, uint64_t i1, void* out, cudaStream_t s) = 0;
+};
+
+template <typename T, int D, int KK, int INTEG>
+struct Engine final : EngineBase {
+  static constexpr int SC_BLOCK = 256;
+  static constexpr int SC_ITEMS = (D * sizeof(T) <= 12) ? 16 : 8;
+  static constexpr int SC_TILE = SC_BLOCK * SC_ITEMS;
+  static constexpr int BK_BLOCK = 256;
+  size_t sc_smem = 0, bk_smem = 0;
+
+  State<T, D> st(rbm_ctx& c, int b) {
+    State<T, D> s;
+    s.id = c.idbuf[b];
+    T* x = reinterpret_cast<T*>(c.xbuf[b]);
+    for (int k = 0; k < 3; ++k) s.x[k] = x + (size_t)(k < D ? k : 0) * c.cfg.n;
+    return s;
+  }
+
+  rbm_status setup(rbm_ctx& c) override {
+    c.tile = SC_TILE;
+    sc_smem = (1024 + 1024 + 64) * 4 + (size_t)SC_TILE * (4 + 2 + D * sizeof(T));
+    bk_smem = bucket_smem(c.cfg, c.L.cap);
+    auto chk = [&](cudaError_t e, const char* what) -> rbm_status {
+      if (e != cudaSuccess) return fail(&c, RBM_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+      return RBM_OK;
+    };
+    rbm_status s;
+    if ((s = chk(cudaFuncSetAttribute(scatter_kernel<T, D, 1, SC_BLOCK, SC_ITEMS>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc_smem),
+                 "smem attr scatter1"))) return s;
+    if ((s = chk(cudaFuncSetAttribute(scatter_kernel<T, D, 2, SC_BLOCK, SC_ITEMS>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc_smem),
+                 "smem attr scatter2"))) return s;
+    if ((s = chk(cudaFuncSetAttribute(bucket_step_kernel<T, D, KK, INTEG, BK_BLOCK>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bk_smem),
+                 "smem attr bucket"))) return s;
+    return RBM_OK;
+  }
+
+  void init_state(rbm_ctx& c, cudaStream_t s) override {
+    const rbm_config& k = c.cfg;
+    init_kernel<T, D><<<grid_for(k.n, 256), 256, 0, s>>>(c.P, st(c, c.cur), k.init, k.iparam[0],
+                                                         k.iparam[1], k.iparam[2], k.iparam[3]);
+  }
+
+  void set_state(rbm_ctx& c, const void* x, cudaStream_t s) override {
+    set_state_kernel<T, D><<<grid_for(c.cfg.n, 256), 256, 0, s>>>(c.cfg.n, st(c, c.cur),
+                                                                  reinterpret_cast<const T*>(x));
+  }
+
+  void gather(rbm_ctx& c, uint64_t i0, uint64_t i1, void* out, cudaStream_t s) override {
+    gather_kernel<T, D><<<grid_for(c.cfg.n, 256), 256, 0, s>>>(c.cfg.n, st(c, c.cur), i0, i1,
+                                                                reinterpret_cast<T*>(out));
+  }
+
+  void step(rbm_ctx& c, cudaStream_t s) override {
+    if (c.cfg.scheme == RBM_SCHEME_RBMR) { step_rbmr(c, s); return; }
+    const DevParams& P = c.P;
+    const Layout& L = c.L;
+    State<T, D> src = st(c, c.cur), tmp = st(c, c.cur ^ 1);
+    const uint64_t n = c.cfg.n;
+    cudaMemsetAsync(c.zero_block, 0, c.zero_bytes, s);
+    if (L.B == 0) {
+      c.mark(s);
+      bucket_step_kernel<T, D, KK, INTEG, BK_BLOCK><<<1, BK_BLOCK, bk_smem, s>>>(P, src, tmp, c.S);
+      c.cur ^= 1;
+    } else {
+      c.mark(s);
+      hist_top_kernel<<<grid_for(n, 512, 148 * 4), 512, 0, s>>>(P, c.hist1);
+      c.mark(s);
+      scan_top_kernel<<<1, 1024, 0, s>>>(P, c.hist1, c.off1, c.cur1, c.tile_off, c.S, SC_TILE);
+      c.mark(s);
+      scatter_kernel<T, D, 1, SC_BLOCK, SC_ITEMS>
+          <<<(unsigned)((n + SC_TILE - 1) / SC_TILE), SC_BLOCK, sc_smem, s>>>(P, src, tmp, c.cur1,
+                                                                               nullptr, nullptr);
+      const unsigned straddle_grid = (unsigned)(((uint64_t)L.nbuckets * 32 + 255) / 256);
+      if (L.b2 == 0) {
+        c.mark(s);
+        bucket_step_kernel<T, D, KK, INTEG, BK_BLOCK><<<L.nbuckets, BK_BLOCK, bk_smem, s>>>(P, tmp, src, c.S);
+        c.mark(s);
+        straddle_kernel<T, D, KK, INTEG><<<straddle_grid, 256, 0, s>>>(P, src, c.S);
+      } else {
+        const unsigned tiles2 = (unsigned)((n + SC_TILE - 1) / SC_TILE + (1u << L.b1));
+        cudaMemsetAsync(c.hist2, 0, (size_t)L.nbuckets * 4, s);
+        c.mark(s);
+        hist_sub_kernel<<<tiles2, 256, 0, s>>>(P, tmp.id, c.off1, c.tile_off, c.hist2, SC_TILE);
+        c.mark(s);
+        scan_sub_kernel<<<1, 1024, 0, s>>>(P, c.hist2, c.S, c.cur2);
+        c.mark(s);
+        scatter_kernel<T, D, 2, SC_BLOCK, SC_ITEMS>
+            <<<tiles2, SC_BLOCK, sc_smem, s>>>(P, tmp, src, c.cur2, c.off1, c.tile_off);
+        c.mark(s);
+        bucket_step_kernel<T, D, KK, INTEG, BK_BLOCK><<<L.nbuckets, BK_BLOCK, bk_smem, s>>>(P, src, tmp, c.S);
+        c.mark(s);
+        straddle_kernel<T, D, KK, INTEG><<<straddle_grid, 256, 0, s>>>(P, tmp, c.S);
+        c.cur ^= 1;
+      }
+    }
+    c.mark(s);
+    advance_kernel<<<1, 1, 0, s>>>(c.step_dev);
+    c.mark(s);
+  }
+
+  void step_rbmr(rbm_ctx& c, cudaStream_t s) {
+    const DevParams& P = c.P;
+    const uint64_t n = c.cfg.n;
+    State<T, D> x = st(c, c.cur);
+    cudaMemsetAsync(c.rcnt, 0, n * 4, s);
+    cudaMemsetAsync(c.rfill, 0, n * 4, s);
+    c.mark(s);
+    rbmr_draw_kernel<<<grid_for(c.nbatch, 128), 128, 0, s>>>(P, c.nbatch, c.js, c.rcnt);
+    const unsigned nparts = (unsigned)((n + SCAN_TILE - 1) / SCAN_TILE);
+    c.mark(s);
+    scan_reduce_kernel<<<nparts, SCAN_BLOCK, 0, s>>>(c.rcnt, n, c.rparts);
+    c.mark(s);
+    scan_parts_kernel<<<1, 1024, 0, s>>>(c.rparts, nparts);
+    c.mark(s);
+    scan_down_kernel<<<nparts, SCAN_BLOCK, 0, s>>>(c.rcnt, n, c.rparts, c.roff);
+    c.mark(s);
+    rbmr_fill_kernel<<<grid_for(c.nslots, 256), 256, 0, s>>>(c.nslots, c.js, c.roff, c.rfill, c.rlst);
+    c.mark(s);
+    rbmr_delta_kernel<T, D, KK, INTEG><<<grid_for(c.nslots, 256), 256, 0, s>>>(
+        P, c.nslots, x, c.js, reinterpret_cast<T*>(c.rdelta));
+    c.mark(s);
+    rbmr_apply_kernel<T, D><<<grid_for(n, 256), 256, 0, s>>>(P, c.nslots, x, c.roff, c.rlst,
+                                                             reinterpret_cast<const T*>(c.rdelta));
+    c.mark(s);
+    advance_kernel<<<1, 1, 0, s>>>(c.step_dev);
+    c.mark(s);
+  }
+};
+
+template <typename T, int D>
+EngineBase* make_for_kernel(uint32_t kernel, uint32_t integ) {
+  switch (kernel) {
+    case RBM_K_ZERO: return new Engine<T, D, KK_ZERO, 0>();
+    case RBM_K_BOUNDED_CONFIDENCE: return new Engine<T, D, KK_BOUNDED, 0>();
+    case RBM_K_GAUSS_ATTR_REP: return new Engine<T, D, KK_GAUSS_AR, 0>();
+    case RBM_K_COULOMB_REG: return new Engine<T, D, KK_COULOMB_REG, 0>();
+    case RBM_K_SMOOTH_TEST: return new Engine<T, D, KK_SMOOTH, 0>();
+    case RBM_K_DYSON:
+      if (D == 1) return integ ? (EngineBase*)new Engine<T, 1, KK_DYSON, 1>() : new Engine<T, 1, KK_DYSON, 0>();
+      return nullptr;
+    case RBM_K_COULOMB:
+      if (D == 3) return integ ? (EngineBase*)new Engine<T, 3, KK_COULOMB, 1>() : new Engine<T, 3, KK_COULOMB, 0>();
+      return nullptr;
+  }
+  return nullptr;
+}
+
+inline const char* const* kernel_names(const rbm_ctx& c, uint32_t* count) {
+  static const char* const r[] = {"rbmr_draw", "scan_reduce", "scan_parts", "scan_down",
+                                  "rbmr_fill", "rbmr_delta", "rbmr_apply", "advance"};
+  static const char* const b0[] = {"bucket_step", "advance"};
+  static const char* const p1[] = {"hist_top", "scan_top", "scatter_top", "bucket_step",
+                                   "straddle", "advance"};
+  static const char* const p2[] = {"hist_top", "scan_top", "scatter_top", "hist_sub", "scan_sub",
+                                   "scatter_sub", "bucket_step", "straddle", "advance"};
+  if (c.cfg.scheme == RBM_SCHEME_RBMR) { *count = 8; return r; }
+  if (c.L.B == 0) { *count = 2; return b0; }
+  if (c.L.b2 == 0) { *count = 6; return p1; }
+  *count = 9;
+  return p2;
+}
+
+EngineBase* make_engine_f32(const rbm_config& k);
+EngineBase* make_engine_f64(const rbm_config& k);
+
+}  // namespace rbmhost

