@@ -65,6 +65,9 @@ rbm_status init_impl(rbm_ctx* c, const rbm_config* cfg, void* wsp, size_t ws_byt
   DevParams& P = c->P;
   P.n = cfg->n;
   P.p = cfg->p;
+  P.pdiv = make_fastdiv(cfg->p);
+  P.nfull = (uint32_t)(cfg->n / cfg->p);
+  P.rem = (uint32_t)(cfg->n % cfg->p);
   P.seed_lo = (uint32_t)cfg->seed;
   P.seed_hi = (uint32_t)(cfg->seed >> 32);
   P.rep_hi = cfg->replica << 8;
@@ -78,6 +81,8 @@ rbm_status init_impl(rbm_ctx* c, const rbm_config* cfg, void* wsp, size_t ws_byt
   P.sq = cfg->sigma * std::sqrt(cfg->dt);
   P.kp0f = (float)P.kp0; P.kp1f = (float)P.kp1; P.betaf = (float)P.beta;
   P.dtf = (float)P.dt; P.sqf = (float)P.sq;
+  P.invp = 1.0 / (double)(cfg->p - 1);
+  P.invpf = (float)P.invp;
   P.B = c->L.B; P.b1 = c->L.b1; P.b2 = c->L.b2; P.nbuckets = c->L.nbuckets; P.cap = c->L.cap;
   P.step = c->step_dev;
   P.nonfinite = c->nonfinite;

@@ -15,10 +15,32 @@ enum : uint32_t { TAG_KEY = 0, TAG_NOISE = 1, TAG_INIT = 2, TAG_INIT_AUX = 3,
 enum : int { KK_ZERO = 0, KK_DYSON = 1, KK_COULOMB = 2, KK_BOUNDED = 3,
              KK_GAUSS_AR = 4, KK_COULOMB_REG = 5, KK_SMOOTH = 6 };
 
+// exact u32 division by a runtime-invariant divisor (Granlund-Montgomery):
+// q = n / d for every 32-bit n.
+struct FastDiv {
+  uint32_t d, m, s;  // s = ceil(log2 d)
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f{d, 0u, 0u};
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  f.s = l;
+  f.m = (d == 1) ? 0u : (uint32_t)((((1ull << 32) * ((1ull << l) - d)) / d) + 1ull);
+  return f;
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  if (f.s == 0) return n;
+  const uint32_t t = __umulhi(n, f.m);
+  return (t + ((n - t) >> 1)) >> (f.s - 1);
+}
+
 // Everything a kernel needs about the configuration; passed by value.
 struct DevParams {
   uint64_t n;          // N
   uint32_t p;          // batch size
+  FastDiv pdiv;        // division by p
+  uint32_t nfull;      // floor(N/p)
+  uint32_t rem;        // N mod p (remainder rule, D:7)
   uint32_t seed_lo, seed_hi;
   uint32_t rep_hi;     // replica << 8, OR-ed into counter word 3
   uint32_t potential;  // 0 none, 1 harmonic
@@ -27,6 +49,8 @@ struct DevParams {
   // model constants in both precisions
   double kp0, kp1, beta, dt, sq;   // sq = sigma*sqrt(dt)
   float kp0f, kp1f, betaf, dtf, sqf;
+  double invp;         // 1/(p-1): prefactor of a regular batch (Eq. 2.2)
+  float invpf;
   // bucket layout of the partition
   uint32_t B;          // prefix bits of the final buckets
   uint32_t b1, b2;     // digit bits of scatter passes 1 and 2 (b2 = 0: one pass)
@@ -35,12 +59,47 @@ struct DevParams {
   const uint64_t* step;     // device step counter m
   unsigned long long* nonfinite;  // atomicMin of (m<<32 | id); ~0 if clean
   uint32_t* capacity_err;         // set to 1 if a bucket overflowed every fallback
-  uint32_t* big_claim;            // slot counter of the global-scratch fallback
+  uint32_t* big_claim;            // NBIG slot flags of the global-scratch fallback
   unsigned char* big_scratch;     // NBIG slots of BIG_CAP elements
 };
 
 constexpr int NBIG = 2;             // concurrent oversized buckets handled per step
 constexpr uint32_t BIG_CAP = 65535; // u16 indices
+// bytes of one oversized-bucket scratch slot (256-B aligned stride)
+__host__ __device__ constexpr size_t big_slot_bytes(size_t rec_x_bytes) {
+  return (((size_t)BIG_CAP * (18 + rec_x_bytes) + 64) + 255) & ~(size_t)255;
+}
+
+// ------------------------------------------------- TMA bulk copy + mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+// 1-D bulk copy global -> shared (TMA, SASS UBLKCP); 16-B aligned, size % 16 == 0
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
 
 // ----------------------------------------------------------------- Philox
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
@@ -77,10 +136,13 @@ __device__ __forceinline__ double u01d(uint32_t a, uint32_t b) {
 }
 
 // ------------------------------------------------------------ Box-Muller
+// fp32: MUFU-based (lg2.approx, sin/cos.approx on [0, 2pi)); the radius is
+// clamped at 0 so u1 -> 1 can never produce a NaN.  Absolute error of z is
+// ~1e-6, far inside the fp32 parity bar.
 __device__ __forceinline__ void bm_pair(float u1, float u2, float& z0, float& z1) {
-  const float r = sqrtf(-2.0f * logf(u1));
+  const float r = sqrtf(fmaxf(-1.3862943611198906f * __log2f(u1), 0.0f));  // -2 ln u1
   float s, c;
-  sincospif(2.0f * u2, &s, &c);
+  __sincosf(6.2831853071795865f * u2, &s, &c);
   z0 = r * c;
   z1 = r * s;
 }
@@ -134,6 +196,7 @@ template <> struct Prm<float> {
   __device__ __forceinline__ static float beta(const DevParams& P) { return P.betaf; }
   __device__ __forceinline__ static float dt(const DevParams& P) { return P.dtf; }
   __device__ __forceinline__ static float sq(const DevParams& P) { return P.sqf; }
+  __device__ __forceinline__ static float invp(const DevParams& P) { return P.invpf; }
 };
 template <> struct Prm<double> {
   __device__ __forceinline__ static double kp0(const DevParams& P) { return P.kp0; }
@@ -141,6 +204,7 @@ template <> struct Prm<double> {
   __device__ __forceinline__ static double beta(const DevParams& P) { return P.beta; }
   __device__ __forceinline__ static double dt(const DevParams& P) { return P.dt; }
   __device__ __forceinline__ static double sq(const DevParams& P) { return P.sq; }
+  __device__ __forceinline__ static double invp(const DevParams& P) { return P.invp; }
 };
 
 __device__ __forceinline__ float inv_cube_sqrt(float q) { const float r = rsqrtf(q); return r * r * r; }

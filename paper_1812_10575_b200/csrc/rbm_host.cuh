@@ -30,7 +30,7 @@ struct Workspace {
   U* take(size_t count) {
     used = (used + 255) & ~size_t(255);
     U* p = reinterpret_cast<U*>(base ? base + used : nullptr);
-    used += count * sizeof(U);
+    used += count * sizeof(U) + 64;  // slack: TMA windows may read 16 B past the end
     return p;
   }
 };
@@ -54,6 +54,7 @@ struct rbm_ctx {
   std::unique_ptr<EngineBase> eng;
   // workspace carve
   void* xbuf[2] = {nullptr, nullptr};
+  uint64_t xstride = 0;  // elements between coordinate arrays of one state buffer
   uint32_t* idbuf[2] = {nullptr, nullptr};
   uint32_t* zero_block = nullptr;  // hist1[1024] + big_claim
   size_t zero_bytes = 0;
@@ -130,7 +131,7 @@ inline Layout choose_layout(const rbm_config& c) {
     L.cap = (uint32_t)((n + 31) & ~31ull);
   } else {
     const double mu = (double)n / L.nbuckets;
-    L.cap = (uint32_t)(mu + 8.0 * std::sqrt(mu) + 64.0);
+    L.cap = (uint32_t)(mu + 6.0 * std::sqrt(mu) + 32.0);
     L.cap = (L.cap + 31) & ~31u;
   }
   if (c.debug_bucket_cap) L.cap = c.debug_bucket_cap;
@@ -138,7 +139,9 @@ inline Layout choose_layout(const rbm_config& c) {
 }
 
 inline size_t bucket_smem(const rbm_config& c, uint32_t cap) {
-  return 576 * 4 + (size_t)cap * (c.d * elt_size(c) + 8 + 4);
+  const size_t es = elt_size(c);
+  return 2320 + (size_t)(cap + 8) * 4 + c.d * ((((size_t)(cap + 8) * es) + 15) & ~(size_t)15) +
+         (size_t)cap * 12 + (((size_t)cap * 2 + 15) & ~(size_t)15);
 }
 
 inline rbm_status validate(const rbm_config* cfg) {
@@ -191,9 +194,10 @@ inline void carve(rbm_ctx& c, Workspace& ws) {
   const rbm_config& k = c.cfg;
   const size_t es = elt_size(k);
   const uint64_t n = k.n;
+  c.xstride = (n + 63) & ~63ull;  // per-coordinate stride: 256-B aligned SoA arrays (TMA)
   for (int b = 0; b < 2; ++b) {
     c.idbuf[b] = ws.take<uint32_t>(n);
-    c.xbuf[b] = ws.take<unsigned char>(n * k.d * es);
+    c.xbuf[b] = ws.take<unsigned char>(c.xstride * k.d * es);
   }
   c.zero_block = ws.take<uint32_t>(1024 + 4);
   c.zero_bytes = (1024 + 4) * 4;
@@ -209,7 +213,7 @@ inline void carve(rbm_ctx& c, Workspace& ws) {
   c.step_dev = ws.take<uint64_t>(1);
   c.nonfinite = ws.take<unsigned long long>(1);
   c.capacity_err = ws.take<uint32_t>(1);
-  c.big_scratch = ws.take<unsigned char>(NBIG * ((size_t)BIG_CAP * (12 + k.d * es) + 64));
+  c.big_scratch = ws.take<unsigned char>(NBIG * big_slot_bytes(k.d * es));
   if (k.scheme == RBM_SCHEME_RBMR) {
     c.nbatch = (n + k.p - 1) / k.p;
     c.nslots = c.nbatch * k.p;
@@ -252,7 +256,7 @@ struct Engine final : EngineBase {
     State<T, D> s;
     s.id = c.idbuf[b];
     T* x = reinterpret_cast<T*>(c.xbuf[b]);
-    for (int k = 0; k < 3; ++k) s.x[k] = x + (size_t)(k < D ? k : 0) * c.cfg.n;
+    for (int k = 0; k < 3; ++k) s.x[k] = x + (size_t)(k < D ? k : 0) * c.xstride;
     return s;
   }
 
@@ -260,6 +264,8 @@ struct Engine final : EngineBase {
     c.tile = SC_TILE;
     sc_smem = (1024 + 1024 + 64) * 4 + (size_t)SC_TILE * (4 + 2 + D * sizeof(T));
     bk_smem = bucket_smem(c.cfg, c.L.cap);
+    if (bk_smem != bucket_smem_bytes<T, D>(c.L.cap))
+      return fail(&c, RBM_ERR_STATE, "bucket smem size mismatch %zu vs %zu", bk_smem, bucket_smem_bytes<T, D>(c.L.cap));
     auto chk = [&](cudaError_t e, const char* what) -> rbm_status {
       if (e != cudaSuccess) return fail(&c, RBM_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
       return RBM_OK;
@@ -325,7 +331,7 @@ struct Engine final : EngineBase {
         c.mark(s);
         hist_sub_kernel<<<tiles2, 256, 0, s>>>(P, tmp.id, c.off1, c.tile_off, c.hist2, SC_TILE);
         c.mark(s);
-        scan_sub_kernel<<<1, 1024, 0, s>>>(P, c.hist2, c.S, c.cur2);
+        scan_sub_kernel<<<1u << L.b1, 512, 0, s>>>(P, c.hist2, c.off1, c.S, c.cur2);
         c.mark(s);
         scatter_kernel<T, D, 2, SC_BLOCK, SC_ITEMS>
             <<<tiles2, SC_BLOCK, sc_smem, s>>>(P, tmp, src, c.cur2, c.off1, c.tile_off);

@@ -61,13 +61,13 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t* a, int n, uint32_t
   return total;
 }
 
-// position P's batch (reading D:7): returns [b0, b1)
-__device__ __forceinline__ void batch_range(uint64_t P, uint64_t n, uint32_t p, uint64_t& b0,
-                                            uint64_t& b1) {
-  const uint64_t nfull = n / p, r = n - nfull * p;
-  uint64_t k = P / p;
-  if (r == 1 && k >= nfull - 1) {
-    k = nfull - 1;
+// position P's batch (reading D:7): returns [b0, b1).  N < 2^32.
+__device__ __forceinline__ void batch_range(uint32_t P, const DevParams& prm, uint32_t& b0,
+                                            uint32_t& b1) {
+  const uint32_t n = (uint32_t)prm.n, p = prm.p;
+  uint32_t k = fdiv(P, prm.pdiv);
+  if (prm.rem == 1 && k + 1 >= prm.nfull) {
+    k = prm.nfull - 1;
     b0 = k * p;
     b1 = n;
   } else {
@@ -216,33 +216,22 @@ static __global__ void __launch_bounds__(1024) scan_top_kernel(DevParams P, cons
   }
 }
 
-// single block: S = excl-scan over all 2^B final buckets; cursor2 = S
-static __global__ void __launch_bounds__(1024) scan_sub_kernel(DevParams P, const uint32_t* __restrict__ hist2,
-                                                        uint32_t* S, uint32_t* cur2) {
-  __shared__ uint32_t ws[34];
-  const uint32_t nb = P.nbuckets;
-  const uint32_t per = (nb + 1023) / 1024;
-  const uint32_t b0 = min(nb, threadIdx.x * per), b1 = min(nb, b0 + per);
-  uint32_t s = 0;
-  for (uint32_t i = b0; i < b1; ++i) s += hist2[i];
-  const uint32_t inc = warp_incl_scan(s);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (lane == 31) ws[w] = inc;
+// one block per top bucket u: S[u<<b2 | i] = off1[u] + excl-scan_i hist2[u<<b2 | .]
+static __global__ void __launch_bounds__(512) scan_sub_kernel(DevParams P, const uint32_t* __restrict__ hist2,
+                                                              const uint32_t* __restrict__ off1,
+                                                              uint32_t* S, uint32_t* cur2) {
+  __shared__ uint32_t a[512];
+  __shared__ uint32_t ws[33];
+  const uint32_t u = blockIdx.x, nb2 = 1u << P.b2, base = u << P.b2;
+  for (uint32_t i = threadIdx.x; i < nb2; i += blockDim.x) a[i] = hist2[base + i];
   __syncthreads();
-  if (w == 0) {
-    const uint32_t v = ws[lane];
-    const uint32_t vi = warp_incl_scan(v);
-    ws[lane] = vi - v;
+  block_excl_scan<512>(a, nb2, ws);
+  const uint32_t o = off1[u];
+  for (uint32_t i = threadIdx.x; i < nb2; i += blockDim.x) {
+    S[base + i] = o + a[i];
+    cur2[base + i] = o + a[i];
   }
-  __syncthreads();
-  uint32_t run = ws[w] + inc - s;
-  for (uint32_t i = b0; i < b1; ++i) {
-    const uint32_t v = hist2[i];
-    S[i] = run;
-    cur2[i] = run;
-    run += v;
-  }
-  if (threadIdx.x == 0) S[nb] = (uint32_t)P.n;
+  if (u == 0 && threadIdx.x == 0) S[P.nbuckets] = (uint32_t)P.n;
 }
 
 // tile t of a bucket-aligned pass: bucket u and element range [lo, hi)
@@ -371,11 +360,14 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(DevParams P, Stat
 // One CTA per final bucket b = positions [S[b], S[b+1]).  All ids in it share
 // the top B key bits, so sorting it by (key, id) in shared memory puts every
 // element at its exact global sorted position S[b] + rank.
+template <typename T> __device__ __forceinline__ T batch_inv(const DevParams& P, uint32_t sz) {
+  return (sz == P.p) ? Prm<T>::invp(P) : T(1) / T(sz - 1);
+}
+
 template <typename T, int D, int KK, int INTEG>
-__device__ __forceinline__ void interior_update(const DevParams& P, uint32_t m, uint64_t P0,
-                                                uint64_t b0, uint64_t b1, uint32_t q,
-                                                const uint16_t* ord, const T* const* xs,
-                                                uint32_t id, T (&xn)[D]) {
+__device__ __forceinline__ void interior_update(const DevParams& P, uint32_t m, uint32_t q,
+                                                uint32_t l0, uint32_t l1, const uint16_t* ord,
+                                                T* const* xs, uint32_t id, T (&xn)[D]) {
   T xi[D];
   const uint32_t e = ord[q];
 #pragma unroll
@@ -388,82 +380,76 @@ __device__ __forceinline__ void interior_update(const DevParams& P, uint32_t m, 
     T f[D];
 #pragma unroll
     for (int c = 0; c < D; ++c) f[c] = T(0);
-    for (uint64_t g = b0; g < b1; ++g) {
-      if (g == P0) continue;
-      const uint32_t e2 = ord[(uint32_t)(g - (P0 - q))];
+    for (uint32_t g = l0; g < l1; ++g) {  // ascending sorted position, self skipped
+      if (g == q) continue;
+      const uint32_t e2 = ord[g];
       T xj[D];
 #pragma unroll
       for (int c = 0; c < D; ++c) xj[c] = xs[c][e2];
       add_interaction<T, D, KK>(xi, xj, f, P);
     }
-    const T inv = T(1) / T((uint32_t)(b1 - b0 - 1));
+    const T inv = batch_inv<T>(P, l1 - l0);
 #pragma unroll
     for (int c = 0; c < D; ++c) f[c] *= inv;
     em_update<T, D>(xi, f, z, xn, P, true);
   } else {
-    const uint32_t ea = ord[(uint32_t)(b0 - (P0 - q))], eb = ord[(uint32_t)(b0 + 1 - (P0 - q))];
+    const uint32_t ea = ord[l0], eb = ord[l0 + 1];
     T xa[D], xb[D], y[D];
 #pragma unroll
     for (int c = 0; c < D; ++c) { xa[c] = xs[c][ea]; xb[c] = xs[c][eb]; }
-    pair_flow<T, D, KK>(xa, xb, P0 == b0, y, P);
+    pair_flow<T, D, KK>(xa, xb, q == l0, y, P);
     split_finish<T, D>(y, z, xn, P, true);
   }
 }
 
+// Sort the loaded bucket by (key, id) and step every interior batch.
+//   id_l, xs : bucket records in load order (n of them)
+//   key_l    : n u32 scratch;  ks : n u64 scratch (16-B aligned);  ord : n u16
 template <typename T, int D, int KK, int INTEG, int BLOCK>
-__device__ __forceinline__ void bucket_body(const DevParams& P, State<T, D> src, State<T, D> dst,
-                                            uint32_t s0, uint32_t n, uint32_t* key_l,
-                                            uint32_t* id_l, T* xbase, uint16_t* ord, uint16_t* lst,
-                                            uint32_t cap, uint32_t* cnt, uint32_t* off,
-                                            uint32_t* wsum) {
+__device__ __forceinline__ void bucket_compute(const DevParams& P, State<T, D> dst, uint32_t s0,
+                                               uint32_t n, const uint32_t* id_l, T* const* xs,
+                                               uint32_t* key_l, unsigned long long* ks,
+                                               uint16_t* ord, uint32_t* cnt, uint32_t* off,
+                                               uint32_t* wsum) {
   const uint32_t m = (uint32_t)*P.step;
-  T* xs[3];
-#pragma unroll
-  for (int c = 0; c < D; ++c) xs[c] = xbase + (size_t)c * cap;
-  for (uint32_t i = threadIdx.x; i < 256; i += BLOCK) cnt[i] = 0;
-  __syncthreads();
-  // 1. load the bucket, recompute keys; 2. counting sort by the next 8 key bits
+  // 1. keys (Philox), counting sort by the next 8 key bits below the B-bit prefix
   const uint32_t sh = (P.B <= 24u) ? (24u - P.B) : 0u;
   for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
-    const uint32_t id = src.id[s0 + e];
-    const uint32_t key = shuffle_key(P, id, m);
+    const uint32_t key = shuffle_key(P, id_l[e], m);
     key_l[e] = key;
-    id_l[e] = id;
-#pragma unroll
-    for (int c = 0; c < D; ++c) xs[c][e] = src.x[c][s0 + e];
     ord[e] = (uint16_t)atomicAdd(&cnt[(key >> sh) & 255u], 1u);
   }
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < 256; i += BLOCK) off[i] = cnt[i];
   __syncthreads();
   block_excl_scan<BLOCK>(off, 256, wsum);
-  for (uint32_t e = threadIdx.x; e < n; e += BLOCK)
-    lst[off[(key_l[e] >> sh) & 255u] + ord[e]] = (uint16_t)e;
-  __syncthreads();
-  // 3. exact rank inside the sub-bucket by (key, id)
+  // 2. composite (key, id) keys grouped by sub-digit, contiguous per sub-bucket
   for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
-    const uint32_t key = key_l[e], id = id_l[e];
+    const uint32_t key = key_l[e];
+    ks[off[(key >> sh) & 255u] + ord[e]] = ((unsigned long long)key << 32) | id_l[e];
+  }
+  __syncthreads();
+  // 3. exact rank = sub-bucket offset + #smaller composites in the sub-bucket
+  for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
+    const uint32_t key = key_l[e];
+    const unsigned long long mine = ((unsigned long long)key << 32) | id_l[e];
     const uint32_t sd = (key >> sh) & 255u;
     const uint32_t a = off[sd], c = cnt[sd];
     uint32_t r = a;
-    for (uint32_t j = a; j < a + c; ++j) {
-      const uint32_t e2 = lst[j];
-      const uint32_t k2 = key_l[e2];
-      r += (k2 < key) || (k2 == key && id_l[e2] < id);
-    }
+    for (uint32_t j = a; j < a + c; ++j) r += (ks[j] < mine) ? 1u : 0u;
     ord[r] = (uint16_t)e;
   }
   __syncthreads();
   // 4. batches inside [s0, s0+n): Eq. (2.2) + update; straddling ones copied through
   for (uint32_t q = threadIdx.x; q < n; q += BLOCK) {
-    const uint64_t P0 = (uint64_t)s0 + q;
-    uint64_t b0, b1;
-    batch_range(P0, P.n, P.p, b0, b1);
+    const uint32_t P0 = s0 + q;
+    uint32_t b0, b1;
+    batch_range(P0, P, b0, b1);
     const uint32_t e = ord[q];
     const uint32_t id = id_l[e];
     T xn[D];
-    if (b0 >= s0 && b1 <= (uint64_t)s0 + n) {
-      interior_update<T, D, KK, INTEG>(P, m, P0, b0, b1, q, ord, xs, id, xn);
+    if (b0 >= s0 && b1 <= s0 + n) {
+      interior_update<T, D, KK, INTEG>(P, m, q, b0 - s0, b1 - s0, ord, xs, id, xn);
       check_finite<T, D>(xn, P, id, m);
     } else {
 #pragma unroll
@@ -475,26 +461,63 @@ __device__ __forceinline__ void bucket_body(const DevParams& P, State<T, D> src,
   }
 }
 
+// shared-memory bytes of the bucket kernel for capacity `cap`
+template <typename T, int D> __host__ __device__ constexpr size_t bucket_smem_bytes(uint32_t cap) {
+  return 2304 + 16                                  // cnt, off, wsum; mbarrier
+         + (size_t)(cap + 8) * 4                    // ids (TMA window)
+         + (size_t)D * (((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15)  // x (TMA windows)
+         + (size_t)cap * 8                          // composite keys
+         + (size_t)cap * 4                          // keys
+         + (((size_t)cap * 2 + 15) & ~(size_t)15);  // ord
+}
+
 template <typename T, int D, int KK, int INTEG, int BLOCK>
 static __global__ void __launch_bounds__(BLOCK) bucket_step_kernel(DevParams P, State<T, D> src,
-                                                            State<T, D> dst,
-                                                            const uint32_t* __restrict__ S) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+                                                                   State<T, D> dst,
+                                                                   const uint32_t* __restrict__ S) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw);
   uint32_t* off = cnt + 256;
   uint32_t* wsum = off + 256;  // 64
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + 2304);
   const uint32_t b = blockIdx.x;
   const uint32_t s0 = S[b], n = S[b + 1] - s0;
   if (n == 0) return;
+  for (uint32_t i = threadIdx.x; i < 256; i += BLOCK) cnt[i] = 0;
   const uint32_t cap = P.cap;
   if (n <= cap) {
-    T* xbase = reinterpret_cast<T*>(wsum + 64);
-    uint32_t* key_l = reinterpret_cast<uint32_t*>(xbase + (size_t)D * cap);
-    uint32_t* id_l = key_l + cap;
-    uint16_t* ord = reinterpret_cast<uint16_t*>(id_l + cap);
-    uint16_t* lst = ord + cap;
-    bucket_body<T, D, KK, INTEG, BLOCK>(P, src, dst, s0, n, key_l, id_l, xbase, ord, lst, cap, cnt,
-                                        off, wsum);
+    // TMA windows: 16-B aligned superset of [s0, s0+n) of every SoA array
+    constexpr uint32_t AX = 16 / sizeof(T);
+    const uint32_t lo_i = s0 & ~3u, oi = s0 - lo_i;
+    const uint32_t lo_x = s0 & ~(AX - 1), ox = s0 - lo_x;
+    const uint32_t bytes_i = ((oi + n + 3) & ~3u) * 4;
+    const uint32_t bytes_x = ((ox + n + AX - 1) & ~(AX - 1)) * (uint32_t)sizeof(T);
+    unsigned char* p = smem_raw + 2320;
+    uint32_t* id_raw = reinterpret_cast<uint32_t*>(p);
+    p += (size_t)(cap + 8) * 4;
+    T* xr[3];
+    const size_t xstride = ((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15;
+#pragma unroll
+    for (int c = 0; c < D; ++c) { xr[c] = reinterpret_cast<T*>(p); p += xstride; }
+    unsigned long long* ks = reinterpret_cast<unsigned long long*>(p);
+    p += (size_t)cap * 8;
+    uint32_t* key_l = reinterpret_cast<uint32_t*>(p);
+    p += (size_t)cap * 4;
+    uint16_t* ord = reinterpret_cast<uint16_t*>(p);
+    if (threadIdx.x == 0) {
+      mbar_init(bar, 1);
+      mbar_expect_tx(bar, bytes_i + D * bytes_x);
+      bulk_g2s(id_raw, src.id + lo_i, bytes_i, bar);
+#pragma unroll
+      for (int c = 0; c < D; ++c) bulk_g2s(xr[c], src.x[c] + lo_x, bytes_x, bar);
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+    T* xs[3];
+#pragma unroll
+    for (int c = 0; c < D; ++c) xs[c] = xr[c] + ox;
+    bucket_compute<T, D, KK, INTEG, BLOCK>(P, dst, s0, n, id_raw + oi, xs, key_l, ks, ord, cnt,
+                                           off, wsum);
   } else {
     // oversized bucket (never expected at the automatic capacity, forced in
     // tests): same algorithm on one of NBIG global-memory scratch slots,
@@ -517,15 +540,22 @@ static __global__ void __launch_bounds__(BLOCK) bucket_step_kernel(DevParams P, 
       if (threadIdx.x == 0) atomicExch(P.capacity_err, 1u);
       return;
     }
-    const size_t per = (size_t)BIG_CAP * (12 + D * sizeof(T)) + 64;
-    unsigned char* base = P.big_scratch + slot * per;
-    T* xbase = reinterpret_cast<T*>(base);
-    uint32_t* key_l = reinterpret_cast<uint32_t*>(xbase + (size_t)D * BIG_CAP);
-    uint32_t* id_l = key_l + BIG_CAP;
-    uint16_t* ord = reinterpret_cast<uint16_t*>(id_l + BIG_CAP);
-    uint16_t* lst = ord + BIG_CAP;
-    bucket_body<T, D, KK, INTEG, BLOCK>(P, src, dst, s0, n, key_l, id_l, xbase, ord, lst, BIG_CAP,
-                                        cnt, off, wsum);
+    unsigned char* base = P.big_scratch + slot * big_slot_bytes(D * sizeof(T));
+    unsigned long long* ks = reinterpret_cast<unsigned long long*>(base);
+    T* xr = reinterpret_cast<T*>(ks + BIG_CAP + 1);
+    uint32_t* id_l = reinterpret_cast<uint32_t*>(xr + (size_t)D * BIG_CAP);
+    uint32_t* key_l = id_l + BIG_CAP;
+    uint16_t* ord = reinterpret_cast<uint16_t*>(key_l + BIG_CAP);
+    T* xs[3];
+#pragma unroll
+    for (int c = 0; c < D; ++c) xs[c] = xr + (size_t)c * BIG_CAP;
+    for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
+      id_l[e] = src.id[s0 + e];
+#pragma unroll
+      for (int c = 0; c < D; ++c) xs[c][e] = src.x[c][s0 + e];
+    }
+    __syncthreads();
+    bucket_compute<T, D, KK, INTEG, BLOCK>(P, dst, s0, n, id_l, xs, key_l, ks, ord, cnt, off, wsum);
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
@@ -543,10 +573,10 @@ static __global__ void __launch_bounds__(256) straddle_kernel(DevParams P, State
   const int lane = threadIdx.x & 31;
   const uint32_t bnd = warp + 1;  // boundaries 1 .. nbuckets-1
   if (bnd >= P.nbuckets) return;
-  const uint64_t Pb = S[bnd];
+  const uint32_t Pb = S[bnd];
   if (Pb == 0 || Pb >= P.n) return;
-  uint64_t b0, b1;
-  batch_range(Pb, P.n, P.p, b0, b1);
+  uint32_t b0, b1;
+  batch_range(Pb, P, b0, b1);
   if (b0 == Pb) return;             // boundary at a batch start: no straddle
   if (S[bnd - 1] > b0) return;      // an earlier boundary inside the batch owns it
   const uint32_t m = (uint32_t)*P.step;
@@ -556,7 +586,7 @@ static __global__ void __launch_bounds__(256) straddle_kernel(DevParams P, State
   uint32_t idv[3];
   int cntm = 0;
   for (uint32_t q = lane; q < sz; q += 32, ++cntm) {
-    const uint64_t g = b0 + q;
+    const uint32_t g = b0 + q;
     const uint32_t id = dst.id[g];
     T xi[D], z[D], xn[D];
 #pragma unroll
@@ -566,14 +596,14 @@ static __global__ void __launch_bounds__(256) straddle_kernel(DevParams P, State
       T f[D];
 #pragma unroll
       for (int c = 0; c < D; ++c) f[c] = T(0);
-      for (uint64_t h = b0; h < b1; ++h) {
+      for (uint32_t h = b0; h < b1; ++h) {
         if (h == g) continue;
         T xj[D];
 #pragma unroll
         for (int c = 0; c < D; ++c) xj[c] = dst.x[c][h];
         add_interaction<T, D, KK>(xi, xj, f, P);
       }
-      const T inv = T(1) / T(sz - 1);
+      const T inv = batch_inv<T>(P, sz);
 #pragma unroll
       for (int c = 0; c < D; ++c) f[c] *= inv;
       em_update<T, D>(xi, f, z, xn, P, true);
