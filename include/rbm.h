@@ -172,11 +172,10 @@ uint32_t rbm_launches_per_step(const rbm_ctx* ctx);
  * scatter passes, per-bucket capacity).  Any out pointer may be NULL. */
 rbm_status rbm_layout(const rbm_ctx* ctx, uint32_t* prefix_bits, uint32_t* passes, uint32_t* bucket_cap);
 
-/* Test hook: write the current storage order (position -> id, N uint32
- * values) to `order_out` (device pointer, stream-ordered).  After an RBM-1
- * step m the state is stored in sorted order, so this is exactly the step-m
- * permutation pi_m (ids sorted by (key_m(id), id)); batch b = positions
- * [b p, (b+1) p) with the remainder rule.  Does not change X or m. */
+/* Test hook (RBM-1): the NEXT rbm_step() also writes its permutation pi_m
+ * (sorted position -> id: ids ordered by (key_m(id), id); batch b = positions
+ * [b p, (b+1) p) with the remainder rule) to `order_out`, N uint32 values,
+ * device pointer, stream-ordered.  rbm_run() ignores and clears it. */
 rbm_status rbm_debug_permutation(rbm_ctx* ctx, uint32_t* order_out);
 
 /* Test hook (RBM_SCHEME_RBMR only): the slot draws j_s of the next step,

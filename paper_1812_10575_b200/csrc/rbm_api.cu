@@ -70,6 +70,10 @@ rbm_status init_impl(rbm_ctx* c, const rbm_config* cfg, void* wsp, size_t ws_byt
   P.rem = (uint32_t)(cfg->n % cfg->p);
   P.seed_lo = (uint32_t)cfg->seed;
   P.seed_hi = (uint32_t)(cfg->seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    P.rk[2 * r] = P.seed_lo + (uint32_t)r * 0x9E3779B9u;
+    P.rk[2 * r + 1] = P.seed_hi + (uint32_t)r * 0xBB67AE85u;
+  }
   P.rep_hi = cfg->replica << 8;
   P.potential = cfg->potential;
   P.constraint = cfg->constraint;
@@ -87,7 +91,11 @@ rbm_status init_impl(rbm_ctx* c, const rbm_config* cfg, void* wsp, size_t ws_byt
   P.step = c->step_dev;
   P.nonfinite = c->nonfinite;
   P.capacity_err = c->capacity_err;
-  P.big_claim = c->zero_block + 1024;
+  P.big_claim = c->big_claim;
+  P.SB = c->L.SB; P.idbits = c->L.idbits; P.lowbits = c->L.lowbits;
+  P.dbg_order = nullptr;
+  P.group = 0;
+  if (cfg->p <= 32) { P.group = 1; while (P.group < cfg->p) P.group <<= 1; }
   P.big_scratch = c->big_scratch;
   rbm_status s = c->eng->setup(*c);
   if (s) return s;
@@ -99,7 +107,8 @@ rbm_status init_impl(rbm_ctx* c, const rbm_config* cfg, void* wsp, size_t ws_byt
   CU(cudaMemcpyAsync(c->nonfinite, &clean, 8, cudaMemcpyHostToDevice, st));
   CU(cudaMemsetAsync(c->capacity_err, 0, 4, st));
   const uint32_t s0[2] = {0u, (uint32_t)cfg->n};
-  if (c->L.B == 0) CU(cudaMemcpyAsync(c->S, s0, 8, cudaMemcpyHostToDevice, st));
+  if (c->L.B == 0) CU(cudaMemcpyAsync(c->S[0], s0, 8, cudaMemcpyHostToDevice, st));
+  CU(cudaMemsetAsync(c->big_claim, 0, NBIG * 4, st));
   if (cfg->init != RBM_INIT_USER) c->eng->init_state(*c, st);
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(st));  // the host-side sources above live on this stack frame
@@ -156,6 +165,7 @@ rbm_status rbm_set_state(rbm_ctx* c, const void* x, uint32_t where) {
 rbm_status rbm_step(rbm_ctx* c) {
   if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
   rbm_status s = enqueue_steps(c, c->stream, 1);
+  c->P.dbg_order = nullptr;
   if (s) return s;
   ++c->step;
   return RBM_OK;
@@ -165,16 +175,24 @@ rbm_status rbm_run(rbm_ctx* c, uint64_t nsteps) {
   if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
   if (c->step + nsteps >= (1ull << 32)) return fail(c, RBM_ERR_INVALID_ARG, "step index would exceed 2^32");
   // steps per graph: even when a step flips the ping-pong buffers
-  const bool flips = (c->cfg.scheme == RBM_SCHEME_RBM1) && (c->L.B == 0 || c->L.b2 != 0);
-  const uint32_t per = flips ? 8 : 8;
+  c->P.dbg_order = nullptr;  // the permutation hook applies to rbm_step only
+  const uint32_t per = 8;  // even: every layout returns to the same (cur, parity)
   c->graph_steps = per;
   uint64_t done = 0;
+  if (c->cfg.scheme == RBM_SCHEME_RBM1 && c->L.B > 0 && !c->partitioned && nsteps > 0) {
+    rbm_status s0 = enqueue_steps(c, c->stream, 1);  // prologue step outside the graph
+    if (s0) return s0;
+    ++c->step;
+    --nsteps;
+  }
   if (nsteps >= per && !c->timing) {
-    const int slot = c->cur;
+    const int slot = (c->cur << 1) | (int)(c->step & 1);
     if (!c->graph[slot]) {
       const int cur0 = c->cur;
       CU(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
-      for (uint32_t i = 0; i < per; ++i) c->eng->step(*c, c->cap_stream);
+      const uint64_t step0 = c->step;
+      for (uint32_t i = 0; i < per; ++i) { c->eng->step(*c, c->cap_stream); ++c->step; }
+      c->step = step0;
       cudaGraph_t g = nullptr;
       CU(cudaStreamEndCapture(c->cap_stream, &g));
       CU(cudaGraphInstantiate(&c->graph[slot], g, 0));
@@ -185,9 +203,12 @@ rbm_status rbm_run(rbm_ctx* c, uint64_t nsteps) {
     for (uint64_t r = 0; r < reps; ++r) CU(cudaGraphLaunch(c->graph[slot], c->stream));
     done = reps * per;
   }
-  rbm_status s = enqueue_steps(c, c->stream, nsteps - done);
-  if (s) return s;
-  c->step += nsteps;
+  c->step += done;
+  for (uint64_t i = done; i < nsteps; ++i) {
+    rbm_status s = enqueue_steps(c, c->stream, 1);
+    if (s) return s;
+    ++c->step;
+  }
   return RBM_OK;
 }
 
@@ -275,8 +296,8 @@ rbm_status rbm_layout(const rbm_ctx* c, uint32_t* prefix_bits, uint32_t* passes,
 rbm_status rbm_debug_permutation(rbm_ctx* c, uint32_t* order_out) {
   if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
   if (!order_out) return fail(c, RBM_ERR_INVALID_ARG, "order_out is NULL");
-  copy_ids_kernel<<<grid_for(c->cfg.n, 256), 256, 0, c->stream>>>(c->cfg.n, c->idbuf[c->cur], order_out);
-  CU(cudaGetLastError());
+  if (c->cfg.scheme != RBM_SCHEME_RBM1) return fail(c, RBM_ERR_STATE, "not an RBM-1 context");
+  c->P.dbg_order = order_out;  // consumed by the next rbm_step
   return RBM_OK;
 }
 
@@ -300,7 +321,7 @@ const char* rbm_last_error(const rbm_ctx* c) { return c ? c->err.c_str() : g_err
 
 rbm_status rbm_destroy(rbm_ctx* c) {
   if (!c) return RBM_OK;
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < 4; ++i)
     if (c->graph[i]) cudaGraphExecDestroy(c->graph[i]);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);

@@ -42,6 +42,7 @@ struct DevParams {
   uint32_t nfull;      // floor(N/p)
   uint32_t rem;        // N mod p (remainder rule, D:7)
   uint32_t seed_lo, seed_hi;
+  uint32_t rk[20];     // Philox round keys (k0, k1) of rounds 0..9 (Weyl schedule)
   uint32_t rep_hi;     // replica << 8, OR-ed into counter word 3
   uint32_t potential;  // 0 none, 1 harmonic
   uint32_t constraint; // 0 none, 1 unit sphere
@@ -56,6 +57,11 @@ struct DevParams {
   uint32_t b1, b2;     // digit bits of scatter passes 1 and 2 (b2 = 0: one pass)
   uint32_t nbuckets;   // 2^B
   uint32_t cap;        // per-bucket shared-memory capacity (elements)
+  uint32_t SB;         // sub-digit bits of the in-bucket counting sort
+  uint32_t idbits;     // bits of an id (ceil log2 N)
+  uint32_t lowbits;    // key bits below prefix+sub-digit: 32 - B - SB (lowbits+idbits <= 32)
+  uint32_t* dbg_order; // if set: sorted position -> id of this step (test hook)
+  uint32_t group;      // lanes per batch in the fused step: pow2 >= p (<= 32), 0 = one thread per batch
   const uint64_t* step;     // device step counter m
   unsigned long long* nonfinite;  // atomicMin of (m<<32 | id); ~0 if clean
   uint32_t* capacity_err;         // set to 1 if a bucket overflowed every fallback
@@ -114,9 +120,22 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
   return c;
 }
 
+// same function with the 20 round keys precomputed on the host (read from the
+// constant bank by LOP3, no per-round key additions)
+__device__ __forceinline__ uint4 philox4x32_10_rk(uint4 c, const uint32_t* rk) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c.x;
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c.z;
+    c = make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ rk[2 * r], (uint32_t)p1,
+                   (uint32_t)(p0 >> 32) ^ c.w ^ rk[2 * r + 1], (uint32_t)p0);
+  }
+  return c;
+}
+
 __device__ __forceinline__ uint4 block_at(const DevParams& P, uint32_t c0, uint32_t c1,
                                           uint32_t m, uint32_t tag) {
-  return philox4x32_10(make_uint4(c0, c1, m, tag | P.rep_hi), P.seed_lo, P.seed_hi);
+  return philox4x32_10_rk(make_uint4(c0, c1, m, tag | P.rep_hi), P.rk);
 }
 
 // shuffle key of particle `id` at step m: word 0 of the TAG_KEY block
@@ -139,8 +158,13 @@ __device__ __forceinline__ double u01d(uint32_t a, uint32_t b) {
 // fp32: MUFU-based (lg2.approx, sin/cos.approx on [0, 2pi)); the radius is
 // clamped at 0 so u1 -> 1 can never produce a NaN.  Absolute error of z is
 // ~1e-6, far inside the fp32 parity bar.
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 __device__ __forceinline__ void bm_pair(float u1, float u2, float& z0, float& z1) {
-  const float r = sqrtf(fmaxf(-1.3862943611198906f * __log2f(u1), 0.0f));  // -2 ln u1
+  const float r = sqrt_approx(fmaxf(-1.3862943611198906f * __log2f(u1), 0.0f));  // -2 ln u1
   float s, c;
   __sincosf(6.2831853071795865f * u2, &s, &c);
   z0 = r * c;

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -37,7 +38,11 @@ struct Workspace {
 
 struct Layout {
   uint32_t B = 0, b1 = 0, b2 = 0, nbuckets = 1, cap = 0;
+  uint32_t SB = 8, idbits = 1, lowbits = 0;
 };
+constexpr int FUSED_BLOCK = 256;
+constexpr int PAIR_BLOCK = 512, PAIR_ITEMS = 5;  // p = 2 lean kernel: capacity <= 2560
+constexpr uint32_t FUSED_CAP_MAX = 4096;  // fast-path bucket capacity (u16 indices, smem)
 
 struct EngineBase;
 
@@ -56,10 +61,13 @@ struct rbm_ctx {
   void* xbuf[2] = {nullptr, nullptr};
   uint64_t xstride = 0;  // elements between coordinate arrays of one state buffer
   uint32_t* idbuf[2] = {nullptr, nullptr};
-  uint32_t* zero_block = nullptr;  // hist1[1024] + big_claim
-  size_t zero_bytes = 0;
-  uint32_t *hist1 = nullptr, *off1 = nullptr, *cur1 = nullptr, *tile_off = nullptr;
-  uint32_t *hist2 = nullptr, *cur2 = nullptr, *S = nullptr;
+  uint32_t* keybuf[2] = {nullptr, nullptr};  // carried shuffle keys (fused pipeline)
+  // per step-parity q = m & 1: histogram/offsets/cursors of pass 1 and the
+  // final-bucket starts of step m (the fused bucket step fills step m+1's)
+  uint32_t *hist1[2] = {nullptr, nullptr}, *off1[2] = {nullptr, nullptr},
+           *cur1[2] = {nullptr, nullptr}, *tile_off[2] = {nullptr, nullptr}, *S[2] = {nullptr, nullptr};
+  uint32_t *hist2 = nullptr, *cur2 = nullptr, *big_claim = nullptr;
+  bool partitioned = false;  // state stored in the pass-1 buckets of step `step`
   uint64_t* step_dev = nullptr;
   unsigned long long* nonfinite = nullptr;
   uint32_t* capacity_err = nullptr;
@@ -74,7 +82,7 @@ struct rbm_ctx {
   uint64_t step = 0;
   uint32_t launches = 0;
   int tile = 4096;
-  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  cudaGraphExec_t graph[4] = {nullptr, nullptr, nullptr, nullptr};  // by (cur, m & 1)
   uint32_t graph_steps = 1;
   // optional per-kernel CUDA-event timing (rbm_timing_begin/end)
   bool timing = false;
@@ -117,28 +125,44 @@ inline size_t elt_size(const rbm_config& c) { return c.dtype == RBM_F64 ? 8 : 4;
 inline Layout choose_layout(const rbm_config& c) {
   Layout L;
   const uint64_t n = c.n;
+  L.idbits = ceil_log2((double)n);
+  if (L.idbits < 1) L.idbits = 1;
   if (n <= 2048) {
-    L.B = 0;
+    L.B = 0;  // one bucket: sorted-output kernel
   } else {
-    L.B = ceil_log2((double)n / 2048.0);
-    if (L.B < 1) L.B = 1;
+    // target mean bucket size (tuning knob RBM_BUCKET_TARGET, default 1024)
+    double target = 1024.0;
+    if (const char* e = std::getenv("RBM_BUCKET_TARGET")) target = std::atof(e);
+    if (!(target >= 64.0 && target <= 2048.0)) target = 1024.0;
+    L.B = ceil_log2((double)n / target);
+    if (L.B < 2) L.B = 2;
     if (L.B > 18) L.B = 18;
   }
   if (L.B <= 10) { L.b1 = L.B; L.b2 = 0; }
-  else { L.b1 = (L.B + 1) / 2; L.b2 = L.B - L.b1; }
+  else {
+    L.b1 = (L.B + 1) / 2;
+    if (const char* e = std::getenv("RBM_B1")) {  // tuning knob: pass-1 / fused-output digit bits
+      const int v = std::atoi(e);
+      if (v >= 6 && v <= 10 && L.B - v >= 6 && L.B - v <= 10) L.b1 = (uint32_t)v;
+    }
+    L.b2 = L.B - L.b1;
+  }
   L.nbuckets = 1u << L.B;
+  L.SB = L.idbits > L.B + 8 ? L.idbits - L.B : 8;  // 32-bit composites: lowbits + idbits <= 32
+  L.lowbits = 32 - L.B - L.SB;
   if (L.B == 0) {
     L.cap = (uint32_t)((n + 31) & ~31ull);
   } else {
     const double mu = (double)n / L.nbuckets;
     L.cap = (uint32_t)(mu + 6.0 * std::sqrt(mu) + 32.0);
     L.cap = (L.cap + 31) & ~31u;
+    if (L.cap > FUSED_CAP_MAX) L.cap = FUSED_CAP_MAX;
   }
   if (c.debug_bucket_cap) L.cap = c.debug_bucket_cap;
   return L;
 }
 
-inline size_t bucket_smem(const rbm_config& c, uint32_t cap) {
+inline size_t bucket_smem(const rbm_config& c, uint32_t cap) {  // sorted-output kernel (B = 0)
   const size_t es = elt_size(c);
   return 2320 + (size_t)(cap + 8) * 4 + c.d * ((((size_t)(cap + 8) * es) + 15) & ~(size_t)15) +
          (size_t)cap * 12 + (((size_t)cap * 2 + 15) & ~(size_t)15);
@@ -184,6 +208,10 @@ inline rbm_status validate(const rbm_config* cfg) {
   if (k.world_size != 1 || k.rank != 0)
     return fail(c, RBM_ERR_UNSUPPORTED, "world_size=%d: multi-process partition mode is not in this build", k.world_size);
   const Layout L = choose_layout(k);
+  if (k.scheme == RBM_SCHEME_RBM1 && L.B > 0 && L.SB > 12)
+    return fail(c, RBM_ERR_UNSUPPORTED, "n=%llu needs %u sub-digit bits (> 12): n <= 2^30 per GPU", (unsigned long long)k.n, L.SB);
+  if (k.scheme == RBM_SCHEME_RBM1 && L.B > 0 && L.cap > FUSED_CAP_MAX)
+    return fail(c, RBM_ERR_INVALID_ARG, "debug_bucket_cap %u > %u", L.cap, FUSED_CAP_MAX);
   if (k.scheme == RBM_SCHEME_RBM1 && bucket_smem(k, L.cap) > 227 * 1024)
     return fail(c, RBM_ERR_INVALID_ARG, "bucket capacity %u needs %zu B of shared memory", L.cap, bucket_smem(k, L.cap));
   return RBM_OK;
@@ -197,18 +225,20 @@ inline void carve(rbm_ctx& c, Workspace& ws) {
   c.xstride = (n + 63) & ~63ull;  // per-coordinate stride: 256-B aligned SoA arrays (TMA)
   for (int b = 0; b < 2; ++b) {
     c.idbuf[b] = ws.take<uint32_t>(n);
+    c.keybuf[b] = ws.take<uint32_t>(n);
     c.xbuf[b] = ws.take<unsigned char>(c.xstride * k.d * es);
   }
-  c.zero_block = ws.take<uint32_t>(1024 + 4);
-  c.zero_bytes = (1024 + 4) * 4;
-  c.hist1 = c.zero_block;
-  c.off1 = ws.take<uint32_t>(1025);
-  c.cur1 = ws.take<uint32_t>(1024);
-  c.tile_off = ws.take<uint32_t>(1025);
-  c.S = ws.take<uint32_t>((size_t)c.L.nbuckets + 1);
+  for (int q = 0; q < 2; ++q) {
+    c.hist1[q] = ws.take<uint32_t>(1024);
+    c.off1[q] = ws.take<uint32_t>(1025);
+    c.cur1[q] = ws.take<uint32_t>(1024 * CUR1_STRIDE);
+    c.tile_off[q] = ws.take<uint32_t>(1025);
+    c.S[q] = ws.take<uint32_t>((size_t)c.L.nbuckets + 1);
+  }
+  c.big_claim = ws.take<uint32_t>(NBIG);
   if (c.L.b2) {
     c.hist2 = ws.take<uint32_t>(c.L.nbuckets);
-    c.cur2 = ws.take<uint32_t>(c.L.nbuckets);
+    c.cur2 = ws.take<uint32_t>((size_t)c.L.nbuckets * CUR2_STRIDE);
   }
   c.step_dev = ws.take<uint64_t>(1);
   c.nonfinite = ws.take<unsigned long long>(1);
@@ -255,15 +285,23 @@ struct Engine final : EngineBase {
   State<T, D> st(rbm_ctx& c, int b) {
     State<T, D> s;
     s.id = c.idbuf[b];
+    s.key = c.keybuf[b];
     T* x = reinterpret_cast<T*>(c.xbuf[b]);
     for (int k = 0; k < 3; ++k) s.x[k] = x + (size_t)(k < D ? k : 0) * c.xstride;
     return s;
   }
 
+  size_t fu_smem = 0, pr_smem = 0;
+  bool use_pair = false;
+
   rbm_status setup(rbm_ctx& c) override {
     c.tile = SC_TILE;
-    sc_smem = (1024 + 1024 + 64) * 4 + (size_t)SC_TILE * (4 + 2 + D * sizeof(T));
+    sc_smem = (1024 + 1024 + 64) * 4 + (size_t)SC_TILE * (8 + 2 + D * sizeof(T));
     bk_smem = bucket_smem(c.cfg, c.L.cap);
+    fu_smem = fused_smem_bytes<T, D>(c.L.cap, c.L.SB);
+    pr_smem = pair_smem_bytes<T, D>(c.L.cap, c.L.SB);
+    use_pair = c.cfg.p == 2 && c.L.B > 0 && c.L.cap <= (uint32_t)(PAIR_BLOCK * PAIR_ITEMS) &&
+               pr_smem <= 227 * 1024;
     if (bk_smem != bucket_smem_bytes<T, D>(c.L.cap))
       return fail(&c, RBM_ERR_STATE, "bucket smem size mismatch %zu vs %zu", bk_smem, bucket_smem_bytes<T, D>(c.L.cap));
     auto chk = [&](cudaError_t e, const char* what) -> rbm_status {
@@ -280,6 +318,16 @@ struct Engine final : EngineBase {
     if ((s = chk(cudaFuncSetAttribute(bucket_step_kernel<T, D, KK, INTEG, BK_BLOCK>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bk_smem),
                  "smem attr bucket"))) return s;
+    if (use_pair) {
+      if ((s = chk(cudaFuncSetAttribute(bucket_pair_kernel<T, D, KK, INTEG, PAIR_BLOCK, PAIR_ITEMS>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pr_smem),
+                   "smem attr pair"))) return s;
+    }
+    if (fu_smem <= 227 * 1024) {
+      if ((s = chk(cudaFuncSetAttribute(bucket_fused_kernel<T, D, KK, INTEG, FUSED_BLOCK>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fu_smem),
+                   "smem attr fused"))) return s;
+    }
     return RBM_OK;
   }
 
@@ -287,11 +335,13 @@ struct Engine final : EngineBase {
     const rbm_config& k = c.cfg;
     init_kernel<T, D><<<grid_for(k.n, 256), 256, 0, s>>>(c.P, st(c, c.cur), k.init, k.iparam[0],
                                                          k.iparam[1], k.iparam[2], k.iparam[3]);
+    c.partitioned = false;
   }
 
   void set_state(rbm_ctx& c, const void* x, cudaStream_t s) override {
     set_state_kernel<T, D><<<grid_for(c.cfg.n, 256), 256, 0, s>>>(c.cfg.n, st(c, c.cur),
                                                                   reinterpret_cast<const T*>(x));
+    c.partitioned = false;
   }
 
   void gather(rbm_ctx& c, uint64_t i0, uint64_t i1, void* out, cudaStream_t s) override {
@@ -299,48 +349,79 @@ struct Engine final : EngineBase {
                                                                 reinterpret_cast<T*>(out));
   }
 
+  // histogram + offsets of the pass-1 digit of step m + mofs into parity slot q
+  void top_hist(rbm_ctx& c, cudaStream_t s, uint32_t mofs, int q, bool mark) {
+    const uint64_t n = c.cfg.n;
+    cudaMemsetAsync(c.hist1[q], 0, 1024 * 4, s);
+    if (mark) c.mark(s);
+    hist_top_kernel<<<grid_for(n, 512, 148 * 4), 512, 0, s>>>(c.P, c.hist1[q], mofs);
+    if (mark) c.mark(s);
+    scan_top_kernel<<<1, 1024, 0, s>>>(c.P, c.hist1[q], c.off1[q], c.cur1[q], c.tile_off[q],
+                                       c.S[q], SC_TILE);
+  }
+
+  void fused(rbm_ctx& c, cudaStream_t s, State<T, D> in, State<T, D> out, const uint32_t* S,
+             uint32_t* cur_next) {
+    if (use_pair)
+      bucket_pair_kernel<T, D, KK, INTEG, PAIR_BLOCK, PAIR_ITEMS>
+          <<<c.L.nbuckets, PAIR_BLOCK, pr_smem, s>>>(c.P, in, out, S, cur_next);
+    else
+      bucket_fused_kernel<T, D, KK, INTEG, FUSED_BLOCK>
+          <<<c.L.nbuckets, FUSED_BLOCK, fu_smem, s>>>(c.P, in, out, S, cur_next);
+  }
+
   void step(rbm_ctx& c, cudaStream_t s) override {
     if (c.cfg.scheme == RBM_SCHEME_RBMR) { step_rbmr(c, s); return; }
     const DevParams& P = c.P;
     const Layout& L = c.L;
-    State<T, D> src = st(c, c.cur), tmp = st(c, c.cur ^ 1);
     const uint64_t n = c.cfg.n;
-    cudaMemsetAsync(c.zero_block, 0, c.zero_bytes, s);
-    if (L.B == 0) {
+    const int q = (int)(c.step & 1);
+    if (L.B == 0) {  // single bucket: sort + step, sorted output
       c.mark(s);
-      bucket_step_kernel<T, D, KK, INTEG, BK_BLOCK><<<1, BK_BLOCK, bk_smem, s>>>(P, src, tmp, c.S);
+      bucket_step_kernel<T, D, KK, INTEG, BK_BLOCK><<<1, BK_BLOCK, bk_smem, s>>>(
+          P, st(c, c.cur), st(c, c.cur ^ 1), c.S[0]);
+      c.cur ^= 1;
+      c.mark(s);
+      advance_kernel<<<1, 1, 0, s>>>(c.step_dev);
+      c.mark(s);
+      return;
+    }
+    if (!c.partitioned) {  // prologue: pass-1 partition of step m from any storage order
+      top_hist(c, s, 0, q, false);
+      scatter_kernel<T, D, 1, SC_BLOCK, SC_ITEMS>
+          <<<(unsigned)((n + SC_TILE - 1) / SC_TILE), SC_BLOCK, sc_smem, s>>>(
+              P, st(c, c.cur), st(c, c.cur ^ 1), c.cur1[q], nullptr, nullptr);
+      c.cur ^= 1;
+      c.partitioned = true;
+    }
+    // pass-1 histogram/offsets of step m+1 (compute-only), consumed by the fused step
+    top_hist(c, s, 1, q ^ 1, true);
+    const unsigned straddle_grid = (unsigned)(((uint64_t)L.nbuckets * 32 + 255) / 256);
+    State<T, D> A = st(c, c.cur), Bf = st(c, c.cur ^ 1);
+    if (L.b2 == 0) {
+      // A holds the final buckets of step m; the fused step writes m+1's into B
+      c.mark(s);
+      fused(c, s, A, Bf, c.S[q], c.cur1[q ^ 1]);
+      c.mark(s);
+      straddle_kernel<T, D, KK, INTEG, true><<<straddle_grid, 256, 0, s>>>(P, A, c.S[q], Bf,
+                                                                           c.cur1[q ^ 1]);
       c.cur ^= 1;
     } else {
+      // A holds the pass-1 buckets of step m: split them by the next b2 bits into B
+      const unsigned tiles2 = (unsigned)((n + SC_TILE - 1) / SC_TILE + (1u << L.b1));
+      cudaMemsetAsync(c.hist2, 0, (size_t)L.nbuckets * 4, s);
       c.mark(s);
-      hist_top_kernel<<<grid_for(n, 512, 148 * 4), 512, 0, s>>>(P, c.hist1);
+      hist_sub_kernel<<<tiles2, 256, 0, s>>>(P, A.key, c.off1[q], c.tile_off[q], c.hist2, SC_TILE);
       c.mark(s);
-      scan_top_kernel<<<1, 1024, 0, s>>>(P, c.hist1, c.off1, c.cur1, c.tile_off, c.S, SC_TILE);
+      scan_sub_kernel<<<1u << L.b1, 512, 0, s>>>(P, c.hist2, c.off1[q], c.S[q], c.cur2);
       c.mark(s);
-      scatter_kernel<T, D, 1, SC_BLOCK, SC_ITEMS>
-          <<<(unsigned)((n + SC_TILE - 1) / SC_TILE), SC_BLOCK, sc_smem, s>>>(P, src, tmp, c.cur1,
-                                                                               nullptr, nullptr);
-      const unsigned straddle_grid = (unsigned)(((uint64_t)L.nbuckets * 32 + 255) / 256);
-      if (L.b2 == 0) {
-        c.mark(s);
-        bucket_step_kernel<T, D, KK, INTEG, BK_BLOCK><<<L.nbuckets, BK_BLOCK, bk_smem, s>>>(P, tmp, src, c.S);
-        c.mark(s);
-        straddle_kernel<T, D, KK, INTEG><<<straddle_grid, 256, 0, s>>>(P, src, c.S);
-      } else {
-        const unsigned tiles2 = (unsigned)((n + SC_TILE - 1) / SC_TILE + (1u << L.b1));
-        cudaMemsetAsync(c.hist2, 0, (size_t)L.nbuckets * 4, s);
-        c.mark(s);
-        hist_sub_kernel<<<tiles2, 256, 0, s>>>(P, tmp.id, c.off1, c.tile_off, c.hist2, SC_TILE);
-        c.mark(s);
-        scan_sub_kernel<<<1u << L.b1, 512, 0, s>>>(P, c.hist2, c.off1, c.S, c.cur2);
-        c.mark(s);
-        scatter_kernel<T, D, 2, SC_BLOCK, SC_ITEMS>
-            <<<tiles2, SC_BLOCK, sc_smem, s>>>(P, tmp, src, c.cur2, c.off1, c.tile_off);
-        c.mark(s);
-        bucket_step_kernel<T, D, KK, INTEG, BK_BLOCK><<<L.nbuckets, BK_BLOCK, bk_smem, s>>>(P, src, tmp, c.S);
-        c.mark(s);
-        straddle_kernel<T, D, KK, INTEG><<<straddle_grid, 256, 0, s>>>(P, tmp, c.S);
-        c.cur ^= 1;
-      }
+      scatter_kernel<T, D, 2, SC_BLOCK, SC_ITEMS>
+          <<<tiles2, SC_BLOCK, sc_smem, s>>>(P, A, Bf, c.cur2, c.off1[q], c.tile_off[q]);
+      c.mark(s);
+      fused(c, s, Bf, A, c.S[q], c.cur1[q ^ 1]);
+      c.mark(s);
+      straddle_kernel<T, D, KK, INTEG, true><<<straddle_grid, 256, 0, s>>>(P, Bf, c.S[q], A,
+                                                                           c.cur1[q ^ 1]);
     }
     c.mark(s);
     advance_kernel<<<1, 1, 0, s>>>(c.step_dev);
@@ -398,14 +479,13 @@ inline const char* const* kernel_names(const rbm_ctx& c, uint32_t* count) {
   static const char* const r[] = {"rbmr_draw", "scan_reduce", "scan_parts", "scan_down",
                                   "rbmr_fill", "rbmr_delta", "rbmr_apply", "advance"};
   static const char* const b0[] = {"bucket_step", "advance"};
-  static const char* const p1[] = {"hist_top", "scan_top", "scatter_top", "bucket_step",
-                                   "straddle", "advance"};
-  static const char* const p2[] = {"hist_top", "scan_top", "scatter_top", "hist_sub", "scan_sub",
-                                   "scatter_sub", "bucket_step", "straddle", "advance"};
+  static const char* const p1[] = {"hist_next", "scan_next", "bucket_step", "straddle", "advance"};
+  static const char* const p2[] = {"hist_next", "scan_next", "hist_sub", "scan_sub", "scatter_sub",
+                                   "bucket_step", "straddle", "advance"};
   if (c.cfg.scheme == RBM_SCHEME_RBMR) { *count = 8; return r; }
   if (c.L.B == 0) { *count = 2; return b0; }
-  if (c.L.b2 == 0) { *count = 6; return p1; }
-  *count = 9;
+  if (c.L.b2 == 0) { *count = 5; return p1; }
+  *count = 8;
   return p2;
 }
 

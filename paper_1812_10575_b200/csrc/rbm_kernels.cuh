@@ -18,9 +18,24 @@
 
 namespace rbm {
 
+// Cursor padding: concurrent CTAs reserve output runs with atomicAdd on the
+// cursors; one cursor per 128-B line (pass 1) / 32-B sector (pass 2) spreads
+// those atomics over the L2 slices instead of serialising them on a few lines.
+constexpr uint32_t CUR1_STRIDE = 32, CUR2_STRIDE = 8;
+
 template <typename T, int D> struct State {
   uint32_t* id;
+  uint32_t* key;  // shuffle key of the step the records are partitioned for (fused pipeline)
   T* x[3];
+};
+
+// D coordinate arrays of a bucket in (shared or scratch) memory: base + c*stride.
+// One base pointer (not an array of pointers) keeps the address space visible
+// to the compiler, so shared-memory accesses stay LDS/STS.
+template <typename T> struct SX {
+  T* base;
+  uint32_t stride;
+  __device__ __forceinline__ T& at(int c, uint32_t e) const { return base[(size_t)c * stride + e]; }
 };
 
 // ----------------------------------------------------------------- helpers
@@ -74,6 +89,21 @@ __device__ __forceinline__ void batch_range(uint32_t P, const DevParams& prm, ui
     b0 = k * p;
     b1 = min(b0 + p, n);
   }
+}
+
+// batch index of position P, and the [start, end) of batch k (reading D:7)
+__device__ __forceinline__ uint32_t batch_index(uint32_t P0, const DevParams& prm) {
+  uint32_t k = fdiv(P0, prm.pdiv);
+  if (prm.rem == 1 && k + 1 >= prm.nfull) k = prm.nfull - 1;
+  return k;
+}
+__device__ __forceinline__ uint32_t batch_end(uint32_t k, const DevParams& prm) {
+  const uint32_t n = (uint32_t)prm.n;
+  if (prm.rem == 1 && k + 1 == prm.nfull) return n;
+  return min(k * prm.p + prm.p, n);
+}
+__device__ __forceinline__ uint32_t num_batches(const DevParams& prm) {
+  return prm.nfull + (prm.rem >= 2 ? 1u : 0u);
 }
 
 // ------------------------------------------------------------------- init
@@ -171,12 +201,13 @@ static __global__ void advance_kernel(uint64_t* step) { *step += 1; }
 
 // ------------------------------------------------------- compute-only histogram
 // histogram of key_m(id) >> (32-b1) over ALL ids 0..N-1: reads no memory.
-static __global__ void __launch_bounds__(512) hist_top_kernel(DevParams P, uint32_t* __restrict__ hist) {
+static __global__ void __launch_bounds__(512) hist_top_kernel(DevParams P, uint32_t* __restrict__ hist,
+                                                              uint32_t mofs) {
   __shared__ uint32_t h[1024];
   const uint32_t nb = 1u << P.b1;
   for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) h[i] = 0;
   __syncthreads();
-  const uint32_t m = (uint32_t)*P.step;
+  const uint32_t m = (uint32_t)*P.step + mofs;
   const uint32_t sh = 32u - P.b1;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < P.n;
        i += (uint64_t)gridDim.x * blockDim.x)
@@ -205,7 +236,7 @@ static __global__ void __launch_bounds__(1024) scan_top_kernel(DevParams P, cons
   const uint32_t ntiles = block_excl_scan<1024>(t, nb, ws);
   for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) {
     off1[i] = a[i];
-    cur1[i] = a[i];
+    cur1[i * CUR1_STRIDE] = a[i];
     tile_off[i] = t[i];
     if (P.b2 == 0) S[i] = a[i];
   }
@@ -229,7 +260,7 @@ static __global__ void __launch_bounds__(512) scan_sub_kernel(DevParams P, const
   const uint32_t o = off1[u];
   for (uint32_t i = threadIdx.x; i < nb2; i += blockDim.x) {
     S[base + i] = o + a[i];
-    cur2[base + i] = o + a[i];
+    cur2[(base + i) * CUR2_STRIDE] = o + a[i];
   }
   if (u == 0 && threadIdx.x == 0) S[P.nbuckets] = (uint32_t)P.n;
 }
@@ -252,7 +283,7 @@ __device__ __forceinline__ bool aligned_tile(const uint32_t* __restrict__ tile_o
 }
 
 // per top-bucket histogram of the next b2 key bits (reads ids only)
-static __global__ void __launch_bounds__(256) hist_sub_kernel(DevParams P, const uint32_t* __restrict__ ids,
+static __global__ void __launch_bounds__(256) hist_sub_kernel(DevParams P, const uint32_t* __restrict__ keys,
                                                        const uint32_t* __restrict__ off1,
                                                        const uint32_t* __restrict__ tile_off,
                                                        uint32_t* hist2, uint32_t tile) {
@@ -262,10 +293,9 @@ static __global__ void __launch_bounds__(256) hist_sub_kernel(DevParams P, const
   const uint32_t nb2 = 1u << P.b2;
   for (uint32_t i = threadIdx.x; i < nb2; i += blockDim.x) h[i] = 0;
   __syncthreads();
-  const uint32_t m = (uint32_t)*P.step;
   const uint32_t sh = 32u - P.b1 - P.b2, mask = nb2 - 1;
   for (uint32_t e = lo + threadIdx.x; e < hi; e += blockDim.x)
-    atomicAdd(&h[(shuffle_key(P, ids[e], m) >> sh) & mask], 1u);
+    atomicAdd(&h[(keys[e] >> sh) & mask], 1u);
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < nb2; i += blockDim.x)
     if (h[i]) atomicAdd(&hist2[(u << P.b2) | i], h[i]);
@@ -287,7 +317,8 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(DevParams P, Stat
   uint32_t* gbase = hist + 1024;                           // 1024
   uint32_t* wsum = gbase + 1024;                           // 64
   uint32_t* st_id = wsum + 64;                             // TILE
-  T* st_x = reinterpret_cast<T*>(st_id + TILE);            // D*TILE
+  uint32_t* st_key = st_id + TILE;                         // TILE
+  T* st_x = reinterpret_cast<T*>(st_key + TILE);           // D*TILE
   uint16_t* st_dig = reinterpret_cast<uint16_t*>(st_x + D * TILE);  // TILE
 
   uint32_t lo, hi, u = 0, bits, sh;
@@ -303,19 +334,21 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(DevParams P, Stat
     sh = 32u - P.b1 - P.b2;
   }
   const uint32_t nbins = 1u << bits, mask = nbins - 1;
-  uint32_t* mycur = cur + (LEVEL == 1 ? 0u : (u << P.b2));
+  constexpr uint32_t CS = (LEVEL == 1) ? CUR1_STRIDE : CUR2_STRIDE;
+  uint32_t* mycur = cur + (LEVEL == 1 ? 0u : (u << P.b2)) * CS;
   for (uint32_t i = threadIdx.x; i < nbins; i += BLOCK) hist[i] = 0;
   __syncthreads();
 
   const uint32_t m = (uint32_t)*P.step;
   const uint32_t cnt = hi - lo;
-  uint32_t rid[ITEMS], rdig[ITEMS], rslot[ITEMS];
+  uint32_t rid[ITEMS], rkey[ITEMS], rds[ITEMS];
   T rx[ITEMS][D];
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t e = k * BLOCK + threadIdx.x;
     if (e < cnt) {
       rid[k] = src.id[lo + e];
+      if (LEVEL != 1) rkey[k] = src.key[lo + e];
 #pragma unroll
       for (int c = 0; c < D; ++c) rx[k][c] = src.x[c][lo + e];
     }
@@ -324,24 +357,27 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(DevParams P, Stat
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t e = k * BLOCK + threadIdx.x;
     if (e < cnt) {
-      rdig[k] = (shuffle_key(P, rid[k], m) >> sh) & mask;
-      rslot[k] = atomicAdd(&hist[rdig[k]], 1u);
+      if (LEVEL == 1) rkey[k] = shuffle_key(P, rid[k], m);  // prologue: keys from ids
+      const uint32_t dg = (rkey[k] >> sh) & mask;
+      rds[k] = (dg << 16) | atomicAdd(&hist[dg], 1u);
     }
   }
   __syncthreads();
   // reserve global space per bin, then local exclusive offsets
   for (uint32_t i = threadIdx.x; i < nbins; i += BLOCK) {
     const uint32_t h = hist[i];
-    gbase[i] = h ? atomicAdd(&mycur[i], h) : 0u;
+    gbase[i] = h ? atomicAdd(&mycur[i * CS], h) : 0u;
   }
   block_excl_scan<BLOCK>(hist, nbins, wsum);  // hist -> local offsets
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t e = k * BLOCK + threadIdx.x;
     if (e < cnt) {
-      const uint32_t s = hist[rdig[k]] + rslot[k];
+      const uint32_t dg = rds[k] >> 16;
+      const uint32_t s = hist[dg] + (rds[k] & 0xffffu);
       st_id[s] = rid[k];
-      st_dig[s] = (uint16_t)rdig[k];
+      st_key[s] = rkey[k];
+      st_dig[s] = (uint16_t)dg;
 #pragma unroll
       for (int c = 0; c < D; ++c) st_x[c * TILE + s] = rx[k][c];
     }
@@ -351,6 +387,7 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(DevParams P, Stat
     const uint32_t dg = st_dig[j];
     const uint32_t g = gbase[dg] + (j - hist[dg]);
     dst.id[g] = st_id[j];
+    dst.key[g] = st_key[j];
 #pragma unroll
     for (int c = 0; c < D; ++c) dst.x[c][g] = st_x[c * TILE + j];
   }
@@ -367,11 +404,11 @@ template <typename T> __device__ __forceinline__ T batch_inv(const DevParams& P,
 template <typename T, int D, int KK, int INTEG>
 __device__ __forceinline__ void interior_update(const DevParams& P, uint32_t m, uint32_t q,
                                                 uint32_t l0, uint32_t l1, const uint16_t* ord,
-                                                T* const* xs, uint32_t id, T (&xn)[D]) {
+                                                SX<T> xs, uint32_t id, T (&xn)[D]) {
   T xi[D];
   const uint32_t e = ord[q];
 #pragma unroll
-  for (int c = 0; c < D; ++c) xi[c] = xs[c][e];
+  for (int c = 0; c < D; ++c) xi[c] = xs.at(c, e);
   T z[D];
 #pragma unroll
   for (int c = 0; c < D; ++c) z[c] = T(0);
@@ -385,7 +422,7 @@ __device__ __forceinline__ void interior_update(const DevParams& P, uint32_t m, 
       const uint32_t e2 = ord[g];
       T xj[D];
 #pragma unroll
-      for (int c = 0; c < D; ++c) xj[c] = xs[c][e2];
+      for (int c = 0; c < D; ++c) xj[c] = xs.at(c, e2);
       add_interaction<T, D, KK>(xi, xj, f, P);
     }
     const T inv = batch_inv<T>(P, l1 - l0);
@@ -396,7 +433,7 @@ __device__ __forceinline__ void interior_update(const DevParams& P, uint32_t m, 
     const uint32_t ea = ord[l0], eb = ord[l0 + 1];
     T xa[D], xb[D], y[D];
 #pragma unroll
-    for (int c = 0; c < D; ++c) { xa[c] = xs[c][ea]; xb[c] = xs[c][eb]; }
+    for (int c = 0; c < D; ++c) { xa[c] = xs.at(c, ea); xb[c] = xs.at(c, eb); }
     pair_flow<T, D, KK>(xa, xb, q == l0, y, P);
     split_finish<T, D>(y, z, xn, P, true);
   }
@@ -407,7 +444,7 @@ __device__ __forceinline__ void interior_update(const DevParams& P, uint32_t m, 
 //   key_l    : n u32 scratch;  ks : n u64 scratch (16-B aligned);  ord : n u16
 template <typename T, int D, int KK, int INTEG, int BLOCK>
 __device__ __forceinline__ void bucket_compute(const DevParams& P, State<T, D> dst, uint32_t s0,
-                                               uint32_t n, const uint32_t* id_l, T* const* xs,
+                                               uint32_t n, const uint32_t* id_l, SX<T> xs,
                                                uint32_t* key_l, unsigned long long* ks,
                                                uint16_t* ord, uint32_t* cnt, uint32_t* off,
                                                uint32_t* wsum) {
@@ -453,11 +490,12 @@ __device__ __forceinline__ void bucket_compute(const DevParams& P, State<T, D> d
       check_finite<T, D>(xn, P, id, m);
     } else {
 #pragma unroll
-      for (int c = 0; c < D; ++c) xn[c] = xs[c][e];
+      for (int c = 0; c < D; ++c) xn[c] = xs.at(c, e);
     }
     dst.id[P0] = id;
 #pragma unroll
     for (int c = 0; c < D; ++c) dst.x[c][P0] = xn[c];
+    if (P.dbg_order) P.dbg_order[P0] = id;
   }
 }
 
@@ -513,9 +551,7 @@ static __global__ void __launch_bounds__(BLOCK) bucket_step_kernel(DevParams P, 
     }
     __syncthreads();
     mbar_wait(bar, 0);
-    T* xs[3];
-#pragma unroll
-    for (int c = 0; c < D; ++c) xs[c] = xr[c] + ox;
+    const SX<T> xs{xr[0] + ox, (uint32_t)(xstride / sizeof(T))};
     bucket_compute<T, D, KK, INTEG, BLOCK>(P, dst, s0, n, id_raw + oi, xs, key_l, ks, ord, cnt,
                                            off, wsum);
   } else {
@@ -546,13 +582,11 @@ static __global__ void __launch_bounds__(BLOCK) bucket_step_kernel(DevParams P, 
     uint32_t* id_l = reinterpret_cast<uint32_t*>(xr + (size_t)D * BIG_CAP);
     uint32_t* key_l = id_l + BIG_CAP;
     uint16_t* ord = reinterpret_cast<uint16_t*>(key_l + BIG_CAP);
-    T* xs[3];
-#pragma unroll
-    for (int c = 0; c < D; ++c) xs[c] = xr + (size_t)c * BIG_CAP;
+    const SX<T> xs{xr, BIG_CAP};
     for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
       id_l[e] = src.id[s0 + e];
 #pragma unroll
-      for (int c = 0; c < D; ++c) xs[c][e] = src.x[c][s0 + e];
+      for (int c = 0; c < D; ++c) xs.at(c, e) = src.x[c][s0 + e];
     }
     __syncthreads();
     bucket_compute<T, D, KK, INTEG, BLOCK>(P, dst, s0, n, id_l, xs, key_l, ks, ord, cnt, off, wsum);
@@ -565,10 +599,13 @@ static __global__ void __launch_bounds__(BLOCK) bucket_step_kernel(DevParams P, 
 }
 
 // batches that straddle bucket boundaries: one warp per owning boundary.
-// Members were copied (unchanged) to their sorted positions in dst.
-template <typename T, int D, int KK, int INTEG>
-static __global__ void __launch_bounds__(256) straddle_kernel(DevParams P, State<T, D> dst,
-                                                       const uint32_t* __restrict__ S) {
+// Members were written (unchanged) at their sorted positions in `strad` by
+// the bucket kernels.  !FUSED: results go back to `strad` (sorted output).
+// FUSED: results are appended to the pass-1 buckets of step m+1 in `dst`.
+template <typename T, int D, int KK, int INTEG, bool FUSED>
+static __global__ void __launch_bounds__(256) straddle_kernel(DevParams P, State<T, D> strad,
+                                                              const uint32_t* __restrict__ S,
+                                                              State<T, D> dst, uint32_t* cur_next) {
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t bnd = warp + 1;  // boundaries 1 .. nbuckets-1
@@ -580,17 +617,16 @@ static __global__ void __launch_bounds__(256) straddle_kernel(DevParams P, State
   if (b0 == Pb) return;             // boundary at a batch start: no straddle
   if (S[bnd - 1] > b0) return;      // an earlier boundary inside the batch owns it
   const uint32_t m = (uint32_t)*P.step;
-  const uint32_t sz = (uint32_t)(b1 - b0);
-  // each lane updates members lane, lane+32, ... ; reads of all members from dst
+  const uint32_t sz = b1 - b0;
   T xnew[3][D];
   uint32_t idv[3];
   int cntm = 0;
   for (uint32_t q = lane; q < sz; q += 32, ++cntm) {
     const uint32_t g = b0 + q;
-    const uint32_t id = dst.id[g];
+    const uint32_t id = strad.id[g];
     T xi[D], z[D], xn[D];
 #pragma unroll
-    for (int c = 0; c < D; ++c) { xi[c] = dst.x[c][g]; z[c] = T(0); }
+    for (int c = 0; c < D; ++c) { xi[c] = strad.x[c][g]; z[c] = T(0); }
     if (P.has_noise) Normals<T, D>::get(P, id, m, TAG_NOISE, z);
     if (INTEG == 0) {
       T f[D];
@@ -600,7 +636,7 @@ static __global__ void __launch_bounds__(256) straddle_kernel(DevParams P, State
         if (h == g) continue;
         T xj[D];
 #pragma unroll
-        for (int c = 0; c < D; ++c) xj[c] = dst.x[c][h];
+        for (int c = 0; c < D; ++c) xj[c] = strad.x[c][h];
         add_interaction<T, D, KK>(xi, xj, f, P);
       }
       const T inv = batch_inv<T>(P, sz);
@@ -610,7 +646,7 @@ static __global__ void __launch_bounds__(256) straddle_kernel(DevParams P, State
     } else {
       T xa[D], xb[D], y[D];
 #pragma unroll
-      for (int c = 0; c < D; ++c) { xa[c] = dst.x[c][b0]; xb[c] = dst.x[c][b0 + 1]; }
+      for (int c = 0; c < D; ++c) { xa[c] = strad.x[c][b0]; xb[c] = strad.x[c][b0 + 1]; }
       pair_flow<T, D, KK>(xa, xb, q == 0, y, P);
       split_finish<T, D>(y, z, xn, P, true);
     }
@@ -622,10 +658,555 @@ static __global__ void __launch_bounds__(256) straddle_kernel(DevParams P, State
   __syncwarp();
   int k = 0;
   for (uint32_t q = lane; q < sz; q += 32, ++k) {
+    if (FUSED) {
+      const uint32_t kn = shuffle_key(P, idv[k], m + 1);
+      const uint32_t g = atomicAdd(&cur_next[(kn >> (32u - P.b1)) * CUR1_STRIDE], 1u);
+      dst.id[g] = idv[k];
+      dst.key[g] = kn;
 #pragma unroll
-    for (int c = 0; c < D; ++c) dst.x[c][b0 + q] = xnew[k][c];
+      for (int c = 0; c < D; ++c) dst.x[c][g] = xnew[k][c];
+    } else {
+#pragma unroll
+      for (int c = 0; c < D; ++c) strad.x[c][b0 + q] = xnew[k][c];
+    }
   }
-  (void)idv;
+}
+
+// ------------------------------------------------ fused bucket step (V3)
+// One CTA per final bucket of step m.  (1) bulk-load the bucket (TMA),
+// (2) exact in-smem sort by (key_m, id) with a counting sort on SB sub-digit
+// bits and 32-bit composite keys, (3) Eq. (2.2) + update of every interior
+// batch, (4) the updated records are partitioned for step m+1 by the top b1
+// bits of key_{m+1} straight into dst (cursor-reserved runs, smem-staged,
+// coalesced), removing the separate pass-1 scatter of the next step.
+template <typename T, int D> __host__ __device__ constexpr size_t fused_smem_bytes(uint32_t cap,
+                                                                                  uint32_t SB) {
+  return (size_t)(2 * (SB > 10 ? (1u << SB) : 1024u) + 1024 + 64) * 4 + 16  // cnt, off, gbase, wsum, mbar
+         + (size_t)(cap + 8) * 8                                            // ids, keys (TMA windows)
+         + (size_t)D * (((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15)  // x (TMA window, in place)
+         + (size_t)cap * 12                                                 // ks, ta, tb
+         + (((size_t)cap * 4 + 15) & ~(size_t)15);                          // ord, inv (u16)
+}
+
+// One batch handled by one thread (remainder batches larger than the lane
+// group, or p > 32): all members computed from the old positions, then
+// written in place.  Returns nothing; sets tb[e] = digit<<16 | slot.
+template <typename T, int D, int KK, int INTEG>
+__device__ __noinline__ void serial_batch(const DevParams& P, uint32_t m, uint32_t l0, uint32_t l1,
+                                          const uint16_t* ord, const uint32_t* id_l, SX<T> xs,
+                                          uint32_t* ta, uint32_t* tb, uint32_t* ocnt, uint32_t osh) {
+  T xn[65][D];
+  const uint32_t sz = l1 - l0;
+  for (uint32_t q = l0; q < l1; ++q) {
+    T out[D];
+    interior_update<T, D, KK, INTEG>(P, m, q, l0, l1, ord, xs, id_l[ord[q]], out);
+#pragma unroll
+    for (int c = 0; c < D; ++c) xn[q - l0][c] = out[c];
+  }
+  for (uint32_t i = 0; i < sz; ++i) {
+    const uint32_t e = ord[l0 + i], id = id_l[e];
+    check_finite<T, D>(xn[i], P, id, m);
+    const uint32_t kn = shuffle_key(P, id, m + 1);
+    const uint32_t dg = kn >> osh;
+    ta[e] = kn;
+    tb[e] = (dg << 16) | atomicAdd(&ocnt[dg], 1u);
+#pragma unroll
+    for (int c = 0; c < D; ++c) xs.at(c, e) = xn[i][c];
+  }
+}
+
+// oversized bucket (never expected at the automatic capacity; forced in
+// tests): sorted-order compute on one of NBIG global scratch slots, claimed
+// from a small pool and released at the end (holders are resident, so waiters
+// always make progress), then a per-element append into the step-(m+1)
+// pass-1 buckets.
+template <typename T, int D, int KK, int INTEG, int BLOCK>
+__device__ __noinline__ void fused_big_path(const DevParams& P, State<T, D> src, State<T, D> dst,
+                                            uint32_t* cur_next, uint32_t s0, uint32_t n, uint32_t m,
+                                            uint32_t* cnt, uint32_t* off, uint32_t* wsum) {
+    // oversized bucket: sorted-order compute on a global scratch slot, then a
+    // per-element append into the step-(m+1) pass-1 buckets (rare path)
+    __shared__ uint32_t slot;
+    if (threadIdx.x == 0) {
+      slot = 0xffffffffu;
+      if (n <= BIG_CAP) {
+        for (;;) {
+          for (uint32_t s = 0; s < (uint32_t)NBIG && slot == 0xffffffffu; ++s)
+            if (atomicCAS(&P.big_claim[s], 0u, 1u) == 0u) slot = s;
+          if (slot != 0xffffffffu) break;
+          __nanosleep(500);
+        }
+      }
+    }
+    __syncthreads();
+    if (slot == 0xffffffffu) {
+      if (threadIdx.x == 0) atomicExch(P.capacity_err, 1u);
+      return;
+    }
+    unsigned char* base = P.big_scratch + slot * big_slot_bytes(D * sizeof(T));
+    unsigned long long* ks = reinterpret_cast<unsigned long long*>(base);
+    T* xr = reinterpret_cast<T*>(ks + BIG_CAP + 1);
+    uint32_t* id_l = reinterpret_cast<uint32_t*>(xr + (size_t)D * BIG_CAP);
+    uint32_t* key_l = id_l + BIG_CAP;
+    uint16_t* ord = reinterpret_cast<uint16_t*>(key_l + BIG_CAP);
+    const SX<T> xs{xr, BIG_CAP};
+    for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
+      id_l[e] = src.id[s0 + e];
+#pragma unroll
+      for (int c = 0; c < D; ++c) xs.at(c, e) = src.x[c][s0 + e];
+    }
+    for (uint32_t i = threadIdx.x; i < 256; i += BLOCK) cnt[i] = 0;
+    __syncthreads();
+    bucket_compute<T, D, KK, INTEG, BLOCK>(P, src, s0, n, id_l, xs, key_l, ks, ord, cnt, off, wsum);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicExch(&P.big_claim[slot], 0u);
+    }
+    for (uint32_t q = threadIdx.x; q < n; q += BLOCK) {
+      const uint32_t P0 = s0 + q;
+      uint32_t b0, b1;
+      batch_range(P0, P, b0, b1);
+      if (b0 >= s0 && b1 <= s0 + n) {
+        const uint32_t id = src.id[P0];
+        const uint32_t kn = shuffle_key(P, id, m + 1);
+        const uint32_t g = atomicAdd(&cur_next[(kn >> (32u - P.b1)) * CUR1_STRIDE], 1u);
+        dst.id[g] = id;
+        dst.key[g] = kn;
+#pragma unroll
+        for (int c = 0; c < D; ++c) dst.x[c][g] = src.x[c][P0];
+      }
+    }
+}
+
+template <typename T, int D, int KK, int INTEG, int BLOCK>
+static __global__ void __launch_bounds__(BLOCK) bucket_fused_kernel(DevParams P, State<T, D> src,
+                                                                    State<T, D> dst,
+                                                                    const uint32_t* __restrict__ S,
+                                                                    uint32_t* __restrict__ cur_next) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const uint32_t nsb = 1u << P.SB;
+  const uint32_t ncnt = nsb > 1024u ? nsb : 1024u;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* off = cnt + ncnt;
+  uint32_t* gbase = off + ncnt;
+  uint32_t* wsum = gbase + 1024;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);
+  const uint32_t b = blockIdx.x;
+  const uint32_t s0 = S[b], n = S[b + 1] - s0;
+  if (n == 0) return;
+  const uint32_t m = (uint32_t)*P.step;
+  const uint32_t cap = P.cap;
+  for (uint32_t i = threadIdx.x; i < nsb; i += BLOCK) cnt[i] = 0;
+  if (n > cap) {
+    fused_big_path<T, D, KK, INTEG, BLOCK>(P, src, dst, cur_next, s0, n, m, cnt, off, wsum);
+    return;
+  }
+
+  // ---- fast path: everything in shared memory
+  constexpr uint32_t AX = 16 / sizeof(T);
+  const uint32_t lo_i = s0 & ~3u, oi = s0 - lo_i;
+  const uint32_t lo_x = s0 & ~(AX - 1), ox = s0 - lo_x;
+  const uint32_t bytes_i = ((oi + n + 3) & ~3u) * 4;
+  const uint32_t bytes_x = ((ox + n + AX - 1) & ~(AX - 1)) * (uint32_t)sizeof(T);
+  unsigned char* p = reinterpret_cast<unsigned char*>(bar + 2);
+  uint32_t* id_raw = reinterpret_cast<uint32_t*>(p);
+  p += (size_t)(cap + 8) * 4;
+  uint32_t* key_raw = reinterpret_cast<uint32_t*>(p);
+  p += (size_t)(cap + 8) * 4;
+  const size_t xst = ((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15;
+  T* xr[3];
+#pragma unroll
+  for (int c = 0; c < D; ++c) { xr[c] = reinterpret_cast<T*>(p); p += xst; }
+  uint32_t* ks = reinterpret_cast<uint32_t*>(p);     // composites grouped by sub-digit
+  uint32_t* ta = ks + cap;                           // composite by e -> key_{m+1} by e
+  uint32_t* tb = ta + cap;                           // sd<<16|slot by e -> out digit<<16|slot by e
+  uint16_t* ord = reinterpret_cast<uint16_t*>(tb + cap);  // sorted position -> e
+  uint16_t* inv = ord + cap;                         // staging index -> e
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_expect_tx(bar, 2 * bytes_i + D * bytes_x);
+    bulk_g2s(id_raw, src.id + lo_i, bytes_i, bar);
+    bulk_g2s(key_raw, src.key + lo_i, bytes_i, bar);
+#pragma unroll
+    for (int c = 0; c < D; ++c) bulk_g2s(xr[c], src.x[c] + lo_x, bytes_x, bar);
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  const uint32_t* id_l = id_raw + oi;
+  const uint32_t* key_l = key_raw + oi;
+  const SX<T> xs{xr[0] + ox, (uint32_t)(xst / sizeof(T))};
+
+  // 1. carried keys; counting sort by SB sub-digit bits; 32-bit (key, id) composites
+  const uint32_t shsb = 32u - P.B - P.SB;
+  const uint32_t lowmask = (P.lowbits >= 32u) ? 0xffffffffu : ((1u << P.lowbits) - 1u);
+  for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
+    const uint32_t id = id_l[e];
+    const uint32_t key = key_l[e];
+    const uint32_t sd = (key >> shsb) & (nsb - 1u);
+    ta[e] = ((key & lowmask) << P.idbits) | id;
+    tb[e] = (sd << 16) | atomicAdd(&cnt[sd], 1u);
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < nsb; i += BLOCK) off[i] = cnt[i];
+  __syncthreads();
+  block_excl_scan<BLOCK>(off, nsb, wsum);
+  // 2. composites grouped by sub-digit
+  for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
+    const uint32_t t = tb[e];
+    ks[off[t >> 16] + (t & 0xffffu)] = ta[e];
+  }
+  __syncthreads();
+  // 3. exact rank of each element inside its (~1 element) sub-bucket
+  for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
+    const uint32_t sd = tb[e] >> 16, v = ta[e];
+    const uint32_t a = off[sd], c = cnt[sd];
+    uint32_t r = a;
+    for (uint32_t i = 0; i < c; ++i) r += (ks[a + i] < v) ? 1u : 0u;
+    ord[r] = (uint16_t)e;
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < 1024u; i += BLOCK) cnt[i] = 0;  // -> output digit counts
+  // interior batches [kfirst, klast) of this bucket; the rest straddle
+  uint32_t kfirst = batch_index(s0, P);
+  if (kfirst * P.p < s0) ++kfirst;
+  uint32_t klast;
+  {
+    const uint32_t kl = batch_index(s0 + n - 1, P);
+    klast = (batch_end(kl, P) <= s0 + n) ? kl + 1 : kl;
+  }
+  const uint32_t head = (kfirst < klast) ? kfirst * P.p - s0 : n;
+  const uint32_t tail = (kfirst < klast) ? batch_end(klast - 1, P) - s0 : n;
+  __syncthreads();
+  if (P.dbg_order)
+    for (uint32_t q = threadIdx.x; q < n; q += BLOCK) P.dbg_order[s0 + q] = id_l[ord[q]];
+  // straddling members: unchanged, to their sorted positions in src (own range)
+  for (uint32_t q = threadIdx.x; q < n; q += BLOCK) {
+    if (q < head || q >= tail) {
+      const uint32_t e = ord[q];
+      tb[e] = 0xffffffffu;
+      src.id[s0 + q] = id_l[e];
+#pragma unroll
+      for (int c = 0; c < D; ++c) src.x[c][s0 + q] = xs.at(c, e);
+    }
+  }
+  // 4. Eq. (2.2) + update: one lane group (G = pow2 >= p lanes) per batch,
+  //    members exchanged by warp shuffles, results written in place
+  const uint32_t osh = 32u - P.b1;
+  const uint32_t G = P.group;
+  if (G != 0) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t gpw = 32u / G, gi = lane / G, li = lane & (G - 1);
+    const uint32_t stride = (BLOCK / 32) * gpw;
+    for (uint32_t kb = kfirst + warp * gpw; kb < klast; kb += stride) {  // warp-uniform
+      const uint32_t k = kb + gi;
+      const bool valid = k < klast;
+      const uint32_t l0 = valid ? k * P.p - s0 : 0;
+      const uint32_t sz = valid ? batch_end(k, P) - s0 - l0 : 0;
+      const bool act = valid && sz <= G && li < sz;
+      const uint32_t e = act ? ord[l0 + li] : 0u;
+      T xi[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) xi[c] = act ? xs.at(c, e) : T(0);
+      const uint32_t id = act ? id_l[e] : 0u;
+      T xn[D];
+      if (INTEG == 0) {
+        T f[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) f[c] = T(0);
+        for (uint32_t j = 0; j < G; ++j) {  // ascending sorted position
+          T xj[D];
+#pragma unroll
+          for (int c = 0; c < D; ++c) xj[c] = __shfl_sync(0xffffffffu, xi[c], (int)j, (int)G);
+          if (act && j < sz && j != li) add_interaction<T, D, KK>(xi, xj, f, P);
+        }
+        if (act) {
+          T z[D];
+#pragma unroll
+          for (int c = 0; c < D; ++c) z[c] = T(0);
+          if (P.has_noise) Normals<T, D>::get(P, id, m, TAG_NOISE, z);
+          const T inv_b = batch_inv<T>(P, sz);
+#pragma unroll
+          for (int c = 0; c < D; ++c) f[c] *= inv_b;
+          em_update<T, D>(xi, f, z, xn, P, true);
+        }
+      } else {  // split exact pair flow, p = 2 = G
+        T xo[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) xo[c] = __shfl_xor_sync(0xffffffffu, xi[c], 1, 2);
+        if (act) {
+          T xa[D], xb[D], y[D], z[D];
+#pragma unroll
+          for (int c = 0; c < D; ++c) {
+            xa[c] = li == 0 ? xi[c] : xo[c];
+            xb[c] = li == 0 ? xo[c] : xi[c];
+            z[c] = T(0);
+          }
+          if (P.has_noise) Normals<T, D>::get(P, id, m, TAG_NOISE, z);
+          pair_flow<T, D, KK>(xa, xb, li == 0, y, P);
+          split_finish<T, D>(y, z, xn, P, true);
+        }
+      }
+      if (act) {
+        check_finite<T, D>(xn, P, id, m);
+        const uint32_t kn = shuffle_key(P, id, m + 1);
+        const uint32_t dg = kn >> osh;
+        ta[e] = kn;
+        tb[e] = (dg << 16) | atomicAdd(&cnt[dg], 1u);
+#pragma unroll
+        for (int c = 0; c < D; ++c) xs.at(c, e) = xn[c];
+      }
+    }
+  }
+  // batches too large for a lane group (remainder batch, or p > 32): one thread each
+  {
+    const uint32_t first_big = (G == 0) ? kfirst : ((klast > kfirst && batch_end(klast - 1, P) - (klast - 1) * P.p > G) ? klast - 1 : klast);
+    for (uint32_t k = first_big + threadIdx.x; k < klast; k += BLOCK)
+      serial_batch<T, D, KK, INTEG>(P, m, k * P.p - s0, batch_end(k, P) - s0, ord, id_l, xs, ta,
+                                    tb, cnt, osh);
+  }
+  __syncthreads();
+  // 5. reserve runs in the step-(m+1) buckets, stage by digit, coalesced write
+  const uint32_t nout = 1u << P.b1;
+  for (uint32_t i = threadIdx.x; i < nout; i += BLOCK) {
+    const uint32_t h = cnt[i];
+    off[i] = h;
+    gbase[i] = h ? atomicAdd(&cur_next[i * CUR1_STRIDE], h) : 0u;
+  }
+  __syncthreads();
+  const uint32_t total = block_excl_scan<BLOCK>(off, nout, wsum);
+  for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
+    const uint32_t t = tb[e];
+    if (t != 0xffffffffu) inv[off[t >> 16] + (t & 0xffffu)] = (uint16_t)e;
+  }
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < total; j += BLOCK) {
+    const uint32_t e = inv[j];
+    const uint32_t dg = tb[e] >> 16;
+    const uint32_t g = gbase[dg] + (j - off[dg]);
+    dst.id[g] = id_l[e];
+    dst.key[g] = ta[e];
+#pragma unroll
+    for (int c = 0; c < D; ++c) dst.x[c][g] = xs.at(c, e);
+  }
+}
+
+// ------------------------------------------- fused bucket step, p = 2 (lean)
+// Same contract as bucket_fused_kernel, specialised for pairs: items held in
+// registers through the sort phases (ITEMS per thread, cap <= BLOCK*ITEMS),
+// one thread per pair; K is odd with s(z) = s(-z), so the partner's force is
+// exactly -f (the same terms the oracle sums).
+template <typename T, int D> __host__ __device__ constexpr size_t pair_smem_bytes(uint32_t cap,
+                                                                                 uint32_t SB) {
+  return (size_t)(2 * (SB > 10 ? (1u << SB) : 1024u) + 1024 + 64) * 4 + 16  // cnt, off, gbase, wsum, mbar
+         + (size_t)(cap + 8) * 8                                           // ids, keys (TMA windows)
+         + (size_t)D * (((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15) // x (TMA window, in place)
+         + (size_t)cap * 4                                                 // ks -> digit|slot
+         + (((size_t)cap * 4 + 15) & ~(size_t)15);                         // ord, inv (u16)
+}
+
+template <typename T, int D, int KK, int INTEG>
+__device__ __forceinline__ void pair_update(const DevParams& P, uint32_t m, const T (&x0)[D],
+                                            const T (&x1)[D], uint32_t id0, uint32_t id1,
+                                            T (&y0)[D], T (&y1)[D]) {
+  T z0[D], z1[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) { z0[c] = T(0); z1[c] = T(0); }
+  if (P.has_noise) {
+    Normals<T, D>::get(P, id0, m, TAG_NOISE, z0);
+    Normals<T, D>::get(P, id1, m, TAG_NOISE, z1);
+  }
+  if (INTEG == 0) {
+    T zz[D], f0[D], f1[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) zz[c] = x0[c] - x1[c];
+    const T sc = kernel_scale<T, D, KK>(zz, P);  // 1/(p-1) = 1
+#pragma unroll
+    for (int c = 0; c < D; ++c) { f0[c] = sc * zz[c]; f1[c] = -f0[c]; }
+    em_update<T, D>(x0, f0, z0, y0, P, true);
+    em_update<T, D>(x1, f1, z1, y1, P, true);
+  } else {
+    T a[D], b[D];
+    pair_flow<T, D, KK>(x0, x1, true, a, P);
+    pair_flow<T, D, KK>(x0, x1, false, b, P);
+    split_finish<T, D>(a, z0, y0, P, true);
+    split_finish<T, D>(b, z1, y1, P, true);
+  }
+}
+
+template <typename T, int D, int KK, int INTEG, int BLOCK, int ITEMS>
+static __global__ void __launch_bounds__(BLOCK) bucket_pair_kernel(DevParams P, State<T, D> src,
+                                                                   State<T, D> dst,
+                                                                   const uint32_t* __restrict__ S,
+                                                                   uint32_t* __restrict__ cur_next) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const uint32_t b = blockIdx.x;
+  const uint32_t s0 = S[b], n = S[b + 1] - s0;
+  if (n == 0) return;
+  const uint32_t nsb = 1u << P.SB;
+  const uint32_t ncnt = nsb > 1024u ? nsb : 1024u;  // also holds the <= 1024 output digits
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* off = cnt + ncnt;
+  uint32_t* gbase = off + nsb;
+  uint32_t* wsum = gbase + 1024;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);
+  const uint32_t cap = P.cap;
+  const uint32_t m = (uint32_t)*P.step;
+  if (n > cap) {  // shared with the general kernel (needs nsb >= 256 entries of cnt/off)
+    fused_big_path<T, D, KK, INTEG, BLOCK>(P, src, dst, cur_next, s0, n, m, cnt, off, wsum);
+    return;
+  }
+  constexpr uint32_t AX = 16 / sizeof(T);
+  const uint32_t lo_i = s0 & ~3u, oi = s0 - lo_i;
+  const uint32_t lo_x = s0 & ~(AX - 1), ox = s0 - lo_x;
+  const uint32_t bytes_i = ((oi + n + 3) & ~3u) * 4;
+  const uint32_t bytes_x = ((ox + n + AX - 1) & ~(AX - 1)) * (uint32_t)sizeof(T);
+  unsigned char* p = reinterpret_cast<unsigned char*>(bar + 2);
+  uint32_t* id_raw = reinterpret_cast<uint32_t*>(p);
+  p += (size_t)(cap + 8) * 4;
+  uint32_t* key_raw = reinterpret_cast<uint32_t*>(p);
+  p += (size_t)(cap + 8) * 4;
+  const uint32_t xst = (uint32_t)((((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15) / sizeof(T));
+  T* xr = reinterpret_cast<T*>(p);
+  p += (size_t)D * xst * sizeof(T);
+  uint32_t* ks = reinterpret_cast<uint32_t*>(p);   // composites; then digit<<16|slot by e
+  uint32_t* tb = ks;
+  uint32_t* ta = key_raw + oi;                      // key_m by e; then key_{m+1} by e
+  uint16_t* ord = reinterpret_cast<uint16_t*>(ks + cap);
+  uint16_t* inv = ord + cap;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_expect_tx(bar, 2 * bytes_i + D * bytes_x);
+    bulk_g2s(id_raw, src.id + lo_i, bytes_i, bar);
+    bulk_g2s(key_raw, src.key + lo_i, bytes_i, bar);
+#pragma unroll
+    for (int c = 0; c < D; ++c) bulk_g2s(xr + (size_t)c * xst, src.x[c] + lo_x, bytes_x, bar);
+  }
+  for (uint32_t i = threadIdx.x; i < nsb; i += BLOCK) cnt[i] = 0;
+  __syncthreads();
+  mbar_wait(bar, 0);
+  const uint32_t* id_l = id_raw + oi;
+  const uint32_t* key_l = key_raw + oi;
+  const SX<T> xs{xr + ox, xst};
+
+  // 1-3. exact (key, id) sort: counting sort on SB sub-digit bits + rank in sub-bucket
+  const uint32_t shsb = 32u - P.B - P.SB;
+  const uint32_t lowmask = (P.lowbits >= 32u) ? 0xffffffffu : ((1u << P.lowbits) - 1u);
+  uint32_t rc[ITEMS], rs[ITEMS];
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const uint32_t e = k * BLOCK + threadIdx.x;
+    if (e < n) {
+      const uint32_t key = key_l[e];
+      const uint32_t sd = (key >> shsb) & (nsb - 1u);
+      rc[k] = ((key & lowmask) << P.idbits) | id_l[e];
+      rs[k] = (sd << 16) | atomicAdd(&cnt[sd], 1u);
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < nsb; i += BLOCK) off[i] = cnt[i];
+  __syncthreads();
+  block_excl_scan<BLOCK>(off, nsb, wsum);
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const uint32_t e = k * BLOCK + threadIdx.x;
+    if (e < n) ks[off[rs[k] >> 16] + (rs[k] & 0xffffu)] = rc[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const uint32_t e = k * BLOCK + threadIdx.x;
+    if (e < n) {
+      const uint32_t sd = rs[k] >> 16;
+      const uint32_t a = off[sd], c = cnt[sd];
+      uint32_t r = a;
+      for (uint32_t i = a; i < a + c; ++i) r += (ks[i] < rc[k]) ? 1u : 0u;
+      ord[r] = (uint16_t)e;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {  // ks is dead: reuse as digit|slot (straddlers keep ~0)
+    const uint32_t e = k * BLOCK + threadIdx.x;
+    if (e < n) tb[e] = 0xffffffffu;
+  }
+  for (uint32_t i = threadIdx.x; i < 1024u; i += BLOCK) cnt[i] = 0;
+  if (P.dbg_order)
+    for (uint32_t q = threadIdx.x; q < n; q += BLOCK) P.dbg_order[s0 + q] = id_l[ord[q]];
+  // interior pairs: even global starts in [s0, end), end excludes a final triple (N odd)
+  const uint32_t N = (uint32_t)P.n;
+  const uint32_t pend = (N & 1u) ? N - 3u : N;
+  const uint32_t head = s0 & 1u;                         // local index of the first pair
+  const uint32_t lim = min(s0 + n, pend) - s0;           // pairs must end at <= lim
+  const uint32_t npairs = (lim > head) ? (lim - head) / 2 : 0u;
+  const uint32_t covered = head + 2 * npairs;            // [head, covered) are interior
+  const bool triple = (N & 1u) && (pend >= s0) && (N <= s0 + n);
+  __syncthreads();
+  // straddlers: unchanged to their sorted positions in src (own range)
+  for (uint32_t q = threadIdx.x; q < n; q += BLOCK) {
+    const bool in_triple = triple && (s0 + q >= pend);
+    if ((q < head || q >= covered) && !in_triple) {
+      const uint32_t e = ord[q];
+      src.id[s0 + q] = id_l[e];
+#pragma unroll
+      for (int c = 0; c < D; ++c) src.x[c][s0 + q] = xs.at(c, e);
+    }
+  }
+  // 4. one thread per pair
+  const uint32_t osh = 32u - P.b1;
+  constexpr int PITEMS = (ITEMS + 1) / 2;
+#pragma unroll
+  for (int k = 0; k < PITEMS; ++k) {
+    const uint32_t j = k * BLOCK + threadIdx.x;
+    if (j < npairs) {
+      const uint32_t q = head + 2 * j;
+      const uint32_t e0 = ord[q], e1 = ord[q + 1];
+      const uint32_t id0 = id_l[e0], id1 = id_l[e1];
+      T x0[D], x1[D], y0[D], y1[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) { x0[c] = xs.at(c, e0); x1[c] = xs.at(c, e1); }
+      pair_update<T, D, KK, INTEG>(P, m, x0, x1, id0, id1, y0, y1);
+      check_finite<T, D>(y0, P, id0, m);
+      check_finite<T, D>(y1, P, id1, m);
+      const uint32_t k0 = shuffle_key(P, id0, m + 1), k1 = shuffle_key(P, id1, m + 1);
+      ta[e0] = k0;
+      ta[e1] = k1;
+      tb[e0] = ((k0 >> osh) << 16) | atomicAdd(&cnt[k0 >> osh], 1u);
+      tb[e1] = ((k1 >> osh) << 16) | atomicAdd(&cnt[k1 >> osh], 1u);
+#pragma unroll
+      for (int c = 0; c < D; ++c) { xs.at(c, e0) = y0[c]; xs.at(c, e1) = y1[c]; }
+    }
+  }
+  if (triple && threadIdx.x == 0)  // the remainder batch of size 3 (N odd), EM only
+    serial_batch<T, D, KK, INTEG>(P, m, pend - s0, n, ord, id_l, xs, ta, tb, cnt, osh);
+  __syncthreads();
+  // 5. reserve runs in the step-(m+1) buckets, stage by digit, coalesced write
+  const uint32_t nout = 1u << P.b1;
+  for (uint32_t i = threadIdx.x; i < nout; i += BLOCK) {
+    const uint32_t h = cnt[i];
+    off[i] = h;
+    gbase[i] = h ? atomicAdd(&cur_next[i * CUR1_STRIDE], h) : 0u;
+  }
+  __syncthreads();
+  const uint32_t total = block_excl_scan<BLOCK>(off, nout, wsum);
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const uint32_t e = k * BLOCK + threadIdx.x;
+    if (e < n) {
+      const uint32_t t = tb[e];
+      if (t != 0xffffffffu) inv[off[t >> 16] + (t & 0xffffu)] = (uint16_t)e;
+    }
+  }
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < total; j += BLOCK) {
+    const uint32_t e = inv[j];
+    const uint32_t dg = tb[e] >> 16;
+    const uint32_t g = gbase[dg] + (j - off[dg]);
+    dst.id[g] = id_l[e];
+    dst.key[g] = ta[e];
+#pragma unroll
+    for (int c = 0; c < D; ++c) dst.x[c][g] = xs.at(c, e);
+  }
 }
 
 // ------------------------------------------------------------------ RBM-r

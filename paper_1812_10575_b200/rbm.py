@@ -261,9 +261,11 @@ class RBM:
         rbm_gather(self.ctx, id_begin, id_end, out.data_ptr(), MEM_DEVICE)
         return out
 
-    def storage_order(self):
-        out = self.torch.empty(self.n, dtype=self.torch.int32, device=self.device)
+    def step_permutation(self):
+        """One rbm_step that also returns its permutation (sorted position -> id)."""
+        out = self.torch.full((self.n,), -1, dtype=self.torch.int32, device=self.device)
         rbm_debug_permutation(self.ctx, out.data_ptr())
+        rbm_step(self.ctx)
         self.stream.synchronize()
         return out.cpu().numpy().view("uint32")
 

@@ -92,8 +92,7 @@ def test_permutation_bit_exact(R, O, n, p, cap):
     m = 7
     c = cfg_of("smooth", 1, p, n, step0=m, debug_bucket_cap=cap)
     s = R.RBM(c)
-    s.step()
-    order = s.storage_order()
+    order = s.step_permutation()
     want = O.permutation(c, m)
     assert np.array_equal(order, want)
     s.sync()
@@ -290,8 +289,7 @@ def test_capacity_fallback_parity(R, O):
     s = R.RBM(c)
     assert s.layout[2] == 512
     x0 = s.gather(host=True)
-    s.step()
-    assert np.array_equal(s.storage_order(), O.permutation(c, 2))
+    assert np.array_equal(s.step_permutation(), O.permutation(c, 2))
     assert E(s.gather(host=True), O.rbm1_step(c, x0, 2)) <= 1e-12
     s.close()
 
@@ -318,8 +316,7 @@ def test_full_size_sampled(R, O, which):
     m = 0
     s = R.RBM(c)
     x0 = s.gather(host=True).astype(np.float64)
-    s.step()
-    order = s.storage_order()
+    order = s.step_permutation()
     x1 = s.gather(host=True).astype(np.float64)
     n, p = c["n"], c["p"]
     assert np.array_equal(np.bincount(order, minlength=n), np.ones(n, dtype=np.int64))
