@@ -107,7 +107,7 @@ rbm_status init_impl(rbm_ctx* c, const rbm_config* cfg, void* wsp, size_t ws_byt
   CU(cudaMemcpyAsync(c->nonfinite, &clean, 8, cudaMemcpyHostToDevice, st));
   CU(cudaMemsetAsync(c->capacity_err, 0, 4, st));
   const uint32_t s0[2] = {0u, (uint32_t)cfg->n};
-  if (c->L.B == 0) CU(cudaMemcpyAsync(c->S[0], s0, 8, cudaMemcpyHostToDevice, st));
+  if (c->L.B == 0) CU(cudaMemcpyAsync(c->S, s0, 8, cudaMemcpyHostToDevice, st));
   CU(cudaMemsetAsync(c->big_claim, 0, NBIG * 4, st));
   if (cfg->init != RBM_INIT_USER) c->eng->init_state(*c, st);
   CU(cudaGetLastError());

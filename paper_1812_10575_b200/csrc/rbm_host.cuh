@@ -39,6 +39,9 @@ struct Workspace {
 struct Layout {
   uint32_t B = 0, b1 = 0, b2 = 0, nbuckets = 1, cap = 0;
   uint32_t SB = 8, idbits = 1, lowbits = 0;
+  uint32_t cap1 = 0;     // gapped capacity of a pass-1 bucket (2-pass layouts)
+  uint32_t cap2 = 0;     // gapped capacity of a final bucket
+  uint64_t slots = 0;    // elements per state buffer: max(N, 2^b1 cap1, 2^B cap2)
 };
 constexpr int FUSED_BLOCK = 256;
 constexpr int PAIR_BLOCK = 512, PAIR_ITEMS = 5;  // p = 2 lean kernel: capacity <= 2560
@@ -62,12 +65,13 @@ struct rbm_ctx {
   uint64_t xstride = 0;  // elements between coordinate arrays of one state buffer
   uint32_t* idbuf[2] = {nullptr, nullptr};
   uint32_t* keybuf[2] = {nullptr, nullptr};  // carried shuffle keys (fused pipeline)
-  // per step-parity q = m & 1: histogram/offsets/cursors of pass 1 and the
-  // final-bucket starts of step m (the fused bucket step fills step m+1's)
-  uint32_t *hist1[2] = {nullptr, nullptr}, *off1[2] = {nullptr, nullptr},
-           *cur1[2] = {nullptr, nullptr}, *tile_off[2] = {nullptr, nullptr}, *S[2] = {nullptr, nullptr};
-  uint32_t *hist2 = nullptr, *cur2 = nullptr, *big_claim = nullptr;
-  bool partitioned = false;  // state stored in the pass-1 buckets of step `step`
+  // gapped-bucket pipeline.  cur1[q]: counts (cursors) of the buckets the
+  // state of step m (q = m & 1) is partitioned into -- pass-1 buckets (2-pass)
+  // or final buckets (1-pass); the fused step fills cur1[q ^ 1] for step m+1.
+  uint32_t *cur1[2] = {nullptr, nullptr};
+  uint32_t *prefix1 = nullptr, *tile_off = nullptr, *S = nullptr, *cur2 = nullptr;
+  uint32_t* big_claim = nullptr;
+  bool partitioned = false;  // state stored in the gapped buckets of step `step`
   uint64_t* step_dev = nullptr;
   unsigned long long* nonfinite = nullptr;
   uint32_t* capacity_err = nullptr;
@@ -130,20 +134,20 @@ inline Layout choose_layout(const rbm_config& c) {
   if (n <= 2048) {
     L.B = 0;  // one bucket: sorted-output kernel
   } else {
-    // target mean bucket size (tuning knob RBM_BUCKET_TARGET, default 1024)
-    double target = 1024.0;
+    // target mean bucket size (tuning knob RBM_BUCKET_TARGET, default 2048)
+    double target = 2048.0;
     if (const char* e = std::getenv("RBM_BUCKET_TARGET")) target = std::atof(e);
-    if (!(target >= 64.0 && target <= 2048.0)) target = 1024.0;
+    if (!(target >= 64.0 && target <= 2048.0)) target = 2048.0;
     L.B = ceil_log2((double)n / target);
     if (L.B < 2) L.B = 2;
     if (L.B > 18) L.B = 18;
   }
   if (L.B <= 10) { L.b1 = L.B; L.b2 = 0; }
   else {
-    L.b1 = (L.B + 1) / 2;
+    L.b1 = L.B / 2;  // fused-output digit <= pass-2 digit: longer runs in the fused scatter
     if (const char* e = std::getenv("RBM_B1")) {  // tuning knob: pass-1 / fused-output digit bits
       const int v = std::atoi(e);
-      if (v >= 6 && v <= 10 && L.B - v >= 6 && L.B - v <= 10) L.b1 = (uint32_t)v;
+      if (v >= 5 && v <= 10 && L.B - v >= 5 && L.B - v <= 10) L.b1 = (uint32_t)v;
     }
     L.b2 = L.B - L.b1;
   }
@@ -159,6 +163,23 @@ inline Layout choose_layout(const rbm_config& c) {
     if (L.cap > FUSED_CAP_MAX) L.cap = FUSED_CAP_MAX;
   }
   if (c.debug_bucket_cap) L.cap = c.debug_bucket_cap;
+  // gapped capacities: mean + 12 sigma + 64 (overflow probability ~1e-33 per
+  // bucket; an overflow is flagged as RBM_ERR_CAPACITY), multiples of 64 so
+  // every bucket starts 256-B aligned (TMA)
+  auto gcap = [](double mu, uint32_t floor_) {
+    uint64_t v = (uint64_t)(mu + 12.0 * std::sqrt(mu) + 64.0);
+    if (v < floor_) v = floor_;
+    return (uint32_t)((v + 63) & ~63ull);
+  };
+  L.slots = n;
+  if (L.B > 0) {
+    L.cap2 = gcap((double)n / L.nbuckets, L.cap + 64);
+    L.slots = std::max<uint64_t>(L.slots, (uint64_t)L.nbuckets * L.cap2);
+    if (L.b2) {
+      L.cap1 = gcap((double)n / (1u << L.b1), 64);
+      L.slots = std::max<uint64_t>(L.slots, (uint64_t)(1u << L.b1) * L.cap1);
+    }
+  }
   return L;
 }
 
@@ -222,24 +243,19 @@ inline void carve(rbm_ctx& c, Workspace& ws) {
   const rbm_config& k = c.cfg;
   const size_t es = elt_size(k);
   const uint64_t n = k.n;
-  c.xstride = (n + 63) & ~63ull;  // per-coordinate stride: 256-B aligned SoA arrays (TMA)
+  const uint64_t slots = (k.scheme == RBM_SCHEME_RBM1) ? c.L.slots : n;
+  c.xstride = (slots + 63) & ~63ull;  // per-coordinate stride: 256-B aligned SoA arrays (TMA)
   for (int b = 0; b < 2; ++b) {
-    c.idbuf[b] = ws.take<uint32_t>(n);
-    c.keybuf[b] = ws.take<uint32_t>(n);
+    c.idbuf[b] = ws.take<uint32_t>(c.xstride);
+    c.keybuf[b] = ws.take<uint32_t>(c.xstride);
     c.xbuf[b] = ws.take<unsigned char>(c.xstride * k.d * es);
   }
-  for (int q = 0; q < 2; ++q) {
-    c.hist1[q] = ws.take<uint32_t>(1024);
-    c.off1[q] = ws.take<uint32_t>(1025);
-    c.cur1[q] = ws.take<uint32_t>(1024 * CUR1_STRIDE);
-    c.tile_off[q] = ws.take<uint32_t>(1025);
-    c.S[q] = ws.take<uint32_t>((size_t)c.L.nbuckets + 1);
-  }
+  for (int q = 0; q < 2; ++q) c.cur1[q] = ws.take<uint32_t>(1024 * CUR1_STRIDE);
+  c.prefix1 = ws.take<uint32_t>(1025);
+  c.tile_off = ws.take<uint32_t>(1025);
+  c.S = ws.take<uint32_t>((size_t)c.L.nbuckets + 1);
   c.big_claim = ws.take<uint32_t>(NBIG);
-  if (c.L.b2) {
-    c.hist2 = ws.take<uint32_t>(c.L.nbuckets);
-    c.cur2 = ws.take<uint32_t>((size_t)c.L.nbuckets * CUR2_STRIDE);
-  }
+  if (c.L.b2) c.cur2 = ws.take<uint32_t>((size_t)c.L.nbuckets * CUR2_STRIDE);
   c.step_dev = ws.take<uint64_t>(1);
   c.nonfinite = ws.take<unsigned long long>(1);
   c.capacity_err = ws.take<uint32_t>(1);
@@ -345,29 +361,28 @@ struct Engine final : EngineBase {
   }
 
   void gather(rbm_ctx& c, uint64_t i0, uint64_t i1, void* out, cudaStream_t s) override {
-    gather_kernel<T, D><<<grid_for(c.cfg.n, 256), 256, 0, s>>>(c.cfg.n, st(c, c.cur), i0, i1,
-                                                                reinterpret_cast<T*>(out));
+    if (c.cfg.scheme == RBM_SCHEME_RBM1 && c.L.B > 0 && c.partitioned) {
+      Gapped g;
+      g.cap = c.L.b2 ? c.L.cap1 : c.L.cap2;
+      g.nb = 1u << c.L.b1;
+      g.cnt = c.cur1[c.step & 1];
+      g.cstride = CUR1_STRIDE;
+      gather_gapped_kernel<T, D><<<grid_for((uint64_t)g.nb * g.cap, 256), 256, 0, s>>>(
+          g, st(c, c.cur), i0, i1, reinterpret_cast<T*>(out));
+    } else {
+      gather_kernel<T, D><<<grid_for(c.cfg.n, 256), 256, 0, s>>>(c.cfg.n, st(c, c.cur), i0, i1,
+                                                                  reinterpret_cast<T*>(out));
+    }
   }
 
-  // histogram + offsets of the pass-1 digit of step m + mofs into parity slot q
-  void top_hist(rbm_ctx& c, cudaStream_t s, uint32_t mofs, int q, bool mark) {
-    const uint64_t n = c.cfg.n;
-    cudaMemsetAsync(c.hist1[q], 0, 1024 * 4, s);
-    if (mark) c.mark(s);
-    hist_top_kernel<<<grid_for(n, 512, 148 * 4), 512, 0, s>>>(c.P, c.hist1[q], mofs);
-    if (mark) c.mark(s);
-    scan_top_kernel<<<1, 1024, 0, s>>>(c.P, c.hist1[q], c.off1[q], c.cur1[q], c.tile_off[q],
-                                       c.S[q], SC_TILE);
-  }
-
-  void fused(rbm_ctx& c, cudaStream_t s, State<T, D> in, State<T, D> out, const uint32_t* S,
+  void fused(rbm_ctx& c, cudaStream_t s, State<T, D> in, State<T, D> out, uint32_t ocap,
              uint32_t* cur_next) {
     if (use_pair)
       bucket_pair_kernel<T, D, KK, INTEG, PAIR_BLOCK, PAIR_ITEMS>
-          <<<c.L.nbuckets, PAIR_BLOCK, pr_smem, s>>>(c.P, in, out, S, cur_next);
+          <<<c.L.nbuckets, PAIR_BLOCK, pr_smem, s>>>(c.P, in, c.L.cap2, c.S, out, ocap, cur_next);
     else
       bucket_fused_kernel<T, D, KK, INTEG, FUSED_BLOCK>
-          <<<c.L.nbuckets, FUSED_BLOCK, fu_smem, s>>>(c.P, in, out, S, cur_next);
+          <<<c.L.nbuckets, FUSED_BLOCK, fu_smem, s>>>(c.P, in, c.L.cap2, c.S, out, ocap, cur_next);
   }
 
   void step(rbm_ctx& c, cudaStream_t s) override {
@@ -376,52 +391,53 @@ struct Engine final : EngineBase {
     const Layout& L = c.L;
     const uint64_t n = c.cfg.n;
     const int q = (int)(c.step & 1);
-    if (L.B == 0) {  // single bucket: sort + step, sorted output
+    if (L.B == 0) {  // single bucket: sort + step, sorted contiguous output
       c.mark(s);
       bucket_step_kernel<T, D, KK, INTEG, BK_BLOCK><<<1, BK_BLOCK, bk_smem, s>>>(
-          P, st(c, c.cur), st(c, c.cur ^ 1), c.S[0]);
+          P, st(c, c.cur), st(c, c.cur ^ 1), c.S);
       c.cur ^= 1;
       c.mark(s);
       advance_kernel<<<1, 1, 0, s>>>(c.step_dev);
       c.mark(s);
       return;
     }
-    if (!c.partitioned) {  // prologue: pass-1 partition of step m from any storage order
-      top_hist(c, s, 0, q, false);
+    // capacity of the buckets the state of a step lives in (pass-1 or final)
+    const uint32_t pcap = L.b2 ? L.cap1 : L.cap2;
+    if (!c.partitioned) {  // prologue: any storage order -> gapped buckets of step m
+      cudaMemsetAsync(c.cur1[q], 0, 1024 * CUR1_STRIDE * 4, s);
       scatter_kernel<T, D, 1, SC_BLOCK, SC_ITEMS>
           <<<(unsigned)((n + SC_TILE - 1) / SC_TILE), SC_BLOCK, sc_smem, s>>>(
-              P, st(c, c.cur), st(c, c.cur ^ 1), c.cur1[q], nullptr, nullptr);
+              P, st(c, c.cur), st(c, c.cur ^ 1), c.cur1[q], pcap, nullptr, nullptr, 0);
       c.cur ^= 1;
       c.partitioned = true;
     }
-    // pass-1 histogram/offsets of step m+1 (compute-only), consumed by the fused step
-    top_hist(c, s, 1, q ^ 1, true);
+    cudaMemsetAsync(c.cur1[q ^ 1], 0, 1024 * CUR1_STRIDE * 4, s);  // step-(m+1) cursors
     const unsigned straddle_grid = (unsigned)(((uint64_t)L.nbuckets * 32 + 255) / 256);
     State<T, D> A = st(c, c.cur), Bf = st(c, c.cur ^ 1);
+    c.mark(s);
+    tile_scan_kernel<<<1, 1024, 0, s>>>(P, c.cur1[q], c.prefix1, c.tile_off, c.S, SC_TILE);
     if (L.b2 == 0) {
       // A holds the final buckets of step m; the fused step writes m+1's into B
       c.mark(s);
-      fused(c, s, A, Bf, c.S[q], c.cur1[q ^ 1]);
+      fused(c, s, A, Bf, L.cap2, c.cur1[q ^ 1]);
       c.mark(s);
-      straddle_kernel<T, D, KK, INTEG, true><<<straddle_grid, 256, 0, s>>>(P, A, c.S[q], Bf,
-                                                                           c.cur1[q ^ 1]);
+      straddle_kernel<T, D, KK, INTEG><<<straddle_grid, 256, 0, s>>>(P, A, L.cap2, c.S, Bf, L.cap2,
+                                                                     c.cur1[q ^ 1]);
       c.cur ^= 1;
     } else {
       // A holds the pass-1 buckets of step m: split them by the next b2 bits into B
       const unsigned tiles2 = (unsigned)((n + SC_TILE - 1) / SC_TILE + (1u << L.b1));
-      cudaMemsetAsync(c.hist2, 0, (size_t)L.nbuckets * 4, s);
-      c.mark(s);
-      hist_sub_kernel<<<tiles2, 256, 0, s>>>(P, A.key, c.off1[q], c.tile_off[q], c.hist2, SC_TILE);
-      c.mark(s);
-      scan_sub_kernel<<<1u << L.b1, 512, 0, s>>>(P, c.hist2, c.off1[q], c.S[q], c.cur2);
+      cudaMemsetAsync(c.cur2, 0, (size_t)L.nbuckets * CUR2_STRIDE * 4, s);
       c.mark(s);
       scatter_kernel<T, D, 2, SC_BLOCK, SC_ITEMS>
-          <<<tiles2, SC_BLOCK, sc_smem, s>>>(P, A, Bf, c.cur2, c.off1[q], c.tile_off[q]);
+          <<<tiles2, SC_BLOCK, sc_smem, s>>>(P, A, Bf, c.cur2, L.cap2, c.cur1[q], c.tile_off, L.cap1);
       c.mark(s);
-      fused(c, s, Bf, A, c.S[q], c.cur1[q ^ 1]);
+      final_scan_kernel<<<1u << L.b1, 512, 0, s>>>(P, c.cur2, c.prefix1, c.S);
       c.mark(s);
-      straddle_kernel<T, D, KK, INTEG, true><<<straddle_grid, 256, 0, s>>>(P, Bf, c.S[q], A,
-                                                                           c.cur1[q ^ 1]);
+      fused(c, s, Bf, A, L.cap1, c.cur1[q ^ 1]);
+      c.mark(s);
+      straddle_kernel<T, D, KK, INTEG><<<straddle_grid, 256, 0, s>>>(P, Bf, L.cap2, c.S, A, L.cap1,
+                                                                     c.cur1[q ^ 1]);
     }
     c.mark(s);
     advance_kernel<<<1, 1, 0, s>>>(c.step_dev);
@@ -479,13 +495,13 @@ inline const char* const* kernel_names(const rbm_ctx& c, uint32_t* count) {
   static const char* const r[] = {"rbmr_draw", "scan_reduce", "scan_parts", "scan_down",
                                   "rbmr_fill", "rbmr_delta", "rbmr_apply", "advance"};
   static const char* const b0[] = {"bucket_step", "advance"};
-  static const char* const p1[] = {"hist_next", "scan_next", "bucket_step", "straddle", "advance"};
-  static const char* const p2[] = {"hist_next", "scan_next", "hist_sub", "scan_sub", "scatter_sub",
-                                   "bucket_step", "straddle", "advance"};
+  static const char* const p1[] = {"tile_scan", "bucket_step", "straddle", "advance"};
+  static const char* const p2[] = {"tile_scan", "scatter_sub", "final_scan", "bucket_step",
+                                   "straddle", "advance"};
   if (c.cfg.scheme == RBM_SCHEME_RBMR) { *count = 8; return r; }
   if (c.L.B == 0) { *count = 2; return b0; }
-  if (c.L.b2 == 0) { *count = 5; return p1; }
-  *count = 8;
+  if (c.L.b2 == 0) { *count = 4; return p1; }
+  *count = 6;
   return p2;
 }
 

@@ -1,27 +1,25 @@
 // rbm_kernels.cuh -- the RBM time-step kernels for sm_100a.
 //
-// RBM-1 step m (Alg. 1) as an MSD partition + fused sort/step:
-//   hist_top      compute-only histogram of the top b1 key bits over ids 0..N-1
-//   scan_top      bucket offsets / cursors of pass 1 (+ tile table of pass 2)
-//   scatter<1>    state -> buckets by the top b1 key bits (smem-staged)
-//   hist_sub      per top-bucket histogram of the next b2 bits (2-pass layouts)
-//   scan_sub      final bucket starts S[0..2^B] and pass-2 cursors
-//   scatter<2>    -> final buckets of the top B = b1+b2 key bits
-//   bucket_step   per bucket: exact in-smem sort by (key, id), then every batch
-//                 that lies inside the bucket does Eq. (2.2) + Euler-Maruyama
-//                 (or the exact pair flow) and writes in sorted order
-//   straddle_step batches that straddle two buckets
+// RBM-1 step m (Alg. 1) as an MSD key partition into GAPPED
+// buckets (fixed capacity per bucket, cursors from zero: no histogram pass)
+// fused with an exact in-bucket sort and the batch update:
+//   prologue      scatter<1>: any storage order -> pass-1 buckets by the top b1
+//                 bits of key_m (keys computed from ids once, then carried)
+//   tile_scan     pass-1 counts -> prefix and tile table
+//   scatter<2>    pass-1 bucket d1 -> final buckets (d1, next b2 bits)
+//   final_scan    final counts -> exact global bucket starts S[0..2^B]
+//   bucket_step   per final bucket: exact in-smem sort by (key_m, id); every
+//                 batch inside the bucket does Eq. (2.2) + Euler-Maruyama (or
+//                 the exact pair flow); the updated records are partitioned
+//                 straight into the pass-1 buckets of step m+1 (key_{m+1})
+//   straddle      batches that straddle two final buckets
 //   advance       m += 1
-// The resulting permutation is exactly "ids sorted by (key_m(id), id)".
+// Batches are defined on global sorted positions S[b] + rank, so the step's
+// permutation is exactly "ids sorted by (key_m(id), id)" whatever the storage.
 #pragma once
 #include "rbm_device.cuh"
 
 namespace rbm {
-
-// Cursor padding: concurrent CTAs reserve output runs with atomicAdd on the
-// cursors; one cursor per 128-B line (pass 1) / 32-B sector (pass 2) spreads
-// those atomics over the L2 slices instead of serialising them on a few lines.
-constexpr uint32_t CUR1_STRIDE = 32, CUR2_STRIDE = 8;
 
 template <typename T, int D> struct State {
   uint32_t* id;
@@ -182,12 +180,6 @@ static __global__ void gather_kernel(uint64_t n, State<T, D> st, uint64_t i0, ui
   }
 }
 
-static __global__ void copy_ids_kernel(uint64_t n, const uint32_t* __restrict__ id, uint32_t* out) {
-  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n;
-       q += (uint64_t)gridDim.x * blockDim.x)
-    out[q] = id[q];
-}
-
 static __global__ void philox_test_kernel(const uint32_t* __restrict__ in, uint32_t* out, uint64_t count) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -199,77 +191,86 @@ static __global__ void philox_test_kernel(const uint32_t* __restrict__ in, uint3
 
 static __global__ void advance_kernel(uint64_t* step) { *step += 1; }
 
-// ------------------------------------------------------- compute-only histogram
-// histogram of key_m(id) >> (32-b1) over ALL ids 0..N-1: reads no memory.
-static __global__ void __launch_bounds__(512) hist_top_kernel(DevParams P, uint32_t* __restrict__ hist,
-                                                              uint32_t mofs) {
-  __shared__ uint32_t h[1024];
-  const uint32_t nb = 1u << P.b1;
-  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) h[i] = 0;
-  __syncthreads();
-  const uint32_t m = (uint32_t)*P.step + mofs;
-  const uint32_t sh = 32u - P.b1;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < P.n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    atomicAdd(&h[shuffle_key(P, (uint32_t)i, m) >> sh], 1u);
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x)
-    if (h[i]) atomicAdd(&hist[i], h[i]);
+// ------------------------------------------------------------ gapped layout
+// nb buckets of fixed capacity cap; bucket u holds cnt[u*cstride] records at
+// physical slots [u*cap, u*cap + cnt).  Cursor padding spreads the run-
+// reservation atomics of concurrent CTAs over the L2 slices.
+constexpr uint32_t CUR1_STRIDE = 32, CUR2_STRIDE = 8;
+
+struct Gapped {
+  uint32_t cap;           // slots per bucket (multiple of 64)
+  uint32_t nb;            // buckets
+  const uint32_t* cnt;    // counts (= final cursor values)
+  uint32_t cstride;       // cursor stride (u32 elements)
+};
+
+// gather from a gapped layout: thread per physical slot, holes skipped
+template <typename T, int D>
+static __global__ void gather_gapped_kernel(Gapped g, State<T, D> st, uint64_t i0, uint64_t i1,
+                                            T* __restrict__ out) {
+  const uint64_t total = (uint64_t)g.nb * g.cap;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < total;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = (uint32_t)(q / g.cap), s = (uint32_t)(q - (uint64_t)u * g.cap);
+    if (s >= g.cnt[(size_t)u * g.cstride]) continue;
+    const uint64_t id = st.id[q];
+    if (id >= i0 && id < i1) {
+#pragma unroll
+      for (int c = 0; c < D; ++c) out[(id - i0) * D + c] = st.x[c][q];
+    }
+  }
 }
 
-// single block: off1 = excl-scan(hist1), cursor1 = off1, tile table for pass 2,
-// and (one-pass layouts) the final bucket starts S.
-static __global__ void __launch_bounds__(1024) scan_top_kernel(DevParams P, const uint32_t* __restrict__ hist,
-                                                        uint32_t* off1, uint32_t* cur1,
-                                                        uint32_t* tile_off, uint32_t* S,
-                                                        uint32_t tile) {
+// single block: pass-1 counts -> prefix1 (exclusive, size nb1+1) and tile table
+// of pass 2; for one-pass layouts the final starts S = prefix of the counts.
+static __global__ void __launch_bounds__(1024) tile_scan_kernel(DevParams P, const uint32_t* __restrict__ cnt1,
+                                                                uint32_t* prefix1, uint32_t* tile_off,
+                                                                uint32_t* S, uint32_t tile) {
   __shared__ uint32_t a[1025];
   __shared__ uint32_t t[1025];
   __shared__ uint32_t ws[33];
   const uint32_t nb = 1u << P.b1;
   for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) {
-    a[i] = hist[i];
-    t[i] = (hist[i] + tile - 1) / tile;
+    const uint32_t c = cnt1[(size_t)i * CUR1_STRIDE];
+    a[i] = c;
+    t[i] = (c + tile - 1) / tile;
   }
   __syncthreads();
   block_excl_scan<1024>(a, nb, ws);
   const uint32_t ntiles = block_excl_scan<1024>(t, nb, ws);
   for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) {
-    off1[i] = a[i];
-    cur1[i * CUR1_STRIDE] = a[i];
+    prefix1[i] = a[i];
     tile_off[i] = t[i];
     if (P.b2 == 0) S[i] = a[i];
   }
   if (threadIdx.x == 0) {
-    off1[nb] = (uint32_t)P.n;
+    prefix1[nb] = (uint32_t)P.n;
     tile_off[nb] = ntiles;
     if (P.b2 == 0) S[nb] = (uint32_t)P.n;
   }
 }
 
-// one block per top bucket u: S[u<<b2 | i] = off1[u] + excl-scan_i hist2[u<<b2 | .]
-static __global__ void __launch_bounds__(512) scan_sub_kernel(DevParams P, const uint32_t* __restrict__ hist2,
-                                                              const uint32_t* __restrict__ off1,
-                                                              uint32_t* S, uint32_t* cur2) {
-  __shared__ uint32_t a[512];
+// one block per pass-1 bucket d1: S[d1<<b2 | d2] = prefix1[d1] + excl-scan of
+// the final counts (d1, .)
+static __global__ void __launch_bounds__(512) final_scan_kernel(DevParams P, const uint32_t* __restrict__ cnt2,
+                                                                const uint32_t* __restrict__ prefix1,
+                                                                uint32_t* S) {
+  __shared__ uint32_t a[1024];
   __shared__ uint32_t ws[33];
   const uint32_t u = blockIdx.x, nb2 = 1u << P.b2, base = u << P.b2;
-  for (uint32_t i = threadIdx.x; i < nb2; i += blockDim.x) a[i] = hist2[base + i];
+  for (uint32_t i = threadIdx.x; i < nb2; i += blockDim.x) a[i] = cnt2[(size_t)(base + i) * CUR2_STRIDE];
   __syncthreads();
   block_excl_scan<512>(a, nb2, ws);
-  const uint32_t o = off1[u];
-  for (uint32_t i = threadIdx.x; i < nb2; i += blockDim.x) {
-    S[base + i] = o + a[i];
-    cur2[(base + i) * CUR2_STRIDE] = o + a[i];
-  }
+  const uint32_t o = prefix1[u];
+  for (uint32_t i = threadIdx.x; i < nb2; i += blockDim.x) S[base + i] = o + a[i];
   if (u == 0 && threadIdx.x == 0) S[P.nbuckets] = (uint32_t)P.n;
 }
 
-// tile t of a bucket-aligned pass: bucket u and element range [lo, hi)
-__device__ __forceinline__ bool aligned_tile(const uint32_t* __restrict__ tile_off,
-                                             const uint32_t* __restrict__ off1, uint32_t nb1,
-                                             uint32_t t, uint32_t tile, uint32_t& u, uint32_t& lo,
-                                             uint32_t& hi) {
+// tile t of pass 2: pass-1 bucket u and its element range [lo, hi) (relative)
+__device__ __forceinline__ bool gapped_tile(const uint32_t* __restrict__ tile_off,
+                                            const uint32_t* __restrict__ cnt1, uint32_t nb1,
+                                            uint32_t t, uint32_t tile, uint32_t& u, uint32_t& lo,
+                                            uint32_t& hi) {
   if (t >= tile_off[nb1]) return false;
   uint32_t a = 0, b = nb1;  // largest u with tile_off[u] <= t
   while (b - a > 1) {
@@ -277,40 +278,26 @@ __device__ __forceinline__ bool aligned_tile(const uint32_t* __restrict__ tile_o
     if (tile_off[mid] <= t) a = mid; else b = mid;
   }
   u = a;
-  lo = off1[u] + (t - tile_off[u]) * tile;
-  hi = min(lo + tile, off1[u + 1]);
+  lo = (t - tile_off[u]) * tile;
+  hi = min(lo + tile, cnt1[(size_t)u * CUR1_STRIDE]);
   return true;
 }
 
-// per top-bucket histogram of the next b2 key bits (reads ids only)
-static __global__ void __launch_bounds__(256) hist_sub_kernel(DevParams P, const uint32_t* __restrict__ keys,
-                                                       const uint32_t* __restrict__ off1,
-                                                       const uint32_t* __restrict__ tile_off,
-                                                       uint32_t* hist2, uint32_t tile) {
-  __shared__ uint32_t h[512];
-  uint32_t u, lo, hi;
-  if (!aligned_tile(tile_off, off1, 1u << P.b1, blockIdx.x, tile, u, lo, hi)) return;
-  const uint32_t nb2 = 1u << P.b2;
-  for (uint32_t i = threadIdx.x; i < nb2; i += blockDim.x) h[i] = 0;
-  __syncthreads();
-  const uint32_t sh = 32u - P.b1 - P.b2, mask = nb2 - 1;
-  for (uint32_t e = lo + threadIdx.x; e < hi; e += blockDim.x)
-    atomicAdd(&h[(keys[e] >> sh) & mask], 1u);
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < nb2; i += blockDim.x)
-    if (h[i]) atomicAdd(&hist2[(u << P.b2) | i], h[i]);
-}
-
 // --------------------------------------------------------------- scatter pass
-// LEVEL 1: tiles over the whole array, digit = top b1 bits, cursors cur[digit].
-// LEVEL 2: tiles aligned to top buckets u, digit = next b2 bits,
-//          cursors cur[(u << b2) | digit].
-// Order inside a bucket is irrelevant: bucket_step sorts each bucket exactly.
+// LEVEL 1 (prologue): contiguous source [0, N); keys computed from ids
+//   (key_m); digit = top b1 bits (= top B bits for one-pass layouts).
+// LEVEL 2: source = pass-1 bucket u (tiles aligned to buckets), carried keys;
+//   digit = next b2 bits; destination bucket (u << b2 | digit).
+// Destination: gapped buckets of capacity dcap, cursors from zero; records are
+// staged in shared memory by digit so each reserved run is written coalesced.
+// Order inside a bucket is irrelevant: the bucket step sorts exactly.
 template <typename T, int D, int LEVEL, int BLOCK, int ITEMS>
 static __global__ void __launch_bounds__(BLOCK) scatter_kernel(DevParams P, State<T, D> src,
-                                                        State<T, D> dst, uint32_t* cur,
-                                                        const uint32_t* __restrict__ off1,
-                                                        const uint32_t* __restrict__ tile_off) {
+                                                               State<T, D> dst, uint32_t* cur,
+                                                               uint32_t dcap,
+                                                               const uint32_t* __restrict__ cnt1,
+                                                               const uint32_t* __restrict__ tile_off,
+                                                               uint32_t scap) {
   constexpr int TILE = BLOCK * ITEMS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw);  // 1024
@@ -321,21 +308,23 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(DevParams P, Stat
   T* st_x = reinterpret_cast<T*>(st_key + TILE);           // D*TILE
   uint16_t* st_dig = reinterpret_cast<uint16_t*>(st_x + D * TILE);  // TILE
 
-  uint32_t lo, hi, u = 0, bits, sh;
+  uint32_t lo, hi, u = 0, bits, sh, sbase;
   if (LEVEL == 1) {
     lo = blockIdx.x * TILE;
     if (lo >= P.n) return;
     hi = (uint32_t)min((uint64_t)lo + TILE, P.n);
     bits = P.b1;
     sh = 32u - P.b1;
+    sbase = 0;
   } else {
-    if (!aligned_tile(tile_off, off1, 1u << P.b1, blockIdx.x, TILE, u, lo, hi)) return;
+    if (!gapped_tile(tile_off, cnt1, 1u << P.b1, blockIdx.x, TILE, u, lo, hi)) return;
     bits = P.b2;
     sh = 32u - P.b1 - P.b2;
+    sbase = u * scap;
   }
-  const uint32_t nbins = 1u << bits, mask = nbins - 1;
   constexpr uint32_t CS = (LEVEL == 1) ? CUR1_STRIDE : CUR2_STRIDE;
-  uint32_t* mycur = cur + (LEVEL == 1 ? 0u : (u << P.b2)) * CS;
+  const uint32_t nbins = 1u << bits, mask = nbins - 1;
+  const uint32_t dbase0 = (LEVEL == 1) ? 0u : (u << P.b2);  // first destination bucket
   for (uint32_t i = threadIdx.x; i < nbins; i += BLOCK) hist[i] = 0;
   __syncthreads();
 
@@ -347,10 +336,10 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(DevParams P, Stat
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t e = k * BLOCK + threadIdx.x;
     if (e < cnt) {
-      rid[k] = src.id[lo + e];
-      if (LEVEL != 1) rkey[k] = src.key[lo + e];
+      rid[k] = src.id[sbase + lo + e];
+      if (LEVEL != 1) rkey[k] = src.key[sbase + lo + e];
 #pragma unroll
-      for (int c = 0; c < D; ++c) rx[k][c] = src.x[c][lo + e];
+      for (int c = 0; c < D; ++c) rx[k][c] = src.x[c][sbase + lo + e];
     }
   }
 #pragma unroll
@@ -363,10 +352,10 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(DevParams P, Stat
     }
   }
   __syncthreads();
-  // reserve global space per bin, then local exclusive offsets
+  // reserve runs in the destination buckets, then local exclusive offsets
   for (uint32_t i = threadIdx.x; i < nbins; i += BLOCK) {
     const uint32_t h = hist[i];
-    gbase[i] = h ? atomicAdd(&mycur[i * CS], h) : 0u;
+    gbase[i] = h ? atomicAdd(&cur[(size_t)(dbase0 + i) * CS], h) : 0u;
   }
   block_excl_scan<BLOCK>(hist, nbins, wsum);  // hist -> local offsets
 #pragma unroll
@@ -385,7 +374,12 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(DevParams P, Stat
   __syncthreads();
   for (uint32_t j = threadIdx.x; j < cnt; j += BLOCK) {
     const uint32_t dg = st_dig[j];
-    const uint32_t g = gbase[dg] + (j - hist[dg]);
+    const uint32_t slot = gbase[dg] + (j - hist[dg]);
+    if (slot >= dcap) {  // bucket capacity exceeded (probability ~1e-30): fail loudly
+      atomicExch(P.capacity_err, 1u);
+      continue;
+    }
+    const uint32_t g = (dbase0 + dg) * dcap + slot;
     dst.id[g] = st_id[j];
     dst.key[g] = st_key[j];
 #pragma unroll
@@ -393,10 +387,7 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(DevParams P, Stat
   }
 }
 
-// ------------------------------------------------------- fused bucket step
-// One CTA per final bucket b = positions [S[b], S[b+1]).  All ids in it share
-// the top B key bits, so sorting it by (key, id) in shared memory puts every
-// element at its exact global sorted position S[b] + rank.
+// ------------------------------------------------------- bucket step pieces
 template <typename T> __device__ __forceinline__ T batch_inv(const DevParams& P, uint32_t sz) {
   return (sz == P.p) ? Prm<T>::invp(P) : T(1) / T(sz - 1);
 }
@@ -439,12 +430,14 @@ __device__ __forceinline__ void interior_update(const DevParams& P, uint32_t m, 
   }
 }
 
-// Sort the loaded bucket by (key, id) and step every interior batch.
+// Sort the loaded bucket by (key, id) and step every interior batch; bucket
+// element at sorted position q (global position s0+q) is written to dst[obase+q].
 //   id_l, xs : bucket records in load order (n of them)
 //   key_l    : n u32 scratch;  ks : n u64 scratch (16-B aligned);  ord : n u16
 template <typename T, int D, int KK, int INTEG, int BLOCK>
 __device__ __forceinline__ void bucket_compute(const DevParams& P, State<T, D> dst, uint32_t s0,
-                                               uint32_t n, const uint32_t* id_l, SX<T> xs,
+                                               uint32_t obase, uint32_t n, const uint32_t* id_l,
+                                               SX<T> xs,
                                                uint32_t* key_l, unsigned long long* ks,
                                                uint16_t* ord, uint32_t* cnt, uint32_t* off,
                                                uint32_t* wsum) {
@@ -492,9 +485,9 @@ __device__ __forceinline__ void bucket_compute(const DevParams& P, State<T, D> d
 #pragma unroll
       for (int c = 0; c < D; ++c) xn[c] = xs.at(c, e);
     }
-    dst.id[P0] = id;
+    dst.id[obase + q] = id;
 #pragma unroll
-    for (int c = 0; c < D; ++c) dst.x[c][P0] = xn[c];
+    for (int c = 0; c < D; ++c) dst.x[c][obase + q] = xn[c];
     if (P.dbg_order) P.dbg_order[P0] = id;
   }
 }
@@ -552,7 +545,7 @@ static __global__ void __launch_bounds__(BLOCK) bucket_step_kernel(DevParams P, 
     __syncthreads();
     mbar_wait(bar, 0);
     const SX<T> xs{xr[0] + ox, (uint32_t)(xstride / sizeof(T))};
-    bucket_compute<T, D, KK, INTEG, BLOCK>(P, dst, s0, n, id_raw + oi, xs, key_l, ks, ord, cnt,
+    bucket_compute<T, D, KK, INTEG, BLOCK>(P, dst, s0, s0, n, id_raw + oi, xs, key_l, ks, ord, cnt,
                                            off, wsum);
   } else {
     // oversized bucket (never expected at the automatic capacity, forced in
@@ -589,7 +582,7 @@ static __global__ void __launch_bounds__(BLOCK) bucket_step_kernel(DevParams P, 
       for (int c = 0; c < D; ++c) xs.at(c, e) = src.x[c][s0 + e];
     }
     __syncthreads();
-    bucket_compute<T, D, KK, INTEG, BLOCK>(P, dst, s0, n, id_l, xs, key_l, ks, ord, cnt, off, wsum);
+    bucket_compute<T, D, KK, INTEG, BLOCK>(P, dst, s0, s0, n, id_l, xs, key_l, ks, ord, cnt, off, wsum);
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
@@ -598,14 +591,17 @@ static __global__ void __launch_bounds__(BLOCK) bucket_step_kernel(DevParams P, 
   }
 }
 
-// batches that straddle bucket boundaries: one warp per owning boundary.
-// Members were written (unchanged) at their sorted positions in `strad` by
-// the bucket kernels.  !FUSED: results go back to `strad` (sorted output).
-// FUSED: results are appended to the pass-1 buckets of step m+1 in `dst`.
-template <typename T, int D, int KK, int INTEG, bool FUSED>
+// batches that straddle final buckets: one warp per owning boundary.  Their
+// members were written (unchanged) by the bucket kernels to their sorted
+// places in their own gapped ranges of `strad`: position P of bucket b sits at
+// physical slot b*cap + (P - S[b]).  Results are appended to the step-(m+1)
+// buckets of `dst` (capacity ocap, cursors cur_next).
+template <typename T, int D, int KK, int INTEG>
 static __global__ void __launch_bounds__(256) straddle_kernel(DevParams P, State<T, D> strad,
+                                                              uint32_t cap,
                                                               const uint32_t* __restrict__ S,
-                                                              State<T, D> dst, uint32_t* cur_next) {
+                                                              State<T, D> dst, uint32_t ocap,
+                                                              uint32_t* cur_next) {
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t bnd = warp + 1;  // boundaries 1 .. nbuckets-1
@@ -618,79 +614,152 @@ static __global__ void __launch_bounds__(256) straddle_kernel(DevParams P, State
   if (S[bnd - 1] > b0) return;      // an earlier boundary inside the batch owns it
   const uint32_t m = (uint32_t)*P.step;
   const uint32_t sz = b1 - b0;
+  // physical slot of every member (buckets walked forward from bnd-1)
+  uint32_t phys[3];
+  {
+    uint32_t bb = bnd - 1;
+    int k = 0;
+    for (uint32_t q = 0; q < sz; ++q) {
+      const uint32_t Pq = b0 + q;
+      while (Pq >= S[bb + 1]) ++bb;
+      if ((q & 31u) == (uint32_t)lane) phys[k++] = bb * cap + (Pq - S[bb]);
+    }
+  }
   T xnew[3][D];
   uint32_t idv[3];
-  int cntm = 0;
-  for (uint32_t q = lane; q < sz; q += 32, ++cntm) {
-    const uint32_t g = b0 + q;
-    const uint32_t id = strad.id[g];
+  const uint32_t rounds = (sz + 31) / 32;
+  for (uint32_t r = 0; r < rounds; ++r) {  // warp-uniform: every lane reaches the shuffles
+    const uint32_t q = r * 32 + lane;
+    const bool act = q < sz;
+    const uint32_t g = act ? (r == 0 ? phys[0] : (r == 1 ? phys[1] : phys[2])) : 0u;
+    const uint32_t id = act ? strad.id[g] : 0u;
     T xi[D], z[D], xn[D];
 #pragma unroll
-    for (int c = 0; c < D; ++c) { xi[c] = strad.x[c][g]; z[c] = T(0); }
-    if (P.has_noise) Normals<T, D>::get(P, id, m, TAG_NOISE, z);
+    for (int c = 0; c < D; ++c) { xi[c] = act ? strad.x[c][g] : T(0); z[c] = T(0); }
+    if (act && P.has_noise) Normals<T, D>::get(P, id, m, TAG_NOISE, z);
     if (INTEG == 0) {
       T f[D];
 #pragma unroll
       for (int c = 0; c < D; ++c) f[c] = T(0);
-      for (uint32_t h = b0; h < b1; ++h) {
-        if (h == g) continue;
+      for (uint32_t h = 0; h < sz; ++h) {  // ascending sorted position
+        const uint32_t hr = h >> 5;
+        const uint32_t src_ph = hr == 0 ? phys[0] : (hr == 1 ? phys[1] : phys[2]);
+        const uint32_t gh = __shfl_sync(0xffffffffu, src_ph, (int)(h & 31u));
+        if (!act || h == q) continue;
         T xj[D];
 #pragma unroll
-        for (int c = 0; c < D; ++c) xj[c] = strad.x[c][h];
+        for (int c = 0; c < D; ++c) xj[c] = strad.x[c][gh];
         add_interaction<T, D, KK>(xi, xj, f, P);
       }
-      const T inv = batch_inv<T>(P, sz);
+      if (act) {
+        const T inv = batch_inv<T>(P, sz);
 #pragma unroll
-      for (int c = 0; c < D; ++c) f[c] *= inv;
-      em_update<T, D>(xi, f, z, xn, P, true);
+        for (int c = 0; c < D; ++c) f[c] *= inv;
+        em_update<T, D>(xi, f, z, xn, P, true);
+      }
     } else {
-      T xa[D], xb[D], y[D];
+      const uint32_t ga = __shfl_sync(0xffffffffu, phys[0], 0), gb = __shfl_sync(0xffffffffu, phys[0], 1);
+      if (act) {
+        T xa[D], xb[D], y[D];
 #pragma unroll
-      for (int c = 0; c < D; ++c) { xa[c] = strad.x[c][b0]; xb[c] = strad.x[c][b0 + 1]; }
-      pair_flow<T, D, KK>(xa, xb, q == 0, y, P);
-      split_finish<T, D>(y, z, xn, P, true);
+        for (int c = 0; c < D; ++c) { xa[c] = strad.x[c][ga]; xb[c] = strad.x[c][gb]; }
+        pair_flow<T, D, KK>(xa, xb, q == 0, y, P);
+        split_finish<T, D>(y, z, xn, P, true);
+      }
     }
-    check_finite<T, D>(xn, P, id, m);
-    idv[cntm] = id;
+    if (act) {
+      check_finite<T, D>(xn, P, id, m);
+      idv[r] = id;
 #pragma unroll
-    for (int c = 0; c < D; ++c) xnew[cntm][c] = xn[c];
+      for (int c = 0; c < D; ++c) xnew[r][c] = xn[c];
+    }
   }
   __syncwarp();
   int k = 0;
+  const uint32_t osh = 32u - P.b1;
   for (uint32_t q = lane; q < sz; q += 32, ++k) {
-    if (FUSED) {
-      const uint32_t kn = shuffle_key(P, idv[k], m + 1);
-      const uint32_t g = atomicAdd(&cur_next[(kn >> (32u - P.b1)) * CUR1_STRIDE], 1u);
-      dst.id[g] = idv[k];
-      dst.key[g] = kn;
+    const uint32_t kn = shuffle_key(P, idv[k], m + 1);
+    const uint32_t dg = kn >> osh;
+    const uint32_t slot = atomicAdd(&cur_next[(size_t)dg * CUR1_STRIDE], 1u);
+    if (slot >= ocap) { atomicExch(P.capacity_err, 1u); continue; }
+    const uint32_t g = dg * ocap + slot;
+    dst.id[g] = idv[k];
+    dst.key[g] = kn;
 #pragma unroll
-      for (int c = 0; c < D; ++c) dst.x[c][g] = xnew[k][c];
-    } else {
-#pragma unroll
-      for (int c = 0; c < D; ++c) strad.x[c][b0 + q] = xnew[k][c];
-    }
+    for (int c = 0; c < D; ++c) dst.x[c][g] = xnew[k][c];
   }
 }
 
-// ------------------------------------------------ fused bucket step (V3)
-// One CTA per final bucket of step m.  (1) bulk-load the bucket (TMA),
-// (2) exact in-smem sort by (key_m, id) with a counting sort on SB sub-digit
-// bits and 32-bit composite keys, (3) Eq. (2.2) + update of every interior
-// batch, (4) the updated records are partitioned for step m+1 by the top b1
-// bits of key_{m+1} straight into dst (cursor-reserved runs, smem-staged,
-// coalesced), removing the separate pass-1 scatter of the next step.
-template <typename T, int D> __host__ __device__ constexpr size_t fused_smem_bytes(uint32_t cap,
-                                                                                  uint32_t SB) {
-  return (size_t)(2 * (SB > 10 ? (1u << SB) : 1024u) + 1024 + 64) * 4 + 16  // cnt, off, gbase, wsum, mbar
-         + (size_t)(cap + 8) * 8                                            // ids, keys (TMA windows)
-         + (size_t)D * (((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15)  // x (TMA window, in place)
-         + (size_t)cap * 12                                                 // ks, ta, tb
-         + (((size_t)cap * 4 + 15) & ~(size_t)15);                          // ord, inv (u16)
+// oversized bucket (never expected at the automatic capacity; forced in
+// tests): sorted-order compute on one of NBIG global scratch slots, claimed
+// from a small pool and released at the end (holders are resident, so waiters
+// always make progress), written back to the bucket's own gapped range, then a
+// per-element append into the step-(m+1) buckets.
+template <typename T, int D, int KK, int INTEG, int BLOCK>
+__device__ __noinline__ void fused_big_path(const DevParams& P, State<T, D> src, State<T, D> dst,
+                                            uint32_t* cur_next, uint32_t s0, uint32_t sb, uint32_t n,
+                                            uint32_t m, uint32_t dcap, uint32_t* cnt, uint32_t* off,
+                                            uint32_t* wsum) {
+  __shared__ uint32_t slot;
+  if (threadIdx.x == 0) {
+    slot = 0xffffffffu;
+    if (n <= BIG_CAP) {
+      for (;;) {
+        for (uint32_t s = 0; s < (uint32_t)NBIG && slot == 0xffffffffu; ++s)
+          if (atomicCAS(&P.big_claim[s], 0u, 1u) == 0u) slot = s;
+        if (slot != 0xffffffffu) break;
+        __nanosleep(500);
+      }
+    }
+  }
+  __syncthreads();
+  if (slot == 0xffffffffu) {
+    if (threadIdx.x == 0) atomicExch(P.capacity_err, 1u);
+    return;
+  }
+  unsigned char* base = P.big_scratch + slot * big_slot_bytes(D * sizeof(T));
+  unsigned long long* ks = reinterpret_cast<unsigned long long*>(base);
+  T* xr = reinterpret_cast<T*>(ks + BIG_CAP + 1);
+  uint32_t* id_l = reinterpret_cast<uint32_t*>(xr + (size_t)D * BIG_CAP);
+  uint32_t* key_l = id_l + BIG_CAP;
+  uint16_t* ord = reinterpret_cast<uint16_t*>(key_l + BIG_CAP);
+  const SX<T> xs{xr, BIG_CAP};
+  for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
+    id_l[e] = src.id[sb + e];
+#pragma unroll
+    for (int c = 0; c < D; ++c) xs.at(c, e) = src.x[c][sb + e];
+  }
+  for (uint32_t i = threadIdx.x; i < 256; i += BLOCK) cnt[i] = 0;
+  __syncthreads();
+  bucket_compute<T, D, KK, INTEG, BLOCK>(P, src, s0, sb, n, id_l, xs, key_l, ks, ord, cnt, off,
+                                         wsum);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicExch(&P.big_claim[slot], 0u);
+  }
+  const uint32_t osh = 32u - P.b1;
+  for (uint32_t q = threadIdx.x; q < n; q += BLOCK) {
+    uint32_t b0, b1;
+    batch_range(s0 + q, P, b0, b1);
+    if (b0 >= s0 && b1 <= s0 + n) {
+      const uint32_t id = src.id[sb + q];
+      const uint32_t kn = shuffle_key(P, id, m + 1);
+      const uint32_t dg = kn >> osh;
+      const uint32_t s = atomicAdd(&cur_next[(size_t)dg * CUR1_STRIDE], 1u);
+      if (s >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
+      const uint32_t g = dg * dcap + s;
+      dst.id[g] = id;
+      dst.key[g] = kn;
+#pragma unroll
+      for (int c = 0; c < D; ++c) dst.x[c][g] = src.x[c][sb + q];
+    }
+  }
 }
 
 // One batch handled by one thread (remainder batches larger than the lane
 // group, or p > 32): all members computed from the old positions, then
-// written in place.  Returns nothing; sets tb[e] = digit<<16 | slot.
+// written in place; sets ta[e] = key_{m+1}, tb[e] = digit<<16 | slot.
 template <typename T, int D, int KK, int INTEG>
 __device__ __noinline__ void serial_batch(const DevParams& P, uint32_t m, uint32_t l0, uint32_t l1,
                                           const uint16_t* ord, const uint32_t* id_l, SX<T> xs,
@@ -715,74 +784,80 @@ __device__ __noinline__ void serial_batch(const DevParams& P, uint32_t m, uint32
   }
 }
 
-// oversized bucket (never expected at the automatic capacity; forced in
-// tests): sorted-order compute on one of NBIG global scratch slots, claimed
-// from a small pool and released at the end (holders are resident, so waiters
-// always make progress), then a per-element append into the step-(m+1)
-// pass-1 buckets.
-template <typename T, int D, int KK, int INTEG, int BLOCK>
-__device__ __noinline__ void fused_big_path(const DevParams& P, State<T, D> src, State<T, D> dst,
-                                            uint32_t* cur_next, uint32_t s0, uint32_t n, uint32_t m,
-                                            uint32_t* cnt, uint32_t* off, uint32_t* wsum) {
-    // oversized bucket: sorted-order compute on a global scratch slot, then a
-    // per-element append into the step-(m+1) pass-1 buckets (rare path)
-    __shared__ uint32_t slot;
-    if (threadIdx.x == 0) {
-      slot = 0xffffffffu;
-      if (n <= BIG_CAP) {
-        for (;;) {
-          for (uint32_t s = 0; s < (uint32_t)NBIG && slot == 0xffffffffu; ++s)
-            if (atomicCAS(&P.big_claim[s], 0u, 1u) == 0u) slot = s;
-          if (slot != 0xffffffffu) break;
-          __nanosleep(500);
-        }
-      }
-    }
-    __syncthreads();
-    if (slot == 0xffffffffu) {
-      if (threadIdx.x == 0) atomicExch(P.capacity_err, 1u);
-      return;
-    }
-    unsigned char* base = P.big_scratch + slot * big_slot_bytes(D * sizeof(T));
-    unsigned long long* ks = reinterpret_cast<unsigned long long*>(base);
-    T* xr = reinterpret_cast<T*>(ks + BIG_CAP + 1);
-    uint32_t* id_l = reinterpret_cast<uint32_t*>(xr + (size_t)D * BIG_CAP);
-    uint32_t* key_l = id_l + BIG_CAP;
-    uint16_t* ord = reinterpret_cast<uint16_t*>(key_l + BIG_CAP);
-    const SX<T> xs{xr, BIG_CAP};
-    for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
-      id_l[e] = src.id[s0 + e];
+// TMA: bulk-load bucket b (gapped, physical base sb = b*scap, n records) into
+// shared memory: ids, carried keys, D coordinate arrays (16-B multiples; the
+// capacity scap >= n + 64 covers the round-up).
+template <typename T, int D>
+__device__ __forceinline__ void load_bucket(State<T, D> src, uint32_t sb, uint32_t n, uint32_t* id_s,
+                                            uint32_t* key_s, T* x_s, uint32_t xst, uint64_t* bar) {
+  if (threadIdx.x == 0) {
+    const uint32_t bytes_i = ((n + 3) & ~3u) * 4;
+    constexpr uint32_t AX = 16 / sizeof(T);
+    const uint32_t bytes_x = ((n + AX - 1) & ~(AX - 1)) * (uint32_t)sizeof(T);
+    mbar_init(bar, 1);
+    mbar_expect_tx(bar, 2 * bytes_i + D * bytes_x);
+    bulk_g2s(id_s, src.id + sb, bytes_i, bar);
+    bulk_g2s(key_s, src.key + sb, bytes_i, bar);
 #pragma unroll
-      for (int c = 0; c < D; ++c) xs.at(c, e) = src.x[c][s0 + e];
-    }
-    for (uint32_t i = threadIdx.x; i < 256; i += BLOCK) cnt[i] = 0;
-    __syncthreads();
-    bucket_compute<T, D, KK, INTEG, BLOCK>(P, src, s0, n, id_l, xs, key_l, ks, ord, cnt, off, wsum);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicExch(&P.big_claim[slot], 0u);
-    }
-    for (uint32_t q = threadIdx.x; q < n; q += BLOCK) {
-      const uint32_t P0 = s0 + q;
-      uint32_t b0, b1;
-      batch_range(P0, P, b0, b1);
-      if (b0 >= s0 && b1 <= s0 + n) {
-        const uint32_t id = src.id[P0];
-        const uint32_t kn = shuffle_key(P, id, m + 1);
-        const uint32_t g = atomicAdd(&cur_next[(kn >> (32u - P.b1)) * CUR1_STRIDE], 1u);
-        dst.id[g] = id;
-        dst.key[g] = kn;
+    for (int c = 0; c < D; ++c) bulk_g2s(x_s + (size_t)c * xst, src.x[c] + sb, bytes_x, bar);
+  }
+}
+
+// Output phase shared by the fused kernels: reserve runs in the step-(m+1)
+// buckets (capacity dcap), stage by digit, coalesced write of id, key_{m+1}, x.
+template <typename T, int D, int BLOCK>
+__device__ __forceinline__ void fused_output(const DevParams& P, State<T, D> dst, uint32_t dcap,
+                                             uint32_t* cur_next, uint32_t n, const uint32_t* id_l,
+                                             const uint32_t* ta, const uint32_t* tb, SX<T> xs,
+                                             uint32_t* cnt, uint32_t* off, uint32_t* gbase,
+                                             uint16_t* inv, uint32_t* wsum) {
+  const uint32_t nout = 1u << P.b1;
+  for (uint32_t i = threadIdx.x; i < nout; i += BLOCK) {
+    const uint32_t h = cnt[i];
+    off[i] = h;
+    gbase[i] = h ? atomicAdd(&cur_next[(size_t)i * CUR1_STRIDE], h) : 0u;
+  }
+  __syncthreads();
+  const uint32_t total = block_excl_scan<BLOCK>(off, nout, wsum);
+  for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
+    const uint32_t t = tb[e];
+    if (t != 0xffffffffu) inv[off[t >> 16] + (t & 0xffffu)] = (uint16_t)e;
+  }
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < total; j += BLOCK) {
+    const uint32_t e = inv[j];
+    const uint32_t dg = tb[e] >> 16;
+    const uint32_t slot = gbase[dg] + (j - off[dg]);
+    if (slot >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
+    const uint32_t g = dg * dcap + slot;
+    dst.id[g] = id_l[e];
+    dst.key[g] = ta[e];
 #pragma unroll
-        for (int c = 0; c < D; ++c) dst.x[c][g] = src.x[c][P0];
-      }
-    }
+    for (int c = 0; c < D; ++c) dst.x[c][g] = xs.at(c, e);
+  }
+}
+
+// ------------------------------------------------ fused bucket step (general p)
+// One CTA per final bucket b of step m (gapped, capacity scap; global start
+// S[b]).  (1) TMA bulk load, (2) exact in-smem sort by (key_m, id): counting
+// sort on SB sub-digit bits + rank among 32-bit composites, (3) Eq. (2.2) +
+// update of every interior batch, one lane group (G = pow2 >= p lanes, warp
+// shuffles) per batch, results in place, (4) the updated records are
+// partitioned by the top b1 bits of key_{m+1} into dst (capacity dcap).
+template <typename T, int D> __host__ __device__ constexpr size_t fused_smem_bytes(uint32_t cap,
+                                                                                  uint32_t SB) {
+  return (size_t)(2 * (SB > 10 ? (1u << SB) : 1024u) + 1024 + 64) * 4 + 16  // cnt, off, gbase, wsum, mbar
+         + (size_t)(cap + 8) * 8                                            // ids, keys (TMA windows)
+         + (size_t)D * (((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15)  // x (TMA window, in place)
+         + (size_t)cap * 12                                                 // ks, ta, tb
+         + (((size_t)cap * 4 + 15) & ~(size_t)15);                          // ord, inv (u16)
 }
 
 template <typename T, int D, int KK, int INTEG, int BLOCK>
 static __global__ void __launch_bounds__(BLOCK) bucket_fused_kernel(DevParams P, State<T, D> src,
-                                                                    State<T, D> dst,
+                                                                    uint32_t scap,
                                                                     const uint32_t* __restrict__ S,
+                                                                    State<T, D> dst, uint32_t dcap,
                                                                     uint32_t* __restrict__ cur_next) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t nsb = 1u << P.SB;
@@ -793,58 +868,40 @@ static __global__ void __launch_bounds__(BLOCK) bucket_fused_kernel(DevParams P,
   uint32_t* wsum = gbase + 1024;
   uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);
   const uint32_t b = blockIdx.x;
-  const uint32_t s0 = S[b], n = S[b + 1] - s0;
+  const uint32_t s0 = S[b], n = S[b + 1] - s0, sb = b * scap;
   if (n == 0) return;
   const uint32_t m = (uint32_t)*P.step;
   const uint32_t cap = P.cap;
   for (uint32_t i = threadIdx.x; i < nsb; i += BLOCK) cnt[i] = 0;
   if (n > cap) {
-    fused_big_path<T, D, KK, INTEG, BLOCK>(P, src, dst, cur_next, s0, n, m, cnt, off, wsum);
+    fused_big_path<T, D, KK, INTEG, BLOCK>(P, src, dst, cur_next, s0, sb, n, m, dcap, cnt, off, wsum);
     return;
   }
-
-  // ---- fast path: everything in shared memory
-  constexpr uint32_t AX = 16 / sizeof(T);
-  const uint32_t lo_i = s0 & ~3u, oi = s0 - lo_i;
-  const uint32_t lo_x = s0 & ~(AX - 1), ox = s0 - lo_x;
-  const uint32_t bytes_i = ((oi + n + 3) & ~3u) * 4;
-  const uint32_t bytes_x = ((ox + n + AX - 1) & ~(AX - 1)) * (uint32_t)sizeof(T);
   unsigned char* p = reinterpret_cast<unsigned char*>(bar + 2);
-  uint32_t* id_raw = reinterpret_cast<uint32_t*>(p);
+  uint32_t* id_l = reinterpret_cast<uint32_t*>(p);
   p += (size_t)(cap + 8) * 4;
-  uint32_t* key_raw = reinterpret_cast<uint32_t*>(p);
+  uint32_t* key_l = reinterpret_cast<uint32_t*>(p);
   p += (size_t)(cap + 8) * 4;
-  const size_t xst = ((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15;
-  T* xr[3];
-#pragma unroll
-  for (int c = 0; c < D; ++c) { xr[c] = reinterpret_cast<T*>(p); p += xst; }
+  const uint32_t xst = (uint32_t)((((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15) / sizeof(T));
+  T* xr = reinterpret_cast<T*>(p);
+  p += (size_t)D * xst * sizeof(T);
   uint32_t* ks = reinterpret_cast<uint32_t*>(p);     // composites grouped by sub-digit
   uint32_t* ta = ks + cap;                           // composite by e -> key_{m+1} by e
-  uint32_t* tb = ta + cap;                           // sd<<16|slot by e -> out digit<<16|slot by e
+  uint32_t* tb = ta + cap;                           // sd<<16|slot by e -> out digit<<16|slot
   uint16_t* ord = reinterpret_cast<uint16_t*>(tb + cap);  // sorted position -> e
   uint16_t* inv = ord + cap;                         // staging index -> e
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    mbar_expect_tx(bar, 2 * bytes_i + D * bytes_x);
-    bulk_g2s(id_raw, src.id + lo_i, bytes_i, bar);
-    bulk_g2s(key_raw, src.key + lo_i, bytes_i, bar);
-#pragma unroll
-    for (int c = 0; c < D; ++c) bulk_g2s(xr[c], src.x[c] + lo_x, bytes_x, bar);
-  }
+  load_bucket<T, D>(src, sb, n, id_l, key_l, xr, xst, bar);
   __syncthreads();
   mbar_wait(bar, 0);
-  const uint32_t* id_l = id_raw + oi;
-  const uint32_t* key_l = key_raw + oi;
-  const SX<T> xs{xr[0] + ox, (uint32_t)(xst / sizeof(T))};
+  const SX<T> xs{xr, xst};
 
   // 1. carried keys; counting sort by SB sub-digit bits; 32-bit (key, id) composites
   const uint32_t shsb = 32u - P.B - P.SB;
   const uint32_t lowmask = (P.lowbits >= 32u) ? 0xffffffffu : ((1u << P.lowbits) - 1u);
   for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
-    const uint32_t id = id_l[e];
     const uint32_t key = key_l[e];
     const uint32_t sd = (key >> shsb) & (nsb - 1u);
-    ta[e] = ((key & lowmask) << P.idbits) | id;
+    ta[e] = ((key & lowmask) << P.idbits) | id_l[e];
     tb[e] = (sd << 16) | atomicAdd(&cnt[sd], 1u);
   }
   __syncthreads();
@@ -880,18 +937,17 @@ static __global__ void __launch_bounds__(BLOCK) bucket_fused_kernel(DevParams P,
   __syncthreads();
   if (P.dbg_order)
     for (uint32_t q = threadIdx.x; q < n; q += BLOCK) P.dbg_order[s0 + q] = id_l[ord[q]];
-  // straddling members: unchanged, to their sorted positions in src (own range)
+  // straddling members: unchanged, to their sorted places in the own gapped range
   for (uint32_t q = threadIdx.x; q < n; q += BLOCK) {
     if (q < head || q >= tail) {
       const uint32_t e = ord[q];
       tb[e] = 0xffffffffu;
-      src.id[s0 + q] = id_l[e];
+      src.id[sb + q] = id_l[e];
 #pragma unroll
-      for (int c = 0; c < D; ++c) src.x[c][s0 + q] = xs.at(c, e);
+      for (int c = 0; c < D; ++c) src.x[c][sb + q] = xs.at(c, e);
     }
   }
-  // 4. Eq. (2.2) + update: one lane group (G = pow2 >= p lanes) per batch,
-  //    members exchanged by warp shuffles, results written in place
+  // 4. Eq. (2.2) + update: one lane group per batch, shuffles, in place
   const uint32_t osh = 32u - P.b1;
   const uint32_t G = P.group;
   if (G != 0) {
@@ -960,42 +1016,23 @@ static __global__ void __launch_bounds__(BLOCK) bucket_fused_kernel(DevParams P,
   }
   // batches too large for a lane group (remainder batch, or p > 32): one thread each
   {
-    const uint32_t first_big = (G == 0) ? kfirst : ((klast > kfirst && batch_end(klast - 1, P) - (klast - 1) * P.p > G) ? klast - 1 : klast);
+    const uint32_t first_big =
+        (G == 0) ? kfirst
+                 : ((klast > kfirst && batch_end(klast - 1, P) - (klast - 1) * P.p > G) ? klast - 1
+                                                                                         : klast);
     for (uint32_t k = first_big + threadIdx.x; k < klast; k += BLOCK)
       serial_batch<T, D, KK, INTEG>(P, m, k * P.p - s0, batch_end(k, P) - s0, ord, id_l, xs, ta,
                                     tb, cnt, osh);
   }
   __syncthreads();
-  // 5. reserve runs in the step-(m+1) buckets, stage by digit, coalesced write
-  const uint32_t nout = 1u << P.b1;
-  for (uint32_t i = threadIdx.x; i < nout; i += BLOCK) {
-    const uint32_t h = cnt[i];
-    off[i] = h;
-    gbase[i] = h ? atomicAdd(&cur_next[i * CUR1_STRIDE], h) : 0u;
-  }
-  __syncthreads();
-  const uint32_t total = block_excl_scan<BLOCK>(off, nout, wsum);
-  for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
-    const uint32_t t = tb[e];
-    if (t != 0xffffffffu) inv[off[t >> 16] + (t & 0xffffu)] = (uint16_t)e;
-  }
-  __syncthreads();
-  for (uint32_t j = threadIdx.x; j < total; j += BLOCK) {
-    const uint32_t e = inv[j];
-    const uint32_t dg = tb[e] >> 16;
-    const uint32_t g = gbase[dg] + (j - off[dg]);
-    dst.id[g] = id_l[e];
-    dst.key[g] = ta[e];
-#pragma unroll
-    for (int c = 0; c < D; ++c) dst.x[c][g] = xs.at(c, e);
-  }
+  fused_output<T, D, BLOCK>(P, dst, dcap, cur_next, n, id_l, ta, tb, xs, cnt, off, gbase, inv, wsum);
 }
 
 // ------------------------------------------- fused bucket step, p = 2 (lean)
-// Same contract as bucket_fused_kernel, specialised for pairs: items held in
-// registers through the sort phases (ITEMS per thread, cap <= BLOCK*ITEMS),
-// one thread per pair; K is odd with s(z) = s(-z), so the partner's force is
-// exactly -f (the same terms the oracle sums).
+// Same contract, specialised for pairs: items in registers through the sort
+// phases (ITEMS per thread, cap <= BLOCK*ITEMS), one thread per pair; K is odd
+// with s(z) = s(-z), so the partner's force is exactly -f (the same terms the
+// oracle sums).
 template <typename T, int D> __host__ __device__ constexpr size_t pair_smem_bytes(uint32_t cap,
                                                                                  uint32_t SB) {
   return (size_t)(2 * (SB > 10 ? (1u << SB) : 1024u) + 1024 + 64) * 4 + 16  // cnt, off, gbase, wsum, mbar
@@ -1034,60 +1071,48 @@ __device__ __forceinline__ void pair_update(const DevParams& P, uint32_t m, cons
   }
 }
 
+
 template <typename T, int D, int KK, int INTEG, int BLOCK, int ITEMS>
 static __global__ void __launch_bounds__(BLOCK) bucket_pair_kernel(DevParams P, State<T, D> src,
-                                                                   State<T, D> dst,
+                                                                   uint32_t scap,
                                                                    const uint32_t* __restrict__ S,
+                                                                   State<T, D> dst, uint32_t dcap,
                                                                    uint32_t* __restrict__ cur_next) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t b = blockIdx.x;
-  const uint32_t s0 = S[b], n = S[b + 1] - s0;
+  const uint32_t s0 = S[b], n = S[b + 1] - s0, sb = b * scap;
   if (n == 0) return;
   const uint32_t nsb = 1u << P.SB;
   const uint32_t ncnt = nsb > 1024u ? nsb : 1024u;  // also holds the <= 1024 output digits
   uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw);
   uint32_t* off = cnt + ncnt;
-  uint32_t* gbase = off + nsb;
+  uint32_t* gbase = off + ncnt;
   uint32_t* wsum = gbase + 1024;
   uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);
   const uint32_t cap = P.cap;
   const uint32_t m = (uint32_t)*P.step;
-  if (n > cap) {  // shared with the general kernel (needs nsb >= 256 entries of cnt/off)
-    fused_big_path<T, D, KK, INTEG, BLOCK>(P, src, dst, cur_next, s0, n, m, cnt, off, wsum);
+  for (uint32_t i = threadIdx.x; i < nsb; i += BLOCK) cnt[i] = 0;
+  if (n > cap) {
+    fused_big_path<T, D, KK, INTEG, BLOCK>(P, src, dst, cur_next, s0, sb, n, m, dcap, cnt, off, wsum);
     return;
   }
-  constexpr uint32_t AX = 16 / sizeof(T);
-  const uint32_t lo_i = s0 & ~3u, oi = s0 - lo_i;
-  const uint32_t lo_x = s0 & ~(AX - 1), ox = s0 - lo_x;
-  const uint32_t bytes_i = ((oi + n + 3) & ~3u) * 4;
-  const uint32_t bytes_x = ((ox + n + AX - 1) & ~(AX - 1)) * (uint32_t)sizeof(T);
   unsigned char* p = reinterpret_cast<unsigned char*>(bar + 2);
-  uint32_t* id_raw = reinterpret_cast<uint32_t*>(p);
+  uint32_t* id_l = reinterpret_cast<uint32_t*>(p);
   p += (size_t)(cap + 8) * 4;
-  uint32_t* key_raw = reinterpret_cast<uint32_t*>(p);
+  uint32_t* key_l = reinterpret_cast<uint32_t*>(p);  // key_m by e; then key_{m+1} by e
   p += (size_t)(cap + 8) * 4;
   const uint32_t xst = (uint32_t)((((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15) / sizeof(T));
   T* xr = reinterpret_cast<T*>(p);
   p += (size_t)D * xst * sizeof(T);
   uint32_t* ks = reinterpret_cast<uint32_t*>(p);   // composites; then digit<<16|slot by e
   uint32_t* tb = ks;
-  uint32_t* ta = key_raw + oi;                      // key_m by e; then key_{m+1} by e
+  uint32_t* ta = key_l;
   uint16_t* ord = reinterpret_cast<uint16_t*>(ks + cap);
   uint16_t* inv = ord + cap;
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    mbar_expect_tx(bar, 2 * bytes_i + D * bytes_x);
-    bulk_g2s(id_raw, src.id + lo_i, bytes_i, bar);
-    bulk_g2s(key_raw, src.key + lo_i, bytes_i, bar);
-#pragma unroll
-    for (int c = 0; c < D; ++c) bulk_g2s(xr + (size_t)c * xst, src.x[c] + lo_x, bytes_x, bar);
-  }
-  for (uint32_t i = threadIdx.x; i < nsb; i += BLOCK) cnt[i] = 0;
+  load_bucket<T, D>(src, sb, n, id_l, key_l, xr, xst, bar);
   __syncthreads();
   mbar_wait(bar, 0);
-  const uint32_t* id_l = id_raw + oi;
-  const uint32_t* key_l = key_raw + oi;
-  const SX<T> xs{xr + ox, xst};
+  const SX<T> xs{xr, xst};
 
   // 1-3. exact (key, id) sort: counting sort on SB sub-digit bits + rank in sub-bucket
   const uint32_t shsb = 32u - P.B - P.SB;
@@ -1137,19 +1162,19 @@ static __global__ void __launch_bounds__(BLOCK) bucket_pair_kernel(DevParams P, 
   const uint32_t N = (uint32_t)P.n;
   const uint32_t pend = (N & 1u) ? N - 3u : N;
   const uint32_t head = s0 & 1u;                         // local index of the first pair
-  const uint32_t lim = min(s0 + n, pend) - s0;           // pairs must end at <= lim
+  const uint32_t lim = (min(s0 + n, pend) > s0) ? min(s0 + n, pend) - s0 : 0u;
   const uint32_t npairs = (lim > head) ? (lim - head) / 2 : 0u;
   const uint32_t covered = head + 2 * npairs;            // [head, covered) are interior
   const bool triple = (N & 1u) && (pend >= s0) && (N <= s0 + n);
   __syncthreads();
-  // straddlers: unchanged to their sorted positions in src (own range)
+  // straddlers: unchanged, to their sorted places in the own gapped range
   for (uint32_t q = threadIdx.x; q < n; q += BLOCK) {
     const bool in_triple = triple && (s0 + q >= pend);
     if ((q < head || q >= covered) && !in_triple) {
       const uint32_t e = ord[q];
-      src.id[s0 + q] = id_l[e];
+      src.id[sb + q] = id_l[e];
 #pragma unroll
-      for (int c = 0; c < D; ++c) src.x[c][s0 + q] = xs.at(c, e);
+      for (int c = 0; c < D; ++c) src.x[c][sb + q] = xs.at(c, e);
     }
   }
   // 4. one thread per pair
@@ -1180,33 +1205,7 @@ static __global__ void __launch_bounds__(BLOCK) bucket_pair_kernel(DevParams P, 
   if (triple && threadIdx.x == 0)  // the remainder batch of size 3 (N odd), EM only
     serial_batch<T, D, KK, INTEG>(P, m, pend - s0, n, ord, id_l, xs, ta, tb, cnt, osh);
   __syncthreads();
-  // 5. reserve runs in the step-(m+1) buckets, stage by digit, coalesced write
-  const uint32_t nout = 1u << P.b1;
-  for (uint32_t i = threadIdx.x; i < nout; i += BLOCK) {
-    const uint32_t h = cnt[i];
-    off[i] = h;
-    gbase[i] = h ? atomicAdd(&cur_next[i * CUR1_STRIDE], h) : 0u;
-  }
-  __syncthreads();
-  const uint32_t total = block_excl_scan<BLOCK>(off, nout, wsum);
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    const uint32_t e = k * BLOCK + threadIdx.x;
-    if (e < n) {
-      const uint32_t t = tb[e];
-      if (t != 0xffffffffu) inv[off[t >> 16] + (t & 0xffffu)] = (uint16_t)e;
-    }
-  }
-  __syncthreads();
-  for (uint32_t j = threadIdx.x; j < total; j += BLOCK) {
-    const uint32_t e = inv[j];
-    const uint32_t dg = tb[e] >> 16;
-    const uint32_t g = gbase[dg] + (j - off[dg]);
-    dst.id[g] = id_l[e];
-    dst.key[g] = ta[e];
-#pragma unroll
-    for (int c = 0; c < D; ++c) dst.x[c][g] = xs.at(c, e);
-  }
+  fused_output<T, D, BLOCK>(P, dst, dcap, cur_next, n, id_l, ta, tb, xs, cnt, off, gbase, inv, wsum);
 }
 
 // ------------------------------------------------------------------ RBM-r
