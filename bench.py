@@ -77,12 +77,14 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def kernel_bytes(name: str, cfg: dict) -> float:
-    """Algorithmic HBM bytes per launch: what the
-    kernel must move at minimum -- R = 4 + d*s bytes per particle record."""
-    n, R = cfg["n"], 4 + cfg["d"] * elt(cfg)
-    return {"scatter_top": 2.0 * R * n, "scatter_sub": 2.0 * R * n, "bucket_step": 2.0 * R * n,
-            "hist_sub": 4.0 * n, "hist_top": 0.0}.get(name, 0.0)
+def kernel_bytes(name: str, cfg: dict, prefix_bits: int) -> float:
+    """Algorithmic HBM bytes per launch: the records the
+    kernel must read and write once in this design.  Records carry id, the
+    shuffle key and d coordinates (R' = 8 + d*s) on the gapped-bucket path;
+    the single-bucket path (prefix_bits == 0) moves id + x (R = 4 + d*s)."""
+    n = cfg["n"]
+    R = (8 if prefix_bits > 0 else 4) + cfg["d"] * elt(cfg)
+    return {"scatter_sub": 2.0 * R * n, "bucket_step": 2.0 * R * n}.get(name, 0.0)
 
 
 class Clocks:
@@ -245,7 +247,7 @@ def main():
     name = max(per_kernel, key=per_kernel.get)
     avg_ms = per_kernel[name] / max(nrec, 1)
     peak, peak_kind = peaks()
-    nbytes = kernel_bytes(name, cfg)
+    nbytes = kernel_bytes(name, cfg, s.layout[0])
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -303,6 +305,7 @@ def main():
             "config": config_dict(args, cfg, world),
             "hbm": {"useful_gbs_per_gpu": useful, "record_bytes": R,
                     "note": "useful = particle-steps/s x 2 d s (state read+write once)"},
+            "layout": {"prefix_bits": s.layout[0], "passes": s.layout[1], "bucket_cap": s.layout[2]},
             "roofline": roof, "kernel_ms_per_step": shares, "clocks": clocks,
             "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu}
     if rank == 0:

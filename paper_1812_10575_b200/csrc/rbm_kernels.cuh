@@ -794,12 +794,13 @@ __device__ __forceinline__ void load_bucket(State<T, D> src, uint32_t sb, uint32
     const uint32_t bytes_i = ((n + 3) & ~3u) * 4;
     constexpr uint32_t AX = 16 / sizeof(T);
     const uint32_t bytes_x = ((n + AX - 1) & ~(AX - 1)) * (uint32_t)sizeof(T);
+    const uint64_t pol = l2_evict_first_policy();
     mbar_init(bar, 1);
     mbar_expect_tx(bar, 2 * bytes_i + D * bytes_x);
-    bulk_g2s(id_s, src.id + sb, bytes_i, bar);
-    bulk_g2s(key_s, src.key + sb, bytes_i, bar);
+    bulk_g2s_stream(id_s, src.id + sb, bytes_i, bar, pol);
+    bulk_g2s_stream(key_s, src.key + sb, bytes_i, bar, pol);
 #pragma unroll
-    for (int c = 0; c < D; ++c) bulk_g2s(x_s + (size_t)c * xst, src.x[c] + sb, bytes_x, bar);
+    for (int c = 0; c < D; ++c) bulk_g2s_stream(x_s + (size_t)c * xst, src.x[c] + sb, bytes_x, bar, pol);
   }
 }
 
