@@ -123,8 +123,8 @@ typedef struct {
   uint64_t seed;         /* Philox key (seed_lo, seed_hi) */
   uint64_t step0;        /* index m of the first step (checkpoint resume) */
   uint32_t replica;      /* ensemble member, enters Philox counter word 3 (< 2^24) */
-  int32_t world_size;    /* 1 (multi-process partition mode: RBM_ERR_UNSUPPORTED) */
-  int32_t rank;          /* 0 */
+  int32_t world_size;    /* 1, or G = 2..64 (power of two): partitioned single system, see rbm_part_* */
+  int32_t rank;          /* 0..G-1: this process's rank (one GPU per rank) */
   uint32_t debug_bucket_cap; /* 0 = automatic; >0 forces the per-bucket smem capacity (tests) */
 } rbm_config;
 
@@ -199,6 +199,73 @@ const char* rbm_kernel_name(const rbm_ctx* ctx, uint32_t i);
  * the number of steps recorded. */
 rbm_status rbm_timing_begin(rbm_ctx* ctx, uint32_t max_steps);
 rbm_status rbm_timing_end(rbm_ctx* ctx, double* ms_per_kernel, uint32_t* steps_recorded);
+
+/* ------------------------------------------------------------------------
+ * Partitioned single system (world_size G > 1).
+ * One global system of N particles is split over G ranks (one GPU each) by
+ * key range: rank r holds, at step m, exactly the particles whose shuffle key
+ * key_m has top log2(G) bits equal to r.  Because the division is the (key,
+ * id) order (reading D:6), rank r's particles are the global
+ * sorted positions [O_r, O_r + n_r), O_r = n_0 + ... + n_{r-1}; every batch
+ * lies in one rank except the one crossing O_r, which rank r completes with
+ * t_r = O_r - (start of that batch) <= p-1 records of rank r-1 (the "halo").
+ * The result is bit-identical to the same config on one GPU (world_size 1).
+ *
+ * The library runs every computation; the caller performs the three
+ * exchanges between the phases (plumbing: torch.distributed over NCCL on
+ * NVLink in bench.py / paper_1812_10575_b200.partition), using byte offsets
+ * into the caller-owned workspace from rbm_part_info_get():
+ *   H  halo:     rank r's halo_send (halo_bytes) -> rank r+1's halo_recv
+ *   C  counts:   all-gather of every rank's counts_send (nseg u32) into
+ *                counts_all (world_size * nseg u32, rank-major)
+ *   R  records:  for each of the narrays exchanged arrays a, an all-to-all
+ *                with equal chunks of chunk_elems elements of elem_bytes[a]:
+ *                chunk j of send_off[a] (to rank j) -> chunk r of rank j's
+ *                recv_off[a]
+ * Protocol: rbm_init; rbm_part_prologue; C; R; then per step
+ *   rbm_part_phase1; H; rbm_part_phase2; C; R.
+ * rbm_step / rbm_run return RBM_ERR_STATE on a partitioned context.
+ * rbm_init draws (or rbm_set_state takes, n0 rows) the particles with ids
+ * [id0, id0 + n0) = [floor(N r/G), floor(N (r+1)/G)); rbm_gather writes, into
+ * a DEVICE buffer, the positions of the ids in the range that this rank holds
+ * and leaves the other rows untouched (host output: RBM_ERR_UNSUPPORTED).
+ * A rank that ends up with fewer than p particles (probability ~0 at the
+ * required n/G >= max(1024, 16p)) is reported as RBM_ERR_CAPACITY.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  uint64_t ws_bytes;        /* workspace bytes (= rbm_workspace_size) */
+  uint32_t world_size, rank;
+  uint32_t nseg;            /* pass-1 buckets 2^b1: u32 counts per rank in exchange C */
+  uint32_t narrays;         /* exchanged arrays: 2 + d (id u32, key u32, x_0 .. x_{d-1} dtype) */
+  uint64_t chunk_elems;     /* elements per destination rank in each exchanged array */
+  uint64_t send_off[5];     /* byte offsets in ws of the exchanged send arrays (a < narrays) */
+  uint64_t recv_off[5];     /* byte offsets in ws of the exchanged receive arrays */
+  uint32_t elem_bytes[5];   /* element size of array a */
+  uint64_t counts_send_off; /* nseg u32 */
+  uint64_t counts_all_off;  /* world_size * nseg u32, rank-major */
+  uint64_t halo_send_off, halo_recv_off, halo_bytes;
+  uint64_t id0, n0;         /* this rank's initial ids [id0, id0 + n0) */
+} rbm_part_info;
+
+/* Exchange layout for cfg (host-only computation, no device work; same
+ * validation as rbm_init).  RBM_ERR_STATE if cfg->world_size == 1. */
+rbm_status rbm_part_info_get(const rbm_config* cfg, rbm_part_info* out);
+
+/* Enqueue the partition of the initial state (id order) into the send
+ * buckets; follow with exchanges C and R.  Once per context. */
+rbm_status rbm_part_prologue(rbm_ctx* ctx);
+
+/* Enqueue the first part of step m (needs C and R done): global offsets from
+ * counts_all, split of the received segments into final buckets, the fused
+ * bucket step (sort by (key_m, id), Eq. 2.2 + update of every batch inside
+ * this rank, partition of the updated records by key_{m+1}), halo_send.
+ * Follow with exchange H. */
+rbm_status rbm_part_phase1(rbm_ctx* ctx);
+
+/* Enqueue the rest of step m: the batches straddling final buckets and the
+ * one crossing O_r (with halo_recv), counts_send; m advances.  Follow with
+ * exchanges C and R. */
+rbm_status rbm_part_phase2(rbm_ctx* ctx);
 
 /* Message for the last failure on ctx (or on this thread if ctx == NULL). */
 const char* rbm_last_error(const rbm_ctx* ctx);

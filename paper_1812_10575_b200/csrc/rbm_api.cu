@@ -24,6 +24,7 @@ rbm_status check_flags(rbm_ctx* c) {
   uint32_t cap = 0;
   CU(cudaMemcpy(&nf, c->nonfinite, sizeof nf, cudaMemcpyDeviceToHost));
   CU(cudaMemcpy(&cap, c->capacity_err, sizeof cap, cudaMemcpyDeviceToHost));
+  if (cap == 2) return fail(c, RBM_ERR_CAPACITY, "a rank of the partitioned system held fewer than p particles; results are invalid");
   if (cap) return fail(c, RBM_ERR_CAPACITY, "a bucket exceeded every capacity fallback; results of that step are invalid");
   if (nf != ~0ull)
     return fail(c, RBM_ERR_NONFINITE, "non-finite position at step %llu, particle id %llu",
@@ -97,6 +98,8 @@ rbm_status init_impl(rbm_ctx* c, const rbm_config* cfg, void* wsp, size_t ws_byt
   P.group = 0;
   if (cfg->p <= 32) { P.group = 1; while (P.group < cfg->p) P.group <<= 1; }
   P.big_scratch = c->big_scratch;
+  P.nb1_loc_mask = ((1u << c->L.b1) >> c->L.g) - 1u;
+  P.halo = (is_partitioned(*cfg) && cfg->rank > 0) ? 1u : 0u;
   rbm_status s = c->eng->setup(*c);
   if (s) return s;
   CU(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
@@ -109,6 +112,7 @@ rbm_status init_impl(rbm_ctx* c, const rbm_config* cfg, void* wsp, size_t ws_byt
   const uint32_t s0[2] = {0u, (uint32_t)cfg->n};
   if (c->L.B == 0) CU(cudaMemcpyAsync(c->S, s0, 8, cudaMemcpyHostToDevice, st));
   CU(cudaMemsetAsync(c->big_claim, 0, NBIG * 4, st));
+  if (c->halo_recv) CU(cudaMemsetAsync(c->halo_recv, 0, 16, st));  // rank 0 never receives one
   if (cfg->init != RBM_INIT_USER) c->eng->init_state(*c, st);
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(st));  // the host-side sources above live on this stack frame
@@ -124,7 +128,8 @@ rbm_status rbm_init(const rbm_config* cfg, void* wsp, size_t ws_bytes, void* cud
   if (s) return s;
   if (!out) return fail(nullptr, RBM_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
-  if (nccl_unique_id) return fail(nullptr, RBM_ERR_UNSUPPORTED, "nccl_unique_id must be NULL (world_size 1)");
+  if (nccl_unique_id)
+    return fail(nullptr, RBM_ERR_UNSUPPORTED, "nccl_unique_id must be NULL: the partition exchanges are the caller's (torch.distributed over NCCL)");
   size_t need = 0;
   rbm_workspace_size(cfg, &need);
   if (!wsp || ws_bytes < need || (reinterpret_cast<uintptr_t>(wsp) & 255))
@@ -146,7 +151,7 @@ rbm_status rbm_init(const rbm_config* cfg, void* wsp, size_t ws_bytes, void* cud
 rbm_status rbm_set_state(rbm_ctx* c, const void* x, uint32_t where) {
   if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
   if (!x) return fail(c, RBM_ERR_INVALID_ARG, "x is NULL");
-  const size_t bytes = c->cfg.n * c->cfg.d * elt_size(c->cfg);
+  const size_t bytes = c->n0 * c->cfg.d * elt_size(c->cfg);  // this rank's ids (all N on one GPU)
   if (where == RBM_MEM_HOST) {
     void* scratch = c->xbuf[c->cur ^ 1];  // inactive buffer as staging
     CU(cudaMemcpyAsync(scratch, x, bytes, cudaMemcpyHostToDevice, c->stream));
@@ -162,8 +167,15 @@ rbm_status rbm_set_state(rbm_ctx* c, const void* x, uint32_t where) {
   return RBM_OK;
 }
 
+static rbm_status not_partitioned(rbm_ctx* c) {
+  if (is_partitioned(c->cfg))
+    return fail(c, RBM_ERR_STATE, "partitioned context (world_size %d): step with rbm_part_phase1/2 and the exchanges", c->cfg.world_size);
+  return RBM_OK;
+}
+
 rbm_status rbm_step(rbm_ctx* c) {
   if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
+  if (rbm_status e = not_partitioned(c)) return e;
   rbm_status s = enqueue_steps(c, c->stream, 1);
   c->P.dbg_order = nullptr;
   if (s) return s;
@@ -173,12 +185,23 @@ rbm_status rbm_step(rbm_ctx* c) {
 
 rbm_status rbm_run(rbm_ctx* c, uint64_t nsteps) {
   if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
+  if (rbm_status e = not_partitioned(c)) return e;
   if (c->step + nsteps >= (1ull << 32)) return fail(c, RBM_ERR_INVALID_ARG, "step index would exceed 2^32");
   // steps per graph: even when a step flips the ping-pong buffers
   c->P.dbg_order = nullptr;  // the permutation hook applies to rbm_step only
   const uint32_t per = 8;  // even: every layout returns to the same (cur, parity)
   c->graph_steps = per;
   uint64_t done = 0;
+  if (c->cfg.scheme == RBM_SCHEME_RBM1 && c->L.B == 0) {  // resident: chunks of <= 4096 steps per launch
+    while (nsteps > 0) {
+      const uint32_t k = (uint32_t)std::min<uint64_t>(nsteps, 4096);
+      c->eng->run_resident(*c, c->stream, k);
+      CU(cudaGetLastError());
+      c->step += k;
+      nsteps -= k;
+    }
+    return RBM_OK;
+  }
   if (c->cfg.scheme == RBM_SCHEME_RBM1 && c->L.B > 0 && !c->partitioned && nsteps > 0) {
     rbm_status s0 = enqueue_steps(c, c->stream, 1);  // prologue step outside the graph
     if (s0) return s0;
@@ -217,6 +240,8 @@ rbm_status rbm_gather(rbm_ctx* c, uint64_t id_begin, uint64_t id_end, void* x_ou
   if (!x_out) return fail(c, RBM_ERR_INVALID_ARG, "x_out is NULL");
   if (id_begin > id_end || id_end > c->cfg.n) return fail(c, RBM_ERR_INVALID_ARG, "bad id range [%llu,%llu)", (unsigned long long)id_begin, (unsigned long long)id_end);
   const size_t bytes = (id_end - id_begin) * c->cfg.d * elt_size(c->cfg);
+  if (where == RBM_MEM_HOST && is_partitioned(c->cfg))
+    return fail(c, RBM_ERR_UNSUPPORTED, "partitioned context: gather to device memory (each rank writes the ids it holds), then combine across ranks");
   if (where == RBM_MEM_HOST) {
     void* scratch = c->xbuf[c->cur ^ 1];
     c->eng->gather(*c, id_begin, id_end, scratch, c->stream);
@@ -316,6 +341,68 @@ rbm_status rbm_debug_philox(const uint32_t* in, uint32_t* out, uint64_t count, v
   CU(cudaGetLastError());
   return RBM_OK;
 }
+
+// ------------------------------------------------ partitioned single system
+rbm_status rbm_part_info_get(const rbm_config* cfg, rbm_part_info* out) {
+  rbm_status s = validate(cfg);
+  if (s) return s;
+  if (!out) return fail(nullptr, RBM_ERR_INVALID_ARG, "out is NULL");
+  if (!is_partitioned(*cfg)) return fail(nullptr, RBM_ERR_STATE, "world_size 1: no partition exchange");
+  rbm_ctx tmp;
+  tmp.cfg = *cfg;
+  tmp.L = choose_layout(*cfg);
+  Workspace ws;
+  unsigned char* const base = reinterpret_cast<unsigned char*>(uintptr_t(1) << 44);  // sentinel
+  ws.base = base;
+  ws.dry = true;
+  carve(tmp, ws);
+  auto off = [&](const void* p) { return (uint64_t)(reinterpret_cast<const unsigned char*>(p) - base); };
+  std::memset(out, 0, sizeof *out);
+  out->ws_bytes = ws.used;
+  out->world_size = (uint32_t)cfg->world_size;
+  out->rank = (uint32_t)cfg->rank;
+  out->nseg = 1u << tmp.L.b1;
+  out->narrays = 2 + cfg->d;
+  out->chunk_elems = (uint64_t)((1u << tmp.L.b1) >> tmp.L.g) * tmp.L.cap1;
+  const uint32_t es = (uint32_t)elt_size(*cfg);
+  for (int b = 1; b <= 2; ++b) {
+    uint64_t* o = b == 1 ? out->send_off : out->recv_off;
+    o[0] = off(tmp.idbuf[b]);
+    o[1] = off(tmp.keybuf[b]);
+    for (uint32_t k = 0; k < cfg->d; ++k) o[2 + k] = off(tmp.xbuf[b]) + (uint64_t)k * tmp.xstride * es;
+  }
+  out->elem_bytes[0] = out->elem_bytes[1] = 4;
+  for (uint32_t k = 0; k < cfg->d; ++k) out->elem_bytes[2 + k] = es;
+  out->counts_send_off = off(tmp.counts_send);
+  out->counts_all_off = off(tmp.counts_all);
+  out->halo_send_off = off(tmp.halo_send);
+  out->halo_recv_off = off(tmp.halo_recv);
+  out->halo_bytes = cfg->dtype == RBM_F64 ? (cfg->d == 3 ? halo_bytes<double, 3>() : cfg->d == 2 ? halo_bytes<double, 2>() : halo_bytes<double, 1>())
+                                          : (cfg->d == 3 ? halo_bytes<float, 3>() : cfg->d == 2 ? halo_bytes<float, 2>() : halo_bytes<float, 1>());
+  out->id0 = tmp.id0;
+  out->n0 = tmp.n0;
+  return RBM_OK;
+}
+
+static rbm_status part_call(rbm_ctx* c, int phase) {
+  if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
+  if (!is_partitioned(c->cfg)) return fail(c, RBM_ERR_STATE, "not a partitioned context (world_size 1)");
+  if (phase == 0 && c->partitioned) return fail(c, RBM_ERR_STATE, "prologue already done (state is partitioned)");
+  if (phase > 0 && !c->partitioned) return fail(c, RBM_ERR_STATE, "run rbm_part_prologue and its exchange first");
+  if (phase == 0) c->eng->part_prologue(*c, c->stream);
+  else if (phase == 1) c->eng->part_phase1(*c, c->stream);
+  else {
+    c->eng->part_phase2(*c, c->stream);
+    c->P.dbg_order = nullptr;  // the permutation hook covers one step (phase1 + phase2)
+    ++c->step;
+  }
+  CU(cudaGetLastError());
+  return RBM_OK;
+}
+
+rbm_status rbm_part_prologue(rbm_ctx* c) { return part_call(c, 0); }
+rbm_status rbm_part_phase1(rbm_ctx* c) { return part_call(c, 1); }
+rbm_status rbm_part_phase2(rbm_ctx* c) { return part_call(c, 2); }
 
 const char* rbm_last_error(const rbm_ctx* c) { return c ? c->err.c_str() : g_err.c_str(); }
 

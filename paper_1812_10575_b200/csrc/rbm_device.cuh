@@ -62,6 +62,13 @@ struct DevParams {
   uint32_t lowbits;    // key bits below prefix+sub-digit: 32 - B - SB (lowbits+idbits <= 32)
   uint32_t* dbg_order; // if set: sorted position -> id of this step (test hook)
   uint32_t group;      // lanes per batch in the fused step: pow2 >= p (<= 32), 0 = one thread per batch
+  // partitioned single system (world_size G > 1): this rank
+  // owns the key range whose top log2 G bits equal its rank.  The 2^b1 pass-1
+  // buckets are global; a rank holds 2^b1/G of them (nb1_loc_mask = that - 1;
+  // 2^b1 - 1 on one GPU).  `halo`: the batch crossing the rank's first
+  // position is completed with records of rank-1 placed at bucket "-1".
+  uint32_t nb1_loc_mask;
+  uint32_t halo;
   const uint64_t* step;     // device step counter m
   unsigned long long* nonfinite;  // atomicMin of (m<<32 | id); ~0 if clean
   uint32_t* capacity_err;         // set to 1 if a bucket overflowed every fallback

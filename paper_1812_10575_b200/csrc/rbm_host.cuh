@@ -27,6 +27,7 @@ extern thread_local std::string g_err;  // failures without a context
 struct Workspace {
   unsigned char* base = nullptr;
   size_t size = 0, used = 0;
+  bool dry = false;  // offsets only: base is a sentinel address, never dereferenced
   template <typename U>
   U* take(size_t count) {
     used = (used + 255) & ~size_t(255);
@@ -37,9 +38,10 @@ struct Workspace {
 };
 
 struct Layout {
-  uint32_t B = 0, b1 = 0, b2 = 0, nbuckets = 1, cap = 0;
+  uint32_t g = 0;        // log2 world_size (partitioned single system; 0 on one GPU)
+  uint32_t B = 0, b1 = 0, b2 = 0, nbuckets = 1, cap = 0;  // nbuckets: final buckets of this rank
   uint32_t SB = 8, idbits = 1, lowbits = 0;
-  uint32_t cap1 = 0;     // gapped capacity of a pass-1 bucket (2-pass layouts)
+  uint32_t cap1 = 0;     // gapped capacity of a pass-1 bucket (2-pass layouts; per source rank when partitioned)
   uint32_t cap2 = 0;     // gapped capacity of a final bucket
   uint64_t slots = 0;    // elements per state buffer: max(N, 2^b1 cap1, 2^B cap2)
 };
@@ -61,10 +63,15 @@ struct rbm_ctx {
   int device = 0;
   std::unique_ptr<EngineBase> eng;
   // workspace carve
-  void* xbuf[2] = {nullptr, nullptr};
+  void* xbuf[3] = {nullptr, nullptr, nullptr};
   uint64_t xstride = 0;  // elements between coordinate arrays of one state buffer
-  uint32_t* idbuf[2] = {nullptr, nullptr};
-  uint32_t* keybuf[2] = {nullptr, nullptr};  // carried shuffle keys (fused pipeline)
+  uint32_t* idbuf[3] = {nullptr, nullptr, nullptr};
+  uint32_t* keybuf[3] = {nullptr, nullptr, nullptr};  // carried shuffle keys (fused pipeline)
+  // partitioned single system (world_size > 1): buffer 0 = this rank's final
+  // buckets A (bucket -1 = halo), 1 = send pass-1 buckets B, 2 = received C
+  uint64_t id0 = 0, n0 = 0;  // initial id range of this rank
+  uint32_t *counts_send = nullptr, *counts_all = nullptr;
+  unsigned char *halo_send = nullptr, *halo_recv = nullptr;
   // gapped-bucket pipeline.  cur1[q]: counts (cursors) of the buckets the
   // state of step m (q = m & 1) is partitioned into -- pass-1 buckets (2-pass)
   // or final buckets (1-pass); the fused step fills cur1[q ^ 1] for step m+1.
@@ -126,12 +133,24 @@ inline uint32_t ceil_log2(double v) {
 
 inline size_t elt_size(const rbm_config& c) { return c.dtype == RBM_F64 ? 8 : 4; }
 
+inline bool is_partitioned(const rbm_config& c) { return c.world_size > 1; }
+
+// this rank's initial id range [id0, id0 + n0) (partitioned: floor(N r / G) ..)
+inline void initial_ids(const rbm_config& c, uint64_t& id0, uint64_t& n0) {
+  if (!is_partitioned(c)) { id0 = 0; n0 = c.n; return; }
+  const uint64_t G = (uint64_t)c.world_size, r = (uint64_t)c.rank;
+  id0 = c.n * r / G;
+  n0 = c.n * (r + 1) / G - id0;
+}
+
 inline Layout choose_layout(const rbm_config& c) {
   Layout L;
   const uint64_t n = c.n;
+  const bool part = is_partitioned(c);
   L.idbits = ceil_log2((double)n);
   if (L.idbits < 1) L.idbits = 1;
-  if (n <= 2048) {
+  if (part) L.g = ceil_log2((double)c.world_size);
+  if (n <= 2048 && !part) {
     L.B = 0;  // one bucket: sorted-output kernel
   } else {
     // target mean bucket size (tuning knob RBM_BUCKET_TARGET, default 2048)
@@ -140,18 +159,21 @@ inline Layout choose_layout(const rbm_config& c) {
     if (!(target >= 64.0 && target <= 2048.0)) target = 2048.0;
     L.B = ceil_log2((double)n / target);
     if (L.B < 2) L.B = 2;
-    if (L.B > 18) L.B = 18;
+    if (part && L.B < L.g + 2) L.B = L.g + 2;  // >= 4 final buckets per rank, two passes
+    if (L.B > (part ? 20u : 18u)) L.B = part ? 20u : 18u;
   }
-  if (L.B <= 10) { L.b1 = L.B; L.b2 = 0; }
+  if (L.B <= 10 && !part) { L.b1 = L.B; L.b2 = 0; }
   else {
     L.b1 = L.B / 2;  // fused-output digit <= pass-2 digit: longer runs in the fused scatter
     if (const char* e = std::getenv("RBM_B1")) {  // tuning knob: pass-1 / fused-output digit bits
       const int v = std::atoi(e);
       if (v >= 5 && v <= 10 && L.B - v >= 5 && L.B - v <= 10) L.b1 = (uint32_t)v;
     }
+    if (part && L.b1 < L.g) L.b1 = L.g;  // the pass-1 digit carries the destination rank
+    if (L.b1 > 10) L.b1 = 10;
     L.b2 = L.B - L.b1;
   }
-  L.nbuckets = 1u << L.B;
+  L.nbuckets = 1u << (L.B - L.g);
   L.SB = L.idbits > L.B + 8 ? L.idbits - L.B : 8;  // 32-bit composites: lowbits + idbits <= 32
   L.lowbits = 32 - L.B - L.SB;
   if (L.B == 0) {
@@ -172,7 +194,16 @@ inline Layout choose_layout(const rbm_config& c) {
     return (uint32_t)((v + 63) & ~63ull);
   };
   L.slots = n;
-  if (L.B > 0) {
+  if (part) {
+    // three buffers (final buckets A with a leading halo bucket, send B,
+    // receive C); pass-1 segments hold one source rank's share
+    uint64_t id0, n0;
+    initial_ids(c, id0, n0);
+    L.cap2 = gcap((double)n / (1u << L.B), L.cap + 64);
+    L.cap1 = gcap((double)n / ((double)c.world_size * (1u << L.b1)), 64);
+    L.slots = std::max<uint64_t>(n0, (uint64_t)(L.nbuckets + 1) * L.cap2);
+    L.slots = std::max<uint64_t>(L.slots, (uint64_t)(1u << L.b1) * L.cap1);
+  } else if (L.B > 0) {
     L.cap2 = gcap((double)n / L.nbuckets, L.cap + 64);
     L.slots = std::max<uint64_t>(L.slots, (uint64_t)L.nbuckets * L.cap2);
     if (L.b2) {
@@ -226,13 +257,26 @@ inline rbm_status validate(const rbm_config* cfg) {
     return fail(c, RBM_ERR_INVALID_ARG, "mixture needs 1 <= K <= 64");
   if (k.replica >= (1u << 24)) return fail(c, RBM_ERR_INVALID_ARG, "replica must be < 2^24");
   if (k.step0 + 1 >= (1ull << 32)) return fail(c, RBM_ERR_INVALID_ARG, "step0 must be < 2^32-1");
-  if (k.world_size != 1 || k.rank != 0)
-    return fail(c, RBM_ERR_UNSUPPORTED, "world_size=%d: multi-process partition mode is not in this build", k.world_size);
+  if (k.world_size < 1 || k.world_size > 64 || (k.world_size & (k.world_size - 1)))
+    return fail(c, RBM_ERR_INVALID_ARG, "world_size=%d must be a power of two in 1..64", k.world_size);
+  if (k.rank < 0 || k.rank >= k.world_size)
+    return fail(c, RBM_ERR_INVALID_ARG, "rank=%d not in [0, world_size=%d)", k.rank, k.world_size);
+  if (is_partitioned(k)) {
+    if (k.scheme != RBM_SCHEME_RBM1)
+      return fail(c, RBM_ERR_UNSUPPORTED, "partitioned single system: RBM-1 only in this build");
+    if (k.p > HALO_MAX)
+      return fail(c, RBM_ERR_INVALID_ARG, "partitioned single system needs p <= %u", HALO_MAX);
+    if (k.n / (uint64_t)k.world_size < 1024 || k.n / (uint64_t)k.world_size < 16ull * k.p)
+      return fail(c, RBM_ERR_INVALID_ARG, "partitioned single system needs n/world_size >= max(1024, 16 p)");
+  }
   const Layout L = choose_layout(k);
   if (k.scheme == RBM_SCHEME_RBM1 && L.B > 0 && L.SB > 12)
     return fail(c, RBM_ERR_UNSUPPORTED, "n=%llu needs %u sub-digit bits (> 12): n <= 2^30 per GPU", (unsigned long long)k.n, L.SB);
   if (k.scheme == RBM_SCHEME_RBM1 && L.B > 0 && L.cap > FUSED_CAP_MAX)
     return fail(c, RBM_ERR_INVALID_ARG, "debug_bucket_cap %u > %u", L.cap, FUSED_CAP_MAX);
+  if (k.scheme == RBM_SCHEME_RBM1 && L.B == 0 &&
+      (k.dtype == RBM_F64 ? resident_smem_bytes<double, 3>(L.cap) : resident_smem_bytes<float, 3>(L.cap)) > 227 * 1024)
+    return fail(c, RBM_ERR_INVALID_ARG, "n=%llu too large for the resident kernel", (unsigned long long)k.n);
   if (k.scheme == RBM_SCHEME_RBM1 && bucket_smem(k, L.cap) > 227 * 1024)
     return fail(c, RBM_ERR_INVALID_ARG, "bucket capacity %u needs %zu B of shared memory", L.cap, bucket_smem(k, L.cap));
   return RBM_OK;
@@ -244,8 +288,10 @@ inline void carve(rbm_ctx& c, Workspace& ws) {
   const size_t es = elt_size(k);
   const uint64_t n = k.n;
   const uint64_t slots = (k.scheme == RBM_SCHEME_RBM1) ? c.L.slots : n;
+  const bool part = is_partitioned(k);
+  initial_ids(k, c.id0, c.n0);
   c.xstride = (slots + 63) & ~63ull;  // per-coordinate stride: 256-B aligned SoA arrays (TMA)
-  for (int b = 0; b < 2; ++b) {
+  for (int b = 0; b < (part ? 3 : 2); ++b) {
     c.idbuf[b] = ws.take<uint32_t>(c.xstride);
     c.keybuf[b] = ws.take<uint32_t>(c.xstride);
     c.xbuf[b] = ws.take<unsigned char>(c.xstride * k.d * es);
@@ -253,7 +299,14 @@ inline void carve(rbm_ctx& c, Workspace& ws) {
   for (int q = 0; q < 2; ++q) c.cur1[q] = ws.take<uint32_t>(1024 * CUR1_STRIDE);
   c.prefix1 = ws.take<uint32_t>(1025);
   c.tile_off = ws.take<uint32_t>(1025);
-  c.S = ws.take<uint32_t>((size_t)c.L.nbuckets + 1);
+  c.S = ws.take<uint32_t>((size_t)c.L.nbuckets + 2);
+  if (c.S) c.S += 1;  // S[-1]: start of the halo bucket (partitioned)
+  if (part) {
+    c.counts_send = ws.take<uint32_t>(1024);
+    c.counts_all = ws.take<uint32_t>((size_t)k.world_size * 1024);
+    c.halo_send = ws.take<unsigned char>(halo_bytes<double, 3>());
+    c.halo_recv = ws.take<unsigned char>(halo_bytes<double, 3>());
+  }
   c.big_claim = ws.take<uint32_t>(NBIG);
   if (c.L.b2) c.cur2 = ws.take<uint32_t>((size_t)c.L.nbuckets * CUR2_STRIDE);
   c.step_dev = ws.take<uint64_t>(1);
@@ -288,6 +341,11 @@ struct EngineBase {
   virtual void set_state(rbm_ctx& c, const void* x, cudaStream_t s) = 0;
   virtual void step(rbm_ctx& c, cudaStream_t s) = 0;
   virtual void gather(rbm_ctx& c, uint64_t i0, uint64_t i1, void* out, cudaStream_t s) = 0;
+  // partitioned single system: the step split around its three exchanges
+  virtual void run_resident(rbm_ctx& c, cudaStream_t s, uint32_t nsteps) = 0;
+  virtual void part_prologue(rbm_ctx& c, cudaStream_t s) = 0;
+  virtual void part_phase1(rbm_ctx& c, cudaStream_t s) = 0;
+  virtual void part_phase2(rbm_ctx& c, cudaStream_t s) = 0;
 };
 
 template <typename T, int D, int KK, int INTEG>
@@ -307,13 +365,14 @@ struct Engine final : EngineBase {
     return s;
   }
 
-  size_t fu_smem = 0, pr_smem = 0;
+  size_t fu_smem = 0, pr_smem = 0, rs_smem = 0;
   bool use_pair = false;
 
   rbm_status setup(rbm_ctx& c) override {
     c.tile = SC_TILE;
     sc_smem = (1024 + 1024 + 64) * 4 + (size_t)SC_TILE * (8 + 2 + D * sizeof(T));
     bk_smem = bucket_smem(c.cfg, c.L.cap);
+    rs_smem = resident_smem_bytes<T, D>(c.L.cap);
     fu_smem = fused_smem_bytes<T, D>(c.L.cap, c.L.SB);
     pr_smem = pair_smem_bytes<T, D>(c.L.cap, c.L.SB);
     use_pair = c.cfg.p == 2 && c.L.B > 0 && c.L.cap <= (uint32_t)(PAIR_BLOCK * PAIR_ITEMS) &&
@@ -334,6 +393,11 @@ struct Engine final : EngineBase {
     if ((s = chk(cudaFuncSetAttribute(bucket_step_kernel<T, D, KK, INTEG, BK_BLOCK>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bk_smem),
                  "smem attr bucket"))) return s;
+    if (c.L.B == 0 && rs_smem <= 227 * 1024) {
+      if ((s = chk(cudaFuncSetAttribute(resident_kernel<T, D, KK, INTEG, BK_BLOCK>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem),
+                   "smem attr resident"))) return s;
+    }
     if (use_pair) {
       if ((s = chk(cudaFuncSetAttribute(bucket_pair_kernel<T, D, KK, INTEG, PAIR_BLOCK, PAIR_ITEMS>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pr_smem),
@@ -347,20 +411,42 @@ struct Engine final : EngineBase {
     return RBM_OK;
   }
 
+  // partitioned: this rank's final buckets, shifted so that bucket -1 (the
+  // halo) sits at physical slots [-cap2, 0)
+  State<T, D> stA(rbm_ctx& c) {
+    State<T, D> a = st(c, 0);
+    a.id += c.L.cap2;
+    a.key += c.L.cap2;
+    for (int k = 0; k < 3; ++k) a.x[k] += c.L.cap2;
+    return a;
+  }
+
   void init_state(rbm_ctx& c, cudaStream_t s) override {
     const rbm_config& k = c.cfg;
-    init_kernel<T, D><<<grid_for(k.n, 256), 256, 0, s>>>(c.P, st(c, c.cur), k.init, k.iparam[0],
-                                                         k.iparam[1], k.iparam[2], k.iparam[3]);
+    init_kernel<T, D><<<grid_for(c.n0, 256), 256, 0, s>>>(c.P, st(c, c.cur), c.id0, c.n0, k.init,
+                                                          k.iparam[0], k.iparam[1], k.iparam[2],
+                                                          k.iparam[3]);
     c.partitioned = false;
   }
 
   void set_state(rbm_ctx& c, const void* x, cudaStream_t s) override {
-    set_state_kernel<T, D><<<grid_for(c.cfg.n, 256), 256, 0, s>>>(c.cfg.n, st(c, c.cur),
-                                                                  reinterpret_cast<const T*>(x));
+    set_state_kernel<T, D><<<grid_for(c.n0, 256), 256, 0, s>>>(c.id0, c.n0, st(c, c.cur),
+                                                               reinterpret_cast<const T*>(x));
     c.partitioned = false;
   }
 
   void gather(rbm_ctx& c, uint64_t i0, uint64_t i1, void* out, cudaStream_t s) override {
+    if (is_partitioned(c.cfg)) {
+      if (c.partitioned) {
+        gather_part_kernel<T, D><<<grid_for((uint64_t)(1u << c.L.b1) * c.L.cap1, 256), 256, 0, s>>>(
+            c.P, st(c, 2), c.L.cap1, c.counts_all, (uint32_t)c.cfg.world_size, (uint32_t)c.cfg.rank,
+            i0, i1, reinterpret_cast<T*>(out));
+      } else {
+        gather_kernel<T, D><<<grid_for(c.n0, 256), 256, 0, s>>>(c.n0, st(c, 0), i0, i1,
+                                                                reinterpret_cast<T*>(out));
+      }
+      return;
+    }
     if (c.cfg.scheme == RBM_SCHEME_RBM1 && c.L.B > 0 && c.partitioned) {
       Gapped g;
       g.cap = c.L.b2 ? c.L.cap1 : c.L.cap2;
@@ -391,14 +477,8 @@ struct Engine final : EngineBase {
     const Layout& L = c.L;
     const uint64_t n = c.cfg.n;
     const int q = (int)(c.step & 1);
-    if (L.B == 0) {  // single bucket: sort + step, sorted contiguous output
-      c.mark(s);
-      bucket_step_kernel<T, D, KK, INTEG, BK_BLOCK><<<1, BK_BLOCK, bk_smem, s>>>(
-          P, st(c, c.cur), st(c, c.cur ^ 1), c.S);
-      c.cur ^= 1;
-      c.mark(s);
-      advance_kernel<<<1, 1, 0, s>>>(c.step_dev);
-      c.mark(s);
+    if (L.B == 0) {  // single bucket, system resident in shared memory
+      run_resident(c, s, 1);
       return;
     }
     // capacity of the buckets the state of a step lives in (pass-1 or final)
@@ -407,7 +487,7 @@ struct Engine final : EngineBase {
       cudaMemsetAsync(c.cur1[q], 0, 1024 * CUR1_STRIDE * 4, s);
       scatter_kernel<T, D, 1, SC_BLOCK, SC_ITEMS>
           <<<(unsigned)((n + SC_TILE - 1) / SC_TILE), SC_BLOCK, sc_smem, s>>>(
-              P, st(c, c.cur), st(c, c.cur ^ 1), c.cur1[q], pcap, nullptr, nullptr, 0);
+              P, st(c, c.cur), st(c, c.cur ^ 1), c.cur1[q], pcap, nullptr, nullptr, 0, n);
       c.cur ^= 1;
       c.partitioned = true;
     }
@@ -430,7 +510,7 @@ struct Engine final : EngineBase {
       cudaMemsetAsync(c.cur2, 0, (size_t)L.nbuckets * CUR2_STRIDE * 4, s);
       c.mark(s);
       scatter_kernel<T, D, 2, SC_BLOCK, SC_ITEMS>
-          <<<tiles2, SC_BLOCK, sc_smem, s>>>(P, A, Bf, c.cur2, L.cap2, c.cur1[q], c.tile_off, L.cap1);
+          <<<tiles2, SC_BLOCK, sc_smem, s>>>(P, A, Bf, c.cur2, L.cap2, c.cur1[q], c.tile_off, L.cap1, 0);
       c.mark(s);
       final_scan_kernel<<<1u << L.b1, 512, 0, s>>>(P, c.cur2, c.prefix1, c.S);
       c.mark(s);
@@ -439,6 +519,73 @@ struct Engine final : EngineBase {
       straddle_kernel<T, D, KK, INTEG><<<straddle_grid, 256, 0, s>>>(P, Bf, L.cap2, c.S, A, L.cap1,
                                                                      c.cur1[q ^ 1]);
     }
+    c.mark(s);
+    advance_kernel<<<1, 1, 0, s>>>(c.step_dev);
+    c.mark(s);
+  }
+
+  // N <= 2048: nsteps steps in one launch of one CTA (state in smem)
+  void run_resident(rbm_ctx& c, cudaStream_t s, uint32_t nsteps) override {
+    c.mark(s);
+    resident_kernel<T, D, KK, INTEG, BK_BLOCK><<<1, BK_BLOCK, rs_smem, s>>>(
+        c.P, st(c, c.cur), st(c, c.cur ^ 1), nsteps, c.step_dev);
+    c.cur ^= 1;
+    c.mark(s);
+  }
+
+  // ---------------------------------------- partitioned single system (a7)
+  // Buffers: A = stA (this rank's final buckets + halo bucket), B = st(c, 1)
+  // (send: 2^b1 pass-1 buckets by the top b1 bits of the key, capacity cap1,
+  // destination rank = top g bits), C = st(c, 2) (received: 2^b1 segments
+  // v = source * 2^b1/G + local pass-1 bucket).  cur1[0] = send cursors,
+  // cur1[1] = received segment counts (strided, for the tile table).
+  // Exchanges between the phases (caller, NCCL over NVLink via torch):
+  //   prologue / phase2 -> all-gather counts_send into counts_all, and
+  //                        all-to-all of B's arrays into C (equal chunks)
+  //   phase1            -> halo_send of rank r to halo_recv of rank r+1
+  void part_prologue(rbm_ctx& c, cudaStream_t s) override {
+    const DevParams& P = c.P;
+    cudaMemsetAsync(c.cur1[0], 0, 1024 * CUR1_STRIDE * 4, s);
+    scatter_kernel<T, D, 1, SC_BLOCK, SC_ITEMS>
+        <<<(unsigned)((c.n0 + SC_TILE - 1) / SC_TILE), SC_BLOCK, sc_smem, s>>>(
+            P, st(c, 0), st(c, 1), c.cur1[0], c.L.cap1, nullptr, nullptr, 0, c.n0);
+    pack_counts_kernel<<<1, 1024, 0, s>>>(c.cur1[0], 1u << c.L.b1, c.counts_send);
+    c.partitioned = true;
+  }
+
+  void part_phase1(rbm_ctx& c, cudaStream_t s) override {
+    const DevParams& P = c.P;
+    const Layout& L = c.L;
+    const uint32_t G = (uint32_t)c.cfg.world_size, rank = (uint32_t)c.cfg.rank;
+    const uint32_t nb1 = 1u << L.b1;
+    c.mark(s);
+    part_scan_kernel<<<1, 1024, 0, s>>>(P, c.counts_all, G, rank, c.cur1[1], c.prefix1, c.tile_off,
+                                        SC_TILE);
+    cudaMemsetAsync(c.cur2, 0, (size_t)L.nbuckets * CUR2_STRIDE * 4, s);
+    cudaMemsetAsync(c.cur1[0], 0, 1024 * CUR1_STRIDE * 4, s);
+    const unsigned tiles2 = (unsigned)(((uint64_t)nb1 * L.cap1 + SC_TILE - 1) / SC_TILE + nb1);
+    c.mark(s);
+    scatter_kernel<T, D, 2, SC_BLOCK, SC_ITEMS><<<tiles2, SC_BLOCK, sc_smem, s>>>(
+        P, st(c, 2), stA(c), c.cur2, L.cap2, c.cur1[1], c.tile_off, L.cap1, 0);
+    c.mark(s);
+    final_scan_kernel<<<nb1 / G, 512, 0, s>>>(P, c.cur2, c.prefix1, c.S);
+    c.mark(s);
+    fused(c, s, stA(c), st(c, 1), L.cap1, c.cur1[0]);
+    c.mark(s);
+    halo_extract_kernel<T, D><<<1, 64, 0, s>>>(P, stA(c), L.cap2, c.S, c.halo_send);
+  }
+
+  void part_phase2(rbm_ctx& c, cudaStream_t s) override {
+    const DevParams& P = c.P;
+    const Layout& L = c.L;
+    c.mark(s);
+    halo_place_kernel<T, D><<<1, 64, 0, s>>>(P, stA(c), L.cap2, c.S, c.halo_recv);
+    const unsigned grid = (unsigned)(((uint64_t)(L.nbuckets + 1) * 32 + 255) / 256);
+    c.mark(s);
+    straddle_kernel<T, D, KK, INTEG><<<grid, 256, 0, s>>>(P, stA(c), L.cap2, c.S, st(c, 1), L.cap1,
+                                                          c.cur1[0]);
+    c.mark(s);
+    pack_counts_kernel<<<1, 1024, 0, s>>>(c.cur1[0], 1u << L.b1, c.counts_send);
     c.mark(s);
     advance_kernel<<<1, 1, 0, s>>>(c.step_dev);
     c.mark(s);
@@ -494,12 +641,15 @@ EngineBase* make_for_kernel(uint32_t kernel, uint32_t integ) {
 inline const char* const* kernel_names(const rbm_ctx& c, uint32_t* count) {
   static const char* const r[] = {"rbmr_draw", "scan_reduce", "scan_parts", "scan_down",
                                   "rbmr_fill", "rbmr_delta", "rbmr_apply", "advance"};
-  static const char* const b0[] = {"bucket_step", "advance"};
+  static const char* const b0[] = {"resident_step"};
   static const char* const p1[] = {"tile_scan", "bucket_step", "straddle", "advance"};
   static const char* const p2[] = {"tile_scan", "scatter_sub", "final_scan", "bucket_step",
                                    "straddle", "advance"};
+  static const char* const pt[] = {"part_scan", "scatter_sub", "final_scan", "bucket_step",
+                                   "halo_extract", "halo_place", "straddle", "pack_counts", "advance"};
+  if (is_partitioned(c.cfg)) { *count = 9; return pt; }
   if (c.cfg.scheme == RBM_SCHEME_RBMR) { *count = 8; return r; }
-  if (c.L.B == 0) { *count = 2; return b0; }
+  if (c.L.B == 0) { *count = 1; return b0; }
   if (c.L.b2 == 0) { *count = 4; return p1; }
   *count = 6;
   return p2;

@@ -107,9 +107,8 @@ __device__ __forceinline__ uint32_t num_batches(const DevParams& prm) {
 // ------------------------------------------------------------------- init
 // X_0 in fp64, rounded to T; state stored in id order.
 template <typename T, int D>
-static __global__ void init_kernel(DevParams P, State<T, D> st, uint32_t kind, double a0, double a1,
-                            double a2, double a3) {
-  const uint64_t n = P.n;
+static __global__ void init_kernel(DevParams P, State<T, D> st, uint64_t id0, uint64_t n, uint32_t kind,
+                                   double a0, double a1, double a2, double a3) {
   // mixture centres (<= 64), computed redundantly per block
   __shared__ double cent[64][3];
   const int K = (kind == 4) ? (int)a0 : 0;
@@ -125,7 +124,7 @@ static __global__ void init_kernel(DevParams P, State<T, D> st, uint32_t kind, d
   __syncthreads();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t id = (uint32_t)i;
+    const uint32_t id = (uint32_t)(id0 + i);
     double x[3] = {0, 0, 0};
     if (kind == 1 || kind == 3 || kind == 4) {
       double z[D];
@@ -157,10 +156,10 @@ static __global__ void init_kernel(DevParams P, State<T, D> st, uint32_t kind, d
 
 // user state (id order, row-major N x D) -> SoA state in id order
 template <typename T, int D>
-static __global__ void set_state_kernel(uint64_t n, State<T, D> st, const T* __restrict__ xin) {
+static __global__ void set_state_kernel(uint64_t id0, uint64_t n, State<T, D> st, const T* __restrict__ xin) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    st.id[i] = (uint32_t)i;
+    st.id[i] = (uint32_t)(id0 + i);
 #pragma unroll
     for (int c = 0; c < D; ++c) st.x[c][i] = xin[i * D + c];
   }
@@ -263,7 +262,7 @@ static __global__ void __launch_bounds__(512) final_scan_kernel(DevParams P, con
   block_excl_scan<512>(a, nb2, ws);
   const uint32_t o = prefix1[u];
   for (uint32_t i = threadIdx.x; i < nb2; i += blockDim.x) S[base + i] = o + a[i];
-  if (u == 0 && threadIdx.x == 0) S[P.nbuckets] = (uint32_t)P.n;
+  if (u == 0 && threadIdx.x == 0) S[P.nbuckets] = prefix1[gridDim.x];  // end of this rank's range
 }
 
 // tile t of pass 2: pass-1 bucket u and its element range [lo, hi) (relative)
@@ -297,7 +296,7 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(DevParams P, Stat
                                                                uint32_t dcap,
                                                                const uint32_t* __restrict__ cnt1,
                                                                const uint32_t* __restrict__ tile_off,
-                                                               uint32_t scap) {
+                                                               uint32_t scap, uint64_t nsrc) {
   constexpr int TILE = BLOCK * ITEMS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw);  // 1024
@@ -311,8 +310,8 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(DevParams P, Stat
   uint32_t lo, hi, u = 0, bits, sh, sbase;
   if (LEVEL == 1) {
     lo = blockIdx.x * TILE;
-    if (lo >= P.n) return;
-    hi = (uint32_t)min((uint64_t)lo + TILE, P.n);
+    if (lo >= nsrc) return;
+    hi = (uint32_t)min((uint64_t)lo + TILE, nsrc);
     bits = P.b1;
     sh = 32u - P.b1;
     sbase = 0;
@@ -324,7 +323,9 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(DevParams P, Stat
   }
   constexpr uint32_t CS = (LEVEL == 1) ? CUR1_STRIDE : CUR2_STRIDE;
   const uint32_t nbins = 1u << bits, mask = nbins - 1;
-  const uint32_t dbase0 = (LEVEL == 1) ? 0u : (u << P.b2);  // first destination bucket
+  // first destination bucket: final buckets of this rank's pass-1 bucket
+  // (segment u of the received pass-1 data on a partitioned system)
+  const uint32_t dbase0 = (LEVEL == 1) ? 0u : ((u & P.nb1_loc_mask) << P.b2);
   for (uint32_t i = threadIdx.x; i < nbins; i += BLOCK) hist[i] = 0;
   __syncthreads();
 
@@ -591,6 +592,101 @@ static __global__ void __launch_bounds__(BLOCK) bucket_step_kernel(DevParams P, 
   }
 }
 
+// ------------------------------------------ resident multi-step (N <= 2048)
+// One CTA keeps the whole system in shared memory for `nsteps` steps (the
+// B = 0 layout, e.g. BASELINE C1): per step, keys (Philox) -> exact sort by
+// (key_m, id) -> Eq. (2.2) + update of every batch into the other smem
+// buffer in sorted order; one launch replaces 2 launches per step.
+template <typename T, int D> __host__ __device__ constexpr size_t resident_smem_bytes(uint32_t cap) {
+  return 2304                                             // cnt, off, wsum
+         + 2 * (size_t)cap * 4                            // ids, two buffers
+         + 2 * (size_t)D * cap * sizeof(T)                // x, two buffers
+         + (size_t)cap * 8 + (size_t)cap * 4              // composites, keys
+         + (((size_t)cap * 2 + 15) & ~(size_t)15);        // ord
+}
+
+template <typename T, int D, int KK, int INTEG, int BLOCK>
+static __global__ void __launch_bounds__(BLOCK) resident_kernel(DevParams P, State<T, D> src,
+                                                                State<T, D> dst, uint32_t nsteps,
+                                                                uint64_t* stepp) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* off = cnt + 256;
+  uint32_t* wsum = off + 256;
+  const uint32_t cap = P.cap, n = (uint32_t)P.n;
+  unsigned char* p = smem_raw + 2304;
+  T* xb = reinterpret_cast<T*>(p);                      // [2][D][cap]
+  p += 2 * (size_t)D * cap * sizeof(T);
+  unsigned long long* ks = reinterpret_cast<unsigned long long*>(p);
+  p += (size_t)cap * 8;
+  uint32_t* idb = reinterpret_cast<uint32_t*>(p);       // [2][cap]
+  p += 2 * (size_t)cap * 4;
+  uint32_t* key_l = reinterpret_cast<uint32_t*>(p);
+  p += (size_t)cap * 4;
+  uint16_t* ord = reinterpret_cast<uint16_t*>(p);
+  for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
+    idb[e] = src.id[e];
+#pragma unroll
+    for (int c = 0; c < D; ++c) xb[(size_t)c * cap + e] = src.x[c][e];
+  }
+  const uint32_t m0 = (uint32_t)*stepp;
+  for (uint32_t it = 0; it < nsteps; ++it) {
+    const uint32_t m = m0 + it, cur = it & 1u;
+    const uint32_t* id_l = idb + cur * cap;
+    const SX<T> xs{xb + (size_t)cur * D * cap, cap};
+    uint32_t* id_o = idb + (cur ^ 1u) * cap;
+    T* x_o = xb + (size_t)(cur ^ 1u) * D * cap;
+    for (uint32_t i = threadIdx.x; i < 256; i += BLOCK) cnt[i] = 0;
+    __syncthreads();
+    // exact sort by (key_m, id): counting sort on the top 8 key bits + rank
+    for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
+      const uint32_t key = shuffle_key(P, id_l[e], m);
+      key_l[e] = key;
+      ord[e] = (uint16_t)atomicAdd(&cnt[key >> 24], 1u);
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < 256; i += BLOCK) off[i] = cnt[i];
+    __syncthreads();
+    block_excl_scan<BLOCK>(off, 256, wsum);
+    for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
+      const uint32_t key = key_l[e];
+      ks[off[key >> 24] + ord[e]] = ((unsigned long long)key << 32) | id_l[e];
+    }
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
+      const uint32_t key = key_l[e];
+      const unsigned long long mine = ((unsigned long long)key << 32) | id_l[e];
+      const uint32_t a = off[key >> 24], c = cnt[key >> 24];
+      uint32_t r = a;
+      for (uint32_t j = a; j < a + c; ++j) r += (ks[j] < mine) ? 1u : 0u;
+      ord[r] = (uint16_t)e;
+    }
+    __syncthreads();
+    if (P.dbg_order)
+      for (uint32_t q = threadIdx.x; q < n; q += BLOCK) P.dbg_order[q] = id_l[ord[q]];
+    // every batch: Eq. (2.2) + update from the old positions, sorted output
+    for (uint32_t q = threadIdx.x; q < n; q += BLOCK) {
+      uint32_t b0, b1;
+      batch_range(q, P, b0, b1);
+      const uint32_t id = id_l[ord[q]];
+      T xn[D];
+      interior_update<T, D, KK, INTEG>(P, m, q, b0, b1, ord, xs, id, xn);
+      check_finite<T, D>(xn, P, id, m);
+      id_o[q] = id;
+#pragma unroll
+      for (int c = 0; c < D; ++c) x_o[(size_t)c * cap + q] = xn[c];
+    }
+    __syncthreads();
+  }
+  const uint32_t fin = nsteps & 1u;
+  for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
+    dst.id[e] = idb[fin * cap + e];
+#pragma unroll
+    for (int c = 0; c < D; ++c) dst.x[c][e] = xb[((size_t)fin * D + c) * cap + e];
+  }
+  if (threadIdx.x == 0) *stepp = m0 + nsteps;
+}
+
 // batches that straddle final buckets: one warp per owning boundary.  Their
 // members were written (unchanged) by the bucket kernels to their sorted
 // places in their own gapped ranges of `strad`: position P of bucket b sits at
@@ -604,25 +700,30 @@ static __global__ void __launch_bounds__(256) straddle_kernel(DevParams P, State
                                                               uint32_t* cur_next) {
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t bnd = warp + 1;  // boundaries 1 .. nbuckets-1
-  if (bnd >= P.nbuckets) return;
+  // boundaries 1 .. nbuckets-1; on a partitioned system with a halo also
+  // boundary 0 (the rank's first position), whose batch starts in the halo
+  // records of rank-1 placed at bucket -1 (physical slots [-cap, -cap + t),
+  // S[-1] = S[0] - t)
+  const int bnd = (int)warp + (P.halo ? 0 : 1);
+  if (bnd >= (int)P.nbuckets) return;
   const uint32_t Pb = S[bnd];
   if (Pb == 0 || Pb >= P.n) return;
   uint32_t b0, b1;
   batch_range(Pb, P, b0, b1);
   if (b0 == Pb) return;             // boundary at a batch start: no straddle
   if (S[bnd - 1] > b0) return;      // an earlier boundary inside the batch owns it
+  if (b1 > S[P.nbuckets]) return;   // ends on the next rank: that rank owns it
   const uint32_t m = (uint32_t)*P.step;
   const uint32_t sz = b1 - b0;
   // physical slot of every member (buckets walked forward from bnd-1)
-  uint32_t phys[3];
+  long long phys[3];
   {
-    uint32_t bb = bnd - 1;
+    int bb = bnd - 1;
     int k = 0;
     for (uint32_t q = 0; q < sz; ++q) {
       const uint32_t Pq = b0 + q;
       while (Pq >= S[bb + 1]) ++bb;
-      if ((q & 31u) == (uint32_t)lane) phys[k++] = bb * cap + (Pq - S[bb]);
+      if ((q & 31u) == (uint32_t)lane) phys[k++] = (long long)bb * cap + (Pq - S[bb]);
     }
   }
   T xnew[3][D];
@@ -631,7 +732,7 @@ static __global__ void __launch_bounds__(256) straddle_kernel(DevParams P, State
   for (uint32_t r = 0; r < rounds; ++r) {  // warp-uniform: every lane reaches the shuffles
     const uint32_t q = r * 32 + lane;
     const bool act = q < sz;
-    const uint32_t g = act ? (r == 0 ? phys[0] : (r == 1 ? phys[1] : phys[2])) : 0u;
+    const long long g = act ? (r == 0 ? phys[0] : (r == 1 ? phys[1] : phys[2])) : 0ll;
     const uint32_t id = act ? strad.id[g] : 0u;
     T xi[D], z[D], xn[D];
 #pragma unroll
@@ -643,8 +744,8 @@ static __global__ void __launch_bounds__(256) straddle_kernel(DevParams P, State
       for (int c = 0; c < D; ++c) f[c] = T(0);
       for (uint32_t h = 0; h < sz; ++h) {  // ascending sorted position
         const uint32_t hr = h >> 5;
-        const uint32_t src_ph = hr == 0 ? phys[0] : (hr == 1 ? phys[1] : phys[2]);
-        const uint32_t gh = __shfl_sync(0xffffffffu, src_ph, (int)(h & 31u));
+        const long long src_ph = hr == 0 ? phys[0] : (hr == 1 ? phys[1] : phys[2]);
+        const long long gh = __shfl_sync(0xffffffffu, src_ph, (int)(h & 31u));
         if (!act || h == q) continue;
         T xj[D];
 #pragma unroll
@@ -658,7 +759,7 @@ static __global__ void __launch_bounds__(256) straddle_kernel(DevParams P, State
         em_update<T, D>(xi, f, z, xn, P, true);
       }
     } else {
-      const uint32_t ga = __shfl_sync(0xffffffffu, phys[0], 0), gb = __shfl_sync(0xffffffffu, phys[0], 1);
+      const long long ga = __shfl_sync(0xffffffffu, phys[0], 0), gb = __shfl_sync(0xffffffffu, phys[0], 1);
       if (act) {
         T xa[D], xb[D], y[D];
 #pragma unroll
@@ -687,6 +788,137 @@ static __global__ void __launch_bounds__(256) straddle_kernel(DevParams P, State
     dst.key[g] = kn;
 #pragma unroll
     for (int c = 0; c < D; ++c) dst.x[c][g] = xnew[k][c];
+  }
+}
+
+// ------------------------------------------ partitioned single system (a7)
+// G ranks, rank r owns keys whose top log2 G bits are r.  After the exchange a
+// rank holds 2^b1 received pass-1 segments v = s*nl + u (source rank s, local
+// pass-1 bucket u < nl = 2^b1/G) of capacity cap1 each; M[s*2^b1 + j] is the
+// all-gathered count of source s's pass-1 bucket j (global j).
+constexpr uint32_t HALO_MAX = 64;  // >= p - 1 records of the batch crossing a rank boundary
+template <typename T, int D> __host__ __device__ constexpr size_t halo_bytes() {
+  return 16 + HALO_MAX * 4 + (size_t)HALO_MAX * D * sizeof(T);
+}
+
+// One block: segment counts (strided, for the pass-2 tile table), the exact
+// global start O_r of this rank (exclusive scan of the rank totals), the
+// global start of each local pass-1 bucket (prefix1[u], prefix1[nl] = O_r +
+// n_r) and the tile table.  Flags capacity_err = 2 if the rank holds fewer
+// than p particles (the halo exchange assumes a crossing batch touches only
+// two ranks).
+static __global__ void __launch_bounds__(1024) part_scan_kernel(DevParams P, const uint32_t* __restrict__ M,
+                                                                uint32_t G, uint32_t rank, uint32_t* cnt1,
+                                                                uint32_t* prefix1, uint32_t* tile_off,
+                                                                uint32_t tile) {
+  __shared__ uint32_t a[1025];
+  __shared__ uint32_t t[1025];
+  __shared__ uint32_t ws[33];
+  __shared__ uint32_t o_r;
+  const uint32_t nb1 = 1u << P.b1, nl = nb1 / G;
+  if (threadIdx.x == 0) o_r = 0;
+  __syncthreads();
+  for (uint32_t v = threadIdx.x; v < nb1; v += blockDim.x) {
+    const uint32_t s = v / nl, u = v - s * nl;
+    const uint32_t c = M[(size_t)s * nb1 + rank * nl + u];
+    cnt1[(size_t)v * CUR1_STRIDE] = c;
+    t[v] = (c + tile - 1) / tile;
+  }
+  for (uint32_t u = threadIdx.x; u < nl; u += blockDim.x) {
+    uint32_t c = 0;
+    for (uint32_t s = 0; s < G; ++s) c += M[(size_t)s * nb1 + rank * nl + u];
+    a[u] = c;
+  }
+  {  // O_r = all records of the ranks below (their pass-1 buckets, every source)
+    uint32_t part = 0;
+    const uint32_t below = rank * nl;
+    for (uint32_t q = threadIdx.x; q < G * below; q += blockDim.x) {
+      const uint32_t s = q / below, j = q - s * below;
+      part += M[(size_t)s * nb1 + j];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if ((threadIdx.x & 31) == 0 && part) atomicAdd(&o_r, part);
+  }
+  __syncthreads();
+  const uint32_t nloc = block_excl_scan<1024>(a, nl, ws);
+  const uint32_t ntiles = block_excl_scan<1024>(t, nb1, ws);
+  const uint32_t O = o_r;
+  for (uint32_t u = threadIdx.x; u < nl; u += blockDim.x) prefix1[u] = O + a[u];
+  for (uint32_t v = threadIdx.x; v < nb1; v += blockDim.x) tile_off[v] = t[v];
+  if (threadIdx.x == 0) {
+    prefix1[nl] = O + nloc;
+    tile_off[nb1] = ntiles;
+    if (nloc < P.p) atomicExch(P.capacity_err, 2u);
+  }
+}
+
+// The batch crossing this rank's end E = S[nbuckets] (global positions
+// [b0, E), t = E - b0 <= p - 1 records, left unchanged in sorted order by the
+// bucket kernels) is owned by rank+1: copy it to the halo buffer
+// {u32 t; ids[HALO_MAX]; x[HALO_MAX][D]}.
+template <typename T, int D>
+static __global__ void halo_extract_kernel(DevParams P, State<T, D> strad, uint32_t cap,
+                                           const uint32_t* __restrict__ S, unsigned char* halo) {
+  const uint32_t E = S[P.nbuckets];
+  uint32_t t = 0, b0 = E, b1 = E;
+  if (E < P.n) {
+    batch_range(E, P, b0, b1);
+    if (b0 < E) t = E - b0;
+  }
+  uint32_t* hid = reinterpret_cast<uint32_t*>(halo + 16);
+  T* hx = reinterpret_cast<T*>(halo + 16 + HALO_MAX * 4);
+  if (threadIdx.x == 0) *reinterpret_cast<uint32_t*>(halo) = t;
+  for (uint32_t q = threadIdx.x; q < t; q += blockDim.x) {
+    const uint32_t Pq = b0 + q;
+    int bb = (int)P.nbuckets - 1;
+    while (bb > 0 && S[bb] > Pq) --bb;
+    const long long g = (long long)bb * cap + (Pq - S[bb]);
+    hid[q] = strad.id[g];
+#pragma unroll
+    for (int c = 0; c < D; ++c) hx[q * D + c] = strad.x[c][g];
+  }
+}
+
+// Received halo (rank-1's trailing records of the crossing batch) -> bucket -1
+// of the local final layout, S[-1] = S[0] - t.
+template <typename T, int D>
+static __global__ void halo_place_kernel(DevParams P, State<T, D> strad, uint32_t cap, uint32_t* S,
+                                         const unsigned char* __restrict__ halo) {
+  const uint32_t t = *reinterpret_cast<const uint32_t*>(halo);
+  const uint32_t* hid = reinterpret_cast<const uint32_t*>(halo + 16);
+  const T* hx = reinterpret_cast<const T*>(halo + 16 + HALO_MAX * 4);
+  for (uint32_t q = threadIdx.x; q < t; q += blockDim.x) {
+    const long long g = -(long long)cap + q;
+    strad.id[g] = hid[q];
+#pragma unroll
+    for (int c = 0; c < D; ++c) strad.x[c][g] = hx[q * D + c];
+  }
+  if (threadIdx.x == 0) S[-1] = S[0] - t;
+}
+
+// cursor counts (stride CUR1_STRIDE) -> contiguous u32 (the all-gathered row)
+static __global__ void pack_counts_kernel(const uint32_t* __restrict__ cur, uint32_t nb, uint32_t* out) {
+  for (uint32_t v = threadIdx.x; v < nb; v += blockDim.x) out[v] = cur[(size_t)v * CUR1_STRIDE];
+}
+
+// gather from the received segments of a partitioned rank (holes skipped)
+template <typename T, int D>
+static __global__ void gather_part_kernel(DevParams P, State<T, D> st, uint32_t cap1,
+                                          const uint32_t* __restrict__ M, uint32_t G, uint32_t rank,
+                                          uint64_t i0, uint64_t i1, T* __restrict__ out) {
+  const uint32_t nb1 = 1u << P.b1, nl = nb1 / G;
+  const uint64_t total = (uint64_t)nb1 * cap1;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < total;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = (uint32_t)(q / cap1), e = (uint32_t)(q - (uint64_t)v * cap1);
+    const uint32_t s = v / nl, u = v - s * nl;
+    if (e >= M[(size_t)s * nb1 + rank * nl + u]) continue;
+    const uint64_t id = st.id[q];
+    if (id >= i0 && id < i1) {
+#pragma unroll
+      for (int c = 0; c < D; ++c) out[(id - i0) * D + c] = st.x[c][q];
+    }
   }
 }
 

@@ -1,0 +1,226 @@
+"""Partitioned single system over G ranks.
+
+librbm.so does every computation of the step (include/rbm.h, "Partitioned
+single system"); this module is the plumbing around its three exchanges:
+
+    H  halo     rank r's halo_send -> rank r+1's halo_recv (<= p-1 records)
+    C  counts   all-gather of counts_send (2^b1 u32 per rank) -> counts_all
+    R  records  all-to-all, equal chunks, of the 2+d exchanged arrays
+
+Protocol per context: rbm_init; prologue; C; R; then per step
+phase1; H; phase2; C; R.
+
+Two interchangeable exchanges move the bytes, both on byte views of the
+caller-owned workspaces (offsets from rbm_part_info_get):
+
+  DistExchange      one rank per process, torch.distributed (NCCL over
+                    NVLink on B200; gloo for the CPU tests of this plumbing)
+  LoopbackExchange  all G ranks in one process on one device: plain device
+                    copies, run in stream order (no kernel waits on another
+                    rank), used to test the G > 1 kernels on one GPU
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+from . import rbm as R
+
+
+class RbmPartInfo(C.Structure):
+    _fields_ = [
+        ("ws_bytes", C.c_uint64), ("world_size", C.c_uint32), ("rank", C.c_uint32),
+        ("nseg", C.c_uint32), ("narrays", C.c_uint32), ("chunk_elems", C.c_uint64),
+        ("send_off", C.c_uint64 * 5), ("recv_off", C.c_uint64 * 5), ("elem_bytes", C.c_uint32 * 5),
+        ("counts_send_off", C.c_uint64), ("counts_all_off", C.c_uint64),
+        ("halo_send_off", C.c_uint64), ("halo_recv_off", C.c_uint64), ("halo_bytes", C.c_uint64),
+        ("id0", C.c_uint64), ("n0", C.c_uint64),
+    ]
+
+
+_sig_done = False
+
+
+def _lib():
+    global _sig_done
+    L = R.lib()
+    if not _sig_done:
+        L.rbm_part_info_get.restype = C.c_int
+        L.rbm_part_info_get.argtypes = [C.POINTER(R.RbmConfig), C.POINTER(RbmPartInfo)]
+        for name in ("rbm_part_prologue", "rbm_part_phase1", "rbm_part_phase2"):
+            f = getattr(L, name)
+            f.restype, f.argtypes = C.c_int, [C.c_void_p]
+        _sig_done = True
+    return L
+
+
+def rbm_part_info_get(cfg: R.RbmConfig) -> RbmPartInfo:
+    out = RbmPartInfo()
+    R._check(_lib().rbm_part_info_get(C.byref(cfg), C.byref(out)))
+    return out
+
+
+def rbm_part_prologue(ctx):
+    R._check(_lib().rbm_part_prologue(ctx), ctx)
+
+
+def rbm_part_phase1(ctx):
+    R._check(_lib().rbm_part_phase1(ctx), ctx)
+
+
+def rbm_part_phase2(ctx):
+    R._check(_lib().rbm_part_phase2(ctx), ctx)
+
+
+class RankBuffers:
+    """Byte views of one rank's exchanged regions inside its workspace tensor."""
+
+    def __init__(self, ws, info: RbmPartInfo):
+        self.ws, self.info = ws, info
+        G = info.world_size
+
+        def v(off, nbytes):
+            return ws[off:off + nbytes]
+
+        self.chunk_bytes = [info.chunk_elems * info.elem_bytes[a] for a in range(info.narrays)]
+        self.send = [v(info.send_off[a], G * self.chunk_bytes[a]) for a in range(info.narrays)]
+        self.recv = [v(info.recv_off[a], G * self.chunk_bytes[a]) for a in range(info.narrays)]
+        self.counts_send = v(info.counts_send_off, 4 * info.nseg)
+        self.counts_all = v(info.counts_all_off, 4 * info.nseg * G)
+        self.halo_send = v(info.halo_send_off, info.halo_bytes)
+        self.halo_recv = v(info.halo_recv_off, info.halo_bytes)
+
+    @property
+    def rank(self) -> int:
+        return int(self.info.rank)
+
+
+class LoopbackExchange:
+    """All G ranks in this process (one device): exchanges are device copies."""
+
+    def counts_records(self, ranks):
+        G = len(ranks)
+        nb = 4 * ranks[0].info.nseg
+        for dst in ranks:
+            for s, src in enumerate(ranks):
+                dst.counts_all[s * nb:(s + 1) * nb].copy_(src.counts_send)
+        for a in range(ranks[0].info.narrays):
+            cb = ranks[0].chunk_bytes[a]
+            for r, src in enumerate(ranks):
+                for j in range(G):
+                    ranks[j].recv[a][r * cb:(r + 1) * cb].copy_(src.send[a][j * cb:(j + 1) * cb])
+
+    def halo(self, ranks):
+        for r in range(len(ranks) - 1):
+            ranks[r + 1].halo_recv.copy_(ranks[r].halo_send)
+
+
+class DistExchange:
+    """One rank per process over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+
+    def counts_records(self, ranks):
+        (me,) = ranks
+        d = self.dist
+        d.all_gather_into_tensor(me.counts_all, me.counts_send, group=self.group)
+        for a in range(me.info.narrays):
+            d.all_to_all_single(me.recv[a], me.send[a], group=self.group)
+
+    def halo(self, ranks):
+        (me,) = ranks
+        d, r, G = self.dist, me.rank, int(me.info.world_size)
+        ops = []
+        if r + 1 < G:
+            ops.append(d.P2POp(d.isend, me.halo_send, r + 1, group=self.group))
+        if r > 0:
+            ops.append(d.P2POp(d.irecv, me.halo_recv, r - 1, group=self.group))
+        if ops:
+            for q in d.batch_isend_irecv(ops):
+                q.wait()
+
+
+class PartitionedRBM:
+    """One global RBM-1 system split over `world_size` ranks.
+
+    `ranks`: the ranks this process drives (all of them for the loopback
+    exchange on one device; [rank] under torch.distributed)."""
+
+    def __init__(self, cfg: dict, world_size: int, ranks, exchange, device=None):
+        import torch
+        self.torch = torch
+        self.cfg, self.G, self.exchange = dict(cfg), int(world_size), exchange
+        self.systems, self.bufs = [], []
+        for r in ranks:
+            c = dict(self.cfg, world_size=self.G, rank=int(r))
+            s = R.RBM(c, device=device)
+            info = rbm_part_info_get(s.c)
+            assert info.ws_bytes == s.ws_bytes
+            self.systems.append(s)
+            self.bufs.append(RankBuffers(s.ws, info))
+        self.n, self.d = int(self.cfg["n"]), int(self.cfg["d"])
+        self.dtype = self.systems[0].dtype
+        self.device = self.systems[0].device
+        self.started = False
+
+    def set_state(self, x_full):
+        """X_0 in id order (N x d, host array or device tensor): each rank takes its ids."""
+        for s, b in zip(self.systems, self.bufs):
+            i0, n0 = int(b.info.id0), int(b.info.n0)
+            s.set_state(x_full[i0:i0 + n0])
+        self.started = False
+
+    def _start(self):
+        for s in self.systems:
+            rbm_part_prologue(s.ctx)
+        self.exchange.counts_records(self.bufs)
+        self.started = True
+
+    def step(self):
+        if not self.started:
+            self._start()
+        for s in self.systems:
+            rbm_part_phase1(s.ctx)
+        self.exchange.halo(self.bufs)
+        for s in self.systems:
+            rbm_part_phase2(s.ctx)
+        self.exchange.counts_records(self.bufs)
+
+    def run(self, nsteps: int):
+        for _ in range(int(nsteps)):
+            self.step()
+
+    def gather_local(self, out=None):
+        """Device tensor (N x d): rows of the ids held by this process's ranks
+        (other rows zero)."""
+        torch = self.torch
+        if out is None:
+            out = torch.zeros((self.n, self.d), dtype=self.dtype, device=self.device)
+        for s in self.systems:
+            R.rbm_gather(s.ctx, 0, self.n, out.data_ptr(), R.MEM_DEVICE)
+        return out
+
+    def gather(self, group=None):
+        """Full state in id order on every process (device tensor).  Under
+        torch.distributed the disjoint per-rank rows are combined by an
+        integer SUM over the bit patterns (exact: every other rank adds 0)."""
+        out = self.gather_local()
+        if not isinstance(self.exchange, DistExchange):
+            return out
+        torch = self.torch
+        iv = out.view(torch.int64 if self.dtype == torch.float64 else torch.int32)
+        self.exchange.dist.all_reduce(iv, group=group)
+        return out
+
+    def sync(self):
+        for s in self.systems:
+            s.sync()
+
+    @property
+    def step_index(self) -> int:
+        return self.systems[0].step_index
+
+    def close(self):
+        for s in self.systems:
+            s.close()

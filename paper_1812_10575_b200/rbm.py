@@ -27,7 +27,8 @@ MEM_DEVICE, MEM_HOST = 0, 1
 EXPORTS = ["rbm_workspace_size", "rbm_init", "rbm_set_state", "rbm_step", "rbm_run",
            "rbm_gather", "rbm_sync", "rbm_step_index", "rbm_launches_per_step", "rbm_layout",
            "rbm_debug_permutation", "rbm_debug_slots", "rbm_debug_philox", "rbm_last_error",
-           "rbm_destroy", "rbm_kernel_name", "rbm_timing_begin", "rbm_timing_end"]
+           "rbm_destroy", "rbm_kernel_name", "rbm_timing_begin", "rbm_timing_end",
+           "rbm_part_info_get", "rbm_part_prologue", "rbm_part_phase1", "rbm_part_phase2"]
 
 
 class RbmError(RuntimeError):
@@ -220,6 +221,10 @@ class RBM:
         self.device = torch.device(device or "cuda")
         self.dtype = torch.float64 if self.cfg.get("dtype", "f64") == "f64" else torch.float32
         self.n, self.d = int(self.c.n), int(self.c.d)
+        # rows this context takes in set_state: its initial id range (all N on one GPU)
+        G, r = int(self.c.world_size), int(self.c.rank)
+        self.id0 = self.n * r // G
+        self.n_rows = self.n * (r + 1) // G - self.id0
         self.ws_bytes = rbm_workspace_size(self.c)
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
         self.stream = torch.cuda.current_stream(self.device)
@@ -236,7 +241,7 @@ class RBM:
         else:
             import numpy as np
             a = np.ascontiguousarray(np.asarray(x), dtype=np.float64 if self.dtype == torch.float64 else np.float32)
-            assert a.size == self.n * self.d
+            assert a.size == self.n_rows * self.d
             rbm_set_state(self.ctx, a.ctypes.data, MEM_HOST)
 
     def step(self):

@@ -26,7 +26,7 @@ def R():
 def declared():
     src = open(HDR).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(rbm_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(rbm_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_exports_every_declared_symbol(R):
@@ -70,7 +70,9 @@ def status_of(R, cfg):
 
 @pytest.mark.parametrize("bad,status", [
     (dict(p=1), 1), (dict(p=600), 1), (dict(d=4), 1), (dict(d=2), 1),  # dyson needs d=1
-    (dict(sigma=-1.0), 1), (dict(dt=0.0), 1), (dict(kernel=99), 2), (dict(world_size=2), 3),
+    (dict(sigma=-1.0), 1), (dict(dt=0.0), 1), (dict(kernel=99), 2), (dict(world_size=2), 1),
+    (dict(world_size=3, n=100000), 1), (dict(world_size=2, rank=2, n=100000), 1),
+    (dict(world_size=2, n=100000, scheme="rbmr"), 3), (dict(world_size=2, n=100000, p=2), 0),
     (dict(integrator="split", p=4), 1), (dict(n=501, integrator="split"), 1),
     (dict(n=1), 1), (dict(replica=1 << 24), 1), (dict(p=65, n=100000), 1),
 ])
@@ -101,3 +103,47 @@ def test_step_without_gpu_is_loud(R):
     out = ctypes.c_void_p()
     st = R.lib().rbm_init(ctypes.byref(c), None, 0, None, None, ctypes.byref(out))
     assert st != 0 and not out.value
+
+
+def test_part_info_layout_matches_header(tmp_path):
+    from paper_1812_10575_b200 import partition as PT
+    fields = [f for f, _ in PT.RbmPartInfo._fields_]
+    prog = tmp_path / "p.c"
+    body = "".join(f'printf("{f} %zu\\n", offsetof(rbm_part_info, {f}));' for f in fields)
+    prog.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "rbm.h"\nint main(void){'
+                    + body + 'printf("sizeof %zu\\n", sizeof(rbm_part_info)); return 0;}\n')
+    exe = tmp_path / "p"
+    subprocess.check_call(["gcc", "-std=c11", f"-I{os.path.join(ROOT, 'include')}", str(prog), "-o", str(exe)])
+    got = dict(l.split() for l in subprocess.check_output([str(exe)], text=True).splitlines())
+    for f in fields:
+        assert int(got[f]) == getattr(PT.RbmPartInfo, f).offset, f
+    assert int(got["sizeof"]) == ctypes.sizeof(PT.RbmPartInfo)
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_part_info_host_layout(R, G):
+    """Exchange layout of the partitioned system (host computation only):
+    regions inside the workspace, disjoint, equal chunks; the initial id
+    ranges tile [0, N)."""
+    from paper_1812_10575_b200 import partition as PT
+    cfg = RI.c5_coulomb_reg(n=200003, p=8)
+    ends = []
+    for r in range(G):
+        info = PT.rbm_part_info_get(R.make_config(dict(cfg, world_size=G, rank=r)))
+        st, ws = status_of(R, dict(cfg, world_size=G, rank=r))
+        assert st == 0 and info.ws_bytes == ws
+        assert info.narrays == 2 + cfg["d"] and info.nseg % G == 0
+        regions = []
+        for a in range(info.narrays):
+            nb = G * info.chunk_elems * info.elem_bytes[a]
+            regions += [(info.send_off[a], nb), (info.recv_off[a], nb)]
+        regions += [(info.counts_send_off, 4 * info.nseg), (info.counts_all_off, 4 * G * info.nseg),
+                    (info.halo_send_off, info.halo_bytes), (info.halo_recv_off, info.halo_bytes)]
+        regions.sort()
+        for (o1, n1), (o2, _) in zip(regions, regions[1:]):
+            assert o1 + n1 <= o2
+        assert regions[-1][0] + regions[-1][1] <= info.ws_bytes
+        ends.append((info.id0, info.n0))
+    assert ends[0][0] == 0 and sum(n for _, n in ends) == cfg["n"]
+    for (a, na), (b, _) in zip(ends, ends[1:]):
+        assert a + na == b
