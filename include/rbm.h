@@ -235,7 +235,7 @@ rbm_status rbm_timing_end(rbm_ctx* ctx, double* ms_per_kernel, uint32_t* steps_r
 typedef struct {
   uint64_t ws_bytes;        /* workspace bytes (= rbm_workspace_size) */
   uint32_t world_size, rank;
-  uint32_t nseg;            /* pass-1 buckets 2^b1: u32 counts per rank in exchange C */
+  uint32_t nseg;            /* pass-1 segments (2^b1 digits x 2^segk cursors): u32 counts per rank in exchange C */
   uint32_t narrays;         /* exchanged arrays: 2 + d (id u32, key u32, x_0 .. x_{d-1} dtype) */
   uint64_t chunk_elems;     /* elements per destination rank in each exchanged array */
   uint64_t send_off[5];     /* byte offsets in ws of the exchanged send arrays (a < narrays) */

@@ -98,7 +98,14 @@ rbm_status init_impl(rbm_ctx* c, const rbm_config* cfg, void* wsp, size_t ws_byt
   P.group = 0;
   if (cfg->p <= 32) { P.group = 1; while (P.group < cfg->p) P.group <<= 1; }
   P.big_scratch = c->big_scratch;
+  P.prof = nullptr;
+  if (std::getenv("RBM_PHASE_PROF")) {  // debug: per-phase cycles of the bucket kernel
+    CU(cudaMalloc(&P.prof, 64 * 8));
+    CU(cudaMemset(P.prof, 0, 64 * 8));
+  }
   P.nb1_loc_mask = ((1u << c->L.b1) >> c->L.g) - 1u;
+  P.segk = c->L.segk;
+  P.segmask = (1u << c->L.segk) - 1u;
   P.halo = (is_partitioned(*cfg) && cfg->rank > 0) ? 1u : 0u;
   rbm_status s = c->eng->setup(*c);
   if (s) return s;
@@ -361,9 +368,9 @@ rbm_status rbm_part_info_get(const rbm_config* cfg, rbm_part_info* out) {
   out->ws_bytes = ws.used;
   out->world_size = (uint32_t)cfg->world_size;
   out->rank = (uint32_t)cfg->rank;
-  out->nseg = 1u << tmp.L.b1;
+  out->nseg = tmp.L.nseg();
   out->narrays = 2 + cfg->d;
-  out->chunk_elems = (uint64_t)((1u << tmp.L.b1) >> tmp.L.g) * tmp.L.cap1;
+  out->chunk_elems = (uint64_t)(tmp.L.nseg() >> tmp.L.g) * tmp.L.cap1;
   const uint32_t es = (uint32_t)elt_size(*cfg);
   for (int b = 1; b <= 2; ++b) {
     uint64_t* o = b == 1 ? out->send_off : out->recv_off;
@@ -408,6 +415,16 @@ const char* rbm_last_error(const rbm_ctx* c) { return c ? c->err.c_str() : g_err
 
 rbm_status rbm_destroy(rbm_ctx* c) {
   if (!c) return RBM_OK;
+  if (c->P.prof) {
+    unsigned long long h[64];
+    if (cudaMemcpy(h, c->P.prof, sizeof h, cudaMemcpyDeviceToHost) == cudaSuccess && h[63]) {
+      std::fprintf(stderr, "RBM_PHASE_PROF bucket kernel, %llu CTAs, mean SM cycles per CTA:", h[63]);
+      for (int i = 0; i < 16; ++i)
+        if (h[i]) std::fprintf(stderr, " p%d=%.0f", i, (double)h[i] / (double)h[63]);
+      std::fprintf(stderr, "\n");
+    }
+    cudaFree(c->P.prof);
+  }
   for (int i = 0; i < 4; ++i)
     if (c->graph[i]) cudaGraphExecDestroy(c->graph[i]);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);

@@ -69,12 +69,30 @@ struct DevParams {
   // position is completed with records of rank-1 placed at bucket "-1".
   uint32_t nb1_loc_mask;
   uint32_t halo;
+  // output segments: every pass-1 bucket is split into K = 2^segk segments
+  // with their own cursors (segment = digit << segk | (producer CTA & (K-1)))
+  // so that the run reservations of concurrent CTAs do not serialise on one
+  // L2 atomic address per digit
+  uint32_t segk, segmask;
   const uint64_t* step;     // device step counter m
   unsigned long long* nonfinite;  // atomicMin of (m<<32 | id); ~0 if clean
   uint32_t* capacity_err;         // set to 1 if a bucket overflowed every fallback
   uint32_t* big_claim;            // NBIG slot flags of the global-scratch fallback
   unsigned char* big_scratch;     // NBIG slots of BIG_CAP elements
+  unsigned long long* prof;       // debug (RBM_PHASE_PROF): summed SM cycles per kernel phase
 };
+
+// phase profiling (debug only, P.prof set by RBM_PHASE_PROF): thread 0 of
+// each CTA adds the cycles since the previous mark to slot i; slot 63 counts CTAs
+#define RBM_PROF_BEGIN(P) long long prof_t_ = (P).prof ? clock64() : 0
+#define RBM_PROF(P, i)                                                  \
+  do {                                                                  \
+    if ((P).prof && threadIdx.x == 0) {                                 \
+      const long long t_ = clock64();                                   \
+      atomicAdd(&(P).prof[i], (unsigned long long)(t_ - prof_t_));     \
+      prof_t_ = t_;                                                     \
+    }                                                                   \
+  } while (0)
 
 constexpr int NBIG = 2;             // concurrent oversized buckets handled per step
 constexpr uint32_t BIG_CAP = 65535; // u16 indices

@@ -6,6 +6,7 @@
 // carving, per-config kernel dispatch, CUDA-graph capture/replay of steps.
 // Every arithmetic step of the RBM path runs in the kernels of
 // rbm_kernels.cuh; there is no CPU fallback.
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -41,12 +42,16 @@ struct Layout {
   uint32_t g = 0;        // log2 world_size (partitioned single system; 0 on one GPU)
   uint32_t B = 0, b1 = 0, b2 = 0, nbuckets = 1, cap = 0;  // nbuckets: final buckets of this rank
   uint32_t SB = 8, idbits = 1, lowbits = 0;
-  uint32_t cap1 = 0;     // gapped capacity of a pass-1 bucket (2-pass layouts; per source rank when partitioned)
+  uint32_t segk = 0;     // log2 segments per pass-1 bucket (2-pass layouts)
+  uint32_t cap1 = 0;     // gapped capacity of a pass-1 segment (2-pass layouts; per source rank when partitioned)
+  uint32_t nseg() const { return (1u << b1) << segk; }
   uint32_t cap2 = 0;     // gapped capacity of a final bucket
   uint64_t slots = 0;    // elements per state buffer: max(N, 2^b1 cap1, 2^B cap2)
 };
 constexpr int FUSED_BLOCK = 256;
 constexpr int PAIR_BLOCK = 512, PAIR_ITEMS = 5;  // p = 2 lean kernel: capacity <= 2560
+constexpr int PAIRS_BLOCK = 256, PAIRS_ITEMS = 6; // p = 2 lean kernel, small buckets: capacity <= 1536
+constexpr int PERSIST_BLOCK = 1024, PERSIST_ITEMS = 3;  // p = 2 persistent kernel: capacity <= 3072
 constexpr uint32_t FUSED_CAP_MAX = 4096;  // fast-path bucket capacity (u16 indices, smem)
 
 struct EngineBase;
@@ -170,8 +175,14 @@ inline Layout choose_layout(const rbm_config& c) {
       if (v >= 5 && v <= 10 && L.B - v >= 5 && L.B - v <= 10) L.b1 = (uint32_t)v;
     }
     if (part && L.b1 < L.g) L.b1 = L.g;  // the pass-1 digit carries the destination rank
+    if (L.b1 < 2) L.b1 = 2;              // >= 4 output digits (uint4 scans)
     if (L.b1 > 10) L.b1 = 10;
     L.b2 = L.B - L.b1;
+    // one cursor per pass-1 digit: splitting each digit into 2^segk salted
+    // segments (to spread the reservation atomics) measured no faster at C5,
+    // and a salt fixed per CTA overfills segments when few CTAs produce
+    // (prologue at small N), so segk stays 0 (the kernels take any segk)
+    L.segk = 0;
   }
   L.nbuckets = 1u << (L.B - L.g);
   L.SB = L.idbits > L.B + 8 ? L.idbits - L.B : 8;  // 32-bit composites: lowbits + idbits <= 32
@@ -200,15 +211,15 @@ inline Layout choose_layout(const rbm_config& c) {
     uint64_t id0, n0;
     initial_ids(c, id0, n0);
     L.cap2 = gcap((double)n / (1u << L.B), L.cap + 64);
-    L.cap1 = gcap((double)n / ((double)c.world_size * (1u << L.b1)), 64);
+    L.cap1 = gcap((double)n / ((double)c.world_size * L.nseg()), 64);
     L.slots = std::max<uint64_t>(n0, (uint64_t)(L.nbuckets + 1) * L.cap2);
-    L.slots = std::max<uint64_t>(L.slots, (uint64_t)(1u << L.b1) * L.cap1);
+    L.slots = std::max<uint64_t>(L.slots, (uint64_t)L.nseg() * L.cap1);
   } else if (L.B > 0) {
     L.cap2 = gcap((double)n / L.nbuckets, L.cap + 64);
     L.slots = std::max<uint64_t>(L.slots, (uint64_t)L.nbuckets * L.cap2);
     if (L.b2) {
-      L.cap1 = gcap((double)n / (1u << L.b1), 64);
-      L.slots = std::max<uint64_t>(L.slots, (uint64_t)(1u << L.b1) * L.cap1);
+      L.cap1 = gcap((double)n / L.nseg(), 64);
+      L.slots = std::max<uint64_t>(L.slots, (uint64_t)L.nseg() * L.cap1);
     }
   }
   return L;
@@ -296,14 +307,14 @@ inline void carve(rbm_ctx& c, Workspace& ws) {
     c.keybuf[b] = ws.take<uint32_t>(c.xstride);
     c.xbuf[b] = ws.take<unsigned char>(c.xstride * k.d * es);
   }
-  for (int q = 0; q < 2; ++q) c.cur1[q] = ws.take<uint32_t>(1024 * CUR1_STRIDE);
+  for (int q = 0; q < 2; ++q) c.cur1[q] = ws.take<uint32_t>((size_t)MAX_SEG * CUR1_STRIDE);
   c.prefix1 = ws.take<uint32_t>(1025);
   c.tile_off = ws.take<uint32_t>(1025);
   c.S = ws.take<uint32_t>((size_t)c.L.nbuckets + 2);
   if (c.S) c.S += 1;  // S[-1]: start of the halo bucket (partitioned)
   if (part) {
-    c.counts_send = ws.take<uint32_t>(1024);
-    c.counts_all = ws.take<uint32_t>((size_t)k.world_size * 1024);
+    c.counts_send = ws.take<uint32_t>(c.L.nseg());
+    c.counts_all = ws.take<uint32_t>((size_t)k.world_size * c.L.nseg());
     c.halo_send = ws.take<unsigned char>(halo_bytes<double, 3>());
     c.halo_recv = ws.take<unsigned char>(halo_bytes<double, 3>());
   }
@@ -365,8 +376,19 @@ struct Engine final : EngineBase {
     return s;
   }
 
-  size_t fu_smem = 0, pr_smem = 0, rs_smem = 0;
-  bool use_pair = false;
+  size_t fu_smem = 0, pr_smem = 0, rs_smem = 0, ps_smem = 0, sp_smem = 0;
+  bool use_pair = false, use_persist = false, use_split = false, use_pair_small = false;
+  size_t prs_smem = 0;
+  // pass-2 splitter configurations: one CTA of 1024 threads per SM with
+  // 4096-record tiles (default; measured fastest at C5), or
+  // RBM_SPLIT_CFG=small: two CTAs of 512 per SM with 2048-record tiles
+  static constexpr int SPLIT_BLOCK = 512;
+  static constexpr int SPLIT_TILE = (8 + D * sizeof(T) <= 20) ? 2048 : 1024;
+  static constexpr int SPLITB_BLOCK = 1024;
+  static constexpr int SPLITB_TILE = 2 * SPLIT_TILE;
+  bool split_big = false;
+  size_t spb_smem = 0;
+  int num_sms = 148;
 
   rbm_status setup(rbm_ctx& c) override {
     c.tile = SC_TILE;
@@ -377,6 +399,28 @@ struct Engine final : EngineBase {
     pr_smem = pair_smem_bytes<T, D>(c.L.cap, c.L.SB);
     use_pair = c.cfg.p == 2 && c.L.B > 0 && c.L.cap <= (uint32_t)(PAIR_BLOCK * PAIR_ITEMS) &&
                pr_smem <= 227 * 1024;
+    ps_smem = persist_smem_bytes<T, D>(c.L.cap, c.L.SB);
+    prs_smem = pr_smem;
+    use_pair_small = use_pair && c.L.cap <= (uint32_t)(PAIRS_BLOCK * PAIRS_ITEMS);
+    {
+      // "persist": one CTA per SM looping over buckets with double-buffered
+      // TMA (measured slower than two one-bucket CTAs per SM; kept selectable)
+      const char* e = std::getenv("RBM_PAIR_KERNEL");
+      use_persist = use_pair && c.L.cap <= (uint32_t)(PERSIST_BLOCK * PERSIST_ITEMS) &&
+                    ps_smem <= 227 * 1024 && (e && std::strcmp(e, "persist") == 0);
+    }
+    sp_smem = split_smem_bytes<T, D, SPLIT_TILE>();
+    spb_smem = split_smem_bytes<T, D, SPLITB_TILE>();
+    {
+      const char* e = std::getenv("RBM_SPLIT_CFG");  // "small": two CTAs per SM, half tiles
+      split_big = !(e && std::strcmp(e, "small") == 0) && spb_smem <= 227 * 1024;
+    }
+    {
+      const char* e = std::getenv("RBM_SPLIT_KERNEL");  // "old": one CTA per tile (comparison)
+      use_split = sp_smem <= 227 * 1024 && !(e && std::strcmp(e, "old") == 0);
+    }
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, c.device);
+    if (num_sms <= 0) num_sms = 148;
     if (bk_smem != bucket_smem_bytes<T, D>(c.L.cap))
       return fail(&c, RBM_ERR_STATE, "bucket smem size mismatch %zu vs %zu", bk_smem, bucket_smem_bytes<T, D>(c.L.cap));
     auto chk = [&](cudaError_t e, const char* what) -> rbm_status {
@@ -397,6 +441,25 @@ struct Engine final : EngineBase {
       if ((s = chk(cudaFuncSetAttribute(resident_kernel<T, D, KK, INTEG, BK_BLOCK>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem),
                    "smem attr resident"))) return s;
+    }
+    if (use_split) {
+      if ((s = chk(cudaFuncSetAttribute(split_persist_kernel<T, D, SPLIT_BLOCK, SPLIT_TILE>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp_smem),
+                   "smem attr split"))) return s;
+      if (split_big &&
+          (s = chk(cudaFuncSetAttribute(split_persist_kernel<T, D, SPLITB_BLOCK, SPLITB_TILE>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spb_smem),
+                   "smem attr split big"))) return s;
+    }
+    if (use_persist) {
+      if ((s = chk(cudaFuncSetAttribute(pair_persist_kernel<T, D, KK, INTEG, PERSIST_BLOCK, PERSIST_ITEMS>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps_smem),
+                   "smem attr persist"))) return s;
+    }
+    if (use_pair_small) {
+      if ((s = chk(cudaFuncSetAttribute(bucket_pair_kernel<T, D, KK, INTEG, PAIRS_BLOCK, PAIRS_ITEMS>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prs_smem),
+                   "smem attr pair small"))) return s;
     }
     if (use_pair) {
       if ((s = chk(cudaFuncSetAttribute(bucket_pair_kernel<T, D, KK, INTEG, PAIR_BLOCK, PAIR_ITEMS>,
@@ -438,7 +501,7 @@ struct Engine final : EngineBase {
   void gather(rbm_ctx& c, uint64_t i0, uint64_t i1, void* out, cudaStream_t s) override {
     if (is_partitioned(c.cfg)) {
       if (c.partitioned) {
-        gather_part_kernel<T, D><<<grid_for((uint64_t)(1u << c.L.b1) * c.L.cap1, 256), 256, 0, s>>>(
+        gather_part_kernel<T, D><<<grid_for((uint64_t)c.L.nseg() * c.L.cap1, 256), 256, 0, s>>>(
             c.P, st(c, 2), c.L.cap1, c.counts_all, (uint32_t)c.cfg.world_size, (uint32_t)c.cfg.rank,
             i0, i1, reinterpret_cast<T*>(out));
       } else {
@@ -450,7 +513,7 @@ struct Engine final : EngineBase {
     if (c.cfg.scheme == RBM_SCHEME_RBM1 && c.L.B > 0 && c.partitioned) {
       Gapped g;
       g.cap = c.L.b2 ? c.L.cap1 : c.L.cap2;
-      g.nb = 1u << c.L.b1;
+      g.nb = c.L.nseg();
       g.cnt = c.cur1[c.step & 1];
       g.cstride = CUR1_STRIDE;
       gather_gapped_kernel<T, D><<<grid_for((uint64_t)g.nb * g.cap, 256), 256, 0, s>>>(
@@ -461,9 +524,37 @@ struct Engine final : EngineBase {
     }
   }
 
+  // pass 2: pass-1 buckets/segments (capacity cap1, counts cnt1 strided) -> final buckets
+  void split2(rbm_ctx& c, cudaStream_t s, State<T, D> in, State<T, D> out, const uint32_t* cnt1) {
+    const Layout& L = c.L;
+    if (use_split && split_big) {
+      split_persist_kernel<T, D, SPLITB_BLOCK, SPLITB_TILE><<<(unsigned)num_sms, SPLITB_BLOCK, spb_smem, s>>>(
+          c.P, in, out, c.cur2, L.cap2, cnt1, c.tile_off, L.cap1);
+    } else if (use_split) {
+      split_persist_kernel<T, D, SPLIT_BLOCK, SPLIT_TILE><<<(unsigned)(2 * num_sms), SPLIT_BLOCK, sp_smem, s>>>(
+          c.P, in, out, c.cur2, L.cap2, cnt1, c.tile_off, L.cap1);
+    } else {  // tile table built with tile2() == SC_TILE
+      const uint32_t ns = L.nseg();
+      const unsigned tiles2 = (unsigned)(((uint64_t)ns * L.cap1 + SC_TILE - 1) / SC_TILE + ns);
+      scatter_kernel<T, D, 2, SC_BLOCK, SC_ITEMS><<<tiles2, SC_BLOCK, sc_smem, s>>>(
+          c.P, in, out, c.cur2, L.cap2, cnt1, c.tile_off, L.cap1, 0);
+    }
+  }
+
+  uint32_t tile2() const {
+    return use_split ? (uint32_t)(split_big ? SPLITB_TILE : SPLIT_TILE) : (uint32_t)SC_TILE;
+  }
+
   void fused(rbm_ctx& c, cudaStream_t s, State<T, D> in, State<T, D> out, uint32_t ocap,
              uint32_t* cur_next) {
-    if (use_pair)
+    if (use_persist)
+      pair_persist_kernel<T, D, KK, INTEG, PERSIST_BLOCK, PERSIST_ITEMS>
+          <<<std::min<uint32_t>(c.L.nbuckets, (uint32_t)num_sms), PERSIST_BLOCK, ps_smem, s>>>(
+              c.P, in, c.L.cap2, c.S, out, ocap, cur_next);
+    else if (use_pair_small)
+      bucket_pair_kernel<T, D, KK, INTEG, PAIRS_BLOCK, PAIRS_ITEMS>
+          <<<c.L.nbuckets, PAIRS_BLOCK, prs_smem, s>>>(c.P, in, c.L.cap2, c.S, out, ocap, cur_next);
+    else if (use_pair)
       bucket_pair_kernel<T, D, KK, INTEG, PAIR_BLOCK, PAIR_ITEMS>
           <<<c.L.nbuckets, PAIR_BLOCK, pr_smem, s>>>(c.P, in, c.L.cap2, c.S, out, ocap, cur_next);
     else
@@ -484,18 +575,18 @@ struct Engine final : EngineBase {
     // capacity of the buckets the state of a step lives in (pass-1 or final)
     const uint32_t pcap = L.b2 ? L.cap1 : L.cap2;
     if (!c.partitioned) {  // prologue: any storage order -> gapped buckets of step m
-      cudaMemsetAsync(c.cur1[q], 0, 1024 * CUR1_STRIDE * 4, s);
+      cudaMemsetAsync(c.cur1[q], 0, (size_t)L.nseg() * CUR1_STRIDE * 4, s);
       scatter_kernel<T, D, 1, SC_BLOCK, SC_ITEMS>
           <<<(unsigned)((n + SC_TILE - 1) / SC_TILE), SC_BLOCK, sc_smem, s>>>(
               P, st(c, c.cur), st(c, c.cur ^ 1), c.cur1[q], pcap, nullptr, nullptr, 0, n);
       c.cur ^= 1;
       c.partitioned = true;
     }
-    cudaMemsetAsync(c.cur1[q ^ 1], 0, 1024 * CUR1_STRIDE * 4, s);  // step-(m+1) cursors
+    cudaMemsetAsync(c.cur1[q ^ 1], 0, (size_t)L.nseg() * CUR1_STRIDE * 4, s);  // step-(m+1) cursors
     const unsigned straddle_grid = (unsigned)(((uint64_t)L.nbuckets * 32 + 255) / 256);
     State<T, D> A = st(c, c.cur), Bf = st(c, c.cur ^ 1);
     c.mark(s);
-    tile_scan_kernel<<<1, 1024, 0, s>>>(P, c.cur1[q], c.prefix1, c.tile_off, c.S, SC_TILE);
+    tile_scan_kernel<<<1, 1024, 0, s>>>(P, c.cur1[q], c.prefix1, c.tile_off, c.S, tile2());
     if (L.b2 == 0) {
       // A holds the final buckets of step m; the fused step writes m+1's into B
       c.mark(s);
@@ -506,11 +597,9 @@ struct Engine final : EngineBase {
       c.cur ^= 1;
     } else {
       // A holds the pass-1 buckets of step m: split them by the next b2 bits into B
-      const unsigned tiles2 = (unsigned)((n + SC_TILE - 1) / SC_TILE + (1u << L.b1));
       cudaMemsetAsync(c.cur2, 0, (size_t)L.nbuckets * CUR2_STRIDE * 4, s);
       c.mark(s);
-      scatter_kernel<T, D, 2, SC_BLOCK, SC_ITEMS>
-          <<<tiles2, SC_BLOCK, sc_smem, s>>>(P, A, Bf, c.cur2, L.cap2, c.cur1[q], c.tile_off, L.cap1, 0);
+      split2(c, s, A, Bf, c.cur1[q]);
       c.mark(s);
       final_scan_kernel<<<1u << L.b1, 512, 0, s>>>(P, c.cur2, c.prefix1, c.S);
       c.mark(s);
@@ -545,11 +634,11 @@ struct Engine final : EngineBase {
   //   phase1            -> halo_send of rank r to halo_recv of rank r+1
   void part_prologue(rbm_ctx& c, cudaStream_t s) override {
     const DevParams& P = c.P;
-    cudaMemsetAsync(c.cur1[0], 0, 1024 * CUR1_STRIDE * 4, s);
+    cudaMemsetAsync(c.cur1[0], 0, (size_t)c.L.nseg() * CUR1_STRIDE * 4, s);
     scatter_kernel<T, D, 1, SC_BLOCK, SC_ITEMS>
         <<<(unsigned)((c.n0 + SC_TILE - 1) / SC_TILE), SC_BLOCK, sc_smem, s>>>(
             P, st(c, 0), st(c, 1), c.cur1[0], c.L.cap1, nullptr, nullptr, 0, c.n0);
-    pack_counts_kernel<<<1, 1024, 0, s>>>(c.cur1[0], 1u << c.L.b1, c.counts_send);
+    pack_counts_kernel<<<1, 1024, 0, s>>>(c.cur1[0], c.L.nseg(), c.counts_send);
     c.partitioned = true;
   }
 
@@ -560,13 +649,11 @@ struct Engine final : EngineBase {
     const uint32_t nb1 = 1u << L.b1;
     c.mark(s);
     part_scan_kernel<<<1, 1024, 0, s>>>(P, c.counts_all, G, rank, c.cur1[1], c.prefix1, c.tile_off,
-                                        SC_TILE);
+                                        tile2());
     cudaMemsetAsync(c.cur2, 0, (size_t)L.nbuckets * CUR2_STRIDE * 4, s);
-    cudaMemsetAsync(c.cur1[0], 0, 1024 * CUR1_STRIDE * 4, s);
-    const unsigned tiles2 = (unsigned)(((uint64_t)nb1 * L.cap1 + SC_TILE - 1) / SC_TILE + nb1);
+    cudaMemsetAsync(c.cur1[0], 0, (size_t)c.L.nseg() * CUR1_STRIDE * 4, s);
     c.mark(s);
-    scatter_kernel<T, D, 2, SC_BLOCK, SC_ITEMS><<<tiles2, SC_BLOCK, sc_smem, s>>>(
-        P, st(c, 2), stA(c), c.cur2, L.cap2, c.cur1[1], c.tile_off, L.cap1, 0);
+    split2(c, s, st(c, 2), stA(c), c.cur1[1]);
     c.mark(s);
     final_scan_kernel<<<nb1 / G, 512, 0, s>>>(P, c.cur2, c.prefix1, c.S);
     c.mark(s);
@@ -585,7 +672,7 @@ struct Engine final : EngineBase {
     straddle_kernel<T, D, KK, INTEG><<<grid, 256, 0, s>>>(P, stA(c), L.cap2, c.S, st(c, 1), L.cap1,
                                                           c.cur1[0]);
     c.mark(s);
-    pack_counts_kernel<<<1, 1024, 0, s>>>(c.cur1[0], 1u << L.b1, c.counts_send);
+    pack_counts_kernel<<<1, 1024, 0, s>>>(c.cur1[0], L.nseg(), c.counts_send);
     c.mark(s);
     advance_kernel<<<1, 1, 0, s>>>(c.step_dev);
     c.mark(s);

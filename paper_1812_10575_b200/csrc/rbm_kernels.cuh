@@ -74,6 +74,49 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t* a, int n, uint32_t
   return total;
 }
 
+// out[0..n) = exclusive scan of in[0..n) (n % 4 == 0, 16-B aligned; in and
+// out may alias), uint4 chunks per thread.  Returns the total; ends synced.
+template <int BLOCK>
+__device__ __forceinline__ uint32_t block_excl_scan4(const uint32_t* in, uint32_t* out, int n,
+                                                     uint32_t* wsum) {
+  const int nq = n >> 2;
+  const int per = (nq + BLOCK - 1) / BLOCK;
+  const int t = threadIdx.x;
+  const int q0 = min(nq, t * per), q1 = min(nq, q0 + per);
+  const uint4* in4 = reinterpret_cast<const uint4*>(in);
+  uint4* out4 = reinterpret_cast<uint4*>(out);
+  uint32_t s = 0;
+  for (int q = q0; q < q1; ++q) {
+    const uint4 v = in4[q];
+    s += v.x + v.y + v.z + v.w;
+  }
+  const uint32_t inc = warp_incl_scan(s);
+  const int lane = t & 31, w = t >> 5;
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const uint32_t v = (lane < BLOCK / 32) ? wsum[lane] : 0u;
+    const uint32_t vi = warp_incl_scan(v);
+    if (lane < BLOCK / 32) wsum[lane] = vi - v;
+    if (lane == 31) wsum[32] = vi;
+  }
+  __syncthreads();
+  uint32_t run = wsum[w] + inc - s;
+  for (int q = q0; q < q1; ++q) {
+    const uint4 v = in4[q];
+    uint4 o;
+    o.x = run;
+    o.y = run + v.x;
+    o.z = o.y + v.y;
+    o.w = o.z + v.z;
+    run = o.w + v.w;
+    out4[q] = o;
+  }
+  const uint32_t total = wsum[32];
+  __syncthreads();
+  return total;
+}
+
 // position P's batch (reading D:7): returns [b0, b1).  N < 2^32.
 __device__ __forceinline__ void batch_range(uint32_t P, const DevParams& prm, uint32_t& b0,
                                             uint32_t& b1) {
@@ -107,7 +150,7 @@ __device__ __forceinline__ uint32_t num_batches(const DevParams& prm) {
 // ------------------------------------------------------------------- init
 // X_0 in fp64, rounded to T; state stored in id order.
 template <typename T, int D>
-static __global__ void init_kernel(DevParams P, State<T, D> st, uint64_t id0, uint64_t n, uint32_t kind,
+static __global__ void init_kernel(const __grid_constant__ DevParams P, State<T, D> st, uint64_t id0, uint64_t n, uint32_t kind,
                                    double a0, double a1, double a2, double a3) {
   // mixture centres (<= 64), computed redundantly per block
   __shared__ double cent[64][3];
@@ -194,7 +237,12 @@ static __global__ void advance_kernel(uint64_t* step) { *step += 1; }
 // nb buckets of fixed capacity cap; bucket u holds cnt[u*cstride] records at
 // physical slots [u*cap, u*cap + cnt).  Cursor padding spreads the run-
 // reservation atomics of concurrent CTAs over the L2 slices.
-constexpr uint32_t CUR1_STRIDE = 32, CUR2_STRIDE = 8;
+constexpr uint32_t CUR1_STRIDE = 8, CUR2_STRIDE = 8;
+constexpr uint32_t MAX_SEG = 16384;  // pass-1 segments: 2^b1 << segk <= 2^10 << 4
+
+__device__ __forceinline__ uint32_t out_seg(const DevParams& P, uint32_t dg, uint32_t salt) {
+  return (dg << P.segk) | (salt & P.segmask);
+}
 
 struct Gapped {
   uint32_t cap;           // slots per bucket (multiple of 64)
@@ -220,38 +268,65 @@ static __global__ void gather_gapped_kernel(Gapped g, State<T, D> st, uint64_t i
   }
 }
 
-// single block: pass-1 counts -> prefix1 (exclusive, size nb1+1) and tile table
-// of pass 2; for one-pass layouts the final starts S = prefix of the counts.
-static __global__ void __launch_bounds__(1024) tile_scan_kernel(DevParams P, const uint32_t* __restrict__ cnt1,
+// tiles of pass 2 over nseg segments (counts cnt[v * CUR1_STRIDE]):
+// tile_off[v] = exclusive prefix of ceil(count/tile), tile_off[nseg] = total.
+// One block of 1024 threads, each a run of consecutive segments.
+__device__ __forceinline__ void seg_tile_table(const uint32_t* __restrict__ cnt, uint32_t nseg,
+                                               uint32_t tile, uint32_t* tile_off, uint32_t* ws) {
+  const uint32_t per = (nseg + 1023) / 1024;
+  const uint32_t v0 = min(nseg, threadIdx.x * per), v1 = min(nseg, v0 + per);
+  uint32_t ts = 0;
+  for (uint32_t v = v0; v < v1; ++v) ts += (cnt[(size_t)v * CUR1_STRIDE] + tile - 1) / tile;
+  const uint32_t inc = warp_incl_scan(ts);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 31) ws[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const uint32_t x = ws[lane];
+    const uint32_t xi = warp_incl_scan(x);
+    ws[lane] = xi - x;
+    if (lane == 31) ws[32] = xi;
+  }
+  __syncthreads();
+  uint32_t run = ws[w] + inc - ts;
+  for (uint32_t v = v0; v < v1; ++v) {
+    tile_off[v] = run;
+    run += (cnt[(size_t)v * CUR1_STRIDE] + tile - 1) / tile;
+  }
+  if (threadIdx.x == 0) tile_off[nseg] = ws[32];
+  __syncthreads();
+}
+
+// single block: pass-1 counts (2^b1 digits x K segments) -> prefix1 over the
+// digits (exclusive, size nb1+1) and the tile table of pass 2 over the
+// segments; for one-pass layouts the final starts S = prefix of the counts.
+static __global__ void __launch_bounds__(1024) tile_scan_kernel(const __grid_constant__ DevParams P, const uint32_t* __restrict__ cnt1,
                                                                 uint32_t* prefix1, uint32_t* tile_off,
                                                                 uint32_t* S, uint32_t tile) {
   __shared__ uint32_t a[1025];
-  __shared__ uint32_t t[1025];
   __shared__ uint32_t ws[33];
-  const uint32_t nb = 1u << P.b1;
+  const uint32_t nb = 1u << P.b1, K = 1u << P.segk;
   for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) {
-    const uint32_t c = cnt1[(size_t)i * CUR1_STRIDE];
+    uint32_t c = 0;
+    for (uint32_t k = 0; k < K; ++k) c += cnt1[(size_t)((i << P.segk) | k) * CUR1_STRIDE];
     a[i] = c;
-    t[i] = (c + tile - 1) / tile;
   }
   __syncthreads();
-  block_excl_scan<1024>(a, nb, ws);
-  const uint32_t ntiles = block_excl_scan<1024>(t, nb, ws);
+  const uint32_t total = block_excl_scan<1024>(a, nb, ws);
   for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) {
     prefix1[i] = a[i];
-    tile_off[i] = t[i];
     if (P.b2 == 0) S[i] = a[i];
   }
   if (threadIdx.x == 0) {
-    prefix1[nb] = (uint32_t)P.n;
-    tile_off[nb] = ntiles;
-    if (P.b2 == 0) S[nb] = (uint32_t)P.n;
+    prefix1[nb] = total;
+    if (P.b2 == 0) S[nb] = total;
   }
+  seg_tile_table(cnt1, nb << P.segk, tile, tile_off, ws);
 }
 
 // one block per pass-1 bucket d1: S[d1<<b2 | d2] = prefix1[d1] + excl-scan of
 // the final counts (d1, .)
-static __global__ void __launch_bounds__(512) final_scan_kernel(DevParams P, const uint32_t* __restrict__ cnt2,
+static __global__ void __launch_bounds__(512) final_scan_kernel(const __grid_constant__ DevParams P, const uint32_t* __restrict__ cnt2,
                                                                 const uint32_t* __restrict__ prefix1,
                                                                 uint32_t* S) {
   __shared__ uint32_t a[1024];
@@ -291,7 +366,7 @@ __device__ __forceinline__ bool gapped_tile(const uint32_t* __restrict__ tile_of
 // staged in shared memory by digit so each reserved run is written coalesced.
 // Order inside a bucket is irrelevant: the bucket step sorts exactly.
 template <typename T, int D, int LEVEL, int BLOCK, int ITEMS>
-static __global__ void __launch_bounds__(BLOCK) scatter_kernel(DevParams P, State<T, D> src,
+static __global__ void __launch_bounds__(BLOCK) scatter_kernel(const __grid_constant__ DevParams P, State<T, D> src,
                                                                State<T, D> dst, uint32_t* cur,
                                                                uint32_t dcap,
                                                                const uint32_t* __restrict__ cnt1,
@@ -316,7 +391,7 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(DevParams P, Stat
     sh = 32u - P.b1;
     sbase = 0;
   } else {
-    if (!gapped_tile(tile_off, cnt1, 1u << P.b1, blockIdx.x, TILE, u, lo, hi)) return;
+    if (!gapped_tile(tile_off, cnt1, (1u << P.b1) << P.segk, blockIdx.x, TILE, u, lo, hi)) return;
     bits = P.b2;
     sh = 32u - P.b1 - P.b2;
     sbase = u * scap;
@@ -325,7 +400,9 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(DevParams P, Stat
   const uint32_t nbins = 1u << bits, mask = nbins - 1;
   // first destination bucket: final buckets of this rank's pass-1 bucket
   // (segment u of the received pass-1 data on a partitioned system)
-  const uint32_t dbase0 = (LEVEL == 1) ? 0u : ((u & P.nb1_loc_mask) << P.b2);
+  const uint32_t dbase0 = (LEVEL == 1) ? 0u : (((u >> P.segk) & P.nb1_loc_mask) << P.b2);
+  // destination bucket of digit dg: level 1 writes output segments
+  auto dest = [&](uint32_t dg) { return LEVEL == 1 ? out_seg(P, dg, blockIdx.x) : dbase0 + dg; };
   for (uint32_t i = threadIdx.x; i < nbins; i += BLOCK) hist[i] = 0;
   __syncthreads();
 
@@ -356,7 +433,7 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(DevParams P, Stat
   // reserve runs in the destination buckets, then local exclusive offsets
   for (uint32_t i = threadIdx.x; i < nbins; i += BLOCK) {
     const uint32_t h = hist[i];
-    gbase[i] = h ? atomicAdd(&cur[(size_t)(dbase0 + i) * CS], h) : 0u;
+    gbase[i] = h ? atomicAdd(&cur[(size_t)dest(i) * CS], h) : 0u;
   }
   block_excl_scan<BLOCK>(hist, nbins, wsum);  // hist -> local offsets
 #pragma unroll
@@ -380,11 +457,132 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(DevParams P, Stat
       atomicExch(P.capacity_err, 1u);
       continue;
     }
-    const uint32_t g = (dbase0 + dg) * dcap + slot;
+    const uint32_t g = dest(dg) * dcap + slot;
     dst.id[g] = st_id[j];
     dst.key[g] = st_key[j];
 #pragma unroll
     for (int c = 0; c < D; ++c) dst.x[c][g] = st_x[c * TILE + j];
+  }
+}
+
+// ------------------------------------------- persistent pass-2 splitter
+// Same contract as scatter_kernel<LEVEL 2>: tiles of the pass-1 buckets
+// (segments) -> final buckets by the next b2 key bits.  One CTA per SM loops
+// over tiles with double-buffered TMA loads; the output permutation goes
+// through a u16 index (no staging copy): slot j of the tile's digit-ordered
+// output reads record inv[j] from the stage and the runs are written
+// coalesced into the reserved ranges of the final buckets.
+template <typename T, int D, int TILE> __host__ __device__ constexpr size_t split_stage_bytes() {
+  return ((size_t)TILE * (8 + D * sizeof(T)) + 127) & ~(size_t)127;
+}
+template <typename T, int D, int TILE> __host__ __device__ constexpr size_t split_smem_bytes() {
+  return (3 * 1024 + 64) * 4 + 64 + 2 * split_stage_bytes<T, D, TILE>() + (size_t)TILE * 4 + (size_t)TILE * 2;
+}
+
+struct TileInfo { uint32_t u, lo, hi, pad; };
+
+template <typename T, int D, int TILE>
+__device__ __forceinline__ void split_stage_load(State<T, D> src, uint32_t base, uint32_t cnt,
+                                                 unsigned char* stg, uint64_t* bar, uint64_t pol) {
+  uint32_t* id_s = reinterpret_cast<uint32_t*>(stg);
+  uint32_t* key_s = id_s + TILE;
+  T* x_s = reinterpret_cast<T*>(key_s + TILE);
+  constexpr uint32_t AX = 16 / sizeof(T);
+  const uint32_t bytes_i = ((cnt + 3) & ~3u) * 4;
+  const uint32_t bytes_x = ((cnt + AX - 1) & ~(AX - 1)) * (uint32_t)sizeof(T);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  mbar_expect_tx(bar, 2 * bytes_i + D * bytes_x);
+  if (cnt) {
+    bulk_g2s_stream(id_s, src.id + base, bytes_i, bar, pol);
+    bulk_g2s_stream(key_s, src.key + base, bytes_i, bar, pol);
+#pragma unroll
+    for (int c = 0; c < D; ++c) bulk_g2s_stream(x_s + (size_t)c * TILE, src.x[c] + base, bytes_x, bar, pol);
+  }
+}
+
+template <typename T, int D, int BLOCK, int TILE>
+static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) split_persist_kernel(const __grid_constant__ DevParams P,
+                                                                        State<T, D> src, State<T, D> dst,
+                                                                        uint32_t* cur, uint32_t dcap,
+                                                                        const uint32_t* __restrict__ cnt1,
+                                                                        const uint32_t* __restrict__ tile_off,
+                                                                        uint32_t scap) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw);  // 1024
+  uint32_t* off = hist + 1024;                             // 1024
+  uint32_t* gbase = off + 1024;                            // 1024
+  uint32_t* wsum = gbase + 1024;                           // 64
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);  // 2
+  TileInfo* tinfo = reinterpret_cast<TileInfo*>(bar + 2);  // 2
+  unsigned char* stg0 = smem_raw + (((3 * 1024 + 64) * 4 + 64 + 127) & ~127);
+  constexpr size_t SBY = split_stage_bytes<T, D, TILE>();
+  uint32_t* rk = reinterpret_cast<uint32_t*>(stg0 + 2 * SBY);  // digit<<16 | rank, by element
+  uint16_t* inv = reinterpret_cast<uint16_t*>(rk + TILE);      // output slot -> element
+  const uint32_t nseg = (1u << P.b1) << P.segk;
+  const uint32_t ntiles = tile_off[nseg];
+  const uint32_t bits = P.b2, sh = 32u - P.b1 - P.b2, nbins = 1u << bits, mask = nbins - 1u;
+  const uint32_t tid = threadIdx.x;
+  uint64_t pol = 0;
+  auto issue = [&](uint32_t t, uint32_t st) {  // thread 0
+    TileInfo ti{0u, 0u, 0u, 0u};
+    if (t < ntiles) gapped_tile(tile_off, cnt1, nseg, t, TILE, ti.u, ti.lo, ti.hi);
+    tinfo[st] = ti;
+    split_stage_load<T, D, TILE>(src, ti.u * scap + ti.lo, ti.hi - ti.lo, stg0 + st * SBY, &bar[st], pol);
+  };
+  if (tid == 0) {
+    pol = l2_evict_first_policy();
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
+  }
+  __syncthreads();
+  uint32_t phase = 0, it = 0;
+  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const uint32_t s = it & 1u;
+    if (tid == 0 && t + gridDim.x < ntiles) issue(t + gridDim.x, s ^ 1u);
+    for (uint32_t i = tid; i < nbins; i += BLOCK) hist[i] = 0;
+    mbar_wait(&bar[s], (phase >> s) & 1u);
+    phase ^= 1u << s;
+    const TileInfo ti = tinfo[s];
+    const uint32_t cnt = ti.hi - ti.lo;
+    const uint32_t dbase0 = ((ti.u >> P.segk) & P.nb1_loc_mask) << P.b2;
+    const unsigned char* stg = stg0 + s * SBY;
+    const uint32_t* id_s = reinterpret_cast<const uint32_t*>(stg);
+    const uint32_t* key_s = id_s + TILE;
+    const T* x_s = reinterpret_cast<const T*>(key_s + TILE);
+    __syncthreads();
+    for (uint32_t e = tid; e < cnt; e += BLOCK) {
+      const uint32_t dg = (key_s[e] >> sh) & mask;
+      rk[e] = (dg << 16) | atomicAdd(&hist[dg], 1u);
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < nbins; i += BLOCK) {
+      const uint32_t h = hist[i];
+      off[i] = h;
+      gbase[i] = h ? atomicAdd(&cur[(size_t)(dbase0 + i) * CUR2_STRIDE], h) : 0u;
+    }
+    __syncthreads();
+    block_excl_scan<BLOCK>(off, nbins, wsum);
+    for (uint32_t e = tid; e < cnt; e += BLOCK) {
+      const uint32_t v = rk[e];
+      inv[off[v >> 16] + (v & 0xffffu)] = (uint16_t)e;
+    }
+    __syncthreads();
+    for (uint32_t j = tid; j < cnt; j += BLOCK) {
+      const uint32_t e = inv[j];
+      const uint32_t dg = rk[e] >> 16;
+      const uint32_t slot = gbase[dg] + (j - off[dg]);
+      if (slot >= dcap) {  // bucket capacity exceeded (probability ~1e-30): fail loudly
+        atomicExch(P.capacity_err, 1u);
+        continue;
+      }
+      const size_t g = (size_t)(dbase0 + dg) * dcap + slot;
+      dst.id[g] = id_s[e];
+      dst.key[g] = key_s[e];
+#pragma unroll
+      for (int c = 0; c < D; ++c) dst.x[c][g] = x_s[(size_t)c * TILE + e];
+    }
+    __syncthreads();  // stage s, rk, inv free
   }
 }
 
@@ -504,7 +702,7 @@ template <typename T, int D> __host__ __device__ constexpr size_t bucket_smem_by
 }
 
 template <typename T, int D, int KK, int INTEG, int BLOCK>
-static __global__ void __launch_bounds__(BLOCK) bucket_step_kernel(DevParams P, State<T, D> src,
+static __global__ void __launch_bounds__(BLOCK) bucket_step_kernel(const __grid_constant__ DevParams P, State<T, D> src,
                                                                    State<T, D> dst,
                                                                    const uint32_t* __restrict__ S) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -606,7 +804,7 @@ template <typename T, int D> __host__ __device__ constexpr size_t resident_smem_
 }
 
 template <typename T, int D, int KK, int INTEG, int BLOCK>
-static __global__ void __launch_bounds__(BLOCK) resident_kernel(DevParams P, State<T, D> src,
+static __global__ void __launch_bounds__(BLOCK) resident_kernel(const __grid_constant__ DevParams P, State<T, D> src,
                                                                 State<T, D> dst, uint32_t nsteps,
                                                                 uint64_t* stepp) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -693,7 +891,7 @@ static __global__ void __launch_bounds__(BLOCK) resident_kernel(DevParams P, Sta
 // physical slot b*cap + (P - S[b]).  Results are appended to the step-(m+1)
 // buckets of `dst` (capacity ocap, cursors cur_next).
 template <typename T, int D, int KK, int INTEG>
-static __global__ void __launch_bounds__(256) straddle_kernel(DevParams P, State<T, D> strad,
+static __global__ void __launch_bounds__(256) straddle_kernel(const __grid_constant__ DevParams P, State<T, D> strad,
                                                               uint32_t cap,
                                                               const uint32_t* __restrict__ S,
                                                               State<T, D> dst, uint32_t ocap,
@@ -780,10 +978,10 @@ static __global__ void __launch_bounds__(256) straddle_kernel(DevParams P, State
   const uint32_t osh = 32u - P.b1;
   for (uint32_t q = lane; q < sz; q += 32, ++k) {
     const uint32_t kn = shuffle_key(P, idv[k], m + 1);
-    const uint32_t dg = kn >> osh;
-    const uint32_t slot = atomicAdd(&cur_next[(size_t)dg * CUR1_STRIDE], 1u);
+    const uint32_t v = out_seg(P, kn >> osh, warp);
+    const uint32_t slot = atomicAdd(&cur_next[(size_t)v * CUR1_STRIDE], 1u);
     if (slot >= ocap) { atomicExch(P.capacity_err, 1u); continue; }
-    const uint32_t g = dg * ocap + slot;
+    const uint32_t g = v * ocap + slot;
     dst.id[g] = idv[k];
     dst.key[g] = kn;
 #pragma unroll
@@ -807,50 +1005,50 @@ template <typename T, int D> __host__ __device__ constexpr size_t halo_bytes() {
 // n_r) and the tile table.  Flags capacity_err = 2 if the rank holds fewer
 // than p particles (the halo exchange assumes a crossing batch touches only
 // two ranks).
-static __global__ void __launch_bounds__(1024) part_scan_kernel(DevParams P, const uint32_t* __restrict__ M,
+static __global__ void __launch_bounds__(1024) part_scan_kernel(const __grid_constant__ DevParams P, const uint32_t* __restrict__ M,
                                                                 uint32_t G, uint32_t rank, uint32_t* cnt1,
                                                                 uint32_t* prefix1, uint32_t* tile_off,
                                                                 uint32_t tile) {
   __shared__ uint32_t a[1025];
-  __shared__ uint32_t t[1025];
   __shared__ uint32_t ws[33];
   __shared__ uint32_t o_r;
-  const uint32_t nb1 = 1u << P.b1, nl = nb1 / G;
+  // nseg = 2^b1 << segk segments per rank row of M; this rank's slice of a
+  // row is nls = nseg/G segments = nlb = 2^b1/G local pass-1 buckets x K
+  const uint32_t nseg = (1u << P.b1) << P.segk, nls = nseg / G, nlb = nls >> P.segk;
+  const uint32_t K = 1u << P.segk;
   if (threadIdx.x == 0) o_r = 0;
   __syncthreads();
-  for (uint32_t v = threadIdx.x; v < nb1; v += blockDim.x) {
-    const uint32_t s = v / nl, u = v - s * nl;
-    const uint32_t c = M[(size_t)s * nb1 + rank * nl + u];
-    cnt1[(size_t)v * CUR1_STRIDE] = c;
-    t[v] = (c + tile - 1) / tile;
+  for (uint32_t v = threadIdx.x; v < nseg; v += blockDim.x) {  // received segment v = s*nls + j
+    const uint32_t s = v / nls, j = v - s * nls;
+    cnt1[(size_t)v * CUR1_STRIDE] = M[(size_t)s * nseg + rank * nls + j];
   }
-  for (uint32_t u = threadIdx.x; u < nl; u += blockDim.x) {
+  for (uint32_t u = threadIdx.x; u < nlb; u += blockDim.x) {
     uint32_t c = 0;
-    for (uint32_t s = 0; s < G; ++s) c += M[(size_t)s * nb1 + rank * nl + u];
+    for (uint32_t s = 0; s < G; ++s)
+      for (uint32_t k = 0; k < K; ++k) c += M[(size_t)s * nseg + rank * nls + (u << P.segk) + k];
     a[u] = c;
   }
-  {  // O_r = all records of the ranks below (their pass-1 buckets, every source)
+  {  // O_r = all records of the ranks below (their segments, every source)
     uint32_t part = 0;
-    const uint32_t below = rank * nl;
+    const uint32_t below = rank * nls;
     for (uint32_t q = threadIdx.x; q < G * below; q += blockDim.x) {
       const uint32_t s = q / below, j = q - s * below;
-      part += M[(size_t)s * nb1 + j];
+      part += M[(size_t)s * nseg + j];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
     if ((threadIdx.x & 31) == 0 && part) atomicAdd(&o_r, part);
   }
   __syncthreads();
-  const uint32_t nloc = block_excl_scan<1024>(a, nl, ws);
-  const uint32_t ntiles = block_excl_scan<1024>(t, nb1, ws);
+  const uint32_t nloc = block_excl_scan<1024>(a, nlb, ws);
   const uint32_t O = o_r;
-  for (uint32_t u = threadIdx.x; u < nl; u += blockDim.x) prefix1[u] = O + a[u];
-  for (uint32_t v = threadIdx.x; v < nb1; v += blockDim.x) tile_off[v] = t[v];
+  for (uint32_t u = threadIdx.x; u < nlb; u += blockDim.x) prefix1[u] = O + a[u];
   if (threadIdx.x == 0) {
-    prefix1[nl] = O + nloc;
-    tile_off[nb1] = ntiles;
+    prefix1[nlb] = O + nloc;
     if (nloc < P.p) atomicExch(P.capacity_err, 2u);
   }
+  __syncthreads();
+  seg_tile_table(cnt1, nseg, tile, tile_off, ws);
 }
 
 // The batch crossing this rank's end E = S[nbuckets] (global positions
@@ -858,7 +1056,7 @@ static __global__ void __launch_bounds__(1024) part_scan_kernel(DevParams P, con
 // bucket kernels) is owned by rank+1: copy it to the halo buffer
 // {u32 t; ids[HALO_MAX]; x[HALO_MAX][D]}.
 template <typename T, int D>
-static __global__ void halo_extract_kernel(DevParams P, State<T, D> strad, uint32_t cap,
+static __global__ void halo_extract_kernel(const __grid_constant__ DevParams P, State<T, D> strad, uint32_t cap,
                                            const uint32_t* __restrict__ S, unsigned char* halo) {
   const uint32_t E = S[P.nbuckets];
   uint32_t t = 0, b0 = E, b1 = E;
@@ -883,7 +1081,7 @@ static __global__ void halo_extract_kernel(DevParams P, State<T, D> strad, uint3
 // Received halo (rank-1's trailing records of the crossing batch) -> bucket -1
 // of the local final layout, S[-1] = S[0] - t.
 template <typename T, int D>
-static __global__ void halo_place_kernel(DevParams P, State<T, D> strad, uint32_t cap, uint32_t* S,
+static __global__ void halo_place_kernel(const __grid_constant__ DevParams P, State<T, D> strad, uint32_t cap, uint32_t* S,
                                          const unsigned char* __restrict__ halo) {
   const uint32_t t = *reinterpret_cast<const uint32_t*>(halo);
   const uint32_t* hid = reinterpret_cast<const uint32_t*>(halo + 16);
@@ -904,16 +1102,16 @@ static __global__ void pack_counts_kernel(const uint32_t* __restrict__ cur, uint
 
 // gather from the received segments of a partitioned rank (holes skipped)
 template <typename T, int D>
-static __global__ void gather_part_kernel(DevParams P, State<T, D> st, uint32_t cap1,
+static __global__ void gather_part_kernel(const __grid_constant__ DevParams P, State<T, D> st, uint32_t cap1,
                                           const uint32_t* __restrict__ M, uint32_t G, uint32_t rank,
                                           uint64_t i0, uint64_t i1, T* __restrict__ out) {
-  const uint32_t nb1 = 1u << P.b1, nl = nb1 / G;
-  const uint64_t total = (uint64_t)nb1 * cap1;
+  const uint32_t nseg = (1u << P.b1) << P.segk, nls = nseg / G;
+  const uint64_t total = (uint64_t)nseg * cap1;
   for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < total;
        q += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t v = (uint32_t)(q / cap1), e = (uint32_t)(q - (uint64_t)v * cap1);
-    const uint32_t s = v / nl, u = v - s * nl;
-    if (e >= M[(size_t)s * nb1 + rank * nl + u]) continue;
+    const uint32_t s = v / nls, j = v - s * nls;
+    if (e >= M[(size_t)s * nseg + rank * nls + j]) continue;
     const uint64_t id = st.id[q];
     if (id >= i0 && id < i1) {
 #pragma unroll
@@ -977,10 +1175,10 @@ __device__ __noinline__ void fused_big_path(const DevParams& P, State<T, D> src,
     if (b0 >= s0 && b1 <= s0 + n) {
       const uint32_t id = src.id[sb + q];
       const uint32_t kn = shuffle_key(P, id, m + 1);
-      const uint32_t dg = kn >> osh;
-      const uint32_t s = atomicAdd(&cur_next[(size_t)dg * CUR1_STRIDE], 1u);
+      const uint32_t v = out_seg(P, kn >> osh, blockIdx.x);
+      const uint32_t s = atomicAdd(&cur_next[(size_t)v * CUR1_STRIDE], 1u);
       if (s >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
-      const uint32_t g = dg * dcap + s;
+      const uint32_t g = v * dcap + s;
       dst.id[g] = id;
       dst.key[g] = kn;
 #pragma unroll
@@ -1047,11 +1245,9 @@ __device__ __forceinline__ void fused_output(const DevParams& P, State<T, D> dst
   const uint32_t nout = 1u << P.b1;
   for (uint32_t i = threadIdx.x; i < nout; i += BLOCK) {
     const uint32_t h = cnt[i];
-    off[i] = h;
-    gbase[i] = h ? atomicAdd(&cur_next[(size_t)i * CUR1_STRIDE], h) : 0u;
+    gbase[i] = h ? atomicAdd(&cur_next[(size_t)out_seg(P, i, blockIdx.x) * CUR1_STRIDE], h) : 0u;
   }
-  __syncthreads();
-  const uint32_t total = block_excl_scan<BLOCK>(off, nout, wsum);
+  const uint32_t total = block_excl_scan4<BLOCK>(cnt, off, nout, wsum);
   for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
     const uint32_t t = tb[e];
     if (t != 0xffffffffu) inv[off[t >> 16] + (t & 0xffffu)] = (uint16_t)e;
@@ -1062,7 +1258,7 @@ __device__ __forceinline__ void fused_output(const DevParams& P, State<T, D> dst
     const uint32_t dg = tb[e] >> 16;
     const uint32_t slot = gbase[dg] + (j - off[dg]);
     if (slot >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
-    const uint32_t g = dg * dcap + slot;
+    const uint32_t g = out_seg(P, dg, blockIdx.x) * dcap + slot;
     dst.id[g] = id_l[e];
     dst.key[g] = ta[e];
 #pragma unroll
@@ -1087,7 +1283,7 @@ template <typename T, int D> __host__ __device__ constexpr size_t fused_smem_byt
 }
 
 template <typename T, int D, int KK, int INTEG, int BLOCK>
-static __global__ void __launch_bounds__(BLOCK) bucket_fused_kernel(DevParams P, State<T, D> src,
+static __global__ void __launch_bounds__(BLOCK) bucket_fused_kernel(const __grid_constant__ DevParams P, State<T, D> src,
                                                                     uint32_t scap,
                                                                     const uint32_t* __restrict__ S,
                                                                     State<T, D> dst, uint32_t dcap,
@@ -1306,12 +1502,13 @@ __device__ __forceinline__ void pair_update(const DevParams& P, uint32_t m, cons
 
 
 template <typename T, int D, int KK, int INTEG, int BLOCK, int ITEMS>
-static __global__ void __launch_bounds__(BLOCK) bucket_pair_kernel(DevParams P, State<T, D> src,
+static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) bucket_pair_kernel(const __grid_constant__ DevParams P, State<T, D> src,
                                                                    uint32_t scap,
                                                                    const uint32_t* __restrict__ S,
                                                                    State<T, D> dst, uint32_t dcap,
                                                                    uint32_t* __restrict__ cur_next) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  RBM_PROF_BEGIN(P);
   const uint32_t b = blockIdx.x;
   const uint32_t s0 = S[b], n = S[b + 1] - s0, sb = b * scap;
   if (n == 0) return;
@@ -1324,7 +1521,7 @@ static __global__ void __launch_bounds__(BLOCK) bucket_pair_kernel(DevParams P, 
   uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);
   const uint32_t cap = P.cap;
   const uint32_t m = (uint32_t)*P.step;
-  for (uint32_t i = threadIdx.x; i < nsb; i += BLOCK) cnt[i] = 0;
+  for (uint32_t i = threadIdx.x; i < nsb / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
   if (n > cap) {
     fused_big_path<T, D, KK, INTEG, BLOCK>(P, src, dst, cur_next, s0, sb, n, m, dcap, cnt, off, wsum);
     return;
@@ -1345,6 +1542,7 @@ static __global__ void __launch_bounds__(BLOCK) bucket_pair_kernel(DevParams P, 
   load_bucket<T, D>(src, sb, n, id_l, key_l, xr, xst, bar);
   __syncthreads();
   mbar_wait(bar, 0);
+  RBM_PROF(P, 0);
   const SX<T> xs{xr, xst};
 
   // 1-3. exact (key, id) sort: counting sort on SB sub-digit bits + rank in sub-bucket
@@ -1362,15 +1560,16 @@ static __global__ void __launch_bounds__(BLOCK) bucket_pair_kernel(DevParams P, 
     }
   }
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < nsb; i += BLOCK) off[i] = cnt[i];
-  __syncthreads();
-  block_excl_scan<BLOCK>(off, nsb, wsum);
+  RBM_PROF(P, 1);
+  block_excl_scan4<BLOCK>(cnt, off, nsb, wsum);
+  RBM_PROF(P, 2);
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t e = k * BLOCK + threadIdx.x;
     if (e < n) ks[off[rs[k] >> 16] + (rs[k] & 0xffffu)] = rc[k];
   }
   __syncthreads();
+  RBM_PROF(P, 3);
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t e = k * BLOCK + threadIdx.x;
@@ -1378,17 +1577,23 @@ static __global__ void __launch_bounds__(BLOCK) bucket_pair_kernel(DevParams P, 
       const uint32_t sd = rs[k] >> 16;
       const uint32_t a = off[sd], c = cnt[sd];
       uint32_t r = a;
-      for (uint32_t i = a; i < a + c; ++i) r += (ks[i] < rc[k]) ? 1u : 0u;
+      if (c > 1) {  // sub-buckets hold ~1 element: a short predicated scan
+#pragma unroll
+        for (uint32_t i = 0; i < 4; ++i)
+          if (i < c) r += (ks[a + i] < rc[k]) ? 1u : 0u;
+        for (uint32_t i = 4; i < c; ++i) r += (ks[a + i] < rc[k]) ? 1u : 0u;
+      }
       ord[r] = (uint16_t)e;
     }
   }
   __syncthreads();
+  RBM_PROF(P, 4);
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {  // ks is dead: reuse as digit|slot (straddlers keep ~0)
     const uint32_t e = k * BLOCK + threadIdx.x;
     if (e < n) tb[e] = 0xffffffffu;
   }
-  for (uint32_t i = threadIdx.x; i < 1024u; i += BLOCK) cnt[i] = 0;
+  for (uint32_t i = threadIdx.x; i < (1u << P.b1) / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
   if (P.dbg_order)
     for (uint32_t q = threadIdx.x; q < n; q += BLOCK) P.dbg_order[s0 + q] = id_l[ord[q]];
   // interior pairs: even global starts in [s0, end), end excludes a final triple (N odd)
@@ -1400,10 +1605,12 @@ static __global__ void __launch_bounds__(BLOCK) bucket_pair_kernel(DevParams P, 
   const uint32_t covered = head + 2 * npairs;            // [head, covered) are interior
   const bool triple = (N & 1u) && (pend >= s0) && (N <= s0 + n);
   __syncthreads();
+  RBM_PROF(P, 5);
   // straddlers: unchanged, to their sorted places in the own gapped range
-  for (uint32_t q = threadIdx.x; q < n; q += BLOCK) {
+  for (uint32_t t = threadIdx.x; t < head + (n - covered); t += BLOCK) {
+    const uint32_t q = t < head ? t : covered + (t - head);
     const bool in_triple = triple && (s0 + q >= pend);
-    if ((q < head || q >= covered) && !in_triple) {
+    if (!in_triple) {
       const uint32_t e = ord[q];
       src.id[sb + q] = id_l[e];
 #pragma unroll
@@ -1438,13 +1645,218 @@ static __global__ void __launch_bounds__(BLOCK) bucket_pair_kernel(DevParams P, 
   if (triple && threadIdx.x == 0)  // the remainder batch of size 3 (N odd), EM only
     serial_batch<T, D, KK, INTEG>(P, m, pend - s0, n, ord, id_l, xs, ta, tb, cnt, osh);
   __syncthreads();
+  RBM_PROF(P, 6);
   fused_output<T, D, BLOCK>(P, dst, dcap, cur_next, n, id_l, ta, tb, xs, cnt, off, gbase, inv, wsum);
+  RBM_PROF(P, 7);
+  if (P.prof && threadIdx.x == 0) atomicAdd(&P.prof[63], 1ull);
+}
+
+// -------------------------------- persistent fused bucket step, p = 2
+// Same contract and arithmetic as bucket_pair_kernel, restructured for the
+// SM: one CTA per SM loops over buckets b = blockIdx.x, += gridDim.x with the
+// TMA loads double-buffered (bucket b + gridDim.x is in flight while b is
+// sorted and stepped), so neither the load latency nor a per-bucket launch
+// prologue is exposed.
+template <typename T, int D> __host__ __device__ constexpr size_t stage_bytes(uint32_t cap) {
+  return ((size_t)(cap + 8) * 8 + (size_t)D * (((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15) + 127) &
+         ~(size_t)127;
+}
+template <typename T, int D> __host__ __device__ constexpr size_t persist_smem_bytes(uint32_t cap,
+                                                                                    uint32_t SB) {
+  return (((size_t)(2 * (SB > 10 ? (1u << SB) : 1024u) + 1024 + 64) * 4 + 16 + 127) & ~(size_t)127)
+         + 2 * stage_bytes<T, D>(cap)                      // two TMA stages: ids, keys, x
+         + (size_t)cap * 4                                 // composites -> digit|slot
+         + (((size_t)cap * 4 + 15) & ~(size_t)15);         // ord, inv (u16)
+}
+
+// thread 0: TMA loads of one bucket into a stage; always one arrival on bar
+// (expect_tx 0 when nothing is loaded), so stage phases advance per use
+template <typename T, int D>
+__device__ __forceinline__ void stage_load(State<T, D> src, uint32_t sb, uint32_t n, bool load,
+                                           unsigned char* stg, uint32_t cap, uint64_t* bar, uint64_t pol) {
+  uint32_t* id_s = reinterpret_cast<uint32_t*>(stg);
+  uint32_t* key_s = id_s + cap + 8;
+  T* x_s = reinterpret_cast<T*>(key_s + cap + 8);
+  const uint32_t xst = (uint32_t)((((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15) / sizeof(T));
+  constexpr uint32_t AX = 16 / sizeof(T);
+  const uint32_t bytes_i = load ? ((n + 3) & ~3u) * 4 : 0u;
+  const uint32_t bytes_x = load ? ((n + AX - 1) & ~(AX - 1)) * (uint32_t)sizeof(T) : 0u;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes before async overwrite
+  mbar_expect_tx(bar, 2 * bytes_i + D * bytes_x);
+  if (load && n) {
+    bulk_g2s_stream(id_s, src.id + sb, bytes_i, bar, pol);
+    bulk_g2s_stream(key_s, src.key + sb, bytes_i, bar, pol);
+#pragma unroll
+    for (int c = 0; c < D; ++c) bulk_g2s_stream(x_s + (size_t)c * xst, src.x[c] + sb, bytes_x, bar, pol);
+  }
+}
+
+template <typename T, int D, int KK, int INTEG, int BLOCK, int ITEMS>
+static __global__ void __launch_bounds__(BLOCK, 1) pair_persist_kernel(const __grid_constant__ DevParams P,
+                                                                       State<T, D> src, uint32_t scap,
+                                                                       const uint32_t* __restrict__ S,
+                                                                       State<T, D> dst, uint32_t dcap,
+                                                                       uint32_t* __restrict__ cur_next) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const uint32_t nsb = 1u << P.SB;
+  const uint32_t ncnt = nsb > 1024u ? nsb : 1024u;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* off = cnt + ncnt;
+  uint32_t* gbase = off + ncnt;
+  uint32_t* wsum = gbase + 1024;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);
+  const uint32_t cap = P.cap;
+  unsigned char* stg0 = smem_raw + (((size_t)(2 * ncnt + 1024 + 64) * 4 + 16 + 127) & ~(size_t)127);
+  const size_t SBY = stage_bytes<T, D>(cap);
+  uint32_t* ks = reinterpret_cast<uint32_t*>(stg0 + 2 * SBY);  // composites; then digit<<16|slot
+  uint32_t* tb = ks;
+  uint16_t* ord = reinterpret_cast<uint16_t*>(ks + cap);
+  uint16_t* inv = ord + cap;
+  const uint32_t xst = (uint32_t)((((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15) / sizeof(T));
+  const uint32_t m = (uint32_t)*P.step;
+  const uint32_t nb = P.nbuckets;
+  const uint32_t tid = threadIdx.x;
+  uint64_t pol = 0;
+  if (tid == 0) {
+    pol = l2_evict_first_policy();
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+  }
+  __syncthreads();
+  if (tid == 0 && blockIdx.x < nb) {
+    const uint32_t b = blockIdx.x, n = S[b + 1] - S[b];
+    stage_load<T, D>(src, b * scap, n, n <= cap, stg0, cap, &bar[0], pol);
+  }
+  uint32_t phase = 0;  // bit s = parity of stage s's next completion
+  const uint32_t shsb = 32u - P.B - P.SB;
+  const uint32_t lowmask = (P.lowbits >= 32u) ? 0xffffffffu : ((1u << P.lowbits) - 1u);
+  const uint32_t N = (uint32_t)P.n;
+  const uint32_t pend = (N & 1u) ? N - 3u : N;
+  const uint32_t osh = 32u - P.b1;
+  const uint32_t nout = 1u << P.b1;
+  uint32_t it = 0;
+  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x, ++it) {
+    const uint32_t s = it & 1u;
+    const uint32_t bn = b + gridDim.x;
+    if (tid == 0 && bn < nb) {  // prefetch the next bucket into the other stage
+      const uint32_t nn = S[bn + 1] - S[bn];
+      stage_load<T, D>(src, bn * scap, nn, nn <= cap, stg0 + (s ^ 1u) * SBY, cap, &bar[s ^ 1u], pol);
+    }
+    const uint32_t s0 = S[b], n = S[b + 1] - s0, sb = b * scap;
+    unsigned char* stg = stg0 + s * SBY;
+    uint32_t* id_l = reinterpret_cast<uint32_t*>(stg);
+    uint32_t* key_l = id_l + cap + 8;  // key_m by e; then key_{m+1} by e
+    uint32_t* ta = key_l;
+    const SX<T> xs{reinterpret_cast<T*>(key_l + cap + 8), xst};
+    mbar_wait(&bar[s], (phase >> s) & 1u);
+    phase ^= 1u << s;
+    if (n == 0) {  // keep thread 0 within one stage phase of the others
+      __syncthreads();
+      continue;
+    }
+    for (uint32_t i = tid; i < nsb; i += BLOCK) cnt[i] = 0;
+    if (n > cap) {
+      __syncthreads();
+      fused_big_path<T, D, KK, INTEG, BLOCK>(P, src, dst, cur_next, s0, sb, n, m, dcap, cnt, off, wsum);
+      __syncthreads();
+      continue;
+    }
+    __syncthreads();
+    // 1-3. exact (key, id) sort: counting sort on SB sub-digit bits + rank in sub-bucket
+    uint32_t rc[ITEMS], rs[ITEMS];
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      const uint32_t e = k * BLOCK + tid;
+      if (e < n) {
+        const uint32_t key = key_l[e];
+        const uint32_t sd = (key >> shsb) & (nsb - 1u);
+        rc[k] = ((key & lowmask) << P.idbits) | id_l[e];
+        rs[k] = (sd << 16) | atomicAdd(&cnt[sd], 1u);
+      }
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < nsb; i += BLOCK) off[i] = cnt[i];
+    __syncthreads();
+    block_excl_scan<BLOCK>(off, nsb, wsum);
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      const uint32_t e = k * BLOCK + tid;
+      if (e < n) ks[off[rs[k] >> 16] + (rs[k] & 0xffffu)] = rc[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      const uint32_t e = k * BLOCK + tid;
+      if (e < n) {
+        const uint32_t sd = rs[k] >> 16;
+        const uint32_t a = off[sd], c = cnt[sd];
+        uint32_t r = a;
+        for (uint32_t i = a; i < a + c; ++i) r += (ks[i] < rc[k]) ? 1u : 0u;
+        ord[r] = (uint16_t)e;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {  // ks is dead: reuse as digit|slot (straddlers keep ~0)
+      const uint32_t e = k * BLOCK + tid;
+      if (e < n) tb[e] = 0xffffffffu;
+    }
+    for (uint32_t i = tid; i < nout; i += BLOCK) cnt[i] = 0;
+    if (P.dbg_order)
+      for (uint32_t q = tid; q < n; q += BLOCK) P.dbg_order[s0 + q] = id_l[ord[q]];
+    // interior pairs: even global starts in [s0, end), end excludes a final triple (N odd)
+    const uint32_t head = s0 & 1u;
+    const uint32_t lim = (min(s0 + n, pend) > s0) ? min(s0 + n, pend) - s0 : 0u;
+    const uint32_t npairs = (lim > head) ? (lim - head) / 2 : 0u;
+    const uint32_t covered = head + 2 * npairs;
+    const bool triple = (N & 1u) && (pend >= s0) && (N <= s0 + n);
+    __syncthreads();
+    // straddlers: unchanged, to their sorted places in the own gapped range
+    for (uint32_t q = tid; q < n; q += BLOCK) {
+      const bool in_triple = triple && (s0 + q >= pend);
+      if ((q < head || q >= covered) && !in_triple) {
+        const uint32_t e = ord[q];
+        src.id[sb + q] = id_l[e];
+#pragma unroll
+        for (int c = 0; c < D; ++c) src.x[c][sb + q] = xs.at(c, e);
+      }
+    }
+    // 4. one thread per pair
+    constexpr int PITEMS = (ITEMS + 1) / 2;
+#pragma unroll
+    for (int k = 0; k < PITEMS; ++k) {
+      const uint32_t j = k * BLOCK + tid;
+      if (j < npairs) {
+        const uint32_t q = head + 2 * j;
+        const uint32_t e0 = ord[q], e1 = ord[q + 1];
+        const uint32_t id0 = id_l[e0], id1 = id_l[e1];
+        T x0[D], x1[D], y0[D], y1[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) { x0[c] = xs.at(c, e0); x1[c] = xs.at(c, e1); }
+        pair_update<T, D, KK, INTEG>(P, m, x0, x1, id0, id1, y0, y1);
+        check_finite<T, D>(y0, P, id0, m);
+        check_finite<T, D>(y1, P, id1, m);
+        const uint32_t k0 = shuffle_key(P, id0, m + 1), k1 = shuffle_key(P, id1, m + 1);
+        ta[e0] = k0;
+        ta[e1] = k1;
+        tb[e0] = ((k0 >> osh) << 16) | atomicAdd(&cnt[k0 >> osh], 1u);
+        tb[e1] = ((k1 >> osh) << 16) | atomicAdd(&cnt[k1 >> osh], 1u);
+#pragma unroll
+        for (int c = 0; c < D; ++c) { xs.at(c, e0) = y0[c]; xs.at(c, e1) = y1[c]; }
+      }
+    }
+    if (triple && tid == 0)  // the remainder batch of size 3 (N odd), EM only
+      serial_batch<T, D, KK, INTEG>(P, m, pend - s0, n, ord, id_l, xs, ta, tb, cnt, osh);
+    __syncthreads();
+    fused_output<T, D, BLOCK>(P, dst, dcap, cur_next, n, id_l, ta, tb, xs, cnt, off, gbase, inv, wsum);
+    __syncthreads();  // stage s and the work arrays are free
+  }
 }
 
 // ------------------------------------------------------------------ RBM-r
 // one sweep of ceil(N/p) with-replacement batches (Alg. 2/3),
 // Jacobi-additive reading D:8.  State stays in id order.
-static __global__ void rbmr_draw_kernel(DevParams P, uint64_t nbatch, uint32_t* __restrict__ js,
+static __global__ void rbmr_draw_kernel(const __grid_constant__ DevParams P, uint64_t nbatch, uint32_t* __restrict__ js,
                                  uint32_t* __restrict__ cnt) {
   const uint32_t m = (uint32_t)*P.step;
   for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nbatch;
@@ -1468,7 +1880,7 @@ static __global__ void rbmr_draw_kernel(DevParams P, uint64_t nbatch, uint32_t* 
 }
 
 template <typename T, int D, int KK, int INTEG>
-static __global__ void rbmr_delta_kernel(DevParams P, uint64_t nslots, State<T, D> st,
+static __global__ void rbmr_delta_kernel(const __grid_constant__ DevParams P, uint64_t nslots, State<T, D> st,
                                   const uint32_t* __restrict__ js, T* __restrict__ delta) {
   const uint32_t m = (uint32_t)*P.step;
   for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < nslots;
@@ -1522,7 +1934,7 @@ static __global__ void rbmr_fill_kernel(uint64_t nslots, const uint32_t* __restr
 
 // x_j += Delta_s for s in ascending order (reading D:8); sphere: renormalise
 template <typename T, int D>
-static __global__ void rbmr_apply_kernel(DevParams P, uint64_t nslots, State<T, D> st,
+static __global__ void rbmr_apply_kernel(const __grid_constant__ DevParams P, uint64_t nslots, State<T, D> st,
                                   const uint32_t* __restrict__ off, uint32_t* __restrict__ lst,
                                   const T* __restrict__ delta) {
   const uint32_t m = (uint32_t)*P.step;
