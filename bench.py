@@ -87,7 +87,7 @@ def kernel_bytes(name: str, cfg: dict, prefix_bits: int) -> float:
     the single-bucket path (prefix_bits == 0) moves id + x (R = 4 + d*s)."""
     n = cfg["n"]
     R = (8 if prefix_bits > 0 else 4) + cfg["d"] * elt(cfg)
-    return {"scatter_sub": 2.0 * R * n, "bucket_step": 2.0 * R * n}.get(name, 0.0)
+    return {"scatter_sub": 2.0 * R * n, "split_owner": 2.0 * R * n, "bucket_step": 2.0 * R * n}.get(name, 0.0)
 
 
 class Clocks:

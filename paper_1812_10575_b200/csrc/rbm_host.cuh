@@ -84,6 +84,7 @@ struct rbm_ctx {
   uint32_t *prefix1 = nullptr, *tile_off = nullptr, *S = nullptr, *cur2 = nullptr;
   uint32_t* big_claim = nullptr;
   bool partitioned = false;  // state stored in the gapped buckets of step `step`
+  bool owner_split = false;  // pass 2 by the owner-computes splitter (writes S itself)
   uint64_t* step_dev = nullptr;
   unsigned long long* nonfinite = nullptr;
   uint32_t* capacity_err = nullptr;
@@ -386,8 +387,10 @@ struct Engine final : EngineBase {
   static constexpr int SPLIT_TILE = (8 + D * sizeof(T) <= 20) ? 2048 : 1024;
   static constexpr int SPLITB_BLOCK = 1024;
   static constexpr int SPLITB_TILE = 2 * SPLIT_TILE;
-  bool split_big = false;
-  size_t spb_smem = 0;
+  bool split_big = false, use_owner = false;
+  size_t spb_smem = 0, ow_smem = 0;
+  static constexpr int OWNER_BLOCK = 512;
+  static constexpr int OWNER_TILE = (8 + D * sizeof(T) <= 20) ? 2048 : 1024;
   int num_sms = 148;
 
   rbm_status setup(rbm_ctx& c) override {
@@ -411,6 +414,15 @@ struct Engine final : EngineBase {
     }
     sp_smem = split_smem_bytes<T, D, SPLIT_TILE>();
     spb_smem = split_smem_bytes<T, D, SPLITB_TILE>();
+    ow_smem = owner_smem_bytes<T, D, OWNER_TILE>();
+    {
+      // pass 2: persistent tiles over all SMs with atomic run reservations
+      // (default); RBM_SPLIT_KERNEL=owner: one CTA owns each pass-1 bucket, no
+      // atomics (measured 3x slower at C5: one CTA cannot stream a bucket fast
+      // enough); =old: one CTA per tile
+      const char* e = std::getenv("RBM_SPLIT_KERNEL");
+      use_owner = ow_smem <= 227 * 1024 && (e && std::strcmp(e, "owner") == 0);
+    }
     {
       const char* e = std::getenv("RBM_SPLIT_CFG");  // "small": two CTAs per SM, half tiles
       split_big = !(e && std::strcmp(e, "small") == 0) && spb_smem <= 227 * 1024;
@@ -419,6 +431,7 @@ struct Engine final : EngineBase {
       const char* e = std::getenv("RBM_SPLIT_KERNEL");  // "old": one CTA per tile (comparison)
       use_split = sp_smem <= 227 * 1024 && !(e && std::strcmp(e, "old") == 0);
     }
+    c.owner_split = use_owner;
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, c.device);
     if (num_sms <= 0) num_sms = 148;
     if (bk_smem != bucket_smem_bytes<T, D>(c.L.cap))
@@ -441,6 +454,11 @@ struct Engine final : EngineBase {
       if ((s = chk(cudaFuncSetAttribute(resident_kernel<T, D, KK, INTEG, BK_BLOCK>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem),
                    "smem attr resident"))) return s;
+    }
+    if (use_owner) {
+      if ((s = chk(cudaFuncSetAttribute(split_owner_kernel<T, D, OWNER_BLOCK, OWNER_TILE>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ow_smem),
+                   "smem attr owner"))) return s;
     }
     if (use_split) {
       if ((s = chk(cudaFuncSetAttribute(split_persist_kernel<T, D, SPLIT_BLOCK, SPLIT_TILE>,
@@ -524,10 +542,18 @@ struct Engine final : EngineBase {
     }
   }
 
-  // pass 2: pass-1 buckets/segments (capacity cap1, counts cnt1 strided) -> final buckets
+  // pass 2: pass-1 buckets/segments (capacity cap1, counts cnt1 strided) -> final
+  // buckets; then the exact global starts S (written by the owner kernel itself)
   void split2(rbm_ctx& c, cudaStream_t s, State<T, D> in, State<T, D> out, const uint32_t* cnt1) {
     const Layout& L = c.L;
-    if (use_split && split_big) {
+    const uint32_t G = (uint32_t)c.cfg.world_size;
+    const uint32_t nlb = (1u << L.b1) / G;
+    if (use_owner) {
+      split_owner_kernel<T, D, OWNER_BLOCK, OWNER_TILE><<<nlb, OWNER_BLOCK, ow_smem, s>>>(
+          c.P, in, out, L.cap2, cnt1, L.cap1, G, c.prefix1, c.S);
+      return;
+    }
+    if (use_split && split_big) {  // (this path and the next need final_scan for S)
       split_persist_kernel<T, D, SPLITB_BLOCK, SPLITB_TILE><<<(unsigned)num_sms, SPLITB_BLOCK, spb_smem, s>>>(
           c.P, in, out, c.cur2, L.cap2, cnt1, c.tile_off, L.cap1);
     } else if (use_split) {
@@ -597,11 +623,13 @@ struct Engine final : EngineBase {
       c.cur ^= 1;
     } else {
       // A holds the pass-1 buckets of step m: split them by the next b2 bits into B
-      cudaMemsetAsync(c.cur2, 0, (size_t)L.nbuckets * CUR2_STRIDE * 4, s);
+      if (!use_owner) cudaMemsetAsync(c.cur2, 0, (size_t)L.nbuckets * CUR2_STRIDE * 4, s);
       c.mark(s);
       split2(c, s, A, Bf, c.cur1[q]);
-      c.mark(s);
-      final_scan_kernel<<<1u << L.b1, 512, 0, s>>>(P, c.cur2, c.prefix1, c.S);
+      if (!use_owner) {
+        c.mark(s);
+        final_scan_kernel<<<1u << L.b1, 512, 0, s>>>(P, c.cur2, c.prefix1, c.S);
+      }
       c.mark(s);
       fused(c, s, Bf, A, L.cap1, c.cur1[q ^ 1]);
       c.mark(s);
@@ -650,12 +678,14 @@ struct Engine final : EngineBase {
     c.mark(s);
     part_scan_kernel<<<1, 1024, 0, s>>>(P, c.counts_all, G, rank, c.cur1[1], c.prefix1, c.tile_off,
                                         tile2());
-    cudaMemsetAsync(c.cur2, 0, (size_t)L.nbuckets * CUR2_STRIDE * 4, s);
+    if (!use_owner) cudaMemsetAsync(c.cur2, 0, (size_t)L.nbuckets * CUR2_STRIDE * 4, s);
     cudaMemsetAsync(c.cur1[0], 0, (size_t)c.L.nseg() * CUR1_STRIDE * 4, s);
     c.mark(s);
     split2(c, s, st(c, 2), stA(c), c.cur1[1]);
-    c.mark(s);
-    final_scan_kernel<<<nb1 / G, 512, 0, s>>>(P, c.cur2, c.prefix1, c.S);
+    if (!use_owner) {
+      c.mark(s);
+      final_scan_kernel<<<nb1 / G, 512, 0, s>>>(P, c.cur2, c.prefix1, c.S);
+    }
     c.mark(s);
     fused(c, s, stA(c), st(c, 1), L.cap1, c.cur1[0]);
     c.mark(s);
@@ -732,12 +762,20 @@ inline const char* const* kernel_names(const rbm_ctx& c, uint32_t* count) {
   static const char* const p1[] = {"tile_scan", "bucket_step", "straddle", "advance"};
   static const char* const p2[] = {"tile_scan", "scatter_sub", "final_scan", "bucket_step",
                                    "straddle", "advance"};
+  static const char* const p2o[] = {"tile_scan", "split_owner", "bucket_step", "straddle", "advance"};
+  static const char* const pto[] = {"part_scan", "split_owner", "bucket_step", "halo_extract",
+                                    "halo_place", "straddle", "pack_counts", "advance"};
   static const char* const pt[] = {"part_scan", "scatter_sub", "final_scan", "bucket_step",
                                    "halo_extract", "halo_place", "straddle", "pack_counts", "advance"};
-  if (is_partitioned(c.cfg)) { *count = 9; return pt; }
+  if (is_partitioned(c.cfg)) {
+    if (c.owner_split) { *count = 8; return pto; }
+    *count = 9;
+    return pt;
+  }
   if (c.cfg.scheme == RBM_SCHEME_RBMR) { *count = 8; return r; }
   if (c.L.B == 0) { *count = 1; return b0; }
   if (c.L.b2 == 0) { *count = 4; return p1; }
+  if (c.owner_split) { *count = 5; return p2o; }
   *count = 6;
   return p2;
 }

@@ -586,6 +586,129 @@ static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) split_persist_kern
   }
 }
 
+// ------------------------------------- owner-computes pass-2 splitter
+// One CTA owns one local pass-1 bucket u and streams all of its segments
+// (every source rank and salt) tile by tile through a double-buffered TMA
+// ring; final-bucket cursors live in shared memory (no global atomics), the
+// runs of consecutive tiles land back to back (the L2 merges their partial
+// sectors), and at the end the CTA writes the exact global starts S of its
+// 2^b2 final buckets (no separate final scan).
+template <typename T, int D, int TILE> __host__ __device__ constexpr size_t owner_smem_bytes() {
+  return (4 * 1024 + 64) * 4 + 64 + 2 * split_stage_bytes<T, D, TILE>() + (size_t)TILE * 4 + (size_t)TILE * 2;
+}
+
+template <typename T, int D, int BLOCK, int TILE>
+static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) split_owner_kernel(const __grid_constant__ DevParams P,
+                                                                                State<T, D> src, State<T, D> dst,
+                                                                                uint32_t dcap,
+                                                                                const uint32_t* __restrict__ cnt1,
+                                                                                uint32_t scap, uint32_t G,
+                                                                                const uint32_t* __restrict__ prefix1,
+                                                                                uint32_t* S) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw);  // 1024
+  uint32_t* off = hist + 1024;                             // 1024
+  uint32_t* lcur = off + 1024;                             // 1024: running count per final bucket
+  uint32_t* gtmp = lcur + 1024;                            // 1024
+  uint32_t* wsum = gtmp + 1024;                            // 64
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);  // 2
+  TileInfo* tinfo = reinterpret_cast<TileInfo*>(bar + 2);  // 2
+  unsigned char* stg0 = smem_raw + (((4 * 1024 + 64) * 4 + 64 + 127) & ~127);
+  constexpr size_t SBY = split_stage_bytes<T, D, TILE>();
+  uint32_t* rk = reinterpret_cast<uint32_t*>(stg0 + 2 * SBY);
+  uint16_t* inv = reinterpret_cast<uint16_t*>(rk + TILE);
+  const uint32_t u = blockIdx.x;  // local pass-1 bucket
+  const uint32_t nseg = (1u << P.b1) << P.segk, nls = nseg / G, K = 1u << P.segk;
+  const uint32_t bits = P.b2, sh = 32u - P.b1 - P.b2, nbins = 1u << bits, mask = nbins - 1u;
+  const uint32_t dbase0 = u << P.b2;
+  const uint32_t nsrc = G * K;  // segments of this bucket: (source s, salt k)
+  const uint32_t tid = threadIdx.x;
+  const uint32_t nb4 = nbins < 4 ? 4u : nbins;
+  for (uint32_t i = tid; i < nb4; i += BLOCK) lcur[i] = 0;
+  // tile walk (thread 0 only): segment index w < nsrc, element offset lo
+  uint32_t wk = 0, wlo = 0;
+  uint64_t pol = 0;
+  auto next_tile = [&](TileInfo& ti) -> bool {  // thread 0
+    while (wk < nsrc) {
+      const uint32_t s = wk / K, k = wk - s * K;
+      const uint32_t v = s * nls + (u << P.segk) + k;
+      const uint32_t c = cnt1[(size_t)v * CUR1_STRIDE];
+      if (wlo < c) {
+        ti.u = v;
+        ti.lo = wlo;
+        ti.hi = min(wlo + (uint32_t)TILE, c);
+        wlo = ti.hi;
+        return true;
+      }
+      ++wk;
+      wlo = 0;
+    }
+    return false;
+  };
+  auto issue = [&](uint32_t st) {  // thread 0: always one arrival on bar[st]
+    TileInfo ti{0u, 0u, 0u, 0u};
+    next_tile(ti);
+    tinfo[st] = ti;
+    split_stage_load<T, D, TILE>(src, ti.u * scap + ti.lo, ti.hi - ti.lo, stg0 + st * SBY, &bar[st], pol);
+  };
+  if (tid == 0) {
+    pol = l2_evict_first_policy();
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    issue(0);
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  for (uint32_t it = 0;; ++it) {
+    const uint32_t s = it & 1u;
+    if (tid == 0) issue(s ^ 1u);  // prefetch (an empty tile when the walk is done)
+    for (uint32_t i = tid; i < nb4; i += BLOCK) hist[i] = 0;
+    mbar_wait(&bar[s], (phase >> s) & 1u);
+    phase ^= 1u << s;
+    const TileInfo ti = tinfo[s];
+    const uint32_t cnt = ti.hi - ti.lo;
+    __syncthreads();
+    if (cnt == 0) break;  // uniform: the walk is exhausted
+    const unsigned char* stg = stg0 + s * SBY;
+    const uint32_t* id_s = reinterpret_cast<const uint32_t*>(stg);
+    const uint32_t* key_s = id_s + TILE;
+    const T* x_s = reinterpret_cast<const T*>(key_s + TILE);
+    for (uint32_t e = tid; e < cnt; e += BLOCK) {
+      const uint32_t dg = (key_s[e] >> sh) & mask;
+      rk[e] = (dg << 16) | atomicAdd(&hist[dg], 1u);
+    }
+    __syncthreads();
+    block_excl_scan4<BLOCK>(hist, off, nb4, wsum);
+    for (uint32_t e = tid; e < cnt; e += BLOCK) {
+      const uint32_t v = rk[e];
+      inv[off[v >> 16] + (v & 0xffffu)] = (uint16_t)e;
+    }
+    __syncthreads();
+    for (uint32_t j = tid; j < cnt; j += BLOCK) {
+      const uint32_t e = inv[j];
+      const uint32_t dg = rk[e] >> 16;
+      const uint32_t slot = lcur[dg] + (j - off[dg]);
+      if (slot >= dcap) {  // bucket capacity exceeded (probability ~1e-30): fail loudly
+        atomicExch(P.capacity_err, 1u);
+        continue;
+      }
+      const size_t g = (size_t)(dbase0 + dg) * dcap + slot;
+      dst.id[g] = id_s[e];
+      dst.key[g] = key_s[e];
+#pragma unroll
+      for (int c = 0; c < D; ++c) dst.x[c][g] = x_s[(size_t)c * TILE + e];
+    }
+    __syncthreads();  // stage s, rk, inv, off free
+    for (uint32_t i = tid; i < nb4; i += BLOCK) lcur[i] += hist[i];
+  }
+  // exact global starts of this bucket's final buckets
+  __syncthreads();
+  block_excl_scan4<BLOCK>(lcur, gtmp, nb4, wsum);
+  const uint32_t o = prefix1[u];
+  for (uint32_t i = tid; i < nbins; i += BLOCK) S[dbase0 + i] = o + gtmp[i];
+  if (u == 0 && tid == 0) S[P.nbuckets] = prefix1[gridDim.x];
+}
+
 // ------------------------------------------------------- bucket step pieces
 template <typename T> __device__ __forceinline__ T batch_inv(const DevParams& P, uint32_t sz) {
   return (sz == P.p) ? Prm<T>::invp(P) : T(1) / T(sz - 1);
@@ -1242,17 +1365,20 @@ __device__ __forceinline__ void fused_output(const DevParams& P, State<T, D> dst
                                              const uint32_t* ta, const uint32_t* tb, SX<T> xs,
                                              uint32_t* cnt, uint32_t* off, uint32_t* gbase,
                                              uint16_t* inv, uint32_t* wsum) {
+  RBM_PROF_BEGIN(P);
   const uint32_t nout = 1u << P.b1;
   for (uint32_t i = threadIdx.x; i < nout; i += BLOCK) {
     const uint32_t h = cnt[i];
     gbase[i] = h ? atomicAdd(&cur_next[(size_t)out_seg(P, i, blockIdx.x) * CUR1_STRIDE], h) : 0u;
   }
   const uint32_t total = block_excl_scan4<BLOCK>(cnt, off, nout, wsum);
+  RBM_PROF(P, 8);
   for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
     const uint32_t t = tb[e];
     if (t != 0xffffffffu) inv[off[t >> 16] + (t & 0xffffu)] = (uint16_t)e;
   }
   __syncthreads();
+  RBM_PROF(P, 9);
   for (uint32_t j = threadIdx.x; j < total; j += BLOCK) {
     const uint32_t e = inv[j];
     const uint32_t dg = tb[e] >> 16;
@@ -1264,7 +1390,7 @@ __device__ __forceinline__ void fused_output(const DevParams& P, State<T, D> dst
 #pragma unroll
     for (int c = 0; c < D; ++c) dst.x[c][g] = xs.at(c, e);
   }
-}
+  RBM_PROF(P, 10);}
 
 // ------------------------------------------------ fused bucket step (general p)
 // One CTA per final bucket b of step m (gapped, capacity scap; global start
@@ -1588,14 +1714,6 @@ static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) bucket_pair_kernel
   }
   __syncthreads();
   RBM_PROF(P, 4);
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {  // ks is dead: reuse as digit|slot (straddlers keep ~0)
-    const uint32_t e = k * BLOCK + threadIdx.x;
-    if (e < n) tb[e] = 0xffffffffu;
-  }
-  for (uint32_t i = threadIdx.x; i < (1u << P.b1) / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
-  if (P.dbg_order)
-    for (uint32_t q = threadIdx.x; q < n; q += BLOCK) P.dbg_order[s0 + q] = id_l[ord[q]];
   // interior pairs: even global starts in [s0, end), end excludes a final triple (N odd)
   const uint32_t N = (uint32_t)P.n;
   const uint32_t pend = (N & 1u) ? N - 3u : N;
@@ -1604,21 +1722,45 @@ static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) bucket_pair_kernel
   const uint32_t npairs = (lim > head) ? (lim - head) / 2 : 0u;
   const uint32_t covered = head + 2 * npairs;            // [head, covered) are interior
   const bool triple = (N & 1u) && (pend >= s0) && (N <= s0 + n);
+  const uint32_t tri0 = triple ? pend - s0 : n;          // [tri0, n): the size-3 remainder batch
+  const uint32_t osh = 32u - P.b1;
+  const uint32_t nout = 1u << P.b1;
+  for (uint32_t i = threadIdx.x; i < nout / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
+  if (P.dbg_order)
+    for (uint32_t q = threadIdx.x; q < n; q += BLOCK) P.dbg_order[s0 + q] = id_l[ord[q]];
   __syncthreads();
   RBM_PROF(P, 5);
-  // straddlers: unchanged, to their sorted places in the own gapped range
-  for (uint32_t t = threadIdx.x; t < head + (n - covered); t += BLOCK) {
-    const uint32_t q = t < head ? t : covered + (t - head);
-    const bool in_triple = triple && (s0 + q >= pend);
-    if (!in_triple) {
-      const uint32_t e = ord[q];
-      src.id[sb + q] = id_l[e];
-#pragma unroll
-      for (int c = 0; c < D; ++c) src.x[c][sb + q] = xs.at(c, e);
-    }
+  // 4. output partition first (key_{m+1} depends on the id only): digit and
+  //    rank of every interior member, so the run reservations below are in
+  //    flight while the batches are computed.  ks is dead: tb = rank by e.
+  for (uint32_t q = head + threadIdx.x; q < n; q += BLOCK) {
+    if (q >= covered && q < tri0) continue;
+    const uint32_t e = ord[q];
+    const uint32_t kn = shuffle_key(P, id_l[e], m + 1);
+    ta[e] = kn;
+    tb[e] = atomicAdd(&cnt[kn >> osh], 1u);
   }
-  // 4. one thread per pair
-  const uint32_t osh = 32u - P.b1;
+  // straddlers: unchanged, to their sorted places in the own gapped range
+  for (uint32_t t = threadIdx.x; t < head + (tri0 - covered); t += BLOCK) {
+    const uint32_t q = t < head ? t : covered + (t - head);
+    const uint32_t e = ord[q];
+    src.id[sb + q] = id_l[e];
+#pragma unroll
+    for (int c = 0; c < D; ++c) src.x[c][sb + q] = xs.at(c, e);
+  }
+  __syncthreads();
+  // run reservations of digits threadIdx.x + r BLOCK, consumed after the batches
+  constexpr int NRES = (1024 + BLOCK - 1) / BLOCK;
+  uint32_t gres[NRES];
+#pragma unroll
+  for (int r = 0; r < NRES; ++r) {
+    const uint32_t i = threadIdx.x + r * BLOCK;
+    const uint32_t h = i < nout ? cnt[i] : 0u;
+    gres[r] = h ? atomicAdd(&cur_next[(size_t)out_seg(P, i, blockIdx.x) * CUR1_STRIDE], h) : 0u;
+  }
+  const uint32_t total = block_excl_scan4<BLOCK>(cnt, off, nout, wsum);
+  RBM_PROF(P, 8);
+  // 5. one thread per pair: Eq. (2.2) + update in place; staging index of each member
   constexpr int PITEMS = (ITEMS + 1) / 2;
 #pragma unroll
   for (int k = 0; k < PITEMS; ++k) {
@@ -1633,20 +1775,42 @@ static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) bucket_pair_kernel
       pair_update<T, D, KK, INTEG>(P, m, x0, x1, id0, id1, y0, y1);
       check_finite<T, D>(y0, P, id0, m);
       check_finite<T, D>(y1, P, id1, m);
-      const uint32_t k0 = shuffle_key(P, id0, m + 1), k1 = shuffle_key(P, id1, m + 1);
-      ta[e0] = k0;
-      ta[e1] = k1;
-      tb[e0] = ((k0 >> osh) << 16) | atomicAdd(&cnt[k0 >> osh], 1u);
-      tb[e1] = ((k1 >> osh) << 16) | atomicAdd(&cnt[k1 >> osh], 1u);
 #pragma unroll
       for (int c = 0; c < D; ++c) { xs.at(c, e0) = y0[c]; xs.at(c, e1) = y1[c]; }
+      inv[off[ta[e0] >> osh] + tb[e0]] = (uint16_t)e0;
+      inv[off[ta[e1] >> osh] + tb[e1]] = (uint16_t)e1;
     }
   }
-  if (triple && threadIdx.x == 0)  // the remainder batch of size 3 (N odd), EM only
-    serial_batch<T, D, KK, INTEG>(P, m, pend - s0, n, ord, id_l, xs, ta, tb, cnt, osh);
+  if (triple && threadIdx.x == 0) {  // the remainder batch of size 3 (N odd), EM only
+    T xn[3][D];
+    for (uint32_t q = tri0; q < n; ++q)
+      interior_update<T, D, KK, INTEG>(P, m, q, tri0, n, ord, xs, id_l[ord[q]], xn[q - tri0]);
+    for (uint32_t q = tri0; q < n; ++q) {
+      const uint32_t e = ord[q];
+      check_finite<T, D>(xn[q - tri0], P, id_l[e], m);
+#pragma unroll
+      for (int c = 0; c < D; ++c) xs.at(c, e) = xn[q - tri0][c];
+      inv[off[ta[e] >> osh] + tb[e]] = (uint16_t)e;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < NRES; ++r)
+    if (threadIdx.x + r * BLOCK < nout) gbase[threadIdx.x + r * BLOCK] = gres[r];
   __syncthreads();
   RBM_PROF(P, 6);
-  fused_output<T, D, BLOCK>(P, dst, dcap, cur_next, n, id_l, ta, tb, xs, cnt, off, gbase, inv, wsum);
+  // 6. staged slots -> coalesced runs of the step-(m+1) pass-1 buckets
+  for (uint32_t j = threadIdx.x; j < total; j += BLOCK) {
+    const uint32_t e = inv[j];
+    const uint32_t kn = ta[e];
+    const uint32_t dg = kn >> osh;
+    const uint32_t slot = gbase[dg] + (j - off[dg]);
+    if (slot >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
+    const uint32_t g = out_seg(P, dg, blockIdx.x) * dcap + slot;
+    dst.id[g] = id_l[e];
+    dst.key[g] = kn;
+#pragma unroll
+    for (int c = 0; c < D; ++c) dst.x[c][g] = xs.at(c, e);
+  }
   RBM_PROF(P, 7);
   if (P.prof && threadIdx.x == 0) atomicAdd(&P.prof[63], 1ull);
 }
