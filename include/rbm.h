@@ -267,6 +267,31 @@ rbm_status rbm_part_phase1(rbm_ctx* ctx);
  * exchanges C and R. */
 rbm_status rbm_part_phase2(rbm_ctx* ctx);
 
+/* ------------------------------------------------------------------------
+ * Direct O(N^2) steps: the fully coupled forward
+ * Euler-Maruyama step of Eq. (1.2),
+ *   x_i' = x_i + dt (-grad V(x_i) + 1/(N-1) sum_{j != i} K(x_i - x_j)) + sigma sqrt(dt) z_i,
+ * the reference solution the paper measures RBM against (Sec. 4.1,
+ * PAPER.md:808-813) and the p = N special case of Eq. (2.2).  z_i at step m
+ * is the Brownian increment RBM step m uses (counter (i, blk, m, TAG_NOISE)),
+ * so an RBM run and a direct run from the same X_0 and seed are
+ * synchronously coupled.  Sphere constraint as in RBM (D:11).  cfg: model
+ * fields only (p, scheme, world_size ignored); integrator must be
+ * Euler-Maruyama; n <= 2^24.  Stateless: no context.
+ * ------------------------------------------------------------------------ */
+/* Bytes of device workspace (ping-pong copy of x + flags). */
+rbm_status rbm_direct_workspace_size(const rbm_config* cfg, size_t* bytes);
+/* Clear the non-finite flag in ws (call once before the first rbm_direct_run). */
+rbm_status rbm_direct_reset(const rbm_config* cfg, void* ws, void* cuda_stream);
+/* Enqueue nsteps direct steps m0, m0+1, ... on x (device, N*d scalars of
+ * dtype, id order, row-major), in place; ws (device, >= the size above,
+ * 256-B aligned, caller-owned).  Asynchronous on cuda_stream. */
+rbm_status rbm_direct_run(const rbm_config* cfg, void* x_dev, uint64_t m0, uint64_t nsteps, void* ws,
+                          size_t ws_bytes, void* cuda_stream);
+/* Synchronise cuda_stream; RBM_ERR_NONFINITE if a direct step produced a
+ * non-finite position (message names step and id). */
+rbm_status rbm_direct_sync(const rbm_config* cfg, void* ws, void* cuda_stream);
+
 /* Message for the last failure on ctx (or on this thread if ctx == NULL). */
 const char* rbm_last_error(const rbm_ctx* ctx);
 

@@ -4,4 +4,4 @@ The product is librbm.so (C ABI in include/rbm.h, CUDA for sm_100a under
 csrc/); ``rbm`` is its thin ctypes binding.
 """
 from . import rbm  # noqa: F401
-from .rbm import RBM, RbmError, make_config  # noqa: F401
+from .rbm import RBM, Direct, RbmError, make_config  # noqa: F401

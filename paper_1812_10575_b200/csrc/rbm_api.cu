@@ -52,6 +52,37 @@ rbm_status rbm_workspace_size(const rbm_config* cfg, size_t* bytes) {
 }  // extern "C"
 
 namespace rbmhost {
+// the configuration-derived constants of DevParams (no device pointers)
+void fill_params(const rbm_config& k, DevParams& P) {
+  P = DevParams{};
+  P.n = k.n;
+  P.p = k.p;
+  P.pdiv = make_fastdiv(k.p);
+  P.nfull = (uint32_t)(k.n / k.p);
+  P.rem = (uint32_t)(k.n % k.p);
+  P.seed_lo = (uint32_t)k.seed;
+  P.seed_hi = (uint32_t)(k.seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    P.rk[2 * r] = P.seed_lo + (uint32_t)r * 0x9E3779B9u;
+    P.rk[2 * r + 1] = P.seed_hi + (uint32_t)r * 0xBB67AE85u;
+  }
+  P.rep_hi = k.replica << 8;
+  P.potential = k.potential;
+  P.constraint = k.constraint;
+  P.has_noise = k.sigma > 0.0;
+  P.kp0 = k.kparam[0];
+  P.kp1 = k.kparam[1];
+  P.beta = k.potential == RBM_V_HARMONIC ? k.vparam[0] : 0.0;
+  P.dt = k.dt;
+  P.sq = k.sigma * std::sqrt(k.dt);
+  P.kp0f = (float)P.kp0; P.kp1f = (float)P.kp1; P.betaf = (float)P.beta;
+  P.dtf = (float)P.dt; P.sqf = (float)P.sq;
+  P.invp = 1.0 / (double)(k.p - 1);
+  P.invpf = (float)P.invp;
+  P.group = 0;
+  if (k.p <= 32) { P.group = 1; while (P.group < k.p) P.group <<= 1; }
+}
+
 rbm_status init_impl(rbm_ctx* c, const rbm_config* cfg, void* wsp, size_t ws_bytes) {
   CU(cudaGetDevice(&c->device));
   int major = 0;
@@ -64,49 +95,22 @@ rbm_status init_impl(rbm_ctx* c, const rbm_config* cfg, void* wsp, size_t ws_byt
   c->eng.reset(make_engine(*cfg));
   if (!c->eng) return fail(c, RBM_ERR_UNKNOWN_KERNEL, "no engine for kernel %u, d=%u", cfg->kernel, cfg->d);
   DevParams& P = c->P;
-  P.n = cfg->n;
-  P.p = cfg->p;
-  P.pdiv = make_fastdiv(cfg->p);
-  P.nfull = (uint32_t)(cfg->n / cfg->p);
-  P.rem = (uint32_t)(cfg->n % cfg->p);
-  P.seed_lo = (uint32_t)cfg->seed;
-  P.seed_hi = (uint32_t)(cfg->seed >> 32);
-  for (int r = 0; r < 10; ++r) {
-    P.rk[2 * r] = P.seed_lo + (uint32_t)r * 0x9E3779B9u;
-    P.rk[2 * r + 1] = P.seed_hi + (uint32_t)r * 0xBB67AE85u;
-  }
-  P.rep_hi = cfg->replica << 8;
-  P.potential = cfg->potential;
-  P.constraint = cfg->constraint;
-  P.has_noise = cfg->sigma > 0.0;
-  P.kp0 = cfg->kparam[0];
-  P.kp1 = cfg->kparam[1];
-  P.beta = cfg->potential == RBM_V_HARMONIC ? cfg->vparam[0] : 0.0;
-  P.dt = cfg->dt;
-  P.sq = cfg->sigma * std::sqrt(cfg->dt);
-  P.kp0f = (float)P.kp0; P.kp1f = (float)P.kp1; P.betaf = (float)P.beta;
-  P.dtf = (float)P.dt; P.sqf = (float)P.sq;
-  P.invp = 1.0 / (double)(cfg->p - 1);
-  P.invpf = (float)P.invp;
+  fill_params(*cfg, P);
   P.B = c->L.B; P.b1 = c->L.b1; P.b2 = c->L.b2; P.nbuckets = c->L.nbuckets; P.cap = c->L.cap;
   P.step = c->step_dev;
   P.nonfinite = c->nonfinite;
   P.capacity_err = c->capacity_err;
   P.big_claim = c->big_claim;
   P.SB = c->L.SB; P.idbits = c->L.idbits; P.lowbits = c->L.lowbits;
-  P.dbg_order = nullptr;
-  P.group = 0;
-  if (cfg->p <= 32) { P.group = 1; while (P.group < cfg->p) P.group <<= 1; }
   P.big_scratch = c->big_scratch;
-  P.prof = nullptr;
-  if (std::getenv("RBM_PHASE_PROF")) {  // debug: per-phase cycles of the bucket kernel
-    CU(cudaMalloc(&P.prof, 64 * 8));
-    CU(cudaMemset(P.prof, 0, 64 * 8));
-  }
   P.nb1_loc_mask = ((1u << c->L.b1) >> c->L.g) - 1u;
   P.segk = c->L.segk;
   P.segmask = (1u << c->L.segk) - 1u;
   P.halo = (is_partitioned(*cfg) && cfg->rank > 0) ? 1u : 0u;
+  if (std::getenv("RBM_PHASE_PROF")) {  // debug: per-phase cycles of the bucket kernel
+    CU(cudaMalloc(&P.prof, 64 * 8));
+    CU(cudaMemset(P.prof, 0, 64 * 8));
+  }
   rbm_status s = c->eng->setup(*c);
   if (s) return s;
   CU(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
@@ -410,6 +414,83 @@ static rbm_status part_call(rbm_ctx* c, int phase) {
 rbm_status rbm_part_prologue(rbm_ctx* c) { return part_call(c, 0); }
 rbm_status rbm_part_phase1(rbm_ctx* c) { return part_call(c, 1); }
 rbm_status rbm_part_phase2(rbm_ctx* c) { return part_call(c, 2); }
+
+// --------------------------------------------- direct O(N^2) steps (f1)
+static rbm_status direct_validate(const rbm_config* cfg, size_t elt_bytes_out[2]) {
+  if (!cfg) return fail(nullptr, RBM_ERR_INVALID_ARG, "cfg is NULL");
+  if (cfg->integrator != RBM_INTEG_EULER_MARUYAMA)
+    return fail(nullptr, RBM_ERR_INVALID_ARG, "direct step: Euler-Maruyama only");
+  if (cfg->n > (1ull << 24)) return fail(nullptr, RBM_ERR_INVALID_ARG, "direct step: n <= 2^24 (O(N^2) work)");
+  rbm_config k = *cfg;  // the batch fields do not apply: validate the model only
+  k.p = 2;
+  k.scheme = RBM_SCHEME_RBM1;
+  k.world_size = 1;
+  k.rank = 0;
+  k.debug_bucket_cap = 0;
+  rbm_status s = validate(&k);
+  if (s) return s;
+  elt_bytes_out[0] = (size_t)cfg->n * cfg->d * elt_size(*cfg);  // ping-pong copy of x
+  elt_bytes_out[1] = 256;                                       // flags
+  return RBM_OK;
+}
+
+rbm_status rbm_direct_workspace_size(const rbm_config* cfg, size_t* bytes) {
+  size_t b[2];
+  rbm_status s = direct_validate(cfg, b);
+  if (s) return s;
+  if (!bytes) return fail(nullptr, RBM_ERR_INVALID_ARG, "bytes is NULL");
+  *bytes = ((b[0] + 255) & ~size_t(255)) + b[1];
+  return RBM_OK;
+}
+
+rbm_status rbm_direct_run(const rbm_config* cfg, void* x, uint64_t m0, uint64_t nsteps, void* ws,
+                          size_t ws_bytes, void* stream) {
+  size_t need = 0;
+  rbm_status s = rbm_direct_workspace_size(cfg, &need);
+  if (s) return s;
+  if (!x || !ws || ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 255))
+    return fail(nullptr, RBM_ERR_WORKSPACE, "direct: x %p, workspace %p of %zu B (need %zu, 256-B aligned)", x, ws, ws_bytes, need);
+  if (m0 + nsteps >= (1ull << 32)) return fail(nullptr, RBM_ERR_INVALID_ARG, "step index would exceed 2^32");
+  std::unique_ptr<EngineBase> eng(make_engine(*cfg));
+  if (!eng) return fail(nullptr, RBM_ERR_UNKNOWN_KERNEL, "no engine for kernel %u, d=%u", cfg->kernel, cfg->d);
+  DevParams P;
+  fill_params(*cfg, P);
+  size_t b[2];
+  direct_validate(cfg, b);
+  unsigned char* w = reinterpret_cast<unsigned char*>(ws);
+  P.nonfinite = reinterpret_cast<unsigned long long*>(w + ((b[0] + 255) & ~size_t(255)));
+  rbm_ctx* c = nullptr;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (nsteps) eng->direct(P, x, w, (uint32_t)cfg->n, (uint32_t)m0, (uint32_t)nsteps, st);
+  CU(cudaGetLastError());
+  return RBM_OK;
+}
+
+rbm_status rbm_direct_sync(const rbm_config* cfg, void* ws, void* stream) {
+  size_t b[2];
+  rbm_status s = direct_validate(cfg, b);
+  if (s) return s;
+  rbm_ctx* c = nullptr;
+  unsigned long long nf = 0;
+  const unsigned long long* flag = reinterpret_cast<const unsigned long long*>(
+      reinterpret_cast<unsigned char*>(ws) + ((b[0] + 255) & ~size_t(255)));
+  CU(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
+  CU(cudaMemcpy(&nf, flag, 8, cudaMemcpyDeviceToHost));
+  if (nf != ~0ull)
+    return fail(nullptr, RBM_ERR_NONFINITE, "direct step: non-finite position at step %llu, particle id %llu",
+                (unsigned long long)(nf >> 32), (unsigned long long)(nf & 0xffffffffull));
+  return RBM_OK;
+}
+
+rbm_status rbm_direct_reset(const rbm_config* cfg, void* ws, void* stream) {
+  size_t b[2];
+  rbm_status s = direct_validate(cfg, b);
+  if (s) return s;
+  rbm_ctx* c = nullptr;
+  CU(cudaMemsetAsync(reinterpret_cast<unsigned char*>(ws) + ((b[0] + 255) & ~size_t(255)), 0xff, 8,
+                     reinterpret_cast<cudaStream_t>(stream)));
+  return RBM_OK;
+}
 
 const char* rbm_last_error(const rbm_ctx* c) { return c ? c->err.c_str() : g_err.c_str(); }
 

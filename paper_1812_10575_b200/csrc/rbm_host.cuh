@@ -355,6 +355,9 @@ struct EngineBase {
   virtual void gather(rbm_ctx& c, uint64_t i0, uint64_t i1, void* out, cudaStream_t s) = 0;
   // partitioned single system: the step split around its three exchanges
   virtual void run_resident(rbm_ctx& c, cudaStream_t s, uint32_t nsteps) = 0;
+  // direct O(N^2) Euler-Maruyama steps on an id-ordered N x d array (f1)
+  virtual void direct(const DevParams& P, void* x, void* tmp, uint32_t n, uint32_t m0,
+                      uint32_t nsteps, cudaStream_t s) = 0;
   virtual void part_prologue(rbm_ctx& c, cudaStream_t s) = 0;
   virtual void part_phase1(rbm_ctx& c, cudaStream_t s) = 0;
   virtual void part_phase2(rbm_ctx& c, cudaStream_t s) = 0;
@@ -639,6 +642,18 @@ struct Engine final : EngineBase {
     c.mark(s);
     advance_kernel<<<1, 1, 0, s>>>(c.step_dev);
     c.mark(s);
+  }
+
+  void direct(const DevParams& P, void* x, void* tmp, uint32_t n, uint32_t m0, uint32_t nsteps,
+              cudaStream_t s) override {
+    constexpr int TB = 128;
+    T* a = reinterpret_cast<T*>(x);
+    T* b = reinterpret_cast<T*>(tmp);
+    for (uint32_t k = 0; k < nsteps; ++k) {
+      direct_kernel<T, D, KK, TB><<<(n + TB - 1) / TB, TB, 0, s>>>(P, a, b, n, m0 + k);
+      std::swap(a, b);
+    }
+    if (nsteps & 1u) cudaMemcpyAsync(x, tmp, (size_t)n * D * sizeof(T), cudaMemcpyDeviceToDevice, s);
   }
 
   // N <= 2048: nsteps steps in one launch of one CTA (state in smem)

@@ -2017,6 +2017,57 @@ static __global__ void __launch_bounds__(BLOCK, 1) pair_persist_kernel(const __g
   }
 }
 
+// -------------------------------------- direct O(N^2) step (next row f1)
+// The fully coupled Euler-Maruyama step of Eq. (1.2): the reference solution
+// the paper measures RBM against (Sec. 4.1, "solving the
+// fully coupled system using the forward Euler scheme").  One thread per
+// particle i (id order), j tiles staged in shared memory, forces summed in
+// ascending j, prefactor 1/(N-1); the Brownian increment of particle i at
+// step m is the one RBM step m uses (counter (i, blk, m, TAG_NOISE)), so RBM
+// and direct runs from one X_0 are synchronously coupled.
+template <typename T, int D, int KK, int TB>
+static __global__ void __launch_bounds__(TB) direct_kernel(const __grid_constant__ DevParams P,
+                                                           const T* __restrict__ xin,
+                                                           T* __restrict__ xout, uint32_t n,
+                                                           uint32_t m) {
+  __shared__ T tile[D][TB];
+  const uint32_t i = blockIdx.x * TB + threadIdx.x;
+  T xi[D], f[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    xi[c] = (i < n) ? xin[(size_t)i * D + c] : T(0);
+    f[c] = T(0);
+  }
+  for (uint32_t j0 = 0; j0 < n; j0 += TB) {
+    const uint32_t jj = j0 + threadIdx.x;
+#pragma unroll
+    for (int c = 0; c < D; ++c) tile[c][threadIdx.x] = (jj < n) ? xin[(size_t)jj * D + c] : T(0);
+    __syncthreads();
+    const uint32_t lim = min((uint32_t)TB, n - j0);
+#pragma unroll 4
+    for (uint32_t t = 0; t < lim; ++t) {
+      if (j0 + t == i) continue;
+      T xj[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) xj[c] = tile[c][t];
+      add_interaction<T, D, KK>(xi, xj, f, P);
+    }
+    __syncthreads();
+  }
+  if (i >= n) return;
+  const T nm1 = T(n - 1);
+#pragma unroll
+  for (int c = 0; c < D; ++c) f[c] /= nm1;
+  T z[D], xn[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) z[c] = T(0);
+  if (P.has_noise) Normals<T, D>::get(P, i, m, TAG_NOISE, z);
+  em_update<T, D>(xi, f, z, xn, P, true);
+  check_finite<T, D>(xn, P, i, m);
+#pragma unroll
+  for (int c = 0; c < D; ++c) xout[(size_t)i * D + c] = xn[c];
+}
+
 // ------------------------------------------------------------------ RBM-r
 // one sweep of ceil(N/p) with-replacement batches (Alg. 2/3),
 // Jacobi-additive reading D:8.  State stays in id order.

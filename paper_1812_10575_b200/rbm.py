@@ -28,7 +28,8 @@ EXPORTS = ["rbm_workspace_size", "rbm_init", "rbm_set_state", "rbm_step", "rbm_r
            "rbm_gather", "rbm_sync", "rbm_step_index", "rbm_launches_per_step", "rbm_layout",
            "rbm_debug_permutation", "rbm_debug_slots", "rbm_debug_philox", "rbm_last_error",
            "rbm_destroy", "rbm_kernel_name", "rbm_timing_begin", "rbm_timing_end",
-           "rbm_part_info_get", "rbm_part_prologue", "rbm_part_phase1", "rbm_part_phase2"]
+           "rbm_part_info_get", "rbm_part_prologue", "rbm_part_phase1", "rbm_part_phase2",
+           "rbm_direct_workspace_size", "rbm_direct_reset", "rbm_direct_run", "rbm_direct_sync"]
 
 
 class RbmError(RuntimeError):
@@ -80,6 +81,10 @@ def lib():
             "rbm_kernel_name": (C.c_char_p, [vp, u32]),
             "rbm_timing_begin": (st, [vp, u32]),
             "rbm_timing_end": (st, [vp, C.POINTER(C.c_double), C.POINTER(u32)]),
+            "rbm_direct_workspace_size": (st, [cfgp, C.POINTER(C.c_size_t)]),
+            "rbm_direct_reset": (st, [cfgp, vp, vp]),
+            "rbm_direct_run": (st, [cfgp, vp, u64, u64, vp, C.c_size_t, vp]),
+            "rbm_direct_sync": (st, [cfgp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -309,3 +314,40 @@ class RBM:
             self.close()
         except Exception:
             pass
+
+
+# ------------------------------------------------ direct O(N^2) steps (f1)
+class Direct:
+    """Fully coupled Euler-Maruyama steps (rbm_direct_run) on an id-ordered
+    device tensor (N x d), synchronously coupled with RBM runs of the same seed."""
+
+    def __init__(self, cfg: dict, x, device=None):
+        import torch
+        self.torch = torch
+        self.c = make_config(dict(cfg, p=2, scheme="rbm1", world_size=1, rank=0))
+        self.c.n = int(cfg["n"])
+        self.device = torch.device(device or "cuda")
+        self.dtype = torch.float64 if cfg.get("dtype", "f64") == "f64" else torch.float32
+        n = C.c_size_t(0)
+        _check(lib().rbm_direct_workspace_size(C.byref(self.c), C.byref(n)))
+        self.ws_bytes = n.value
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+        self.stream = torch.cuda.current_stream(self.device)
+        self.x = torch.as_tensor(x, dtype=self.dtype).to(self.device).contiguous().reshape(self.c.n, self.c.d)
+        _check(lib().rbm_direct_reset(C.byref(self.c), C.c_void_p(self.ws.data_ptr()),
+                                      C.c_void_p(self.stream.cuda_stream)))
+        self.step_index = int(cfg.get("step0", 0))
+
+    def run(self, nsteps: int):
+        _check(lib().rbm_direct_run(C.byref(self.c), C.c_void_p(self.x.data_ptr()), self.step_index,
+                                    int(nsteps), C.c_void_p(self.ws.data_ptr()), self.ws_bytes,
+                                    C.c_void_p(self.stream.cuda_stream)))
+        self.step_index += int(nsteps)
+
+    def sync(self):
+        _check(lib().rbm_direct_sync(C.byref(self.c), C.c_void_p(self.ws.data_ptr()),
+                                     C.c_void_p(self.stream.cuda_stream)))
+
+    def gather(self):
+        self.sync()
+        return self.x.cpu().numpy()

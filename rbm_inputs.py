@@ -78,3 +78,16 @@ def user_x0(n: int, d: int, seed: int, dist: str = "normal", scale: float = 1.0)
         z = rng.standard_normal((n, d))
         return z / np.linalg.norm(z, axis=1, keepdims=True)
     raise ValueError(dist)
+
+
+def semicircle_x0(n: int, seed: int, radius: float = 2.0) -> np.ndarray:
+    """Seeded iid sample of rho_0(x) = sqrt(R^2 - x^2) / (pi R^2 / 2) on [-R, R]
+    (PAPER.md:823-825 with R = 2; the paper draws it by Metropolis-Hastings,
+    here by exact rejection sampling), shape (n, 1)."""
+    rng = np.random.default_rng(seed)
+    out = np.empty(0)
+    while out.size < n:
+        x = rng.uniform(-radius, radius, 2 * n)
+        keep = rng.uniform(0.0, 1.0, 2 * n) < np.sqrt(np.maximum(radius * radius - x * x, 0.0)) / radius
+        out = np.concatenate([out, x[keep]])
+    return out[:n].reshape(n, 1)
