@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="particles per GPU override")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--direct", action="store_true",
+                    help="time the direct O(N^2) step (row f1) on the workload's model instead")
     ap.add_argument("--mode", default=None, choices=["partition", "ensemble"],
                     help="N>1 GPUs: one partitioned global system (default) or independent replicas")
     return ap.parse_args()
@@ -190,6 +192,58 @@ def config_dict(args, cfg, world):
         if cfg["n"] * (4 + cfg["d"] * elt(cfg)) > 2 * 126e6 else "state fits in L2; no flush"}
 
 
+def direct_peak(cfg):
+    """ALU roofline of one fp32/fp64 interaction on B200:
+    148 SMs x 1.965 GHz x (128 fp32 | 64 fp64 FMA-pipe lanes per SM per clock)
+    / (pipe instructions per interaction), and the MUFU bound (16/clk/SM)."""
+    lanes = 64.0 if cfg["dtype"] == "f64" else 128.0
+    instr = {"coulomb_reg": 12, "smooth": 10, "gauss_attr_rep": 14, "bounded_confidence": 8,
+             "dyson": 6, "coulomb": 12, "zero": 4}[cfg["kernel"]] + 2 * cfg["d"]
+    return 148 * 1.965e9 * lanes / instr
+
+
+def bench_direct(args, cfg, dev, local):
+    """Row f1: fully coupled Euler-Maruyama steps, interactions per second."""
+    import numpy as np
+    import torch
+
+    from paper_1812_10575_b200 import Direct
+    n = args.n or (1 << 16)
+    c = dict(cfg, n=n)
+    x0 = RI.user_x0(n, c["d"], seed=1).astype(np.float32 if c["dtype"] == "f32" else np.float64)
+    d = Direct(c, x0, device=dev)
+    clk = Clocks(local)
+    clk.start()
+    time.sleep(0.3)
+    d.run(args.warmup)
+    d.sync()
+    K = args.steps
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(d.stream)
+    d.run(K)
+    e1.record(d.stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    d.sync()
+    inter = float(n) * (n - 1) * K / (ms / 1e3)
+    peak = direct_peak(c)
+    line = {"metric": "pair interactions/s (direct O(N^2) step, row f1)", "value": inter,
+            "unit": "interactions/s", "n_gpus": 1, "steps": K, "warmup": args.warmup,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": c["dtype"], "data": "synthetic (seeded normal X0)",
+            "config": {"workload": f"{args.workload} model, direct step", "n": n, "d": c["d"],
+                       "kernel": c["kernel"], "l2": "state fits in L2; no flush"},
+            "particle_steps_per_s": n * K / (ms / 1e3),
+            "roofline": {"bound": "alu", "kernel": "direct_kernel", "achieved": inter, "peak": peak,
+                         "unit": "interactions/s", "frac": inter / peak, "traffic": None,
+                         "peak_source": "derived: 148 SMs x 1.965 GHz x FMA-pipe lanes / pipe instructions per interaction"},
+            "clocks": clocks, "gpu_launches": K, "e2e": None, "cpu_baseline": None}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def bench_partition(args, cfg, world, rank, local, dev, barrier, max_over_ranks):
     """One global system of world x n particles split by key range over the
     ranks; exchanges over torch.distributed (NCCL/NVLink)."""
@@ -264,6 +318,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    if args.direct:
+        return bench_direct(args, cfg, dev, local)
     mode = args.mode or ("partition" if world > 1 else "single")
     K = args.steps
     if mode == "partition":

@@ -213,7 +213,9 @@ rbm_status rbm_run(rbm_ctx* c, uint64_t nsteps) {
     }
     return RBM_OK;
   }
-  if (c->cfg.scheme == RBM_SCHEME_RBM1 && c->L.B > 0 && !c->partitioned && nsteps > 0) {
+  const bool needs_prologue = (c->cfg.scheme == RBM_SCHEME_RBM1 && c->L.B > 0 && !c->partitioned) ||
+                              (c->cfg.scheme == RBM_SCHEME_RBMR && !c->aos_valid);
+  if (needs_prologue && nsteps > 0) {  // layout change of the state: first step outside the graphs
     rbm_status s0 = enqueue_steps(c, c->stream, 1);  // prologue step outside the graph
     if (s0) return s0;
     ++c->step;

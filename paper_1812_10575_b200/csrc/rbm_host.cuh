@@ -90,9 +90,10 @@ struct rbm_ctx {
   uint32_t* capacity_err = nullptr;
   unsigned char* big_scratch = nullptr;
   // RBM-r
-  uint32_t *js = nullptr, *rcnt = nullptr, *roff = nullptr, *rfill = nullptr, *rlst = nullptr,
-           *rparts = nullptr;
-  void* rdelta = nullptr;
+  uint32_t *js = nullptr, *rmcnt = nullptr, *rmbox = nullptr, *rovf = nullptr, *rnovf = nullptr;
+  void* rdelta = nullptr;  // Delta_s, 4 scalars per slot
+  void* rxa = nullptr;     // AoS state (4 scalars per particle, id order)
+  bool aos_valid = false;  // RBM-r state currently in rxa
   uint64_t nbatch = 0, nslots = 0;
   // state
   int cur = 0;
@@ -329,12 +330,12 @@ inline void carve(rbm_ctx& c, Workspace& ws) {
     c.nbatch = (n + k.p - 1) / k.p;
     c.nslots = c.nbatch * k.p;
     c.js = ws.take<uint32_t>(c.nslots);
-    c.rdelta = ws.take<unsigned char>(c.nslots * k.d * es);
-    c.rcnt = ws.take<uint32_t>(n);
-    c.rfill = ws.take<uint32_t>(n);
-    c.roff = ws.take<uint32_t>(n + 1);
-    c.rlst = ws.take<uint32_t>(c.nslots);
-    c.rparts = ws.take<uint32_t>((n + SCAN_TILE - 1) / SCAN_TILE + 1);
+    c.rdelta = ws.take<unsigned char>(c.nslots * 4 * es);
+    c.rxa = ws.take<unsigned char>(n * 4 * es);
+    c.rmcnt = ws.take<uint32_t>(n);
+    c.rmbox = ws.take<uint32_t>(n * MBOX);
+    c.rovf = ws.take<uint32_t>(2 * (size_t)OVF_CAP);
+    c.rnovf = ws.take<uint32_t>(1);
   }
   ws.used = (ws.used + 255) & ~size_t(255);
 }
@@ -511,12 +512,14 @@ struct Engine final : EngineBase {
                                                           k.iparam[0], k.iparam[1], k.iparam[2],
                                                           k.iparam[3]);
     c.partitioned = false;
+    c.aos_valid = false;
   }
 
   void set_state(rbm_ctx& c, const void* x, cudaStream_t s) override {
     set_state_kernel<T, D><<<grid_for(c.n0, 256), 256, 0, s>>>(c.id0, c.n0, st(c, c.cur),
                                                                reinterpret_cast<const T*>(x));
     c.partitioned = false;
+    c.aos_valid = false;
   }
 
   void gather(rbm_ctx& c, uint64_t i0, uint64_t i1, void* out, cudaStream_t s) override {
@@ -529,6 +532,12 @@ struct Engine final : EngineBase {
         gather_kernel<T, D><<<grid_for(c.n0, 256), 256, 0, s>>>(c.n0, st(c, 0), i0, i1,
                                                                 reinterpret_cast<T*>(out));
       }
+      return;
+    }
+    if (c.cfg.scheme == RBM_SCHEME_RBMR && c.aos_valid) {
+      if (i1 > i0)
+        gather_aos_kernel<T, D><<<grid_for(i1 - i0, 256), 256, 0, s>>>(reinterpret_cast<const T*>(c.rxa), i0,
+                                                                     i1, reinterpret_cast<T*>(out));
       return;
     }
     if (c.cfg.scheme == RBM_SCHEME_RBM1 && c.L.B > 0 && c.partitioned) {
@@ -726,26 +735,19 @@ struct Engine final : EngineBase {
   void step_rbmr(rbm_ctx& c, cudaStream_t s) {
     const DevParams& P = c.P;
     const uint64_t n = c.cfg.n;
-    State<T, D> x = st(c, c.cur);
-    cudaMemsetAsync(c.rcnt, 0, n * 4, s);
-    cudaMemsetAsync(c.rfill, 0, n * 4, s);
+    T* xa = reinterpret_cast<T*>(c.rxa);
+    if (!c.aos_valid) {  // state set by init / set_state (SoA) -> AoS, once
+      rbmr_pack_kernel<T, D><<<grid_for(n, 256), 256, 0, s>>>(n, st(c, c.cur), xa);
+      c.aos_valid = true;
+    }
+    cudaMemsetAsync(c.rmcnt, 0, n * 4, s);
+    cudaMemsetAsync(c.rnovf, 0, 4, s);
     c.mark(s);
-    rbmr_draw_kernel<<<grid_for(c.nbatch, 128), 128, 0, s>>>(P, c.nbatch, c.js, c.rcnt);
-    const unsigned nparts = (unsigned)((n + SCAN_TILE - 1) / SCAN_TILE);
+    rbmr_batch_kernel<T, D, KK, INTEG><<<grid_for(c.nbatch, 128, 148 * 64), 128, 0, s>>>(
+        P, c.nbatch, xa, c.js, reinterpret_cast<T*>(c.rdelta), c.rmcnt, c.rmbox, c.rovf, c.rnovf);
     c.mark(s);
-    scan_reduce_kernel<<<nparts, SCAN_BLOCK, 0, s>>>(c.rcnt, n, c.rparts);
-    c.mark(s);
-    scan_parts_kernel<<<1, 1024, 0, s>>>(c.rparts, nparts);
-    c.mark(s);
-    scan_down_kernel<<<nparts, SCAN_BLOCK, 0, s>>>(c.rcnt, n, c.rparts, c.roff);
-    c.mark(s);
-    rbmr_fill_kernel<<<grid_for(c.nslots, 256), 256, 0, s>>>(c.nslots, c.js, c.roff, c.rfill, c.rlst);
-    c.mark(s);
-    rbmr_delta_kernel<T, D, KK, INTEG><<<grid_for(c.nslots, 256), 256, 0, s>>>(
-        P, c.nslots, x, c.js, reinterpret_cast<T*>(c.rdelta));
-    c.mark(s);
-    rbmr_apply_kernel<T, D><<<grid_for(n, 256), 256, 0, s>>>(P, c.nslots, x, c.roff, c.rlst,
-                                                             reinterpret_cast<const T*>(c.rdelta));
+    rbmr_apply_kernel<T, D><<<grid_for(n, 256), 256, 0, s>>>(P, n, xa, reinterpret_cast<const T*>(c.rdelta),
+                                                             c.rmcnt, c.rmbox, c.rovf, c.rnovf);
     c.mark(s);
     advance_kernel<<<1, 1, 0, s>>>(c.step_dev);
     c.mark(s);
@@ -771,8 +773,7 @@ EngineBase* make_for_kernel(uint32_t kernel, uint32_t integ) {
 }
 
 inline const char* const* kernel_names(const rbm_ctx& c, uint32_t* count) {
-  static const char* const r[] = {"rbmr_draw", "scan_reduce", "scan_parts", "scan_down",
-                                  "rbmr_fill", "rbmr_delta", "rbmr_apply", "advance"};
+  static const char* const r[] = {"rbmr_batch", "rbmr_apply", "advance"};
   static const char* const b0[] = {"resident_step"};
   static const char* const p1[] = {"tile_scan", "bucket_step", "straddle", "advance"};
   static const char* const p2[] = {"tile_scan", "scatter_sub", "final_scan", "bucket_step",
@@ -787,7 +788,7 @@ inline const char* const* kernel_names(const rbm_ctx& c, uint32_t* count) {
     *count = 9;
     return pt;
   }
-  if (c.cfg.scheme == RBM_SCHEME_RBMR) { *count = 8; return r; }
+  if (c.cfg.scheme == RBM_SCHEME_RBMR) { *count = 3; return r; }
   if (c.L.B == 0) { *count = 1; return b0; }
   if (c.L.b2 == 0) { *count = 4; return p1; }
   if (c.owner_split) { *count = 5; return p2o; }

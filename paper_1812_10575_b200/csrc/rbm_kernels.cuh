@@ -2069,182 +2069,225 @@ static __global__ void __launch_bounds__(TB) direct_kernel(const __grid_constant
 }
 
 // ------------------------------------------------------------------ RBM-r
-// one sweep of ceil(N/p) with-replacement batches (Alg. 2/3),
-// Jacobi-additive reading D:8.  State stays in id order.
-static __global__ void rbmr_draw_kernel(const __grid_constant__ DevParams P, uint64_t nbatch, uint32_t* __restrict__ js,
-                                 uint32_t* __restrict__ cnt) {
+// One sweep of ceil(N/p) with-replacement batches (Alg. 2/3),
+// Jacobi-additive reading D:8: every batch evaluated from X_m, then
+// x_j <- x_j + sum over the slots s with j_s = j of Delta_s, in ascending s.
+// State in id order as AoS (4 scalars per particle, one sector per gather);
+// slots are registered in per-particle mailboxes (MBOX entries, overflow list
+// for the ~1e-6 of particles drawn more often), sorted by s when applied.
+constexpr uint32_t MBOX = 8;
+constexpr uint32_t OVF_CAP = 1u << 20;
+
+template <typename T, int D>
+static __global__ void rbmr_pack_kernel(uint64_t n, State<T, D> st, T* __restrict__ xa) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) xa[i * 4 + c] = (c < D) ? st.x[c < D ? c : 0][i] : T(0);
+  }
+}
+
+template <typename T, int D>
+static __global__ void rbmr_unpack_kernel(uint64_t n, const T* __restrict__ xa, State<T, D> st) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    st.id[i] = (uint32_t)i;
+#pragma unroll
+    for (int c = 0; c < D; ++c) st.x[c][i] = xa[i * 4 + c];
+  }
+}
+
+template <typename T, int D>
+__device__ __forceinline__ void load4(const T* __restrict__ xa, uint32_t j, T (&x)[D]) {
+#pragma unroll
+  for (int c = 0; c < D; ++c) x[c] = xa[(size_t)j * 4 + c];
+}
+
+// one thread per batch b: draws j_s (s = b p + l, distinct in the batch, D:9),
+// the increments Delta_s from X_m, and the mailbox registration of each slot
+template <typename T, int D, int KK, int INTEG>
+static __global__ void __launch_bounds__(128) rbmr_batch_kernel(const __grid_constant__ DevParams P, uint64_t nbatch,
+                                                                const T* __restrict__ xa, uint32_t* __restrict__ js,
+                                                                T* __restrict__ delta, uint32_t* __restrict__ mcnt,
+                                                                uint32_t* __restrict__ mbox, uint32_t* __restrict__ ovf,
+                                                                uint32_t* __restrict__ novf) {
   const uint32_t m = (uint32_t)*P.step;
+  const uint32_t p = P.p;
+  if (p == 2) {  // pairs: every memory access of a batch issued before its first use
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nbatch;
+         b += (uint64_t)gridDim.x * blockDim.x) {
+      const uint64_t s0 = 2 * b;
+      uint32_t j0, j1;
+      {
+        const uint4 w = block_at(P, (uint32_t)s0, 0u, m, TAG_SLOT);
+        j0 = (uint32_t)__umul64hi(P.n, (((uint64_t)w.x) << 32) | w.y);
+      }
+      for (uint32_t t = 0;; ++t) {
+        const uint4 w = block_at(P, (uint32_t)(s0 + 1), t, m, TAG_SLOT);
+        j1 = (uint32_t)__umul64hi(P.n, (((uint64_t)w.x) << 32) | w.y);
+        if (j1 != j0) break;
+      }
+      T x0[D], x1[D];
+      load4<T, D>(xa, j0, x0);
+      load4<T, D>(xa, j1, x1);
+      const uint32_t pos0 = atomicAdd(&mcnt[j0], 1u);
+      const uint32_t pos1 = atomicAdd(&mcnt[j1], 1u);
+      js[s0] = j0;
+      js[s0 + 1] = j1;
+      T z0[D], z1[D], y0[D], y1[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) { z0[c] = T(0); z1[c] = T(0); }
+      if (P.has_noise) {
+        Normals<T, D>::get(P, (uint32_t)s0, m, TAG_NOISE_SLOT, z0);
+        Normals<T, D>::get(P, (uint32_t)(s0 + 1), m, TAG_NOISE_SLOT, z1);
+      }
+      if (INTEG == 0) {
+        T f0[D], f1[D], zz[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) { f0[c] = T(0); f1[c] = T(0); }
+        add_interaction<T, D, KK>(x0, x1, f0, P);  // 1/(p-1) = 1
+        add_interaction<T, D, KK>(x1, x0, f1, P);
+        (void)zz;
+        em_update<T, D>(x0, f0, z0, y0, P, false);
+        em_update<T, D>(x1, f1, z1, y1, P, false);
+      } else {
+        T a[D], bb[D];
+        pair_flow<T, D, KK>(x0, x1, true, a, P);
+        pair_flow<T, D, KK>(x0, x1, false, bb, P);
+        split_finish<T, D>(a, z0, y0, P, false);
+        split_finish<T, D>(bb, z1, y1, P, false);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        delta[s0 * 4 + c] = (c < D) ? y0[c < D ? c : 0] - x0[c < D ? c : 0] : T(0);
+        delta[(s0 + 1) * 4 + c] = (c < D) ? y1[c < D ? c : 0] - x1[c < D ? c : 0] : T(0);
+      }
+      const uint32_t jj[2] = {j0, j1}, pp[2] = {pos0, pos1};
+#pragma unroll
+      for (int l = 0; l < 2; ++l) {
+        if (pp[l] < MBOX) {
+          mbox[(size_t)jj[l] * MBOX + pp[l]] = (uint32_t)(s0 + l);
+        } else {
+          const uint32_t q = atomicAdd(novf, 1u);
+          if (q < OVF_CAP) { ovf[2 * q] = jj[l]; ovf[2 * q + 1] = (uint32_t)(s0 + l); }
+          else atomicExch(P.capacity_err, 1u);
+        }
+      }
+    }
+    return;
+  }
   for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nbatch;
        b += (uint64_t)gridDim.x * blockDim.x) {
-    for (uint32_t l = 0; l < P.p; ++l) {
-      const uint64_t s = b * P.p + l;
+    const uint64_t s0 = b * p;
+    for (uint32_t l = 0; l < p; ++l) {
+      const uint64_t s = s0 + l;
       uint32_t t = 0, j;
       for (;;) {
         const uint4 w = block_at(P, (uint32_t)s, t, m, TAG_SLOT);
         const uint64_t u = (((uint64_t)w.x) << 32) | w.y;
         j = (uint32_t)__umul64hi(P.n, u);
         bool dup = false;
-        for (uint32_t l2 = 0; l2 < l; ++l2) dup |= (js[b * P.p + l2] == j);
+        for (uint32_t l2 = 0; l2 < l; ++l2) dup |= (js[s0 + l2] == j);
         if (!dup) break;
         ++t;
       }
       js[s] = j;
-      atomicAdd(&cnt[j], 1u);
     }
-  }
-}
-
-template <typename T, int D, int KK, int INTEG>
-static __global__ void rbmr_delta_kernel(const __grid_constant__ DevParams P, uint64_t nslots, State<T, D> st,
-                                  const uint32_t* __restrict__ js, T* __restrict__ delta) {
-  const uint32_t m = (uint32_t)*P.step;
-  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < nslots;
-       s += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t b = s / P.p, s0 = b * P.p;
-    const uint32_t l = (uint32_t)(s - s0);
-    const uint32_t i = js[s];
-    T xi[D], z[D], xn[D];
+    for (uint32_t l = 0; l < p; ++l) {
+      const uint64_t s = s0 + l;
+      const uint32_t j = js[s];
+      T xi[D], z[D], xn[D];
+      load4<T, D>(xa, j, xi);
 #pragma unroll
-    for (int c = 0; c < D; ++c) { xi[c] = st.x[c][i]; z[c] = T(0); }
-    if (P.has_noise) Normals<T, D>::get(P, (uint32_t)s, m, TAG_NOISE_SLOT, z);
-    if (INTEG == 0) {
-      T f[D];
+      for (int c = 0; c < D; ++c) z[c] = T(0);
+      if (P.has_noise) Normals<T, D>::get(P, (uint32_t)s, m, TAG_NOISE_SLOT, z);
+      if (INTEG == 0) {
+        T f[D];
 #pragma unroll
-      for (int c = 0; c < D; ++c) f[c] = T(0);
-      for (uint32_t l2 = 0; l2 < P.p; ++l2) {
-        if (l2 == l) continue;
-        const uint32_t j = js[s0 + l2];
-        T xj[D];
+        for (int c = 0; c < D; ++c) f[c] = T(0);
+        for (uint32_t l2 = 0; l2 < p; ++l2) {  // ascending lane, self skipped
+          if (l2 == l) continue;
+          T xj[D];
+          load4<T, D>(xa, js[s0 + l2], xj);
+          add_interaction<T, D, KK>(xi, xj, f, P);
+        }
+        const T inv = T(1) / T(p - 1);
 #pragma unroll
-        for (int c = 0; c < D; ++c) xj[c] = st.x[c][j];
-        add_interaction<T, D, KK>(xi, xj, f, P);
+        for (int c = 0; c < D; ++c) f[c] *= inv;
+        em_update<T, D>(xi, f, z, xn, P, false);
+      } else {
+        T xa0[D], xb0[D], y[D];
+        load4<T, D>(xa, js[s0], xa0);
+        load4<T, D>(xa, js[s0 + 1], xb0);
+        pair_flow<T, D, KK>(xa0, xb0, l == 0, y, P);
+        split_finish<T, D>(y, z, xn, P, false);
       }
-      const T inv = T(1) / T(P.p - 1);
 #pragma unroll
-      for (int c = 0; c < D; ++c) f[c] *= inv;
-      em_update<T, D>(xi, f, z, xn, P, false);
-    } else {
-      T xa[D], xb[D], y[D];
-      const uint32_t ia = js[s0], ib = js[s0 + 1];
-#pragma unroll
-      for (int c = 0; c < D; ++c) { xa[c] = st.x[c][ia]; xb[c] = st.x[c][ib]; }
-      pair_flow<T, D, KK>(xa, xb, l == 0, y, P);
-      split_finish<T, D>(y, z, xn, P, false);
+      for (int c = 0; c < 4; ++c) delta[s * 4 + c] = (c < D) ? xn[c < D ? c : 0] - xi[c < D ? c : 0] : T(0);
+      const uint32_t pos = atomicAdd(&mcnt[j], 1u);
+      if (pos < MBOX) {
+        mbox[(size_t)j * MBOX + pos] = (uint32_t)s;
+      } else {
+        const uint32_t q = atomicAdd(novf, 1u);
+        if (q < OVF_CAP) { ovf[2 * q] = j; ovf[2 * q + 1] = (uint32_t)s; }
+        else atomicExch(P.capacity_err, 1u);
+      }
     }
-#pragma unroll
-    for (int c = 0; c < D; ++c) delta[(size_t)c * nslots + s] = xn[c] - xi[c];
   }
 }
 
-// CSR fill: slot s appended to particle js[s]'s list (order fixed later)
-static __global__ void rbmr_fill_kernel(uint64_t nslots, const uint32_t* __restrict__ js,
-                                 const uint32_t* __restrict__ off, uint32_t* __restrict__ fillc,
-                                 uint32_t* __restrict__ lst) {
-  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < nslots;
-       s += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t j = js[s];
-    lst[off[j] + atomicAdd(&fillc[j], 1u)] = (uint32_t)s;
-  }
-}
-
-// x_j += Delta_s for s in ascending order (reading D:8); sphere: renormalise
+// x_j += Delta_s over j's slots in ascending s (reading D:8); sphere: renormalise
 template <typename T, int D>
-static __global__ void rbmr_apply_kernel(const __grid_constant__ DevParams P, uint64_t nslots, State<T, D> st,
-                                  const uint32_t* __restrict__ off, uint32_t* __restrict__ lst,
-                                  const T* __restrict__ delta) {
+static __global__ void rbmr_apply_kernel(const __grid_constant__ DevParams P, uint64_t n, T* __restrict__ xa,
+                                         const T* __restrict__ delta, const uint32_t* __restrict__ mcnt,
+                                         const uint32_t* __restrict__ mbox, const uint32_t* __restrict__ ovf,
+                                         const uint32_t* __restrict__ novf) {
   const uint32_t m = (uint32_t)*P.step;
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < P.n;
+  constexpr uint32_t MAXL = 32;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
        j += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t a = off[j], b = off[j + 1];
-    if (a == b) continue;
-    for (uint32_t u = a + 1; u < b; ++u) {  // insertion sort of the (short) slot list
-      const uint32_t v = lst[u];
-      uint32_t w = u;
-      while (w > a && lst[w - 1] > v) { lst[w] = lst[w - 1]; --w; }
-      lst[w] = v;
+    const uint32_t c = mcnt[j];
+    if (c == 0) continue;
+    uint32_t sl[MAXL];
+    uint32_t k = 0;
+    const uint32_t cm = c < MBOX ? c : MBOX;
+    for (uint32_t q = 0; q < cm; ++q) sl[k++] = mbox[j * MBOX + q];
+    if (c > MBOX) {  // rare: the rest of j's slots are in the overflow list
+      const uint32_t no = min(*novf, OVF_CAP);
+      for (uint32_t q = 0; q < no; ++q)
+        if (ovf[2 * q] == (uint32_t)j) {
+          if (k < MAXL) sl[k++] = ovf[2 * q + 1];
+          else atomicExch(P.capacity_err, 1u);
+        }
+    }
+    for (uint32_t a = 1; a < k; ++a) {  // insertion sort of the (short) slot list
+      const uint32_t v = sl[a];
+      uint32_t w = a;
+      while (w > 0 && sl[w - 1] > v) { sl[w] = sl[w - 1]; --w; }
+      sl[w] = v;
     }
     T x[D];
+    load4<T, D>(xa, (uint32_t)j, x);
+    for (uint32_t a = 0; a < k; ++a) {
+      const uint64_t s = sl[a];
 #pragma unroll
-    for (int c = 0; c < D; ++c) x[c] = st.x[c][j];
-    for (uint32_t u = a; u < b; ++u) {
-      const uint32_t s = lst[u];
-#pragma unroll
-      for (int c = 0; c < D; ++c) x[c] += delta[(size_t)c * nslots + s];
+      for (int cc = 0; cc < D; ++cc) x[cc] += delta[s * 4 + cc];
     }
     if (P.constraint == 1) renormalise<T, D>(x);
     check_finite<T, D>(x, P, (uint32_t)j, m);
 #pragma unroll
-    for (int c = 0; c < D; ++c) st.x[c][j] = x[c];
+    for (int cc = 0; cc < D; ++cc) xa[j * 4 + cc] = x[cc];
   }
 }
 
-// ------------------------------------------------------ device-wide scan (RBM-r)
-// exclusive scan of a[0..n) into out[0..n], out[n] = total; 3 phases.
-constexpr int SCAN_BLOCK = 1024, SCAN_ITEMS = 4, SCAN_TILE = SCAN_BLOCK * SCAN_ITEMS;
-static __global__ void __launch_bounds__(SCAN_BLOCK) scan_reduce_kernel(const uint32_t* __restrict__ a,
-                                                                 uint64_t n, uint32_t* part) {
-  __shared__ uint32_t ws[33];
-  const uint64_t base = (uint64_t)blockIdx.x * SCAN_TILE;
-  uint32_t s = 0;
-  for (int k = 0; k < SCAN_ITEMS; ++k) {
-    const uint64_t i = base + (uint64_t)k * SCAN_BLOCK + threadIdx.x;
-    if (i < n) s += a[i];
-  }
-  const uint32_t inc = warp_incl_scan(s);
-  if ((threadIdx.x & 31) == 31) ws[threadIdx.x >> 5] = inc;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    const uint32_t v = warp_incl_scan(ws[threadIdx.x]);
-    if (threadIdx.x == 31) part[blockIdx.x] = v;
-  }
-}
-
-static __global__ void __launch_bounds__(1024) scan_parts_kernel(uint32_t* part, uint32_t nparts) {
-  __shared__ uint32_t ws[34];
-  const uint32_t per = (nparts + 1023) / 1024;
-  const uint32_t b0 = min(nparts, threadIdx.x * per), b1 = min(nparts, b0 + per);
-  uint32_t s = 0;
-  for (uint32_t i = b0; i < b1; ++i) s += part[i];
-  const uint32_t inc = warp_incl_scan(s);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (lane == 31) ws[w] = inc;
-  __syncthreads();
-  if (w == 0) {
-    const uint32_t v = ws[lane];
-    ws[lane] = warp_incl_scan(v) - v;
-  }
-  __syncthreads();
-  uint32_t run = ws[w] + inc - s;
-  for (uint32_t i = b0; i < b1; ++i) { const uint32_t v = part[i]; part[i] = run; run += v; }
-}
-
-static __global__ void __launch_bounds__(SCAN_BLOCK) scan_down_kernel(const uint32_t* __restrict__ a,
-                                                               uint64_t n,
-                                                               const uint32_t* __restrict__ part,
-                                                               uint32_t* out) {
-  __shared__ uint32_t ws[34];
-  const uint64_t base = (uint64_t)blockIdx.x * SCAN_TILE + (uint64_t)threadIdx.x * SCAN_ITEMS;
-  uint32_t v[SCAN_ITEMS], s = 0;
-  for (int k = 0; k < SCAN_ITEMS; ++k) {
-    const uint64_t i = base + k;
-    v[k] = (i < n) ? a[i] : 0u;
-    s += v[k];
-  }
-  const uint32_t inc = warp_incl_scan(s);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (lane == 31) ws[w] = inc;
-  __syncthreads();
-  if (w == 0) {
-    const uint32_t x = ws[lane];
-    ws[lane] = warp_incl_scan(x) - x;
-  }
-  __syncthreads();
-  uint32_t run = part[blockIdx.x] + ws[w] + inc - s;
-  for (int k = 0; k < SCAN_ITEMS; ++k) {
-    const uint64_t i = base + k;
-    if (i < n) out[i] = run;
-    if (i == n - 1) out[n] = run + v[k];
-    run += v[k];
+// gather from the AoS RBM-r state (id order)
+template <typename T, int D>
+static __global__ void gather_aos_kernel(const T* __restrict__ xa, uint64_t i0, uint64_t i1,
+                                         T* __restrict__ out) {
+  for (uint64_t i = i0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < i1;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int c = 0; c < D; ++c) out[(i - i0) * D + c] = xa[i * 4 + c];
   }
 }
 
