@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="particles per GPU override")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
+                    help="partitioned mode: records stored into the peers' buffers over NVLink "
+                         "by the kernels (fused, CUDA IPC) or moved by NCCL all-to-all")
     ap.add_argument("--direct", action="store_true",
                     help="time the direct O(N^2) step (row f1) on the workload's model instead")
     ap.add_argument("--mode", default=None, choices=["partition", "ensemble"],
@@ -253,6 +256,12 @@ def bench_partition(args, cfg, world, rank, local, dev, barrier, max_over_ranks)
     K = args.steps
     gcfg = dict(cfg, n=cfg["n"] * world, replica=0)
     ps = PT.PartitionedRBM(gcfg, world, [rank], PT.DistExchange(), device=dev)
+    exchange = "nccl"
+    if args.exchange == "fused" and world <= 8:
+        if ps.enable_fused():  # collective; all ranks agree
+            exchange = "fused"
+        elif rank == 0:
+            print("fused exchange unavailable (peer mapping); using the NCCL all-to-all", file=sys.stderr)
     stream = ps.systems[0].stream
     clk = Clocks(local)
     clk.start()
@@ -276,7 +285,9 @@ def bench_partition(args, cfg, world, rank, local, dev, barrier, max_over_ranks)
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": cfg["dtype"], "data": "synthetic (Philox init from seed, BASELINE.json config)",
             "config": dict(config_dict(args, cfg, world), n_total=gcfg["n"],
-                           multi_gpu="partitioned single system (key-range split, NCCL all-to-all + halo)"),
+                           multi_gpu="partitioned single system (key-range split, halo; records "
+                                     + ("stored into peer buffers by the kernels over NVLink"
+                                        if exchange == "fused" else "moved by NCCL all-to-all") + ")"),
             "roofline": None, "clocks": clocks,
             "gpu_launches": ps.systems[0].launches_per_step * K, "e2e": None, "cpu_baseline": None,
             "note": "per-kernel roofline and e2e are reported by the 1-GPU run"}

@@ -251,6 +251,17 @@ typedef struct {
  * validation as rbm_init).  RBM_ERR_STATE if cfg->world_size == 1. */
 rbm_status rbm_part_info_get(const rbm_config* cfg, rbm_part_info* out);
 
+/* Fused exchange (optional, world_size <= 8; SURVEY.md 8(e) "G9"): give the
+ * context every rank's workspace base as a device pointer usable from this
+ * GPU (peer-mapped over NVLink, e.g. a CUDA IPC mapping; peer_ws[rank] = this
+ * context's own ws).  From then on the bucket step, the straddle kernel and
+ * the prologue store each updated record straight into the destination
+ * rank's receive buffer (double-buffered by step parity), so exchange R is
+ * not performed: the all-to-all is fused into the kernels' output stores.
+ * Exchanges H and C stay (C, an all-gather, also orders the steps).  Call
+ * before rbm_part_prologue; all ranks must use the same config. */
+rbm_status rbm_part_set_peers(rbm_ctx* ctx, const uint64_t* peer_ws, uint32_t count);
+
 /* Enqueue the partition of the initial state (id order) into the send
  * buckets; follow with exchanges C and R.  Once per context. */
 rbm_status rbm_part_prologue(rbm_ctx* ctx);

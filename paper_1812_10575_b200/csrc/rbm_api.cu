@@ -92,6 +92,7 @@ rbm_status init_impl(rbm_ctx* c, const rbm_config* cfg, void* wsp, size_t ws_byt
   ws.base = reinterpret_cast<unsigned char*>(wsp);
   ws.size = ws_bytes;
   carve(*c, ws);
+  c->ws_base = ws.base;
   c->eng.reset(make_engine(*cfg));
   if (!c->eng) return fail(c, RBM_ERR_UNKNOWN_KERNEL, "no engine for kernel %u, d=%u", cfg->kernel, cfg->d);
   DevParams& P = c->P;
@@ -410,6 +411,24 @@ static rbm_status part_call(rbm_ctx* c, int phase) {
     ++c->step;
   }
   CU(cudaGetLastError());
+  return RBM_OK;
+}
+
+rbm_status rbm_part_set_peers(rbm_ctx* c, const uint64_t* peer_ws, uint32_t count) {
+  if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
+  if (!is_partitioned(c->cfg)) return fail(c, RBM_ERR_STATE, "not a partitioned context (world_size 1)");
+  if (c->partitioned) return fail(c, RBM_ERR_STATE, "set the peers before rbm_part_prologue");
+  if (!peer_ws || count != (uint32_t)c->cfg.world_size)
+    return fail(c, RBM_ERR_INVALID_ARG, "need world_size=%d peer workspace pointers", c->cfg.world_size);
+  if (count > (uint32_t)MAXG_FUSED)
+    return fail(c, RBM_ERR_UNSUPPORTED, "fused exchange supports world_size <= %d (one NVSwitch node)", MAXG_FUSED);
+  if (reinterpret_cast<unsigned char*>(peer_ws[c->cfg.rank]) != c->ws_base)
+    return fail(c, RBM_ERR_INVALID_ARG, "peer_ws[rank] must be this context's own workspace");
+  for (uint32_t j = 0; j < count; ++j) {
+    if (!peer_ws[j] || (peer_ws[j] & 255)) return fail(c, RBM_ERR_INVALID_ARG, "peer workspace %u is NULL or misaligned", j);
+    c->peer_base[j] = reinterpret_cast<unsigned char*>(peer_ws[j]);
+  }
+  c->fused = true;
   return RBM_OK;
 }
 

@@ -75,6 +75,9 @@ struct rbm_ctx {
   // partitioned single system (world_size > 1): buffer 0 = this rank's final
   // buckets A (bucket -1 = halo), 1 = send pass-1 buckets B, 2 = received C
   uint64_t id0 = 0, n0 = 0;  // initial id range of this rank
+  unsigned char* ws_base = nullptr;            // this rank's workspace (device)
+  bool fused = false;                          // G9: outputs stored into the peers' receive buffers
+  unsigned char* peer_base[MAXG_FUSED] = {};   // every rank's workspace base (peer-mapped)
   uint32_t *counts_send = nullptr, *counts_all = nullptr;
   unsigned char *halo_send = nullptr, *halo_recv = nullptr;
   // gapped-bucket pipeline.  cur1[q]: counts (cursors) of the buckets the
@@ -210,8 +213,9 @@ inline Layout choose_layout(const rbm_config& c) {
   if (part) {
     // three buffers (final buckets A with a leading halo bucket, send B,
     // receive C); pass-1 segments hold one source rank's share
-    uint64_t id0, n0;
-    initial_ids(c, id0, n0);
+    // the largest initial share, so every rank has the same workspace layout
+    // (fused mode addresses the peers' buffers with this rank's offsets)
+    const uint64_t n0 = (n + (uint64_t)c.world_size - 1) / (uint64_t)c.world_size;
     L.cap2 = gcap((double)n / (1u << L.B), L.cap + 64);
     L.cap1 = gcap((double)n / ((double)c.world_size * L.nseg()), 64);
     L.slots = std::max<uint64_t>(n0, (uint64_t)(L.nbuckets + 1) * L.cap2);
@@ -506,6 +510,36 @@ struct Engine final : EngineBase {
     return a;
   }
 
+  static OutDst<T, D> od(State<T, D> d) {
+    OutDst<T, D> o{};
+    o.st[0] = d;
+    o.fused = 0;
+    return o;
+  }
+  // buffer b of rank j's workspace (same layout on every rank)
+  State<T, D> st_peer(rbm_ctx& c, int b, uint32_t j) {
+    State<T, D> a = st(c, b);
+    const ptrdiff_t sh = c.peer_base[j] - c.ws_base;
+    a.id = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(a.id) + sh);
+    a.key = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(a.key) + sh);
+    for (int k = 0; k < 3; ++k) a.x[k] = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(a.x[k]) + sh);
+    return a;
+  }
+  // partitioned: receive buffer holding the data of step m (fused: double-buffered)
+  static int recv_buf(const rbm_ctx& c, uint64_t m) { return c.fused ? ((m & 1) ? 1 : 2) : 2; }
+  // partitioned: where a step writes the records of step m
+  OutDst<T, D> part_dst(rbm_ctx& c, uint64_t m) {
+    if (!c.fused) return od(st(c, 1));
+    OutDst<T, D> o{};
+    const uint32_t G = (uint32_t)c.cfg.world_size;
+    for (uint32_t j = 0; j < G; ++j) o.st[j] = st_peer(c, recv_buf(c, m), j);
+    o.fused = 1;
+    o.nls_log = 0;
+    while ((1u << o.nls_log) < c.L.nseg() / G) ++o.nls_log;
+    o.rank = (uint32_t)c.cfg.rank;
+    return o;
+  }
+
   void init_state(rbm_ctx& c, cudaStream_t s) override {
     const rbm_config& k = c.cfg;
     init_kernel<T, D><<<grid_for(c.n0, 256), 256, 0, s>>>(c.P, st(c, c.cur), c.id0, c.n0, k.init,
@@ -526,7 +560,7 @@ struct Engine final : EngineBase {
     if (is_partitioned(c.cfg)) {
       if (c.partitioned) {
         gather_part_kernel<T, D><<<grid_for((uint64_t)c.L.nseg() * c.L.cap1, 256), 256, 0, s>>>(
-            c.P, st(c, 2), c.L.cap1, c.counts_all, (uint32_t)c.cfg.world_size, (uint32_t)c.cfg.rank,
+            c.P, st(c, recv_buf(c, c.step)), c.L.cap1, c.counts_all, (uint32_t)c.cfg.world_size, (uint32_t)c.cfg.rank,
             i0, i1, reinterpret_cast<T*>(out));
       } else {
         gather_kernel<T, D><<<grid_for(c.n0, 256), 256, 0, s>>>(c.n0, st(c, 0), i0, i1,
@@ -575,7 +609,7 @@ struct Engine final : EngineBase {
       const uint32_t ns = L.nseg();
       const unsigned tiles2 = (unsigned)(((uint64_t)ns * L.cap1 + SC_TILE - 1) / SC_TILE + ns);
       scatter_kernel<T, D, 2, SC_BLOCK, SC_ITEMS><<<tiles2, SC_BLOCK, sc_smem, s>>>(
-          c.P, in, out, c.cur2, L.cap2, cnt1, c.tile_off, L.cap1, 0);
+          c.P, in, od(out), c.cur2, L.cap2, cnt1, c.tile_off, L.cap1, 0);
     }
   }
 
@@ -583,7 +617,7 @@ struct Engine final : EngineBase {
     return use_split ? (uint32_t)(split_big ? SPLITB_TILE : SPLIT_TILE) : (uint32_t)SC_TILE;
   }
 
-  void fused(rbm_ctx& c, cudaStream_t s, State<T, D> in, State<T, D> out, uint32_t ocap,
+  void fused(rbm_ctx& c, cudaStream_t s, State<T, D> in, const OutDst<T, D>& out, uint32_t ocap,
              uint32_t* cur_next) {
     if (use_persist)
       pair_persist_kernel<T, D, KK, INTEG, PERSIST_BLOCK, PERSIST_ITEMS>
@@ -616,7 +650,7 @@ struct Engine final : EngineBase {
       cudaMemsetAsync(c.cur1[q], 0, (size_t)L.nseg() * CUR1_STRIDE * 4, s);
       scatter_kernel<T, D, 1, SC_BLOCK, SC_ITEMS>
           <<<(unsigned)((n + SC_TILE - 1) / SC_TILE), SC_BLOCK, sc_smem, s>>>(
-              P, st(c, c.cur), st(c, c.cur ^ 1), c.cur1[q], pcap, nullptr, nullptr, 0, n);
+              P, st(c, c.cur), od(st(c, c.cur ^ 1)), c.cur1[q], pcap, nullptr, nullptr, 0, n);
       c.cur ^= 1;
       c.partitioned = true;
     }
@@ -628,9 +662,9 @@ struct Engine final : EngineBase {
     if (L.b2 == 0) {
       // A holds the final buckets of step m; the fused step writes m+1's into B
       c.mark(s);
-      fused(c, s, A, Bf, L.cap2, c.cur1[q ^ 1]);
+      fused(c, s, A, od(Bf), L.cap2, c.cur1[q ^ 1]);
       c.mark(s);
-      straddle_kernel<T, D, KK, INTEG><<<straddle_grid, 256, 0, s>>>(P, A, L.cap2, c.S, Bf, L.cap2,
+      straddle_kernel<T, D, KK, INTEG><<<straddle_grid, 256, 0, s>>>(P, A, L.cap2, c.S, od(Bf), L.cap2,
                                                                      c.cur1[q ^ 1]);
       c.cur ^= 1;
     } else {
@@ -643,9 +677,9 @@ struct Engine final : EngineBase {
         final_scan_kernel<<<1u << L.b1, 512, 0, s>>>(P, c.cur2, c.prefix1, c.S);
       }
       c.mark(s);
-      fused(c, s, Bf, A, L.cap1, c.cur1[q ^ 1]);
+      fused(c, s, Bf, od(A), L.cap1, c.cur1[q ^ 1]);
       c.mark(s);
-      straddle_kernel<T, D, KK, INTEG><<<straddle_grid, 256, 0, s>>>(P, Bf, L.cap2, c.S, A, L.cap1,
+      straddle_kernel<T, D, KK, INTEG><<<straddle_grid, 256, 0, s>>>(P, Bf, L.cap2, c.S, od(A), L.cap1,
                                                                      c.cur1[q ^ 1]);
     }
     c.mark(s);
@@ -689,7 +723,7 @@ struct Engine final : EngineBase {
     cudaMemsetAsync(c.cur1[0], 0, (size_t)c.L.nseg() * CUR1_STRIDE * 4, s);
     scatter_kernel<T, D, 1, SC_BLOCK, SC_ITEMS>
         <<<(unsigned)((c.n0 + SC_TILE - 1) / SC_TILE), SC_BLOCK, sc_smem, s>>>(
-            P, st(c, 0), st(c, 1), c.cur1[0], c.L.cap1, nullptr, nullptr, 0, c.n0);
+            P, st(c, 0), part_dst(c, c.step), c.cur1[0], c.L.cap1, nullptr, nullptr, 0, c.n0);
     pack_counts_kernel<<<1, 1024, 0, s>>>(c.cur1[0], c.L.nseg(), c.counts_send);
     c.partitioned = true;
   }
@@ -705,13 +739,13 @@ struct Engine final : EngineBase {
     if (!use_owner) cudaMemsetAsync(c.cur2, 0, (size_t)L.nbuckets * CUR2_STRIDE * 4, s);
     cudaMemsetAsync(c.cur1[0], 0, (size_t)c.L.nseg() * CUR1_STRIDE * 4, s);
     c.mark(s);
-    split2(c, s, st(c, 2), stA(c), c.cur1[1]);
+    split2(c, s, st(c, recv_buf(c, c.step)), stA(c), c.cur1[1]);
     if (!use_owner) {
       c.mark(s);
       final_scan_kernel<<<nb1 / G, 512, 0, s>>>(P, c.cur2, c.prefix1, c.S);
     }
     c.mark(s);
-    fused(c, s, stA(c), st(c, 1), L.cap1, c.cur1[0]);
+    fused(c, s, stA(c), part_dst(c, c.step + 1), L.cap1, c.cur1[0]);
     c.mark(s);
     halo_extract_kernel<T, D><<<1, 64, 0, s>>>(P, stA(c), L.cap2, c.S, c.halo_send);
   }
@@ -723,8 +757,8 @@ struct Engine final : EngineBase {
     halo_place_kernel<T, D><<<1, 64, 0, s>>>(P, stA(c), L.cap2, c.S, c.halo_recv);
     const unsigned grid = (unsigned)(((uint64_t)(L.nbuckets + 1) * 32 + 255) / 256);
     c.mark(s);
-    straddle_kernel<T, D, KK, INTEG><<<grid, 256, 0, s>>>(P, stA(c), L.cap2, c.S, st(c, 1), L.cap1,
-                                                          c.cur1[0]);
+    straddle_kernel<T, D, KK, INTEG><<<grid, 256, 0, s>>>(P, stA(c), L.cap2, c.S, part_dst(c, c.step + 1),
+                                                          L.cap1, c.cur1[0]);
     c.mark(s);
     pack_counts_kernel<<<1, 1024, 0, s>>>(c.cur1[0], L.nseg(), c.counts_send);
     c.mark(s);

@@ -27,6 +27,36 @@ template <typename T, int D> struct State {
   T* x[3];
 };
 
+// Destination of the records a step writes into the pass-1 segments of the
+// next step.  On one GPU (and with the NCCL exchange) st[0] is the local send
+// buffer and segment v sits at v * cap.  Fused partitioned mode (row a7, G9):
+// segment v belongs to rank v >> nls_log and is stored straight into that
+// rank's receive buffer st[rank'] (peer memory over NVLink) as its segment
+// (this rank << nls_log) | (v & (nls - 1)) -- the all-to-all is the store.
+constexpr int MAXG_FUSED = 8;
+template <typename T, int D> struct OutDst {
+  State<T, D> st[MAXG_FUSED];
+  uint32_t fused, nls_log, rank;
+};
+
+template <typename T, int D>
+__device__ __forceinline__ void out_put(const OutDst<T, D>& o, uint32_t v, uint32_t cap, uint32_t slot,
+                                        uint32_t id, uint32_t key, const T (&x)[D]) {
+  uint32_t w = 0;
+  size_t g;
+  if (o.fused) {
+    w = v >> o.nls_log;
+    g = (size_t)((o.rank << o.nls_log) | (v & ((1u << o.nls_log) - 1u))) * cap + slot;
+  } else {
+    g = (size_t)v * cap + slot;
+  }
+  const State<T, D>& d = o.st[w];
+  d.id[g] = id;
+  d.key[g] = key;
+#pragma unroll
+  for (int c = 0; c < D; ++c) d.x[c][g] = x[c];
+}
+
 // D coordinate arrays of a bucket in (shared or scratch) memory: base + c*stride.
 // One base pointer (not an array of pointers) keeps the address space visible
 // to the compiler, so shared-memory accesses stay LDS/STS.
@@ -367,7 +397,7 @@ __device__ __forceinline__ bool gapped_tile(const uint32_t* __restrict__ tile_of
 // Order inside a bucket is irrelevant: the bucket step sorts exactly.
 template <typename T, int D, int LEVEL, int BLOCK, int ITEMS>
 static __global__ void __launch_bounds__(BLOCK) scatter_kernel(const __grid_constant__ DevParams P, State<T, D> src,
-                                                               State<T, D> dst, uint32_t* cur,
+                                                               const __grid_constant__ OutDst<T, D> dst, uint32_t* cur,
                                                                uint32_t dcap,
                                                                const uint32_t* __restrict__ cnt1,
                                                                const uint32_t* __restrict__ tile_off,
@@ -457,11 +487,10 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(const __grid_cons
       atomicExch(P.capacity_err, 1u);
       continue;
     }
-    const uint32_t g = dest(dg) * dcap + slot;
-    dst.id[g] = st_id[j];
-    dst.key[g] = st_key[j];
+    T xo[D];
 #pragma unroll
-    for (int c = 0; c < D; ++c) dst.x[c][g] = st_x[c * TILE + j];
+    for (int c = 0; c < D; ++c) xo[c] = st_x[c * TILE + j];
+    out_put<T, D>(dst, dest(dg), dcap, slot, st_id[j], st_key[j], xo);
   }
 }
 
@@ -1017,7 +1046,7 @@ template <typename T, int D, int KK, int INTEG>
 static __global__ void __launch_bounds__(256) straddle_kernel(const __grid_constant__ DevParams P, State<T, D> strad,
                                                               uint32_t cap,
                                                               const uint32_t* __restrict__ S,
-                                                              State<T, D> dst, uint32_t ocap,
+                                                              const __grid_constant__ OutDst<T, D> dst, uint32_t ocap,
                                                               uint32_t* cur_next) {
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -1104,11 +1133,10 @@ static __global__ void __launch_bounds__(256) straddle_kernel(const __grid_const
     const uint32_t v = out_seg(P, kn >> osh, warp);
     const uint32_t slot = atomicAdd(&cur_next[(size_t)v * CUR1_STRIDE], 1u);
     if (slot >= ocap) { atomicExch(P.capacity_err, 1u); continue; }
-    const uint32_t g = v * ocap + slot;
-    dst.id[g] = idv[k];
-    dst.key[g] = kn;
+    T xo[D];
 #pragma unroll
-    for (int c = 0; c < D; ++c) dst.x[c][g] = xnew[k][c];
+    for (int c = 0; c < D; ++c) xo[c] = xnew[k][c];
+    out_put<T, D>(dst, v, ocap, slot, idv[k], kn, xo);
   }
 }
 
@@ -1249,7 +1277,7 @@ static __global__ void gather_part_kernel(const __grid_constant__ DevParams P, S
 // always make progress), written back to the bucket's own gapped range, then a
 // per-element append into the step-(m+1) buckets.
 template <typename T, int D, int KK, int INTEG, int BLOCK>
-__device__ __noinline__ void fused_big_path(const DevParams& P, State<T, D> src, State<T, D> dst,
+__device__ __noinline__ void fused_big_path(const DevParams& P, State<T, D> src, const OutDst<T, D>& dst,
                                             uint32_t* cur_next, uint32_t s0, uint32_t sb, uint32_t n,
                                             uint32_t m, uint32_t dcap, uint32_t* cnt, uint32_t* off,
                                             uint32_t* wsum) {
@@ -1301,11 +1329,10 @@ __device__ __noinline__ void fused_big_path(const DevParams& P, State<T, D> src,
       const uint32_t v = out_seg(P, kn >> osh, blockIdx.x);
       const uint32_t s = atomicAdd(&cur_next[(size_t)v * CUR1_STRIDE], 1u);
       if (s >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
-      const uint32_t g = v * dcap + s;
-      dst.id[g] = id;
-      dst.key[g] = kn;
+      T xo[D];
 #pragma unroll
-      for (int c = 0; c < D; ++c) dst.x[c][g] = src.x[c][sb + q];
+      for (int c = 0; c < D; ++c) xo[c] = src.x[c][sb + q];
+      out_put<T, D>(dst, v, dcap, s, id, kn, xo);
     }
   }
 }
@@ -1360,7 +1387,7 @@ __device__ __forceinline__ void load_bucket(State<T, D> src, uint32_t sb, uint32
 // Output phase shared by the fused kernels: reserve runs in the step-(m+1)
 // buckets (capacity dcap), stage by digit, coalesced write of id, key_{m+1}, x.
 template <typename T, int D, int BLOCK>
-__device__ __forceinline__ void fused_output(const DevParams& P, State<T, D> dst, uint32_t dcap,
+__device__ __forceinline__ void fused_output(const DevParams& P, const OutDst<T, D>& dst, uint32_t dcap,
                                              uint32_t* cur_next, uint32_t n, const uint32_t* id_l,
                                              const uint32_t* ta, const uint32_t* tb, SX<T> xs,
                                              uint32_t* cnt, uint32_t* off, uint32_t* gbase,
@@ -1384,11 +1411,10 @@ __device__ __forceinline__ void fused_output(const DevParams& P, State<T, D> dst
     const uint32_t dg = tb[e] >> 16;
     const uint32_t slot = gbase[dg] + (j - off[dg]);
     if (slot >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
-    const uint32_t g = out_seg(P, dg, blockIdx.x) * dcap + slot;
-    dst.id[g] = id_l[e];
-    dst.key[g] = ta[e];
+    T xo[D];
 #pragma unroll
-    for (int c = 0; c < D; ++c) dst.x[c][g] = xs.at(c, e);
+    for (int c = 0; c < D; ++c) xo[c] = xs.at(c, e);
+    out_put<T, D>(dst, out_seg(P, dg, blockIdx.x), dcap, slot, id_l[e], ta[e], xo);
   }
   RBM_PROF(P, 10);}
 
@@ -1412,7 +1438,7 @@ template <typename T, int D, int KK, int INTEG, int BLOCK>
 static __global__ void __launch_bounds__(BLOCK) bucket_fused_kernel(const __grid_constant__ DevParams P, State<T, D> src,
                                                                     uint32_t scap,
                                                                     const uint32_t* __restrict__ S,
-                                                                    State<T, D> dst, uint32_t dcap,
+                                                                    const __grid_constant__ OutDst<T, D> dst, uint32_t dcap,
                                                                     uint32_t* __restrict__ cur_next) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t nsb = 1u << P.SB;
@@ -1631,7 +1657,7 @@ template <typename T, int D, int KK, int INTEG, int BLOCK, int ITEMS>
 static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) bucket_pair_kernel(const __grid_constant__ DevParams P, State<T, D> src,
                                                                    uint32_t scap,
                                                                    const uint32_t* __restrict__ S,
-                                                                   State<T, D> dst, uint32_t dcap,
+                                                                   const __grid_constant__ OutDst<T, D> dst, uint32_t dcap,
                                                                    uint32_t* __restrict__ cur_next) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   RBM_PROF_BEGIN(P);
@@ -1805,11 +1831,10 @@ static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) bucket_pair_kernel
     const uint32_t dg = kn >> osh;
     const uint32_t slot = gbase[dg] + (j - off[dg]);
     if (slot >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
-    const uint32_t g = out_seg(P, dg, blockIdx.x) * dcap + slot;
-    dst.id[g] = id_l[e];
-    dst.key[g] = kn;
+    T xo[D];
 #pragma unroll
-    for (int c = 0; c < D; ++c) dst.x[c][g] = xs.at(c, e);
+    for (int c = 0; c < D; ++c) xo[c] = xs.at(c, e);
+    out_put<T, D>(dst, out_seg(P, dg, blockIdx.x), dcap, slot, id_l[e], kn, xo);
   }
   RBM_PROF(P, 7);
   if (P.prof && threadIdx.x == 0) atomicAdd(&P.prof[63], 1ull);
@@ -1859,7 +1884,7 @@ template <typename T, int D, int KK, int INTEG, int BLOCK, int ITEMS>
 static __global__ void __launch_bounds__(BLOCK, 1) pair_persist_kernel(const __grid_constant__ DevParams P,
                                                                        State<T, D> src, uint32_t scap,
                                                                        const uint32_t* __restrict__ S,
-                                                                       State<T, D> dst, uint32_t dcap,
+                                                                       const __grid_constant__ OutDst<T, D> dst, uint32_t dcap,
                                                                        uint32_t* __restrict__ cur_next) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t nsb = 1u << P.SB;

@@ -18,6 +18,10 @@ caller-owned workspaces (offsets from rbm_part_info_get):
   LoopbackExchange  all G ranks in one process on one device: plain device
                     copies, run in stream order (no kernel waits on another
                     rank), used to test the G > 1 kernels on one GPU
+
+fused=True (either exchange, G <= 8): the kernels store the records straight
+into the destination rank's receive buffer (peer memory over NVLink, mapped
+with CUDA IPC by DistExchange) and exchange R disappears.
 """
 from __future__ import annotations
 
@@ -49,6 +53,8 @@ def _lib():
         for name in ("rbm_part_prologue", "rbm_part_phase1", "rbm_part_phase2"):
             f = getattr(L, name)
             f.restype, f.argtypes = C.c_int, [C.c_void_p]
+        L.rbm_part_set_peers.restype = C.c_int
+        L.rbm_part_set_peers.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.c_uint32]
         _sig_done = True
     return L
 
@@ -57,6 +63,11 @@ def rbm_part_info_get(cfg: R.RbmConfig) -> RbmPartInfo:
     out = RbmPartInfo()
     R._check(_lib().rbm_part_info_get(C.byref(cfg), C.byref(out)))
     return out
+
+
+def rbm_part_set_peers(ctx, peer_ws_ptrs):
+    arr = (C.c_uint64 * len(peer_ws_ptrs))(*[int(p) for p in peer_ws_ptrs])
+    R._check(_lib().rbm_part_set_peers(ctx, arr, len(peer_ws_ptrs)), ctx)
 
 
 def rbm_part_prologue(ctx):
@@ -95,7 +106,16 @@ class RankBuffers:
 
 
 class LoopbackExchange:
-    """All G ranks in this process (one device): exchanges are device copies."""
+    """All G ranks in this process (one device): exchanges are device copies.
+    With fused=True the records are already in place (the kernels stored them
+    into the peers' receive buffers); only the counts are gathered."""
+
+    def __init__(self, fused: bool = False):
+        self.fused = fused
+
+    def peers(self, ranks):
+        """Workspace base of every rank, as usable from this device."""
+        return [b.ws.data_ptr() for b in ranks]
 
     def counts_records(self, ranks):
         G = len(ranks)
@@ -103,6 +123,8 @@ class LoopbackExchange:
         for dst in ranks:
             for s, src in enumerate(ranks):
                 dst.counts_all[s * nb:(s + 1) * nb].copy_(src.counts_send)
+        if self.fused:
+            return
         for a in range(ranks[0].info.narrays):
             cb = ranks[0].chunk_bytes[a]
             for r, src in enumerate(ranks):
@@ -117,14 +139,36 @@ class LoopbackExchange:
 class DistExchange:
     """One rank per process over torch.distributed (NCCL on GPUs, gloo on CPU)."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, fused: bool = False):
         import torch.distributed as dist
-        self.dist, self.group = dist, group
+        self.dist, self.group, self.fused = dist, group, fused
+        self._peer_tensors = []
+
+    def peers(self, ranks):
+        """Fused mode: map every rank's workspace into this process (CUDA IPC,
+        peer access over NVLink) and return the base pointers."""
+        from torch.multiprocessing.reductions import reduce_tensor
+        (me,) = ranks
+        G = int(me.info.world_size)
+        fn, args = reduce_tensor(me.ws)
+        allh = [None] * G
+        self.dist.all_gather_object(allh, (fn, args), group=self.group)
+        ptrs = []
+        for j, (f, a) in enumerate(allh):
+            if j == me.rank:
+                ptrs.append(me.ws.data_ptr())
+            else:
+                t = f(*a)
+                self._peer_tensors.append(t)
+                ptrs.append(t.data_ptr())
+        return ptrs
 
     def counts_records(self, ranks):
         (me,) = ranks
         d = self.dist
         d.all_gather_into_tensor(me.counts_all, me.counts_send, group=self.group)
+        if self.fused:
+            return
         for a in range(me.info.narrays):
             d.all_to_all_single(me.recv[a], me.send[a], group=self.group)
 
@@ -159,10 +203,34 @@ class PartitionedRBM:
             assert info.ws_bytes == s.ws_bytes
             self.systems.append(s)
             self.bufs.append(RankBuffers(s.ws, info))
+        if getattr(exchange, "fused", False):
+            exchange.fused = False
+            if not self.enable_fused():
+                raise RuntimeError("fused exchange: peer workspaces could not be mapped on every rank")
         self.n, self.d = int(self.cfg["n"]), int(self.cfg["d"])
         self.dtype = self.systems[0].dtype
         self.device = self.systems[0].device
         self.started = False
+
+    def enable_fused(self) -> bool:
+        """Map every rank's workspace (collective under torch.distributed) and
+        switch the kernels to storing records straight into the peers'
+        receive buffers.  All ranks agree; on any failure none switches."""
+        torch = self.torch
+        ok, ptrs = 1, None
+        try:
+            ptrs = self.exchange.peers(self.bufs)
+        except Exception:
+            ok = 0
+        if isinstance(self.exchange, DistExchange):
+            t = torch.tensor([ok], dtype=torch.int32, device=self.device)
+            self.exchange.dist.all_reduce(t, op=self.exchange.dist.ReduceOp.MIN, group=self.exchange.group)
+            ok = int(t.item())
+        if ok:
+            for s in self.systems:
+                rbm_part_set_peers(s.ctx, ptrs)
+            self.exchange.fused = True
+        return bool(ok)
 
     def set_state(self, x_full):
         """X_0 in id order (N x d, host array or device tensor): each rank takes its ids."""

@@ -29,6 +29,7 @@ EXPORTS = ["rbm_workspace_size", "rbm_init", "rbm_set_state", "rbm_step", "rbm_r
            "rbm_debug_permutation", "rbm_debug_slots", "rbm_debug_philox", "rbm_last_error",
            "rbm_destroy", "rbm_kernel_name", "rbm_timing_begin", "rbm_timing_end",
            "rbm_part_info_get", "rbm_part_prologue", "rbm_part_phase1", "rbm_part_phase2",
+           "rbm_part_set_peers",
            "rbm_direct_workspace_size", "rbm_direct_reset", "rbm_direct_run", "rbm_direct_sync"]
 
 

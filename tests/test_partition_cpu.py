@@ -33,16 +33,16 @@ def _bufs(G, torch_mod=torch):
     return out
 
 
-def _expected(G):
+def _expected(G, fused=False):
     from paper_1812_10575_b200 import partition as PT
     bufs = _bufs(G)
-    ex = PT.LoopbackExchange()
+    ex = PT.LoopbackExchange(fused=fused)
     ex.halo(bufs)
     ex.counts_records(bufs)
     return bufs
 
 
-def _worker(rank, G, port, q):
+def _worker(rank, G, port, q, fused=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     import torch.distributed as dist
@@ -50,10 +50,10 @@ def _worker(rank, G, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=G)
     try:
         me = _bufs(G)[rank]
-        ex = PT.DistExchange()
+        ex = PT.DistExchange(fused=fused)
         ex.halo([me])
         ex.counts_records([me])
-        want = _expected(G)[rank]
+        want = _expected(G, fused)[rank]
         ok = all(torch.equal(a, b) for a, b in zip(me.recv, want.recv))
         ok = ok and torch.equal(me.counts_all, want.counts_all)
         ok = ok and torch.equal(me.halo_recv, want.halo_recv)
@@ -69,14 +69,16 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("G", [2, 4])
-def test_dist_exchange_matches_loopback_gloo(G):
+@pytest.mark.parametrize("G,fused", [(2, False), (4, False), (2, True)])
+def test_dist_exchange_matches_loopback_gloo(G, fused):
+    """fused=True: only the counts move (the records were stored in place by
+    the kernels); the receive regions must stay untouched."""
     from paper_1812_10575_b200 import build
     build.build()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, G, port, q)) for r in range(G)]
+    procs = [ctx.Process(target=_worker, args=(r, G, port, q, fused)) for r in range(G)]
     for p in procs:
         p.start()
     for p in procs:

@@ -127,3 +127,21 @@ def test_partitioned_protocol_errors(PT):
     with pytest.raises(R.RbmError):
         PT.rbm_part_prologue(s.ctx)    # twice
     s.close()
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+@pytest.mark.parametrize("name,cfg", [CASES[0], CASES[2], CASES[4], CASES[7]], ids=["c5p2", "c5p32", "c3", "ragged5"])
+def test_fused_exchange_bit_identical(PT, name, cfg, G):
+    """G9: the bucket step / straddle / prologue store their records straight
+    into the destination ranks' receive buffers (double-buffered by step
+    parity); the result is bit-identical to one GPU and to the NCCL form."""
+    if cfg["n"] // G < max(1024, 16 * cfg["p"]):
+        pytest.skip("too few particles per rank")
+    steps = 6
+    a = single(cfg, steps)
+    ps = PT.PartitionedRBM(cfg, G, range(G), PT.LoopbackExchange(fused=True))
+    ps.run(steps)
+    b = ps.gather().cpu().numpy()
+    ps.sync()
+    ps.close()
+    assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
