@@ -21,8 +21,8 @@ SRC = os.path.join(HERE, "rbm_oracle.c")
 LIB = os.path.join(HERE, "librbm_oracle.so")
 
 KERNELS = {"zero": 0, "dyson": 1, "coulomb": 2, "bounded_confidence": 3,
-           "gauss_attr_rep": 4, "coulomb_reg": 5, "smooth": 6}
-INITS = {"user": 0, "normal": 1, "box": 2, "sphere": 3, "mixture": 4}
+           "gauss_attr_rep": 4, "coulomb_reg": 5, "smooth": 6, "linear": 7}
+INITS = {"user": 0, "normal": 1, "box": 2, "sphere": 3, "mixture": 4, "abs_normal": 5}
 
 
 class OracleCfg(C.Structure):
@@ -30,7 +30,7 @@ class OracleCfg(C.Structure):
         ("d", C.c_uint32), ("p", C.c_uint32), ("n", C.c_uint64),
         ("scheme", C.c_int32), ("integrator", C.c_int32), ("kernel", C.c_int32),
         ("potential", C.c_int32), ("constraint", C.c_int32), ("fp32", C.c_int32),
-        ("init_kind", C.c_int32), ("replica", C.c_uint32), ("pad0", C.c_uint32),
+        ("init_kind", C.c_int32), ("replica", C.c_uint32), ("noise", C.c_int32),
         ("kparam", C.c_double * 4), ("vparam", C.c_double * 2), ("iparam", C.c_double * 8),
         ("sigma", C.c_double), ("dt", C.c_double), ("seed", C.c_uint64),
     ]
@@ -97,6 +97,7 @@ def make_cfg(cfg: dict) -> OracleCfg:
     c.fp32 = 1 if cfg.get("dtype", "f64") == "f32" else 0
     c.init_kind = INITS[cfg.get("init", "normal")]
     c.replica = int(cfg.get("replica", 0))
+    c.noise = {"additive": 0, "geometric": 1}[cfg.get("noise", "additive")]
     for i, v in enumerate(cfg.get("kparam", [])):
         c.kparam[i] = float(v)
     vp = cfg.get("vparam", [1.0])

@@ -43,7 +43,7 @@ typedef struct {
   int32_t fp32;        /* 1: product works in fp32 (uniform map + window test) */
   int32_t init_kind;   /* 1 normal, 2 box, 3 sphere, 4 gaussian mixture */
   uint32_t replica;
-  uint32_t pad0;
+  int32_t noise;       /* 0 additive sigma dB; 1 multiplicative sigma X dB (Sec. 5.2.1) */
   double kparam[4];
   double vparam[2];
   double iparam[8];
@@ -52,7 +52,7 @@ typedef struct {
 } oracle_cfg;
 
 enum { K_ZERO = 0, K_DYSON = 1, K_COULOMB = 2, K_BOUNDED_CONF = 3,
-       K_GAUSS_AR = 4, K_COULOMB_REG = 5, K_SMOOTH = 6 };
+       K_GAUSS_AR = 4, K_COULOMB_REG = 5, K_SMOOTH = 6, K_LINEAR = 7 };
 enum { TAG_KEY = 0, TAG_NOISE = 1, TAG_INIT = 2, TAG_INIT_AUX = 3,
        TAG_SLOT = 4, TAG_NOISE_SLOT = 5 };
 
@@ -170,6 +170,8 @@ static void ok_kernel(const oracle_cfg* c, const double* z, double* out) {
     }
     case K_SMOOTH: /* z/(1+|z|^2) */
       s = 1.0 / (1.0 + r2); break;
+    case K_LINEAR: /* -kappa z: quadratic trading potential phi = y^2/2 */
+      s = -c->kparam[0]; break;
     default: s = NAN;
   }
   for (uint32_t k = 0; k < d; ++k) out[k] = s * z[k];
@@ -242,6 +244,10 @@ int oracle_init(const oracle_cfg* c, double* x) {
         for (uint32_t k = 0; k < d; ++k) xi[k] = z[k] / r;
         break;
       }
+      case 5: /* |normal(mean, std)|: the wealth model's X = |Y|, Y ~ N(0,1) */
+        normals(c, 0, (uint32_t)i, 0, TAG_INIT, z);
+        for (uint32_t k = 0; k < d; ++k) xi[k] = fabs(c->iparam[0] + c->iparam[1] * z[k]);
+        break;
       case 4: { /* equal-weight Gaussian mixture (D:14) */
         uint32_t w[4];
         philox_block(c, (uint32_t)i, 1, 0, TAG_INIT_AUX, w);
@@ -347,7 +353,9 @@ static void em_member(const oracle_cfg* c, const double* x, const double* f,
     for (uint32_t k = 0; k < d; ++k) { drift[k] -= a * x[k]; zz[k] -= b * x[k]; }
   }
   double sq = c->sigma * sqrt(c->dt);
-  for (uint32_t k = 0; k < d; ++k) xn[k] = x[k] + c->dt * drift[k] + sq * zz[k];
+  /* multiplicative noise sigma X dB: Ito Euler-Maruyama term sigma x sqrt(dt) z */
+  for (uint32_t k = 0; k < d; ++k)
+    xn[k] = x[k] + c->dt * drift[k] + sq * (c->noise == 1 ? x[k] * zz[k] : zz[k]);
 }
 
 static void renormalise(const oracle_cfg* c, double* x) {
@@ -370,6 +378,10 @@ void oracle_pair_flow(const oracle_cfg* c, const double* xi, const double* xj,
   if (c->kernel == K_DYSON) {
     double s = D[0] >= 0.0 ? 1.0 : -1.0;
     Dn[0] = s * sqrt(D[0] * D[0] + 4.0 * tau);
+  } else if (c->kernel == K_LINEAR) {
+    /* dD/dt = K(D) - K(-D) = -2 kappa D (wealth trading): D' = D e^{-2 kappa tau} */
+    double e = exp(-2.0 * c->kparam[0] * tau);
+    for (uint32_t k = 0; k < d; ++k) Dn[k] = D[k] * e;
   } else { /* K_COULOMB */
     double r2 = 0.0;
     for (uint32_t k = 0; k < d; ++k) r2 += D[k] * D[k];
@@ -380,12 +392,18 @@ void oracle_pair_flow(const oracle_cfg* c, const double* xi, const double* xj,
   for (uint32_t k = 0; k < d; ++k) { yi[k] = mid[k] + 0.5 * Dn[k]; yj[k] = mid[k] - 0.5 * Dn[k]; }
 }
 
-/* split step, second half: x' = y - tau grad V(y) + sigma sqrt(tau) z */
+/* split step, second half: x' = y - tau grad V(y) + sigma sqrt(tau) z;
+ * multiplicative noise ("solved by the splitting strategy" P:1175):
+ * the exact geometric Brownian motion step x' = w exp(sigma sqrt(tau) z - sigma^2 tau/2),
+ * w = y - tau grad V(y) */
 static void split_member(const oracle_cfg* c, const double* y, const double* z, double* xn) {
   double g[3];
   grad_v(c, y, g);
   double sq = c->sigma * sqrt(c->dt);
-  for (uint32_t k = 0; k < c->d; ++k) xn[k] = y[k] - c->dt * g[k] + sq * z[k];
+  for (uint32_t k = 0; k < c->d; ++k) {
+    double w = y[k] - c->dt * g[k];
+    xn[k] = (c->noise == 1) ? w * exp(sq * z[k] - 0.5 * c->sigma * c->sigma * c->dt) : w + sq * z[k];
+  }
   if (c->constraint == 1) renormalise(c, xn);
 }
 

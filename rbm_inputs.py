@@ -64,6 +64,17 @@ def smooth_test(n: int, p: int = 2, beta: float = 1.0, dtype: str = "f64", seed:
                 init="normal", iparam=[0.0, 1.0], steps=128)
 
 
+def wealth(n: int = 10**5, integrator: str = "split", seed: int = 1, kappa: float = 1.0,
+           diff: float = 1.0, dtype: str = "f64") -> dict:
+    """Wealth model (Sec. 5.2.1): dY = -kappa (Y - Y_theta) dt +
+    sqrt(2D) Y dB (quadratic trading phi = y^2/2, multiplicative noise), RBM-1
+    with p = 2 solved by splitting; X_0 = |N(0,1)|; tau = 1e-3, T = 3."""
+    return dict(d=1, n=n, p=2, dtype=dtype, scheme="rbm1", integrator=integrator,
+                kernel="linear", kparam=[kappa], potential="none", vparam=[1.0],
+                constraint="none", noise="geometric", sigma=math.sqrt(2.0 * diff), dt=1e-3,
+                seed=seed, init="abs_normal", iparam=[0.0, 1.0], steps=3000)
+
+
 ALL = {"C1": c1_dyson, "C2": c2_sphere, "C3": c3_opinion, "C4": c4_aggregation, "C5": c5_coulomb_reg}
 
 

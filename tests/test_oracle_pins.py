@@ -569,3 +569,81 @@ def test_sphere_stays_on_sphere(O):
     x = O.init(cfg)
     x = O.run(cfg, x, 0, 20)
     assert np.allclose(np.linalg.norm(x, axis=1), 1.0, atol=1e-14)
+
+
+# ----------------------------------------------------- wealth model (row f4)
+def inv_gamma2_cdf(y, beta):
+    """Inverse-Gamma(shape 2, scale beta) CDF: e^{-beta/y} (1 + beta/y) (P:1155-1158
+    with kappa = D = 1: rho = beta^2 y^{-3} e^{-beta/y})."""
+    y = np.maximum(np.asarray(y, np.float64), 1e-300)
+    return np.exp(-beta / y) * (1.0 + beta / y)
+
+
+def test_linear_pair_flow_closed_form_and_rk4(O):
+    """Wealth trading pair flow: D' = D e^{-2 kappa tau}, midpoint kept."""
+    c = RI.wealth(n=2, kappa=0.7)
+    xi, xj = np.array([2.5]), np.array([-0.5])
+    for tau in (1e-3, 0.1, 1.0):
+        yi, yj = O.pair_flow(c, xi, xj, tau)
+        assert abs((yi - yj)[0] - 3.0 * math.exp(-1.4 * tau)) < 1e-14
+        assert abs((yi + yj)[0] - 2.0) < 1e-14
+    # RK4 of dxi = -k(xi-xj), dxj = -k(xj-xi)
+    a, b, k, h = 2.5, -0.5, 0.7, 1e-3
+    for _ in range(1000):
+        def f(u, v):
+            return -k * (u - v), -k * (v - u)
+        k1 = f(a, b); k2 = f(a + h / 2 * k1[0], b + h / 2 * k1[1])
+        k3 = f(a + h / 2 * k2[0], b + h / 2 * k2[1]); k4 = f(a + h * k3[0], b + h * k3[1])
+        a += h / 6 * (k1[0] + 2 * k2[0] + 2 * k3[0] + k4[0])
+        b += h / 6 * (k1[1] + 2 * k2[1] + 2 * k3[1] + k4[1])
+    yi, yj = O.pair_flow(c, xi, xj, 1.0)
+    assert abs(yi[0] - a) < 1e-10 and abs(yj[0] - b) < 1e-10
+
+
+def test_geometric_noise_step_is_exact_gbm(O):
+    """Split second half with multiplicative noise: x' = y exp(s sqrt(t) z - s^2 t/2),
+    the exact GBM step: mean factor 1, log-factor variance s^2 t (checked on
+    one split step of a pair with equal members, so the pair flow is the identity)."""
+    c = dict(RI.wealth(n=2), dt=0.04)
+    s2t = c["sigma"] ** 2 * c["dt"]
+    logs = []
+    for m in range(4000):
+        x = np.array([[1.0], [1.0]])
+        y = O.rbm1_step(c, x, m)
+        logs.extend(np.log(y.ravel()))
+        z = np.array([O.noise(c, i, m)[0] for i in range(2)])
+        assert np.allclose(y.ravel(), np.exp(math.sqrt(s2t) * z - 0.5 * s2t), rtol=1e-14)
+    logs = np.array(logs)
+    assert abs(logs.mean() + 0.5 * s2t) < 4 * math.sqrt(s2t / logs.size)
+    assert abs(logs.var() / s2t - 1.0) < 0.06
+    assert abs(np.exp(logs).mean() - 1.0) < 4 * math.sqrt((math.exp(s2t) - 1) / logs.size)
+
+
+def test_linear_em_conserves_pair_sums(O):
+    c = dict(RI.wealth(n=1000, integrator="em"), sigma=0.0)
+    x = O.init(c)
+    y = O.rbm1_step(c, x, 0)
+    assert abs(x.sum() - y.sum()) < 1e-10
+    # EM with multiplicative noise: x' = x - k dt (x - x_theta) + s x sqrt(dt) z
+    c2 = RI.wealth(n=2, integrator="em")
+    x = np.array([[1.5], [0.25]])
+    y = O.rbm1_step(c2, x, 3)
+    z = [O.noise(c2, i, 3)[0] for i in range(2)]
+    sq = c2["sigma"] * math.sqrt(c2["dt"])
+    assert abs(y[0, 0] - (1.5 - 1e-3 * 1.25 + sq * 1.5 * z[0])) < 1e-15
+    assert abs(y[1, 0] - (0.25 + 1e-3 * 1.25 + sq * 0.25 * z[1])) < 1e-15
+
+
+def test_wealth_reaches_inverse_gamma(O):
+    """Fig. wealth (P:1161-1179): RBM-1, p=2, splitting, tau=1e-3, T=3 from
+    X_0 = |N(0,1)|: the empirical law matches the inverse-Gamma equilibrium
+    (shape kappa/D+1 = 2, scale kappa eta/D) with eta = sqrt(2/pi) the mean wealth."""
+    c = RI.wealth(n=20_000, seed=2)
+    x = O.init(c)
+    eta = math.sqrt(2.0 / math.pi)
+    assert abs(x.mean() - eta) < 4 * math.sqrt((1 - 2 / math.pi) / c["n"])
+    x = O.run(c, x, 0, 3000).ravel()
+    s = np.sort(x)
+    ks = np.max(np.abs(np.arange(1, s.size + 1) / s.size - inv_gamma2_cdf(s, eta)))
+    assert ks < 0.03, ks
+    assert np.all(x > 0)
