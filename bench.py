@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C5", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--workload", default="C5", choices=["C1", "C2", "C3", "C4", "C5", "wealth"])
     ap.add_argument("--p", type=int, default=None, help="batch size override (C5: 2, 8, 32)")
     ap.add_argument("--scheme", default="rbm1", choices=["rbm1", "rbmr"])
     ap.add_argument("--n", type=int, default=None, help="particles per GPU override")
@@ -64,6 +64,8 @@ def workload(args, rank: int) -> dict:
         kw["n"] = args.n
     if args.workload == "C5":
         cfg = RI.c5_coulomb_reg(p=args.p or 2, **kw)
+    elif args.workload == "wealth":
+        cfg = RI.wealth(**{k: v for k, v in kw.items() if k != "scheme"})
     else:
         cfg = RI.ALL[args.workload](**kw)
         if args.p:
@@ -186,7 +188,8 @@ def config_dict(args, cfg, world):
     return {"workload": f"{args.workload} " + {
         "C1": "Dyson Brownian motion", "C2": "Thomson-type Coulomb on S^2",
         "C3": "bounded-confidence opinion", "C4": "2-D Gaussian aggregation",
-        "C5": "3-D regularised Coulomb, partitioned-system size per GPU"}[args.workload],
+        "C5": "3-D regularised Coulomb, partitioned-system size per GPU",
+        "wealth": "wealth model (paper Sec. 5.2.1, row f4)"}[args.workload],
         "n_per_gpu": cfg["n"], "d": cfg["d"], "p": cfg["p"], "scheme": cfg["scheme"],
         "kernel": cfg["kernel"], "integrator": cfg["integrator"], "dt": cfg["dt"],
         "sigma": cfg["sigma"],

@@ -85,8 +85,15 @@ typedef enum {
   RBM_K_BOUNDED_CONFIDENCE = 3, /* -a z 1{|z|<r}, kparam={a, r} (Eq. 5.12) */
   RBM_K_GAUSS_ATTR_REP = 4,     /* z e^{-|z|^2/2} - z e^{-|z|^2/8}/4 (BASELINE.json C4)       */
   RBM_K_COULOMB_REG = 5,        /* z/(|z|^2+eps)^{3/2}, kparam={eps} (BASELINE.json C5)       */
-  RBM_K_SMOOTH_TEST = 6         /* z/(1+|z|^2)                             */
+  RBM_K_SMOOTH_TEST = 6,        /* z/(1+|z|^2)                             */
+  RBM_K_LINEAR = 7              /* -kappa z, kparam={kappa}: wealth trading phi=y^2/2 */
 } rbm_kernel;
+
+/* Noise term of Eq. (1.2): additive sigma dB^i, or multiplicative sigma X^i dB^i
+ * (componentwise; the wealth model, Sec. 5.2.1).  With the
+ * split integrator the multiplicative step is the exact geometric Brownian
+ * motion x' = w exp(sigma sqrt(dt) z - sigma^2 dt / 2). */
+typedef enum { RBM_NOISE_ADDITIVE = 0, RBM_NOISE_GEOMETRIC = 1 } rbm_noise;
 
 typedef enum { RBM_V_NONE = 0, RBM_V_HARMONIC = 1 /* beta|x|^2/2, vparam={beta} */ } rbm_potential;
 typedef enum { RBM_CONSTRAINT_NONE = 0, RBM_CONSTRAINT_UNIT_SPHERE = 1 /* d=3 */ } rbm_constraint;
@@ -98,7 +105,8 @@ typedef enum {
   RBM_INIT_NORMAL = 1,        /* iparam = {mean, std}                                */
   RBM_INIT_UNIFORM_BOX = 2,   /* iparam = {a, b}: U[a,b]^d                           */
   RBM_INIT_UNIFORM_SPHERE = 3,/* uniform on S^{d-1}                                  */
-  RBM_INIT_GAUSS_MIXTURE = 4  /* iparam = {K, std, lo, hi}: equal weights, centres U[lo,hi]^d */
+  RBM_INIT_GAUSS_MIXTURE = 4, /* iparam = {K, std, lo, hi}: equal weights, centres U[lo,hi]^d */
+  RBM_INIT_ABS_NORMAL = 5     /* iparam = {mean, std}: |mean + std z| (wealth) */
 } rbm_init_kind;
 
 typedef enum { RBM_MEM_DEVICE = 0, RBM_MEM_HOST = 1 } rbm_mem;
@@ -126,6 +134,7 @@ typedef struct {
   int32_t world_size;    /* 1, or G = 2..64 (power of two): partitioned single system, see rbm_part_* */
   int32_t rank;          /* 0..G-1: this process's rank (one GPU per rank) */
   uint32_t debug_bucket_cap; /* 0 = automatic; >0 forces the per-bucket smem capacity (tests) */
+  uint32_t noise;        /* rbm_noise */
 } rbm_config;
 
 /* Bytes of device workspace rbm_init() needs for this config.

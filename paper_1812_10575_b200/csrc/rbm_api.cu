@@ -79,6 +79,11 @@ void fill_params(const rbm_config& k, DevParams& P) {
   P.dtf = (float)P.dt; P.sqf = (float)P.sq;
   P.invp = 1.0 / (double)(k.p - 1);
   P.invpf = (float)P.invp;
+  P.geo_noise = k.noise == RBM_NOISE_GEOMETRIC ? 1u : 0u;
+  P.half_s2dt = 0.5 * k.sigma * k.sigma * k.dt;
+  P.lin_decay = std::exp(-2.0 * k.kparam[0] * k.dt);
+  P.half_s2dtf = (float)P.half_s2dt;
+  P.lin_decayf = (float)P.lin_decay;
   P.group = 0;
   if (k.p <= 32) { P.group = 1; while (P.group < k.p) P.group <<= 1; }
 }

@@ -13,7 +13,7 @@ namespace rbm {
 enum : uint32_t { TAG_KEY = 0, TAG_NOISE = 1, TAG_INIT = 2, TAG_INIT_AUX = 3,
                   TAG_SLOT = 4, TAG_NOISE_SLOT = 5 };
 enum : int { KK_ZERO = 0, KK_DYSON = 1, KK_COULOMB = 2, KK_BOUNDED = 3,
-             KK_GAUSS_AR = 4, KK_COULOMB_REG = 5, KK_SMOOTH = 6 };
+             KK_GAUSS_AR = 4, KK_COULOMB_REG = 5, KK_SMOOTH = 6, KK_LINEAR = 7 };
 
 // exact u32 division by a runtime-invariant divisor (Granlund-Montgomery):
 // q = n / d for every 32-bit n.
@@ -52,6 +52,9 @@ struct DevParams {
   float kp0f, kp1f, betaf, dtf, sqf;
   double invp;         // 1/(p-1): prefactor of a regular batch (Eq. 2.2)
   float invpf;
+  uint32_t geo_noise;  // multiplicative noise sigma x dB (wealth model)
+  double half_s2dt, lin_decay;     // sigma^2 dt / 2; e^{-2 kappa dt} (linear pair flow)
+  float half_s2dtf, lin_decayf;
   // bucket layout of the partition
   uint32_t B;          // prefix bits of the final buckets
   uint32_t b1, b2;     // digit bits of scatter passes 1 and 2 (b2 = 0: one pass)
@@ -261,6 +264,8 @@ template <> struct Prm<float> {
   __device__ __forceinline__ static float dt(const DevParams& P) { return P.dtf; }
   __device__ __forceinline__ static float sq(const DevParams& P) { return P.sqf; }
   __device__ __forceinline__ static float invp(const DevParams& P) { return P.invpf; }
+  __device__ __forceinline__ static float half_s2dt(const DevParams& P) { return P.half_s2dtf; }
+  __device__ __forceinline__ static float lin_decay(const DevParams& P) { return P.lin_decayf; }
 };
 template <> struct Prm<double> {
   __device__ __forceinline__ static double kp0(const DevParams& P) { return P.kp0; }
@@ -269,6 +274,8 @@ template <> struct Prm<double> {
   __device__ __forceinline__ static double dt(const DevParams& P) { return P.dt; }
   __device__ __forceinline__ static double sq(const DevParams& P) { return P.sq; }
   __device__ __forceinline__ static double invp(const DevParams& P) { return P.invp; }
+  __device__ __forceinline__ static double half_s2dt(const DevParams& P) { return P.half_s2dt; }
+  __device__ __forceinline__ static double lin_decay(const DevParams& P) { return P.lin_decay; }
 };
 
 __device__ __forceinline__ float inv_cube_sqrt(float q) { const float r = rsqrtf(q); return r * r * r; }
@@ -290,6 +297,7 @@ __device__ __forceinline__ T kernel_scale(const T (&z)[D], const DevParams& P) {
   if (KK == KK_GAUSS_AR) return exp(T(-0.5) * r2) - T(0.25) * exp(T(-0.125) * r2);
   if (KK == KK_COULOMB_REG) return inv_cube_sqrt(r2 + Prm<T>::kp0(P));
   if (KK == KK_SMOOTH) return T(1) / (T(1) + r2);
+  if (KK == KK_LINEAR) return -Prm<T>::kp0(P);                                // -kappa z
   return T(0);
 }
 
@@ -336,6 +344,10 @@ __device__ __forceinline__ void em_update(const T (&x)[D], const T (&f)[D], cons
     for (int c = 0; c < D; ++c) { drift[c] -= a * x[c]; zz[c] -= b * x[c]; }
   }
   const T dt = Prm<T>::dt(P), sq = Prm<T>::sq(P);
+  if (P.geo_noise) {  // multiplicative noise: Ito term sigma x sqrt(dt) z
+#pragma unroll
+    for (int c = 0; c < D; ++c) zz[c] *= x[c];
+  }
 #pragma unroll
   for (int c = 0; c < D; ++c) xn[c] = x[c] + dt * drift[c] + sq * zz[c];
   if (normalise && P.constraint == 1) renormalise<T, D>(xn);
@@ -355,6 +367,10 @@ __device__ __forceinline__ void pair_flow(const T (&xi)[D], const T (&xj)[D], bo
     Dn[0] = s * sqrt(Dv[0] * Dv[0] + T(4) * dt);
 #pragma unroll
     for (int c = 1; c < D; ++c) Dn[c] = T(0);
+  } else if (KK == KK_LINEAR) {  // dD/dt = -2 kappa D (wealth trading): D' = D e^{-2 kappa dt}
+    const T e = Prm<T>::lin_decay(P);
+#pragma unroll
+    for (int c = 0; c < D; ++c) Dn[c] = Dv[c] * e;
   } else {  // KK_COULOMB
     T r2 = Dv[0] * Dv[0];
 #pragma unroll
@@ -377,7 +393,9 @@ __device__ __forceinline__ void split_finish(const T (&y)[D], const T (&z)[D], T
 #pragma unroll
   for (int c = 0; c < D; ++c) {
     const T g = (P.potential == 1) ? beta * y[c] : T(0);
-    xn[c] = y[c] - dt * g + sq * z[c];
+    const T w = y[c] - dt * g;
+    // multiplicative noise: the exact geometric Brownian motion step
+    xn[c] = P.geo_noise ? w * exp(sq * z[c] - Prm<T>::half_s2dt(P)) : w + sq * z[c];
   }
   if (normalise && P.constraint == 1) renormalise<T, D>(xn);
 }

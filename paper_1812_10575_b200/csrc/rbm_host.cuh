@@ -251,7 +251,8 @@ inline rbm_status validate(const rbm_config* cfg) {
     return fail(c, RBM_ERR_INVALID_ARG, "p=%u: need p <= 64, or p == n <= 2048", k.p);
   if (k.scheme > RBM_SCHEME_RBMR) return fail(c, RBM_ERR_INVALID_ARG, "scheme %u", k.scheme);
   if (k.integrator > RBM_INTEG_SPLIT_EXACT_PAIR) return fail(c, RBM_ERR_INVALID_ARG, "integrator %u", k.integrator);
-  if (k.kernel > RBM_K_SMOOTH_TEST) return fail(c, RBM_ERR_UNKNOWN_KERNEL, "kernel %u not in registry", k.kernel);
+  if (k.kernel > RBM_K_LINEAR) return fail(c, RBM_ERR_UNKNOWN_KERNEL, "kernel %u not in registry", k.kernel);
+  if (k.noise > RBM_NOISE_GEOMETRIC) return fail(c, RBM_ERR_INVALID_ARG, "noise %u", k.noise);
   if (k.potential > RBM_V_HARMONIC) return fail(c, RBM_ERR_UNKNOWN_KERNEL, "potential %u not in registry", k.potential);
   if (k.constraint > RBM_CONSTRAINT_UNIT_SPHERE) return fail(c, RBM_ERR_INVALID_ARG, "constraint %u", k.constraint);
   if (k.kernel == RBM_K_DYSON && k.d != 1) return fail(c, RBM_ERR_INVALID_ARG, "Dyson kernel needs d=1");
@@ -259,8 +260,8 @@ inline rbm_status validate(const rbm_config* cfg) {
   if (k.constraint == RBM_CONSTRAINT_UNIT_SPHERE && k.d != 3) return fail(c, RBM_ERR_INVALID_ARG, "sphere constraint needs d=3");
   if (k.integrator == RBM_INTEG_SPLIT_EXACT_PAIR) {
     if (k.p != 2) return fail(c, RBM_ERR_INVALID_ARG, "split integrator needs p=2");
-    if (k.kernel != RBM_K_DYSON && k.kernel != RBM_K_COULOMB)
-      return fail(c, RBM_ERR_INVALID_ARG, "split integrator needs the Dyson or Coulomb kernel");
+    if (k.kernel != RBM_K_DYSON && k.kernel != RBM_K_COULOMB && !(k.kernel == RBM_K_LINEAR && k.d == 1))
+      return fail(c, RBM_ERR_INVALID_ARG, "split integrator needs the Dyson, Coulomb or (d=1) linear kernel");
     if (k.scheme == RBM_SCHEME_RBM1 && (k.n % 2))
       return fail(c, RBM_ERR_INVALID_ARG, "split integrator with RBM-1 needs even n");
   }
@@ -268,7 +269,7 @@ inline rbm_status validate(const rbm_config* cfg) {
   if (!(k.dt > 0.0) || !std::isfinite(k.dt)) return fail(c, RBM_ERR_INVALID_ARG, "dt must be finite and > 0");
   if (k.kernel == RBM_K_COULOMB_REG && !(k.kparam[0] > 0.0)) return fail(c, RBM_ERR_INVALID_ARG, "coulomb_reg needs kparam[0]=eps > 0");
   if (k.kernel == RBM_K_BOUNDED_CONFIDENCE && !(k.kparam[1] > 0.0)) return fail(c, RBM_ERR_INVALID_ARG, "bounded confidence needs kparam[1]=radius > 0");
-  if (k.init > RBM_INIT_GAUSS_MIXTURE) return fail(c, RBM_ERR_INVALID_ARG, "init %u", k.init);
+  if (k.init > RBM_INIT_ABS_NORMAL) return fail(c, RBM_ERR_INVALID_ARG, "init %u", k.init);
   if (k.init == RBM_INIT_UNIFORM_SPHERE && k.d != 3) return fail(c, RBM_ERR_INVALID_ARG, "sphere init needs d=3");
   if (k.init == RBM_INIT_GAUSS_MIXTURE && !(k.iparam[0] >= 1 && k.iparam[0] <= 64))
     return fail(c, RBM_ERR_INVALID_ARG, "mixture needs 1 <= K <= 64");
@@ -802,6 +803,9 @@ EngineBase* make_for_kernel(uint32_t kernel, uint32_t integ) {
     case RBM_K_COULOMB:
       if (D == 3) return integ ? (EngineBase*)new Engine<T, 3, KK_COULOMB, 1>() : new Engine<T, 3, KK_COULOMB, 0>();
       return nullptr;
+    case RBM_K_LINEAR:
+      if (integ) return D == 1 ? (EngineBase*)new Engine<T, 1, KK_LINEAR, 1>() : nullptr;
+      return new Engine<T, D, KK_LINEAR, 0>();
   }
   return nullptr;
 }

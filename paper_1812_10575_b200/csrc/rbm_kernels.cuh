@@ -199,11 +199,11 @@ static __global__ void init_kernel(const __grid_constant__ DevParams P, State<T,
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t id = (uint32_t)(id0 + i);
     double x[3] = {0, 0, 0};
-    if (kind == 1 || kind == 3 || kind == 4) {
+    if (kind == 1 || kind == 3 || kind == 4 || kind == 5) {
       double z[D];
       Normals<double, D>::get(P, id, 0u, TAG_INIT, z);
-      if (kind == 1) {
-        for (int c = 0; c < D; ++c) x[c] = a0 + a1 * z[c];
+      if (kind == 1 || kind == 5) {
+        for (int c = 0; c < D; ++c) x[c] = kind == 5 ? fabs(a0 + a1 * z[c]) : a0 + a1 * z[c];
       } else if (kind == 3) {
         double r2 = 0;
         for (int c = 0; c < D; ++c) r2 += z[c] * z[c];

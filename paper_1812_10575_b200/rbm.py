@@ -21,8 +21,9 @@ STATUS = {0: "RBM_OK", 1: "RBM_ERR_INVALID_ARG", 2: "RBM_ERR_UNKNOWN_KERNEL",
           3: "RBM_ERR_UNSUPPORTED", 4: "RBM_ERR_WORKSPACE", 5: "RBM_ERR_CUDA",
           6: "RBM_ERR_NCCL", 7: "RBM_ERR_NONFINITE", 8: "RBM_ERR_STATE", 9: "RBM_ERR_CAPACITY"}
 KERNELS = {"zero": 0, "dyson": 1, "coulomb": 2, "bounded_confidence": 3,
-           "gauss_attr_rep": 4, "coulomb_reg": 5, "smooth": 6}
-INITS = {"user": 0, "normal": 1, "box": 2, "sphere": 3, "mixture": 4}
+           "gauss_attr_rep": 4, "coulomb_reg": 5, "smooth": 6, "linear": 7}
+INITS = {"user": 0, "normal": 1, "box": 2, "sphere": 3, "mixture": 4, "abs_normal": 5}
+NOISES = {"additive": 0, "geometric": 1}
 MEM_DEVICE, MEM_HOST = 0, 1
 EXPORTS = ["rbm_workspace_size", "rbm_init", "rbm_set_state", "rbm_step", "rbm_run",
            "rbm_gather", "rbm_sync", "rbm_step_index", "rbm_launches_per_step", "rbm_layout",
@@ -48,7 +49,7 @@ class RbmConfig(C.Structure):
         ("kparam", C.c_double * 4), ("vparam", C.c_double * 2), ("iparam", C.c_double * 8),
         ("sigma", C.c_double), ("dt", C.c_double), ("seed", C.c_uint64), ("step0", C.c_uint64),
         ("replica", C.c_uint32), ("world_size", C.c_int32), ("rank", C.c_int32),
-        ("debug_bucket_cap", C.c_uint32),
+        ("debug_bucket_cap", C.c_uint32), ("noise", C.c_uint32),
     ]
 
 
@@ -128,6 +129,7 @@ def make_config(cfg: dict) -> RbmConfig:
     c.world_size = int(cfg.get("world_size", 1))
     c.rank = int(cfg.get("rank", 0))
     c.debug_bucket_cap = int(cfg.get("debug_bucket_cap", 0))
+    c.noise = NOISES[cfg.get("noise", "additive")]
     return c
 
 
