@@ -74,6 +74,7 @@ def lib():
             "oracle_slot_draw": (C.c_uint32, [cfgp, C.c_uint64, C.c_uint32, C.c_uint64]),
             "oracle_rbmr_slots": (C.c_int, [cfgp, C.c_uint64, u32p]),
             "oracle_rbmr_step": (C.c_int, [cfgp, C.c_uint64, f64p]),
+            "oracle_rbmr_seq_step": (C.c_int, [cfgp, C.c_uint64, f64p]),
             "oracle_run": (C.c_int, [cfgp, C.c_uint64, C.c_uint64, f64p]),
         }
         for name, (res, args) in sig.items():
@@ -89,7 +90,7 @@ def make_cfg(cfg: dict) -> OracleCfg:
     c.d = int(cfg["d"])
     c.p = int(cfg["p"])
     c.n = int(cfg["n"])
-    c.scheme = {"rbm1": 0, "rbmr": 1}[cfg.get("scheme", "rbm1")]
+    c.scheme = {"rbm1": 0, "rbmr": 1, "rbmr_seq": 2}[cfg.get("scheme", "rbm1")]
     c.integrator = {"em": 0, "split": 1}[cfg.get("integrator", "em")]
     c.kernel = KERNELS[cfg["kernel"]]
     c.potential = {"none": 0, "harmonic": 1}[cfg.get("potential", "none")]
@@ -217,6 +218,7 @@ def _stepper(name):
 rbm1_step = _stepper("oracle_rbm1_step")
 direct_step = _stepper("oracle_direct_step")
 rbmr_step = _stepper("oracle_rbmr_step")
+rbmr_seq_step = _stepper("oracle_rbmr_seq_step")
 
 
 def run(cfg: dict, x: np.ndarray, m0: int, nsteps: int) -> np.ndarray:

@@ -587,10 +587,63 @@ int oracle_rbmr_step(const oracle_cfg* c, uint64_t m, double* x) {
   return 0;
 }
 
+/* ------------------------------------------------------------------ */
+/* RBM-r' exactly as Algorithm 2 is written: */
+/* within step m, for k = 1 .. ceil(N/p) in order, the batch C_k (the     */
+/* slot draws of oracle_rbmr_slots, D:9) is updated from the CURRENT      */
+/* positions, "set X^i <- Y^i(tau)", before the next batch is drawn.      */
+/* The per-batch solve is the same as RBM-1's (Eq. 2.2 + EM with noise    */
+/* from counter (s, blk, m, TAG_NOISE_SLOT), or the split pair flow).     */
+/* ------------------------------------------------------------------ */
+int oracle_rbmr_seq_step(const oracle_cfg* c, uint64_t m, double* x) {
+  uint64_t n = c->n;
+  uint32_t d = c->d, p = c->p;
+  if (p < 2 || p > n) return 1;
+  uint64_t nb = (n + p - 1) / p, ns = nb * p;
+  uint32_t* js = (uint32_t*)malloc(sizeof(uint32_t) * ns);
+  double* xo = (double*)malloc(sizeof(double) * p * d);
+  if (!js || !xo) return 2;
+  oracle_rbmr_slots(c, m, js);
+  double inv = 1.0 / (double)(p - 1);
+  for (uint64_t b = 0; b < nb; ++b) {
+    uint64_t s0 = b * p;
+    if (c->integrator == 0) {
+      for (uint32_t l = 0; l < p; ++l) {
+        uint32_t i = js[s0 + l];
+        double f[3] = {0, 0, 0}, z[3];
+        for (uint32_t l2 = 0; l2 < p; ++l2) {
+          if (l2 == l) continue;
+          double zz[3], kz[3];
+          diff(c, x + (uint64_t)i * d, x + (uint64_t)js[s0 + l2] * d, zz);
+          ok_kernel(c, zz, kz);
+          for (uint32_t k = 0; k < d; ++k) f[k] += kz[k];
+        }
+        for (uint32_t k = 0; k < d; ++k) f[k] *= inv;
+        normals(c, c->fp32, (uint32_t)(s0 + l), m, TAG_NOISE_SLOT, z);
+        em_member(c, x + (uint64_t)i * d, f, z, xo + (uint64_t)l * d);
+        if (c->constraint == 1) renormalise(c, xo + (uint64_t)l * d);
+      }
+    } else {
+      uint32_t i = js[s0], j = js[s0 + 1];
+      double y[2][3], z[3];
+      oracle_pair_flow(c, x + (uint64_t)i * d, x + (uint64_t)j * d, c->dt, y[0], y[1]);
+      for (uint32_t l = 0; l < 2; ++l) {
+        normals(c, c->fp32, (uint32_t)(s0 + l), m, TAG_NOISE_SLOT, z);
+        split_member(c, y[l], z, xo + (uint64_t)l * d);
+      }
+    }
+    for (uint32_t l = 0; l < p; ++l)  /* X^i <- Y^i(tau) for the batch's members */
+      for (uint32_t k = 0; k < d; ++k) x[(uint64_t)js[s0 + l] * d + k] = xo[(uint64_t)l * d + k];
+  }
+  free(js); free(xo);
+  return 0;
+}
+
 /* convenience: steps m0 .. m0+nsteps-1 of the configured scheme */
 int oracle_run(const oracle_cfg* c, uint64_t m0, uint64_t nsteps, double* x) {
   for (uint64_t s = 0; s < nsteps; ++s) {
-    int rc = (c->scheme == 0) ? oracle_rbm1_step(c, m0 + s, x) : oracle_rbmr_step(c, m0 + s, x);
+    int rc = (c->scheme == 0) ? oracle_rbm1_step(c, m0 + s, x)
+             : (c->scheme == 1) ? oracle_rbmr_step(c, m0 + s, x) : oracle_rbmr_seq_step(c, m0 + s, x);
     if (rc) return rc;
   }
   return 0;

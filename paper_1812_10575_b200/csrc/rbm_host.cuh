@@ -51,6 +51,7 @@ struct Layout {
 constexpr int FUSED_BLOCK = 256;
 constexpr int PAIR_BLOCK = 512, PAIR_ITEMS = 5;  // p = 2 lean kernel: capacity <= 2560
 constexpr int PAIRS_BLOCK = 256, PAIRS_ITEMS = 6; // p = 2 lean kernel, small buckets: capacity <= 1536
+constexpr int PAIR3_BLOCK = 256, PAIR3_ITEMS = 10; // p = 2 compact kernel, 3 CTAs per SM: capacity <= 2560
 constexpr int PERSIST_BLOCK = 1024, PERSIST_ITEMS = 3;  // p = 2 persistent kernel: capacity <= 3072
 constexpr uint32_t FUSED_CAP_MAX = 4096;  // fast-path bucket capacity (u16 indices, smem)
 
@@ -387,8 +388,8 @@ struct Engine final : EngineBase {
   }
 
   size_t fu_smem = 0, pr_smem = 0, rs_smem = 0, ps_smem = 0, sp_smem = 0;
-  bool use_pair = false, use_persist = false, use_split = false, use_pair_small = false;
-  size_t prs_smem = 0;
+  bool use_pair = false, use_persist = false, use_split = false, use_pair_small = false, use_pair3 = false;
+  size_t prs_smem = 0, p3_smem = 0;
   // pass-2 splitter configurations: one CTA of 1024 threads per SM with
   // 4096-record tiles (default; measured fastest at C5), or
   // RBM_SPLIT_CFG=small: two CTAs of 512 per SM with 2048-record tiles
@@ -414,6 +415,12 @@ struct Engine final : EngineBase {
     ps_smem = persist_smem_bytes<T, D>(c.L.cap, c.L.SB);
     prs_smem = pr_smem;
     use_pair_small = use_pair && c.L.cap <= (uint32_t)(PAIRS_BLOCK * PAIRS_ITEMS);
+    p3_smem = pair3_smem_bytes<T, D>(c.L.cap, c.L.SB, c.L.b1);
+    {
+      const char* e = std::getenv("RBM_PAIR_KERNEL");  // "pair3": compact, 3 CTAs per SM
+      use_pair3 = use_pair && !use_pair_small && c.L.cap <= (uint32_t)(PAIR3_BLOCK * PAIR3_ITEMS) &&
+                  p3_smem + 2400 <= 74 * 1024 && (e && std::strcmp(e, "pair3") == 0);
+    }
     {
       // "persist": one CTA per SM looping over buckets with double-buffered
       // TMA (measured slower than two one-bucket CTAs per SM; kept selectable)
@@ -482,6 +489,11 @@ struct Engine final : EngineBase {
       if ((s = chk(cudaFuncSetAttribute(pair_persist_kernel<T, D, KK, INTEG, PERSIST_BLOCK, PERSIST_ITEMS>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps_smem),
                    "smem attr persist"))) return s;
+    }
+    if (use_pair3) {
+      if ((s = chk(cudaFuncSetAttribute(bucket_pair3_kernel<T, D, KK, INTEG, PAIR3_BLOCK, PAIR3_ITEMS>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p3_smem),
+                   "smem attr pair3"))) return s;
     }
     if (use_pair_small) {
       if ((s = chk(cudaFuncSetAttribute(bucket_pair_kernel<T, D, KK, INTEG, PAIRS_BLOCK, PAIRS_ITEMS>,
@@ -624,6 +636,9 @@ struct Engine final : EngineBase {
       pair_persist_kernel<T, D, KK, INTEG, PERSIST_BLOCK, PERSIST_ITEMS>
           <<<std::min<uint32_t>(c.L.nbuckets, (uint32_t)num_sms), PERSIST_BLOCK, ps_smem, s>>>(
               c.P, in, c.L.cap2, c.S, out, ocap, cur_next);
+    else if (use_pair3)
+      bucket_pair3_kernel<T, D, KK, INTEG, PAIR3_BLOCK, PAIR3_ITEMS>
+          <<<c.L.nbuckets, PAIR3_BLOCK, p3_smem, s>>>(c.P, in, c.L.cap2, c.S, out, ocap, cur_next);
     else if (use_pair_small)
       bucket_pair_kernel<T, D, KK, INTEG, PAIRS_BLOCK, PAIRS_ITEMS>
           <<<c.L.nbuckets, PAIRS_BLOCK, prs_smem, s>>>(c.P, in, c.L.cap2, c.S, out, ocap, cur_next);

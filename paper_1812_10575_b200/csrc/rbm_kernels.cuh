@@ -147,6 +147,49 @@ __device__ __forceinline__ uint32_t block_excl_scan4(const uint32_t* in, uint32_
   return total;
 }
 
+// exclusive scan of nw*2 u16 counts packed in u32 words (low half first);
+// out[] gets the packed u16 offsets (totals < 2^16).  nw % 4 == 0.  Ends synced.
+template <int BLOCK>
+__device__ __forceinline__ void block_excl_scan_u16x2(const uint32_t* in, uint32_t* out, int nw,
+                                                      uint32_t* wsum) {
+  const int nq = nw >> 2;  // uint4 chunks of 8 counts
+  const int per = (nq + BLOCK - 1) / BLOCK;
+  const int t = threadIdx.x;
+  const int q0 = min(nq, t * per), q1 = min(nq, q0 + per);
+  const uint4* in4 = reinterpret_cast<const uint4*>(in);
+  uint4* out4 = reinterpret_cast<uint4*>(out);
+  uint32_t s = 0;
+  for (int q = q0; q < q1; ++q) {
+    const uint4 v = in4[q];
+    s += (v.x & 0xffffu) + (v.x >> 16) + (v.y & 0xffffu) + (v.y >> 16) + (v.z & 0xffffu) + (v.z >> 16) +
+         (v.w & 0xffffu) + (v.w >> 16);
+  }
+  const uint32_t inc = warp_incl_scan(s);
+  const int lane = t & 31, wp = t >> 5;
+  if (lane == 31) wsum[wp] = inc;
+  __syncthreads();
+  if (wp == 0) {
+    const uint32_t v = (lane < BLOCK / 32) ? wsum[lane] : 0u;
+    const uint32_t vi = warp_incl_scan(v);
+    if (lane < BLOCK / 32) wsum[lane] = vi - v;
+  }
+  __syncthreads();
+  uint32_t run = wsum[wp] + inc - s;
+  for (int q = q0; q < q1; ++q) {
+    const uint4 v = in4[q];
+    const uint32_t c[4] = {v.x, v.y, v.z, v.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t lo = run, hi = run + (c[k] & 0xffffu);
+      o[k] = lo | (hi << 16);
+      run = hi + (c[k] >> 16);
+    }
+    out4[q] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+  __syncthreads();
+}
+
 // position P's batch (reading D:7): returns [b0, b1).  N < 2^32.
 __device__ __forceinline__ void batch_range(uint32_t P, const DevParams& prm, uint32_t& b0,
                                             uint32_t& b1) {
@@ -1765,6 +1808,213 @@ static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) bucket_pair_kernel
     const uint32_t kn = shuffle_key(P, id_l[e], m + 1);
     ta[e] = kn;
     tb[e] = atomicAdd(&cnt[kn >> osh], 1u);
+  }
+  // straddlers: unchanged, to their sorted places in the own gapped range
+  for (uint32_t t = threadIdx.x; t < head + (tri0 - covered); t += BLOCK) {
+    const uint32_t q = t < head ? t : covered + (t - head);
+    const uint32_t e = ord[q];
+    src.id[sb + q] = id_l[e];
+#pragma unroll
+    for (int c = 0; c < D; ++c) src.x[c][sb + q] = xs.at(c, e);
+  }
+  __syncthreads();
+  // run reservations of digits threadIdx.x + r BLOCK, consumed after the batches
+  constexpr int NRES = (1024 + BLOCK - 1) / BLOCK;
+  uint32_t gres[NRES];
+#pragma unroll
+  for (int r = 0; r < NRES; ++r) {
+    const uint32_t i = threadIdx.x + r * BLOCK;
+    const uint32_t h = i < nout ? cnt[i] : 0u;
+    gres[r] = h ? atomicAdd(&cur_next[(size_t)out_seg(P, i, blockIdx.x) * CUR1_STRIDE], h) : 0u;
+  }
+  const uint32_t total = block_excl_scan4<BLOCK>(cnt, off, nout, wsum);
+  RBM_PROF(P, 8);
+  // 5. one thread per pair: Eq. (2.2) + update in place; staging index of each member
+  constexpr int PITEMS = (ITEMS + 1) / 2;
+#pragma unroll
+  for (int k = 0; k < PITEMS; ++k) {
+    const uint32_t j = k * BLOCK + threadIdx.x;
+    if (j < npairs) {
+      const uint32_t q = head + 2 * j;
+      const uint32_t e0 = ord[q], e1 = ord[q + 1];
+      const uint32_t id0 = id_l[e0], id1 = id_l[e1];
+      T x0[D], x1[D], y0[D], y1[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) { x0[c] = xs.at(c, e0); x1[c] = xs.at(c, e1); }
+      pair_update<T, D, KK, INTEG>(P, m, x0, x1, id0, id1, y0, y1);
+      check_finite<T, D>(y0, P, id0, m);
+      check_finite<T, D>(y1, P, id1, m);
+#pragma unroll
+      for (int c = 0; c < D; ++c) { xs.at(c, e0) = y0[c]; xs.at(c, e1) = y1[c]; }
+      inv[off[ta[e0] >> osh] + tb[e0]] = (uint16_t)e0;
+      inv[off[ta[e1] >> osh] + tb[e1]] = (uint16_t)e1;
+    }
+  }
+  if (triple && threadIdx.x == 0) {  // the remainder batch of size 3 (N odd), EM only
+    T xn[3][D];
+    for (uint32_t q = tri0; q < n; ++q)
+      interior_update<T, D, KK, INTEG>(P, m, q, tri0, n, ord, xs, id_l[ord[q]], xn[q - tri0]);
+    for (uint32_t q = tri0; q < n; ++q) {
+      const uint32_t e = ord[q];
+      check_finite<T, D>(xn[q - tri0], P, id_l[e], m);
+#pragma unroll
+      for (int c = 0; c < D; ++c) xs.at(c, e) = xn[q - tri0][c];
+      inv[off[ta[e] >> osh] + tb[e]] = (uint16_t)e;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < NRES; ++r)
+    if (threadIdx.x + r * BLOCK < nout) gbase[threadIdx.x + r * BLOCK] = gres[r];
+  __syncthreads();
+  RBM_PROF(P, 6);
+  // 6. staged slots -> coalesced runs of the step-(m+1) pass-1 buckets
+  for (uint32_t j = threadIdx.x; j < total; j += BLOCK) {
+    const uint32_t e = inv[j];
+    const uint32_t kn = ta[e];
+    const uint32_t dg = kn >> osh;
+    const uint32_t slot = gbase[dg] + (j - off[dg]);
+    if (slot >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
+    T xo[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) xo[c] = xs.at(c, e);
+    out_put<T, D>(dst, out_seg(P, dg, blockIdx.x), dcap, slot, id_l[e], kn, xo);
+  }
+  RBM_PROF(P, 7);
+  if (P.prof && threadIdx.x == 0) atomicAdd(&P.prof[63], 1ull);
+}
+
+// The p = 2 bucket step with a compact shared-memory footprint (packed u16
+// sub-digit counters, u16 staging aliased over the dead composites) so that
+// three 256-thread CTAs -- three buckets in flight -- fit on one SM.
+template <typename T, int D> __host__ __device__ constexpr size_t pair3_smem_bytes(uint32_t cap, uint32_t SB,
+                                                                                  uint32_t b1) {
+  return (size_t)(2 * (((1u << SB) / 2 > (1u << b1)) ? (1u << SB) / 2 : (1u << b1)) + (1u << b1) + 64) * 4 + 16
+         + (size_t)(cap + 8) * 8                                            // ids, keys (TMA windows)
+         + (size_t)D * (((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15)  // x (TMA window, in place)
+         + (size_t)cap * 4                                                 // composites -> tb | inv
+         + (((size_t)cap * 2 + 15) & ~(size_t)15);                         // ord (u16)
+}
+
+template <typename T, int D, int KK, int INTEG, int BLOCK, int ITEMS>
+static __global__ void __launch_bounds__(BLOCK, 3) bucket_pair3_kernel(const __grid_constant__ DevParams P, State<T, D> src,
+                                                                   uint32_t scap,
+                                                                   const uint32_t* __restrict__ S,
+                                                                   const __grid_constant__ OutDst<T, D> dst, uint32_t dcap,
+                                                                   uint32_t* __restrict__ cur_next) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  RBM_PROF_BEGIN(P);
+  const uint32_t b = blockIdx.x;
+  const uint32_t s0 = S[b], n = S[b + 1] - s0, sb = b * scap;
+  if (n == 0) return;
+  const uint32_t nsb = 1u << P.SB;
+  const uint32_t nout = 1u << P.b1;
+  // sub-digit counts and offsets as packed u16 pairs (bucket sizes < 2^16);
+  // the same words later hold the <= 1024 output digit counts / offsets
+  const uint32_t ncw = (nsb / 2 > nout) ? nsb / 2 : nout;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* off = cnt + ncw;
+  uint32_t* gbase = off + ncw;
+  uint32_t* wsum = gbase + nout;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);
+  const uint32_t cap = P.cap;
+  const uint32_t m = (uint32_t)*P.step;
+  for (uint32_t i = threadIdx.x; i < ncw / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
+  if (n > cap) {  // oversized bucket: the global-scratch path with its own 8-bit counters
+    __shared__ uint32_t bigc[2 * 256 + 64];
+    __syncthreads();
+    fused_big_path<T, D, KK, INTEG, BLOCK>(P, src, dst, cur_next, s0, sb, n, m, dcap, bigc, bigc + 256, bigc + 512);
+    return;
+  }
+  unsigned char* p = reinterpret_cast<unsigned char*>(bar + 2);
+  uint32_t* id_l = reinterpret_cast<uint32_t*>(p);
+  p += (size_t)(cap + 8) * 4;
+  uint32_t* key_l = reinterpret_cast<uint32_t*>(p);  // key_m by e; then key_{m+1} by e
+  p += (size_t)(cap + 8) * 4;
+  const uint32_t xst = (uint32_t)((((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15) / sizeof(T));
+  T* xr = reinterpret_cast<T*>(p);
+  p += (size_t)D * xst * sizeof(T);
+  uint32_t* ks = reinterpret_cast<uint32_t*>(p);   // composites (sort); then tb | inv (u16 each)
+  uint16_t* tb = reinterpret_cast<uint16_t*>(ks);
+  uint16_t* inv = tb + cap;
+  uint32_t* ta = key_l;
+  uint16_t* ord = reinterpret_cast<uint16_t*>(ks + cap);
+  load_bucket<T, D>(src, sb, n, id_l, key_l, xr, xst, bar);
+  __syncthreads();
+  mbar_wait(bar, 0);
+  RBM_PROF(P, 0);
+  const SX<T> xs{xr, xst};
+
+  // 1-3. exact (key, id) sort: counting sort on SB sub-digit bits + rank in sub-bucket
+  const uint32_t shsb = 32u - P.B - P.SB;
+  const uint32_t lowmask = (P.lowbits >= 32u) ? 0xffffffffu : ((1u << P.lowbits) - 1u);
+  uint32_t rc[ITEMS], rs[ITEMS];
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const uint32_t e = k * BLOCK + threadIdx.x;
+    if (e < n) {
+      const uint32_t key = key_l[e];
+      const uint32_t sd = (key >> shsb) & (nsb - 1u);
+      rc[k] = ((key & lowmask) << P.idbits) | id_l[e];
+      const uint32_t sh16 = (sd & 1u) << 4;
+      rs[k] = (sd << 16) | ((atomicAdd(&cnt[sd >> 1], 1u << sh16) >> sh16) & 0xffffu);
+    }
+  }
+  __syncthreads();
+  RBM_PROF(P, 1);
+  block_excl_scan_u16x2<BLOCK>(cnt, off, nsb / 2, wsum);
+  RBM_PROF(P, 2);
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const uint32_t e = k * BLOCK + threadIdx.x;
+    if (e < n) {
+      const uint32_t sd = rs[k] >> 16;
+      ks[((off[sd >> 1] >> ((sd & 1u) << 4)) & 0xffffu) + (rs[k] & 0xffffu)] = rc[k];
+    }
+  }
+  __syncthreads();
+  RBM_PROF(P, 3);
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const uint32_t e = k * BLOCK + threadIdx.x;
+    if (e < n) {
+      const uint32_t sd = rs[k] >> 16, sh16 = (sd & 1u) << 4;
+      const uint32_t a = (off[sd >> 1] >> sh16) & 0xffffu, c = (cnt[sd >> 1] >> sh16) & 0xffffu;
+      uint32_t r = a;
+      if (c > 1) {  // sub-buckets hold ~1 element: a short predicated scan
+#pragma unroll
+        for (uint32_t i = 0; i < 4; ++i)
+          if (i < c) r += (ks[a + i] < rc[k]) ? 1u : 0u;
+        for (uint32_t i = 4; i < c; ++i) r += (ks[a + i] < rc[k]) ? 1u : 0u;
+      }
+      ord[r] = (uint16_t)e;
+    }
+  }
+  __syncthreads();
+  RBM_PROF(P, 4);
+  // interior pairs: even global starts in [s0, end), end excludes a final triple (N odd)
+  const uint32_t N = (uint32_t)P.n;
+  const uint32_t pend = (N & 1u) ? N - 3u : N;
+  const uint32_t head = s0 & 1u;                         // local index of the first pair
+  const uint32_t lim = (min(s0 + n, pend) > s0) ? min(s0 + n, pend) - s0 : 0u;
+  const uint32_t npairs = (lim > head) ? (lim - head) / 2 : 0u;
+  const uint32_t covered = head + 2 * npairs;            // [head, covered) are interior
+  const bool triple = (N & 1u) && (pend >= s0) && (N <= s0 + n);
+  const uint32_t tri0 = triple ? pend - s0 : n;          // [tri0, n): the size-3 remainder batch
+  const uint32_t osh = 32u - P.b1;
+  for (uint32_t i = threadIdx.x; i < nout / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
+  if (P.dbg_order)
+    for (uint32_t q = threadIdx.x; q < n; q += BLOCK) P.dbg_order[s0 + q] = id_l[ord[q]];
+  __syncthreads();
+  RBM_PROF(P, 5);
+  // 4. output partition first (key_{m+1} depends on the id only): digit and
+  //    rank of every interior member, so the run reservations below are in
+  //    flight while the batches are computed.  ks is dead: tb = rank by e.
+  for (uint32_t q = head + threadIdx.x; q < n; q += BLOCK) {
+    if (q >= covered && q < tri0) continue;
+    const uint32_t e = ord[q];
+    const uint32_t kn = shuffle_key(P, id_l[e], m + 1);
+    ta[e] = kn;
+    tb[e] = (uint16_t)atomicAdd(&cnt[kn >> osh], 1u);
   }
   // straddlers: unchanged, to their sorted places in the own gapped range
   for (uint32_t t = threadIdx.x; t < head + (tri0 - covered); t += BLOCK) {

@@ -647,3 +647,35 @@ def test_wealth_reaches_inverse_gamma(O):
     ks = np.max(np.abs(np.arange(1, s.size + 1) / s.size - inv_gamma2_cdf(s, eta)))
     assert ks < 0.03, ks
     assert np.all(x > 0)
+
+
+# ------------------------------------- exact sequential RBM-r' (row f2, Alg. 2)
+def test_rbmr_seq_single_batch_equals_jacobi(O):
+    """p = N: one batch per sweep, so Algorithm 2's sequential update and the
+    Jacobi sweep (D:8) are the same map (two independent code paths)."""
+    c = dict(RI.smooth_test(40, p=40), sigma=0.3, scheme="rbmr_seq")
+    x = O.init(c)
+    a = O.rbmr_seq_step(c, x, 5)
+    b = O.rbmr_step(dict(c, scheme="rbmr"), x, 5)
+    assert np.max(np.abs(a - b)) < 1e-14
+
+
+def test_rbmr_seq_conserves_momentum_and_differs_from_jacobi(O):
+    c = dict(RI.smooth_test(1000, p=4), potential="none", sigma=0.0, scheme="rbmr_seq")
+    x = O.init(c)
+    y = O.rbmr_seq_step(c, x, 0)
+    assert abs(y.sum() - x.sum()) < 1e-11  # each batch conserves its sum (odd K, V = 0)
+    j = O.rbmr_step(dict(c, scheme="rbmr"), x, 0)
+    assert np.max(np.abs(y - j)) > 1e-6     # later batches see earlier updates
+
+
+def test_rbmr_seq_dyson_second_moment(O):
+    """P:200 (N/p iterations ~ time tau): the sequential sweep reproduces the
+    Dyson m2(t) closed form like RBM-1 (split, N = 2000, T = 1)."""
+    c = dict(RI.c1_dyson(n=2000, integrator="split", seed=4), scheme="rbmr_seq")
+    x = O.init(c)
+    s2 = c["sigma"] ** 2
+    m20 = float((x ** 2).mean())
+    x = O.run(c, x, 0, 1000)
+    pred = (1 + s2) / 2 + (m20 - (1 + s2) / 2) * math.exp(-2.0)
+    assert abs(float((x ** 2).mean()) - pred) < 0.02
