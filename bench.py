@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C5", choices=["C1", "C2", "C3", "C4", "C5", "wealth"])
     ap.add_argument("--p", type=int, default=None, help="batch size override (C5: 2, 8, 32)")
-    ap.add_argument("--scheme", default="rbm1", choices=["rbm1", "rbmr"])
+    ap.add_argument("--scheme", default="rbm1", choices=["rbm1", "rbmr", "rbmr_seq"])
     ap.add_argument("--n", type=int, default=None, help="particles per GPU override")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

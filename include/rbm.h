@@ -74,7 +74,13 @@ typedef enum {
 } rbm_status;
 
 typedef enum { RBM_F32 = 0, RBM_F64 = 1 } rbm_dtype;
-typedef enum { RBM_SCHEME_RBM1 = 0, RBM_SCHEME_RBMR = 1 } rbm_scheme;
+/* RBM_SCHEME_RBMR_SEQ: Algorithm 2 (RBM-r') exactly as
+ * written: the ceil(N/p) batches of a sweep (the same slot draws as RBMR) are
+ * applied in draw order, each from the positions left by the earlier ones.
+ * Run level by level on the GPU (a batch's level = the longest chain of
+ * earlier batches sharing a member); each rbm_step synchronises the stream
+ * once per sweep to size the levels (no CUDA graph). */
+typedef enum { RBM_SCHEME_RBM1 = 0, RBM_SCHEME_RBMR = 1, RBM_SCHEME_RBMR_SEQ = 2 } rbm_scheme;
 typedef enum { RBM_INTEG_EULER_MARUYAMA = 0, RBM_INTEG_SPLIT_EXACT_PAIR = 1 } rbm_integrator;
 
 /* Interaction kernels K(z), z = X^i - X^j (Eq. 1.2). */
@@ -187,7 +193,7 @@ rbm_status rbm_layout(const rbm_ctx* ctx, uint32_t* prefix_bits, uint32_t* passe
  * device pointer, stream-ordered.  rbm_run() ignores and clears it. */
 rbm_status rbm_debug_permutation(rbm_ctx* ctx, uint32_t* order_out);
 
-/* Test hook (RBM_SCHEME_RBMR only): the slot draws j_s of the next step,
+/* Test hook (RBM_SCHEME_RBMR / _SEQ only): the slot draws j_s of the next step,
  * ceil(N/p)*p uint32 values (device). */
 rbm_status rbm_debug_slots(rbm_ctx* ctx, uint32_t* slots_out);
 

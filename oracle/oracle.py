@@ -31,6 +31,7 @@ class OracleCfg(C.Structure):
         ("scheme", C.c_int32), ("integrator", C.c_int32), ("kernel", C.c_int32),
         ("potential", C.c_int32), ("constraint", C.c_int32), ("fp32", C.c_int32),
         ("init_kind", C.c_int32), ("replica", C.c_uint32), ("noise", C.c_int32),
+        ("state_form", C.c_int32), ("pad1", C.c_int32),
         ("kparam", C.c_double * 4), ("vparam", C.c_double * 2), ("iparam", C.c_double * 8),
         ("sigma", C.c_double), ("dt", C.c_double), ("seed", C.c_uint64),
     ]
@@ -76,6 +77,7 @@ def lib():
             "oracle_rbmr_step": (C.c_int, [cfgp, C.c_uint64, f64p]),
             "oracle_rbmr_seq_step": (C.c_int, [cfgp, C.c_uint64, f64p]),
             "oracle_run": (C.c_int, [cfgp, C.c_uint64, C.c_uint64, f64p]),
+            "oracle_direct_run": (C.c_int, [cfgp, C.c_uint64, C.c_uint64, f64p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -91,7 +93,8 @@ def make_cfg(cfg: dict) -> OracleCfg:
     c.p = int(cfg["p"])
     c.n = int(cfg["n"])
     c.scheme = {"rbm1": 0, "rbmr": 1, "rbmr_seq": 2}[cfg.get("scheme", "rbm1")]
-    c.integrator = {"em": 0, "split": 1}[cfg.get("integrator", "em")]
+    c.integrator = {"em": 0, "split": 1, "verlet": 2}[cfg.get("integrator", "em")]
+    c.state_form = {"xv": 0, "xx": 1}[cfg.get("state_form", "xv")]
     c.kernel = KERNELS[cfg["kernel"]]
     c.potential = {"none": 0, "harmonic": 1}[cfg.get("potential", "none")]
     c.constraint = {"none": 0, "sphere": 1}[cfg.get("constraint", "none")]
@@ -227,6 +230,15 @@ def run(cfg: dict, x: np.ndarray, m0: int, nsteps: int) -> np.ndarray:
     rc = lib().oracle_run(C.byref(c), int(m0), int(nsteps), _p(y, C.c_double))
     if rc:
         raise ValueError(f"oracle_run rc={rc}")
+    return y
+
+
+def direct_run(cfg: dict, x: np.ndarray, m0: int, nsteps: int) -> np.ndarray:
+    c = make_cfg(cfg)
+    y = np.array(x, dtype=np.float64, copy=True).reshape(c.n, c.d)
+    rc = lib().oracle_direct_run(C.byref(c), int(m0), int(nsteps), _p(y, C.c_double))
+    if rc:
+        raise ValueError(f"oracle_direct_run rc={rc}")
     return y
 
 

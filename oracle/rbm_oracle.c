@@ -36,7 +36,7 @@ typedef struct {
   uint32_t p;          /* batch size */
   uint64_t n;          /* number of particles N */
   int32_t scheme;      /* 0 RBM-1, 1 RBM-r (Jacobi sweep) */
-  int32_t integrator;  /* 0 Euler-Maruyama, 1 split with exact pair flow */
+  int32_t integrator;  /* 0 Euler-Maruyama, 1 split with exact pair flow, 2 Verlet (second order) */
   int32_t kernel;      /* see ok_kernel() */
   int32_t potential;   /* 0 none, 1 harmonic beta|x|^2/2 */
   int32_t constraint;  /* 0 none, 1 unit sphere */
@@ -44,6 +44,8 @@ typedef struct {
   int32_t init_kind;   /* 1 normal, 2 box, 3 sphere, 4 gaussian mixture */
   uint32_t replica;
   int32_t noise;       /* 0 additive sigma dB; 1 multiplicative sigma X dB (Sec. 5.2.1) */
+  int32_t state_form;  /* Verlet: 0 the state is (X_0, V_0), 1 it is (X_n, X_{n-1}) */
+  int32_t pad1;
   double kparam[4];
   double vparam[2];
   double iparam[8];
@@ -407,6 +409,28 @@ static void split_member(const oracle_cfg* c, const double* y, const double* z, 
   if (c->constraint == 1) renormalise(c, xn);
 }
 
+/* Second-order system (Appendix A): X' = V, V' = -grad V(X) +
+ * force, with a 1-D particle stored as d = 2 components (x, w).  Verlet in
+ * the paper's position form:
+ *   first step  (state_form 0, w = V_0):     X_1 = X_0 + V_0 tau + F_0 tau^2 / 2
+ *   later steps (state_form 1, w = X_{n-1}): X_{n+1} = 2 X_n - X_{n-1} + F_n tau^2
+ * with F the batch force (RBM-1) or the full force (direct); new state (X_{n+1}, X_n). */
+static double verlet_pair_force(const oracle_cfg* c, double xi, double xj) {
+  oracle_cfg c1 = *c;
+  c1.d = 1;
+  double z = xi - xj, kz;
+  ok_kernel(&c1, &z, &kz);
+  return kz;
+}
+
+static void verlet_member(const oracle_cfg* c, const double* x, double f, double* xn) {
+  double g = (c->potential == 1) ? c->vparam[0] * x[0] : 0.0;  /* grad V on the position */
+  double F = -g + f;
+  double t = c->dt;
+  xn[0] = (c->state_form == 0) ? x[0] + x[1] * t + 0.5 * F * t * t : 2.0 * x[0] - x[1] + F * t * t;
+  xn[1] = x[0];
+}
+
 /* ------------------------------------------------------------------ */
 /* one batch C_q of Alg. 1 line 4: members ids[0..b) in sorted  */
 /* order with positions xb (b x d, X_m) -> xo (b x d, X_{m+1}).             */
@@ -417,7 +441,18 @@ int oracle_batch_update(const oracle_cfg* c, uint64_t m, const uint32_t* ids,
                         const double* xb, uint32_t b, double* xo) {
   uint32_t d = c->d;
   if (b < 2) return 1;
-  if (c->integrator == 0) {
+  if (c->integrator == 2) {  /* Verlet: batch force on the positions (component 0) */
+    double inv = 1.0 / (double)(b - 1);
+    for (uint32_t q = 0; q < b; ++q) {
+      double acc = 0.0;
+      for (uint32_t q2 = 0; q2 < b; ++q2) {  /* ascending sorted position */
+        if (q2 == q) continue;
+        acc += verlet_pair_force(c, xb[(uint64_t)q * d], xb[(uint64_t)q2 * d]);
+      }
+      verlet_member(c, xb + (uint64_t)q * d, acc * inv, xo + (uint64_t)q * d);
+    }
+    (void)ids; (void)m;
+  } else if (c->integrator == 0) {
     double inv = 1.0 / (double)(b - 1);
     for (uint32_t q = 0; q < b; ++q) {
       double acc[3] = {0, 0, 0}, f[3], z[3];
@@ -485,6 +520,13 @@ int oracle_direct_step(const oracle_cfg* c, uint64_t m, double* x) {
   if (!xn) return 2;
   for (uint64_t i = 0; i < n; ++i) {
     double f[3] = {0, 0, 0}, z[3];
+    if (c->integrator == 2) {  /* full-force Verlet (the reference of P:866-868) */
+      double acc = 0.0;
+      for (uint64_t j = 0; j < n; ++j)
+        if (j != i) acc += verlet_pair_force(c, x[i * d], x[j * d]);
+      verlet_member(c, x + i * d, acc / (double)(n - 1), xn + i * d);
+      continue;
+    }
     for (uint64_t j = 0; j < n; ++j) {
       if (j == i) continue;
       double zz[3], kz[3];
@@ -641,10 +683,23 @@ int oracle_rbmr_seq_step(const oracle_cfg* c, uint64_t m, double* x) {
 
 /* convenience: steps m0 .. m0+nsteps-1 of the configured scheme */
 int oracle_run(const oracle_cfg* c, uint64_t m0, uint64_t nsteps, double* x) {
+  oracle_cfg c2 = *c;
   for (uint64_t s = 0; s < nsteps; ++s) {
-    int rc = (c->scheme == 0) ? oracle_rbm1_step(c, m0 + s, x)
-             : (c->scheme == 1) ? oracle_rbmr_step(c, m0 + s, x) : oracle_rbmr_seq_step(c, m0 + s, x);
+    int rc = (c2.scheme == 0) ? oracle_rbm1_step(&c2, m0 + s, x)
+             : (c2.scheme == 1) ? oracle_rbmr_step(&c2, m0 + s, x) : oracle_rbmr_seq_step(&c2, m0 + s, x);
     if (rc) return rc;
+    c2.state_form = 1;  /* Verlet: (X_0, V_0) -> (X_n, X_{n-1}) after the first step */
+  }
+  return 0;
+}
+
+/* nsteps direct (full-force) steps, same state-form convention */
+int oracle_direct_run(const oracle_cfg* c, uint64_t m0, uint64_t nsteps, double* x) {
+  oracle_cfg c2 = *c;
+  for (uint64_t s = 0; s < nsteps; ++s) {
+    int rc = oracle_direct_step(&c2, m0 + s, x);
+    if (rc) return rc;
+    c2.state_form = 1;
   }
   return 0;
 }

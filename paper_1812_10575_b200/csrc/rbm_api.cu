@@ -220,14 +220,14 @@ rbm_status rbm_run(rbm_ctx* c, uint64_t nsteps) {
     return RBM_OK;
   }
   const bool needs_prologue = (c->cfg.scheme == RBM_SCHEME_RBM1 && c->L.B > 0 && !c->partitioned) ||
-                              (c->cfg.scheme == RBM_SCHEME_RBMR && !c->aos_valid);
+                              (c->cfg.scheme != RBM_SCHEME_RBM1 && !c->aos_valid);
   if (needs_prologue && nsteps > 0) {  // layout change of the state: first step outside the graphs
     rbm_status s0 = enqueue_steps(c, c->stream, 1);  // prologue step outside the graph
     if (s0) return s0;
     ++c->step;
     --nsteps;
   }
-  if (nsteps >= per && !c->timing) {
+  if (nsteps >= per && !c->timing && c->cfg.scheme != RBM_SCHEME_RBMR_SEQ) {  // (the sequential sweep syncs per step)
     const int slot = (c->cur << 1) | (int)(c->step & 1);
     if (!c->graph[slot]) {
       const int cur0 = c->cur;
@@ -347,7 +347,7 @@ rbm_status rbm_debug_permutation(rbm_ctx* c, uint32_t* order_out) {
 
 rbm_status rbm_debug_slots(rbm_ctx* c, uint32_t* slots_out) {
   if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
-  if (c->cfg.scheme != RBM_SCHEME_RBMR) return fail(c, RBM_ERR_STATE, "not an RBM-r context");
+  if (c->cfg.scheme == RBM_SCHEME_RBM1) return fail(c, RBM_ERR_STATE, "not an RBM-r context");
   if (!slots_out) return fail(c, RBM_ERR_INVALID_ARG, "slots_out is NULL");
   CU(cudaMemcpyAsync(slots_out, c->js, c->nslots * 4, cudaMemcpyDeviceToDevice, c->stream));
   return RBM_OK;

@@ -97,6 +97,8 @@ struct rbm_ctx {
   uint32_t *js = nullptr, *rmcnt = nullptr, *rmbox = nullptr, *rovf = nullptr, *rnovf = nullptr;
   void* rdelta = nullptr;  // Delta_s, 4 scalars per slot
   void* rxa = nullptr;     // AoS state (4 scalars per particle, id order)
+  uint32_t *rprevb = nullptr, *rlevel = nullptr, *rorder = nullptr, *rlcnt = nullptr, *rloff = nullptr,
+           *rlcur = nullptr, *rflags = nullptr;  // sequential RBM-r' (levels)
   bool aos_valid = false;  // RBM-r state currently in rxa
   uint64_t nbatch = 0, nslots = 0;
   // state
@@ -250,7 +252,7 @@ inline rbm_status validate(const rbm_config* cfg) {
   if (k.p < 2 || k.p > k.n) return fail(c, RBM_ERR_INVALID_ARG, "p=%u must satisfy 2 <= p <= n", k.p);
   if (k.p > 64 && !(k.p == k.n && k.n <= 2048))
     return fail(c, RBM_ERR_INVALID_ARG, "p=%u: need p <= 64, or p == n <= 2048", k.p);
-  if (k.scheme > RBM_SCHEME_RBMR) return fail(c, RBM_ERR_INVALID_ARG, "scheme %u", k.scheme);
+  if (k.scheme > RBM_SCHEME_RBMR_SEQ) return fail(c, RBM_ERR_INVALID_ARG, "scheme %u", k.scheme);
   if (k.integrator > RBM_INTEG_SPLIT_EXACT_PAIR) return fail(c, RBM_ERR_INVALID_ARG, "integrator %u", k.integrator);
   if (k.kernel > RBM_K_LINEAR) return fail(c, RBM_ERR_UNKNOWN_KERNEL, "kernel %u not in registry", k.kernel);
   if (k.noise > RBM_NOISE_GEOMETRIC) return fail(c, RBM_ERR_INVALID_ARG, "noise %u", k.noise);
@@ -332,7 +334,7 @@ inline void carve(rbm_ctx& c, Workspace& ws) {
   c.nonfinite = ws.take<unsigned long long>(1);
   c.capacity_err = ws.take<uint32_t>(1);
   c.big_scratch = ws.take<unsigned char>(NBIG * big_slot_bytes(k.d * es));
-  if (k.scheme == RBM_SCHEME_RBMR) {
+  if (k.scheme != RBM_SCHEME_RBM1) {
     c.nbatch = (n + k.p - 1) / k.p;
     c.nslots = c.nbatch * k.p;
     c.js = ws.take<uint32_t>(c.nslots);
@@ -342,6 +344,15 @@ inline void carve(rbm_ctx& c, Workspace& ws) {
     c.rmbox = ws.take<uint32_t>(n * MBOX);
     c.rovf = ws.take<uint32_t>(2 * (size_t)OVF_CAP);
     c.rnovf = ws.take<uint32_t>(1);
+    if (k.scheme == RBM_SCHEME_RBMR_SEQ) {
+      c.rprevb = ws.take<uint32_t>(c.nslots);
+      c.rlevel = ws.take<uint32_t>(c.nbatch);
+      c.rorder = ws.take<uint32_t>(c.nbatch);
+      c.rlcnt = ws.take<uint32_t>(MAX_LEVELS + 1);
+      c.rloff = ws.take<uint32_t>(MAX_LEVELS + 1);
+      c.rlcur = ws.take<uint32_t>(MAX_LEVELS + 1);
+      c.rflags = ws.take<uint32_t>(2);
+    }
   }
   ws.used = (ws.used + 255) & ~size_t(255);
 }
@@ -417,9 +428,11 @@ struct Engine final : EngineBase {
     use_pair_small = use_pair && c.L.cap <= (uint32_t)(PAIRS_BLOCK * PAIRS_ITEMS);
     p3_smem = pair3_smem_bytes<T, D>(c.L.cap, c.L.SB, c.L.b1);
     {
-      const char* e = std::getenv("RBM_PAIR_KERNEL");  // "pair3": compact, 3 CTAs per SM
+      // compact kernel, 3 CTAs per SM (default, measured 3% faster at C5);
+      // RBM_PAIR_KERNEL=lean: 2 CTAs of 512 threads per SM
+      const char* e = std::getenv("RBM_PAIR_KERNEL");
       use_pair3 = use_pair && !use_pair_small && c.L.cap <= (uint32_t)(PAIR3_BLOCK * PAIR3_ITEMS) &&
-                  p3_smem + 2400 <= 74 * 1024 && (e && std::strcmp(e, "pair3") == 0);
+                  p3_smem + 2400 <= 74 * 1024 && !(e && (std::strcmp(e, "lean") == 0 || std::strcmp(e, "persist") == 0));
     }
     {
       // "persist": one CTA per SM looping over buckets with double-buffered
@@ -581,7 +594,7 @@ struct Engine final : EngineBase {
       }
       return;
     }
-    if (c.cfg.scheme == RBM_SCHEME_RBMR && c.aos_valid) {
+    if (c.cfg.scheme != RBM_SCHEME_RBM1 && c.aos_valid) {
       if (i1 > i0)
         gather_aos_kernel<T, D><<<grid_for(i1 - i0, 256), 256, 0, s>>>(reinterpret_cast<const T*>(c.rxa), i0,
                                                                      i1, reinterpret_cast<T*>(out));
@@ -652,6 +665,7 @@ struct Engine final : EngineBase {
 
   void step(rbm_ctx& c, cudaStream_t s) override {
     if (c.cfg.scheme == RBM_SCHEME_RBMR) { step_rbmr(c, s); return; }
+    if (c.cfg.scheme == RBM_SCHEME_RBMR_SEQ) { step_rbmr_seq(c, s); return; }
     const DevParams& P = c.P;
     const Layout& L = c.L;
     const uint64_t n = c.cfg.n;
@@ -782,6 +796,58 @@ struct Engine final : EngineBase {
     c.mark(s);
   }
 
+  // Algorithm 2 as written (row f2): draws, per-particle slot chains, levels
+  // by relaxation (host-checked convergence), counting sort of the batches by
+  // level, then one launch per level
+  void step_rbmr_seq(rbm_ctx& c, cudaStream_t s) {
+    const DevParams& P = c.P;
+    const uint64_t n = c.cfg.n;
+    T* xa = reinterpret_cast<T*>(c.rxa);
+    if (!c.aos_valid) {
+      rbmr_pack_kernel<T, D><<<grid_for(n, 256), 256, 0, s>>>(n, st(c, c.cur), xa);
+      c.aos_valid = true;
+    }
+    cudaMemsetAsync(c.rmcnt, 0, n * 4, s);
+    cudaMemsetAsync(c.rnovf, 0, 4, s);
+    cudaMemsetAsync(c.rlcnt, 0, (MAX_LEVELS + 1) * 4, s);
+    cudaMemsetAsync(c.rflags, 0, 8, s);
+    const unsigned gb = grid_for(c.nbatch, 128, 148 * 64);
+    c.mark(s);
+    rbmr_draw_reg_kernel<<<gb, 128, 0, s>>>(P, c.nbatch, c.js, c.rmcnt, c.rmbox, c.rovf, c.rnovf, c.rlevel);
+    c.mark(s);
+    rbmr_prev_kernel<<<grid_for(n, 256), 256, 0, s>>>(P, n, c.rmcnt, c.rmbox, c.rovf, c.rnovf, c.rprevb);
+    c.mark(s);
+    for (uint32_t it = 0; it < MAX_LEVELS; it += 4) {
+      cudaMemsetAsync(c.rflags, 0, 4, s);
+      for (int k = 0; k < 4; ++k)
+        rbmr_level_kernel<<<grid_for(c.nbatch, 256), 256, 0, s>>>(P, c.nbatch, c.rprevb, c.rlevel, c.rflags);
+      uint32_t changed = 1;
+      cudaMemcpyAsync(&changed, c.rflags, 4, cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      if (!changed) break;
+    }
+    rbmr_level_hist_kernel<<<grid_for(c.nbatch, 256), 256, 0, s>>>(c.nbatch, c.rlevel, c.rlcnt, c.rflags + 1);
+    rbmr_level_scan_kernel<<<1, 1024, 0, s>>>(c.rlcnt, c.rloff, c.rlcur);
+    rbmr_level_scatter_kernel<<<grid_for(c.nbatch, 256), 256, 0, s>>>(c.nbatch, c.rlevel, c.rlcur, c.rorder);
+    std::vector<uint32_t> loff(MAX_LEVELS + 1);
+    uint32_t lerr = 0;
+    cudaMemcpyAsync(loff.data(), c.rloff, (MAX_LEVELS + 1) * 4, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&lerr, c.rflags + 1, 4, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    if (lerr) cudaMemsetAsync(c.capacity_err, 1, 1, s);  // deeper than MAX_LEVELS: flagged
+    c.mark(s);
+    for (uint32_t lv = 0; lv < MAX_LEVELS; ++lv) {
+      const uint32_t o0 = loff[lv], o1 = loff[lv + 1];
+      if (o1 > o0)
+        rbmr_seq_apply_kernel<T, D, KK, INTEG><<<grid_for(o1 - o0, 128), 128, 0, s>>>(P, c.rorder, o0, o1,
+                                                                                      c.js, xa);
+      if (o1 == loff[MAX_LEVELS]) break;
+    }
+    c.mark(s);
+    advance_kernel<<<1, 1, 0, s>>>(c.step_dev);
+    c.mark(s);
+  }
+
   void step_rbmr(rbm_ctx& c, cudaStream_t s) {
     const DevParams& P = c.P;
     const uint64_t n = c.cfg.n;
@@ -827,6 +893,8 @@ EngineBase* make_for_kernel(uint32_t kernel, uint32_t integ) {
 
 inline const char* const* kernel_names(const rbm_ctx& c, uint32_t* count) {
   static const char* const r[] = {"rbmr_batch", "rbmr_apply", "advance"};
+  static const char* const rs[] = {"rbmr_draw", "rbmr_prev", "rbmr_levels", "rbmr_seq_apply", "advance"};
+  if (c.cfg.scheme == RBM_SCHEME_RBMR_SEQ) { *count = 5; return rs; }
   static const char* const b0[] = {"resident_step"};
   static const char* const p1[] = {"tile_scan", "bucket_step", "straddle", "advance"};
   static const char* const p2[] = {"tile_scan", "scatter_sub", "final_scan", "bucket_step",

@@ -2555,6 +2555,197 @@ static __global__ void rbmr_apply_kernel(const __grid_constant__ DevParams P, ui
   }
 }
 
+// ----------------------- exact sequential RBM-r' (Alg. 2, row f2)
+// Batches of one sweep are applied in draw order from the current positions.
+// Batch b depends on the earlier batches that share a member; its level is
+// the longest such chain.  Batches of one level have disjoint members, so the
+// sweep runs level by level with every batch of a level in parallel, and each
+// batch sees exactly the positions the sequential loop would give it.
+constexpr uint32_t NO_BATCH = 0xffffffffu;
+constexpr uint32_t MAX_LEVELS = 4096;
+
+// draws j_s of batch b (as rbmr_batch_kernel) and mailbox registration only
+static __global__ void __launch_bounds__(128) rbmr_draw_reg_kernel(const __grid_constant__ DevParams P, uint64_t nbatch,
+                                                                   uint32_t* __restrict__ js, uint32_t* __restrict__ mcnt,
+                                                                   uint32_t* __restrict__ mbox, uint32_t* __restrict__ ovf,
+                                                                   uint32_t* __restrict__ novf, uint32_t* __restrict__ level) {
+  const uint32_t m = (uint32_t)*P.step;
+  const uint32_t p = P.p;
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nbatch;
+       b += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s0 = b * p;
+    for (uint32_t l = 0; l < p; ++l) {
+      const uint64_t s = s0 + l;
+      uint32_t t = 0, j;
+      for (;;) {
+        const uint4 w = block_at(P, (uint32_t)s, t, m, TAG_SLOT);
+        j = (uint32_t)__umul64hi(P.n, (((uint64_t)w.x) << 32) | w.y);
+        bool dup = false;
+        for (uint32_t l2 = 0; l2 < l; ++l2) dup |= (js[s0 + l2] == j);
+        if (!dup) break;
+        ++t;
+      }
+      js[s] = j;
+      const uint32_t pos = atomicAdd(&mcnt[j], 1u);
+      if (pos < MBOX) {
+        mbox[(size_t)j * MBOX + pos] = (uint32_t)s;
+      } else {
+        const uint32_t q = atomicAdd(novf, 1u);
+        if (q < OVF_CAP) { ovf[2 * q] = j; ovf[2 * q + 1] = (uint32_t)s; }
+        else atomicExch(P.capacity_err, 1u);
+      }
+    }
+    level[b] = 0;
+  }
+}
+
+// per particle: its slots in ascending order; prevb[s] = batch of the slot of
+// the same particle drawn just before s (NO_BATCH for the first)
+static __global__ void rbmr_prev_kernel(const __grid_constant__ DevParams P, uint64_t n,
+                                        const uint32_t* __restrict__ mcnt, const uint32_t* __restrict__ mbox,
+                                        const uint32_t* __restrict__ ovf, const uint32_t* __restrict__ novf,
+                                        uint32_t* __restrict__ prevb) {
+  constexpr uint32_t MAXL = 32;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = mcnt[j];
+    if (c == 0) continue;
+    uint32_t sl[MAXL];
+    uint32_t k = 0;
+    const uint32_t cm = c < MBOX ? c : MBOX;
+    for (uint32_t q = 0; q < cm; ++q) sl[k++] = mbox[j * MBOX + q];
+    if (c > MBOX) {
+      const uint32_t no = min(*novf, OVF_CAP);
+      for (uint32_t q = 0; q < no; ++q)
+        if (ovf[2 * q] == (uint32_t)j) {
+          if (k < MAXL) sl[k++] = ovf[2 * q + 1];
+          else atomicExch(P.capacity_err, 1u);
+        }
+    }
+    for (uint32_t a = 1; a < k; ++a) {
+      const uint32_t v = sl[a];
+      uint32_t w = a;
+      while (w > 0 && sl[w - 1] > v) { sl[w] = sl[w - 1]; --w; }
+      sl[w] = v;
+    }
+    prevb[sl[0]] = NO_BATCH;
+    for (uint32_t a = 1; a < k; ++a) prevb[sl[a]] = sl[a - 1] / P.p;
+  }
+}
+
+// one relaxation sweep of level[b] = max over members (level[prevb] + 1);
+// monotone, reaches the longest-chain levels after (depth + 1) sweeps
+static __global__ void rbmr_level_kernel(const __grid_constant__ DevParams P, uint64_t nbatch,
+                                         const uint32_t* __restrict__ prevb, uint32_t* level,
+                                         uint32_t* changed) {
+  const uint32_t p = P.p;
+  uint32_t ch = 0;
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nbatch;
+       b += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t lv = 0;
+    for (uint32_t l = 0; l < p; ++l) {
+      const uint32_t pb = prevb[b * p + l];
+      if (pb != NO_BATCH) lv = max(lv, level[pb] + 1u);
+    }
+    if (lv > level[b]) {
+      level[b] = lv;
+      ch = 1;
+    }
+  }
+  if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) atomicExch(changed, 1u);
+}
+
+// batches grouped by level: histogram, then order[] by level (counting sort)
+static __global__ void rbmr_level_hist_kernel(uint64_t nbatch, const uint32_t* __restrict__ level,
+                                              uint32_t* lcnt, uint32_t* err) {
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nbatch;
+       b += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t lv = level[b];
+    if (lv < MAX_LEVELS) atomicAdd(&lcnt[lv], 1u);
+    else atomicExch(err, 1u);
+  }
+}
+
+static __global__ void __launch_bounds__(1024) rbmr_level_scan_kernel(const uint32_t* __restrict__ lcnt,
+                                                                      uint32_t* loff, uint32_t* lcur) {
+  __shared__ uint32_t a[MAX_LEVELS];
+  __shared__ uint32_t ws[33];
+  for (uint32_t i = threadIdx.x; i < MAX_LEVELS; i += blockDim.x) a[i] = lcnt[i];
+  __syncthreads();
+  const uint32_t total = block_excl_scan<1024>(a, MAX_LEVELS, ws);
+  for (uint32_t i = threadIdx.x; i < MAX_LEVELS; i += blockDim.x) { loff[i] = a[i]; lcur[i] = a[i]; }
+  if (threadIdx.x == 0) loff[MAX_LEVELS] = total;
+}
+
+static __global__ void rbmr_level_scatter_kernel(uint64_t nbatch, const uint32_t* __restrict__ level,
+                                                 uint32_t* lcur, uint32_t* order) {
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nbatch;
+       b += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t lv = level[b];
+    if (lv < MAX_LEVELS) order[atomicAdd(&lcur[lv], 1u)] = (uint32_t)b;
+  }
+}
+
+// the batches order[o0 .. o1) of one level: Eq. (2.2) + update from the
+// current positions, written in place (members are disjoint within a level)
+template <typename T, int D, int KK, int INTEG>
+static __global__ void __launch_bounds__(128) rbmr_seq_apply_kernel(const __grid_constant__ DevParams P,
+                                                                    const uint32_t* __restrict__ order, uint32_t o0,
+                                                                    uint32_t o1, const uint32_t* __restrict__ js,
+                                                                    T* __restrict__ xa) {
+  const uint32_t m = (uint32_t)*P.step;
+  const uint32_t p = P.p;
+  for (uint32_t o = o0 + blockIdx.x * blockDim.x + threadIdx.x; o < o1; o += gridDim.x * blockDim.x) {
+    const uint64_t b = order[o], s0 = b * p;
+    if (INTEG == 0) {
+      T xn[64][D];  // p <= 64; new positions of all members before any is written
+      for (uint32_t l = 0; l < p; ++l) {
+        T xi[D], f[D], z[D];
+        load4<T, D>(xa, js[s0 + l], xi);
+#pragma unroll
+        for (int c = 0; c < D; ++c) { f[c] = T(0); z[c] = T(0); }
+        for (uint32_t l2 = 0; l2 < p; ++l2) {
+          if (l2 == l) continue;
+          T xj[D];
+          load4<T, D>(xa, js[s0 + l2], xj);
+          add_interaction<T, D, KK>(xi, xj, f, P);
+        }
+        const T inv = T(1) / T(p - 1);
+#pragma unroll
+        for (int c = 0; c < D; ++c) f[c] *= inv;
+        if (P.has_noise) Normals<T, D>::get(P, (uint32_t)(s0 + l), m, TAG_NOISE_SLOT, z);
+        em_update<T, D>(xi, f, z, xn[l], P, true);
+        check_finite<T, D>(xn[l], P, js[s0 + l], m);
+      }
+      for (uint32_t l = 0; l < p; ++l) {
+        const uint32_t j = js[s0 + l];
+#pragma unroll
+        for (int c = 0; c < D; ++c) xa[(size_t)j * 4 + c] = xn[l][c];
+      }
+    } else {
+      const uint32_t i = js[s0], j = js[s0 + 1];
+      T xi[D], xj[D], y[D], z[D], xn[D];
+      load4<T, D>(xa, i, xi);
+      load4<T, D>(xa, j, xj);
+#pragma unroll
+      for (int c = 0; c < D; ++c) z[c] = T(0);
+      pair_flow<T, D, KK>(xi, xj, true, y, P);
+      if (P.has_noise) Normals<T, D>::get(P, (uint32_t)s0, m, TAG_NOISE_SLOT, z);
+      split_finish<T, D>(y, z, xn, P, true);
+      check_finite<T, D>(xn, P, i, m);
+      T yj[D], xnj[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) z[c] = T(0);
+      pair_flow<T, D, KK>(xi, xj, false, yj, P);
+      if (P.has_noise) Normals<T, D>::get(P, (uint32_t)(s0 + 1), m, TAG_NOISE_SLOT, z);
+      split_finish<T, D>(yj, z, xnj, P, true);
+      check_finite<T, D>(xnj, P, j, m);
+#pragma unroll
+      for (int c = 0; c < D; ++c) { xa[(size_t)i * 4 + c] = xn[c]; xa[(size_t)j * 4 + c] = xnj[c]; }
+    }
+  }
+}
+
 // gather from the AoS RBM-r state (id order)
 template <typename T, int D>
 static __global__ void gather_aos_kernel(const T* __restrict__ xa, uint64_t i0, uint64_t i1,

@@ -109,7 +109,7 @@ def make_config(cfg: dict) -> RbmConfig:
     c.d = int(cfg["d"])
     c.p = int(cfg["p"])
     c.n = int(cfg["n"])
-    c.scheme = {"rbm1": 0, "rbmr": 1}[cfg.get("scheme", "rbm1")]
+    c.scheme = {"rbm1": 0, "rbmr": 1, "rbmr_seq": 2}[cfg.get("scheme", "rbm1")]
     c.integrator = {"em": 0, "split": 1}[cfg.get("integrator", "em")]
     c.kernel = KERNELS[cfg["kernel"]] if isinstance(cfg["kernel"], str) else int(cfg["kernel"])
     c.potential = {"none": 0, "harmonic": 1}[cfg.get("potential", "none")]

@@ -679,3 +679,61 @@ def test_rbmr_seq_dyson_second_moment(O):
     x = O.run(c, x, 0, 1000)
     pred = (1 + s2) / 2 + (m20 - (1 + s2) / 2) * math.exp(-2.0)
     assert abs(float((x ** 2).mean()) - pred) < 0.02
+
+
+# -------------------------------------- second-order RBM, Verlet (row f3)
+def verlet_cfg(n, p=2, kernel="smooth", beta=0.0, dt=2.0 ** -7, seed=1):
+    """The paper's 1-D Hamiltonian test: X' = V, V' = mean K, stored
+    as d = 2 components (x, v) at the start, (x_n, x_{n-1}) after."""
+    return dict(d=2, n=n, p=p, dtype="f64", scheme="rbm1", integrator="verlet", kernel=kernel,
+                kparam=[], potential="harmonic" if beta else "none", vparam=[beta], constraint="none",
+                sigma=0.0, dt=dt, seed=seed, init="user", iparam=[], state_form="xv")
+
+
+def test_verlet_harmonic_closed_form(O):
+    """K = 0, V = beta x^2/2: the Verlet recurrence has the closed-form solution
+    x_n = A cos(n th) + B sin(n th), cos th = 1 - beta tau^2 / 2, with x_0 and
+    x_1 = x_0 + v_0 tau - beta x_0 tau^2 / 2."""
+    beta, tau, n = 2.0, 0.01, 1000
+    c = dict(verlet_cfg(3, kernel="zero", beta=beta, dt=tau), p=3)
+    x0 = np.array([[1.0, 0.0], [-0.5, 2.0], [0.25, -1.0]])
+    y = O.direct_run(c, x0, 0, n)
+    th = math.acos(1 - beta * tau * tau / 2)
+    for i in range(3):
+        a = x0[i, 0]
+        x1 = x0[i, 0] + x0[i, 1] * tau - 0.5 * beta * x0[i, 0] * tau * tau
+        b = (x1 - a * math.cos(th)) / math.sin(th)
+        want = [a * math.cos(n * th) + b * math.sin(n * th), a * math.cos((n - 1) * th) + b * math.sin((n - 1) * th)]
+        assert np.allclose(y[i], want, atol=1e-11)
+    z = O.run(c, x0, 0, n)  # RBM with p = N: the same map
+    assert np.max(np.abs(z - y)) < 1e-12
+
+
+def test_verlet_p_equals_n_and_momentum(O):
+    rng = np.random.default_rng(3)
+    n = 60
+    x0 = np.stack([RI.semicircle_x0(n, seed=3).ravel(), rng.standard_normal(n)], axis=1)
+    c = verlet_cfg(n, p=n)
+    a = O.run(c, x0, 0, 50)
+    b = O.direct_run(c, x0, 0, 50)
+    assert np.max(np.abs(a - b)) < 1e-12
+    c2 = verlet_cfg(n, p=2)
+    y = O.run(c2, x0, 0, 50)
+    # V = 0, odd K: total momentum sum_i (x_n - x_{n-1}) / tau stays sum_i v_0 + O(tau) start term
+    p50 = (y[:, 0] - y[:, 1]).sum()
+    y51 = O.run(dict(c2, state_form="xx"), y, 50, 1)
+    assert abs((y51[:, 0] - y51[:, 1]).sum() - p50) < 1e-12
+
+
+def test_verlet_rbm_error_decreases_with_tau(O):
+    """Fig. second on a small system: RBM-1 (p = 2) Verlet against the
+    full-force Verlet reference (tau = 2^-13) at T = 1; the error shrinks with tau."""
+    n = 100
+    rng = np.random.default_rng(7)
+    x0 = np.stack([RI.semicircle_x0(n, seed=7).ravel(), rng.standard_normal(n)], axis=1)
+    ref = O.direct_run(verlet_cfg(n, dt=2.0 ** -13), x0, 0, 2 ** 13)
+    errs = []
+    for k in (4, 7):
+        y = O.run(verlet_cfg(n, dt=2.0 ** -k, seed=11), x0, 0, 2 ** k)
+        errs.append(float(np.sqrt(np.mean((y[:, 0] - ref[:, 0]) ** 2))))
+    assert errs[1] < 0.6 * errs[0], errs

@@ -1,0 +1,82 @@
+"""Exact sequential RBM-r' (Algorithm 2)
+on the GPU, -m gpu: the level-by-level sweep equals the oracle's sequential
+loop over the batches (same slot draws, bit-exact; states within the
+BASELINE.json tolerances)."""
+import numpy as np
+import pytest
+
+import rbm_inputs as RI
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def R():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1812_10575_b200 import rbm
+    rbm.lib()
+    return rbm
+
+
+def E(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b)) / max(1.0, float(np.max(np.abs(b)))))
+
+
+def model(kernel, d, n, p, dtype="f64", **kw):
+    kp = {"bounded_confidence": [1.0, 1.0], "coulomb_reg": [0.01]}.get(kernel, [])
+    c = dict(d=d, n=n, p=p, dtype=dtype, scheme="rbmr_seq", integrator="em", kernel=kernel, kparam=kp,
+             potential="harmonic", vparam=[1.0], constraint="none", sigma=0.1, dt=1e-3, seed=31,
+             init="normal", iparam=[0.0, 1.0])
+    c.update(kw)
+    return c
+
+
+CASES = [("smooth", 1, 5001, 2), ("smooth", 1, 5001, 3), ("gauss_attr_rep", 2, 20011, 8),
+         ("coulomb_reg", 3, 30000, 2), ("coulomb_reg", 3, 1_000_003, 2)]
+
+
+@pytest.mark.parametrize("kernel,d,n,p", CASES)
+def test_seq_slots_and_one_step(R, O, kernel, d, n, p):
+    c = model(kernel, d, n, p, step0=2)
+    s = R.RBM(c)
+    x0 = s.gather(host=True)
+    s.step()
+    assert np.array_equal(s.slots(), O.rbmr_slots(c, 2))
+    assert E(s.gather(host=True), O.rbmr_seq_step(c, x0, 2)) <= 1e-12
+    s.close()
+
+
+def test_seq_split_dyson_and_sphere(R, O):
+    c = dict(RI.c1_dyson(n=3000, integrator="split", seed=6), scheme="rbmr_seq")
+    s = R.RBM(c)
+    x0 = s.gather(host=True)
+    s.run(20)
+    assert E(s.gather(host=True), O.run(c, x0, 0, 20)) <= 1e-9
+    s.close()
+    c = dict(RI.c2_sphere(n=20000, seed=2), scheme="rbmr_seq")
+    s = R.RBM(c)
+    x0 = s.gather(host=True)
+    s.step()
+    g = s.gather(host=True)
+    assert E(g, O.rbmr_seq_step(c, x0, 0)) <= 1e-12
+    assert np.max(np.abs(np.linalg.norm(g, axis=1) - 1)) < 1e-14
+    s.close()
+
+
+def test_seq_many_steps_and_fp32(R, O):
+    c = model("smooth", 1, 4000, 4)
+    s = R.RBM(c)
+    x0 = s.gather(host=True)
+    s.run(30)
+    assert E(s.gather(host=True), O.run(c, x0, 0, 30)) <= 1e-9
+    s.close()
+    c32 = model("coulomb_reg", 3, 50000, 2, dtype="f32")
+    s = R.RBM(c32)
+    x0 = s.gather(host=True).astype(np.float64)
+    s.step()
+    assert E(s.gather(host=True), O.rbmr_seq_step(c32, x0, 0)) <= 1e-4
+    s.close()
