@@ -81,7 +81,14 @@ typedef enum { RBM_F32 = 0, RBM_F64 = 1 } rbm_dtype;
  * earlier batches sharing a member); each rbm_step synchronises the stream
  * once per sweep to size the levels (no CUDA graph). */
 typedef enum { RBM_SCHEME_RBM1 = 0, RBM_SCHEME_RBMR = 1, RBM_SCHEME_RBMR_SEQ = 2 } rbm_scheme;
-typedef enum { RBM_INTEG_EULER_MARUYAMA = 0, RBM_INTEG_SPLIT_EXACT_PAIR = 1 } rbm_integrator;
+/* RBM_INTEG_VERLET (row f3): the second-order (Hamiltonian) system of
+ * PAPER.md:848-870, X' = V, V' = -grad V(X) + mean K, for 1-D particles
+ * stored as d = 2 components; position Verlet with the RBM-1
+ * batch force of each step.  The state at step0 is (x_0, v_0) when
+ * state_form == 0 (first step x_1 = x_0 + v_0 tau + F_0 tau^2/2), or
+ * (x_n, x_{n-1}) when state_form == 1 (x_{n+1} = 2 x_n - x_{n-1} + F_n tau^2);
+ * after any step it is (x_n, x_{n-1}).  sigma must be 0; kernel smooth or zero. */
+typedef enum { RBM_INTEG_EULER_MARUYAMA = 0, RBM_INTEG_SPLIT_EXACT_PAIR = 1, RBM_INTEG_VERLET = 2 } rbm_integrator;
 
 /* Interaction kernels K(z), z = X^i - X^j (Eq. 1.2). */
 typedef enum {
@@ -141,6 +148,7 @@ typedef struct {
   int32_t rank;          /* 0..G-1: this process's rank (one GPU per rank) */
   uint32_t debug_bucket_cap; /* 0 = automatic; >0 forces the per-bucket smem capacity (tests) */
   uint32_t noise;        /* rbm_noise */
+  uint32_t state_form;   /* RBM_INTEG_VERLET: 0 = (x, v) at step0, 1 = (x_n, x_{n-1}) */
 } rbm_config;
 
 /* Bytes of device workspace rbm_init() needs for this config.

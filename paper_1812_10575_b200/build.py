@@ -2,8 +2,8 @@
 
     python -m paper_1812_10575_b200.build [--force]
 
-Three translation units (C ABI + fp32 engines + fp64 engines) compile in
-parallel and link into paper_1812_10575_b200/librbm.so.
+Seven translation units (the C ABI + one engine unit per (dtype, d)) compile
+in parallel and link into paper_1812_10575_b200/librbm.so.
 """
 from __future__ import annotations
 
@@ -17,7 +17,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "librbm.so")
 BUILD = os.path.join(PKG, "_build")
-UNITS = ["rbm_api.cu", "rbm_engines_f32.cu", "rbm_engines_f64.cu"]
+UNITS = ["rbm_api.cu"] + [f"rbm_engines_{t}_d{d}.cu" for t in ("f32", "f64") for d in (1, 2, 3)]
 HEADERS = ["rbm_device.cuh", "rbm_kernels.cuh", "rbm_host.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -10,11 +10,22 @@ namespace rbmhost {
 thread_local std::string g_err;
 
 EngineBase* make_engine(const rbm_config& k) {
-  return k.dtype == RBM_F64 ? make_engine_f64(k) : make_engine_f32(k);
+  const bool f64 = k.dtype == RBM_F64;
+  switch (k.d) {
+    case 1: return f64 ? make_engine_f64_d1(k.kernel, k.integrator) : make_engine_f32_d1(k.kernel, k.integrator);
+    case 2: return f64 ? make_engine_f64_d2(k.kernel, k.integrator) : make_engine_f32_d2(k.kernel, k.integrator);
+    case 3: return f64 ? make_engine_f64_d3(k.kernel, k.integrator) : make_engine_f32_d3(k.kernel, k.integrator);
+  }
+  return nullptr;
 }
 
 rbm_status enqueue_steps(rbm_ctx* c, cudaStream_t s, uint64_t k) {
-  for (uint64_t i = 0; i < k; ++i) c->eng->step(*c, s);
+  for (uint64_t i = 0; i < k; ++i) {
+    c->P.verlet_start = c->verlet_start ? 1u : 0u;  // by value into this step's launches
+    c->eng->step(*c, s);
+    c->verlet_start = false;
+  }
+  c->P.verlet_start = 0u;
   CU(cudaGetLastError());
   return RBM_OK;
 }
@@ -80,6 +91,7 @@ void fill_params(const rbm_config& k, DevParams& P) {
   P.invp = 1.0 / (double)(k.p - 1);
   P.invpf = (float)P.invp;
   P.geo_noise = k.noise == RBM_NOISE_GEOMETRIC ? 1u : 0u;
+  P.verlet_start = (k.integrator == RBM_INTEG_VERLET && k.state_form == 0) ? 1u : 0u;
   P.half_s2dt = 0.5 * k.sigma * k.sigma * k.dt;
   P.lin_decay = std::exp(-2.0 * k.kparam[0] * k.dt);
   P.half_s2dtf = (float)P.half_s2dt;
@@ -130,6 +142,7 @@ rbm_status init_impl(rbm_ctx* c, const rbm_config* cfg, void* wsp, size_t ws_byt
   if (c->L.B == 0) CU(cudaMemcpyAsync(c->S, s0, 8, cudaMemcpyHostToDevice, st));
   CU(cudaMemsetAsync(c->big_claim, 0, NBIG * 4, st));
   if (c->halo_recv) CU(cudaMemsetAsync(c->halo_recv, 0, 16, st));  // rank 0 never receives one
+  c->verlet_start = cfg->integrator == RBM_INTEG_VERLET && cfg->state_form == 0;
   if (cfg->init != RBM_INIT_USER) c->eng->init_state(*c, st);
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(st));  // the host-side sources above live on this stack frame
@@ -212,7 +225,10 @@ rbm_status rbm_run(rbm_ctx* c, uint64_t nsteps) {
   if (c->cfg.scheme == RBM_SCHEME_RBM1 && c->L.B == 0) {  // resident: chunks of <= 4096 steps per launch
     while (nsteps > 0) {
       const uint32_t k = (uint32_t)std::min<uint64_t>(nsteps, 4096);
+      c->P.verlet_start = c->verlet_start ? 1u : 0u;  // first step of this launch only
       c->eng->run_resident(*c, c->stream, k);
+      c->verlet_start = false;
+      c->P.verlet_start = 0u;
       CU(cudaGetLastError());
       c->step += k;
       nsteps -= k;
@@ -220,7 +236,7 @@ rbm_status rbm_run(rbm_ctx* c, uint64_t nsteps) {
     return RBM_OK;
   }
   const bool needs_prologue = (c->cfg.scheme == RBM_SCHEME_RBM1 && c->L.B > 0 && !c->partitioned) ||
-                              (c->cfg.scheme != RBM_SCHEME_RBM1 && !c->aos_valid);
+                              (c->cfg.scheme != RBM_SCHEME_RBM1 && !c->aos_valid) || c->verlet_start;
   if (needs_prologue && nsteps > 0) {  // layout change of the state: first step outside the graphs
     rbm_status s0 = enqueue_steps(c, c->stream, 1);  // prologue step outside the graph
     if (s0) return s0;
@@ -408,10 +424,12 @@ static rbm_status part_call(rbm_ctx* c, int phase) {
   if (!is_partitioned(c->cfg)) return fail(c, RBM_ERR_STATE, "not a partitioned context (world_size 1)");
   if (phase == 0 && c->partitioned) return fail(c, RBM_ERR_STATE, "prologue already done (state is partitioned)");
   if (phase > 0 && !c->partitioned) return fail(c, RBM_ERR_STATE, "run rbm_part_prologue and its exchange first");
+  c->P.verlet_start = c->verlet_start ? 1u : 0u;  // both phases compute batches of this step
   if (phase == 0) c->eng->part_prologue(*c, c->stream);
   else if (phase == 1) c->eng->part_phase1(*c, c->stream);
   else {
     c->eng->part_phase2(*c, c->stream);
+    c->verlet_start = false;
     c->P.dbg_order = nullptr;  // the permutation hook covers one step (phase1 + phase2)
     ++c->step;
   }
@@ -444,12 +462,13 @@ rbm_status rbm_part_phase2(rbm_ctx* c) { return part_call(c, 2); }
 // --------------------------------------------- direct O(N^2) steps (f1)
 static rbm_status direct_validate(const rbm_config* cfg, size_t elt_bytes_out[2]) {
   if (!cfg) return fail(nullptr, RBM_ERR_INVALID_ARG, "cfg is NULL");
-  if (cfg->integrator != RBM_INTEG_EULER_MARUYAMA)
-    return fail(nullptr, RBM_ERR_INVALID_ARG, "direct step: Euler-Maruyama only");
+  if (cfg->integrator == RBM_INTEG_SPLIT_EXACT_PAIR)
+    return fail(nullptr, RBM_ERR_INVALID_ARG, "direct step: Euler-Maruyama or Verlet");
   if (cfg->n > (1ull << 24)) return fail(nullptr, RBM_ERR_INVALID_ARG, "direct step: n <= 2^24 (O(N^2) work)");
   rbm_config k = *cfg;  // the batch fields do not apply: validate the model only
   k.p = 2;
   k.scheme = RBM_SCHEME_RBM1;
+  if (k.n < 2) k.n = 2;
   k.world_size = 1;
   k.rank = 0;
   k.debug_bucket_cap = 0;

@@ -53,6 +53,7 @@ struct DevParams {
   double invp;         // 1/(p-1): prefactor of a regular batch (Eq. 2.2)
   float invpf;
   uint32_t geo_noise;  // multiplicative noise sigma x dB (wealth model)
+  uint32_t verlet_start;  // Verlet (row f3): this step starts from (x_0, v_0), not (x_n, x_{n-1})
   double half_s2dt, lin_decay;     // sigma^2 dt / 2; e^{-2 kappa dt} (linear pair flow)
   float half_s2dtf, lin_decayf;
   // bucket layout of the partition
@@ -353,6 +354,37 @@ __device__ __forceinline__ void em_update(const T (&x)[D], const T (&f)[D], cons
   if (normalise && P.constraint == 1) renormalise<T, D>(xn);
 }
 
+// ---------------------------------------------- second order (Verlet, f3)
+// A 1-D particle of the Hamiltonian test system stored as
+// D = 2 components: (x_0, v_0) at the start, (x_n, x_{n-1}) afterwards.  The
+// force acts on the positions (component 0).  Position Verlet:
+//   start: x_1 = x_0 + v_0 tau + F_0 tau^2 / 2;  later: x_{n+1} = 2 x_n - x_{n-1} + F_n tau^2
+template <typename T, int D, int KK>
+__device__ __forceinline__ void add_force1(const T (&xi)[D], const T (&xj)[D], T (&f)[D],
+                                           const DevParams& P) {
+  T z[1] = {xi[0] - xj[0]};
+  const T s = kernel_scale<T, 1, KK>(z, P);
+  f[0] += s * z[0];
+}
+
+template <typename T, int D>
+__device__ __forceinline__ void verlet_update(const T (&x)[D], const T (&f)[D], T (&xn)[D],
+                                              const DevParams& P, bool start) {
+  const T g = (P.potential == 1) ? Prm<T>::beta(P) * x[0] : T(0);
+  const T F = -g + f[0];
+  const T t = Prm<T>::dt(P);
+  xn[0] = start ? x[0] + x[D > 1 ? 1 : 0] * t + T(0.5) * F * t * t : T(2) * x[0] - x[D > 1 ? 1 : 0] + F * t * t;
+  if (D > 1) xn[D > 1 ? 1 : 0] = x[0];
+}
+
+// force accumulation and member update of Eq. (2.2) for EM (INTEG 0) and Verlet (2)
+template <typename T, int D, int KK, int INTEG>
+__device__ __forceinline__ void member_force(const T (&xi)[D], const T (&xj)[D], T (&f)[D],
+                                             const DevParams& P) {
+  if (INTEG == 2) add_force1<T, D, KK>(xi, xj, f, P);
+  else add_interaction<T, D, KK>(xi, xj, f, P);
+}
+
 // exact pair flow (Dyson 922-943, Coulomb 1029-1045, with
 // the 1/2 of reading D:3): returns y for the member `first` (true) or second.
 template <typename T, int D, int KK>
@@ -398,6 +430,13 @@ __device__ __forceinline__ void split_finish(const T (&y)[D], const T (&z)[D], T
     xn[c] = P.geo_noise ? w * exp(sq * z[c] - Prm<T>::half_s2dt(P)) : w + sq * z[c];
   }
   if (normalise && P.constraint == 1) renormalise<T, D>(xn);
+}
+
+template <typename T, int D, int INTEG>
+__device__ __forceinline__ void member_update(const T (&x)[D], const T (&f)[D], const T (&z)[D], T (&xn)[D],
+                                              const DevParams& P, bool vstart) {
+  if (INTEG == 2) verlet_update<T, D>(x, f, xn, P, vstart);
+  else em_update<T, D>(x, f, z, xn, P, true);
 }
 
 template <typename T, int D>

@@ -100,6 +100,7 @@ struct rbm_ctx {
   uint32_t *rprevb = nullptr, *rlevel = nullptr, *rorder = nullptr, *rlcnt = nullptr, *rloff = nullptr,
            *rlcur = nullptr, *rflags = nullptr;  // sequential RBM-r' (levels)
   bool aos_valid = false;  // RBM-r state currently in rxa
+  bool verlet_start = false;  // the next step starts a Verlet run from (x_0, v_0)
   uint64_t nbatch = 0, nslots = 0;
   // state
   int cur = 0;
@@ -253,7 +254,16 @@ inline rbm_status validate(const rbm_config* cfg) {
   if (k.p > 64 && !(k.p == k.n && k.n <= 2048))
     return fail(c, RBM_ERR_INVALID_ARG, "p=%u: need p <= 64, or p == n <= 2048", k.p);
   if (k.scheme > RBM_SCHEME_RBMR_SEQ) return fail(c, RBM_ERR_INVALID_ARG, "scheme %u", k.scheme);
-  if (k.integrator > RBM_INTEG_SPLIT_EXACT_PAIR) return fail(c, RBM_ERR_INVALID_ARG, "integrator %u", k.integrator);
+  if (k.integrator > RBM_INTEG_VERLET) return fail(c, RBM_ERR_INVALID_ARG, "integrator %u", k.integrator);
+  if (k.integrator == RBM_INTEG_VERLET) {
+    if (k.d != 2) return fail(c, RBM_ERR_INVALID_ARG, "Verlet: d must be 2 (x and v / x_prev of a 1-D particle)");
+    if (k.sigma != 0.0) return fail(c, RBM_ERR_INVALID_ARG, "Verlet: the Hamiltonian system has no noise (sigma = 0)");
+    if (k.kernel != RBM_K_SMOOTH_TEST && k.kernel != RBM_K_ZERO)
+      return fail(c, RBM_ERR_UNSUPPORTED, "Verlet: kernel smooth or zero in this build");
+    if (k.scheme != RBM_SCHEME_RBM1 || k.constraint != RBM_CONSTRAINT_NONE)
+      return fail(c, RBM_ERR_UNSUPPORTED, "Verlet: RBM-1 without constraint");
+    if (k.state_form > 1) return fail(c, RBM_ERR_INVALID_ARG, "state_form %u", k.state_form);
+  }
   if (k.kernel > RBM_K_LINEAR) return fail(c, RBM_ERR_UNKNOWN_KERNEL, "kernel %u not in registry", k.kernel);
   if (k.noise > RBM_NOISE_GEOMETRIC) return fail(c, RBM_ERR_INVALID_ARG, "noise %u", k.noise);
   if (k.potential > RBM_V_HARMONIC) return fail(c, RBM_ERR_UNKNOWN_KERNEL, "potential %u not in registry", k.potential);
@@ -573,6 +583,7 @@ struct Engine final : EngineBase {
                                                           k.iparam[3]);
     c.partitioned = false;
     c.aos_valid = false;
+    c.verlet_start = k.integrator == RBM_INTEG_VERLET && k.state_form == 0;
   }
 
   void set_state(rbm_ctx& c, const void* x, cudaStream_t s) override {
@@ -580,6 +591,7 @@ struct Engine final : EngineBase {
                                                                reinterpret_cast<const T*>(x));
     c.partitioned = false;
     c.aos_valid = false;
+    c.verlet_start = c.cfg.integrator == RBM_INTEG_VERLET && c.cfg.state_form == 0;
   }
 
   void gather(rbm_ctx& c, uint64_t i0, uint64_t i1, void* out, cudaStream_t s) override {
@@ -722,8 +734,10 @@ struct Engine final : EngineBase {
     constexpr int TB = 128;
     T* a = reinterpret_cast<T*>(x);
     T* b = reinterpret_cast<T*>(tmp);
+    DevParams Q = P;
     for (uint32_t k = 0; k < nsteps; ++k) {
-      direct_kernel<T, D, KK, TB><<<(n + TB - 1) / TB, TB, 0, s>>>(P, a, b, n, m0 + k);
+      Q.verlet_start = (k == 0) ? P.verlet_start : 0u;
+      direct_kernel<T, D, KK, (INTEG == 2 ? 2 : 0), TB><<<(n + TB - 1) / TB, TB, 0, s>>>(Q, a, b, n, m0 + k);
       std::swap(a, b);
     }
     if (nsteps & 1u) cudaMemcpyAsync(x, tmp, (size_t)n * D * sizeof(T), cudaMemcpyDeviceToDevice, s);
@@ -872,6 +886,12 @@ struct Engine final : EngineBase {
 
 template <typename T, int D>
 EngineBase* make_for_kernel(uint32_t kernel, uint32_t integ) {
+  if (integ == RBM_INTEG_VERLET) {  // second order: 1-D particles stored as (x, v | x_prev)
+    if (D != 2) return nullptr;
+    if (kernel == RBM_K_SMOOTH_TEST) return new Engine<T, 2, KK_SMOOTH, 2>();
+    if (kernel == RBM_K_ZERO) return new Engine<T, 2, KK_ZERO, 2>();
+    return nullptr;
+  }
   switch (kernel) {
     case RBM_K_ZERO: return new Engine<T, D, KK_ZERO, 0>();
     case RBM_K_BOUNDED_CONFIDENCE: return new Engine<T, D, KK_BOUNDED, 0>();
@@ -917,7 +937,12 @@ inline const char* const* kernel_names(const rbm_ctx& c, uint32_t* count) {
   return p2;
 }
 
-EngineBase* make_engine_f32(const rbm_config& k);
-EngineBase* make_engine_f64(const rbm_config& k);
+#define RBM_DECLARE_ENGINES(T) \
+  EngineBase* make_engine_##T##_d1(uint32_t, uint32_t); \
+  EngineBase* make_engine_##T##_d2(uint32_t, uint32_t); \
+  EngineBase* make_engine_##T##_d3(uint32_t, uint32_t);
+RBM_DECLARE_ENGINES(f32)
+RBM_DECLARE_ENGINES(f64)
+#undef RBM_DECLARE_ENGINES
 
 }  // namespace rbmhost

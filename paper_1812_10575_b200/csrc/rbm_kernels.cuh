@@ -789,7 +789,7 @@ template <typename T> __device__ __forceinline__ T batch_inv(const DevParams& P,
 template <typename T, int D, int KK, int INTEG>
 __device__ __forceinline__ void interior_update(const DevParams& P, uint32_t m, uint32_t q,
                                                 uint32_t l0, uint32_t l1, const uint16_t* ord,
-                                                SX<T> xs, uint32_t id, T (&xn)[D]) {
+                                                SX<T> xs, uint32_t id, T (&xn)[D], int vstart = -1) {
   T xi[D];
   const uint32_t e = ord[q];
 #pragma unroll
@@ -798,7 +798,7 @@ __device__ __forceinline__ void interior_update(const DevParams& P, uint32_t m, 
 #pragma unroll
   for (int c = 0; c < D; ++c) z[c] = T(0);
   if (P.has_noise) Normals<T, D>::get(P, id, m, TAG_NOISE, z);
-  if (INTEG == 0) {
+  if (INTEG != 1) {
     T f[D];
 #pragma unroll
     for (int c = 0; c < D; ++c) f[c] = T(0);
@@ -808,12 +808,12 @@ __device__ __forceinline__ void interior_update(const DevParams& P, uint32_t m, 
       T xj[D];
 #pragma unroll
       for (int c = 0; c < D; ++c) xj[c] = xs.at(c, e2);
-      add_interaction<T, D, KK>(xi, xj, f, P);
+      member_force<T, D, KK, INTEG>(xi, xj, f, P);
     }
     const T inv = batch_inv<T>(P, l1 - l0);
 #pragma unroll
     for (int c = 0; c < D; ++c) f[c] *= inv;
-    em_update<T, D>(xi, f, z, xn, P, true);
+    member_update<T, D, INTEG>(xi, f, z, xn, P, vstart < 0 ? P.verlet_start != 0 : vstart != 0);
   } else {
     const uint32_t ea = ord[l0], eb = ord[l0 + 1];
     T xa[D], xb[D], y[D];
@@ -1063,7 +1063,8 @@ static __global__ void __launch_bounds__(BLOCK) resident_kernel(const __grid_con
       batch_range(q, P, b0, b1);
       const uint32_t id = id_l[ord[q]];
       T xn[D];
-      interior_update<T, D, KK, INTEG>(P, m, q, b0, b1, ord, xs, id, xn);
+      interior_update<T, D, KK, INTEG>(P, m, q, b0, b1, ord, xs, id, xn,
+                                       (P.verlet_start && it == 0) ? 1 : 0);
       check_finite<T, D>(xn, P, id, m);
       id_o[q] = id;
 #pragma unroll
@@ -1131,7 +1132,7 @@ static __global__ void __launch_bounds__(256) straddle_kernel(const __grid_const
 #pragma unroll
     for (int c = 0; c < D; ++c) { xi[c] = act ? strad.x[c][g] : T(0); z[c] = T(0); }
     if (act && P.has_noise) Normals<T, D>::get(P, id, m, TAG_NOISE, z);
-    if (INTEG == 0) {
+    if (INTEG != 1) {
       T f[D];
 #pragma unroll
       for (int c = 0; c < D; ++c) f[c] = T(0);
@@ -1143,13 +1144,13 @@ static __global__ void __launch_bounds__(256) straddle_kernel(const __grid_const
         T xj[D];
 #pragma unroll
         for (int c = 0; c < D; ++c) xj[c] = strad.x[c][gh];
-        add_interaction<T, D, KK>(xi, xj, f, P);
+        member_force<T, D, KK, INTEG>(xi, xj, f, P);
       }
       if (act) {
         const T inv = batch_inv<T>(P, sz);
 #pragma unroll
         for (int c = 0; c < D; ++c) f[c] *= inv;
-        em_update<T, D>(xi, f, z, xn, P, true);
+        member_update<T, D, INTEG>(xi, f, z, xn, P, P.verlet_start != 0);
       }
     } else {
       const long long ga = __shfl_sync(0xffffffffu, phys[0], 0), gb = __shfl_sync(0xffffffffu, phys[0], 1);
@@ -1590,7 +1591,7 @@ static __global__ void __launch_bounds__(BLOCK) bucket_fused_kernel(const __grid
       for (int c = 0; c < D; ++c) xi[c] = act ? xs.at(c, e) : T(0);
       const uint32_t id = act ? id_l[e] : 0u;
       T xn[D];
-      if (INTEG == 0) {
+      if (INTEG != 1) {
         T f[D];
 #pragma unroll
         for (int c = 0; c < D; ++c) f[c] = T(0);
@@ -1598,7 +1599,7 @@ static __global__ void __launch_bounds__(BLOCK) bucket_fused_kernel(const __grid
           T xj[D];
 #pragma unroll
           for (int c = 0; c < D; ++c) xj[c] = __shfl_sync(0xffffffffu, xi[c], (int)j, (int)G);
-          if (act && j < sz && j != li) add_interaction<T, D, KK>(xi, xj, f, P);
+          if (act && j < sz && j != li) member_force<T, D, KK, INTEG>(xi, xj, f, P);
         }
         if (act) {
           T z[D];
@@ -1608,7 +1609,7 @@ static __global__ void __launch_bounds__(BLOCK) bucket_fused_kernel(const __grid
           const T inv_b = batch_inv<T>(P, sz);
 #pragma unroll
           for (int c = 0; c < D; ++c) f[c] *= inv_b;
-          em_update<T, D>(xi, f, z, xn, P, true);
+          member_update<T, D, INTEG>(xi, f, z, xn, P, P.verlet_start != 0);
         }
       } else {  // split exact pair flow, p = 2 = G
         T xo[D];
@@ -1686,6 +1687,14 @@ __device__ __forceinline__ void pair_update(const DevParams& P, uint32_t m, cons
     for (int c = 0; c < D; ++c) { f0[c] = sc * zz[c]; f1[c] = -f0[c]; }
     em_update<T, D>(x0, f0, z0, y0, P, true);
     em_update<T, D>(x1, f1, z1, y1, P, true);
+  } else if (INTEG == 2) {  // Verlet: 1-D force on the positions; the partner gets -f
+    T f0[D], f1[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) { f0[c] = T(0); f1[c] = T(0); }
+    add_force1<T, D, KK>(x0, x1, f0, P);
+    f1[0] = -f0[0];
+    verlet_update<T, D>(x0, f0, y0, P, P.verlet_start != 0);
+    verlet_update<T, D>(x1, f1, y1, P, P.verlet_start != 0);
   } else {
     T a[D], b[D];
     pair_flow<T, D, KK>(x0, x1, true, a, P);
@@ -2300,7 +2309,7 @@ static __global__ void __launch_bounds__(BLOCK, 1) pair_persist_kernel(const __g
 // ascending j, prefactor 1/(N-1); the Brownian increment of particle i at
 // step m is the one RBM step m uses (counter (i, blk, m, TAG_NOISE)), so RBM
 // and direct runs from one X_0 are synchronously coupled.
-template <typename T, int D, int KK, int TB>
+template <typename T, int D, int KK, int INTEG, int TB>
 static __global__ void __launch_bounds__(TB) direct_kernel(const __grid_constant__ DevParams P,
                                                            const T* __restrict__ xin,
                                                            T* __restrict__ xout, uint32_t n,
@@ -2325,7 +2334,7 @@ static __global__ void __launch_bounds__(TB) direct_kernel(const __grid_constant
       T xj[D];
 #pragma unroll
       for (int c = 0; c < D; ++c) xj[c] = tile[c][t];
-      add_interaction<T, D, KK>(xi, xj, f, P);
+      member_force<T, D, KK, INTEG>(xi, xj, f, P);
     }
     __syncthreads();
   }
@@ -2337,7 +2346,7 @@ static __global__ void __launch_bounds__(TB) direct_kernel(const __grid_constant
 #pragma unroll
   for (int c = 0; c < D; ++c) z[c] = T(0);
   if (P.has_noise) Normals<T, D>::get(P, i, m, TAG_NOISE, z);
-  em_update<T, D>(xi, f, z, xn, P, true);
+  member_update<T, D, INTEG>(xi, f, z, xn, P, P.verlet_start != 0);
   check_finite<T, D>(xn, P, i, m);
 #pragma unroll
   for (int c = 0; c < D; ++c) xout[(size_t)i * D + c] = xn[c];

@@ -49,7 +49,7 @@ class RbmConfig(C.Structure):
         ("kparam", C.c_double * 4), ("vparam", C.c_double * 2), ("iparam", C.c_double * 8),
         ("sigma", C.c_double), ("dt", C.c_double), ("seed", C.c_uint64), ("step0", C.c_uint64),
         ("replica", C.c_uint32), ("world_size", C.c_int32), ("rank", C.c_int32),
-        ("debug_bucket_cap", C.c_uint32), ("noise", C.c_uint32),
+        ("debug_bucket_cap", C.c_uint32), ("noise", C.c_uint32), ("state_form", C.c_uint32),
     ]
 
 
@@ -110,7 +110,8 @@ def make_config(cfg: dict) -> RbmConfig:
     c.p = int(cfg["p"])
     c.n = int(cfg["n"])
     c.scheme = {"rbm1": 0, "rbmr": 1, "rbmr_seq": 2}[cfg.get("scheme", "rbm1")]
-    c.integrator = {"em": 0, "split": 1}[cfg.get("integrator", "em")]
+    c.integrator = {"em": 0, "split": 1, "verlet": 2}[cfg.get("integrator", "em")]
+    c.state_form = {"xv": 0, "xx": 1}[cfg.get("state_form", "xv")]
     c.kernel = KERNELS[cfg["kernel"]] if isinstance(cfg["kernel"], str) else int(cfg["kernel"])
     c.potential = {"none": 0, "harmonic": 1}[cfg.get("potential", "none")]
     c.constraint = {"none": 0, "sphere": 1}[cfg.get("constraint", "none")]
