@@ -95,7 +95,8 @@ typedef enum {
   RBM_K_ZERO = 0,
   RBM_K_DYSON = 1,              /* 1/z, d=1 (Eq. 4.4); K(0):=0            */
   RBM_K_COULOMB = 2,            /* z/|z|^3, d=3; K(0):=0                 */
-  RBM_K_BOUNDED_CONFIDENCE = 3, /* -a z 1{|z|<r}, kparam={a, r} (Eq. 5.12) */
+  RBM_K_BOUNDED_CONFIDENCE = 3, /* -a z 1{|z|<r}, kparam={a, r, closed}; closed != 0: the paper's
+                                   closed window |z| <= r, phi = chi_[0,1] (Eq. 5.12) */
   RBM_K_GAUSS_ATTR_REP = 4,     /* z e^{-|z|^2/2} - z e^{-|z|^2/8}/4 (BASELINE.json C4)       */
   RBM_K_COULOMB_REG = 5,        /* z/(|z|^2+eps)^{3/2}, kparam={eps} (BASELINE.json C5)       */
   RBM_K_SMOOTH_TEST = 6,        /* z/(1+|z|^2)                             */

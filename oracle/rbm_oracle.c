@@ -151,14 +151,16 @@ static void ok_kernel(const oracle_cfg* c, const double* z, double* out) {
       s = (r2 == 0.0) ? 0.0 : 1.0 / r2; break;
     case K_COULOMB: /* x/|x|^3; K(0):=0 (D:12) */
       s = (r2 == 0.0) ? 0.0 : 1.0 / (r2 * sqrt(r2)); break;
-    case K_BOUNDED_CONF: { /* -alpha x 1{|x|<r} (Eq. 5.12; D:10) */
+    case K_BOUNDED_CONF: { /* -alpha x 1{|x|<r} (Eq. 5.12; D:10);
+                            kparam[2] != 0: the paper's closed window phi = chi_[0,1] */
       double alpha = c->kparam[0], rad = c->kparam[1];
+      int closed = c->kparam[2] != 0.0;
       int inside;
       if (c->fp32 && d == 1) {
         float zf = (float)z[0];  /* z already holds fl32(x_i - x_j), D:10 */
-        inside = fabsf(zf) < (float)rad;
+        inside = closed ? fabsf(zf) <= (float)rad : fabsf(zf) < (float)rad;
       } else {
-        inside = sqrt(r2) < rad;
+        inside = closed ? sqrt(r2) <= rad : sqrt(r2) < rad;
       }
       s = inside ? -alpha : 0.0;
       break;

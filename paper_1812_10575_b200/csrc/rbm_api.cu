@@ -91,6 +91,7 @@ void fill_params(const rbm_config& k, DevParams& P) {
   P.invp = 1.0 / (double)(k.p - 1);
   P.invpf = (float)P.invp;
   P.geo_noise = k.noise == RBM_NOISE_GEOMETRIC ? 1u : 0u;
+  P.closed_window = (k.kernel == RBM_K_BOUNDED_CONFIDENCE && k.kparam[2] != 0.0) ? 1u : 0u;
   P.verlet_start = (k.integrator == RBM_INTEG_VERLET && k.state_form == 0) ? 1u : 0u;
   P.half_s2dt = 0.5 * k.sigma * k.sigma * k.dt;
   P.lin_decay = std::exp(-2.0 * k.kparam[0] * k.dt);

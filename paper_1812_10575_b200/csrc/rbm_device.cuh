@@ -54,6 +54,7 @@ struct DevParams {
   float invpf;
   uint32_t geo_noise;  // multiplicative noise sigma x dB (wealth model)
   uint32_t verlet_start;  // Verlet (row f3): this step starts from (x_0, v_0), not (x_n, x_{n-1})
+  uint32_t closed_window; // bounded confidence: closed window |z| <= r (the paper's chi_[0,1])
   double half_s2dt, lin_decay;     // sigma^2 dt / 2; e^{-2 kappa dt} (linear pair flow)
   float half_s2dtf, lin_decayf;
   // bucket layout of the partition
@@ -291,8 +292,9 @@ __device__ __forceinline__ T kernel_scale(const T (&z)[D], const DevParams& P) {
   if (KK == KK_ZERO) return T(0);
   if (KK == KK_DYSON) return r2 == T(0) ? T(0) : T(1) / r2;               // 1/z, K(0):=0
   if (KK == KK_COULOMB) return r2 == T(0) ? T(0) : T(1) / (r2 * sqrt(r2));  // z/|z|^3
-  if (KK == KK_BOUNDED) {                                                   // -a z 1{|z|<r}
-    const bool inside = (D == 1) ? (fabs(z[0]) < Prm<T>::kp1(P)) : (sqrt(r2) < Prm<T>::kp1(P));
+  if (KK == KK_BOUNDED) {  // -a z 1{|z|<r}; closed window |z| <= r if kparam[2] != 0
+    const T az = (D == 1) ? fabs(z[0]) : sqrt(r2), rad = Prm<T>::kp1(P);
+    const bool inside = P.closed_window ? (az <= rad) : (az < rad);
     return inside ? -Prm<T>::kp0(P) : T(0);
   }
   if (KK == KK_GAUSS_AR) return exp(T(-0.5) * r2) - T(0.25) * exp(T(-0.125) * r2);

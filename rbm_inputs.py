@@ -40,6 +40,16 @@ def c3_opinion(n: int = 10**7, seed: int = 1, scheme: str = "rbm1") -> dict:
                 init="box", iparam=[-5.0, 5.0], steps=500)
 
 
+def opinion_paper(n: int = 1000, noise: bool = False, seed: int = 1, dtype: str = "f64") -> dict:
+    """The paper's stochastic opinion dynamics: alpha = 40,
+    closed window phi = chi_[0,1], tau = 1e-4, N = 1e3, eps_N = 0 or N^{-1/3}.
+    The paper does not state the initial data; U[-5, 5] as in C3 (D:25)."""
+    return dict(d=1, n=n, p=2, dtype=dtype, scheme="rbm1", integrator="em",
+                kernel="bounded_confidence", kparam=[40.0, 1.0, 1.0], potential="none",
+                vparam=[1.0], constraint="none", sigma=(n ** (-1.0 / 3.0)) if noise else 0.0,
+                dt=1e-4, seed=seed, init="box", iparam=[-5.0, 5.0], steps=10000)
+
+
 def c4_aggregation(n: int = 10**8, seed: int = 1, scheme: str = "rbm1") -> dict:
     """BASELINE.json configs[3]: 2-D Gaussian attraction-repulsion (synthetic)."""
     return dict(d=2, n=n, p=4, dtype="f32", scheme=scheme, integrator="em",
@@ -102,3 +112,4 @@ def semicircle_x0(n: int, seed: int, radius: float = 2.0) -> np.ndarray:
         keep = rng.uniform(0.0, 1.0, 2 * n) < np.sqrt(np.maximum(radius * radius - x * x, 0.0)) / radius
         out = np.concatenate([out, x[keep]])
     return out[:n].reshape(n, 1)
+

@@ -737,3 +737,17 @@ def test_verlet_rbm_error_decreases_with_tau(O):
         y = O.run(verlet_cfg(n, dt=2.0 ** -k, seed=11), x0, 0, 2 ** k)
         errs.append(float(np.sqrt(np.mean((y[:, 0] - ref[:, 0]) ** 2))))
     assert errs[1] < 0.6 * errs[0], errs
+
+
+def test_bounded_confidence_closed_window(O):
+    """P:1208: phi = chi_[0,1] is closed -- partners exactly r apart interact;
+    the strict window (BASELINE C3, D:10) excludes them."""
+    for dtype in ("f64", "f32"):
+        base = dict(RI.opinion_paper(n=2, dtype=dtype), dt=0.01)
+        z = np.array([1.0])
+        closed = O.kernel_eval(base, z)
+        strict = O.kernel_eval(dict(base, kparam=[40.0, 1.0, 0.0]), z)
+        assert closed[0] == -40.0 and strict[0] == 0.0
+        x = np.array([[0.0], [1.0]])
+        y = O.rbm1_step(base, x, 0)
+        assert np.allclose(y.ravel(), [0.4, 0.6], atol=1e-15)  # x -+ dt * 40 * 1
