@@ -550,6 +550,12 @@ rbm_status rbm_destroy(rbm_ctx* c) {
         if (h[i]) std::fprintf(stderr, " p%d=%.0f", i, (double)h[i] / (double)h[63]);
       std::fprintf(stderr, "\n");
     }
+    if (cudaMemcpy(h, c->P.prof, sizeof h, cudaMemcpyDeviceToHost) == cudaSuccess && h[62]) {
+      std::fprintf(stderr, "RBM_PHASE_PROF pass-2 splitter, %llu tiles, mean SM cycles per tile:", h[62]);
+      for (int i = 16; i < 32; ++i)
+        if (h[i]) std::fprintf(stderr, " s%d=%.0f", i, (double)h[i] / (double)h[62]);
+      std::fprintf(stderr, "\n");
+    }
     cudaFree(c->P.prof);
   }
   for (int i = 0; i < 4; ++i)

@@ -312,6 +312,7 @@ static __global__ void advance_kernel(uint64_t* step) { *step += 1; }
 // reservation atomics of concurrent CTAs over the L2 slices.
 constexpr uint32_t CUR1_STRIDE = 8, CUR2_STRIDE = 8;
 constexpr uint32_t MAX_SEG = 16384;  // pass-1 segments: 2^b1 << segk <= 2^10 << 4
+constexpr uint32_t MAX_SEG_SPLIT = 1024;  // segments the pass-2 splitter's smem tile table holds
 
 __device__ __forceinline__ uint32_t out_seg(const DevParams& P, uint32_t dg, uint32_t salt) {
   return (dg << P.segk) | (salt & P.segmask);
@@ -548,7 +549,8 @@ template <typename T, int D, int TILE> __host__ __device__ constexpr size_t spli
   return ((size_t)TILE * (8 + D * sizeof(T)) + 127) & ~(size_t)127;
 }
 template <typename T, int D, int TILE> __host__ __device__ constexpr size_t split_smem_bytes() {
-  return (3 * 1024 + 64) * 4 + 64 + 2 * split_stage_bytes<T, D, TILE>() + (size_t)TILE * 4 + (size_t)TILE * 2;
+  return (3 * 1024 + 64) * 4 + 64 + 2 * split_stage_bytes<T, D, TILE>() + (size_t)TILE * 4 + (size_t)TILE * 2 +
+         (size_t)(MAX_SEG_SPLIT + 1) * 4;  // + tile table copy
 }
 
 struct TileInfo { uint32_t u, lo, hi, pad; };
@@ -580,6 +582,7 @@ static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) split_persist_kern
                                                                         const uint32_t* __restrict__ tile_off,
                                                                         uint32_t scap) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  RBM_PROF_BEGIN(P);
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw);  // 1024
   uint32_t* off = hist + 1024;                             // 1024
   uint32_t* gbase = off + 1024;                            // 1024
@@ -590,14 +593,17 @@ static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) split_persist_kern
   constexpr size_t SBY = split_stage_bytes<T, D, TILE>();
   uint32_t* rk = reinterpret_cast<uint32_t*>(stg0 + 2 * SBY);  // digit<<16 | rank, by element
   uint16_t* inv = reinterpret_cast<uint16_t*>(rk + TILE);      // output slot -> element
+  uint32_t* toff = reinterpret_cast<uint32_t*>(inv + TILE);    // copy of tile_off (binary search in smem)
   const uint32_t nseg = (1u << P.b1) << P.segk;
   const uint32_t ntiles = tile_off[nseg];
   const uint32_t bits = P.b2, sh = 32u - P.b1 - P.b2, nbins = 1u << bits, mask = nbins - 1u;
   const uint32_t tid = threadIdx.x;
   uint64_t pol = 0;
+  for (uint32_t i = tid; i <= nseg; i += BLOCK) toff[i] = tile_off[i];
+  __syncthreads();
   auto issue = [&](uint32_t t, uint32_t st) {  // thread 0
     TileInfo ti{0u, 0u, 0u, 0u};
-    if (t < ntiles) gapped_tile(tile_off, cnt1, nseg, t, TILE, ti.u, ti.lo, ti.hi);
+    if (t < ntiles) gapped_tile(toff, cnt1, nseg, t, TILE, ti.u, ti.lo, ti.hi);
     tinfo[st] = ti;
     split_stage_load<T, D, TILE>(src, ti.u * scap + ti.lo, ti.hi - ti.lo, stg0 + st * SBY, &bar[st], pol);
   };
@@ -611,10 +617,12 @@ static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) split_persist_kern
   uint32_t phase = 0, it = 0;
   for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
     const uint32_t s = it & 1u;
-    if (tid == 0 && t + gridDim.x < ntiles) issue(t + gridDim.x, s ^ 1u);
+    if (tid == 0 && t + gridDim.x < ntiles) issue(t + gridDim.x, s ^ 1u);  // prefetch into the free stage
     for (uint32_t i = tid; i < nbins; i += BLOCK) hist[i] = 0;
+    RBM_PROF(P, 16);
     mbar_wait(&bar[s], (phase >> s) & 1u);
     phase ^= 1u << s;
+    RBM_PROF(P, 17);
     const TileInfo ti = tinfo[s];
     const uint32_t cnt = ti.hi - ti.lo;
     const uint32_t dbase0 = ((ti.u >> P.segk) & P.nb1_loc_mask) << P.b2;
@@ -628,18 +636,31 @@ static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) split_persist_kern
       rk[e] = (dg << 16) | atomicAdd(&hist[dg], 1u);
     }
     __syncthreads();
-    for (uint32_t i = tid; i < nbins; i += BLOCK) {
-      const uint32_t h = hist[i];
-      off[i] = h;
-      gbase[i] = h ? atomicAdd(&cur[(size_t)(dbase0 + i) * CUR2_STRIDE], h) : 0u;
+    RBM_PROF(P, 18);
+    // run reservations issued now and consumed after the staging index
+    // (their L2 round trip overlaps the scan and the placement)
+    constexpr int NRES = (1024 + BLOCK - 1) / BLOCK;
+    uint32_t gres[NRES];
+#pragma unroll
+    for (int r = 0; r < NRES; ++r) {
+      const uint32_t i = tid + r * BLOCK;
+      const uint32_t h = i < nbins ? hist[i] : 0u;
+      if (i < nbins) off[i] = h;
+      gres[r] = h ? atomicAdd(&cur[(size_t)(dbase0 + i) * CUR2_STRIDE], h) : 0u;
     }
     __syncthreads();
     block_excl_scan<BLOCK>(off, nbins, wsum);
+    RBM_PROF(P, 19);
     for (uint32_t e = tid; e < cnt; e += BLOCK) {
       const uint32_t v = rk[e];
       inv[off[v >> 16] + (v & 0xffffu)] = (uint16_t)e;
     }
+#pragma unroll
+    for (int r = 0; r < NRES; ++r)
+      if (tid + r * BLOCK < nbins) gbase[tid + r * BLOCK] = gres[r];
     __syncthreads();
+
+    RBM_PROF(P, 20);
     for (uint32_t j = tid; j < cnt; j += BLOCK) {
       const uint32_t e = inv[j];
       const uint32_t dg = rk[e] >> 16;
@@ -655,6 +676,8 @@ static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) split_persist_kern
       for (int c = 0; c < D; ++c) dst.x[c][g] = x_s[(size_t)c * TILE + e];
     }
     __syncthreads();  // stage s, rk, inv free
+    RBM_PROF(P, 21);
+    if (P.prof && threadIdx.x == 0) atomicAdd(&P.prof[62], 1ull);
   }
 }
 
