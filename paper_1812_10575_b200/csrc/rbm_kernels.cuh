@@ -1915,6 +1915,25 @@ static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) bucket_pair_kernel
   if (P.prof && threadIdx.x == 0) atomicAdd(&P.prof[63], 1ull);
 }
 
+// the size-3 remainder batch of the p = 2 kernels (N odd; one bucket per
+// step): out of line so the hot loops stay compact in the instruction cache
+template <typename T, int D, int KK, int INTEG>
+__device__ __noinline__ void pair3_triple(const DevParams& P, uint32_t m, uint32_t tri0, uint32_t n,
+                                          const uint16_t* ord, SX<T> xs, const uint32_t* id_l,
+                                          const uint32_t* ta, const uint16_t* tb, const uint32_t* off,
+                                          uint16_t* inv, uint32_t osh) {
+  T xn[3][D];
+  for (uint32_t q = tri0; q < n; ++q)
+    interior_update<T, D, KK, INTEG>(P, m, q, tri0, n, ord, xs, id_l[ord[q]], xn[q - tri0]);
+  for (uint32_t q = tri0; q < n; ++q) {
+    const uint32_t e = ord[q];
+    check_finite<T, D>(xn[q - tri0], P, id_l[e], m);
+#pragma unroll
+    for (int c = 0; c < D; ++c) xs.at(c, e) = xn[q - tri0][c];
+    inv[off[ta[e] >> osh] + tb[e]] = (uint16_t)e;
+  }
+}
+
 // The p = 2 bucket step with a compact shared-memory footprint (packed u16
 // sub-digit counters, u16 staging aliased over the dead composites) so that
 // three 256-thread CTAs -- three buckets in flight -- fit on one SM.
@@ -2041,6 +2060,7 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_pair3_kernel(const __g
   // 4. output partition first (key_{m+1} depends on the id only): digit and
   //    rank of every interior member, so the run reservations below are in
   //    flight while the batches are computed.  ks is dead: tb = rank by e.
+#pragma unroll 1
   for (uint32_t q = head + threadIdx.x; q < n; q += BLOCK) {
     if (q >= covered && q < tri0) continue;
     const uint32_t e = ord[q];
@@ -2070,7 +2090,7 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_pair3_kernel(const __g
   RBM_PROF(P, 8);
   // 5. one thread per pair: Eq. (2.2) + update in place; staging index of each member
   constexpr int PITEMS = (ITEMS + 1) / 2;
-#pragma unroll
+#pragma unroll 1  // one copy of the pair update: the hot loop stays in the instruction cache
   for (int k = 0; k < PITEMS; ++k) {
     const uint32_t j = k * BLOCK + threadIdx.x;
     if (j < npairs) {
@@ -2089,18 +2109,8 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_pair3_kernel(const __g
       inv[off[ta[e1] >> osh] + tb[e1]] = (uint16_t)e1;
     }
   }
-  if (triple && threadIdx.x == 0) {  // the remainder batch of size 3 (N odd), EM only
-    T xn[3][D];
-    for (uint32_t q = tri0; q < n; ++q)
-      interior_update<T, D, KK, INTEG>(P, m, q, tri0, n, ord, xs, id_l[ord[q]], xn[q - tri0]);
-    for (uint32_t q = tri0; q < n; ++q) {
-      const uint32_t e = ord[q];
-      check_finite<T, D>(xn[q - tri0], P, id_l[e], m);
-#pragma unroll
-      for (int c = 0; c < D; ++c) xs.at(c, e) = xn[q - tri0][c];
-      inv[off[ta[e] >> osh] + tb[e]] = (uint16_t)e;
-    }
-  }
+  if (triple && threadIdx.x == 0)  // the remainder batch of size 3 (N odd), EM only
+    pair3_triple<T, D, KK, INTEG>(P, m, tri0, n, ord, xs, id_l, ta, tb, off, inv, osh);
 #pragma unroll
   for (int r = 0; r < NRES; ++r)
     if (threadIdx.x + r * BLOCK < nout) gbase[threadIdx.x + r * BLOCK] = gres[r];
