@@ -402,12 +402,17 @@ def main():
         xin[:] = np.resize(RI.user_x0(min(cfg["n"], 1 << 20), cfg["d"], seed=rank).astype(npdt),
                            (cfg["n"], cfg["d"]))
         ue = s
+        from paper_1812_10575_b200 import rbm as RB
+        # one untimed pass of the same job first (graph capture for the K-step
+        # chunking and the first host-copy setup are one-time costs)
+        ue.set_state(xin)
+        ue.run(K)
+        RB.rbm_gather(ue.ctx, 0, cfg["n"], hout.data_ptr(), RB.MEM_HOST)
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         ue.set_state(xin)                       # pinned host -> device (inside the timed region)
         ue.run(K)                               # graph-replayed steps
-        from paper_1812_10575_b200 import rbm as RB
         RB.rbm_gather(ue.ctx, 0, cfg["n"], hout.data_ptr(), RB.MEM_HOST)  # device -> pinned host
         t = time.perf_counter() - t0
         barrier()
