@@ -550,7 +550,7 @@ template <typename T, int D, int TILE> __host__ __device__ constexpr size_t spli
 }
 template <typename T, int D, int TILE> __host__ __device__ constexpr size_t split_smem_bytes() {
   return (3 * 1024 + 64) * 4 + 64 + 2 * split_stage_bytes<T, D, TILE>() + (size_t)TILE * 4 + (size_t)TILE * 2 +
-         (size_t)(MAX_SEG_SPLIT + 1) * 4;  // + tile table copy
+         (size_t)TILE * 2 + (size_t)(MAX_SEG_SPLIT + 1) * 4;  // + slot digits, tile table copy
 }
 
 struct TileInfo { uint32_t u, lo, hi, pad; };
@@ -593,7 +593,8 @@ static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) split_persist_kern
   constexpr size_t SBY = split_stage_bytes<T, D, TILE>();
   uint32_t* rk = reinterpret_cast<uint32_t*>(stg0 + 2 * SBY);  // digit<<16 | rank, by element
   uint16_t* inv = reinterpret_cast<uint16_t*>(rk + TILE);      // output slot -> element
-  uint32_t* toff = reinterpret_cast<uint32_t*>(inv + TILE);    // copy of tile_off (binary search in smem)
+  uint16_t* idg = inv + TILE;                                  // output slot -> digit
+  uint32_t* toff = reinterpret_cast<uint32_t*>(idg + TILE);    // copy of tile_off (binary search in smem)
   const uint32_t nseg = (1u << P.b1) << P.segk;
   const uint32_t ntiles = tile_off[nseg];
   const uint32_t bits = P.b2, sh = 32u - P.b1 - P.b2, nbins = 1u << bits, mask = nbins - 1u;
@@ -653,18 +654,20 @@ static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) split_persist_kern
     RBM_PROF(P, 19);
     for (uint32_t e = tid; e < cnt; e += BLOCK) {
       const uint32_t v = rk[e];
-      inv[off[v >> 16] + (v & 0xffffu)] = (uint16_t)e;
+      const uint32_t pos = off[v >> 16] + (v & 0xffffu);
+      inv[pos] = (uint16_t)e;
+      idg[pos] = (uint16_t)(v >> 16);
     }
+    // gbase[d] - off[d]: the global slot of output position j is gbase[dg] + j
 #pragma unroll
     for (int r = 0; r < NRES; ++r)
-      if (tid + r * BLOCK < nbins) gbase[tid + r * BLOCK] = gres[r];
+      if (tid + r * BLOCK < nbins) gbase[tid + r * BLOCK] = gres[r] - off[tid + r * BLOCK];
     __syncthreads();
 
     RBM_PROF(P, 20);
     for (uint32_t j = tid; j < cnt; j += BLOCK) {
-      const uint32_t e = inv[j];
-      const uint32_t dg = rk[e] >> 16;
-      const uint32_t slot = gbase[dg] + (j - off[dg]);
+      const uint32_t e = inv[j], dg = idg[j];
+      const uint32_t slot = gbase[dg] + j;
       if (slot >= dcap) {  // bucket capacity exceeded (probability ~1e-30): fail loudly
         atomicExch(P.capacity_err, 1u);
         continue;
@@ -2112,8 +2115,8 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_pair3_kernel(const __g
   if (triple && threadIdx.x == 0)  // the remainder batch of size 3 (N odd), EM only
     pair3_triple<T, D, KK, INTEG>(P, m, tri0, n, ord, xs, id_l, ta, tb, off, inv, osh);
 #pragma unroll
-  for (int r = 0; r < NRES; ++r)
-    if (threadIdx.x + r * BLOCK < nout) gbase[threadIdx.x + r * BLOCK] = gres[r];
+  for (int r = 0; r < NRES; ++r)  // gbase[d] - off[d]: output position j goes to slot gbase[dg] + j
+    if (threadIdx.x + r * BLOCK < nout) gbase[threadIdx.x + r * BLOCK] = gres[r] - off[threadIdx.x + r * BLOCK];
   __syncthreads();
   RBM_PROF(P, 6);
   // 6. staged slots -> coalesced runs of the step-(m+1) pass-1 buckets
@@ -2121,7 +2124,7 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_pair3_kernel(const __g
     const uint32_t e = inv[j];
     const uint32_t kn = ta[e];
     const uint32_t dg = kn >> osh;
-    const uint32_t slot = gbase[dg] + (j - off[dg]);
+    const uint32_t slot = gbase[dg] + j;
     if (slot >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
     T xo[D];
 #pragma unroll
