@@ -387,6 +387,79 @@ __device__ __forceinline__ void member_force(const T (&xi)[D], const T (&xj)[D],
   else add_interaction<T, D, KK>(xi, xj, f, P);
 }
 
+// ---------------------------------------------- canonical partner order
+// A batch of sz <= G = P.group members (p <= 32) is summed in the rotation
+// order of the lane-group kernel: for o = 1 .. G/2 the partner (li + o) mod G,
+// then (li - o) mod G for o < G/2 (partners >= sz skipped).  The lane-group
+// kernel evaluates each pair once (K is odd with s(z) = s(-z), so the
+// partner's term is exactly the negation) and every other kernel that steps
+// such a batch (straddlers, halo, resident, serial) sums the same terms in the
+// same order with the same roundings (explicit _rn: no FMA contraction), so a
+// batch gives bit-identical results wherever it is computed.  Batches larger
+// than G (p > 32, or the long remainder batch) are summed in ascending order.
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+// t = K(xi - xj) (Verlet: the 1-D force on the position coordinate only)
+template <typename T, int D, int KK, int INTEG>
+__device__ __forceinline__ void pair_term(const T (&xi)[D], const T (&xj)[D], T (&t)[D],
+                                          const DevParams& P) {
+  if (INTEG == 2) {
+    T z[1] = {xi[0] - xj[0]};
+    const T s = kernel_scale<T, 1, KK>(z, P);
+#pragma unroll
+    for (int c = 0; c < D; ++c) t[c] = T(0);
+    t[0] = mul_rn(s, z[0]);
+  } else {
+    T z[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) z[c] = xi[c] - xj[c];
+    const T s = kernel_scale<T, D, KK>(z, P);
+#pragma unroll
+    for (int c = 0; c < D; ++c) t[c] = mul_rn(s, z[c]);
+  }
+}
+
+// f += K(x_li - x_j) over the partners of member li in the canonical order;
+// getx(j, xj) loads member j (0 <= j < sz) of the batch
+template <typename T, int D, int KK, int INTEG, typename GetX>
+__device__ __forceinline__ void batch_force(const DevParams& P, uint32_t li, uint32_t sz,
+                                            const T (&xi)[D], GetX getx, T (&f)[D]) {
+  const uint32_t G = P.group;
+  if (G != 0 && sz <= G) {
+    for (uint32_t o = 1; o <= G / 2; ++o) {
+      const uint32_t jp = (li + o) & (G - 1);
+      if (jp < sz) {
+        T xj[D], t[D];
+        getx(jp, xj);
+        pair_term<T, D, KK, INTEG>(xi, xj, t, P);
+#pragma unroll
+        for (int c = 0; c < D; ++c) f[c] = add_rn(f[c], t[c]);
+      }
+      const uint32_t jm = (li - o) & (G - 1);
+      if (o < G / 2 && jm < sz) {
+        T xj[D], t[D];
+        getx(jm, xj);
+        pair_term<T, D, KK, INTEG>(xi, xj, t, P);
+#pragma unroll
+        for (int c = 0; c < D; ++c) f[c] = add_rn(f[c], t[c]);
+      }
+    }
+  } else {
+    for (uint32_t j = 0; j < sz; ++j) {  // ascending, self skipped
+      if (j == li) continue;
+      T xj[D];
+      getx(j, xj);
+      member_force<T, D, KK, INTEG>(xi, xj, f, P);
+    }
+  }
+}
+
+
 // exact pair flow (Dyson 922-943, Coulomb 1029-1045, with
 // the 1/2 of reading D:3): returns y for the member `first` (true) or second.
 template <typename T, int D, int KK>

@@ -828,14 +828,11 @@ __device__ __forceinline__ void interior_update(const DevParams& P, uint32_t m, 
     T f[D];
 #pragma unroll
     for (int c = 0; c < D; ++c) f[c] = T(0);
-    for (uint32_t g = l0; g < l1; ++g) {  // ascending sorted position, self skipped
-      if (g == q) continue;
-      const uint32_t e2 = ord[g];
-      T xj[D];
+    batch_force<T, D, KK, INTEG>(P, q - l0, l1 - l0, xi, [&](uint32_t j, T (&xj)[D]) {
+      const uint32_t e2 = ord[l0 + j];
 #pragma unroll
       for (int c = 0; c < D; ++c) xj[c] = xs.at(c, e2);
-      member_force<T, D, KK, INTEG>(xi, xj, f, P);
-    }
+    }, f);
     const T inv = batch_inv<T>(P, l1 - l0);
 #pragma unroll
     for (int c = 0; c < D; ++c) f[c] *= inv;
@@ -1118,6 +1115,7 @@ static __global__ void __launch_bounds__(256) straddle_kernel(const __grid_const
                                                               const uint32_t* __restrict__ S,
                                                               const __grid_constant__ OutDst<T, D> dst, uint32_t ocap,
                                                               uint32_t* cur_next) {
+  __shared__ long long strad_phys[(256 / 32) * 96];  // member slots per warp (sz <= 96)
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   // boundaries 1 .. nbuckets-1; on a partitioned system with a halo also
@@ -1162,16 +1160,24 @@ static __global__ void __launch_bounds__(256) straddle_kernel(const __grid_const
       T f[D];
 #pragma unroll
       for (int c = 0; c < D; ++c) f[c] = T(0);
-      for (uint32_t h = 0; h < sz; ++h) {  // ascending sorted position
+      // the physical slot of every member, staged per warp (lane l holds
+      // members l, l+32, l+64): shuffled out once, then read in the
+      // canonical partner order
+      long long* ph_w = strad_phys + (threadIdx.x >> 5) * 96;
+      for (uint32_t h = 0; h < sz; ++h) {
         const uint32_t hr = h >> 5;
         const long long src_ph = hr == 0 ? phys[0] : (hr == 1 ? phys[1] : phys[2]);
         const long long gh = __shfl_sync(0xffffffffu, src_ph, (int)(h & 31u));
-        if (!act || h == q) continue;
-        T xj[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) xj[c] = strad.x[c][gh];
-        member_force<T, D, KK, INTEG>(xi, xj, f, P);
+        if (lane == 0) ph_w[h] = gh;
       }
+      __syncwarp();
+      if (act)
+        batch_force<T, D, KK, INTEG>(P, q, sz, xi, [&](uint32_t j, T (&xj)[D]) {
+          const long long gh = ph_w[j];
+#pragma unroll
+          for (int c = 0; c < D; ++c) xj[c] = strad.x[c][gh];
+        }, f);
+      __syncwarp();
       if (act) {
         const T inv = batch_inv<T>(P, sz);
 #pragma unroll
@@ -1618,14 +1624,32 @@ static __global__ void __launch_bounds__(BLOCK) bucket_fused_kernel(const __grid
       const uint32_t id = act ? id_l[e] : 0u;
       T xn[D];
       if (INTEG != 1) {
+        // canonical rotation order (batch_force): each pair once, the
+        // partner's term returned by a shuffle (K odd: exactly -t)
         T f[D];
 #pragma unroll
         for (int c = 0; c < D; ++c) f[c] = T(0);
-        for (uint32_t j = 0; j < G; ++j) {  // ascending sorted position
-          T xj[D];
+        for (uint32_t o = 1; o <= G / 2; ++o) {
+          const uint32_t jp = (li + o) & (G - 1), jm = (li - o) & (G - 1);
+          T xj[D], t[D];
 #pragma unroll
-          for (int c = 0; c < D; ++c) xj[c] = __shfl_sync(0xffffffffu, xi[c], (int)j, (int)G);
-          if (act && j < sz && j != li) member_force<T, D, KK, INTEG>(xi, xj, f, P);
+          for (int c = 0; c < D; ++c) xj[c] = __shfl_sync(0xffffffffu, xi[c], (int)jp, (int)G);
+          const bool vp = act && jp < sz;
+          if (vp) {
+            pair_term<T, D, KK, INTEG>(xi, xj, t, P);
+#pragma unroll
+            for (int c = 0; c < D; ++c) f[c] = add_rn(f[c], t[c]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < D; ++c) t[c] = T(0);
+          }
+          if (o < G / 2) {  // warp-uniform
+#pragma unroll
+            for (int c = 0; c < (INTEG == 2 ? 1 : D); ++c) {
+              const T r = __shfl_sync(0xffffffffu, t[c], (int)jm, (int)G);
+              if (act && jm < sz) f[c] = sub_rn(f[c], r);
+            }
+          }
         }
         if (act) {
           T z[D];
