@@ -1529,7 +1529,10 @@ static __global__ void __launch_bounds__(BLOCK) bucket_fused_kernel(const __grid
   if (n == 0) return;
   const uint32_t m = (uint32_t)*P.step;
   const uint32_t cap = P.cap;
-  for (uint32_t i = threadIdx.x; i < nsb; i += BLOCK) cnt[i] = 0;
+  if (nsb >= 4)
+    for (uint32_t i = threadIdx.x; i < nsb / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
+  else
+    for (uint32_t i = threadIdx.x; i < nsb; i += BLOCK) cnt[i] = 0;
   if (n > cap) {
     fused_big_path<T, D, KK, INTEG, BLOCK>(P, src, dst, cur_next, s0, sb, n, m, dcap, cnt, off, wsum);
     return;
@@ -1576,11 +1579,12 @@ static __global__ void __launch_bounds__(BLOCK) bucket_fused_kernel(const __grid
     const uint32_t sd = tb[e] >> 16, v = ta[e];
     const uint32_t a = off[sd], c = cnt[sd];
     uint32_t r = a;
-    for (uint32_t i = 0; i < c; ++i) r += (ks[a + i] < v) ? 1u : 0u;
+    if (c > 1)  // most sub-buckets hold one element
+      for (uint32_t i = 0; i < c; ++i) r += (ks[a + i] < v) ? 1u : 0u;
     ord[r] = (uint16_t)e;
   }
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < 1024u; i += BLOCK) cnt[i] = 0;  // -> output digit counts
+  for (uint32_t i = threadIdx.x; i < 256u; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);  // -> output digit counts
   // interior batches [kfirst, klast) of this bucket; the rest straddle
   uint32_t kfirst = batch_index(s0, P);
   if (kfirst * P.p < s0) ++kfirst;
