@@ -410,6 +410,7 @@ struct Engine final : EngineBase {
 
   size_t fu_smem = 0, pr_smem = 0, rs_smem = 0, ps_smem = 0, sp_smem = 0;
   bool use_pair = false, use_persist = false, use_split = false, use_pair_small = false, use_pair3 = false;
+  bool use_group3 = false;
   size_t prs_smem = 0, p3_smem = 0;
   // pass-2 splitter configurations: one CTA of 1024 threads per SM with
   // 4096-record tiles (default; measured fastest at C5), or
@@ -443,6 +444,14 @@ struct Engine final : EngineBase {
       const char* e = std::getenv("RBM_PAIR_KERNEL");
       use_pair3 = use_pair && !use_pair_small && c.L.cap <= (uint32_t)(PAIR3_BLOCK * PAIR3_ITEMS) &&
                   p3_smem + 2400 <= 74 * 1024 && !(e && (std::strcmp(e, "lean") == 0 || std::strcmp(e, "persist") == 0));
+    }
+    {
+      // 2 < p <= 32 (EM / Verlet): the compact 3-CTA kernel with lane-group
+      // batches; RBM_GROUP_KERNEL=fused: the general 2-CTA kernel
+      const char* e = std::getenv("RBM_GROUP_KERNEL");
+      use_group3 = c.cfg.p > 2 && c.cfg.p <= 32 && c.cfg.integrator != RBM_INTEG_SPLIT_EXACT_PAIR && c.L.B > 0 &&
+                   c.L.cap <= (uint32_t)(PAIR3_BLOCK * PAIR3_ITEMS) && p3_smem + 2400 <= 74 * 1024 &&
+                   !(e && std::strcmp(e, "fused") == 0);
     }
     {
       // "persist": one CTA per SM looping over buckets with double-buffered
@@ -512,6 +521,11 @@ struct Engine final : EngineBase {
       if ((s = chk(cudaFuncSetAttribute(pair_persist_kernel<T, D, KK, INTEG, PERSIST_BLOCK, PERSIST_ITEMS>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps_smem),
                    "smem attr persist"))) return s;
+    }
+    if (use_group3) {
+      if ((s = chk(cudaFuncSetAttribute(bucket_group3_kernel<T, D, KK, INTEG, PAIR3_BLOCK, PAIR3_ITEMS>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p3_smem),
+                   "smem attr group3"))) return s;
     }
     if (use_pair3) {
       if ((s = chk(cudaFuncSetAttribute(bucket_pair3_kernel<T, D, KK, INTEG, PAIR3_BLOCK, PAIR3_ITEMS>,
@@ -661,6 +675,9 @@ struct Engine final : EngineBase {
       pair_persist_kernel<T, D, KK, INTEG, PERSIST_BLOCK, PERSIST_ITEMS>
           <<<std::min<uint32_t>(c.L.nbuckets, (uint32_t)num_sms), PERSIST_BLOCK, ps_smem, s>>>(
               c.P, in, c.L.cap2, c.S, out, ocap, cur_next);
+    else if (use_group3)
+      bucket_group3_kernel<T, D, KK, INTEG, PAIR3_BLOCK, PAIR3_ITEMS>
+          <<<c.L.nbuckets, PAIR3_BLOCK, p3_smem, s>>>(c.P, in, c.L.cap2, c.S, out, ocap, cur_next);
     else if (use_pair3)
       bucket_pair3_kernel<T, D, KK, INTEG, PAIR3_BLOCK, PAIR3_ITEMS>
           <<<c.L.nbuckets, PAIR3_BLOCK, p3_smem, s>>>(c.P, in, c.L.cap2, c.S, out, ocap, cur_next);

@@ -2163,6 +2163,256 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_pair3_kernel(const __g
   if (P.prof && threadIdx.x == 0) atomicAdd(&P.prof[63], 1ull);
 }
 
+// batch of more than G members (p a power of two, N mod p = 1): all members
+// from the old positions (canonical order: ascending), then written in place
+template <typename T, int D, int KK, int INTEG>
+__device__ __noinline__ void group3_big(const DevParams& P, uint32_t m, uint32_t l0, uint32_t l1,
+                                        const uint16_t* ord, SX<T> xs, const uint32_t* id_l,
+                                        const uint32_t* ta, const uint16_t* tb, const uint32_t* off,
+                                        uint16_t* inv, uint32_t osh) {
+  T xn[33][D];
+  for (uint32_t q = l0; q < l1; ++q)
+    interior_update<T, D, KK, INTEG>(P, m, q, l0, l1, ord, xs, id_l[ord[q]], xn[q - l0]);
+  for (uint32_t q = l0; q < l1; ++q) {
+    const uint32_t e = ord[q];
+    check_finite<T, D>(xn[q - l0], P, id_l[e], m);
+#pragma unroll
+    for (int c = 0; c < D; ++c) xs.at(c, e) = xn[q - l0][c];
+    inv[off[ta[e] >> osh] + tb[e]] = (uint16_t)e;
+  }
+}
+
+// Bucket step for 2 < p <= 32 with the compact footprint of bucket_pair3_kernel
+// (packed u16 sub-digit counters, register items through the sort, three
+// 256-thread CTAs per SM) and the lane-group batch update of
+// bucket_fused_kernel.
+template <typename T, int D, int KK, int INTEG, int BLOCK, int ITEMS>
+static __global__ void __launch_bounds__(BLOCK, 3) bucket_group3_kernel(const __grid_constant__ DevParams P, State<T, D> src,
+                                                                   uint32_t scap,
+                                                                   const uint32_t* __restrict__ S,
+                                                                   const __grid_constant__ OutDst<T, D> dst, uint32_t dcap,
+                                                                   uint32_t* __restrict__ cur_next) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  RBM_PROF_BEGIN(P);
+  const uint32_t b = blockIdx.x;
+  const uint32_t s0 = S[b], n = S[b + 1] - s0, sb = b * scap;
+  if (n == 0) return;
+  const uint32_t nsb = 1u << P.SB;
+  const uint32_t nout = 1u << P.b1;
+  // sub-digit counts and offsets as packed u16 pairs (bucket sizes < 2^16);
+  // the same words later hold the <= 1024 output digit counts / offsets
+  const uint32_t ncw = (nsb / 2 > nout) ? nsb / 2 : nout;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* off = cnt + ncw;
+  uint32_t* gbase = off + ncw;
+  uint32_t* wsum = gbase + nout;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);
+  const uint32_t cap = P.cap;
+  const uint32_t m = (uint32_t)*P.step;
+  for (uint32_t i = threadIdx.x; i < ncw / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
+  if (n > cap) {  // oversized bucket: the global-scratch path with its own 8-bit counters
+    __shared__ uint32_t bigc[2 * 256 + 64];
+    __syncthreads();
+    fused_big_path<T, D, KK, INTEG, BLOCK>(P, src, dst, cur_next, s0, sb, n, m, dcap, bigc, bigc + 256, bigc + 512);
+    return;
+  }
+  unsigned char* p = reinterpret_cast<unsigned char*>(bar + 2);
+  uint32_t* id_l = reinterpret_cast<uint32_t*>(p);
+  p += (size_t)(cap + 8) * 4;
+  uint32_t* key_l = reinterpret_cast<uint32_t*>(p);  // key_m by e; then key_{m+1} by e
+  p += (size_t)(cap + 8) * 4;
+  const uint32_t xst = (uint32_t)((((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15) / sizeof(T));
+  T* xr = reinterpret_cast<T*>(p);
+  p += (size_t)D * xst * sizeof(T);
+  uint32_t* ks = reinterpret_cast<uint32_t*>(p);   // composites (sort); then tb | inv (u16 each)
+  uint16_t* tb = reinterpret_cast<uint16_t*>(ks);
+  uint16_t* inv = tb + cap;
+  uint32_t* ta = key_l;
+  uint16_t* ord = reinterpret_cast<uint16_t*>(ks + cap);
+  load_bucket<T, D>(src, sb, n, id_l, key_l, xr, xst, bar);
+  __syncthreads();
+  mbar_wait(bar, 0);
+  RBM_PROF(P, 0);
+  const SX<T> xs{xr, xst};
+
+  // 1-3. exact (key, id) sort: counting sort on SB sub-digit bits + rank in sub-bucket
+  const uint32_t shsb = 32u - P.B - P.SB;
+  const uint32_t lowmask = (P.lowbits >= 32u) ? 0xffffffffu : ((1u << P.lowbits) - 1u);
+  uint32_t rc[ITEMS], rs[ITEMS];
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const uint32_t e = k * BLOCK + threadIdx.x;
+    if (e < n) {
+      const uint32_t key = key_l[e];
+      const uint32_t sd = (key >> shsb) & (nsb - 1u);
+      rc[k] = ((key & lowmask) << P.idbits) | id_l[e];
+      const uint32_t sh16 = (sd & 1u) << 4;
+      rs[k] = (sd << 16) | ((atomicAdd(&cnt[sd >> 1], 1u << sh16) >> sh16) & 0xffffu);
+    }
+  }
+  __syncthreads();
+  RBM_PROF(P, 1);
+  block_excl_scan_u16x2<BLOCK>(cnt, off, nsb / 2, wsum);
+  RBM_PROF(P, 2);
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const uint32_t e = k * BLOCK + threadIdx.x;
+    if (e < n) {
+      const uint32_t sd = rs[k] >> 16;
+      ks[((off[sd >> 1] >> ((sd & 1u) << 4)) & 0xffffu) + (rs[k] & 0xffffu)] = rc[k];
+    }
+  }
+  __syncthreads();
+  RBM_PROF(P, 3);
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const uint32_t e = k * BLOCK + threadIdx.x;
+    if (e < n) {
+      const uint32_t sd = rs[k] >> 16, sh16 = (sd & 1u) << 4;
+      const uint32_t a = (off[sd >> 1] >> sh16) & 0xffffu, c = (cnt[sd >> 1] >> sh16) & 0xffffu;
+      uint32_t r = a;
+      if (c > 1) {  // sub-buckets hold ~1 element: a short predicated scan
+#pragma unroll
+        for (uint32_t i = 0; i < 4; ++i)
+          if (i < c) r += (ks[a + i] < rc[k]) ? 1u : 0u;
+        for (uint32_t i = 4; i < c; ++i) r += (ks[a + i] < rc[k]) ? 1u : 0u;
+      }
+      ord[r] = (uint16_t)e;
+    }
+  }
+  __syncthreads();
+  RBM_PROF(P, 4);
+  // interior batches [kfirst, klast) of this bucket (as bucket_fused_kernel);
+  // positions [0, head) and [tail, n) belong to straddling batches
+  uint32_t kfirst = batch_index(s0, P);
+  if (kfirst * P.p < s0) ++kfirst;
+  uint32_t klast;
+  {
+    const uint32_t kl = batch_index(s0 + n - 1, P);
+    klast = (batch_end(kl, P) <= s0 + n) ? kl + 1 : kl;
+  }
+  const uint32_t head = (kfirst < klast) ? kfirst * P.p - s0 : n;
+  const uint32_t tail = (kfirst < klast) ? batch_end(klast - 1, P) - s0 : n;
+  const uint32_t osh = 32u - P.b1;
+  for (uint32_t i = threadIdx.x; i < nout / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
+  if (P.dbg_order)
+    for (uint32_t q = threadIdx.x; q < n; q += BLOCK) P.dbg_order[s0 + q] = id_l[ord[q]];
+  __syncthreads();
+  RBM_PROF(P, 5);
+  // 4. output partition first (key_{m+1} depends on the id only): digit and
+  //    rank of every interior member; ks is dead: tb = rank by e
+#pragma unroll 1
+  for (uint32_t q = head + threadIdx.x; q < tail; q += BLOCK) {
+    const uint32_t e = ord[q];
+    const uint32_t kn = shuffle_key(P, id_l[e], m + 1);
+    ta[e] = kn;
+    tb[e] = (uint16_t)atomicAdd(&cnt[kn >> osh], 1u);
+  }
+  // straddlers: unchanged, to their sorted places in the own gapped range
+  for (uint32_t t = threadIdx.x; t < head + (n - tail); t += BLOCK) {
+    const uint32_t q = t < head ? t : tail + (t - head);
+    const uint32_t e = ord[q];
+    src.id[sb + q] = id_l[e];
+#pragma unroll
+    for (int c = 0; c < D; ++c) src.x[c][sb + q] = xs.at(c, e);
+  }
+  __syncthreads();
+  constexpr int NRES = (1024 + BLOCK - 1) / BLOCK;
+  uint32_t gres[NRES];
+#pragma unroll
+  for (int r = 0; r < NRES; ++r) {
+    const uint32_t i = threadIdx.x + r * BLOCK;
+    const uint32_t h = i < nout ? cnt[i] : 0u;
+    gres[r] = h ? atomicAdd(&cur_next[(size_t)out_seg(P, i, blockIdx.x) * CUR1_STRIDE], h) : 0u;
+  }
+  const uint32_t total = block_excl_scan4<BLOCK>(cnt, off, nout, wsum);
+  RBM_PROF(P, 8);
+  // 5. Eq. (2.2) + update in place: one lane group of G = P.group lanes per
+  //    batch, each pair evaluated once in the canonical rotation order
+  //    (batch_force); staging index of each member
+  const uint32_t G = P.group;
+  {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t gpw = 32u / G, gi = lane / G, li = lane & (G - 1);
+    const uint32_t stride = (BLOCK / 32) * gpw;
+    for (uint32_t kb = kfirst + warp * gpw; kb < klast; kb += stride) {  // warp-uniform
+      const uint32_t k = kb + gi;
+      const bool valid = k < klast;
+      const uint32_t l0 = valid ? k * P.p - s0 : 0;
+      const uint32_t sz = valid ? batch_end(k, P) - s0 - l0 : 0;
+      const bool act = valid && sz <= G && li < sz;
+      const uint32_t e = act ? ord[l0 + li] : 0u;
+      T xi[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) xi[c] = act ? xs.at(c, e) : T(0);
+      const uint32_t id = act ? id_l[e] : 0u;
+      T f[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) f[c] = T(0);
+      for (uint32_t o = 1; o <= G / 2; ++o) {
+        const uint32_t jp = (li + o) & (G - 1), jm = (li - o) & (G - 1);
+        T xj[D], t[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) xj[c] = __shfl_sync(0xffffffffu, xi[c], (int)jp, (int)G);
+        if (act && jp < sz) {
+          pair_term<T, D, KK, INTEG>(xi, xj, t, P);
+#pragma unroll
+          for (int c = 0; c < D; ++c) f[c] = add_rn(f[c], t[c]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < D; ++c) t[c] = T(0);
+        }
+        if (o < G / 2) {  // warp-uniform
+#pragma unroll
+          for (int c = 0; c < (INTEG == 2 ? 1 : D); ++c) {
+            const T r = __shfl_sync(0xffffffffu, t[c], (int)jm, (int)G);
+            if (act && jm < sz) f[c] = sub_rn(f[c], r);
+          }
+        }
+      }
+      if (act) {
+        T z[D], xn[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) z[c] = T(0);
+        if (P.has_noise) Normals<T, D>::get(P, id, m, TAG_NOISE, z);
+        const T inv_b = batch_inv<T>(P, sz);
+#pragma unroll
+        for (int c = 0; c < D; ++c) f[c] *= inv_b;
+        member_update<T, D, INTEG>(xi, f, z, xn, P, P.verlet_start != 0);
+        check_finite<T, D>(xn, P, id, m);
+#pragma unroll
+        for (int c = 0; c < D; ++c) xs.at(c, e) = xn[c];
+        inv[off[ta[e] >> osh] + tb[e]] = (uint16_t)e;
+      }
+    }
+  }
+  // a batch larger than the lane group (p a power of two and N mod p = 1: the
+  // last batch has p + 1 members): one thread, out of line
+  if (threadIdx.x == 0 && klast > kfirst) {
+    const uint32_t lb0 = (klast - 1) * P.p - s0, lb1 = batch_end(klast - 1, P) - s0;
+    if (lb1 - lb0 > G) group3_big<T, D, KK, INTEG>(P, m, lb0, lb1, ord, xs, id_l, ta, tb, off, inv, osh);
+  }
+#pragma unroll
+  for (int r = 0; r < NRES; ++r)  // gbase[d] - off[d]: output position j goes to slot gbase[dg] + j
+    if (threadIdx.x + r * BLOCK < nout) gbase[threadIdx.x + r * BLOCK] = gres[r] - off[threadIdx.x + r * BLOCK];
+  __syncthreads();
+  RBM_PROF(P, 6);
+  // 6. staged slots -> coalesced runs of the step-(m+1) pass-1 buckets
+  for (uint32_t j = threadIdx.x; j < total; j += BLOCK) {
+    const uint32_t e = inv[j];
+    const uint32_t kn = ta[e];
+    const uint32_t dg = kn >> osh;
+    const uint32_t slot = gbase[dg] + j;
+    if (slot >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
+    T xo[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) xo[c] = xs.at(c, e);
+    out_put<T, D>(dst, out_seg(P, dg, blockIdx.x), dcap, slot, id_l[e], kn, xo);
+  }
+  RBM_PROF(P, 7);
+  if (P.prof && threadIdx.x == 0) atomicAdd(&P.prof[63], 1ull);
+}
+
 // -------------------------------- persistent fused bucket step, p = 2
 // Same contract and arithmetic as bucket_pair_kernel, restructured for the
 // SM: one CTA per SM loops over buckets b = blockIdx.x, += gridDim.x with the
