@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C5", choices=["C1", "C2", "C3", "C4", "C5", "wealth"])
+    ap.add_argument("--workload", default="C5", choices=["C1", "C2", "C3", "C4", "C5", "wealth", "verlet", "opinion"])
     ap.add_argument("--p", type=int, default=None, help="batch size override (C5: 2, 8, 32)")
     ap.add_argument("--scheme", default="rbm1", choices=["rbm1", "rbmr", "rbmr_seq"])
     ap.add_argument("--n", type=int, default=None, help="particles per GPU override")
@@ -66,6 +66,8 @@ def workload(args, rank: int) -> dict:
         cfg = RI.c5_coulomb_reg(p=args.p or 2, **kw)
     elif args.workload == "wealth":
         cfg = RI.wealth(**{k: v for k, v in kw.items() if k != "scheme"})
+    elif args.workload == "opinion":  # the paper's opinion dynamics with eps_N noise (row f4)
+        cfg = RI.opinion_paper(noise=True, **{k: v for k, v in kw.items() if k != "scheme"})
     else:
         cfg = RI.ALL[args.workload](**kw)
         if args.p:
@@ -94,7 +96,12 @@ def kernel_bytes(name: str, cfg: dict, prefix_bits: int) -> float:
     the single-bucket path (prefix_bits == 0) moves id + x (R = 4 + d*s)."""
     n = cfg["n"]
     R = (8 if prefix_bits > 0 else 4) + cfg["d"] * elt(cfg)
-    return {"scatter_sub": 2.0 * R * n, "split_owner": 2.0 * R * n, "bucket_step": 2.0 * R * n}.get(name, 0.0)
+    # RBM-r (Jacobi) batch kernel, per slot (N slots): gather x_j as a padded
+    # 4-scalar AoS record, write Delta_s (4 scalars), j_s (4 B), the mailbox
+    # entry (4 B) and read+write the per-particle counter (8 B)
+    rbmr = n * (4 * elt(cfg) + 4 * elt(cfg) + 4 + 4 + 8)
+    return {"scatter_sub": 2.0 * R * n, "split_owner": 2.0 * R * n, "bucket_step": 2.0 * R * n,
+            "rbmr_batch": float(rbmr)}.get(name, 0.0)
 
 
 class Clocks:
@@ -189,7 +196,9 @@ def config_dict(args, cfg, world):
         "C1": "Dyson Brownian motion", "C2": "Thomson-type Coulomb on S^2",
         "C3": "bounded-confidence opinion", "C4": "2-D Gaussian aggregation",
         "C5": "3-D regularised Coulomb, partitioned-system size per GPU",
-        "wealth": "wealth model (paper Sec. 5.2.1, row f4)"}[args.workload],
+        "wealth": "wealth model (paper Sec. 5.2.1, row f4)",
+        "verlet": "second-order system, position Verlet (paper Sec. 4.3, row f3)",
+        "opinion": "opinion dynamics, closed window, eps_N noise (paper Sec. 5.2.2, row f4)"}[args.workload],
         "n_per_gpu": cfg["n"], "d": cfg["d"], "p": cfg["p"], "scheme": cfg["scheme"],
         "kernel": cfg["kernel"], "integrator": cfg["integrator"], "dt": cfg["dt"],
         "sigma": cfg["sigma"],
@@ -382,9 +391,10 @@ def main():
         roof = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": ach / peak, "peak_source": peak_kind, "traffic": traffic,
                 "algorithmic_bytes_per_launch": nbytes, "avg_launch_ms": avg_ms}
-    else:
-        roof = {"bound": "alu", "kernel": name, "achieved": None, "peak": None, "unit": "GB/s",
-                "frac": None, "traffic": traffic, "avg_launch_ms": avg_ms}
+    else:  # resident multi-step kernel (N <= 2048) / RBM-r' levels: latency-bound, no byte roofline
+        roof = {"bound": "latency", "kernel": name, "achieved": None, "peak": None, "unit": "GB/s",
+                "frac": None, "traffic": traffic, "avg_launch_ms": avg_ms,
+                "note": "one CTA (resident) or one launch per level: bounded by barrier and launch latency, not by HBM or ALU throughput"}
     step_ms = ms / K
     shares = {k: round(v / max(nrec, 1), 4) for k, v in per_kernel.items()}
     R = 4 + cfg["d"] * elt(cfg)

@@ -85,7 +85,20 @@ def wealth(n: int = 10**5, integrator: str = "split", seed: int = 1, kappa: floa
                 seed=seed, init="abs_normal", iparam=[0.0, 1.0], steps=3000)
 
 
-ALL = {"C1": c1_dyson, "C2": c2_sphere, "C3": c3_opinion, "C4": c4_aggregation, "C5": c5_coulomb_reg}
+def second_order(n: int = 2**24, p: int = 2, seed: int = 1, scheme: str = "rbm1") -> dict:
+    """The paper's second-order system at scale: X' = V, V' = mean
+    over the batch of K(X^i - X^j) - beta X^i with the smooth test kernel,
+    position Verlet with the paper's start step, fp64, stored as d = 2
+    components (x, v) at the start and (x_n, x_{n-1}) after; (x_0, v_0) iid
+    N(0, 1) (the paper's example size is N = 500; this is the same system at
+    2^24 particles for the throughput line)."""
+    return dict(d=2, n=n, p=p, dtype="f64", scheme=scheme, integrator="verlet", kernel="smooth",
+                kparam=[], potential="harmonic", vparam=[1.0], constraint="none", sigma=0.0,
+                dt=2.0 ** -7, seed=seed, init="normal", iparam=[0.0, 1.0], state_form="xv", steps=100)
+
+
+ALL = {"C1": c1_dyson, "C2": c2_sphere, "C3": c3_opinion, "C4": c4_aggregation, "C5": c5_coulomb_reg,
+       "verlet": second_order}
 
 
 def user_x0(n: int, d: int, seed: int, dist: str = "normal", scale: float = 1.0) -> np.ndarray:

@@ -8,13 +8,15 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>
 timeout 1500 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider -rf > $O/pytest_gpu.log 2>&1; echo pytest_rc=$? >> $O/pytest_gpu.log
 timeout 900 python bench.py > $O/bench_default.log 2>&1; echo rc=$? >> $O/bench_default.log
 timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > $O/bench_reference.log 2>&1; echo rc=$? >> $O/bench_reference.log
-for W in C1 C2 C3 C4; do timeout 300 python bench.py --workload $W --steps 20 --warmup 3 --no-cpu-baseline > $O/bench_$W.log 2>&1; done
+for W in C1 C2 C3 C4; do timeout 300 python bench.py --workload $W --steps 20 --warmup 3 > $O/bench_$W.log 2>&1; done
 timeout 300 python bench.py --workload C1 --steps 1000 --warmup 10 --no-cpu-baseline > $O/bench_C1_1000.log 2>&1
 for P in 8 32; do timeout 300 python bench.py --p $P --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > $O/bench_C5p$P.log 2>&1; done
 timeout 300 python bench.py --scheme rbmr --steps 5 --warmup 2 --no-cpu-baseline --no-e2e > $O/bench_C5rbmr.log 2>&1
 timeout 300 python bench.py --scheme rbmr_seq --steps 5 --warmup 2 --no-cpu-baseline --no-e2e > $O/bench_C5rbmr_seq.log 2>&1
 timeout 300 python bench.py --workload wealth --steps 20 --warmup 3 --no-cpu-baseline > $O/bench_wealth.log 2>&1
 timeout 300 python bench.py --direct --steps 5 --warmup 2 --no-cpu-baseline > $O/bench_direct.log 2>&1
+timeout 300 python bench.py --workload verlet --steps 20 --warmup 3 --no-cpu-baseline > $O/bench_verlet.log 2>&1
+timeout 300 python bench.py --workload opinion --steps 1000 --warmup 10 --no-cpu-baseline > $O/bench_opinion.log 2>&1
 CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
 timeout 300 $CMD > $O/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 60 --csv --log-file $O/launches_C5.csv $CMD > $O/ncu_launch.log 2>&1
