@@ -107,7 +107,11 @@ KCASES = [("smooth", 1), ("smooth", 2), ("gauss_attr_rep", 2), ("gauss_attr_rep"
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("kernel,d", KCASES)
-@pytest.mark.parametrize("n,p", [(3001, 2), (20011, 3), (20011, 8), (4099, 32), (999, 999)])
+# N mod p = 1 with p a power of two: the last batch has p + 1 > G members
+# (out-of-line serial path of the group kernel); p = 5: a 6-member last batch
+# inside an 8-lane group
+@pytest.mark.parametrize("n,p", [(3001, 2), (20011, 3), (20011, 8), (4099, 32), (999, 999),
+                                 (20009, 4), (20009, 8), (4129, 32), (20006, 5)])
 def test_one_step_parity(R, O, dtype, kernel, d, n, p):
     c = cfg_of(kernel, d, p, n, dtype=dtype, step0=3)
     x0 = RI.user_x0(n, d, seed=n + p, dist="normal")
