@@ -308,29 +308,32 @@ def test_replicas_differ_and_match_own_run(R):
 
 
 # ----------------------------------------------- full-size sampled checks
-@pytest.mark.parametrize("which", ["C4", "C5p8"])
+@pytest.mark.parametrize("which", ["C4", "C5p8", "C5p2"])
 def test_full_size_sampled(R, O, which):
     """BASELINE.json sizes in the bench launch configuration: the whole
     permutation is checked by properties (partition + (key,id) order with the
-    oracle's keys), and 3000 sampled batches against the oracle's batch update."""
+    oracle's keys), and 3000 sampled batches against the oracle's batch update,
+    at step 0 (first-step prologue) and step 1 (the steady-state path the
+    bench times: pass-2 split of the carried partition, then the bucket step)."""
     if which == "C4":
         c = RI.c4_aggregation()
     else:
-        c = RI.c5_coulomb_reg(p=8)
-    m = 0
+        c = RI.c5_coulomb_reg(p=8 if which == "C5p8" else 2)
     s = R.RBM(c)
-    x0 = s.gather(host=True).astype(np.float64)
-    order = s.step_permutation()
-    x1 = s.gather(host=True).astype(np.float64)
     n, p = c["n"], c["p"]
-    assert np.array_equal(np.bincount(order, minlength=n), np.ones(n, dtype=np.int64))
-    keys = O.keys(c, m)
-    k = keys[order].astype(np.uint64) << np.uint64(32) | order.astype(np.uint64)
-    assert np.all(k[1:] > k[:-1])
-    del k, keys
     rng = np.random.default_rng(0)
-    for b in rng.choice(n // p, 3000, replace=False):
-        ids = order[b * p:(b + 1) * p]
-        want = O.batch_update(c, m, ids, x0[ids])
-        assert E(x1[ids], want) <= 1e-4
+    for m in (0, 1):
+        x0 = s.gather(host=True).astype(np.float64)
+        order = s.step_permutation()
+        x1 = s.gather(host=True).astype(np.float64)
+        assert np.array_equal(np.bincount(order, minlength=n), np.ones(n, dtype=np.int64))
+        keys = O.keys(c, m)
+        k = keys[order].astype(np.uint64) << np.uint64(32) | order.astype(np.uint64)
+        assert np.all(k[1:] > k[:-1])
+        del k, keys
+        for b in rng.choice(n // p, 3000, replace=False):
+            ids = order[b * p:(b + 1) * p]
+            want = O.batch_update(c, m, ids, x0[ids])
+            assert E(x1[ids], want) <= 1e-4
+        del x0, x1, order
     s.close()
