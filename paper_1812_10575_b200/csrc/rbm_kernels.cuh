@@ -2049,8 +2049,10 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_pair3_kernel(const __g
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t e = k * BLOCK + threadIdx.x;
     if (e < n) {
-      const uint32_t sd = rs[k] >> 16;
-      ks[((off[sd >> 1] >> ((sd & 1u) << 4)) & 0xffffu) + (rs[k] & 0xffffu)] = rc[k];
+      const uint32_t sd = rs[k] >> 16, sh16 = (sd & 1u) << 4;
+      const uint32_t a = (off[sd >> 1] >> sh16) & 0xffffu, c = (cnt[sd >> 1] >> sh16) & 0xffffu;
+      ks[a + (rs[k] & 0xffffu)] = rc[k];
+      rs[k] = (a << 16) | c;  // sub-bucket start and size, for the rank below
     }
   }
   __syncthreads();
@@ -2059,8 +2061,7 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_pair3_kernel(const __g
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t e = k * BLOCK + threadIdx.x;
     if (e < n) {
-      const uint32_t sd = rs[k] >> 16, sh16 = (sd & 1u) << 4;
-      const uint32_t a = (off[sd >> 1] >> sh16) & 0xffffu, c = (cnt[sd >> 1] >> sh16) & 0xffffu;
+      const uint32_t a = rs[k] >> 16, c = rs[k] & 0xffffu;
       uint32_t r = a;
       if (c > 1) {  // sub-buckets hold ~1 element: a short predicated scan
 #pragma unroll
@@ -2258,8 +2259,10 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_group3_kernel(const __
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t e = k * BLOCK + threadIdx.x;
     if (e < n) {
-      const uint32_t sd = rs[k] >> 16;
-      ks[((off[sd >> 1] >> ((sd & 1u) << 4)) & 0xffffu) + (rs[k] & 0xffffu)] = rc[k];
+      const uint32_t sd = rs[k] >> 16, sh16 = (sd & 1u) << 4;
+      const uint32_t a = (off[sd >> 1] >> sh16) & 0xffffu, c = (cnt[sd >> 1] >> sh16) & 0xffffu;
+      ks[a + (rs[k] & 0xffffu)] = rc[k];
+      rs[k] = (a << 16) | c;  // sub-bucket start and size, for the rank below
     }
   }
   __syncthreads();
@@ -2268,8 +2271,7 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_group3_kernel(const __
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t e = k * BLOCK + threadIdx.x;
     if (e < n) {
-      const uint32_t sd = rs[k] >> 16, sh16 = (sd & 1u) << 4;
-      const uint32_t a = (off[sd >> 1] >> sh16) & 0xffffu, c = (cnt[sd >> 1] >> sh16) & 0xffffu;
+      const uint32_t a = rs[k] >> 16, c = rs[k] & 0xffffu;
       uint32_t r = a;
       if (c > 1) {  // sub-buckets hold ~1 element: a short predicated scan
 #pragma unroll
