@@ -2072,6 +2072,8 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_pair3_kernel(const __g
       ord[r] = (uint16_t)e;
     }
   }
+  // the packed sub-digit counters are dead: they become the output digit counts
+  for (uint32_t i = threadIdx.x; i < nout / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   RBM_PROF(P, 4);
   // interior pairs: even global starts in [s0, end), end excludes a final triple (N odd)
@@ -2084,10 +2086,8 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_pair3_kernel(const __g
   const bool triple = (N & 1u) && (pend >= s0) && (N <= s0 + n);
   const uint32_t tri0 = triple ? pend - s0 : n;          // [tri0, n): the size-3 remainder batch
   const uint32_t osh = 32u - P.b1;
-  for (uint32_t i = threadIdx.x; i < nout / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
   if (P.dbg_order)
     for (uint32_t q = threadIdx.x; q < n; q += BLOCK) P.dbg_order[s0 + q] = id_l[ord[q]];
-  __syncthreads();
   RBM_PROF(P, 5);
   // 4. output partition first (key_{m+1} depends on the id only): digit and
   //    rank of every interior member, so the run reservations below are in
@@ -2282,6 +2282,8 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_group3_kernel(const __
       ord[r] = (uint16_t)e;
     }
   }
+  // the packed sub-digit counters are dead: they become the output digit counts
+  for (uint32_t i = threadIdx.x; i < nout / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   RBM_PROF(P, 4);
   // interior batches [kfirst, klast) of this bucket (as bucket_fused_kernel);
@@ -2296,10 +2298,8 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_group3_kernel(const __
   const uint32_t head = (kfirst < klast) ? kfirst * P.p - s0 : n;
   const uint32_t tail = (kfirst < klast) ? batch_end(klast - 1, P) - s0 : n;
   const uint32_t osh = 32u - P.b1;
-  for (uint32_t i = threadIdx.x; i < nout / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
   if (P.dbg_order)
     for (uint32_t q = threadIdx.x; q < n; q += BLOCK) P.dbg_order[s0 + q] = id_l[ord[q]];
-  __syncthreads();
   RBM_PROF(P, 5);
   // 4. output partition first (key_{m+1} depends on the id only): digit and
   //    rank of every interior member; ks is dead: tb = rank by e
