@@ -189,14 +189,20 @@ __device__ __forceinline__ uint32_t shuffle_key(const DevParams& P, uint32_t id,
 }
 
 // ------------------------------------------------------------ uniform maps
-// fp32: (2 (w>>9) + 1) 2^-24 == ((w >> 8) | 1) 2^-24, exact
+// fp32: (2 (w>>9) + 1) 2^-24 == ((w >> 8) | 1) 2^-24, exact.  Computed as
+// (1 + (w>>9) 2^-23) - (1 - 2^-24): the float with mantissa w>>9 minus one
+// constant; the exact result is an odd multiple of 2^-24 below 1, so the one
+// rounding is exact (checked for all 2^23 values of w>>9) and no int->float
+// conversion is issued
 __device__ __forceinline__ float u01f(uint32_t w) {
-  return __uint2float_rn((w >> 8) | 1u) * 0x1p-24f;
+  return __uint_as_float(0x3f800000u | (w >> 9)) + __uint_as_float(0xbf7fffffu);
 }
-// fp64: (2k+1) 2^-53 with k = (a:b) >> 12, exact
+// fp64: (2k+1) 2^-53 with k = (a:b) >> 12, exact; as (1 + k 2^-52) - (1 - 2^-53)
+// (one exact rounding, as for fp32)
 __device__ __forceinline__ double u01d(uint32_t a, uint32_t b) {
   const uint64_t k = ((((uint64_t)a) << 32) | b) >> 12;
-  return (double)(2ull * k + 1ull) * 0x1p-53;
+  return __longlong_as_double((long long)(0x3ff0000000000000ull | k)) +
+         __longlong_as_double((long long)0xbfefffffffffffffull);
 }
 
 // ------------------------------------------------------------ Box-Muller

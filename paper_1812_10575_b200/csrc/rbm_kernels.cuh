@@ -1837,9 +1837,12 @@ static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) bucket_pair_kernel
       uint32_t r = a;
       if (c > 1) {  // sub-buckets hold ~1 element: a short predicated scan
 #pragma unroll
-        for (uint32_t i = 0; i < 4; ++i)
+        for (uint32_t i = 0; i < 6; ++i)
           if (i < c) r += (ks[a + i] < rc[k]) ? 1u : 0u;
-        for (uint32_t i = 4; i < c; ++i) r += (ks[a + i] < rc[k]) ? 1u : 0u;
+        // more than 6 (probability ~6e-4 per element): a plain loop, not
+        // unrolled, so warps that never take it pay no loop prologue
+#pragma unroll 1
+        for (uint32_t i = 6; i < c; ++i) r += (ks[a + i] < rc[k]) ? 1u : 0u;
       }
       ord[r] = (uint16_t)e;
     }
@@ -2065,9 +2068,12 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_pair3_kernel(const __g
       uint32_t r = a;
       if (c > 1) {  // sub-buckets hold ~1 element: a short predicated scan
 #pragma unroll
-        for (uint32_t i = 0; i < 4; ++i)
+        for (uint32_t i = 0; i < 6; ++i)
           if (i < c) r += (ks[a + i] < rc[k]) ? 1u : 0u;
-        for (uint32_t i = 4; i < c; ++i) r += (ks[a + i] < rc[k]) ? 1u : 0u;
+        // more than 6 (probability ~6e-4 per element): a plain loop, not
+        // unrolled, so warps that never take it pay no loop prologue
+#pragma unroll 1
+        for (uint32_t i = 6; i < c; ++i) r += (ks[a + i] < rc[k]) ? 1u : 0u;
       }
       ord[r] = (uint16_t)e;
     }
@@ -2275,9 +2281,12 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_group3_kernel(const __
       uint32_t r = a;
       if (c > 1) {  // sub-buckets hold ~1 element: a short predicated scan
 #pragma unroll
-        for (uint32_t i = 0; i < 4; ++i)
+        for (uint32_t i = 0; i < 6; ++i)
           if (i < c) r += (ks[a + i] < rc[k]) ? 1u : 0u;
-        for (uint32_t i = 4; i < c; ++i) r += (ks[a + i] < rc[k]) ? 1u : 0u;
+        // more than 6 (probability ~6e-4 per element): a plain loop, not
+        // unrolled, so warps that never take it pay no loop prologue
+#pragma unroll 1
+        for (uint32_t i = 6; i < c; ++i) r += (ks[a + i] < rc[k]) ? 1u : 0u;
       }
       ord[r] = (uint16_t)e;
     }
