@@ -63,7 +63,8 @@ __device__ __forceinline__ void out_put(const OutDst<T, D>& o, uint32_t v, uint3
 template <typename T> struct SX {
   T* base;
   uint32_t stride;
-  __device__ __forceinline__ T& at(int c, uint32_t e) const { return base[(size_t)c * stride + e]; }
+  // 32-bit index: every window is < 2^32 elements (shared memory or a bucket's scratch)
+  __device__ __forceinline__ T& at(int c, uint32_t e) const { return base[(uint32_t)c * stride + e]; }
 };
 
 // ----------------------------------------------------------------- helpers
@@ -2098,14 +2099,15 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_pair3_kernel(const __g
   // 4. output partition first (key_{m+1} depends on the id only): digit and
   //    rank of every interior member, so the run reservations below are in
   //    flight while the batches are computed.  ks is dead: tb = rank by e.
-#pragma unroll 1
-  for (uint32_t q = head + threadIdx.x; q < n; q += BLOCK) {
-    if (q >= covered && q < tri0) continue;
+  auto out_rank = [&](uint32_t q) {
     const uint32_t e = ord[q];
     const uint32_t kn = shuffle_key(P, id_l[e], m + 1);
     ta[e] = kn;
     tb[e] = (uint16_t)atomicAdd(&cnt[kn >> osh], 1u);
-  }
+  };
+#pragma unroll 1
+  for (uint32_t q = head + threadIdx.x; q < covered; q += BLOCK) out_rank(q);
+  for (uint32_t q = tri0 + threadIdx.x; q < n; q += BLOCK) out_rank(q);  // the size-3 batch (N odd)
   // straddlers: unchanged, to their sorted places in the own gapped range
   for (uint32_t t = threadIdx.x; t < head + (tri0 - covered); t += BLOCK) {
     const uint32_t q = t < head ? t : covered + (t - head);
