@@ -170,7 +170,13 @@ rbm_status rbm_init(const rbm_config* cfg, void* ws, size_t ws_bytes, void* cuda
  * before the call returns (synchronous); device input is stream-ordered. */
 rbm_status rbm_set_state(rbm_ctx* ctx, const void* x, uint32_t where);
 
-/* Enqueue one step X_m -> X_{m+1} (async); m advances by one. */
+/* Enqueue one step X_m -> X_{m+1} (async); m advances by one.
+ * Determinism: the result is a function of (cfg, X_m, m) only -- not of the
+ * launch geometry, the bucket layout or world_size.  Inside a batch of
+ * p <= 32 members the partner terms K(x_i - x_j) are summed in a fixed
+ * rotation order (each pair evaluated once, K odd);
+ * Eq. (2.2) as written sums in ascending order, so results differ from that
+ * order by rounding only. */
 rbm_status rbm_step(rbm_ctx* ctx);
 
 /* Enqueue nsteps steps as CUDA-graph replays (async); no host work per step. */
