@@ -51,7 +51,7 @@ struct Layout {
 constexpr int FUSED_BLOCK = 256;
 constexpr int PAIR_BLOCK = 512, PAIR_ITEMS = 5;  // p = 2 lean kernel: capacity <= 2560
 constexpr int PAIRS_BLOCK = 256, PAIRS_ITEMS = 6; // p = 2 lean kernel, small buckets: capacity <= 1536
-constexpr int PAIR3_BLOCK = 256, PAIR3_ITEMS = 10; // p = 2 compact kernel, 3 CTAs per SM: capacity <= 2560
+constexpr int PAIR3_BLOCK = 320, PAIR3_ITEMS = 8; // compact kernels, 3 CTAs x 10 warps per SM (64 regs): capacity <= 2560
 constexpr int PERSIST_BLOCK = 1024, PERSIST_ITEMS = 3;  // p = 2 persistent kernel: capacity <= 3072
 constexpr uint32_t FUSED_CAP_MAX = 4096;  // fast-path bucket capacity (u16 indices, smem)
 
