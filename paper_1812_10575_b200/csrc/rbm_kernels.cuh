@@ -2096,17 +2096,16 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_pair3_kernel(const __g
   if (P.dbg_order)
     for (uint32_t q = threadIdx.x; q < n; q += BLOCK) P.dbg_order[s0 + q] = id_l[ord[q]];
   RBM_PROF(P, 5);
-  // 4. output partition first (key_{m+1} depends on the id only): digit and
-  //    rank of every interior member, so the run reservations below are in
-  //    flight while the batches are computed.  ks is dead: tb = rank by e.
+  // 4. key_{m+1} depends on the id only: each pair thread computes its two
+  //    next keys beside the two noise blocks (four independent Philox chains)
+  //    and ranks them in their output digits; ks is dead: tb = rank by e.
   auto out_rank = [&](uint32_t q) {
     const uint32_t e = ord[q];
     const uint32_t kn = shuffle_key(P, id_l[e], m + 1);
     ta[e] = kn;
     tb[e] = (uint16_t)atomicAdd(&cnt[kn >> osh], 1u);
   };
-#pragma unroll 1
-  for (uint32_t q = head + threadIdx.x; q < covered; q += BLOCK) out_rank(q);
+  // (the pairs' next keys and ranks are computed in the pair loop below)
   for (uint32_t q = tri0 + threadIdx.x; q < n; q += BLOCK) out_rank(q);  // the size-3 batch (N odd)
   // straddlers: unchanged, to their sorted places in the own gapped range
   for (uint32_t t = threadIdx.x; t < head + (tri0 - covered); t += BLOCK) {
@@ -2116,17 +2115,6 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_pair3_kernel(const __g
 #pragma unroll
     for (int c = 0; c < D; ++c) src.x[c][sb + q] = xs.at(c, e);
   }
-  __syncthreads();
-  // run reservations of digits threadIdx.x + r BLOCK, consumed after the batches
-  constexpr int NRES = (1024 + BLOCK - 1) / BLOCK;
-  uint32_t gres[NRES];
-#pragma unroll
-  for (int r = 0; r < NRES; ++r) {
-    const uint32_t i = threadIdx.x + r * BLOCK;
-    const uint32_t h = i < nout ? cnt[i] : 0u;
-    gres[r] = h ? atomicAdd(&cur_next[(size_t)out_seg(P, i, blockIdx.x) * CUR1_STRIDE], h) : 0u;
-  }
-  const uint32_t total = block_excl_scan4<BLOCK>(cnt, off, nout, wsum);
   RBM_PROF(P, 8);
   // 5. one thread per pair: Eq. (2.2) + update in place; staging index of each member
   constexpr int PITEMS = (ITEMS + 1) / 2;
@@ -2140,14 +2128,32 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_pair3_kernel(const __g
       T x0[D], x1[D], y0[D], y1[D];
 #pragma unroll
       for (int c = 0; c < D; ++c) { x0[c] = xs.at(c, e0); x1[c] = xs.at(c, e1); }
+      const uint32_t kn0 = shuffle_key(P, id0, m + 1), kn1 = shuffle_key(P, id1, m + 1);
       pair_update<T, D, KK, INTEG>(P, m, x0, x1, id0, id1, y0, y1);
       check_finite<T, D>(y0, P, id0, m);
       check_finite<T, D>(y1, P, id1, m);
 #pragma unroll
       for (int c = 0; c < D; ++c) { xs.at(c, e0) = y0[c]; xs.at(c, e1) = y1[c]; }
-      inv[off[ta[e0] >> osh] + tb[e0]] = (uint16_t)e0;
-      inv[off[ta[e1] >> osh] + tb[e1]] = (uint16_t)e1;
+      ta[e0] = kn0;
+      ta[e1] = kn1;
+      tb[e0] = (uint16_t)atomicAdd(&cnt[kn0 >> osh], 1u);
+      tb[e1] = (uint16_t)atomicAdd(&cnt[kn1 >> osh], 1u);
     }
+  }
+  __syncthreads();
+  // run reservations of digits threadIdx.x + r BLOCK, consumed after the staging index
+  constexpr int NRES = (1024 + BLOCK - 1) / BLOCK;
+  uint32_t gres[NRES];
+#pragma unroll
+  for (int r = 0; r < NRES; ++r) {
+    const uint32_t i = threadIdx.x + r * BLOCK;
+    const uint32_t h = i < nout ? cnt[i] : 0u;
+    gres[r] = h ? atomicAdd(&cur_next[(size_t)out_seg(P, i, blockIdx.x) * CUR1_STRIDE], h) : 0u;
+  }
+  const uint32_t total = block_excl_scan4<BLOCK>(cnt, off, nout, wsum);
+  for (uint32_t q = head + threadIdx.x; q < covered; q += BLOCK) {
+    const uint32_t e = ord[q];
+    inv[off[ta[e] >> osh] + tb[e]] = (uint16_t)e;
   }
   if (triple && threadIdx.x == 0)  // the remainder batch of size 3 (N odd), EM only
     pair3_triple<T, D, KK, INTEG>(P, m, tri0, n, ord, xs, id_l, ta, tb, off, inv, osh);
