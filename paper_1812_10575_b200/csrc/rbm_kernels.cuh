@@ -2320,13 +2320,19 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_group3_kernel(const __
   RBM_PROF(P, 5);
   // 4. output partition first (key_{m+1} depends on the id only): digit and
   //    rank of every interior member; ks is dead: tb = rank by e
-#pragma unroll 1
-  for (uint32_t q = head + threadIdx.x; q < tail; q += BLOCK) {
-    const uint32_t e = ord[q];
-    const uint32_t kn = shuffle_key(P, id_l[e], m + 1);
-    ta[e] = kn;
-    tb[e] = (uint16_t)atomicAdd(&cnt[kn >> osh], 1u);
-  }
+  // keys and ranks of lane-group members are computed in the batch loop
+  // below; here only those of a batch larger than the lane group
+  const uint32_t G = P.group;
+  const uint32_t lb0 = (klast > kfirst) ? (klast - 1) * P.p - s0 : 0u;
+  const uint32_t lb1 = (klast > kfirst) ? batch_end(klast - 1, P) - s0 : 0u;
+  const bool big = lb1 - lb0 > G;
+  if (big)
+    for (uint32_t q = lb0 + threadIdx.x; q < lb1; q += BLOCK) {
+      const uint32_t e = ord[q];
+      const uint32_t kn = shuffle_key(P, id_l[e], m + 1);
+      ta[e] = kn;
+      tb[e] = (uint16_t)atomicAdd(&cnt[kn >> osh], 1u);
+    }
   // straddlers: unchanged, to their sorted places in the own gapped range
   for (uint32_t t = threadIdx.x; t < head + (n - tail); t += BLOCK) {
     const uint32_t q = t < head ? t : tail + (t - head);
@@ -2335,21 +2341,10 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_group3_kernel(const __
 #pragma unroll
     for (int c = 0; c < D; ++c) src.x[c][sb + q] = xs.at(c, e);
   }
-  __syncthreads();
-  constexpr int NRES = (1024 + BLOCK - 1) / BLOCK;
-  uint32_t gres[NRES];
-#pragma unroll
-  for (int r = 0; r < NRES; ++r) {
-    const uint32_t i = threadIdx.x + r * BLOCK;
-    const uint32_t h = i < nout ? cnt[i] : 0u;
-    gres[r] = h ? atomicAdd(&cur_next[(size_t)out_seg(P, i, blockIdx.x) * CUR1_STRIDE], h) : 0u;
-  }
-  const uint32_t total = block_excl_scan4<BLOCK>(cnt, off, nout, wsum);
   RBM_PROF(P, 8);
   // 5. Eq. (2.2) + update in place: one lane group of G = P.group lanes per
   //    batch, each pair evaluated once in the canonical rotation order
   //    (batch_force); staging index of each member
-  const uint32_t G = P.group;
   {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t gpw = 32u / G, gi = lane / G, li = lane & (G - 1);
@@ -2401,16 +2396,29 @@ static __global__ void __launch_bounds__(BLOCK, 3) bucket_group3_kernel(const __
         check_finite<T, D>(xn, P, id, m);
 #pragma unroll
         for (int c = 0; c < D; ++c) xs.at(c, e) = xn[c];
-        inv[off[ta[e] >> osh] + tb[e]] = (uint16_t)e;
+        const uint32_t kn = shuffle_key(P, id, m + 1);
+        ta[e] = kn;
+        tb[e] = (uint16_t)atomicAdd(&cnt[kn >> osh], 1u);
       }
     }
   }
+  __syncthreads();
+  constexpr int NRES = (1024 + BLOCK - 1) / BLOCK;
+  uint32_t gres[NRES];
+#pragma unroll
+  for (int r = 0; r < NRES; ++r) {
+    const uint32_t i = threadIdx.x + r * BLOCK;
+    const uint32_t h = i < nout ? cnt[i] : 0u;
+    gres[r] = h ? atomicAdd(&cur_next[(size_t)out_seg(P, i, blockIdx.x) * CUR1_STRIDE], h) : 0u;
+  }
+  const uint32_t total = block_excl_scan4<BLOCK>(cnt, off, nout, wsum);
+  for (uint32_t q = head + threadIdx.x; q < tail; q += BLOCK) {
+    const uint32_t e = ord[q];
+    inv[off[ta[e] >> osh] + tb[e]] = (uint16_t)e;
+  }
   // a batch larger than the lane group (p a power of two and N mod p = 1: the
   // last batch has p + 1 members): one thread, out of line
-  if (threadIdx.x == 0 && klast > kfirst) {
-    const uint32_t lb0 = (klast - 1) * P.p - s0, lb1 = batch_end(klast - 1, P) - s0;
-    if (lb1 - lb0 > G) group3_big<T, D, KK, INTEG>(P, m, lb0, lb1, ord, xs, id_l, ta, tb, off, inv, osh);
-  }
+  if (threadIdx.x == 0 && big) group3_big<T, D, KK, INTEG>(P, m, lb0, lb1, ord, xs, id_l, ta, tb, off, inv, osh);
 #pragma unroll
   for (int r = 0; r < NRES; ++r)  // gbase[d] - off[d]: output position j goes to slot gbase[dg] + j
     if (threadIdx.x + r * BLOCK < nout) gbase[threadIdx.x + r * BLOCK] = gres[r] - off[threadIdx.x + r * BLOCK];
