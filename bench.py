@@ -13,12 +13,14 @@ is C5's partitioned single system: one global system of N x 2^28 particles
 split by key range over the ranks, exchanges over NCCL (weak scaling);
 --mode ensemble runs independent replicas instead (replica = rank).
 
-Timing: W untimed warm-up steps, then exactly K steps (rbm_run, the user API)
-bracketed by a barrier and torch.cuda.synchronize() on both sides, measured
-with CUDA events on the library's stream, max over ranks.  The state (5.4 GB
-at C5) is larger than the 126 MB L2, so no flush is needed between steps.
-Per-kernel device times come from CUDA events the library records around its
-kernels in the same timed region (rbm_timing_begin/end).
+Timing: W untimed warm-up steps, then exactly K steps (rbm_run, the user API,
+CUDA-graph replays) bracketed by a barrier and torch.cuda.synchronize() on
+both sides, measured with CUDA events on the library's stream, max over
+ranks.  The state (4-5 GB at C5) is larger than the 126 MB L2, so no flush is
+needed between steps.  Per-kernel device times come from a second window of K
+eager steps in which the library records CUDA events around its kernels
+(rbm_timing_begin/end); roofline.frac uses SURVEY 8(d)'s algorithmic bytes
+(2 d s per particle-step) over the dominant kernel's mean launch time.
 """
 from __future__ import annotations
 
@@ -89,18 +91,26 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def kernel_bytes(name: str, cfg: dict, prefix_bits: int) -> float:
-    """Algorithmic HBM bytes per launch: the records the
-    kernel must read and write once in this design.  Records carry id, the
-    shuffle key and d coordinates (R' = 8 + d*s) on the gapped-bucket path;
-    the single-bucket path (prefix_bits == 0) moves id + x (R = 4 + d*s)."""
+def alg_bytes(name: str, cfg: dict) -> float:
+    """ALGORITHMIC HBM bytes per launch: the method reads and
+    writes each particle's state once per step, 2 d s bytes per particle-step
+    (s = bytes per scalar).  Only the kernel that performs the step's update
+    (the bucket step / resident step / RBM-r apply) is credited with them; ids,
+    shuffle keys and the permutation moves are the overhead of realising a
+    random division on a bandwidth machine (8(d) "Algorithmic bytes")."""
+    per = 2.0 * cfg["d"] * elt(cfg) * cfg["n"]
+    return {"bucket_step": per, "rbmr_apply": per}.get(name, 0.0)
+
+
+def design_bytes(name: str, cfg: dict, prefix_bits: int) -> float:
+    """Bytes per launch THIS design must move: the
+    records it reads and writes once (id, carried key, d coordinates on the
+    gapped-bucket path).  Reported beside the algorithmic figure so that
+    traffic-inflating designs cannot hide (8(d) "useful GB/s")."""
     n = cfg["n"]
     R = (8 if prefix_bits > 0 else 4) + cfg["d"] * elt(cfg)
-    # RBM-r (Jacobi) batch kernel, per slot (N slots): gather x_j as a padded
-    # 4-scalar AoS record, write Delta_s (4 scalars), j_s (4 B), the mailbox
-    # entry (4 B) and read+write the per-particle counter (8 B)
     rbmr = n * (4 * elt(cfg) + 4 * elt(cfg) + 4 + 4 + 8)
-    return {"scatter_sub": 2.0 * R * n, "split_owner": 2.0 * R * n, "bucket_step": 2.0 * R * n,
+    return {"scatter_sub": 2.0 * R * n, "bucket_step": 2.0 * R * n,
             "rbmr_batch": float(rbmr)}.get(name, 0.0)
 
 
@@ -183,7 +193,7 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(args, cfg, args.gpus),
+            "config": dict(config_dict(args, c, args.gpus), sample_of=f"{args.workload} at n_per_gpu={cfg['n']}"),
             "cpu_baseline": {"value": v, "unit": "particle-steps/s", "cores": 1, "kind": "oracle",
                              "sample": f"{c['n']} particles of the workload per step (oracle, 1 thread)"},
             "e2e": {"value": v, "unit": "particle-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -352,12 +362,11 @@ def main():
     clk = Clocks(local)
     clk.start()
     time.sleep(0.3)
-    # warm-up right before the timed region (no idle gap: clocks stay up)
+    # warm-up right before the timed region (no idle gap: clocks stay up); it
+    # also captures the CUDA graphs rbm_run replays
     s.run(args.warmup)
     s.sync()
-    # timed region: K steps through rbm_run (the user API); the library records
-    # a CUDA event on its stream around every kernel in these K steps
-    s.timing_begin(K)
+    # timed region: K steps through rbm_run (the user API, graph-replayed)
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -366,8 +375,18 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
-    clocks = clk.stop()
     ms = max_over_ranks(e0.elapsed_time(e1))
+    # per-kernel split: the same K steps again with the library's CUDA events
+    # around every kernel (rbm_timing_begin: eager launches on the same stream)
+    s.timing_begin(K)
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    s.run(K)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    eager_ms = f0.elapsed_time(f1)
+    clocks = clk.stop()
     per_kernel, nrec = s.timing_end()
     s.sync()
     lay = s.layout
@@ -379,7 +398,8 @@ def main():
     name = max(per_kernel, key=per_kernel.get)
     avg_ms = per_kernel[name] / max(nrec, 1)
     peak, peak_kind = peaks()
-    nbytes = kernel_bytes(name, cfg, s.layout[0])
+    nbytes = alg_bytes(name, cfg)
+    dbytes = design_bytes(name, cfg, lay[0])
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -390,7 +410,10 @@ def main():
         ach = nbytes / (avg_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": ach / peak, "peak_source": peak_kind, "traffic": traffic,
-                "algorithmic_bytes_per_launch": nbytes, "avg_launch_ms": avg_ms}
+                "algorithmic_bytes_per_launch": nbytes, "avg_launch_ms": avg_ms,
+                "algorithmic": "2 d s bytes per particle-step (SURVEY 8(d)) x N particles per launch",
+                "design_bytes_per_launch": dbytes,
+                "design_frac": (dbytes / (avg_ms / 1e3) / 1e9) / peak if dbytes else None}
     else:  # resident multi-step kernel (N <= 2048) / RBM-r' levels: latency-bound, no byte roofline
         roof = {"bound": "latency", "kernel": name, "achieved": None, "peak": None, "unit": "GB/s",
                 "frac": None, "traffic": traffic, "avg_launch_ms": avg_ms,
@@ -441,8 +464,11 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": cfg["dtype"], "data": "synthetic (Philox init from seed, BASELINE.json config)",
             "config": config_dict(args, cfg, world),
-            "hbm": {"useful_gbs_per_gpu": useful, "record_bytes": R,
-                    "note": "useful = particle-steps/s x 2 d s (state read+write once)"},
+            "hbm": {"useful_gbs_per_gpu": useful, "useful_frac": useful / peak, "record_bytes": R,
+                    "note": "useful = particle-steps/s x 2 d s (state read+write once), whole step"},
+            "timing": {"headline": "rbm_run graph replays, CUDA events on the library stream",
+                       "eager_ms_per_step": eager_ms / K,
+                       "per_kernel": "second window of K eager steps with library events around each kernel"},
             "layout": {"prefix_bits": s.layout[0], "passes": s.layout[1], "bucket_cap": s.layout[2]},
             "roofline": roof, "kernel_ms_per_step": shares, "clocks": clocks,
             "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu}

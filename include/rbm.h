@@ -129,7 +129,7 @@ typedef struct {
   uint32_t abi_version;  /* must be RBM_ABI_VERSION */
   uint32_t dtype;        /* rbm_dtype: arithmetic and storage precision of X */
   uint32_t d;            /* spatial dimension, 1..3 */
-  uint32_t p;            /* batch size, 2..64 (or p == n for n <= 4096) */
+  uint32_t p;            /* batch size, 2..64 (or p == n for n <= 2048) */
   uint64_t n;            /* number of particles N, 2..2^31 */
   uint32_t scheme;       /* rbm_scheme */
   uint32_t integrator;   /* rbm_integrator */
@@ -317,8 +317,11 @@ rbm_status rbm_part_phase2(rbm_ctx* ctx);
  * is the Brownian increment RBM step m uses (counter (i, blk, m, TAG_NOISE)),
  * so an RBM run and a direct run from the same X_0 and seed are
  * synchronously coupled.  Sphere constraint as in RBM (D:11).  cfg: model
- * fields only (p, scheme, world_size ignored); integrator must be
- * Euler-Maruyama; n <= 2^24.  Stateless: no context.
+ * fields only (p, scheme, world_size ignored); integrator Euler-Maruyama or
+ * Verlet (row f3: the full-force reference of PAPER.md:866-868; the start
+ * formula x_1 = x_0 + v_0 tau + F_0 tau^2/2 applies to the step with index
+ * cfg->step0 when state_form == 0, so consecutive runs compose); n <= 2^24.
+ * Stateless: no context.
  * ------------------------------------------------------------------------ */
 /* Bytes of device workspace (ping-pong copy of x + flags). */
 rbm_status rbm_direct_workspace_size(const rbm_config* cfg, size_t* bytes);

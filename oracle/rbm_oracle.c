@@ -191,10 +191,14 @@ static void grad_v(const oracle_cfg* c, const double* x, double* g) {
     g[k] = (c->potential == 1) ? c->vparam[0] * x[k] : 0.0;
 }
 
-/* difference z = x_i - x_j in the product's working precision (D:10) */
+/* difference z = x_i - x_j in IEEE double.  The one decision that follows
+ * the product's working precision is the bounded-confidence window test
+ * (reading D:10): in fp32 mode that kernel's z is fl32(x_i - x_j), so the
+ * strict |z| < r test sees the same value as an fp32 product.  Every other
+ * kernel takes the exact difference. */
 static void diff(const oracle_cfg* c, const double* xi, const double* xj, double* z) {
   for (uint32_t k = 0; k < c->d; ++k) {
-    if (c->fp32) z[k] = (double)((float)xi[k] - (float)xj[k]);
+    if (c->fp32 && c->kernel == K_BOUNDED_CONF) z[k] = (double)((float)xi[k] - (float)xj[k]);
     else z[k] = xi[k] - xj[k];
   }
 }

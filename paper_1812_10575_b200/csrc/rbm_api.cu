@@ -207,6 +207,7 @@ static rbm_status not_partitioned(rbm_ctx* c) {
 rbm_status rbm_step(rbm_ctx* c) {
   if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
   if (rbm_status e = not_partitioned(c)) return e;
+  if (c->step + 1 >= (1ull << 32)) return fail(c, RBM_ERR_INVALID_ARG, "step index would exceed 2^32");
   rbm_status s = enqueue_steps(c, c->stream, 1);
   c->P.dbg_order = nullptr;
   if (s) return s;
@@ -425,6 +426,7 @@ static rbm_status part_call(rbm_ctx* c, int phase) {
   if (!is_partitioned(c->cfg)) return fail(c, RBM_ERR_STATE, "not a partitioned context (world_size 1)");
   if (phase == 0 && c->partitioned) return fail(c, RBM_ERR_STATE, "prologue already done (state is partitioned)");
   if (phase > 0 && !c->partitioned) return fail(c, RBM_ERR_STATE, "run rbm_part_prologue and its exchange first");
+  if (phase == 2 && c->step + 1 >= (1ull << 32)) return fail(c, RBM_ERR_INVALID_ARG, "step index would exceed 2^32");
   c->P.verlet_start = c->verlet_start ? 1u : 0u;  // both phases compute batches of this step
   if (phase == 0) c->eng->part_prologue(*c, c->stream);
   else if (phase == 1) c->eng->part_phase1(*c, c->stream);
@@ -501,6 +503,9 @@ rbm_status rbm_direct_run(const rbm_config* cfg, void* x, uint64_t m0, uint64_t 
   if (!eng) return fail(nullptr, RBM_ERR_UNKNOWN_KERNEL, "no engine for kernel %u, d=%u", cfg->kernel, cfg->d);
   DevParams P;
   fill_params(*cfg, P);
+  // Verlet (row f3): the start formula applies to the step with index step0
+  // only, so run(a) followed by run(b) equals run(a + b)
+  if (m0 != cfg->step0) P.verlet_start = 0u;
   size_t b[2];
   direct_validate(cfg, b);
   unsigned char* w = reinterpret_cast<unsigned char*>(ws);

@@ -298,13 +298,86 @@ def test_capacity_fallback_parity(R, O):
     s.close()
 
 
-def test_replicas_differ_and_match_own_run(R):
+def test_replicas_differ(R):
+    """Ensemble members (replica in Philox word 3) are independent systems.
+    The multi-process ensemble invariant is tests/test_ensemble_gpu.py."""
     c = RI.c3_opinion(n=100_000)
     a = R.RBM(dict(c, replica=1))
     b = R.RBM(dict(c, replica=2))
     a.run(5)
     b.run(5)
     assert not np.array_equal(a.gather(host=True), b.gather(host=True))
+
+
+# ------------------------- p = 2 oversized-bucket path (forced small capacity)
+@pytest.mark.parametrize("case", ["em", "split_dyson", "split_coulomb"])
+def test_pair_kernel_oversized_bucket_parity(R, O, case):
+    """The p = 2 kernel's global-scratch path for a bucket above its smem
+    capacity (forced: capacity 300 against a mean bucket of ~1900): the
+    permutation bit-exactly and one step of EM and of the split pair flows."""
+    if case == "em":
+        c = cfg_of("coulomb_reg", 3, 2, 60_001, debug_bucket_cap=300, step0=4)
+    elif case == "split_dyson":
+        c = dict(RI.c1_dyson(n=60_000, integrator="split", seed=3), debug_bucket_cap=300, step0=4)
+    else:
+        c = dict(RI.c2_sphere(n=60_000, seed=3), integrator="split", debug_bucket_cap=300, step0=4)
+    s = R.RBM(c)
+    assert s.layout[2] == 300
+    x0 = s.gather(host=True)
+    assert np.array_equal(s.step_permutation(), O.permutation(c, 4))
+    assert E(s.gather(host=True), O.rbm1_step(c, x0, 4)) <= 1e-12
+    s.close()
+
+
+# ------------------ element-wise full-state parity on the 2-pass layout
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("p", [2, 8])
+def test_two_pass_full_state_one_step(R, O, dtype, p):
+    """C5 physics at N = 4,194,319 (B = 12 prefix bits: the non-partitioned
+    2-pass layout -- pass-2 split then the bucket step -- that the bench
+    times), every particle compared with the oracle after one step, at the
+    prologue step and at the steady-state step after it."""
+    c = dict(RI.c5_coulomb_reg(n=4_194_319, p=p), dtype=dtype)
+    s = R.RBM(c)
+    assert s.layout[:2] == (12, 2)
+    tol = 1e-12 if dtype == "f64" else 1e-4
+    for m in (0, 1):
+        x0 = s.gather(host=True).astype(np.float64)
+        s.step()
+        g = s.gather(host=True)
+        assert E(g, O.rbm1_step(c, x0, m)) <= tol, m
+    s.close()
+
+
+def test_two_pass_100_steps_fp64(R, O):
+    """100 steps in fp64 on the 2-pass layout (N = 2,200,013: B = 11), regularised
+    Coulomb (C5 physics), p = 2, against the oracle's 100-step run."""
+    c = dict(RI.c5_coulomb_reg(n=2_200_013, p=2), dtype="f64")
+    s = R.RBM(c)
+    assert s.layout[:2] == (11, 2)
+    x0 = s.gather(host=True)
+    s.run(100)
+    assert E(s.gather(host=True), O.run(c, x0, 0, 100)) <= 1e-9
+    s.close()
+
+
+def test_c2_configured_size(R, O):
+    """BASELINE.json configs[1] at its configured N = 10^6 (sphere Coulomb,
+    fp64, Euler + tangent projection): one step element-wise within 1e-12,
+    then 10 more steps with the per-particle error quantiles of SURVEY 8(c.11)
+    (near-collisions of the singular kernel amplify ulp differences)."""
+    c = RI.c2_sphere()
+    s = R.RBM(c)
+    x0 = s.gather(host=True)
+    s.step()
+    g = s.gather(host=True)
+    assert E(g, O.rbm1_step(c, x0, 0)) <= 1e-12
+    assert np.max(np.abs(np.linalg.norm(g, axis=1) - 1)) < 1e-14
+    s.run(10)
+    o = O.run(c, g, 1, 10)
+    err = np.max(np.abs(s.gather(host=True) - o), axis=1)
+    assert np.quantile(err, 0.99) <= 1e-9
+    s.close()
 
 
 # ----------------------------------------------- full-size sampled checks

@@ -97,18 +97,67 @@ def test_init_sphere_uniform(O):
     assert np.all(np.abs(x.mean(0)) < 0.02)
 
 
-def test_init_mixture_equal_weights(O):
-    """D:14: 5 equal-weight components, std 0.5, centres in [-4,4]^2."""
-    c = base(d=2, n=60000, init="mixture", iparam=[5, 0.5, -4.0, 4.0])
+def _mixture_parts(O, seed, n, std, K=5, lo=-4.0, hi=4.0):
+    """Centres and component labels of the mixture init (D:14): with the
+    component std at 1e-12 every point sits on its centre, and neither the
+    centres nor the labels depend on the std (their Philox blocks are
+    (k, {0,2}, 0, INIT_AUX) and (id, 1, 0, INIT_AUX))."""
+    c = base(d=2, n=n, init="mixture", iparam=[K, 1e-12, lo, hi], seed=seed)
     x = O.init(c)
-    # recover the centres by the nearest of 5 k-means-ish modes: use the
-    # fact that points lie within 6 std of some centre and count per centre
-    from scipy.cluster.vq import kmeans2
-    cent, lab = kmeans2(x, 5, seed=1, minit="++")
-    assert np.all(np.abs(cent) < 4.5)
-    counts = np.bincount(lab, minlength=5)
-    # equal weights only if the centres are separated; accept merged clusters
-    assert counts.sum() == 60000
+    _, lab = np.unique(np.round(x, 6), axis=0, return_inverse=True)
+    lab = lab.ravel()
+    cent = np.array([x[lab == k].mean(0) for k in range(lab.max() + 1)])  # within 1e-12 of the centres
+    return cent, lab, O.init(dict(c, iparam=[K, std, lo, hi]))
+
+
+def mixture_pin(O, seeds, n, std_claimed, std_used):
+    """Return the p-values of the mixture pins for data drawn with std_used
+    while the configuration claims std_claimed (they differ only in the
+    deliberately-wrong sensitivity check)."""
+    K = 5
+    cx, chi2, dof, resid = [], 0.0, 0, []
+    for sd in seeds:
+        cent, lab, x = _mixture_parts(O, sd, n, std_used, K=K)
+        assert cent.shape[0] == K                       # every component drawn
+        cx.append(cent)
+        cnt = np.bincount(lab, minlength=K)
+        chi2 += float(np.sum((cnt - n / K) ** 2 / (n / K)))  # Binomial(n, 1/K) each
+        dof += K - 1
+        resid.append((x - cent[lab]) / std_claimed)
+    cx = np.concatenate(cx)
+    r = np.concatenate(resid).ravel()
+    return {"centres_x": stats.kstest(cx[:, 0], "uniform", args=(-4.0, 8.0)).pvalue,
+            "centres_y": stats.kstest(cx[:, 1], "uniform", args=(-4.0, 8.0)).pvalue,
+            "weights": float(stats.chi2.sf(chi2, dof)),
+            "resid_normal": stats.kstest(r, "norm").pvalue,
+            "resid_std": float(r.std())}
+
+
+def test_init_mixture_pinned(O):
+    """D:14 (BASELINE.json C4: 5 isotropic Gaussians, std 0.5, centres U[-4,4]^2,
+    equal weights).  Over 200 seeds: the 1000 centres are U[-4,4] per axis (KS),
+    the per-component counts are Binomial(N, 1/5) (chi^2), and the offsets from
+    the own centre are N(0, 0.5^2) per coordinate (KS and std)."""
+    pv = mixture_pin(O, range(1, 201), 2000, 0.5, 0.5)
+    assert pv["centres_x"] > 1e-3 and pv["centres_y"] > 1e-3, pv
+    assert pv["weights"] > 1e-3, pv
+    assert pv["resid_normal"] > 1e-3 and abs(pv["resid_std"] - 1.0) < 0.01, pv
+
+
+def test_init_mixture_pin_rejects_wrong_std(O):
+    """The pin above fails on a deliberately wrong component std (1.0 drawn,
+    0.5 claimed): the residual test must reject it."""
+    pv = mixture_pin(O, range(1, 21), 2000, 0.5, 1.0)
+    assert pv["resid_normal"] < 1e-6 and abs(pv["resid_std"] - 2.0) < 0.05, pv
+
+
+def test_init_mixture_offsets_are_the_normal_draws(O):
+    """The offset of x_i from its centre is std * z_i with z_i the same
+    Brownian-free normal block as the NORMAL init (D:13/D:14):
+    mixture(std) - centre == NORMAL(0, std) for every particle."""
+    cent, lab, x = _mixture_parts(O, 7, 5000, 0.5)
+    z = O.init(base(d=2, n=5000, init="normal", iparam=[0.0, 0.5], seed=7))
+    assert np.max(np.abs((x - cent[lab]) - z)) < 1e-11
 
 
 # ------------------------------------------------------- random division (Alg. 1)

@@ -70,6 +70,19 @@ def test_verlet_direct_vs_oracle(R, O):
     assert E(d.gather(), O.direct_run(c, x0, 0, 25)) <= 1e-11
 
 
+def test_verlet_direct_chunked_runs_compose(R):
+    """run(10) then run(15) == run(25): the Verlet start formula
+    applies to the first step of the whole run only."""
+    c = verlet_cfg(700, p=2)
+    x0 = xv0(700, 3)
+    a = R.Direct(c, x0)
+    a.run(25)
+    b = R.Direct(c, x0)
+    b.run(10)
+    b.run(15)
+    assert np.array_equal(a.gather(), b.gather())
+
+
 def test_verlet_convergence_half_order(R):
     """Fig. second: N = 500, T = 1, reference tau = 2^-15 (full force), RBM-1 p=2."""
     n = 500
