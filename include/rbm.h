@@ -266,7 +266,7 @@ typedef struct {
   uint64_t ws_bytes;        /* workspace bytes (= rbm_workspace_size) */
   uint32_t world_size, rank;
   uint32_t nseg;            /* pass-1 segments (2^b1 digits x 2^segk cursors): u32 counts per rank in exchange C */
-  uint32_t narrays;         /* exchanged arrays: 2 + d (id u32, key u32, x_0 .. x_{d-1} dtype) */
+  uint32_t narrays;         /* exchanged arrays: 1 (the state records: id, [key,] x; elem_bytes[0] = 8, 16 or 32) */
   uint64_t chunk_elems;     /* elements per destination rank in each exchanged array */
   uint64_t send_off[5];     /* byte offsets in ws of the exchanged send arrays (a < narrays) */
   uint64_t recv_off[5];     /* byte offsets in ws of the exchanged receive arrays */

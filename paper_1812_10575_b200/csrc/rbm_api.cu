@@ -126,6 +126,7 @@ rbm_status init_impl(rbm_ctx* c, const rbm_config* cfg, void* wsp, size_t ws_byt
   P.segk = c->L.segk;
   P.segmask = (1u << c->L.segk) - 1u;
   P.halo = (is_partitioned(*cfg) && cfg->rank > 0) ? 1u : 0u;
+  P.side_key = (cfg->scheme == RBM_SCHEME_RBM1 && !rec_keyed(*cfg) && c->L.b2 > 0) ? 1u : 0u;
   if (std::getenv("RBM_PHASE_PROF")) {  // debug: per-phase cycles of the bucket kernel
     CU(cudaMalloc(&P.prof, 64 * 8));
     CU(cudaMemset(P.prof, 0, 64 * 8));
@@ -184,7 +185,7 @@ rbm_status rbm_set_state(rbm_ctx* c, const void* x, uint32_t where) {
   if (!x) return fail(c, RBM_ERR_INVALID_ARG, "x is NULL");
   const size_t bytes = c->n0 * c->cfg.d * elt_size(c->cfg);  // this rank's ids (all N on one GPU)
   if (where == RBM_MEM_HOST) {
-    void* scratch = c->xbuf[c->cur ^ 1];  // inactive buffer as staging
+    void* scratch = c->recbuf[c->cur ^ 1];  // inactive buffer as staging
     CU(cudaMemcpyAsync(scratch, x, bytes, cudaMemcpyHostToDevice, c->stream));
     c->eng->set_state(*c, scratch, c->stream);
     CU(cudaGetLastError());
@@ -280,7 +281,7 @@ rbm_status rbm_gather(rbm_ctx* c, uint64_t id_begin, uint64_t id_end, void* x_ou
   if (where == RBM_MEM_HOST && is_partitioned(c->cfg))
     return fail(c, RBM_ERR_UNSUPPORTED, "partitioned context: gather to device memory (each rank writes the ids it holds), then combine across ranks");
   if (where == RBM_MEM_HOST) {
-    void* scratch = c->xbuf[c->cur ^ 1];
+    void* scratch = c->recbuf[c->cur ^ 1];
     c->eng->gather(*c, id_begin, id_end, scratch, c->stream);
     CU(cudaGetLastError());
     if (bytes) CU(cudaMemcpyAsync(x_out, scratch, bytes, cudaMemcpyDeviceToHost, c->stream));
@@ -399,23 +400,16 @@ rbm_status rbm_part_info_get(const rbm_config* cfg, rbm_part_info* out) {
   out->world_size = (uint32_t)cfg->world_size;
   out->rank = (uint32_t)cfg->rank;
   out->nseg = tmp.L.nseg();
-  out->narrays = 2 + cfg->d;
+  out->narrays = 1;  // the state records (id, [key,] x), rec_bytes each
   out->chunk_elems = (uint64_t)(tmp.L.nseg() >> tmp.L.g) * tmp.L.cap1;
-  const uint32_t es = (uint32_t)elt_size(*cfg);
-  for (int b = 1; b <= 2; ++b) {
-    uint64_t* o = b == 1 ? out->send_off : out->recv_off;
-    o[0] = off(tmp.idbuf[b]);
-    o[1] = off(tmp.keybuf[b]);
-    for (uint32_t k = 0; k < cfg->d; ++k) o[2 + k] = off(tmp.xbuf[b]) + (uint64_t)k * tmp.xstride * es;
-  }
-  out->elem_bytes[0] = out->elem_bytes[1] = 4;
-  for (uint32_t k = 0; k < cfg->d; ++k) out->elem_bytes[2 + k] = es;
+  out->send_off[0] = off(tmp.recbuf[1]);
+  out->recv_off[0] = off(tmp.recbuf[2]);
+  out->elem_bytes[0] = rec_bytes(*cfg);
   out->counts_send_off = off(tmp.counts_send);
   out->counts_all_off = off(tmp.counts_all);
   out->halo_send_off = off(tmp.halo_send);
   out->halo_recv_off = off(tmp.halo_recv);
-  out->halo_bytes = cfg->dtype == RBM_F64 ? (cfg->d == 3 ? halo_bytes<double, 3>() : cfg->d == 2 ? halo_bytes<double, 2>() : halo_bytes<double, 1>())
-                                          : (cfg->d == 3 ? halo_bytes<float, 3>() : cfg->d == 2 ? halo_bytes<float, 2>() : halo_bytes<float, 1>());
+  out->halo_bytes = 16 + (uint64_t)HALO_MAX * rec_bytes(*cfg);
   out->id0 = tmp.id0;
   out->n0 = tmp.n0;
   return RBM_OK;

@@ -66,6 +66,7 @@ struct DevParams {
   uint32_t idbits;     // bits of an id (ceil log2 N)
   uint32_t lowbits;    // key bits below prefix+sub-digit: 32 - B - SB (lowbits+idbits <= 32)
   uint32_t* dbg_order; // if set: sorted position -> id of this step (test hook)
+  uint32_t side_key;   // the bucket step reads key_m from the side array pass 2 wrote (unkeyed records, 2-pass layouts)
   uint32_t group;      // lanes per batch in the fused step: pow2 >= p (<= 32), 0 = one thread per batch
   // partitioned single system (world_size G > 1): this rank
   // owns the key range whose top log2 G bits equal its rank.  The 2^b1 pass-1
@@ -104,6 +105,86 @@ constexpr uint32_t BIG_CAP = 65535; // u16 indices
 // bytes of one oversized-bucket scratch slot (256-B aligned stride)
 __host__ __device__ constexpr size_t big_slot_bytes(size_t rec_x_bytes) {
   return (((size_t)BIG_CAP * (18 + rec_x_bytes) + 64) + 255) & ~(size_t)255;
+}
+
+// ------------------------------------------------------------ record layout
+// The state is an array of fixed-size records (AoS) so that every move of a
+// particle is one vector access: word 0 = id, then (if it fits) word 1 = the
+// carried shuffle key of the step the record is partitioned for, then the d
+// coordinates.  RS = 8, 16 or 32 bytes:
+//   f32 d=1 {id, x} 8 B        f32 d=2 {id, key, x, y} 16 B   f32 d=3 {id, x, y, z} 16 B
+//   f64 d=1 {id, key, x} 16 B  f64 d=2 {id, key, x, y} 32 B   f64 d=3 {id, key, x, y, z} 32 B
+// Unkeyed layouts recompute key_m from the id (Philox) where it is needed;
+// pass 2 hands it to the bucket step in a side array.
+template <typename T, int D> struct RecL {
+  static constexpr int XB = D * (int)sizeof(T);
+  static constexpr int RS = (4 + XB <= 8) ? 8 : ((4 + XB <= 16) ? 16 : 32);
+  static constexpr bool KEYED = 8 + XB <= RS;
+  static constexpr int XW = KEYED ? 2 : (sizeof(T) == 8 ? 2 : 1);  // word offset of x[0]
+  static constexpr int NW = RS / 4;
+};
+template <typename T, int D> struct Rec {
+  uint32_t id, key;
+  T x[D];
+};
+__device__ __forceinline__ void from_w(float& x, const uint32_t* w) { x = __uint_as_float(w[0]); }
+__device__ __forceinline__ void from_w(double& x, const uint32_t* w) { x = __hiloint2double((int)w[1], (int)w[0]); }
+__device__ __forceinline__ void to_w(float x, uint32_t* w) { w[0] = __float_as_uint(x); }
+__device__ __forceinline__ void to_w(double x, uint32_t* w) {
+  w[0] = (uint32_t)__double2loint(x);
+  w[1] = (uint32_t)__double2hiint(x);
+}
+template <int NW>
+__device__ __forceinline__ void ld_words(const unsigned char* p, uint32_t (&w)[NW]) {
+  if (NW == 2) {
+    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    w[0] = v.x; w[NW > 1 ? 1 : 0] = v.y;
+  } else {
+#pragma unroll
+    for (int h = 0; h < NW / 4; ++h) {
+      const uint4 v = reinterpret_cast<const uint4*>(p)[h];
+      w[4 * h] = v.x; w[4 * h + 1] = v.y; w[4 * h + 2] = v.z; w[4 * h + 3] = v.w;
+    }
+  }
+}
+template <int NW>
+__device__ __forceinline__ void st_words(unsigned char* p, const uint32_t (&w)[NW]) {
+  if (NW == 2) {
+    *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[NW > 1 ? 1 : 0]);
+  } else {
+#pragma unroll
+    for (int h = 0; h < NW / 4; ++h)
+      reinterpret_cast<uint4*>(p)[h] = make_uint4(w[4 * h], w[4 * h + 1], w[4 * h + 2], w[4 * h + 3]);
+  }
+}
+// record i of the array at base (global or shared memory)
+template <typename T, int D>
+__device__ __forceinline__ Rec<T, D> ld_rec(const unsigned char* base, long long i) {
+  using L = RecL<T, D>;
+  uint32_t w[L::NW];
+  ld_words<L::NW>(base + i * L::RS, w);
+  Rec<T, D> r;
+  r.id = w[0];
+  r.key = L::KEYED ? w[1] : 0u;
+#pragma unroll
+  for (int c = 0; c < D; ++c) from_w(r.x[c], w + L::XW + c * (int)(sizeof(T) / 4));
+  return r;
+}
+template <typename T, int D>
+__device__ __forceinline__ void st_rec(unsigned char* base, long long i, const Rec<T, D>& r) {
+  using L = RecL<T, D>;
+  uint32_t w[L::NW];
+#pragma unroll
+  for (int k = 0; k < L::NW; ++k) w[k] = 0u;
+  w[0] = r.id;
+  if (L::KEYED) w[1] = r.key;
+#pragma unroll
+  for (int c = 0; c < D; ++c) to_w(r.x[c], w + L::XW + c * (int)(sizeof(T) / 4));
+  st_words<L::NW>(base + i * L::RS, w);
+}
+template <typename T, int D>
+__device__ __forceinline__ uint32_t ld_id(const unsigned char* base, long long i) {
+  return *reinterpret_cast<const uint32_t*>(base + i * RecL<T, D>::RS);
 }
 
 // ------------------------------------------------- TMA bulk copy + mbarrier

@@ -48,12 +48,16 @@ struct Layout {
   uint32_t cap2 = 0;     // gapped capacity of a final bucket
   uint64_t slots = 0;    // elements per state buffer: max(N, 2^b1 cap1, 2^B cap2)
 };
-constexpr int FUSED_BLOCK = 256;
-constexpr int PAIR_BLOCK = 512, PAIR_ITEMS = 5;  // p = 2 lean kernel: capacity <= 2560
-constexpr int PAIRS_BLOCK = 256, PAIRS_ITEMS = 6; // p = 2 lean kernel, small buckets: capacity <= 1536
-constexpr int PAIR3_BLOCK = 320, PAIR3_ITEMS = 8; // compact kernels, 3 CTAs x 10 warps per SM (64 regs): capacity <= 2560
-constexpr int PERSIST_BLOCK = 1024, PERSIST_ITEMS = 3;  // p = 2 persistent kernel: capacity <= 3072
-constexpr uint32_t FUSED_CAP_MAX = 4096;  // fast-path bucket capacity (u16 indices, smem)
+constexpr uint32_t FUSED_CAP_MAX = 4096;  // largest per-bucket smem capacity (u16 indices)
+
+// bytes of one state record and whether it carries the shuffle key (RecL)
+inline uint32_t rec_bytes(const rbm_config& c) {
+  const uint32_t xb = c.d * (c.dtype == RBM_F64 ? 8u : 4u);
+  return (4 + xb <= 8) ? 8u : ((4 + xb <= 16) ? 16u : 32u);
+}
+inline bool rec_keyed(const rbm_config& c) {
+  return 8 + c.d * (c.dtype == RBM_F64 ? 8u : 4u) <= rec_bytes(c);
+}
 
 struct EngineBase;
 
@@ -69,10 +73,9 @@ struct rbm_ctx {
   int device = 0;
   std::unique_ptr<EngineBase> eng;
   // workspace carve
-  void* xbuf[3] = {nullptr, nullptr, nullptr};
-  uint64_t xstride = 0;  // elements between coordinate arrays of one state buffer
-  uint32_t* idbuf[3] = {nullptr, nullptr, nullptr};
-  uint32_t* keybuf[3] = {nullptr, nullptr, nullptr};  // carried shuffle keys (fused pipeline)
+  unsigned char* recbuf[3] = {nullptr, nullptr, nullptr};  // state records (RS bytes each)
+  uint32_t* skey[3] = {nullptr, nullptr, nullptr};         // side keys (unkeyed records, 2-pass layouts)
+  uint64_t xstride = 0;  // record slots per state buffer (multiple of 64)
   // partitioned single system (world_size > 1): buffer 0 = this rank's final
   // buckets A (bucket -1 = halo), 1 = send pass-1 buckets B, 2 = received C
   uint64_t id0 = 0, n0 = 0;  // initial id range of this rank
@@ -88,7 +91,6 @@ struct rbm_ctx {
   uint32_t *prefix1 = nullptr, *tile_off = nullptr, *S = nullptr, *cur2 = nullptr;
   uint32_t* big_claim = nullptr;
   bool partitioned = false;  // state stored in the gapped buckets of step `step`
-  bool owner_split = false;  // pass 2 by the owner-computes splitter (writes S itself)
   uint64_t* step_dev = nullptr;
   unsigned long long* nonfinite = nullptr;
   uint32_t* capacity_err = nullptr;
@@ -235,10 +237,11 @@ inline Layout choose_layout(const rbm_config& c) {
   return L;
 }
 
-inline size_t bucket_smem(const rbm_config& c, uint32_t cap) {  // sorted-output kernel (B = 0)
-  const size_t es = elt_size(c);
-  return 2320 + (size_t)(cap + 8) * 4 + c.d * ((((size_t)(cap + 8) * es) + 15) & ~(size_t)15) +
-         (size_t)cap * 12 + (((size_t)cap * 2 + 15) & ~(size_t)15);
+// shared memory of the bucket kernel (bucket_smem_bytes in rbm_kernels.cuh)
+inline size_t bucket_smem(const rbm_config& c, const Layout& L) {
+  const size_t ncw = std::max<size_t>((1u << L.SB) / 2, 1u << L.b1);
+  return (2 * ncw + (1u << L.b1) + 64) * 4 + 16 + (size_t)(L.cap + 8) * rec_bytes(c) + (size_t)(L.cap + 8) * 4 +
+         (size_t)L.cap * 4 + (((size_t)L.cap * 2 + 15) & ~(size_t)15);
 }
 
 inline rbm_status validate(const rbm_config* cfg) {
@@ -308,8 +311,8 @@ inline rbm_status validate(const rbm_config* cfg) {
   if (k.scheme == RBM_SCHEME_RBM1 && L.B == 0 &&
       (k.dtype == RBM_F64 ? resident_smem_bytes<double, 3>(L.cap) : resident_smem_bytes<float, 3>(L.cap)) > 227 * 1024)
     return fail(c, RBM_ERR_INVALID_ARG, "n=%llu too large for the resident kernel", (unsigned long long)k.n);
-  if (k.scheme == RBM_SCHEME_RBM1 && bucket_smem(k, L.cap) > 227 * 1024)
-    return fail(c, RBM_ERR_INVALID_ARG, "bucket capacity %u needs %zu B of shared memory", L.cap, bucket_smem(k, L.cap));
+  if (k.scheme == RBM_SCHEME_RBM1 && L.B > 0 && bucket_smem(k, L) > 227 * 1024)
+    return fail(c, RBM_ERR_INVALID_ARG, "bucket capacity %u needs %zu B of shared memory", L.cap, bucket_smem(k, L));
   return RBM_OK;
 }
 
@@ -320,12 +323,13 @@ inline void carve(rbm_ctx& c, Workspace& ws) {
   const uint64_t n = k.n;
   const uint64_t slots = (k.scheme == RBM_SCHEME_RBM1) ? c.L.slots : n;
   const bool part = is_partitioned(k);
+  const size_t RS = rec_bytes(k);
+  const bool side = k.scheme == RBM_SCHEME_RBM1 && !rec_keyed(k) && c.L.b2 > 0;
   initial_ids(k, c.id0, c.n0);
-  c.xstride = (slots + 63) & ~63ull;  // per-coordinate stride: 256-B aligned SoA arrays (TMA)
+  c.xstride = (slots + 63) & ~63ull;  // 256-B aligned buffers (TMA)
   for (int b = 0; b < (part ? 3 : 2); ++b) {
-    c.idbuf[b] = ws.take<uint32_t>(c.xstride);
-    c.keybuf[b] = ws.take<uint32_t>(c.xstride);
-    c.xbuf[b] = ws.take<unsigned char>(c.xstride * k.d * es);
+    c.recbuf[b] = ws.take<unsigned char>(c.xstride * RS);
+    c.skey[b] = side ? ws.take<uint32_t>(c.xstride) : nullptr;
   }
   for (int q = 0; q < 2; ++q) c.cur1[q] = ws.take<uint32_t>((size_t)MAX_SEG * CUR1_STRIDE);
   c.prefix1 = ws.take<uint32_t>(1025);
@@ -335,15 +339,15 @@ inline void carve(rbm_ctx& c, Workspace& ws) {
   if (part) {
     c.counts_send = ws.take<uint32_t>(c.L.nseg());
     c.counts_all = ws.take<uint32_t>((size_t)k.world_size * c.L.nseg());
-    c.halo_send = ws.take<unsigned char>(halo_bytes<double, 3>());
-    c.halo_recv = ws.take<unsigned char>(halo_bytes<double, 3>());
+    c.halo_send = ws.take<unsigned char>(16 + (size_t)HALO_MAX * 32);
+    c.halo_recv = ws.take<unsigned char>(16 + (size_t)HALO_MAX * 32);
   }
   c.big_claim = ws.take<uint32_t>(NBIG);
   if (c.L.b2) c.cur2 = ws.take<uint32_t>((size_t)c.L.nbuckets * CUR2_STRIDE);
   c.step_dev = ws.take<uint64_t>(1);
   c.nonfinite = ws.take<unsigned long long>(1);
   c.capacity_err = ws.take<uint32_t>(1);
-  c.big_scratch = ws.take<unsigned char>(NBIG * big_slot_bytes(k.d * es));
+  c.big_scratch = ws.take<unsigned char>(NBIG * big_slot_bytes(RS));
   if (k.scheme != RBM_SCHEME_RBM1) {
     c.nbatch = (n + k.p - 1) / k.p;
     c.nslots = c.nbatch * k.p;
@@ -393,159 +397,44 @@ struct EngineBase {
 
 template <typename T, int D, int KK, int INTEG>
 struct Engine final : EngineBase {
-  static constexpr int SC_BLOCK = 256;
-  static constexpr int SC_ITEMS = (D * sizeof(T) <= 12) ? 16 : 8;
-  static constexpr int SC_TILE = SC_BLOCK * SC_ITEMS;
-  static constexpr int BK_BLOCK = 256;
-  size_t sc_smem = 0, bk_smem = 0;
-
-  State<T, D> st(rbm_ctx& c, int b) {
-    State<T, D> s;
-    s.id = c.idbuf[b];
-    s.key = c.keybuf[b];
-    T* x = reinterpret_cast<T*>(c.xbuf[b]);
-    for (int k = 0; k < 3; ++k) s.x[k] = x + (size_t)(k < D ? k : 0) * c.xstride;
-    return s;
-  }
-
-  size_t fu_smem = 0, pr_smem = 0, rs_smem = 0, ps_smem = 0, sp_smem = 0;
-  bool use_pair = false, use_persist = false, use_split = false, use_pair_small = false, use_pair3 = false;
-  bool use_group3 = false;
-  size_t prs_smem = 0, p3_smem = 0;
-  // pass-2 splitter configurations: one CTA of 1024 threads per SM with
-  // 4096-record tiles (default; measured fastest at C5), or
-  // RBM_SPLIT_CFG=small: two CTAs of 512 per SM with 2048-record tiles
-  static constexpr int SPLIT_BLOCK = 512;
-  static constexpr int SPLIT_TILE = (8 + D * sizeof(T) <= 20) ? 2048 : 1024;
-  static constexpr int SPLITB_BLOCK = 1024;
-  static constexpr int SPLITB_TILE = 2 * SPLIT_TILE;
-  bool split_big = false, use_owner = false;
-  size_t spb_smem = 0, ow_smem = 0;
-  static constexpr int OWNER_BLOCK = 512;
-  static constexpr int OWNER_TILE = (8 + D * sizeof(T) <= 20) ? 2048 : 1024;
+  using RL = RecL<T, D>;
+  static constexpr int PR_BLOCK = 256;
+  static constexpr int SPLIT_BLOCK = 1024;
+  static constexpr int MINB = (RL::RS <= 16) ? 3 : 2;  // CTAs per SM the bucket kernel is register-budgeted for
+  size_t pr_smem = 0, sp_smem = 0, bk_smem = 0, rs_smem = 0;
+  bool pair_mode = false;
   int num_sms = 148;
 
+  State<T, D> st(rbm_ctx& c, int b) { return State<T, D>{c.recbuf[b], c.skey[b]}; }
+
   rbm_status setup(rbm_ctx& c) override {
-    c.tile = SC_TILE;
-    sc_smem = (1024 + 1024 + 64) * 4 + (size_t)SC_TILE * (8 + 2 + D * sizeof(T));
-    bk_smem = bucket_smem(c.cfg, c.L.cap);
+    c.tile = split_tile<T, D>();
+    pr_smem = prologue_smem_bytes<T, D, PR_BLOCK>();
+    sp_smem = split_smem_bytes<T, D>();
+    bk_smem = bucket_smem_bytes<T, D>(c.L.cap, c.L.SB, c.L.b1);
     rs_smem = resident_smem_bytes<T, D>(c.L.cap);
-    fu_smem = fused_smem_bytes<T, D>(c.L.cap, c.L.SB);
-    pr_smem = pair_smem_bytes<T, D>(c.L.cap, c.L.SB);
-    use_pair = c.cfg.p == 2 && c.L.B > 0 && c.L.cap <= (uint32_t)(PAIR_BLOCK * PAIR_ITEMS) &&
-               pr_smem <= 227 * 1024;
-    ps_smem = persist_smem_bytes<T, D>(c.L.cap, c.L.SB);
-    prs_smem = pr_smem;
-    use_pair_small = use_pair && c.L.cap <= (uint32_t)(PAIRS_BLOCK * PAIRS_ITEMS);
-    p3_smem = pair3_smem_bytes<T, D>(c.L.cap, c.L.SB, c.L.b1);
-    {
-      // compact kernel, 3 CTAs per SM (default, measured 3% faster at C5);
-      // RBM_PAIR_KERNEL=lean: 2 CTAs of 512 threads per SM
-      const char* e = std::getenv("RBM_PAIR_KERNEL");
-      use_pair3 = use_pair && !use_pair_small && c.L.cap <= (uint32_t)(PAIR3_BLOCK * PAIR3_ITEMS) &&
-                  p3_smem + 2400 <= 74 * 1024 && !(e && (std::strcmp(e, "lean") == 0 || std::strcmp(e, "persist") == 0));
-    }
-    {
-      // 2 < p <= 32 (EM / Verlet): the compact 3-CTA kernel with lane-group
-      // batches; RBM_GROUP_KERNEL=fused: the general 2-CTA kernel
-      const char* e = std::getenv("RBM_GROUP_KERNEL");
-      use_group3 = c.cfg.p > 2 && c.cfg.p <= 32 && c.cfg.integrator != RBM_INTEG_SPLIT_EXACT_PAIR && c.L.B > 0 &&
-                   c.L.cap <= (uint32_t)(PAIR3_BLOCK * PAIR3_ITEMS) && p3_smem + 2400 <= 74 * 1024 &&
-                   !(e && std::strcmp(e, "fused") == 0);
-    }
-    {
-      // "persist": one CTA per SM looping over buckets with double-buffered
-      // TMA (measured slower than two one-bucket CTAs per SM; kept selectable)
-      const char* e = std::getenv("RBM_PAIR_KERNEL");
-      use_persist = use_pair && c.L.cap <= (uint32_t)(PERSIST_BLOCK * PERSIST_ITEMS) &&
-                    ps_smem <= 227 * 1024 && (e && std::strcmp(e, "persist") == 0);
-    }
-    sp_smem = split_smem_bytes<T, D, SPLIT_TILE>();
-    spb_smem = split_smem_bytes<T, D, SPLITB_TILE>();
-    ow_smem = owner_smem_bytes<T, D, OWNER_TILE>();
-    {
-      // pass 2: persistent tiles over all SMs with atomic run reservations
-      // (default); RBM_SPLIT_KERNEL=owner: one CTA owns each pass-1 bucket, no
-      // atomics (measured 3x slower at C5: one CTA cannot stream a bucket fast
-      // enough); =old: one CTA per tile
-      const char* e = std::getenv("RBM_SPLIT_KERNEL");
-      use_owner = ow_smem <= 227 * 1024 && (e && std::strcmp(e, "owner") == 0);
-    }
-    {
-      const char* e = std::getenv("RBM_SPLIT_CFG");  // "small": two CTAs per SM, half tiles
-      split_big = !(e && std::strcmp(e, "small") == 0) && spb_smem <= 227 * 1024;
-    }
-    {
-      const char* e = std::getenv("RBM_SPLIT_KERNEL");  // "old": one CTA per tile (comparison)
-      use_split = sp_smem <= 227 * 1024 && !(e && std::strcmp(e, "old") == 0);
-    }
-    c.owner_split = use_owner;
+    pair_mode = c.cfg.p == 2;
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, c.device);
     if (num_sms <= 0) num_sms = 148;
-    if (bk_smem != bucket_smem_bytes<T, D>(c.L.cap))
-      return fail(&c, RBM_ERR_STATE, "bucket smem size mismatch %zu vs %zu", bk_smem, bucket_smem_bytes<T, D>(c.L.cap));
     auto chk = [&](cudaError_t e, const char* what) -> rbm_status {
       if (e != cudaSuccess) return fail(&c, RBM_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
       return RBM_OK;
     };
     rbm_status s;
-    if ((s = chk(cudaFuncSetAttribute(scatter_kernel<T, D, 1, SC_BLOCK, SC_ITEMS>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc_smem),
-                 "smem attr scatter1"))) return s;
-    if ((s = chk(cudaFuncSetAttribute(scatter_kernel<T, D, 2, SC_BLOCK, SC_ITEMS>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc_smem),
-                 "smem attr scatter2"))) return s;
-    if ((s = chk(cudaFuncSetAttribute(bucket_step_kernel<T, D, KK, INTEG, BK_BLOCK>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bk_smem),
-                 "smem attr bucket"))) return s;
-    if (c.L.B == 0 && rs_smem <= 227 * 1024) {
-      if ((s = chk(cudaFuncSetAttribute(resident_kernel<T, D, KK, INTEG, BK_BLOCK>,
+    if ((s = chk(cudaFuncSetAttribute(prologue_kernel<T, D, PR_BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)pr_smem), "smem attr prologue"))) return s;
+    if ((s = chk(cudaFuncSetAttribute(split_kernel<T, D, SPLIT_BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sp_smem), "smem attr split"))) return s;
+    if (c.L.B > 0) {
+      if ((s = chk(pair_mode ? cudaFuncSetAttribute(bucket_kernel<T, D, KK, INTEG, MODE_PAIR, MINB>,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bk_smem)
+                             : cudaFuncSetAttribute(bucket_kernel<T, D, KK, INTEG, MODE_GROUP, MINB>,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bk_smem),
+                   "smem attr bucket"))) return s;
+    } else if (rs_smem <= 227 * 1024) {
+      if ((s = chk(cudaFuncSetAttribute(resident_kernel<T, D, KK, INTEG, 256>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem),
                    "smem attr resident"))) return s;
-    }
-    if (use_owner) {
-      if ((s = chk(cudaFuncSetAttribute(split_owner_kernel<T, D, OWNER_BLOCK, OWNER_TILE>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ow_smem),
-                   "smem attr owner"))) return s;
-    }
-    if (use_split) {
-      if ((s = chk(cudaFuncSetAttribute(split_persist_kernel<T, D, SPLIT_BLOCK, SPLIT_TILE>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp_smem),
-                   "smem attr split"))) return s;
-      if (split_big &&
-          (s = chk(cudaFuncSetAttribute(split_persist_kernel<T, D, SPLITB_BLOCK, SPLITB_TILE>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spb_smem),
-                   "smem attr split big"))) return s;
-    }
-    if (use_persist) {
-      if ((s = chk(cudaFuncSetAttribute(pair_persist_kernel<T, D, KK, INTEG, PERSIST_BLOCK, PERSIST_ITEMS>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps_smem),
-                   "smem attr persist"))) return s;
-    }
-    if (use_group3) {
-      if ((s = chk(cudaFuncSetAttribute(bucket_group3_kernel<T, D, KK, INTEG, PAIR3_BLOCK, PAIR3_ITEMS>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p3_smem),
-                   "smem attr group3"))) return s;
-    }
-    if (use_pair3) {
-      if ((s = chk(cudaFuncSetAttribute(bucket_pair3_kernel<T, D, KK, INTEG, PAIR3_BLOCK, PAIR3_ITEMS>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p3_smem),
-                   "smem attr pair3"))) return s;
-    }
-    if (use_pair_small) {
-      if ((s = chk(cudaFuncSetAttribute(bucket_pair_kernel<T, D, KK, INTEG, PAIRS_BLOCK, PAIRS_ITEMS>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prs_smem),
-                   "smem attr pair small"))) return s;
-    }
-    if (use_pair) {
-      if ((s = chk(cudaFuncSetAttribute(bucket_pair_kernel<T, D, KK, INTEG, PAIR_BLOCK, PAIR_ITEMS>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pr_smem),
-                   "smem attr pair"))) return s;
-    }
-    if (fu_smem <= 227 * 1024) {
-      if ((s = chk(cudaFuncSetAttribute(bucket_fused_kernel<T, D, KK, INTEG, FUSED_BLOCK>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fu_smem),
-                   "smem attr fused"))) return s;
     }
     return RBM_OK;
   }
@@ -554,9 +443,8 @@ struct Engine final : EngineBase {
   // halo) sits at physical slots [-cap2, 0)
   State<T, D> stA(rbm_ctx& c) {
     State<T, D> a = st(c, 0);
-    a.id += c.L.cap2;
-    a.key += c.L.cap2;
-    for (int k = 0; k < 3; ++k) a.x[k] += c.L.cap2;
+    a.rec += (size_t)c.L.cap2 * RL::RS;
+    if (a.key) a.key += c.L.cap2;
     return a;
   }
 
@@ -570,9 +458,8 @@ struct Engine final : EngineBase {
   State<T, D> st_peer(rbm_ctx& c, int b, uint32_t j) {
     State<T, D> a = st(c, b);
     const ptrdiff_t sh = c.peer_base[j] - c.ws_base;
-    a.id = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(a.id) + sh);
-    a.key = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(a.key) + sh);
-    for (int k = 0; k < 3; ++k) a.x[k] = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(a.x[k]) + sh);
+    a.rec += sh;
+    if (a.key) a.key = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(a.key) + sh);
     return a;
   }
   // partitioned: receive buffer holding the data of step m (fused: double-buffered)
@@ -640,56 +527,29 @@ struct Engine final : EngineBase {
     }
   }
 
-  // pass 2: pass-1 buckets/segments (capacity cap1, counts cnt1 strided) -> final
-  // buckets; then the exact global starts S (written by the owner kernel itself)
+  // pass 2: pass-1 buckets/segments (capacity cap1, counts cnt1 strided) -> final buckets
   void split2(rbm_ctx& c, cudaStream_t s, State<T, D> in, State<T, D> out, const uint32_t* cnt1) {
-    const Layout& L = c.L;
-    const uint32_t G = (uint32_t)c.cfg.world_size;
-    const uint32_t nlb = (1u << L.b1) / G;
-    if (use_owner) {
-      split_owner_kernel<T, D, OWNER_BLOCK, OWNER_TILE><<<nlb, OWNER_BLOCK, ow_smem, s>>>(
-          c.P, in, out, L.cap2, cnt1, L.cap1, G, c.prefix1, c.S);
-      return;
-    }
-    if (use_split && split_big) {  // (this path and the next need final_scan for S)
-      split_persist_kernel<T, D, SPLITB_BLOCK, SPLITB_TILE><<<(unsigned)num_sms, SPLITB_BLOCK, spb_smem, s>>>(
-          c.P, in, out, c.cur2, L.cap2, cnt1, c.tile_off, L.cap1);
-    } else if (use_split) {
-      split_persist_kernel<T, D, SPLIT_BLOCK, SPLIT_TILE><<<(unsigned)(2 * num_sms), SPLIT_BLOCK, sp_smem, s>>>(
-          c.P, in, out, c.cur2, L.cap2, cnt1, c.tile_off, L.cap1);
-    } else {  // tile table built with tile2() == SC_TILE
-      const uint32_t ns = L.nseg();
-      const unsigned tiles2 = (unsigned)(((uint64_t)ns * L.cap1 + SC_TILE - 1) / SC_TILE + ns);
-      scatter_kernel<T, D, 2, SC_BLOCK, SC_ITEMS><<<tiles2, SC_BLOCK, sc_smem, s>>>(
-          c.P, in, od(out), c.cur2, L.cap2, cnt1, c.tile_off, L.cap1, 0);
-    }
+    split_kernel<T, D, SPLIT_BLOCK><<<(unsigned)num_sms, SPLIT_BLOCK, sp_smem, s>>>(
+        c.P, in, out, c.cur2, c.L.cap2, cnt1, c.tile_off, c.L.cap1);
   }
 
-  uint32_t tile2() const {
-    return use_split ? (uint32_t)(split_big ? SPLITB_TILE : SPLIT_TILE) : (uint32_t)SC_TILE;
-  }
+  uint32_t tile2() const { return (uint32_t)split_tile<T, D>(); }
 
   void fused(rbm_ctx& c, cudaStream_t s, State<T, D> in, const OutDst<T, D>& out, uint32_t ocap,
              uint32_t* cur_next) {
-    if (use_persist)
-      pair_persist_kernel<T, D, KK, INTEG, PERSIST_BLOCK, PERSIST_ITEMS>
-          <<<std::min<uint32_t>(c.L.nbuckets, (uint32_t)num_sms), PERSIST_BLOCK, ps_smem, s>>>(
-              c.P, in, c.L.cap2, c.S, out, ocap, cur_next);
-    else if (use_group3)
-      bucket_group3_kernel<T, D, KK, INTEG, PAIR3_BLOCK, PAIR3_ITEMS>
-          <<<c.L.nbuckets, PAIR3_BLOCK, p3_smem, s>>>(c.P, in, c.L.cap2, c.S, out, ocap, cur_next);
-    else if (use_pair3)
-      bucket_pair3_kernel<T, D, KK, INTEG, PAIR3_BLOCK, PAIR3_ITEMS>
-          <<<c.L.nbuckets, PAIR3_BLOCK, p3_smem, s>>>(c.P, in, c.L.cap2, c.S, out, ocap, cur_next);
-    else if (use_pair_small)
-      bucket_pair_kernel<T, D, KK, INTEG, PAIRS_BLOCK, PAIRS_ITEMS>
-          <<<c.L.nbuckets, PAIRS_BLOCK, prs_smem, s>>>(c.P, in, c.L.cap2, c.S, out, ocap, cur_next);
-    else if (use_pair)
-      bucket_pair_kernel<T, D, KK, INTEG, PAIR_BLOCK, PAIR_ITEMS>
-          <<<c.L.nbuckets, PAIR_BLOCK, pr_smem, s>>>(c.P, in, c.L.cap2, c.S, out, ocap, cur_next);
+    if (pair_mode)
+      bucket_kernel<T, D, KK, INTEG, MODE_PAIR, MINB>
+          <<<c.L.nbuckets, BUCKET_BLOCK, bk_smem, s>>>(c.P, in, c.L.cap2, c.S, out, ocap, cur_next);
     else
-      bucket_fused_kernel<T, D, KK, INTEG, FUSED_BLOCK>
-          <<<c.L.nbuckets, FUSED_BLOCK, fu_smem, s>>>(c.P, in, c.L.cap2, c.S, out, ocap, cur_next);
+      bucket_kernel<T, D, KK, INTEG, MODE_GROUP, MINB>
+          <<<c.L.nbuckets, BUCKET_BLOCK, bk_smem, s>>>(c.P, in, c.L.cap2, c.S, out, ocap, cur_next);
+  }
+
+  void prologue(rbm_ctx& c, cudaStream_t s, State<T, D> src, const OutDst<T, D>& dst, uint32_t* cur,
+                uint32_t dcap, uint64_t nsrc) {
+    constexpr int TILE = prologue_tile<T, D>();
+    prologue_kernel<T, D, PR_BLOCK><<<(unsigned)((nsrc + TILE - 1) / TILE), PR_BLOCK, pr_smem, s>>>(
+        c.P, src, dst, cur, dcap, nsrc);
   }
 
   void step(rbm_ctx& c, cudaStream_t s) override {
@@ -707,9 +567,7 @@ struct Engine final : EngineBase {
     const uint32_t pcap = L.b2 ? L.cap1 : L.cap2;
     if (!c.partitioned) {  // prologue: any storage order -> gapped buckets of step m
       cudaMemsetAsync(c.cur1[q], 0, (size_t)L.nseg() * CUR1_STRIDE * 4, s);
-      scatter_kernel<T, D, 1, SC_BLOCK, SC_ITEMS>
-          <<<(unsigned)((n + SC_TILE - 1) / SC_TILE), SC_BLOCK, sc_smem, s>>>(
-              P, st(c, c.cur), od(st(c, c.cur ^ 1)), c.cur1[q], pcap, nullptr, nullptr, 0, n);
+      prologue(c, s, st(c, c.cur), od(st(c, c.cur ^ 1)), c.cur1[q], pcap, n);
       c.cur ^= 1;
       c.partitioned = true;
     }
@@ -728,13 +586,11 @@ struct Engine final : EngineBase {
       c.cur ^= 1;
     } else {
       // A holds the pass-1 buckets of step m: split them by the next b2 bits into B
-      if (!use_owner) cudaMemsetAsync(c.cur2, 0, (size_t)L.nbuckets * CUR2_STRIDE * 4, s);
+      cudaMemsetAsync(c.cur2, 0, (size_t)L.nbuckets * CUR2_STRIDE * 4, s);
       c.mark(s);
       split2(c, s, A, Bf, c.cur1[q]);
-      if (!use_owner) {
-        c.mark(s);
-        final_scan_kernel<<<1u << L.b1, 512, 0, s>>>(P, c.cur2, c.prefix1, c.S);
-      }
+      c.mark(s);
+      final_scan_kernel<<<1u << L.b1, 512, 0, s>>>(P, c.cur2, c.prefix1, c.S);
       c.mark(s);
       fused(c, s, Bf, od(A), L.cap1, c.cur1[q ^ 1]);
       c.mark(s);
@@ -763,8 +619,8 @@ struct Engine final : EngineBase {
   // N <= 2048: nsteps steps in one launch of one CTA (state in smem)
   void run_resident(rbm_ctx& c, cudaStream_t s, uint32_t nsteps) override {
     c.mark(s);
-    resident_kernel<T, D, KK, INTEG, BK_BLOCK><<<1, BK_BLOCK, rs_smem, s>>>(
-        c.P, st(c, c.cur), st(c, c.cur ^ 1), nsteps, c.step_dev);
+    resident_kernel<T, D, KK, INTEG, 256><<<1, 256, rs_smem, s>>>(c.P, st(c, c.cur), st(c, c.cur ^ 1), nsteps,
+                                                                  c.step_dev);
     c.cur ^= 1;
     c.mark(s);
   }
@@ -775,16 +631,13 @@ struct Engine final : EngineBase {
   // destination rank = top g bits), C = st(c, 2) (received: 2^b1 segments
   // v = source * 2^b1/G + local pass-1 bucket).  cur1[0] = send cursors,
   // cur1[1] = received segment counts (strided, for the tile table).
-  // Exchanges between the phases (caller, NCCL over NVLink via torch):
+  // Exchanges between the phases:
   //   prologue / phase2 -> all-gather counts_send into counts_all, and
-  //                        all-to-all of B's arrays into C (equal chunks)
+  //                        all-to-all of B's records into C (equal chunks)
   //   phase1            -> halo_send of rank r to halo_recv of rank r+1
   void part_prologue(rbm_ctx& c, cudaStream_t s) override {
-    const DevParams& P = c.P;
     cudaMemsetAsync(c.cur1[0], 0, (size_t)c.L.nseg() * CUR1_STRIDE * 4, s);
-    scatter_kernel<T, D, 1, SC_BLOCK, SC_ITEMS>
-        <<<(unsigned)((c.n0 + SC_TILE - 1) / SC_TILE), SC_BLOCK, sc_smem, s>>>(
-            P, st(c, 0), part_dst(c, c.step), c.cur1[0], c.L.cap1, nullptr, nullptr, 0, c.n0);
+    prologue(c, s, st(c, 0), part_dst(c, c.step), c.cur1[0], c.L.cap1, c.n0);
     pack_counts_kernel<<<1, 1024, 0, s>>>(c.cur1[0], c.L.nseg(), c.counts_send);
     c.partitioned = true;
   }
@@ -797,14 +650,12 @@ struct Engine final : EngineBase {
     c.mark(s);
     part_scan_kernel<<<1, 1024, 0, s>>>(P, c.counts_all, G, rank, c.cur1[1], c.prefix1, c.tile_off,
                                         tile2());
-    if (!use_owner) cudaMemsetAsync(c.cur2, 0, (size_t)L.nbuckets * CUR2_STRIDE * 4, s);
+    cudaMemsetAsync(c.cur2, 0, (size_t)L.nbuckets * CUR2_STRIDE * 4, s);
     cudaMemsetAsync(c.cur1[0], 0, (size_t)c.L.nseg() * CUR1_STRIDE * 4, s);
     c.mark(s);
     split2(c, s, st(c, recv_buf(c, c.step)), stA(c), c.cur1[1]);
-    if (!use_owner) {
-      c.mark(s);
-      final_scan_kernel<<<nb1 / G, 512, 0, s>>>(P, c.cur2, c.prefix1, c.S);
-    }
+    c.mark(s);
+    final_scan_kernel<<<nb1 / G, 512, 0, s>>>(P, c.cur2, c.prefix1, c.S);
     c.mark(s);
     fused(c, s, stA(c), part_dst(c, c.step + 1), L.cap1, c.cur1[0]);
     c.mark(s);
@@ -904,9 +755,10 @@ struct Engine final : EngineBase {
 template <typename T, int D>
 EngineBase* make_for_kernel(uint32_t kernel, uint32_t integ) {
   if (integ == RBM_INTEG_VERLET) {  // second order: 1-D particles stored as (x, v | x_prev)
-    if (D != 2) return nullptr;
-    if (kernel == RBM_K_SMOOTH_TEST) return new Engine<T, 2, KK_SMOOTH, 2>();
-    if (kernel == RBM_K_ZERO) return new Engine<T, 2, KK_ZERO, 2>();
+    if constexpr (D == 2) {
+      if (kernel == RBM_K_SMOOTH_TEST) return new Engine<T, 2, KK_SMOOTH, 2>();
+      if (kernel == RBM_K_ZERO) return new Engine<T, 2, KK_ZERO, 2>();
+    }
     return nullptr;
   }
   switch (kernel) {
@@ -916,13 +768,17 @@ EngineBase* make_for_kernel(uint32_t kernel, uint32_t integ) {
     case RBM_K_COULOMB_REG: return new Engine<T, D, KK_COULOMB_REG, 0>();
     case RBM_K_SMOOTH_TEST: return new Engine<T, D, KK_SMOOTH, 0>();
     case RBM_K_DYSON:
-      if (D == 1) return integ ? (EngineBase*)new Engine<T, 1, KK_DYSON, 1>() : new Engine<T, 1, KK_DYSON, 0>();
+      if constexpr (D == 1) return integ ? (EngineBase*)new Engine<T, 1, KK_DYSON, 1>() : new Engine<T, 1, KK_DYSON, 0>();
       return nullptr;
     case RBM_K_COULOMB:
-      if (D == 3) return integ ? (EngineBase*)new Engine<T, 3, KK_COULOMB, 1>() : new Engine<T, 3, KK_COULOMB, 0>();
+      if constexpr (D == 3) return integ ? (EngineBase*)new Engine<T, 3, KK_COULOMB, 1>() : new Engine<T, 3, KK_COULOMB, 0>();
       return nullptr;
     case RBM_K_LINEAR:
-      if (integ) return D == 1 ? (EngineBase*)new Engine<T, 1, KK_LINEAR, 1>() : nullptr;
+      if constexpr (D == 1) {
+        if (integ) return new Engine<T, 1, KK_LINEAR, 1>();
+      } else {
+        if (integ) return nullptr;
+      }
       return new Engine<T, D, KK_LINEAR, 0>();
   }
   return nullptr;
@@ -934,22 +790,13 @@ inline const char* const* kernel_names(const rbm_ctx& c, uint32_t* count) {
   if (c.cfg.scheme == RBM_SCHEME_RBMR_SEQ) { *count = 5; return rs; }
   static const char* const b0[] = {"resident_step"};
   static const char* const p1[] = {"tile_scan", "bucket_step", "straddle", "advance"};
-  static const char* const p2[] = {"tile_scan", "scatter_sub", "final_scan", "bucket_step",
-                                   "straddle", "advance"};
-  static const char* const p2o[] = {"tile_scan", "split_owner", "bucket_step", "straddle", "advance"};
-  static const char* const pto[] = {"part_scan", "split_owner", "bucket_step", "halo_extract",
-                                    "halo_place", "straddle", "pack_counts", "advance"};
-  static const char* const pt[] = {"part_scan", "scatter_sub", "final_scan", "bucket_step",
+  static const char* const p2[] = {"tile_scan", "split", "final_scan", "bucket_step", "straddle", "advance"};
+  static const char* const pt[] = {"part_scan", "split", "final_scan", "bucket_step",
                                    "halo_extract", "halo_place", "straddle", "pack_counts", "advance"};
-  if (is_partitioned(c.cfg)) {
-    if (c.owner_split) { *count = 8; return pto; }
-    *count = 9;
-    return pt;
-  }
+  if (is_partitioned(c.cfg)) { *count = 9; return pt; }
   if (c.cfg.scheme == RBM_SCHEME_RBMR) { *count = 3; return r; }
   if (c.L.B == 0) { *count = 1; return b0; }
   if (c.L.b2 == 0) { *count = 4; return p1; }
-  if (c.owner_split) { *count = 5; return p2o; }
   *count = 6;
   return p2;
 }

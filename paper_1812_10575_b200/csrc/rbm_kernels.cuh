@@ -3,28 +3,31 @@
 // RBM-1 step m (Alg. 1) as an MSD key partition into GAPPED
 // buckets (fixed capacity per bucket, cursors from zero: no histogram pass)
 // fused with an exact in-bucket sort and the batch update:
-//   prologue      scatter<1>: any storage order -> pass-1 buckets by the top b1
-//                 bits of key_m (keys computed from ids once, then carried)
+//   prologue      records in id order -> pass-1 buckets by the top b1 bits of
+//                 key_m (first step after init / set_state only)
 //   tile_scan     pass-1 counts -> prefix and tile table
-//   scatter<2>    pass-1 bucket d1 -> final buckets (d1, next b2 bits)
+//   split         pass-1 bucket d1 -> final buckets (d1, next b2 bits)
 //   final_scan    final counts -> exact global bucket starts S[0..2^B]
 //   bucket_step   per final bucket: exact in-smem sort by (key_m, id); every
 //                 batch inside the bucket does Eq. (2.2) + Euler-Maruyama (or
-//                 the exact pair flow); the updated records are partitioned
-//                 straight into the pass-1 buckets of step m+1 (key_{m+1})
+//                 the exact pair flow / Verlet); the updated records are
+//                 partitioned straight into the pass-1 buckets of step m+1
 //   straddle      batches that straddle two final buckets
 //   advance       m += 1
 // Batches are defined on global sorted positions S[b] + rank, so the step's
 // permutation is exactly "ids sorted by (key_m(id), id)" whatever the storage.
+// The state is an array of RS-byte records (RecL in rbm_device.cuh): every
+// move of a particle is one 8/16/32-byte vector access.
 #pragma once
 #include "rbm_device.cuh"
 
 namespace rbm {
 
+// State buffer: records, plus the side array of shuffle keys that pass 2
+// writes for the bucket step when the record has no room for the key.
 template <typename T, int D> struct State {
-  uint32_t* id;
-  uint32_t* key;  // shuffle key of the step the records are partitioned for (fused pipeline)
-  T* x[3];
+  unsigned char* rec;
+  uint32_t* key;
 };
 
 // Destination of the records a step writes into the pass-1 segments of the
@@ -41,7 +44,7 @@ template <typename T, int D> struct OutDst {
 
 template <typename T, int D>
 __device__ __forceinline__ void out_put(const OutDst<T, D>& o, uint32_t v, uint32_t cap, uint32_t slot,
-                                        uint32_t id, uint32_t key, const T (&x)[D]) {
+                                        const Rec<T, D>& r) {
   uint32_t w = 0;
   size_t g;
   if (o.fused) {
@@ -50,22 +53,8 @@ __device__ __forceinline__ void out_put(const OutDst<T, D>& o, uint32_t v, uint3
   } else {
     g = (size_t)v * cap + slot;
   }
-  const State<T, D>& d = o.st[w];
-  d.id[g] = id;
-  d.key[g] = key;
-#pragma unroll
-  for (int c = 0; c < D; ++c) d.x[c][g] = x[c];
+  st_rec<T, D>(o.st[w].rec, (long long)g, r);
 }
-
-// D coordinate arrays of a bucket in (shared or scratch) memory: base + c*stride.
-// One base pointer (not an array of pointers) keeps the address space visible
-// to the compiler, so shared-memory accesses stay LDS/STS.
-template <typename T> struct SX {
-  T* base;
-  uint32_t stride;
-  // 32-bit index: every window is < 2^32 elements (shared memory or a bucket's scratch)
-  __device__ __forceinline__ T& at(int c, uint32_t e) const { return base[(uint32_t)c * stride + e]; }
-};
 
 // ----------------------------------------------------------------- helpers
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
@@ -78,8 +67,8 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
   return v;
 }
 
-// exclusive scan of a[0..n) in shared memory by the whole block (n <= 4*BLOCK*k)
-// wsum: >= 32 uint32 of shared scratch. Returns the total.
+// exclusive scan of a[0..n) in shared memory by the whole block
+// wsum: >= 33 uint32 of shared scratch. Returns the total.
 template <int BLOCK>
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t* a, int n, uint32_t* wsum) {
   const int per = (n + BLOCK - 1) / BLOCK;
@@ -217,12 +206,9 @@ __device__ __forceinline__ uint32_t batch_end(uint32_t k, const DevParams& prm) 
   if (prm.rem == 1 && k + 1 == prm.nfull) return n;
   return min(k * prm.p + prm.p, n);
 }
-__device__ __forceinline__ uint32_t num_batches(const DevParams& prm) {
-  return prm.nfull + (prm.rem >= 2 ? 1u : 0u);
-}
 
 // ------------------------------------------------------------------- init
-// X_0 in fp64, rounded to T; state stored in id order.
+// X_0 in fp64, rounded to T; records stored in id order.
 template <typename T, int D>
 static __global__ void init_kernel(const __grid_constant__ DevParams P, State<T, D> st, uint64_t id0, uint64_t n, uint32_t kind,
                                    double a0, double a1, double a2, double a3) {
@@ -265,33 +251,40 @@ static __global__ void init_kernel(const __grid_constant__ DevParams P, State<T,
       const double u[4] = {u01d(w.x, w.y), u01d(w.z, w.w), u01d(v.x, v.y), u01d(v.z, v.w)};
       for (int c = 0; c < D; ++c) x[c] = a0 + (a1 - a0) * u[c];
     }
-    st.id[i] = id;
+    Rec<T, D> r;
+    r.id = id;
+    r.key = 0u;
 #pragma unroll
-    for (int c = 0; c < D; ++c) st.x[c][i] = (T)x[c];
+    for (int c = 0; c < D; ++c) r.x[c] = (T)x[c];
+    st_rec<T, D>(st.rec, (long long)i, r);
   }
 }
 
-// user state (id order, row-major N x D) -> SoA state in id order
+// user state (id order, row-major N x D) -> records in id order
 template <typename T, int D>
 static __global__ void set_state_kernel(uint64_t id0, uint64_t n, State<T, D> st, const T* __restrict__ xin) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    st.id[i] = (uint32_t)(id0 + i);
+    Rec<T, D> r;
+    r.id = (uint32_t)(id0 + i);
+    r.key = 0u;
 #pragma unroll
-    for (int c = 0; c < D; ++c) st.x[c][i] = xin[i * D + c];
+    for (int c = 0; c < D; ++c) r.x[c] = xin[i * D + c];
+    st_rec<T, D>(st.rec, (long long)i, r);
   }
 }
 
-// SoA state in storage order -> x_out (id order, row-major) for ids [i0, i1)
+// records in storage order -> x_out (id order, row-major) for ids [i0, i1)
 template <typename T, int D>
 static __global__ void gather_kernel(uint64_t n, State<T, D> st, uint64_t i0, uint64_t i1,
-                              T* __restrict__ out) {
+                                     T* __restrict__ out) {
   for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n;
        q += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t id = st.id[q];
+    const Rec<T, D> r = ld_rec<T, D>(st.rec, (long long)q);
+    const uint64_t id = r.id;
     if (id >= i0 && id < i1) {
 #pragma unroll
-      for (int c = 0; c < D; ++c) out[(id - i0) * D + c] = st.x[c][q];
+      for (int c = 0; c < D; ++c) out[(id - i0) * D + c] = r.x[c];
     }
   }
 }
@@ -335,10 +328,11 @@ static __global__ void gather_gapped_kernel(Gapped g, State<T, D> st, uint64_t i
        q += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t u = (uint32_t)(q / g.cap), s = (uint32_t)(q - (uint64_t)u * g.cap);
     if (s >= g.cnt[(size_t)u * g.cstride]) continue;
-    const uint64_t id = st.id[q];
+    const Rec<T, D> r = ld_rec<T, D>(st.rec, (long long)q);
+    const uint64_t id = r.id;
     if (id >= i0 && id < i1) {
 #pragma unroll
-      for (int c = 0; c < D; ++c) out[(id - i0) * D + c] = st.x[c][q];
+      for (int c = 0; c < D; ++c) out[(id - i0) * D + c] = r.x[c];
     }
   }
 }
@@ -432,75 +426,53 @@ __device__ __forceinline__ bool gapped_tile(const uint32_t* __restrict__ tile_of
   return true;
 }
 
-// --------------------------------------------------------------- scatter pass
-// LEVEL 1 (prologue): contiguous source [0, N); keys computed from ids
-//   (key_m); digit = top b1 bits (= top B bits for one-pass layouts).
-// LEVEL 2: source = pass-1 bucket u (tiles aligned to buckets), carried keys;
-//   digit = next b2 bits; destination bucket (u << b2 | digit).
-// Destination: gapped buckets of capacity dcap, cursors from zero; records are
-// staged in shared memory by digit so each reserved run is written coalesced.
-// Order inside a bucket is irrelevant: the bucket step sorts exactly.
-template <typename T, int D, int LEVEL, int BLOCK, int ITEMS>
-static __global__ void __launch_bounds__(BLOCK) scatter_kernel(const __grid_constant__ DevParams P, State<T, D> src,
-                                                               const __grid_constant__ OutDst<T, D> dst, uint32_t* cur,
-                                                               uint32_t dcap,
-                                                               const uint32_t* __restrict__ cnt1,
-                                                               const uint32_t* __restrict__ tile_off,
-                                                               uint32_t scap, uint64_t nsrc) {
-  constexpr int TILE = BLOCK * ITEMS;
+// ------------------------------------------------------------- prologue
+// Records in any storage order (contiguous [0, nsrc)) -> the gapped buckets
+// of step m by the top b1 bits of key_m (computed from the ids; carried in
+// keyed records).  Records are staged in shared memory by digit so that each
+// reserved run is written coalesced.  Order inside a bucket is irrelevant:
+// the bucket step sorts exactly.
+template <typename T, int D> __host__ __device__ constexpr int prologue_tile() {
+  return (65536 / RecL<T, D>::RS) < 4096 ? (65536 / RecL<T, D>::RS) : 4096;  // <= 64 KB of staged records
+}
+template <typename T, int D, int BLOCK> __host__ __device__ constexpr size_t prologue_smem_bytes() {
+  return (1024 + 1024 + 64) * 4 + (size_t)prologue_tile<T, D>() * (RecL<T, D>::RS + 2);
+}
+
+template <typename T, int D, int BLOCK>
+static __global__ void __launch_bounds__(BLOCK) prologue_kernel(const __grid_constant__ DevParams P, State<T, D> src,
+                                                                const __grid_constant__ OutDst<T, D> dst, uint32_t* cur,
+                                                                uint32_t dcap, uint64_t nsrc) {
+  constexpr int TILE = prologue_tile<T, D>();
+  constexpr int ITEMS = TILE / BLOCK;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw);  // 1024
   uint32_t* gbase = hist + 1024;                           // 1024
   uint32_t* wsum = gbase + 1024;                           // 64
-  uint32_t* st_id = wsum + 64;                             // TILE
-  uint32_t* st_key = st_id + TILE;                         // TILE
-  T* st_x = reinterpret_cast<T*>(st_key + TILE);           // D*TILE
-  uint16_t* st_dig = reinterpret_cast<uint16_t*>(st_x + D * TILE);  // TILE
+  unsigned char* stg = reinterpret_cast<unsigned char*>(wsum + 64);  // TILE records
+  uint16_t* st_dig = reinterpret_cast<uint16_t*>(stg + (size_t)TILE * RecL<T, D>::RS);
 
-  uint32_t lo, hi, u = 0, bits, sh, sbase;
-  if (LEVEL == 1) {
-    lo = blockIdx.x * TILE;
-    if (lo >= nsrc) return;
-    hi = (uint32_t)min((uint64_t)lo + TILE, nsrc);
-    bits = P.b1;
-    sh = 32u - P.b1;
-    sbase = 0;
-  } else {
-    if (!gapped_tile(tile_off, cnt1, (1u << P.b1) << P.segk, blockIdx.x, TILE, u, lo, hi)) return;
-    bits = P.b2;
-    sh = 32u - P.b1 - P.b2;
-    sbase = u * scap;
-  }
-  constexpr uint32_t CS = (LEVEL == 1) ? CUR1_STRIDE : CUR2_STRIDE;
-  const uint32_t nbins = 1u << bits, mask = nbins - 1;
-  // first destination bucket: final buckets of this rank's pass-1 bucket
-  // (segment u of the received pass-1 data on a partitioned system)
-  const uint32_t dbase0 = (LEVEL == 1) ? 0u : (((u >> P.segk) & P.nb1_loc_mask) << P.b2);
-  // destination bucket of digit dg: level 1 writes output segments
-  auto dest = [&](uint32_t dg) { return LEVEL == 1 ? out_seg(P, dg, blockIdx.x) : dbase0 + dg; };
+  const uint32_t lo = blockIdx.x * TILE;
+  if (lo >= nsrc) return;
+  const uint32_t hi = (uint32_t)min((uint64_t)lo + TILE, nsrc);
+  const uint32_t sh = 32u - P.b1, nbins = 1u << P.b1;
   for (uint32_t i = threadIdx.x; i < nbins; i += BLOCK) hist[i] = 0;
   __syncthreads();
-
   const uint32_t m = (uint32_t)*P.step;
   const uint32_t cnt = hi - lo;
-  uint32_t rid[ITEMS], rkey[ITEMS], rds[ITEMS];
-  T rx[ITEMS][D];
+  uint32_t rds[ITEMS];
+  Rec<T, D> rr[ITEMS];
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t e = k * BLOCK + threadIdx.x;
-    if (e < cnt) {
-      rid[k] = src.id[sbase + lo + e];
-      if (LEVEL != 1) rkey[k] = src.key[sbase + lo + e];
-#pragma unroll
-      for (int c = 0; c < D; ++c) rx[k][c] = src.x[c][sbase + lo + e];
-    }
+    if (e < cnt) rr[k] = ld_rec<T, D>(src.rec, (long long)(lo + e));
   }
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t e = k * BLOCK + threadIdx.x;
     if (e < cnt) {
-      if (LEVEL == 1) rkey[k] = shuffle_key(P, rid[k], m);  // prologue: keys from ids
-      const uint32_t dg = (rkey[k] >> sh) & mask;
+      rr[k].key = shuffle_key(P, rr[k].id, m);
+      const uint32_t dg = rr[k].key >> sh;
       rds[k] = (dg << 16) | atomicAdd(&hist[dg], 1u);
     }
   }
@@ -508,7 +480,7 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(const __grid_cons
   // reserve runs in the destination buckets, then local exclusive offsets
   for (uint32_t i = threadIdx.x; i < nbins; i += BLOCK) {
     const uint32_t h = hist[i];
-    gbase[i] = h ? atomicAdd(&cur[(size_t)dest(i) * CS], h) : 0u;
+    gbase[i] = h ? atomicAdd(&cur[(size_t)out_seg(P, i, blockIdx.x) * CUR1_STRIDE], h) : 0u;
   }
   block_excl_scan<BLOCK>(hist, nbins, wsum);  // hist -> local offsets
 #pragma unroll
@@ -517,11 +489,8 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(const __grid_cons
     if (e < cnt) {
       const uint32_t dg = rds[k] >> 16;
       const uint32_t s = hist[dg] + (rds[k] & 0xffffu);
-      st_id[s] = rid[k];
-      st_key[s] = rkey[k];
+      st_rec<T, D>(stg, s, rr[k]);
       st_dig[s] = (uint16_t)dg;
-#pragma unroll
-      for (int c = 0; c < D; ++c) st_x[c * TILE + s] = rx[k][c];
     }
   }
   __syncthreads();
@@ -532,56 +501,38 @@ static __global__ void __launch_bounds__(BLOCK) scatter_kernel(const __grid_cons
       atomicExch(P.capacity_err, 1u);
       continue;
     }
-    T xo[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c) xo[c] = st_x[c * TILE + j];
-    out_put<T, D>(dst, dest(dg), dcap, slot, st_id[j], st_key[j], xo);
+    out_put<T, D>(dst, out_seg(P, dg, blockIdx.x), dcap, slot, ld_rec<T, D>(stg, j));
   }
 }
 
 // ------------------------------------------- persistent pass-2 splitter
-// Same contract as scatter_kernel<LEVEL 2>: tiles of the pass-1 buckets
-// (segments) -> final buckets by the next b2 key bits.  One CTA per SM loops
-// over tiles with double-buffered TMA loads; the output permutation goes
-// through a u16 index (no staging copy): slot j of the tile's digit-ordered
-// output reads record inv[j] from the stage and the runs are written
-// coalesced into the reserved ranges of the final buckets.
-template <typename T, int D, int TILE> __host__ __device__ constexpr size_t split_stage_bytes() {
-  return ((size_t)TILE * (8 + D * sizeof(T)) + 127) & ~(size_t)127;
+// Tiles of the pass-1 buckets (segments) -> final buckets by the next b2 key
+// bits.  One 1024-thread CTA per SM loops over tiles with a two-stage TMA
+// ring (one bulk copy of TILE records per stage, L2 evict-first); each record
+// is ranked in its digit with a shared-memory atomic, the tile's output order
+// goes through a u16 index, and the runs are written coalesced (one vector
+// store per record) into the reserved ranges of the final buckets.  Unkeyed
+// records: key_m is computed from the id here and written to the side key
+// array for the bucket step.
+template <typename T, int D> __host__ __device__ constexpr int split_tile() {
+  return (65536 / RecL<T, D>::RS) < 4096 ? (65536 / RecL<T, D>::RS) : 4096;  // <= 64 KB per stage
 }
-template <typename T, int D, int TILE> __host__ __device__ constexpr size_t split_smem_bytes() {
-  return (3 * 1024 + 64) * 4 + 64 + 2 * split_stage_bytes<T, D, TILE>() + (size_t)TILE * 4 + (size_t)TILE * 2 +
-         (size_t)TILE * 2 + (size_t)(MAX_SEG_SPLIT + 1) * 4;  // + slot digits, tile table copy
+template <typename T, int D> __host__ __device__ constexpr size_t split_smem_bytes() {
+  return (3 * 1024 + 64) * 4 + 64 + 2 * (size_t)split_tile<T, D>() * RecL<T, D>::RS +
+         (size_t)split_tile<T, D>() * (4 + 4 + 2 + 2) + (size_t)(MAX_SEG_SPLIT + 1) * 4;
 }
 
 struct TileInfo { uint32_t u, lo, hi, pad; };
 
-template <typename T, int D, int TILE>
-__device__ __forceinline__ void split_stage_load(State<T, D> src, uint32_t base, uint32_t cnt,
-                                                 unsigned char* stg, uint64_t* bar, uint64_t pol) {
-  uint32_t* id_s = reinterpret_cast<uint32_t*>(stg);
-  uint32_t* key_s = id_s + TILE;
-  T* x_s = reinterpret_cast<T*>(key_s + TILE);
-  constexpr uint32_t AX = 16 / sizeof(T);
-  const uint32_t bytes_i = ((cnt + 3) & ~3u) * 4;
-  const uint32_t bytes_x = ((cnt + AX - 1) & ~(AX - 1)) * (uint32_t)sizeof(T);
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  mbar_expect_tx(bar, 2 * bytes_i + D * bytes_x);
-  if (cnt) {
-    bulk_g2s_stream(id_s, src.id + base, bytes_i, bar, pol);
-    bulk_g2s_stream(key_s, src.key + base, bytes_i, bar, pol);
-#pragma unroll
-    for (int c = 0; c < D; ++c) bulk_g2s_stream(x_s + (size_t)c * TILE, src.x[c] + base, bytes_x, bar, pol);
-  }
-}
-
-template <typename T, int D, int BLOCK, int TILE>
-static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) split_persist_kernel(const __grid_constant__ DevParams P,
-                                                                        State<T, D> src, State<T, D> dst,
-                                                                        uint32_t* cur, uint32_t dcap,
-                                                                        const uint32_t* __restrict__ cnt1,
-                                                                        const uint32_t* __restrict__ tile_off,
-                                                                        uint32_t scap) {
+template <typename T, int D, int BLOCK>
+static __global__ void __launch_bounds__(BLOCK, 1) split_kernel(const __grid_constant__ DevParams P,
+                                                                State<T, D> src, State<T, D> dst,
+                                                                uint32_t* cur, uint32_t dcap,
+                                                                const uint32_t* __restrict__ cnt1,
+                                                                const uint32_t* __restrict__ tile_off,
+                                                                uint32_t scap) {
+  using L = RecL<T, D>;
+  constexpr int TILE = split_tile<T, D>();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   RBM_PROF_BEGIN(P);
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw);  // 1024
@@ -591,15 +542,17 @@ static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) split_persist_kern
   uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);  // 2
   TileInfo* tinfo = reinterpret_cast<TileInfo*>(bar + 2);  // 2
   unsigned char* stg0 = smem_raw + (((3 * 1024 + 64) * 4 + 64 + 127) & ~127);
-  constexpr size_t SBY = split_stage_bytes<T, D, TILE>();
+  constexpr size_t SBY = (size_t)TILE * L::RS;
   uint32_t* rk = reinterpret_cast<uint32_t*>(stg0 + 2 * SBY);  // digit<<16 | rank, by element
-  uint16_t* inv = reinterpret_cast<uint16_t*>(rk + TILE);      // output slot -> element
+  uint32_t* kl = rk + TILE;                                    // key_m by element (unkeyed records)
+  uint16_t* inv = reinterpret_cast<uint16_t*>(kl + TILE);      // output slot -> element
   uint16_t* idg = inv + TILE;                                  // output slot -> digit
   uint32_t* toff = reinterpret_cast<uint32_t*>(idg + TILE);    // copy of tile_off (binary search in smem)
   const uint32_t nseg = (1u << P.b1) << P.segk;
   const uint32_t ntiles = tile_off[nseg];
   const uint32_t bits = P.b2, sh = 32u - P.b1 - P.b2, nbins = 1u << bits, mask = nbins - 1u;
   const uint32_t tid = threadIdx.x;
+  const uint32_t m = (uint32_t)*P.step;
   uint64_t pol = 0;
   for (uint32_t i = tid; i <= nseg; i += BLOCK) toff[i] = tile_off[i];
   __syncthreads();
@@ -607,7 +560,11 @@ static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) split_persist_kern
     TileInfo ti{0u, 0u, 0u, 0u};
     if (t < ntiles) gapped_tile(toff, cnt1, nseg, t, TILE, ti.u, ti.lo, ti.hi);
     tinfo[st] = ti;
-    split_stage_load<T, D, TILE>(src, ti.u * scap + ti.lo, ti.hi - ti.lo, stg0 + st * SBY, &bar[st], pol);
+    const uint32_t cnt = ti.hi - ti.lo;
+    const uint32_t bytes = (cnt * (uint32_t)L::RS + 15u) & ~15u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&bar[st], bytes);
+    if (cnt) bulk_g2s_stream(stg0 + st * SBY, src.rec + ((size_t)ti.u * scap + ti.lo) * L::RS, bytes, &bar[st], pol);
   };
   if (tid == 0) {
     pol = l2_evict_first_policy();
@@ -629,12 +586,16 @@ static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) split_persist_kern
     const uint32_t cnt = ti.hi - ti.lo;
     const uint32_t dbase0 = ((ti.u >> P.segk) & P.nb1_loc_mask) << P.b2;
     const unsigned char* stg = stg0 + s * SBY;
-    const uint32_t* id_s = reinterpret_cast<const uint32_t*>(stg);
-    const uint32_t* key_s = id_s + TILE;
-    const T* x_s = reinterpret_cast<const T*>(key_s + TILE);
     __syncthreads();
     for (uint32_t e = tid; e < cnt; e += BLOCK) {
-      const uint32_t dg = (key_s[e] >> sh) & mask;
+      uint32_t key;
+      if (L::KEYED) {
+        key = reinterpret_cast<const uint32_t*>(stg + (size_t)e * L::RS)[1];
+      } else {
+        key = shuffle_key(P, ld_id<T, D>(stg, e), m);
+        kl[e] = key;
+      }
+      const uint32_t dg = (key >> sh) & mask;
       rk[e] = (dg << 16) | atomicAdd(&hist[dg], 1u);
     }
     __syncthreads();
@@ -674,10 +635,10 @@ static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) split_persist_kern
         continue;
       }
       const size_t g = (size_t)(dbase0 + dg) * dcap + slot;
-      dst.id[g] = id_s[e];
-      dst.key[g] = key_s[e];
-#pragma unroll
-      for (int c = 0; c < D; ++c) dst.x[c][g] = x_s[(size_t)c * TILE + e];
+      uint32_t w[L::NW];
+      ld_words<L::NW>(stg + (size_t)e * L::RS, w);
+      st_words<L::NW>(dst.rec + g * L::RS, w);
+      if (!L::KEYED) dst.key[g] = kl[e];
     }
     __syncthreads();  // stage s, rk, inv free
     RBM_PROF(P, 21);
@@ -685,127 +646,23 @@ static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) split_persist_kern
   }
 }
 
-// ------------------------------------- owner-computes pass-2 splitter
-// One CTA owns one local pass-1 bucket u and streams all of its segments
-// (every source rank and salt) tile by tile through a double-buffered TMA
-// ring; final-bucket cursors live in shared memory (no global atomics), the
-// runs of consecutive tiles land back to back (the L2 merges their partial
-// sectors), and at the end the CTA writes the exact global starts S of its
-// 2^b2 final buckets (no separate final scan).
-template <typename T, int D, int TILE> __host__ __device__ constexpr size_t owner_smem_bytes() {
-  return (4 * 1024 + 64) * 4 + 64 + 2 * split_stage_bytes<T, D, TILE>() + (size_t)TILE * 4 + (size_t)TILE * 2;
-}
-
-template <typename T, int D, int BLOCK, int TILE>
-static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) split_owner_kernel(const __grid_constant__ DevParams P,
-                                                                                State<T, D> src, State<T, D> dst,
-                                                                                uint32_t dcap,
-                                                                                const uint32_t* __restrict__ cnt1,
-                                                                                uint32_t scap, uint32_t G,
-                                                                                const uint32_t* __restrict__ prefix1,
-                                                                                uint32_t* S) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw);  // 1024
-  uint32_t* off = hist + 1024;                             // 1024
-  uint32_t* lcur = off + 1024;                             // 1024: running count per final bucket
-  uint32_t* gtmp = lcur + 1024;                            // 1024
-  uint32_t* wsum = gtmp + 1024;                            // 64
-  uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);  // 2
-  TileInfo* tinfo = reinterpret_cast<TileInfo*>(bar + 2);  // 2
-  unsigned char* stg0 = smem_raw + (((4 * 1024 + 64) * 4 + 64 + 127) & ~127);
-  constexpr size_t SBY = split_stage_bytes<T, D, TILE>();
-  uint32_t* rk = reinterpret_cast<uint32_t*>(stg0 + 2 * SBY);
-  uint16_t* inv = reinterpret_cast<uint16_t*>(rk + TILE);
-  const uint32_t u = blockIdx.x;  // local pass-1 bucket
-  const uint32_t nseg = (1u << P.b1) << P.segk, nls = nseg / G, K = 1u << P.segk;
-  const uint32_t bits = P.b2, sh = 32u - P.b1 - P.b2, nbins = 1u << bits, mask = nbins - 1u;
-  const uint32_t dbase0 = u << P.b2;
-  const uint32_t nsrc = G * K;  // segments of this bucket: (source s, salt k)
-  const uint32_t tid = threadIdx.x;
-  const uint32_t nb4 = nbins < 4 ? 4u : nbins;
-  for (uint32_t i = tid; i < nb4; i += BLOCK) lcur[i] = 0;
-  // tile walk (thread 0 only): segment index w < nsrc, element offset lo
-  uint32_t wk = 0, wlo = 0;
-  uint64_t pol = 0;
-  auto next_tile = [&](TileInfo& ti) -> bool {  // thread 0
-    while (wk < nsrc) {
-      const uint32_t s = wk / K, k = wk - s * K;
-      const uint32_t v = s * nls + (u << P.segk) + k;
-      const uint32_t c = cnt1[(size_t)v * CUR1_STRIDE];
-      if (wlo < c) {
-        ti.u = v;
-        ti.lo = wlo;
-        ti.hi = min(wlo + (uint32_t)TILE, c);
-        wlo = ti.hi;
-        return true;
-      }
-      ++wk;
-      wlo = 0;
-    }
-    return false;
-  };
-  auto issue = [&](uint32_t st) {  // thread 0: always one arrival on bar[st]
-    TileInfo ti{0u, 0u, 0u, 0u};
-    next_tile(ti);
-    tinfo[st] = ti;
-    split_stage_load<T, D, TILE>(src, ti.u * scap + ti.lo, ti.hi - ti.lo, stg0 + st * SBY, &bar[st], pol);
-  };
-  if (tid == 0) {
-    pol = l2_evict_first_policy();
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    issue(0);
+// copy one record (NW words) from src_rec to segment v, slot `slot` of dst
+template <typename T, int D>
+__device__ __forceinline__ void out_copy(const OutDst<T, D>& o, uint32_t v, uint32_t cap, uint32_t slot,
+                                         const unsigned char* src_rec, uint32_t key) {
+  using L = RecL<T, D>;
+  uint32_t w = 0;
+  size_t g;
+  if (o.fused) {
+    w = v >> o.nls_log;
+    g = (size_t)((o.rank << o.nls_log) | (v & ((1u << o.nls_log) - 1u))) * cap + slot;
+  } else {
+    g = (size_t)v * cap + slot;
   }
-  __syncthreads();
-  uint32_t phase = 0;
-  for (uint32_t it = 0;; ++it) {
-    const uint32_t s = it & 1u;
-    if (tid == 0) issue(s ^ 1u);  // prefetch (an empty tile when the walk is done)
-    for (uint32_t i = tid; i < nb4; i += BLOCK) hist[i] = 0;
-    mbar_wait(&bar[s], (phase >> s) & 1u);
-    phase ^= 1u << s;
-    const TileInfo ti = tinfo[s];
-    const uint32_t cnt = ti.hi - ti.lo;
-    __syncthreads();
-    if (cnt == 0) break;  // uniform: the walk is exhausted
-    const unsigned char* stg = stg0 + s * SBY;
-    const uint32_t* id_s = reinterpret_cast<const uint32_t*>(stg);
-    const uint32_t* key_s = id_s + TILE;
-    const T* x_s = reinterpret_cast<const T*>(key_s + TILE);
-    for (uint32_t e = tid; e < cnt; e += BLOCK) {
-      const uint32_t dg = (key_s[e] >> sh) & mask;
-      rk[e] = (dg << 16) | atomicAdd(&hist[dg], 1u);
-    }
-    __syncthreads();
-    block_excl_scan4<BLOCK>(hist, off, nb4, wsum);
-    for (uint32_t e = tid; e < cnt; e += BLOCK) {
-      const uint32_t v = rk[e];
-      inv[off[v >> 16] + (v & 0xffffu)] = (uint16_t)e;
-    }
-    __syncthreads();
-    for (uint32_t j = tid; j < cnt; j += BLOCK) {
-      const uint32_t e = inv[j];
-      const uint32_t dg = rk[e] >> 16;
-      const uint32_t slot = lcur[dg] + (j - off[dg]);
-      if (slot >= dcap) {  // bucket capacity exceeded (probability ~1e-30): fail loudly
-        atomicExch(P.capacity_err, 1u);
-        continue;
-      }
-      const size_t g = (size_t)(dbase0 + dg) * dcap + slot;
-      dst.id[g] = id_s[e];
-      dst.key[g] = key_s[e];
-#pragma unroll
-      for (int c = 0; c < D; ++c) dst.x[c][g] = x_s[(size_t)c * TILE + e];
-    }
-    __syncthreads();  // stage s, rk, inv, off free
-    for (uint32_t i = tid; i < nb4; i += BLOCK) lcur[i] += hist[i];
-  }
-  // exact global starts of this bucket's final buckets
-  __syncthreads();
-  block_excl_scan4<BLOCK>(lcur, gtmp, nb4, wsum);
-  const uint32_t o = prefix1[u];
-  for (uint32_t i = tid; i < nbins; i += BLOCK) S[dbase0 + i] = o + gtmp[i];
-  if (u == 0 && tid == 0) S[P.nbuckets] = prefix1[gridDim.x];
+  uint32_t wd[L::NW];
+  ld_words<L::NW>(src_rec, wd);
+  if (L::KEYED) wd[1] = key;
+  st_words<L::NW>(o.st[w].rec + g * L::RS, wd);
 }
 
 // ------------------------------------------------------- bucket step pieces
@@ -813,14 +670,25 @@ template <typename T> __device__ __forceinline__ T batch_inv(const DevParams& P,
   return (sz == P.p) ? Prm<T>::invp(P) : T(1) / T(sz - 1);
 }
 
-template <typename T, int D, int KK, int INTEG>
+// coordinates of record e in a shared-memory (or scratch) record array
+template <typename T, int D> struct RX {
+  unsigned char* base;
+  __device__ __forceinline__ void get(uint32_t e, T (&x)[D]) const {
+    const Rec<T, D> r = ld_rec<T, D>(base, e);
+#pragma unroll
+    for (int c = 0; c < D; ++c) x[c] = r.x[c];
+  }
+};
+
+// member q of batch [l0, l1) (sorted positions, ord -> element): Eq. (2.2) +
+// Euler-Maruyama / Verlet, or the exact pair flow (INTEG 1, p = 2)
+template <typename T, int D, int KK, int INTEG, typename GetX>
 __device__ __forceinline__ void interior_update(const DevParams& P, uint32_t m, uint32_t q,
                                                 uint32_t l0, uint32_t l1, const uint16_t* ord,
-                                                SX<T> xs, uint32_t id, T (&xn)[D], int vstart = -1) {
+                                                GetX xs, uint32_t id, T (&xn)[D], int vstart = -1) {
   T xi[D];
   const uint32_t e = ord[q];
-#pragma unroll
-  for (int c = 0; c < D; ++c) xi[c] = xs.at(c, e);
+  xs.get(e, xi);
   T z[D];
 #pragma unroll
   for (int c = 0; c < D; ++c) z[c] = T(0);
@@ -830,40 +698,132 @@ __device__ __forceinline__ void interior_update(const DevParams& P, uint32_t m, 
 #pragma unroll
     for (int c = 0; c < D; ++c) f[c] = T(0);
     batch_force<T, D, KK, INTEG>(P, q - l0, l1 - l0, xi, [&](uint32_t j, T (&xj)[D]) {
-      const uint32_t e2 = ord[l0 + j];
-#pragma unroll
-      for (int c = 0; c < D; ++c) xj[c] = xs.at(c, e2);
+      xs.get(ord[l0 + j], xj);
     }, f);
     const T inv = batch_inv<T>(P, l1 - l0);
 #pragma unroll
     for (int c = 0; c < D; ++c) f[c] *= inv;
     member_update<T, D, INTEG>(xi, f, z, xn, P, vstart < 0 ? P.verlet_start != 0 : vstart != 0);
   } else {
-    const uint32_t ea = ord[l0], eb = ord[l0 + 1];
     T xa[D], xb[D], y[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c) { xa[c] = xs.at(c, ea); xb[c] = xs.at(c, eb); }
+    xs.get(ord[l0], xa);
+    xs.get(ord[l0 + 1], xb);
     pair_flow<T, D, KK>(xa, xb, q == l0, y, P);
     split_finish<T, D>(y, z, xn, P, true);
   }
 }
 
-// Sort the loaded bucket by (key, id) and step every interior batch; bucket
-// element at sorted position q (global position s0+q) is written to dst[obase+q].
-//   id_l, xs : bucket records in load order (n of them)
-//   key_l    : n u32 scratch;  ks : n u64 scratch (16-B aligned);  ord : n u16
+// One batch [l0, l1) handled by one thread (a remainder batch larger than the
+// lane group, or p > 32): every member from the old positions, then written
+// back in place; ta[e] = key_{m+1}, tb[e] = rank in its output digit.
+template <typename T, int D, int KK, int INTEG>
+__device__ __noinline__ void serial_batch(const DevParams& P, uint32_t m, uint32_t l0, uint32_t l1,
+                                          const uint16_t* ord, unsigned char* rs, uint32_t* ta,
+                                          uint16_t* tb, uint32_t* ocnt, uint32_t osh) {
+  T xn[65][D];
+  const RX<T, D> xs{rs};
+  for (uint32_t q = l0; q < l1; ++q) {
+    T out[D];
+    interior_update<T, D, KK, INTEG>(P, m, q, l0, l1, ord, xs, ld_id<T, D>(rs, ord[q]), out);
+#pragma unroll
+    for (int c = 0; c < D; ++c) xn[q - l0][c] = out[c];
+  }
+  for (uint32_t q = l0; q < l1; ++q) {
+    const uint32_t e = ord[q];
+    Rec<T, D> r = ld_rec<T, D>(rs, e);
+    check_finite<T, D>(xn[q - l0], P, r.id, m);
+    const uint32_t kn = shuffle_key(P, r.id, m + 1);
+#pragma unroll
+    for (int c = 0; c < D; ++c) r.x[c] = xn[q - l0][c];
+    r.key = kn;
+    st_rec<T, D>(rs, e, r);
+    ta[e] = kn;
+    tb[e] = (uint16_t)atomicAdd(&ocnt[kn >> osh], 1u);
+  }
+}
+
+template <typename T, int D, int KK, int INTEG>
+__device__ __forceinline__ void pair_update(const DevParams& P, uint32_t m, const T (&x0)[D],
+                                            const T (&x1)[D], uint32_t id0, uint32_t id1,
+                                            T (&y0)[D], T (&y1)[D]) {
+  T z0[D], z1[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) { z0[c] = T(0); z1[c] = T(0); }
+  if (P.has_noise) {
+    Normals<T, D>::get(P, id0, m, TAG_NOISE, z0);
+    Normals<T, D>::get(P, id1, m, TAG_NOISE, z1);
+  }
+  if (INTEG == 0) {
+    T zz[D], f0[D], f1[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) zz[c] = x0[c] - x1[c];
+    const T sc = kernel_scale<T, D, KK>(zz, P);  // 1/(p-1) = 1
+#pragma unroll
+    for (int c = 0; c < D; ++c) { f0[c] = sc * zz[c]; f1[c] = -f0[c]; }
+    em_update<T, D>(x0, f0, z0, y0, P, true);
+    em_update<T, D>(x1, f1, z1, y1, P, true);
+  } else if (INTEG == 2) {  // Verlet: 1-D force on the positions; the partner gets -f
+    T f0[D], f1[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) { f0[c] = T(0); f1[c] = T(0); }
+    add_force1<T, D, KK>(x0, x1, f0, P);
+    f1[0] = -f0[0];
+    verlet_update<T, D>(x0, f0, y0, P, P.verlet_start != 0);
+    verlet_update<T, D>(x1, f1, y1, P, P.verlet_start != 0);
+  } else {
+    T a[D], b[D];
+    pair_flow<T, D, KK>(x0, x1, true, a, P);
+    pair_flow<T, D, KK>(x0, x1, false, b, P);
+    split_finish<T, D>(a, z0, y0, P, true);
+    split_finish<T, D>(b, z1, y1, P, true);
+  }
+}
+
+// Oversized bucket (never expected at the automatic capacity; forced in
+// tests): the same sort and update on one of NBIG global-memory scratch slots,
+// claimed from a small pool and released at the end (holders are resident, so
+// waiters always make progress).  All records are written back to the
+// bucket's own gapped range in sorted order (straddlers unchanged, for the
+// straddle kernel); the interior ones are then appended one by one to the
+// step-(m+1) buckets.
 template <typename T, int D, int KK, int INTEG, int BLOCK>
-__device__ __forceinline__ void bucket_compute(const DevParams& P, State<T, D> dst, uint32_t s0,
-                                               uint32_t obase, uint32_t n, const uint32_t* id_l,
-                                               SX<T> xs,
-                                               uint32_t* key_l, unsigned long long* ks,
-                                               uint16_t* ord, uint32_t* cnt, uint32_t* off,
-                                               uint32_t* wsum) {
-  const uint32_t m = (uint32_t)*P.step;
-  // 1. keys (Philox), counting sort by the next 8 key bits below the B-bit prefix
+__device__ __noinline__ void big_bucket(const DevParams& P, State<T, D> src, const OutDst<T, D>& dst,
+                                        uint32_t* cur_next, uint32_t s0, uint32_t sb, uint32_t n,
+                                        uint32_t m, uint32_t dcap, uint32_t* cnt, uint32_t* off,
+                                        uint32_t* wsum) {
+  using L = RecL<T, D>;
+  __shared__ uint32_t slot;
+  if (threadIdx.x == 0) {
+    slot = 0xffffffffu;
+    if (n <= BIG_CAP) {
+      for (;;) {
+        for (uint32_t s = 0; s < (uint32_t)NBIG && slot == 0xffffffffu; ++s)
+          if (atomicCAS(&P.big_claim[s], 0u, 1u) == 0u) slot = s;
+        if (slot != 0xffffffffu) break;
+        __nanosleep(500);
+      }
+    }
+  }
+  __syncthreads();
+  if (slot == 0xffffffffu) {
+    if (threadIdx.x == 0) atomicExch(P.capacity_err, 1u);
+    return;
+  }
+  unsigned char* base = P.big_scratch + slot * big_slot_bytes(L::RS);
+  unsigned long long* ks = reinterpret_cast<unsigned long long*>(base);
+  unsigned char* rs = reinterpret_cast<unsigned char*>(ks + BIG_CAP + 1);
+  uint32_t* key_l = reinterpret_cast<uint32_t*>(rs + (size_t)BIG_CAP * L::RS);
+  uint16_t* ord = reinterpret_cast<uint16_t*>(key_l + BIG_CAP);
+  const RX<T, D> xs{rs};
+  for (uint32_t i = threadIdx.x; i < 256; i += BLOCK) cnt[i] = 0;
+  __syncthreads();
+  // keys (carried, side array or Philox); counting sort by the 8 key bits
+  // below the B-bit prefix
   const uint32_t sh = (P.B <= 24u) ? (24u - P.B) : 0u;
   for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
-    const uint32_t key = shuffle_key(P, id_l[e], m);
+    const Rec<T, D> r = ld_rec<T, D>(src.rec, (long long)sb + e);
+    st_rec<T, D>(rs, e, r);
+    const uint32_t key = L::KEYED ? r.key : (P.side_key ? src.key[sb + e] : shuffle_key(P, r.id, m));
     key_l[e] = key;
     ord[e] = (uint16_t)atomicAdd(&cnt[(key >> sh) & 255u], 1u);
   }
@@ -871,16 +831,15 @@ __device__ __forceinline__ void bucket_compute(const DevParams& P, State<T, D> d
   for (uint32_t i = threadIdx.x; i < 256; i += BLOCK) off[i] = cnt[i];
   __syncthreads();
   block_excl_scan<BLOCK>(off, 256, wsum);
-  // 2. composite (key, id) keys grouped by sub-digit, contiguous per sub-bucket
   for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
     const uint32_t key = key_l[e];
-    ks[off[(key >> sh) & 255u] + ord[e]] = ((unsigned long long)key << 32) | id_l[e];
+    ks[off[(key >> sh) & 255u] + ord[e]] = ((unsigned long long)key << 32) | ld_id<T, D>(rs, e);
   }
   __syncthreads();
-  // 3. exact rank = sub-bucket offset + #smaller composites in the sub-bucket
+  // exact rank = sub-bucket offset + #smaller (key, id) composites in the sub-bucket
   for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
     const uint32_t key = key_l[e];
-    const unsigned long long mine = ((unsigned long long)key << 32) | id_l[e];
+    const unsigned long long mine = ((unsigned long long)key << 32) | ld_id<T, D>(rs, e);
     const uint32_t sd = (key >> sh) & 255u;
     const uint32_t a = off[sd], c = cnt[sd];
     uint32_t r = a;
@@ -888,125 +847,375 @@ __device__ __forceinline__ void bucket_compute(const DevParams& P, State<T, D> d
     ord[r] = (uint16_t)e;
   }
   __syncthreads();
-  // 4. batches inside [s0, s0+n): Eq. (2.2) + update; straddling ones copied through
+  // batches inside [s0, s0+n): Eq. (2.2) + update from the scratch copy,
+  // written to the own gapped range in sorted order; straddlers copied through
   for (uint32_t q = threadIdx.x; q < n; q += BLOCK) {
     const uint32_t P0 = s0 + q;
     uint32_t b0, b1;
     batch_range(P0, P, b0, b1);
-    const uint32_t e = ord[q];
-    const uint32_t id = id_l[e];
-    T xn[D];
+    Rec<T, D> r = ld_rec<T, D>(rs, ord[q]);
     if (b0 >= s0 && b1 <= s0 + n) {
-      interior_update<T, D, KK, INTEG>(P, m, q, b0 - s0, b1 - s0, ord, xs, id, xn);
-      check_finite<T, D>(xn, P, id, m);
-    } else {
+      T xn[D];
+      interior_update<T, D, KK, INTEG>(P, m, q, b0 - s0, b1 - s0, ord, xs, r.id, xn);
+      check_finite<T, D>(xn, P, r.id, m);
 #pragma unroll
-      for (int c = 0; c < D; ++c) xn[c] = xs.at(c, e);
+      for (int c = 0; c < D; ++c) r.x[c] = xn[c];
     }
-    dst.id[obase + q] = id;
-#pragma unroll
-    for (int c = 0; c < D; ++c) dst.x[c][obase + q] = xn[c];
-    if (P.dbg_order) P.dbg_order[P0] = id;
+    st_rec<T, D>(src.rec, (long long)sb + q, r);
+    if (P.dbg_order) P.dbg_order[P0] = r.id;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicExch(&P.big_claim[slot], 0u);
+  }
+  const uint32_t osh = 32u - P.b1;
+  for (uint32_t q = threadIdx.x; q < n; q += BLOCK) {
+    uint32_t b0, b1;
+    batch_range(s0 + q, P, b0, b1);
+    if (b0 >= s0 && b1 <= s0 + n) {
+      Rec<T, D> r = ld_rec<T, D>(src.rec, (long long)sb + q);
+      r.key = shuffle_key(P, r.id, m + 1);
+      const uint32_t v = out_seg(P, r.key >> osh, blockIdx.x);
+      const uint32_t s = atomicAdd(&cur_next[(size_t)v * CUR1_STRIDE], 1u);
+      if (s >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
+      out_put<T, D>(dst, v, dcap, s, r);
+    }
   }
 }
 
-// shared-memory bytes of the bucket kernel for capacity `cap`
-template <typename T, int D> __host__ __device__ constexpr size_t bucket_smem_bytes(uint32_t cap) {
-  return 2304 + 16                                  // cnt, off, wsum; mbarrier
-         + (size_t)(cap + 8) * 4                    // ids (TMA window)
-         + (size_t)D * (((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15)  // x (TMA windows)
-         + (size_t)cap * 8                          // composite keys
-         + (size_t)cap * 4                          // keys
-         + (((size_t)cap * 2 + 15) & ~(size_t)15);  // ord
+// ------------------------------------------------------------ bucket step
+// One CTA per final bucket b of step m (gapped, capacity scap; global start
+// S[b]):
+//   (1) TMA bulk load of the bucket's records (and side keys) into smem;
+//   (2) exact sort by (key_m, id): counting sort on SB sub-digit bits (packed
+//       u16 counters) + rank among 32-bit (low key bits, id) composites;
+//   (3) Eq. (2.2) + update of every batch inside the bucket, in place:
+//       MODE_PAIR (p = 2): one thread per pair; MODE_GROUP: one lane group
+//       of G = pow2 >= p lanes per batch (p <= 32; shuffles, each pair once
+//       in the canonical rotation order), one thread per larger batch;
+//       each member's key_{m+1} and its rank in its output digit;
+//   (4) runs reserved in the step-(m+1) pass-1 buckets, staged through a u16
+//       index, written coalesced (one vector store per record).
+// Members of batches that straddle the bucket's ends are written unchanged to
+// their sorted places in the own gapped range (the straddle kernel steps them).
+constexpr int MODE_PAIR = 0, MODE_GROUP = 1;
+constexpr int BUCKET_BLOCK = 320, BUCKET_ITEMS = 8;  // 10 warps, capacity <= 2560 in registers
+
+template <typename T, int D> __host__ __device__ constexpr size_t bucket_smem_bytes(uint32_t cap, uint32_t SB,
+                                                                                   uint32_t b1) {
+  return (size_t)(2 * (((1u << SB) / 2 > (1u << b1)) ? (1u << SB) / 2 : (1u << b1)) + (1u << b1) + 64) * 4 + 16
+         + (size_t)(cap + 8) * RecL<T, D>::RS              // records (TMA window, updated in place)
+         + (size_t)(cap + 8) * 4                           // side keys (TMA window) -> key_{m+1}
+         + (size_t)cap * 4                                 // composites -> tb | inv (u16 each)
+         + (((size_t)cap * 2 + 15) & ~(size_t)15);         // ord (u16)
 }
 
-template <typename T, int D, int KK, int INTEG, int BLOCK>
-static __global__ void __launch_bounds__(BLOCK) bucket_step_kernel(const __grid_constant__ DevParams P, State<T, D> src,
-                                                                   State<T, D> dst,
-                                                                   const uint32_t* __restrict__ S) {
+template <typename T, int D, int KK, int INTEG, int MODE, int MINB>
+static __global__ void __launch_bounds__(BUCKET_BLOCK, MINB) bucket_kernel(const __grid_constant__ DevParams P, State<T, D> src,
+                                                                           uint32_t scap,
+                                                                           const uint32_t* __restrict__ S,
+                                                                           const __grid_constant__ OutDst<T, D> dst, uint32_t dcap,
+                                                                           uint32_t* __restrict__ cur_next) {
+  using L = RecL<T, D>;
+  constexpr int BLOCK = BUCKET_BLOCK, ITEMS = BUCKET_ITEMS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw);
-  uint32_t* off = cnt + 256;
-  uint32_t* wsum = off + 256;  // 64
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + 2304);
+  RBM_PROF_BEGIN(P);
   const uint32_t b = blockIdx.x;
-  const uint32_t s0 = S[b], n = S[b + 1] - s0;
+  const uint32_t s0 = S[b], n = S[b + 1] - s0, sb = b * scap;
   if (n == 0) return;
-  for (uint32_t i = threadIdx.x; i < 256; i += BLOCK) cnt[i] = 0;
+  const uint32_t nsb = 1u << P.SB;
+  const uint32_t nout = 1u << P.b1;
+  // sub-digit counts and offsets as packed u16 pairs (bucket sizes < 2^16);
+  // the same words later hold the <= 1024 output digit counts / offsets
+  const uint32_t ncw = (nsb / 2 > nout) ? nsb / 2 : nout;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* off = cnt + ncw;
+  uint32_t* gbase = off + ncw;
+  uint32_t* wsum = gbase + nout;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);
   const uint32_t cap = P.cap;
-  if (n <= cap) {
-    // TMA windows: 16-B aligned superset of [s0, s0+n) of every SoA array
-    constexpr uint32_t AX = 16 / sizeof(T);
-    const uint32_t lo_i = s0 & ~3u, oi = s0 - lo_i;
-    const uint32_t lo_x = s0 & ~(AX - 1), ox = s0 - lo_x;
-    const uint32_t bytes_i = ((oi + n + 3) & ~3u) * 4;
-    const uint32_t bytes_x = ((ox + n + AX - 1) & ~(AX - 1)) * (uint32_t)sizeof(T);
-    unsigned char* p = smem_raw + 2320;
-    uint32_t* id_raw = reinterpret_cast<uint32_t*>(p);
-    p += (size_t)(cap + 8) * 4;
-    T* xr[3];
-    const size_t xstride = ((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15;
-#pragma unroll
-    for (int c = 0; c < D; ++c) { xr[c] = reinterpret_cast<T*>(p); p += xstride; }
-    unsigned long long* ks = reinterpret_cast<unsigned long long*>(p);
-    p += (size_t)cap * 8;
-    uint32_t* key_l = reinterpret_cast<uint32_t*>(p);
-    p += (size_t)cap * 4;
-    uint16_t* ord = reinterpret_cast<uint16_t*>(p);
-    if (threadIdx.x == 0) {
-      mbar_init(bar, 1);
-      mbar_expect_tx(bar, bytes_i + D * bytes_x);
-      bulk_g2s(id_raw, src.id + lo_i, bytes_i, bar);
-#pragma unroll
-      for (int c = 0; c < D; ++c) bulk_g2s(xr[c], src.x[c] + lo_x, bytes_x, bar);
-    }
+  const uint32_t m = (uint32_t)*P.step;
+  for (uint32_t i = threadIdx.x; i < ncw / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
+  if (n > cap || n > (uint32_t)(BLOCK * ITEMS)) {  // oversized bucket: global scratch
     __syncthreads();
-    mbar_wait(bar, 0);
-    const SX<T> xs{xr[0] + ox, (uint32_t)(xstride / sizeof(T))};
-    bucket_compute<T, D, KK, INTEG, BLOCK>(P, dst, s0, s0, n, id_raw + oi, xs, key_l, ks, ord, cnt,
-                                           off, wsum);
+    big_bucket<T, D, KK, INTEG, BLOCK>(P, src, dst, cur_next, s0, sb, n, m, dcap, cnt, off, wsum);
+    return;
+  }
+  unsigned char* rs = reinterpret_cast<unsigned char*>(bar + 2);
+  uint32_t* key_l = reinterpret_cast<uint32_t*>(rs + (size_t)(cap + 8) * L::RS);
+  uint32_t* ks = key_l + cap + 8;  // composites (sort); then tb | inv (u16 each)
+  uint16_t* tb = reinterpret_cast<uint16_t*>(ks);
+  uint16_t* inv = tb + cap;
+  uint32_t* ta = key_l;            // key_{m+1} by element
+  uint16_t* ord = reinterpret_cast<uint16_t*>(ks + cap);
+  const bool side = !L::KEYED && P.side_key;
+  if (threadIdx.x == 0) {
+    const uint32_t bytes_r = (n * (uint32_t)L::RS + 15u) & ~15u;
+    const uint32_t bytes_k = side ? ((n + 3u) & ~3u) * 4u : 0u;
+    const uint64_t pol = l2_evict_first_policy();
+    mbar_init(bar, 1);
+    mbar_expect_tx(bar, bytes_r + bytes_k);
+    bulk_g2s_stream(rs, src.rec + (size_t)sb * L::RS, bytes_r, bar, pol);
+    if (side) bulk_g2s_stream(key_l, src.key + sb, bytes_k, bar, pol);
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  RBM_PROF(P, 0);
+  if (!L::KEYED && !side) {  // one-pass layouts: key_m from the ids
+    for (uint32_t e = threadIdx.x; e < n; e += BLOCK) key_l[e] = shuffle_key(P, ld_id<T, D>(rs, e), m);
+    __syncthreads();
+  }
+
+  // 1-3. exact (key, id) sort: counting sort on SB sub-digit bits + rank in sub-bucket
+  const uint32_t shsb = 32u - P.B - P.SB;
+  const uint32_t lowmask = (P.lowbits >= 32u) ? 0xffffffffu : ((1u << P.lowbits) - 1u);
+  uint32_t rc[ITEMS], rsd[ITEMS];
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const uint32_t e = k * BLOCK + threadIdx.x;
+    if (e < n) {
+      const unsigned char* re = rs + (size_t)e * L::RS;
+      const uint32_t id = reinterpret_cast<const uint32_t*>(re)[0];
+      const uint32_t key = L::KEYED ? reinterpret_cast<const uint32_t*>(re)[1] : key_l[e];
+      const uint32_t sd = (key >> shsb) & (nsb - 1u);
+      rc[k] = ((key & lowmask) << P.idbits) | id;
+      const uint32_t sh16 = (sd & 1u) << 4;
+      rsd[k] = (sd << 16) | ((atomicAdd(&cnt[sd >> 1], 1u << sh16) >> sh16) & 0xffffu);
+    }
+  }
+  __syncthreads();
+  RBM_PROF(P, 1);
+  block_excl_scan_u16x2<BLOCK>(cnt, off, nsb / 2, wsum);
+  RBM_PROF(P, 2);
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const uint32_t e = k * BLOCK + threadIdx.x;
+    if (e < n) {
+      const uint32_t sd = rsd[k] >> 16, sh16 = (sd & 1u) << 4;
+      const uint32_t a = (off[sd >> 1] >> sh16) & 0xffffu, c = (cnt[sd >> 1] >> sh16) & 0xffffu;
+      ks[a + (rsd[k] & 0xffffu)] = rc[k];
+      rsd[k] = (a << 16) | c;  // sub-bucket start and size, for the rank below
+    }
+  }
+  __syncthreads();
+  RBM_PROF(P, 3);
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const uint32_t e = k * BLOCK + threadIdx.x;
+    if (e < n) {
+      const uint32_t a = rsd[k] >> 16, c = rsd[k] & 0xffffu;
+      uint32_t r = a;
+      if (c > 1) {  // sub-buckets hold ~1 element: a short predicated scan
+#pragma unroll
+        for (uint32_t i = 0; i < 6; ++i)
+          if (i < c) r += (ks[a + i] < rc[k]) ? 1u : 0u;
+        // more than 6 (probability ~6e-4 per element): a plain loop, not
+        // unrolled, so warps that never take it pay no loop prologue
+#pragma unroll 1
+        for (uint32_t i = 6; i < c; ++i) r += (ks[a + i] < rc[k]) ? 1u : 0u;
+      }
+      ord[r] = (uint16_t)e;
+    }
+  }
+  // the packed sub-digit counters are dead: they become the output digit counts
+  for (uint32_t i = threadIdx.x; i < nout / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  RBM_PROF(P, 4);
+  if (P.dbg_order)
+    for (uint32_t q = threadIdx.x; q < n; q += BLOCK) P.dbg_order[s0 + q] = ld_id<T, D>(rs, ord[q]);
+  const uint32_t osh = 32u - P.b1;
+  // interior sorted positions [head, tail); the rest belong to straddling batches
+  uint32_t head, tail;
+  if (MODE == MODE_PAIR) {
+    // pairs start at even global positions; N odd: the last batch is a triple
+    const uint32_t N = (uint32_t)P.n;
+    const uint32_t pend = (N & 1u) ? N - 3u : N;
+    head = s0 & 1u;
+    const uint32_t lim = (min(s0 + n, pend) > s0) ? min(s0 + n, pend) - s0 : 0u;
+    const uint32_t npairs = (lim > head) ? (lim - head) / 2 : 0u;
+    tail = head + 2 * npairs;
+    const bool triple = (N & 1u) && (pend >= s0) && (N <= s0 + n);
+    // straddlers: unchanged, to their sorted places in the own gapped range
+    const uint32_t tri0 = triple ? pend - s0 : n;
+    for (uint32_t t = threadIdx.x; t < head + (tri0 - tail); t += BLOCK) {
+      const uint32_t q = t < head ? t : tail + (t - head);
+      uint32_t wd[L::NW];
+      ld_words<L::NW>(rs + (size_t)ord[q] * L::RS, wd);
+      st_words<L::NW>(src.rec + ((size_t)sb + q) * L::RS, wd);
+    }
+    RBM_PROF(P, 5);
+    // one thread per pair: Eq. (2.2) + update in place; next keys and ranks
+    constexpr int PITEMS = (ITEMS + 1) / 2;
+#pragma unroll 1  // one copy of the pair update: the hot loop stays in the instruction cache
+    for (int k = 0; k < PITEMS; ++k) {
+      const uint32_t j = k * BLOCK + threadIdx.x;
+      if (j < npairs) {
+        const uint32_t q = head + 2 * j;
+        const uint32_t e0 = ord[q], e1 = ord[q + 1];
+        Rec<T, D> r0 = ld_rec<T, D>(rs, e0), r1 = ld_rec<T, D>(rs, e1);
+        const uint32_t kn0 = shuffle_key(P, r0.id, m + 1), kn1 = shuffle_key(P, r1.id, m + 1);
+        T y0[D], y1[D];
+        pair_update<T, D, KK, INTEG>(P, m, r0.x, r1.x, r0.id, r1.id, y0, y1);
+        check_finite<T, D>(y0, P, r0.id, m);
+        check_finite<T, D>(y1, P, r1.id, m);
+#pragma unroll
+        for (int c = 0; c < D; ++c) { r0.x[c] = y0[c]; r1.x[c] = y1[c]; }
+        r0.key = kn0;
+        r1.key = kn1;
+        st_rec<T, D>(rs, e0, r0);
+        st_rec<T, D>(rs, e1, r1);
+        ta[e0] = kn0;
+        ta[e1] = kn1;
+        tb[e0] = (uint16_t)atomicAdd(&cnt[kn0 >> osh], 1u);
+        tb[e1] = (uint16_t)atomicAdd(&cnt[kn1 >> osh], 1u);
+      }
+    }
+    // the size-3 remainder batch (N odd, EM): one thread, out of line
+    if (triple && threadIdx.x == 0) serial_batch<T, D, KK, INTEG>(P, m, tri0, n, ord, rs, ta, tb, cnt, osh);
+    if (triple) tail = n;
   } else {
-    // oversized bucket (never expected at the automatic capacity, forced in
-    // tests): same algorithm on one of NBIG global-memory scratch slots,
-    // claimed from a small pool and released at the end (holders are resident,
-    // so waiters always make progress).
-    __shared__ uint32_t slot;
-    if (threadIdx.x == 0) {
-      slot = 0xffffffffu;
-      if (n <= BIG_CAP) {
-        for (;;) {
-          for (uint32_t s = 0; s < (uint32_t)NBIG && slot == 0xffffffffu; ++s)
-            if (atomicCAS(&P.big_claim[s], 0u, 1u) == 0u) slot = s;
-          if (slot != 0xffffffffu) break;
-          __nanosleep(500);
+    // interior batches [kfirst, klast) of this bucket
+    uint32_t kfirst = batch_index(s0, P);
+    if (kfirst * P.p < s0) ++kfirst;
+    uint32_t klast;
+    {
+      const uint32_t kl = batch_index(s0 + n - 1, P);
+      klast = (batch_end(kl, P) <= s0 + n) ? kl + 1 : kl;
+    }
+    head = (kfirst < klast) ? kfirst * P.p - s0 : n;
+    tail = (kfirst < klast) ? batch_end(klast - 1, P) - s0 : n;
+    for (uint32_t t = threadIdx.x; t < head + (n - tail); t += BLOCK) {
+      const uint32_t q = t < head ? t : tail + (t - head);
+      uint32_t wd[L::NW];
+      ld_words<L::NW>(rs + (size_t)ord[q] * L::RS, wd);
+      st_words<L::NW>(src.rec + ((size_t)sb + q) * L::RS, wd);
+    }
+    RBM_PROF(P, 5);
+    const uint32_t G = P.group;
+    if (G != 0) {
+      // lane groups: batches with sz <= G; each pair evaluated once in the
+      // canonical rotation order (batch_force), the partner's term by shuffle
+      const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      const uint32_t gpw = 32u / G, gi = lane / G, li = lane & (G - 1);
+      const uint32_t stride = (BLOCK / 32) * gpw;
+      for (uint32_t kb = kfirst + warp * gpw; kb < klast; kb += stride) {  // warp-uniform
+        const uint32_t k = kb + gi;
+        const bool valid = k < klast;
+        const uint32_t l0 = valid ? k * P.p - s0 : 0;
+        const uint32_t sz = valid ? batch_end(k, P) - s0 - l0 : 0;
+        const bool act = valid && sz <= G && li < sz;
+        const uint32_t e = act ? ord[l0 + li] : 0u;
+        Rec<T, D> ri;
+        if (act) ri = ld_rec<T, D>(rs, e);
+        T xi[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) xi[c] = act ? ri.x[c] : T(0);
+        const uint32_t id = act ? ri.id : 0u;
+        T xn[D];
+        if (INTEG != 1) {
+          T f[D];
+#pragma unroll
+          for (int c = 0; c < D; ++c) f[c] = T(0);
+          for (uint32_t o = 1; o <= G / 2; ++o) {
+            const uint32_t jp = (li + o) & (G - 1), jm = (li - o) & (G - 1);
+            T xj[D], t[D];
+#pragma unroll
+            for (int c = 0; c < D; ++c) xj[c] = __shfl_sync(0xffffffffu, xi[c], (int)jp, (int)G);
+            if (act && jp < sz) {
+              pair_term<T, D, KK, INTEG>(xi, xj, t, P);
+#pragma unroll
+              for (int c = 0; c < D; ++c) f[c] = add_rn(f[c], t[c]);
+            } else {
+#pragma unroll
+              for (int c = 0; c < D; ++c) t[c] = T(0);
+            }
+            if (o < G / 2) {  // warp-uniform
+#pragma unroll
+              for (int c = 0; c < (INTEG == 2 ? 1 : D); ++c) {
+                const T r = __shfl_sync(0xffffffffu, t[c], (int)jm, (int)G);
+                if (act && jm < sz) f[c] = sub_rn(f[c], r);
+              }
+            }
+          }
+          if (act) {
+            T z[D];
+#pragma unroll
+            for (int c = 0; c < D; ++c) z[c] = T(0);
+            if (P.has_noise) Normals<T, D>::get(P, id, m, TAG_NOISE, z);
+            const T inv_b = batch_inv<T>(P, sz);
+#pragma unroll
+            for (int c = 0; c < D; ++c) f[c] *= inv_b;
+            member_update<T, D, INTEG>(xi, f, z, xn, P, P.verlet_start != 0);
+          }
+        } else {  // split exact pair flow, p = 2 = G
+          T xo[D];
+#pragma unroll
+          for (int c = 0; c < D; ++c) xo[c] = __shfl_xor_sync(0xffffffffu, xi[c], 1, 2);
+          if (act) {
+            T xa[D], xb[D], y[D], z[D];
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+              xa[c] = li == 0 ? xi[c] : xo[c];
+              xb[c] = li == 0 ? xo[c] : xi[c];
+              z[c] = T(0);
+            }
+            if (P.has_noise) Normals<T, D>::get(P, id, m, TAG_NOISE, z);
+            pair_flow<T, D, KK>(xa, xb, li == 0, y, P);
+            split_finish<T, D>(y, z, xn, P, true);
+          }
+        }
+        if (act) {
+          check_finite<T, D>(xn, P, id, m);
+          const uint32_t kn = shuffle_key(P, id, m + 1);
+#pragma unroll
+          for (int c = 0; c < D; ++c) ri.x[c] = xn[c];
+          ri.key = kn;
+          st_rec<T, D>(rs, e, ri);
+          ta[e] = kn;
+          tb[e] = (uint16_t)atomicAdd(&cnt[kn >> osh], 1u);
         }
       }
     }
-    __syncthreads();
-    if (slot == 0xffffffffu) {
-      if (threadIdx.x == 0) atomicExch(P.capacity_err, 1u);
-      return;
-    }
-    unsigned char* base = P.big_scratch + slot * big_slot_bytes(D * sizeof(T));
-    unsigned long long* ks = reinterpret_cast<unsigned long long*>(base);
-    T* xr = reinterpret_cast<T*>(ks + BIG_CAP + 1);
-    uint32_t* id_l = reinterpret_cast<uint32_t*>(xr + (size_t)D * BIG_CAP);
-    uint32_t* key_l = id_l + BIG_CAP;
-    uint16_t* ord = reinterpret_cast<uint16_t*>(key_l + BIG_CAP);
-    const SX<T> xs{xr, BIG_CAP};
-    for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
-      id_l[e] = src.id[s0 + e];
-#pragma unroll
-      for (int c = 0; c < D; ++c) xs.at(c, e) = src.x[c][s0 + e];
-    }
-    __syncthreads();
-    bucket_compute<T, D, KK, INTEG, BLOCK>(P, dst, s0, s0, n, id_l, xs, key_l, ks, ord, cnt, off, wsum);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicExch(&P.big_claim[slot], 0u);
-    }
+    // batches too large for a lane group (the remainder batch, or p > 32): one thread each
+    const uint32_t first_big =
+        (G == 0) ? kfirst
+                 : ((klast > kfirst && batch_end(klast - 1, P) - (klast - 1) * P.p > G) ? klast - 1 : klast);
+    for (uint32_t k = first_big + threadIdx.x; k < klast; k += BLOCK)
+      serial_batch<T, D, KK, INTEG>(P, m, k * P.p - s0, batch_end(k, P) - s0, ord, rs, ta, tb, cnt, osh);
   }
+  __syncthreads();
+  RBM_PROF(P, 6);
+  // run reservations of digits threadIdx.x + r BLOCK, consumed after the staging index
+  constexpr int NRES = (1024 + BLOCK - 1) / BLOCK;
+  uint32_t gres[NRES];
+#pragma unroll
+  for (int r = 0; r < NRES; ++r) {
+    const uint32_t i = threadIdx.x + r * BLOCK;
+    const uint32_t h = i < nout ? cnt[i] : 0u;
+    gres[r] = h ? atomicAdd(&cur_next[(size_t)out_seg(P, i, blockIdx.x) * CUR1_STRIDE], h) : 0u;
+  }
+  const uint32_t total = block_excl_scan4<BLOCK>(cnt, off, nout, wsum);
+  for (uint32_t q = head + threadIdx.x; q < tail; q += BLOCK) {
+    const uint32_t e = ord[q];
+    inv[off[ta[e] >> osh] + tb[e]] = (uint16_t)e;
+  }
+#pragma unroll
+  for (int r = 0; r < NRES; ++r)  // gbase[d] - off[d]: output position j goes to slot gbase[dg] + j
+    if (threadIdx.x + r * BLOCK < nout) gbase[threadIdx.x + r * BLOCK] = gres[r] - off[threadIdx.x + r * BLOCK];
+  __syncthreads();
+  RBM_PROF(P, 7);
+  // staged slots -> coalesced runs of the step-(m+1) pass-1 buckets
+  for (uint32_t j = threadIdx.x; j < total; j += BLOCK) {
+    const uint32_t e = inv[j];
+    const uint32_t kn = ta[e];
+    const uint32_t dg = kn >> osh;
+    const uint32_t slot = gbase[dg] + j;
+    if (slot >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
+    out_copy<T, D>(dst, out_seg(P, dg, blockIdx.x), dcap, slot, rs + (size_t)e * L::RS, kn);
+  }
+  RBM_PROF(P, 8);
+  if (P.prof && threadIdx.x == 0) atomicAdd(&P.prof[63], 1ull);
 }
 
 // ------------------------------------------ resident multi-step (N <= 2048)
@@ -1014,6 +1223,15 @@ static __global__ void __launch_bounds__(BLOCK) bucket_step_kernel(const __grid_
 // B = 0 layout, e.g. BASELINE C1): per step, keys (Philox) -> exact sort by
 // (key_m, id) -> Eq. (2.2) + update of every batch into the other smem
 // buffer in sorted order; one launch replaces 2 launches per step.
+template <typename T, int D> struct SX {  // D coordinate arrays base + c*stride (shared memory)
+  T* base;
+  uint32_t stride;
+  __device__ __forceinline__ void get(uint32_t e, T (&x)[D]) const {
+#pragma unroll
+    for (int c = 0; c < D; ++c) x[c] = base[(uint32_t)c * stride + e];
+  }
+};
+
 template <typename T, int D> __host__ __device__ constexpr size_t resident_smem_bytes(uint32_t cap) {
   return 2304                                             // cnt, off, wsum
          + 2 * (size_t)cap * 4                            // ids, two buffers
@@ -1042,15 +1260,16 @@ static __global__ void __launch_bounds__(BLOCK) resident_kernel(const __grid_con
   p += (size_t)cap * 4;
   uint16_t* ord = reinterpret_cast<uint16_t*>(p);
   for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
-    idb[e] = src.id[e];
+    const Rec<T, D> r = ld_rec<T, D>(src.rec, e);
+    idb[e] = r.id;
 #pragma unroll
-    for (int c = 0; c < D; ++c) xb[(size_t)c * cap + e] = src.x[c][e];
+    for (int c = 0; c < D; ++c) xb[(size_t)c * cap + e] = r.x[c];
   }
   const uint32_t m0 = (uint32_t)*stepp;
   for (uint32_t it = 0; it < nsteps; ++it) {
     const uint32_t m = m0 + it, cur = it & 1u;
     const uint32_t* id_l = idb + cur * cap;
-    const SX<T> xs{xb + (size_t)cur * D * cap, cap};
+    const SX<T, D> xs{xb + (size_t)cur * D * cap, cap};
     uint32_t* id_o = idb + (cur ^ 1u) * cap;
     T* x_o = xb + (size_t)(cur ^ 1u) * D * cap;
     for (uint32_t i = threadIdx.x; i < 256; i += BLOCK) cnt[i] = 0;
@@ -1098,9 +1317,12 @@ static __global__ void __launch_bounds__(BLOCK) resident_kernel(const __grid_con
   }
   const uint32_t fin = nsteps & 1u;
   for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
-    dst.id[e] = idb[fin * cap + e];
+    Rec<T, D> r;
+    r.id = idb[fin * cap + e];
+    r.key = 0u;
 #pragma unroll
-    for (int c = 0; c < D; ++c) dst.x[c][e] = xb[((size_t)fin * D + c) * cap + e];
+    for (int c = 0; c < D; ++c) r.x[c] = xb[((size_t)fin * D + c) * cap + e];
+    st_rec<T, D>(dst.rec, e, r);
   }
   if (threadIdx.x == 0) *stepp = m0 + nsteps;
 }
@@ -1145,6 +1367,11 @@ static __global__ void __launch_bounds__(256) straddle_kernel(const __grid_const
       if ((q & 31u) == (uint32_t)lane) phys[k++] = (long long)bb * cap + (Pq - S[bb]);
     }
   }
+  auto getx = [&](long long g, T (&x)[D]) {
+    const Rec<T, D> r = ld_rec<T, D>(strad.rec, g);
+#pragma unroll
+    for (int c = 0; c < D; ++c) x[c] = r.x[c];
+  };
   T xnew[3][D];
   uint32_t idv[3];
   const uint32_t rounds = (sz + 31) / 32;
@@ -1152,10 +1379,12 @@ static __global__ void __launch_bounds__(256) straddle_kernel(const __grid_const
     const uint32_t q = r * 32 + lane;
     const bool act = q < sz;
     const long long g = act ? (r == 0 ? phys[0] : (r == 1 ? phys[1] : phys[2])) : 0ll;
-    const uint32_t id = act ? strad.id[g] : 0u;
+    Rec<T, D> rec;
+    if (act) rec = ld_rec<T, D>(strad.rec, g);
+    const uint32_t id = act ? rec.id : 0u;
     T xi[D], z[D], xn[D];
 #pragma unroll
-    for (int c = 0; c < D; ++c) { xi[c] = act ? strad.x[c][g] : T(0); z[c] = T(0); }
+    for (int c = 0; c < D; ++c) { xi[c] = act ? rec.x[c] : T(0); z[c] = T(0); }
     if (act && P.has_noise) Normals<T, D>::get(P, id, m, TAG_NOISE, z);
     if (INTEG != 1) {
       T f[D];
@@ -1173,11 +1402,7 @@ static __global__ void __launch_bounds__(256) straddle_kernel(const __grid_const
       }
       __syncwarp();
       if (act)
-        batch_force<T, D, KK, INTEG>(P, q, sz, xi, [&](uint32_t j, T (&xj)[D]) {
-          const long long gh = ph_w[j];
-#pragma unroll
-          for (int c = 0; c < D; ++c) xj[c] = strad.x[c][gh];
-        }, f);
+        batch_force<T, D, KK, INTEG>(P, q, sz, xi, [&](uint32_t j, T (&xj)[D]) { getx(ph_w[j], xj); }, f);
       __syncwarp();
       if (act) {
         const T inv = batch_inv<T>(P, sz);
@@ -1189,8 +1414,8 @@ static __global__ void __launch_bounds__(256) straddle_kernel(const __grid_const
       const long long ga = __shfl_sync(0xffffffffu, phys[0], 0), gb = __shfl_sync(0xffffffffu, phys[0], 1);
       if (act) {
         T xa[D], xb[D], y[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) { xa[c] = strad.x[c][ga]; xb[c] = strad.x[c][gb]; }
+        getx(ga, xa);
+        getx(gb, xb);
         pair_flow<T, D, KK>(xa, xb, q == 0, y, P);
         split_finish<T, D>(y, z, xn, P, true);
       }
@@ -1206,14 +1431,15 @@ static __global__ void __launch_bounds__(256) straddle_kernel(const __grid_const
   int k = 0;
   const uint32_t osh = 32u - P.b1;
   for (uint32_t q = lane; q < sz; q += 32, ++k) {
-    const uint32_t kn = shuffle_key(P, idv[k], m + 1);
-    const uint32_t v = out_seg(P, kn >> osh, warp);
+    Rec<T, D> o;
+    o.id = idv[k];
+    o.key = shuffle_key(P, o.id, m + 1);
+#pragma unroll
+    for (int c = 0; c < D; ++c) o.x[c] = xnew[k][c];
+    const uint32_t v = out_seg(P, o.key >> osh, warp);
     const uint32_t slot = atomicAdd(&cur_next[(size_t)v * CUR1_STRIDE], 1u);
     if (slot >= ocap) { atomicExch(P.capacity_err, 1u); continue; }
-    T xo[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c) xo[c] = xnew[k][c];
-    out_put<T, D>(dst, v, ocap, slot, idv[k], kn, xo);
+    out_put<T, D>(dst, v, ocap, slot, o);
   }
 }
 
@@ -1224,7 +1450,7 @@ static __global__ void __launch_bounds__(256) straddle_kernel(const __grid_const
 // all-gathered count of source s's pass-1 bucket j (global j).
 constexpr uint32_t HALO_MAX = 64;  // >= p - 1 records of the batch crossing a rank boundary
 template <typename T, int D> __host__ __device__ constexpr size_t halo_bytes() {
-  return 16 + HALO_MAX * 4 + (size_t)HALO_MAX * D * sizeof(T);
+  return 16 + (size_t)HALO_MAX * RecL<T, D>::RS;
 }
 
 // One block: segment counts (strided, for the pass-2 tile table), the exact
@@ -1282,7 +1508,7 @@ static __global__ void __launch_bounds__(1024) part_scan_kernel(const __grid_con
 // The batch crossing this rank's end E = S[nbuckets] (global positions
 // [b0, E), t = E - b0 <= p - 1 records, left unchanged in sorted order by the
 // bucket kernels) is owned by rank+1: copy it to the halo buffer
-// {u32 t; ids[HALO_MAX]; x[HALO_MAX][D]}.
+// {u32 t; pad; records[HALO_MAX]}.
 template <typename T, int D>
 static __global__ void halo_extract_kernel(const __grid_constant__ DevParams P, State<T, D> strad, uint32_t cap,
                                            const uint32_t* __restrict__ S, unsigned char* halo) {
@@ -1292,17 +1518,13 @@ static __global__ void halo_extract_kernel(const __grid_constant__ DevParams P, 
     batch_range(E, P, b0, b1);
     if (b0 < E) t = E - b0;
   }
-  uint32_t* hid = reinterpret_cast<uint32_t*>(halo + 16);
-  T* hx = reinterpret_cast<T*>(halo + 16 + HALO_MAX * 4);
   if (threadIdx.x == 0) *reinterpret_cast<uint32_t*>(halo) = t;
   for (uint32_t q = threadIdx.x; q < t; q += blockDim.x) {
     const uint32_t Pq = b0 + q;
     int bb = (int)P.nbuckets - 1;
     while (bb > 0 && S[bb] > Pq) --bb;
     const long long g = (long long)bb * cap + (Pq - S[bb]);
-    hid[q] = strad.id[g];
-#pragma unroll
-    for (int c = 0; c < D; ++c) hx[q * D + c] = strad.x[c][g];
+    st_rec<T, D>(halo + 16, q, ld_rec<T, D>(strad.rec, g));
   }
 }
 
@@ -1312,14 +1534,8 @@ template <typename T, int D>
 static __global__ void halo_place_kernel(const __grid_constant__ DevParams P, State<T, D> strad, uint32_t cap, uint32_t* S,
                                          const unsigned char* __restrict__ halo) {
   const uint32_t t = *reinterpret_cast<const uint32_t*>(halo);
-  const uint32_t* hid = reinterpret_cast<const uint32_t*>(halo + 16);
-  const T* hx = reinterpret_cast<const T*>(halo + 16 + HALO_MAX * 4);
-  for (uint32_t q = threadIdx.x; q < t; q += blockDim.x) {
-    const long long g = -(long long)cap + q;
-    strad.id[g] = hid[q];
-#pragma unroll
-    for (int c = 0; c < D; ++c) strad.x[c][g] = hx[q * D + c];
-  }
+  for (uint32_t q = threadIdx.x; q < t; q += blockDim.x)
+    st_rec<T, D>(strad.rec, -(long long)cap + q, ld_rec<T, D>(halo + 16, q));
   if (threadIdx.x == 0) S[-1] = S[0] - t;
 }
 
@@ -1340,1305 +1556,12 @@ static __global__ void gather_part_kernel(const __grid_constant__ DevParams P, S
     const uint32_t v = (uint32_t)(q / cap1), e = (uint32_t)(q - (uint64_t)v * cap1);
     const uint32_t s = v / nls, j = v - s * nls;
     if (e >= M[(size_t)s * nseg + rank * nls + j]) continue;
-    const uint64_t id = st.id[q];
+    const Rec<T, D> r = ld_rec<T, D>(st.rec, (long long)q);
+    const uint64_t id = r.id;
     if (id >= i0 && id < i1) {
 #pragma unroll
-      for (int c = 0; c < D; ++c) out[(id - i0) * D + c] = st.x[c][q];
+      for (int c = 0; c < D; ++c) out[(id - i0) * D + c] = r.x[c];
     }
-  }
-}
-
-// oversized bucket (never expected at the automatic capacity; forced in
-// tests): sorted-order compute on one of NBIG global scratch slots, claimed
-// from a small pool and released at the end (holders are resident, so waiters
-// always make progress), written back to the bucket's own gapped range, then a
-// per-element append into the step-(m+1) buckets.
-template <typename T, int D, int KK, int INTEG, int BLOCK>
-__device__ __noinline__ void fused_big_path(const DevParams& P, State<T, D> src, const OutDst<T, D>& dst,
-                                            uint32_t* cur_next, uint32_t s0, uint32_t sb, uint32_t n,
-                                            uint32_t m, uint32_t dcap, uint32_t* cnt, uint32_t* off,
-                                            uint32_t* wsum) {
-  __shared__ uint32_t slot;
-  if (threadIdx.x == 0) {
-    slot = 0xffffffffu;
-    if (n <= BIG_CAP) {
-      for (;;) {
-        for (uint32_t s = 0; s < (uint32_t)NBIG && slot == 0xffffffffu; ++s)
-          if (atomicCAS(&P.big_claim[s], 0u, 1u) == 0u) slot = s;
-        if (slot != 0xffffffffu) break;
-        __nanosleep(500);
-      }
-    }
-  }
-  __syncthreads();
-  if (slot == 0xffffffffu) {
-    if (threadIdx.x == 0) atomicExch(P.capacity_err, 1u);
-    return;
-  }
-  unsigned char* base = P.big_scratch + slot * big_slot_bytes(D * sizeof(T));
-  unsigned long long* ks = reinterpret_cast<unsigned long long*>(base);
-  T* xr = reinterpret_cast<T*>(ks + BIG_CAP + 1);
-  uint32_t* id_l = reinterpret_cast<uint32_t*>(xr + (size_t)D * BIG_CAP);
-  uint32_t* key_l = id_l + BIG_CAP;
-  uint16_t* ord = reinterpret_cast<uint16_t*>(key_l + BIG_CAP);
-  const SX<T> xs{xr, BIG_CAP};
-  for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
-    id_l[e] = src.id[sb + e];
-#pragma unroll
-    for (int c = 0; c < D; ++c) xs.at(c, e) = src.x[c][sb + e];
-  }
-  for (uint32_t i = threadIdx.x; i < 256; i += BLOCK) cnt[i] = 0;
-  __syncthreads();
-  bucket_compute<T, D, KK, INTEG, BLOCK>(P, src, s0, sb, n, id_l, xs, key_l, ks, ord, cnt, off,
-                                         wsum);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicExch(&P.big_claim[slot], 0u);
-  }
-  const uint32_t osh = 32u - P.b1;
-  for (uint32_t q = threadIdx.x; q < n; q += BLOCK) {
-    uint32_t b0, b1;
-    batch_range(s0 + q, P, b0, b1);
-    if (b0 >= s0 && b1 <= s0 + n) {
-      const uint32_t id = src.id[sb + q];
-      const uint32_t kn = shuffle_key(P, id, m + 1);
-      const uint32_t v = out_seg(P, kn >> osh, blockIdx.x);
-      const uint32_t s = atomicAdd(&cur_next[(size_t)v * CUR1_STRIDE], 1u);
-      if (s >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
-      T xo[D];
-#pragma unroll
-      for (int c = 0; c < D; ++c) xo[c] = src.x[c][sb + q];
-      out_put<T, D>(dst, v, dcap, s, id, kn, xo);
-    }
-  }
-}
-
-// One batch handled by one thread (remainder batches larger than the lane
-// group, or p > 32): all members computed from the old positions, then
-// written in place; sets ta[e] = key_{m+1}, tb[e] = digit<<16 | slot.
-template <typename T, int D, int KK, int INTEG>
-__device__ __noinline__ void serial_batch(const DevParams& P, uint32_t m, uint32_t l0, uint32_t l1,
-                                          const uint16_t* ord, const uint32_t* id_l, SX<T> xs,
-                                          uint32_t* ta, uint32_t* tb, uint32_t* ocnt, uint32_t osh) {
-  T xn[65][D];
-  const uint32_t sz = l1 - l0;
-  for (uint32_t q = l0; q < l1; ++q) {
-    T out[D];
-    interior_update<T, D, KK, INTEG>(P, m, q, l0, l1, ord, xs, id_l[ord[q]], out);
-#pragma unroll
-    for (int c = 0; c < D; ++c) xn[q - l0][c] = out[c];
-  }
-  for (uint32_t i = 0; i < sz; ++i) {
-    const uint32_t e = ord[l0 + i], id = id_l[e];
-    check_finite<T, D>(xn[i], P, id, m);
-    const uint32_t kn = shuffle_key(P, id, m + 1);
-    const uint32_t dg = kn >> osh;
-    ta[e] = kn;
-    tb[e] = (dg << 16) | atomicAdd(&ocnt[dg], 1u);
-#pragma unroll
-    for (int c = 0; c < D; ++c) xs.at(c, e) = xn[i][c];
-  }
-}
-
-// TMA: bulk-load bucket b (gapped, physical base sb = b*scap, n records) into
-// shared memory: ids, carried keys, D coordinate arrays (16-B multiples; the
-// capacity scap >= n + 64 covers the round-up).
-template <typename T, int D>
-__device__ __forceinline__ void load_bucket(State<T, D> src, uint32_t sb, uint32_t n, uint32_t* id_s,
-                                            uint32_t* key_s, T* x_s, uint32_t xst, uint64_t* bar) {
-  if (threadIdx.x == 0) {
-    const uint32_t bytes_i = ((n + 3) & ~3u) * 4;
-    constexpr uint32_t AX = 16 / sizeof(T);
-    const uint32_t bytes_x = ((n + AX - 1) & ~(AX - 1)) * (uint32_t)sizeof(T);
-    const uint64_t pol = l2_evict_first_policy();
-    mbar_init(bar, 1);
-    mbar_expect_tx(bar, 2 * bytes_i + D * bytes_x);
-    bulk_g2s_stream(id_s, src.id + sb, bytes_i, bar, pol);
-    bulk_g2s_stream(key_s, src.key + sb, bytes_i, bar, pol);
-#pragma unroll
-    for (int c = 0; c < D; ++c) bulk_g2s_stream(x_s + (size_t)c * xst, src.x[c] + sb, bytes_x, bar, pol);
-  }
-}
-
-// Output phase shared by the fused kernels: reserve runs in the step-(m+1)
-// buckets (capacity dcap), stage by digit, coalesced write of id, key_{m+1}, x.
-template <typename T, int D, int BLOCK>
-__device__ __forceinline__ void fused_output(const DevParams& P, const OutDst<T, D>& dst, uint32_t dcap,
-                                             uint32_t* cur_next, uint32_t n, const uint32_t* id_l,
-                                             const uint32_t* ta, const uint32_t* tb, SX<T> xs,
-                                             uint32_t* cnt, uint32_t* off, uint32_t* gbase,
-                                             uint16_t* inv, uint32_t* wsum) {
-  RBM_PROF_BEGIN(P);
-  const uint32_t nout = 1u << P.b1;
-  for (uint32_t i = threadIdx.x; i < nout; i += BLOCK) {
-    const uint32_t h = cnt[i];
-    gbase[i] = h ? atomicAdd(&cur_next[(size_t)out_seg(P, i, blockIdx.x) * CUR1_STRIDE], h) : 0u;
-  }
-  const uint32_t total = block_excl_scan4<BLOCK>(cnt, off, nout, wsum);
-  RBM_PROF(P, 8);
-  for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
-    const uint32_t t = tb[e];
-    if (t != 0xffffffffu) inv[off[t >> 16] + (t & 0xffffu)] = (uint16_t)e;
-  }
-  __syncthreads();
-  RBM_PROF(P, 9);
-  for (uint32_t j = threadIdx.x; j < total; j += BLOCK) {
-    const uint32_t e = inv[j];
-    const uint32_t dg = tb[e] >> 16;
-    const uint32_t slot = gbase[dg] + (j - off[dg]);
-    if (slot >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
-    T xo[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c) xo[c] = xs.at(c, e);
-    out_put<T, D>(dst, out_seg(P, dg, blockIdx.x), dcap, slot, id_l[e], ta[e], xo);
-  }
-  RBM_PROF(P, 10);}
-
-// ------------------------------------------------ fused bucket step (general p)
-// One CTA per final bucket b of step m (gapped, capacity scap; global start
-// S[b]).  (1) TMA bulk load, (2) exact in-smem sort by (key_m, id): counting
-// sort on SB sub-digit bits + rank among 32-bit composites, (3) Eq. (2.2) +
-// update of every interior batch, one lane group (G = pow2 >= p lanes, warp
-// shuffles) per batch, results in place, (4) the updated records are
-// partitioned by the top b1 bits of key_{m+1} into dst (capacity dcap).
-template <typename T, int D> __host__ __device__ constexpr size_t fused_smem_bytes(uint32_t cap,
-                                                                                  uint32_t SB) {
-  return (size_t)(2 * (SB > 10 ? (1u << SB) : 1024u) + 1024 + 64) * 4 + 16  // cnt, off, gbase, wsum, mbar
-         + (size_t)(cap + 8) * 8                                            // ids, keys (TMA windows)
-         + (size_t)D * (((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15)  // x (TMA window, in place)
-         + (size_t)cap * 12                                                 // ks, ta, tb
-         + (((size_t)cap * 4 + 15) & ~(size_t)15);                          // ord, inv (u16)
-}
-
-template <typename T, int D, int KK, int INTEG, int BLOCK>
-static __global__ void __launch_bounds__(BLOCK) bucket_fused_kernel(const __grid_constant__ DevParams P, State<T, D> src,
-                                                                    uint32_t scap,
-                                                                    const uint32_t* __restrict__ S,
-                                                                    const __grid_constant__ OutDst<T, D> dst, uint32_t dcap,
-                                                                    uint32_t* __restrict__ cur_next) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const uint32_t nsb = 1u << P.SB;
-  const uint32_t ncnt = nsb > 1024u ? nsb : 1024u;
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw);
-  uint32_t* off = cnt + ncnt;
-  uint32_t* gbase = off + ncnt;
-  uint32_t* wsum = gbase + 1024;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);
-  const uint32_t b = blockIdx.x;
-  const uint32_t s0 = S[b], n = S[b + 1] - s0, sb = b * scap;
-  if (n == 0) return;
-  const uint32_t m = (uint32_t)*P.step;
-  const uint32_t cap = P.cap;
-  if (nsb >= 4)
-    for (uint32_t i = threadIdx.x; i < nsb / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
-  else
-    for (uint32_t i = threadIdx.x; i < nsb; i += BLOCK) cnt[i] = 0;
-  if (n > cap) {
-    fused_big_path<T, D, KK, INTEG, BLOCK>(P, src, dst, cur_next, s0, sb, n, m, dcap, cnt, off, wsum);
-    return;
-  }
-  unsigned char* p = reinterpret_cast<unsigned char*>(bar + 2);
-  uint32_t* id_l = reinterpret_cast<uint32_t*>(p);
-  p += (size_t)(cap + 8) * 4;
-  uint32_t* key_l = reinterpret_cast<uint32_t*>(p);
-  p += (size_t)(cap + 8) * 4;
-  const uint32_t xst = (uint32_t)((((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15) / sizeof(T));
-  T* xr = reinterpret_cast<T*>(p);
-  p += (size_t)D * xst * sizeof(T);
-  uint32_t* ks = reinterpret_cast<uint32_t*>(p);     // composites grouped by sub-digit
-  uint32_t* ta = ks + cap;                           // composite by e -> key_{m+1} by e
-  uint32_t* tb = ta + cap;                           // sd<<16|slot by e -> out digit<<16|slot
-  uint16_t* ord = reinterpret_cast<uint16_t*>(tb + cap);  // sorted position -> e
-  uint16_t* inv = ord + cap;                         // staging index -> e
-  load_bucket<T, D>(src, sb, n, id_l, key_l, xr, xst, bar);
-  __syncthreads();
-  mbar_wait(bar, 0);
-  const SX<T> xs{xr, xst};
-
-  // 1. carried keys; counting sort by SB sub-digit bits; 32-bit (key, id) composites
-  const uint32_t shsb = 32u - P.B - P.SB;
-  const uint32_t lowmask = (P.lowbits >= 32u) ? 0xffffffffu : ((1u << P.lowbits) - 1u);
-  for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
-    const uint32_t key = key_l[e];
-    const uint32_t sd = (key >> shsb) & (nsb - 1u);
-    ta[e] = ((key & lowmask) << P.idbits) | id_l[e];
-    tb[e] = (sd << 16) | atomicAdd(&cnt[sd], 1u);
-  }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < nsb; i += BLOCK) off[i] = cnt[i];
-  __syncthreads();
-  block_excl_scan<BLOCK>(off, nsb, wsum);
-  // 2. composites grouped by sub-digit
-  for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
-    const uint32_t t = tb[e];
-    ks[off[t >> 16] + (t & 0xffffu)] = ta[e];
-  }
-  __syncthreads();
-  // 3. exact rank of each element inside its (~1 element) sub-bucket
-  for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
-    const uint32_t sd = tb[e] >> 16, v = ta[e];
-    const uint32_t a = off[sd], c = cnt[sd];
-    uint32_t r = a;
-    if (c > 1)  // most sub-buckets hold one element
-      for (uint32_t i = 0; i < c; ++i) r += (ks[a + i] < v) ? 1u : 0u;
-    ord[r] = (uint16_t)e;
-  }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < 256u; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);  // -> output digit counts
-  // interior batches [kfirst, klast) of this bucket; the rest straddle
-  uint32_t kfirst = batch_index(s0, P);
-  if (kfirst * P.p < s0) ++kfirst;
-  uint32_t klast;
-  {
-    const uint32_t kl = batch_index(s0 + n - 1, P);
-    klast = (batch_end(kl, P) <= s0 + n) ? kl + 1 : kl;
-  }
-  const uint32_t head = (kfirst < klast) ? kfirst * P.p - s0 : n;
-  const uint32_t tail = (kfirst < klast) ? batch_end(klast - 1, P) - s0 : n;
-  __syncthreads();
-  if (P.dbg_order)
-    for (uint32_t q = threadIdx.x; q < n; q += BLOCK) P.dbg_order[s0 + q] = id_l[ord[q]];
-  // straddling members: unchanged, to their sorted places in the own gapped range
-  for (uint32_t q = threadIdx.x; q < n; q += BLOCK) {
-    if (q < head || q >= tail) {
-      const uint32_t e = ord[q];
-      tb[e] = 0xffffffffu;
-      src.id[sb + q] = id_l[e];
-#pragma unroll
-      for (int c = 0; c < D; ++c) src.x[c][sb + q] = xs.at(c, e);
-    }
-  }
-  // 4. Eq. (2.2) + update: one lane group per batch, shuffles, in place
-  const uint32_t osh = 32u - P.b1;
-  const uint32_t G = P.group;
-  if (G != 0) {
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t gpw = 32u / G, gi = lane / G, li = lane & (G - 1);
-    const uint32_t stride = (BLOCK / 32) * gpw;
-    for (uint32_t kb = kfirst + warp * gpw; kb < klast; kb += stride) {  // warp-uniform
-      const uint32_t k = kb + gi;
-      const bool valid = k < klast;
-      const uint32_t l0 = valid ? k * P.p - s0 : 0;
-      const uint32_t sz = valid ? batch_end(k, P) - s0 - l0 : 0;
-      const bool act = valid && sz <= G && li < sz;
-      const uint32_t e = act ? ord[l0 + li] : 0u;
-      T xi[D];
-#pragma unroll
-      for (int c = 0; c < D; ++c) xi[c] = act ? xs.at(c, e) : T(0);
-      const uint32_t id = act ? id_l[e] : 0u;
-      T xn[D];
-      if (INTEG != 1) {
-        // canonical rotation order (batch_force): each pair once, the
-        // partner's term returned by a shuffle (K odd: exactly -t)
-        T f[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) f[c] = T(0);
-        for (uint32_t o = 1; o <= G / 2; ++o) {
-          const uint32_t jp = (li + o) & (G - 1), jm = (li - o) & (G - 1);
-          T xj[D], t[D];
-#pragma unroll
-          for (int c = 0; c < D; ++c) xj[c] = __shfl_sync(0xffffffffu, xi[c], (int)jp, (int)G);
-          const bool vp = act && jp < sz;
-          if (vp) {
-            pair_term<T, D, KK, INTEG>(xi, xj, t, P);
-#pragma unroll
-            for (int c = 0; c < D; ++c) f[c] = add_rn(f[c], t[c]);
-          } else {
-#pragma unroll
-            for (int c = 0; c < D; ++c) t[c] = T(0);
-          }
-          if (o < G / 2) {  // warp-uniform
-#pragma unroll
-            for (int c = 0; c < (INTEG == 2 ? 1 : D); ++c) {
-              const T r = __shfl_sync(0xffffffffu, t[c], (int)jm, (int)G);
-              if (act && jm < sz) f[c] = sub_rn(f[c], r);
-            }
-          }
-        }
-        if (act) {
-          T z[D];
-#pragma unroll
-          for (int c = 0; c < D; ++c) z[c] = T(0);
-          if (P.has_noise) Normals<T, D>::get(P, id, m, TAG_NOISE, z);
-          const T inv_b = batch_inv<T>(P, sz);
-#pragma unroll
-          for (int c = 0; c < D; ++c) f[c] *= inv_b;
-          member_update<T, D, INTEG>(xi, f, z, xn, P, P.verlet_start != 0);
-        }
-      } else {  // split exact pair flow, p = 2 = G
-        T xo[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) xo[c] = __shfl_xor_sync(0xffffffffu, xi[c], 1, 2);
-        if (act) {
-          T xa[D], xb[D], y[D], z[D];
-#pragma unroll
-          for (int c = 0; c < D; ++c) {
-            xa[c] = li == 0 ? xi[c] : xo[c];
-            xb[c] = li == 0 ? xo[c] : xi[c];
-            z[c] = T(0);
-          }
-          if (P.has_noise) Normals<T, D>::get(P, id, m, TAG_NOISE, z);
-          pair_flow<T, D, KK>(xa, xb, li == 0, y, P);
-          split_finish<T, D>(y, z, xn, P, true);
-        }
-      }
-      if (act) {
-        check_finite<T, D>(xn, P, id, m);
-        const uint32_t kn = shuffle_key(P, id, m + 1);
-        const uint32_t dg = kn >> osh;
-        ta[e] = kn;
-        tb[e] = (dg << 16) | atomicAdd(&cnt[dg], 1u);
-#pragma unroll
-        for (int c = 0; c < D; ++c) xs.at(c, e) = xn[c];
-      }
-    }
-  }
-  // batches too large for a lane group (remainder batch, or p > 32): one thread each
-  {
-    const uint32_t first_big =
-        (G == 0) ? kfirst
-                 : ((klast > kfirst && batch_end(klast - 1, P) - (klast - 1) * P.p > G) ? klast - 1
-                                                                                         : klast);
-    for (uint32_t k = first_big + threadIdx.x; k < klast; k += BLOCK)
-      serial_batch<T, D, KK, INTEG>(P, m, k * P.p - s0, batch_end(k, P) - s0, ord, id_l, xs, ta,
-                                    tb, cnt, osh);
-  }
-  __syncthreads();
-  fused_output<T, D, BLOCK>(P, dst, dcap, cur_next, n, id_l, ta, tb, xs, cnt, off, gbase, inv, wsum);
-}
-
-// ------------------------------------------- fused bucket step, p = 2 (lean)
-// Same contract, specialised for pairs: items in registers through the sort
-// phases (ITEMS per thread, cap <= BLOCK*ITEMS), one thread per pair; K is odd
-// with s(z) = s(-z), so the partner's force is exactly -f (the same terms the
-// oracle sums).
-template <typename T, int D> __host__ __device__ constexpr size_t pair_smem_bytes(uint32_t cap,
-                                                                                 uint32_t SB) {
-  return (size_t)(2 * (SB > 10 ? (1u << SB) : 1024u) + 1024 + 64) * 4 + 16  // cnt, off, gbase, wsum, mbar
-         + (size_t)(cap + 8) * 8                                           // ids, keys (TMA windows)
-         + (size_t)D * (((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15) // x (TMA window, in place)
-         + (size_t)cap * 4                                                 // ks -> digit|slot
-         + (((size_t)cap * 4 + 15) & ~(size_t)15);                         // ord, inv (u16)
-}
-
-template <typename T, int D, int KK, int INTEG>
-__device__ __forceinline__ void pair_update(const DevParams& P, uint32_t m, const T (&x0)[D],
-                                            const T (&x1)[D], uint32_t id0, uint32_t id1,
-                                            T (&y0)[D], T (&y1)[D]) {
-  T z0[D], z1[D];
-#pragma unroll
-  for (int c = 0; c < D; ++c) { z0[c] = T(0); z1[c] = T(0); }
-  if (P.has_noise) {
-    Normals<T, D>::get(P, id0, m, TAG_NOISE, z0);
-    Normals<T, D>::get(P, id1, m, TAG_NOISE, z1);
-  }
-  if (INTEG == 0) {
-    T zz[D], f0[D], f1[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c) zz[c] = x0[c] - x1[c];
-    const T sc = kernel_scale<T, D, KK>(zz, P);  // 1/(p-1) = 1
-#pragma unroll
-    for (int c = 0; c < D; ++c) { f0[c] = sc * zz[c]; f1[c] = -f0[c]; }
-    em_update<T, D>(x0, f0, z0, y0, P, true);
-    em_update<T, D>(x1, f1, z1, y1, P, true);
-  } else if (INTEG == 2) {  // Verlet: 1-D force on the positions; the partner gets -f
-    T f0[D], f1[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c) { f0[c] = T(0); f1[c] = T(0); }
-    add_force1<T, D, KK>(x0, x1, f0, P);
-    f1[0] = -f0[0];
-    verlet_update<T, D>(x0, f0, y0, P, P.verlet_start != 0);
-    verlet_update<T, D>(x1, f1, y1, P, P.verlet_start != 0);
-  } else {
-    T a[D], b[D];
-    pair_flow<T, D, KK>(x0, x1, true, a, P);
-    pair_flow<T, D, KK>(x0, x1, false, b, P);
-    split_finish<T, D>(a, z0, y0, P, true);
-    split_finish<T, D>(b, z1, y1, P, true);
-  }
-}
-
-
-template <typename T, int D, int KK, int INTEG, int BLOCK, int ITEMS>
-static __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) bucket_pair_kernel(const __grid_constant__ DevParams P, State<T, D> src,
-                                                                   uint32_t scap,
-                                                                   const uint32_t* __restrict__ S,
-                                                                   const __grid_constant__ OutDst<T, D> dst, uint32_t dcap,
-                                                                   uint32_t* __restrict__ cur_next) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  RBM_PROF_BEGIN(P);
-  const uint32_t b = blockIdx.x;
-  const uint32_t s0 = S[b], n = S[b + 1] - s0, sb = b * scap;
-  if (n == 0) return;
-  const uint32_t nsb = 1u << P.SB;
-  const uint32_t ncnt = nsb > 1024u ? nsb : 1024u;  // also holds the <= 1024 output digits
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw);
-  uint32_t* off = cnt + ncnt;
-  uint32_t* gbase = off + ncnt;
-  uint32_t* wsum = gbase + 1024;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);
-  const uint32_t cap = P.cap;
-  const uint32_t m = (uint32_t)*P.step;
-  for (uint32_t i = threadIdx.x; i < nsb / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
-  if (n > cap) {
-    fused_big_path<T, D, KK, INTEG, BLOCK>(P, src, dst, cur_next, s0, sb, n, m, dcap, cnt, off, wsum);
-    return;
-  }
-  unsigned char* p = reinterpret_cast<unsigned char*>(bar + 2);
-  uint32_t* id_l = reinterpret_cast<uint32_t*>(p);
-  p += (size_t)(cap + 8) * 4;
-  uint32_t* key_l = reinterpret_cast<uint32_t*>(p);  // key_m by e; then key_{m+1} by e
-  p += (size_t)(cap + 8) * 4;
-  const uint32_t xst = (uint32_t)((((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15) / sizeof(T));
-  T* xr = reinterpret_cast<T*>(p);
-  p += (size_t)D * xst * sizeof(T);
-  uint32_t* ks = reinterpret_cast<uint32_t*>(p);   // composites; then digit<<16|slot by e
-  uint32_t* tb = ks;
-  uint32_t* ta = key_l;
-  uint16_t* ord = reinterpret_cast<uint16_t*>(ks + cap);
-  uint16_t* inv = ord + cap;
-  load_bucket<T, D>(src, sb, n, id_l, key_l, xr, xst, bar);
-  __syncthreads();
-  mbar_wait(bar, 0);
-  RBM_PROF(P, 0);
-  const SX<T> xs{xr, xst};
-
-  // 1-3. exact (key, id) sort: counting sort on SB sub-digit bits + rank in sub-bucket
-  const uint32_t shsb = 32u - P.B - P.SB;
-  const uint32_t lowmask = (P.lowbits >= 32u) ? 0xffffffffu : ((1u << P.lowbits) - 1u);
-  uint32_t rc[ITEMS], rs[ITEMS];
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    const uint32_t e = k * BLOCK + threadIdx.x;
-    if (e < n) {
-      const uint32_t key = key_l[e];
-      const uint32_t sd = (key >> shsb) & (nsb - 1u);
-      rc[k] = ((key & lowmask) << P.idbits) | id_l[e];
-      rs[k] = (sd << 16) | atomicAdd(&cnt[sd], 1u);
-    }
-  }
-  __syncthreads();
-  RBM_PROF(P, 1);
-  block_excl_scan4<BLOCK>(cnt, off, nsb, wsum);
-  RBM_PROF(P, 2);
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    const uint32_t e = k * BLOCK + threadIdx.x;
-    if (e < n) ks[off[rs[k] >> 16] + (rs[k] & 0xffffu)] = rc[k];
-  }
-  __syncthreads();
-  RBM_PROF(P, 3);
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    const uint32_t e = k * BLOCK + threadIdx.x;
-    if (e < n) {
-      const uint32_t sd = rs[k] >> 16;
-      const uint32_t a = off[sd], c = cnt[sd];
-      uint32_t r = a;
-      if (c > 1) {  // sub-buckets hold ~1 element: a short predicated scan
-#pragma unroll
-        for (uint32_t i = 0; i < 6; ++i)
-          if (i < c) r += (ks[a + i] < rc[k]) ? 1u : 0u;
-        // more than 6 (probability ~6e-4 per element): a plain loop, not
-        // unrolled, so warps that never take it pay no loop prologue
-#pragma unroll 1
-        for (uint32_t i = 6; i < c; ++i) r += (ks[a + i] < rc[k]) ? 1u : 0u;
-      }
-      ord[r] = (uint16_t)e;
-    }
-  }
-  __syncthreads();
-  RBM_PROF(P, 4);
-  // interior pairs: even global starts in [s0, end), end excludes a final triple (N odd)
-  const uint32_t N = (uint32_t)P.n;
-  const uint32_t pend = (N & 1u) ? N - 3u : N;
-  const uint32_t head = s0 & 1u;                         // local index of the first pair
-  const uint32_t lim = (min(s0 + n, pend) > s0) ? min(s0 + n, pend) - s0 : 0u;
-  const uint32_t npairs = (lim > head) ? (lim - head) / 2 : 0u;
-  const uint32_t covered = head + 2 * npairs;            // [head, covered) are interior
-  const bool triple = (N & 1u) && (pend >= s0) && (N <= s0 + n);
-  const uint32_t tri0 = triple ? pend - s0 : n;          // [tri0, n): the size-3 remainder batch
-  const uint32_t osh = 32u - P.b1;
-  const uint32_t nout = 1u << P.b1;
-  for (uint32_t i = threadIdx.x; i < nout / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
-  if (P.dbg_order)
-    for (uint32_t q = threadIdx.x; q < n; q += BLOCK) P.dbg_order[s0 + q] = id_l[ord[q]];
-  __syncthreads();
-  RBM_PROF(P, 5);
-  // 4. output partition first (key_{m+1} depends on the id only): digit and
-  //    rank of every interior member, so the run reservations below are in
-  //    flight while the batches are computed.  ks is dead: tb = rank by e.
-  for (uint32_t q = head + threadIdx.x; q < n; q += BLOCK) {
-    if (q >= covered && q < tri0) continue;
-    const uint32_t e = ord[q];
-    const uint32_t kn = shuffle_key(P, id_l[e], m + 1);
-    ta[e] = kn;
-    tb[e] = atomicAdd(&cnt[kn >> osh], 1u);
-  }
-  // straddlers: unchanged, to their sorted places in the own gapped range
-  for (uint32_t t = threadIdx.x; t < head + (tri0 - covered); t += BLOCK) {
-    const uint32_t q = t < head ? t : covered + (t - head);
-    const uint32_t e = ord[q];
-    src.id[sb + q] = id_l[e];
-#pragma unroll
-    for (int c = 0; c < D; ++c) src.x[c][sb + q] = xs.at(c, e);
-  }
-  __syncthreads();
-  // run reservations of digits threadIdx.x + r BLOCK, consumed after the batches
-  constexpr int NRES = (1024 + BLOCK - 1) / BLOCK;
-  uint32_t gres[NRES];
-#pragma unroll
-  for (int r = 0; r < NRES; ++r) {
-    const uint32_t i = threadIdx.x + r * BLOCK;
-    const uint32_t h = i < nout ? cnt[i] : 0u;
-    gres[r] = h ? atomicAdd(&cur_next[(size_t)out_seg(P, i, blockIdx.x) * CUR1_STRIDE], h) : 0u;
-  }
-  const uint32_t total = block_excl_scan4<BLOCK>(cnt, off, nout, wsum);
-  RBM_PROF(P, 8);
-  // 5. one thread per pair: Eq. (2.2) + update in place; staging index of each member
-  constexpr int PITEMS = (ITEMS + 1) / 2;
-#pragma unroll
-  for (int k = 0; k < PITEMS; ++k) {
-    const uint32_t j = k * BLOCK + threadIdx.x;
-    if (j < npairs) {
-      const uint32_t q = head + 2 * j;
-      const uint32_t e0 = ord[q], e1 = ord[q + 1];
-      const uint32_t id0 = id_l[e0], id1 = id_l[e1];
-      T x0[D], x1[D], y0[D], y1[D];
-#pragma unroll
-      for (int c = 0; c < D; ++c) { x0[c] = xs.at(c, e0); x1[c] = xs.at(c, e1); }
-      pair_update<T, D, KK, INTEG>(P, m, x0, x1, id0, id1, y0, y1);
-      check_finite<T, D>(y0, P, id0, m);
-      check_finite<T, D>(y1, P, id1, m);
-#pragma unroll
-      for (int c = 0; c < D; ++c) { xs.at(c, e0) = y0[c]; xs.at(c, e1) = y1[c]; }
-      inv[off[ta[e0] >> osh] + tb[e0]] = (uint16_t)e0;
-      inv[off[ta[e1] >> osh] + tb[e1]] = (uint16_t)e1;
-    }
-  }
-  if (triple && threadIdx.x == 0) {  // the remainder batch of size 3 (N odd), EM only
-    T xn[3][D];
-    for (uint32_t q = tri0; q < n; ++q)
-      interior_update<T, D, KK, INTEG>(P, m, q, tri0, n, ord, xs, id_l[ord[q]], xn[q - tri0]);
-    for (uint32_t q = tri0; q < n; ++q) {
-      const uint32_t e = ord[q];
-      check_finite<T, D>(xn[q - tri0], P, id_l[e], m);
-#pragma unroll
-      for (int c = 0; c < D; ++c) xs.at(c, e) = xn[q - tri0][c];
-      inv[off[ta[e] >> osh] + tb[e]] = (uint16_t)e;
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < NRES; ++r)
-    if (threadIdx.x + r * BLOCK < nout) gbase[threadIdx.x + r * BLOCK] = gres[r];
-  __syncthreads();
-  RBM_PROF(P, 6);
-  // 6. staged slots -> coalesced runs of the step-(m+1) pass-1 buckets
-  for (uint32_t j = threadIdx.x; j < total; j += BLOCK) {
-    const uint32_t e = inv[j];
-    const uint32_t kn = ta[e];
-    const uint32_t dg = kn >> osh;
-    const uint32_t slot = gbase[dg] + (j - off[dg]);
-    if (slot >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
-    T xo[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c) xo[c] = xs.at(c, e);
-    out_put<T, D>(dst, out_seg(P, dg, blockIdx.x), dcap, slot, id_l[e], kn, xo);
-  }
-  RBM_PROF(P, 7);
-  if (P.prof && threadIdx.x == 0) atomicAdd(&P.prof[63], 1ull);
-}
-
-// the size-3 remainder batch of the p = 2 kernels (N odd; one bucket per
-// step): out of line so the hot loops stay compact in the instruction cache
-template <typename T, int D, int KK, int INTEG>
-__device__ __noinline__ void pair3_triple(const DevParams& P, uint32_t m, uint32_t tri0, uint32_t n,
-                                          const uint16_t* ord, SX<T> xs, const uint32_t* id_l,
-                                          const uint32_t* ta, const uint16_t* tb, const uint32_t* off,
-                                          uint16_t* inv, uint32_t osh) {
-  T xn[3][D];
-  for (uint32_t q = tri0; q < n; ++q)
-    interior_update<T, D, KK, INTEG>(P, m, q, tri0, n, ord, xs, id_l[ord[q]], xn[q - tri0]);
-  for (uint32_t q = tri0; q < n; ++q) {
-    const uint32_t e = ord[q];
-    check_finite<T, D>(xn[q - tri0], P, id_l[e], m);
-#pragma unroll
-    for (int c = 0; c < D; ++c) xs.at(c, e) = xn[q - tri0][c];
-    inv[off[ta[e] >> osh] + tb[e]] = (uint16_t)e;
-  }
-}
-
-// The p = 2 bucket step with a compact shared-memory footprint (packed u16
-// sub-digit counters, u16 staging aliased over the dead composites) so that
-// three 256-thread CTAs -- three buckets in flight -- fit on one SM.
-template <typename T, int D> __host__ __device__ constexpr size_t pair3_smem_bytes(uint32_t cap, uint32_t SB,
-                                                                                  uint32_t b1) {
-  return (size_t)(2 * (((1u << SB) / 2 > (1u << b1)) ? (1u << SB) / 2 : (1u << b1)) + (1u << b1) + 64) * 4 + 16
-         + (size_t)(cap + 8) * 8                                            // ids, keys (TMA windows)
-         + (size_t)D * (((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15)  // x (TMA window, in place)
-         + (size_t)cap * 4                                                 // composites -> tb | inv
-         + (((size_t)cap * 2 + 15) & ~(size_t)15);                         // ord (u16)
-}
-
-template <typename T, int D, int KK, int INTEG, int BLOCK, int ITEMS>
-static __global__ void __launch_bounds__(BLOCK, 3) bucket_pair3_kernel(const __grid_constant__ DevParams P, State<T, D> src,
-                                                                   uint32_t scap,
-                                                                   const uint32_t* __restrict__ S,
-                                                                   const __grid_constant__ OutDst<T, D> dst, uint32_t dcap,
-                                                                   uint32_t* __restrict__ cur_next) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  RBM_PROF_BEGIN(P);
-  const uint32_t b = blockIdx.x;
-  const uint32_t s0 = S[b], n = S[b + 1] - s0, sb = b * scap;
-  if (n == 0) return;
-  const uint32_t nsb = 1u << P.SB;
-  const uint32_t nout = 1u << P.b1;
-  // sub-digit counts and offsets as packed u16 pairs (bucket sizes < 2^16);
-  // the same words later hold the <= 1024 output digit counts / offsets
-  const uint32_t ncw = (nsb / 2 > nout) ? nsb / 2 : nout;
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw);
-  uint32_t* off = cnt + ncw;
-  uint32_t* gbase = off + ncw;
-  uint32_t* wsum = gbase + nout;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);
-  const uint32_t cap = P.cap;
-  const uint32_t m = (uint32_t)*P.step;
-  for (uint32_t i = threadIdx.x; i < ncw / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
-  if (n > cap) {  // oversized bucket: the global-scratch path with its own 8-bit counters
-    __shared__ uint32_t bigc[2 * 256 + 64];
-    __syncthreads();
-    fused_big_path<T, D, KK, INTEG, BLOCK>(P, src, dst, cur_next, s0, sb, n, m, dcap, bigc, bigc + 256, bigc + 512);
-    return;
-  }
-  unsigned char* p = reinterpret_cast<unsigned char*>(bar + 2);
-  uint32_t* id_l = reinterpret_cast<uint32_t*>(p);
-  p += (size_t)(cap + 8) * 4;
-  uint32_t* key_l = reinterpret_cast<uint32_t*>(p);  // key_m by e; then key_{m+1} by e
-  p += (size_t)(cap + 8) * 4;
-  const uint32_t xst = (uint32_t)((((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15) / sizeof(T));
-  T* xr = reinterpret_cast<T*>(p);
-  p += (size_t)D * xst * sizeof(T);
-  uint32_t* ks = reinterpret_cast<uint32_t*>(p);   // composites (sort); then tb | inv (u16 each)
-  uint16_t* tb = reinterpret_cast<uint16_t*>(ks);
-  uint16_t* inv = tb + cap;
-  uint32_t* ta = key_l;
-  uint16_t* ord = reinterpret_cast<uint16_t*>(ks + cap);
-  load_bucket<T, D>(src, sb, n, id_l, key_l, xr, xst, bar);
-  __syncthreads();
-  mbar_wait(bar, 0);
-  RBM_PROF(P, 0);
-  const SX<T> xs{xr, xst};
-
-  // 1-3. exact (key, id) sort: counting sort on SB sub-digit bits + rank in sub-bucket
-  const uint32_t shsb = 32u - P.B - P.SB;
-  const uint32_t lowmask = (P.lowbits >= 32u) ? 0xffffffffu : ((1u << P.lowbits) - 1u);
-  uint32_t rc[ITEMS], rs[ITEMS];
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    const uint32_t e = k * BLOCK + threadIdx.x;
-    if (e < n) {
-      const uint32_t key = key_l[e];
-      const uint32_t sd = (key >> shsb) & (nsb - 1u);
-      rc[k] = ((key & lowmask) << P.idbits) | id_l[e];
-      const uint32_t sh16 = (sd & 1u) << 4;
-      rs[k] = (sd << 16) | ((atomicAdd(&cnt[sd >> 1], 1u << sh16) >> sh16) & 0xffffu);
-    }
-  }
-  __syncthreads();
-  RBM_PROF(P, 1);
-  block_excl_scan_u16x2<BLOCK>(cnt, off, nsb / 2, wsum);
-  RBM_PROF(P, 2);
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    const uint32_t e = k * BLOCK + threadIdx.x;
-    if (e < n) {
-      const uint32_t sd = rs[k] >> 16, sh16 = (sd & 1u) << 4;
-      const uint32_t a = (off[sd >> 1] >> sh16) & 0xffffu, c = (cnt[sd >> 1] >> sh16) & 0xffffu;
-      ks[a + (rs[k] & 0xffffu)] = rc[k];
-      rs[k] = (a << 16) | c;  // sub-bucket start and size, for the rank below
-    }
-  }
-  __syncthreads();
-  RBM_PROF(P, 3);
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    const uint32_t e = k * BLOCK + threadIdx.x;
-    if (e < n) {
-      const uint32_t a = rs[k] >> 16, c = rs[k] & 0xffffu;
-      uint32_t r = a;
-      if (c > 1) {  // sub-buckets hold ~1 element: a short predicated scan
-#pragma unroll
-        for (uint32_t i = 0; i < 6; ++i)
-          if (i < c) r += (ks[a + i] < rc[k]) ? 1u : 0u;
-        // more than 6 (probability ~6e-4 per element): a plain loop, not
-        // unrolled, so warps that never take it pay no loop prologue
-#pragma unroll 1
-        for (uint32_t i = 6; i < c; ++i) r += (ks[a + i] < rc[k]) ? 1u : 0u;
-      }
-      ord[r] = (uint16_t)e;
-    }
-  }
-  // the packed sub-digit counters are dead: they become the output digit counts
-  for (uint32_t i = threadIdx.x; i < nout / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
-  __syncthreads();
-  RBM_PROF(P, 4);
-  // interior pairs: even global starts in [s0, end), end excludes a final triple (N odd)
-  const uint32_t N = (uint32_t)P.n;
-  const uint32_t pend = (N & 1u) ? N - 3u : N;
-  const uint32_t head = s0 & 1u;                         // local index of the first pair
-  const uint32_t lim = (min(s0 + n, pend) > s0) ? min(s0 + n, pend) - s0 : 0u;
-  const uint32_t npairs = (lim > head) ? (lim - head) / 2 : 0u;
-  const uint32_t covered = head + 2 * npairs;            // [head, covered) are interior
-  const bool triple = (N & 1u) && (pend >= s0) && (N <= s0 + n);
-  const uint32_t tri0 = triple ? pend - s0 : n;          // [tri0, n): the size-3 remainder batch
-  const uint32_t osh = 32u - P.b1;
-  if (P.dbg_order)
-    for (uint32_t q = threadIdx.x; q < n; q += BLOCK) P.dbg_order[s0 + q] = id_l[ord[q]];
-  RBM_PROF(P, 5);
-  // 4. key_{m+1} depends on the id only: each pair thread computes its two
-  //    next keys beside the two noise blocks (four independent Philox chains)
-  //    and ranks them in their output digits; ks is dead: tb = rank by e.
-  auto out_rank = [&](uint32_t q) {
-    const uint32_t e = ord[q];
-    const uint32_t kn = shuffle_key(P, id_l[e], m + 1);
-    ta[e] = kn;
-    tb[e] = (uint16_t)atomicAdd(&cnt[kn >> osh], 1u);
-  };
-  // (the pairs' next keys and ranks are computed in the pair loop below)
-  for (uint32_t q = tri0 + threadIdx.x; q < n; q += BLOCK) out_rank(q);  // the size-3 batch (N odd)
-  // straddlers: unchanged, to their sorted places in the own gapped range
-  for (uint32_t t = threadIdx.x; t < head + (tri0 - covered); t += BLOCK) {
-    const uint32_t q = t < head ? t : covered + (t - head);
-    const uint32_t e = ord[q];
-    src.id[sb + q] = id_l[e];
-#pragma unroll
-    for (int c = 0; c < D; ++c) src.x[c][sb + q] = xs.at(c, e);
-  }
-  RBM_PROF(P, 8);
-  // 5. one thread per pair: Eq. (2.2) + update in place; staging index of each member
-  constexpr int PITEMS = (ITEMS + 1) / 2;
-#pragma unroll 1  // one copy of the pair update: the hot loop stays in the instruction cache
-  for (int k = 0; k < PITEMS; ++k) {
-    const uint32_t j = k * BLOCK + threadIdx.x;
-    if (j < npairs) {
-      const uint32_t q = head + 2 * j;
-      const uint32_t e0 = ord[q], e1 = ord[q + 1];
-      const uint32_t id0 = id_l[e0], id1 = id_l[e1];
-      T x0[D], x1[D], y0[D], y1[D];
-#pragma unroll
-      for (int c = 0; c < D; ++c) { x0[c] = xs.at(c, e0); x1[c] = xs.at(c, e1); }
-      const uint32_t kn0 = shuffle_key(P, id0, m + 1), kn1 = shuffle_key(P, id1, m + 1);
-      pair_update<T, D, KK, INTEG>(P, m, x0, x1, id0, id1, y0, y1);
-      check_finite<T, D>(y0, P, id0, m);
-      check_finite<T, D>(y1, P, id1, m);
-#pragma unroll
-      for (int c = 0; c < D; ++c) { xs.at(c, e0) = y0[c]; xs.at(c, e1) = y1[c]; }
-      ta[e0] = kn0;
-      ta[e1] = kn1;
-      tb[e0] = (uint16_t)atomicAdd(&cnt[kn0 >> osh], 1u);
-      tb[e1] = (uint16_t)atomicAdd(&cnt[kn1 >> osh], 1u);
-    }
-  }
-  __syncthreads();
-  // run reservations of digits threadIdx.x + r BLOCK, consumed after the staging index
-  constexpr int NRES = (1024 + BLOCK - 1) / BLOCK;
-  uint32_t gres[NRES];
-#pragma unroll
-  for (int r = 0; r < NRES; ++r) {
-    const uint32_t i = threadIdx.x + r * BLOCK;
-    const uint32_t h = i < nout ? cnt[i] : 0u;
-    gres[r] = h ? atomicAdd(&cur_next[(size_t)out_seg(P, i, blockIdx.x) * CUR1_STRIDE], h) : 0u;
-  }
-  const uint32_t total = block_excl_scan4<BLOCK>(cnt, off, nout, wsum);
-  for (uint32_t q = head + threadIdx.x; q < covered; q += BLOCK) {
-    const uint32_t e = ord[q];
-    inv[off[ta[e] >> osh] + tb[e]] = (uint16_t)e;
-  }
-  if (triple && threadIdx.x == 0)  // the remainder batch of size 3 (N odd), EM only
-    pair3_triple<T, D, KK, INTEG>(P, m, tri0, n, ord, xs, id_l, ta, tb, off, inv, osh);
-#pragma unroll
-  for (int r = 0; r < NRES; ++r)  // gbase[d] - off[d]: output position j goes to slot gbase[dg] + j
-    if (threadIdx.x + r * BLOCK < nout) gbase[threadIdx.x + r * BLOCK] = gres[r] - off[threadIdx.x + r * BLOCK];
-  __syncthreads();
-  RBM_PROF(P, 6);
-  // 6. staged slots -> coalesced runs of the step-(m+1) pass-1 buckets
-  for (uint32_t j = threadIdx.x; j < total; j += BLOCK) {
-    const uint32_t e = inv[j];
-    const uint32_t kn = ta[e];
-    const uint32_t dg = kn >> osh;
-    const uint32_t slot = gbase[dg] + j;
-    if (slot >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
-    T xo[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c) xo[c] = xs.at(c, e);
-    out_put<T, D>(dst, out_seg(P, dg, blockIdx.x), dcap, slot, id_l[e], kn, xo);
-  }
-  RBM_PROF(P, 7);
-  if (P.prof && threadIdx.x == 0) atomicAdd(&P.prof[63], 1ull);
-}
-
-// batch of more than G members (p a power of two, N mod p = 1): all members
-// from the old positions (canonical order: ascending), then written in place
-template <typename T, int D, int KK, int INTEG>
-__device__ __noinline__ void group3_big(const DevParams& P, uint32_t m, uint32_t l0, uint32_t l1,
-                                        const uint16_t* ord, SX<T> xs, const uint32_t* id_l,
-                                        const uint32_t* ta, const uint16_t* tb, const uint32_t* off,
-                                        uint16_t* inv, uint32_t osh) {
-  T xn[33][D];
-  for (uint32_t q = l0; q < l1; ++q)
-    interior_update<T, D, KK, INTEG>(P, m, q, l0, l1, ord, xs, id_l[ord[q]], xn[q - l0]);
-  for (uint32_t q = l0; q < l1; ++q) {
-    const uint32_t e = ord[q];
-    check_finite<T, D>(xn[q - l0], P, id_l[e], m);
-#pragma unroll
-    for (int c = 0; c < D; ++c) xs.at(c, e) = xn[q - l0][c];
-    inv[off[ta[e] >> osh] + tb[e]] = (uint16_t)e;
-  }
-}
-
-// Bucket step for 2 < p <= 32 with the compact footprint of bucket_pair3_kernel
-// (packed u16 sub-digit counters, register items through the sort, three
-// 256-thread CTAs per SM) and the lane-group batch update of
-// bucket_fused_kernel.
-template <typename T, int D, int KK, int INTEG, int BLOCK, int ITEMS>
-static __global__ void __launch_bounds__(BLOCK, 3) bucket_group3_kernel(const __grid_constant__ DevParams P, State<T, D> src,
-                                                                   uint32_t scap,
-                                                                   const uint32_t* __restrict__ S,
-                                                                   const __grid_constant__ OutDst<T, D> dst, uint32_t dcap,
-                                                                   uint32_t* __restrict__ cur_next) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  RBM_PROF_BEGIN(P);
-  const uint32_t b = blockIdx.x;
-  const uint32_t s0 = S[b], n = S[b + 1] - s0, sb = b * scap;
-  if (n == 0) return;
-  const uint32_t nsb = 1u << P.SB;
-  const uint32_t nout = 1u << P.b1;
-  // sub-digit counts and offsets as packed u16 pairs (bucket sizes < 2^16);
-  // the same words later hold the <= 1024 output digit counts / offsets
-  const uint32_t ncw = (nsb / 2 > nout) ? nsb / 2 : nout;
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw);
-  uint32_t* off = cnt + ncw;
-  uint32_t* gbase = off + ncw;
-  uint32_t* wsum = gbase + nout;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);
-  const uint32_t cap = P.cap;
-  const uint32_t m = (uint32_t)*P.step;
-  for (uint32_t i = threadIdx.x; i < ncw / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
-  if (n > cap) {  // oversized bucket: the global-scratch path with its own 8-bit counters
-    __shared__ uint32_t bigc[2 * 256 + 64];
-    __syncthreads();
-    fused_big_path<T, D, KK, INTEG, BLOCK>(P, src, dst, cur_next, s0, sb, n, m, dcap, bigc, bigc + 256, bigc + 512);
-    return;
-  }
-  unsigned char* p = reinterpret_cast<unsigned char*>(bar + 2);
-  uint32_t* id_l = reinterpret_cast<uint32_t*>(p);
-  p += (size_t)(cap + 8) * 4;
-  uint32_t* key_l = reinterpret_cast<uint32_t*>(p);  // key_m by e; then key_{m+1} by e
-  p += (size_t)(cap + 8) * 4;
-  const uint32_t xst = (uint32_t)((((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15) / sizeof(T));
-  T* xr = reinterpret_cast<T*>(p);
-  p += (size_t)D * xst * sizeof(T);
-  uint32_t* ks = reinterpret_cast<uint32_t*>(p);   // composites (sort); then tb | inv (u16 each)
-  uint16_t* tb = reinterpret_cast<uint16_t*>(ks);
-  uint16_t* inv = tb + cap;
-  uint32_t* ta = key_l;
-  uint16_t* ord = reinterpret_cast<uint16_t*>(ks + cap);
-  load_bucket<T, D>(src, sb, n, id_l, key_l, xr, xst, bar);
-  __syncthreads();
-  mbar_wait(bar, 0);
-  RBM_PROF(P, 0);
-  const SX<T> xs{xr, xst};
-
-  // 1-3. exact (key, id) sort: counting sort on SB sub-digit bits + rank in sub-bucket
-  const uint32_t shsb = 32u - P.B - P.SB;
-  const uint32_t lowmask = (P.lowbits >= 32u) ? 0xffffffffu : ((1u << P.lowbits) - 1u);
-  uint32_t rc[ITEMS], rs[ITEMS];
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    const uint32_t e = k * BLOCK + threadIdx.x;
-    if (e < n) {
-      const uint32_t key = key_l[e];
-      const uint32_t sd = (key >> shsb) & (nsb - 1u);
-      rc[k] = ((key & lowmask) << P.idbits) | id_l[e];
-      const uint32_t sh16 = (sd & 1u) << 4;
-      rs[k] = (sd << 16) | ((atomicAdd(&cnt[sd >> 1], 1u << sh16) >> sh16) & 0xffffu);
-    }
-  }
-  __syncthreads();
-  RBM_PROF(P, 1);
-  block_excl_scan_u16x2<BLOCK>(cnt, off, nsb / 2, wsum);
-  RBM_PROF(P, 2);
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    const uint32_t e = k * BLOCK + threadIdx.x;
-    if (e < n) {
-      const uint32_t sd = rs[k] >> 16, sh16 = (sd & 1u) << 4;
-      const uint32_t a = (off[sd >> 1] >> sh16) & 0xffffu, c = (cnt[sd >> 1] >> sh16) & 0xffffu;
-      ks[a + (rs[k] & 0xffffu)] = rc[k];
-      rs[k] = (a << 16) | c;  // sub-bucket start and size, for the rank below
-    }
-  }
-  __syncthreads();
-  RBM_PROF(P, 3);
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    const uint32_t e = k * BLOCK + threadIdx.x;
-    if (e < n) {
-      const uint32_t a = rs[k] >> 16, c = rs[k] & 0xffffu;
-      uint32_t r = a;
-      if (c > 1) {  // sub-buckets hold ~1 element: a short predicated scan
-#pragma unroll
-        for (uint32_t i = 0; i < 6; ++i)
-          if (i < c) r += (ks[a + i] < rc[k]) ? 1u : 0u;
-        // more than 6 (probability ~6e-4 per element): a plain loop, not
-        // unrolled, so warps that never take it pay no loop prologue
-#pragma unroll 1
-        for (uint32_t i = 6; i < c; ++i) r += (ks[a + i] < rc[k]) ? 1u : 0u;
-      }
-      ord[r] = (uint16_t)e;
-    }
-  }
-  // the packed sub-digit counters are dead: they become the output digit counts
-  for (uint32_t i = threadIdx.x; i < nout / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
-  __syncthreads();
-  RBM_PROF(P, 4);
-  // interior batches [kfirst, klast) of this bucket (as bucket_fused_kernel);
-  // positions [0, head) and [tail, n) belong to straddling batches
-  uint32_t kfirst = batch_index(s0, P);
-  if (kfirst * P.p < s0) ++kfirst;
-  uint32_t klast;
-  {
-    const uint32_t kl = batch_index(s0 + n - 1, P);
-    klast = (batch_end(kl, P) <= s0 + n) ? kl + 1 : kl;
-  }
-  const uint32_t head = (kfirst < klast) ? kfirst * P.p - s0 : n;
-  const uint32_t tail = (kfirst < klast) ? batch_end(klast - 1, P) - s0 : n;
-  const uint32_t osh = 32u - P.b1;
-  if (P.dbg_order)
-    for (uint32_t q = threadIdx.x; q < n; q += BLOCK) P.dbg_order[s0 + q] = id_l[ord[q]];
-  RBM_PROF(P, 5);
-  // 4. output partition first (key_{m+1} depends on the id only): digit and
-  //    rank of every interior member; ks is dead: tb = rank by e
-  // keys and ranks of lane-group members are computed in the batch loop
-  // below; here only those of a batch larger than the lane group
-  const uint32_t G = P.group;
-  const uint32_t lb0 = (klast > kfirst) ? (klast - 1) * P.p - s0 : 0u;
-  const uint32_t lb1 = (klast > kfirst) ? batch_end(klast - 1, P) - s0 : 0u;
-  const bool big = lb1 - lb0 > G;
-  if (big)
-    for (uint32_t q = lb0 + threadIdx.x; q < lb1; q += BLOCK) {
-      const uint32_t e = ord[q];
-      const uint32_t kn = shuffle_key(P, id_l[e], m + 1);
-      ta[e] = kn;
-      tb[e] = (uint16_t)atomicAdd(&cnt[kn >> osh], 1u);
-    }
-  // straddlers: unchanged, to their sorted places in the own gapped range
-  for (uint32_t t = threadIdx.x; t < head + (n - tail); t += BLOCK) {
-    const uint32_t q = t < head ? t : tail + (t - head);
-    const uint32_t e = ord[q];
-    src.id[sb + q] = id_l[e];
-#pragma unroll
-    for (int c = 0; c < D; ++c) src.x[c][sb + q] = xs.at(c, e);
-  }
-  RBM_PROF(P, 8);
-  // 5. Eq. (2.2) + update in place: one lane group of G = P.group lanes per
-  //    batch, each pair evaluated once in the canonical rotation order
-  //    (batch_force); staging index of each member
-  {
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t gpw = 32u / G, gi = lane / G, li = lane & (G - 1);
-    const uint32_t stride = (BLOCK / 32) * gpw;
-    for (uint32_t kb = kfirst + warp * gpw; kb < klast; kb += stride) {  // warp-uniform
-      const uint32_t k = kb + gi;
-      const bool valid = k < klast;
-      const uint32_t l0 = valid ? k * P.p - s0 : 0;
-      const uint32_t sz = valid ? batch_end(k, P) - s0 - l0 : 0;
-      const bool act = valid && sz <= G && li < sz;
-      const uint32_t e = act ? ord[l0 + li] : 0u;
-      T xi[D];
-#pragma unroll
-      for (int c = 0; c < D; ++c) xi[c] = act ? xs.at(c, e) : T(0);
-      const uint32_t id = act ? id_l[e] : 0u;
-      T f[D];
-#pragma unroll
-      for (int c = 0; c < D; ++c) f[c] = T(0);
-      for (uint32_t o = 1; o <= G / 2; ++o) {
-        const uint32_t jp = (li + o) & (G - 1), jm = (li - o) & (G - 1);
-        T xj[D], t[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) xj[c] = __shfl_sync(0xffffffffu, xi[c], (int)jp, (int)G);
-        if (act && jp < sz) {
-          pair_term<T, D, KK, INTEG>(xi, xj, t, P);
-#pragma unroll
-          for (int c = 0; c < D; ++c) f[c] = add_rn(f[c], t[c]);
-        } else {
-#pragma unroll
-          for (int c = 0; c < D; ++c) t[c] = T(0);
-        }
-        if (o < G / 2) {  // warp-uniform
-#pragma unroll
-          for (int c = 0; c < (INTEG == 2 ? 1 : D); ++c) {
-            const T r = __shfl_sync(0xffffffffu, t[c], (int)jm, (int)G);
-            if (act && jm < sz) f[c] = sub_rn(f[c], r);
-          }
-        }
-      }
-      if (act) {
-        T z[D], xn[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) z[c] = T(0);
-        if (P.has_noise) Normals<T, D>::get(P, id, m, TAG_NOISE, z);
-        const T inv_b = batch_inv<T>(P, sz);
-#pragma unroll
-        for (int c = 0; c < D; ++c) f[c] *= inv_b;
-        member_update<T, D, INTEG>(xi, f, z, xn, P, P.verlet_start != 0);
-        check_finite<T, D>(xn, P, id, m);
-#pragma unroll
-        for (int c = 0; c < D; ++c) xs.at(c, e) = xn[c];
-        const uint32_t kn = shuffle_key(P, id, m + 1);
-        ta[e] = kn;
-        tb[e] = (uint16_t)atomicAdd(&cnt[kn >> osh], 1u);
-      }
-    }
-  }
-  __syncthreads();
-  constexpr int NRES = (1024 + BLOCK - 1) / BLOCK;
-  uint32_t gres[NRES];
-#pragma unroll
-  for (int r = 0; r < NRES; ++r) {
-    const uint32_t i = threadIdx.x + r * BLOCK;
-    const uint32_t h = i < nout ? cnt[i] : 0u;
-    gres[r] = h ? atomicAdd(&cur_next[(size_t)out_seg(P, i, blockIdx.x) * CUR1_STRIDE], h) : 0u;
-  }
-  const uint32_t total = block_excl_scan4<BLOCK>(cnt, off, nout, wsum);
-  for (uint32_t q = head + threadIdx.x; q < tail; q += BLOCK) {
-    const uint32_t e = ord[q];
-    inv[off[ta[e] >> osh] + tb[e]] = (uint16_t)e;
-  }
-  // a batch larger than the lane group (p a power of two and N mod p = 1: the
-  // last batch has p + 1 members): one thread, out of line
-  if (threadIdx.x == 0 && big) group3_big<T, D, KK, INTEG>(P, m, lb0, lb1, ord, xs, id_l, ta, tb, off, inv, osh);
-#pragma unroll
-  for (int r = 0; r < NRES; ++r)  // gbase[d] - off[d]: output position j goes to slot gbase[dg] + j
-    if (threadIdx.x + r * BLOCK < nout) gbase[threadIdx.x + r * BLOCK] = gres[r] - off[threadIdx.x + r * BLOCK];
-  __syncthreads();
-  RBM_PROF(P, 6);
-  // 6. staged slots -> coalesced runs of the step-(m+1) pass-1 buckets
-  for (uint32_t j = threadIdx.x; j < total; j += BLOCK) {
-    const uint32_t e = inv[j];
-    const uint32_t kn = ta[e];
-    const uint32_t dg = kn >> osh;
-    const uint32_t slot = gbase[dg] + j;
-    if (slot >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
-    T xo[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c) xo[c] = xs.at(c, e);
-    out_put<T, D>(dst, out_seg(P, dg, blockIdx.x), dcap, slot, id_l[e], kn, xo);
-  }
-  RBM_PROF(P, 7);
-  if (P.prof && threadIdx.x == 0) atomicAdd(&P.prof[63], 1ull);
-}
-
-// -------------------------------- persistent fused bucket step, p = 2
-// Same contract and arithmetic as bucket_pair_kernel, restructured for the
-// SM: one CTA per SM loops over buckets b = blockIdx.x, += gridDim.x with the
-// TMA loads double-buffered (bucket b + gridDim.x is in flight while b is
-// sorted and stepped), so neither the load latency nor a per-bucket launch
-// prologue is exposed.
-template <typename T, int D> __host__ __device__ constexpr size_t stage_bytes(uint32_t cap) {
-  return ((size_t)(cap + 8) * 8 + (size_t)D * (((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15) + 127) &
-         ~(size_t)127;
-}
-template <typename T, int D> __host__ __device__ constexpr size_t persist_smem_bytes(uint32_t cap,
-                                                                                    uint32_t SB) {
-  return (((size_t)(2 * (SB > 10 ? (1u << SB) : 1024u) + 1024 + 64) * 4 + 16 + 127) & ~(size_t)127)
-         + 2 * stage_bytes<T, D>(cap)                      // two TMA stages: ids, keys, x
-         + (size_t)cap * 4                                 // composites -> digit|slot
-         + (((size_t)cap * 4 + 15) & ~(size_t)15);         // ord, inv (u16)
-}
-
-// thread 0: TMA loads of one bucket into a stage; always one arrival on bar
-// (expect_tx 0 when nothing is loaded), so stage phases advance per use
-template <typename T, int D>
-__device__ __forceinline__ void stage_load(State<T, D> src, uint32_t sb, uint32_t n, bool load,
-                                           unsigned char* stg, uint32_t cap, uint64_t* bar, uint64_t pol) {
-  uint32_t* id_s = reinterpret_cast<uint32_t*>(stg);
-  uint32_t* key_s = id_s + cap + 8;
-  T* x_s = reinterpret_cast<T*>(key_s + cap + 8);
-  const uint32_t xst = (uint32_t)((((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15) / sizeof(T));
-  constexpr uint32_t AX = 16 / sizeof(T);
-  const uint32_t bytes_i = load ? ((n + 3) & ~3u) * 4 : 0u;
-  const uint32_t bytes_x = load ? ((n + AX - 1) & ~(AX - 1)) * (uint32_t)sizeof(T) : 0u;
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes before async overwrite
-  mbar_expect_tx(bar, 2 * bytes_i + D * bytes_x);
-  if (load && n) {
-    bulk_g2s_stream(id_s, src.id + sb, bytes_i, bar, pol);
-    bulk_g2s_stream(key_s, src.key + sb, bytes_i, bar, pol);
-#pragma unroll
-    for (int c = 0; c < D; ++c) bulk_g2s_stream(x_s + (size_t)c * xst, src.x[c] + sb, bytes_x, bar, pol);
-  }
-}
-
-template <typename T, int D, int KK, int INTEG, int BLOCK, int ITEMS>
-static __global__ void __launch_bounds__(BLOCK, 1) pair_persist_kernel(const __grid_constant__ DevParams P,
-                                                                       State<T, D> src, uint32_t scap,
-                                                                       const uint32_t* __restrict__ S,
-                                                                       const __grid_constant__ OutDst<T, D> dst, uint32_t dcap,
-                                                                       uint32_t* __restrict__ cur_next) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const uint32_t nsb = 1u << P.SB;
-  const uint32_t ncnt = nsb > 1024u ? nsb : 1024u;
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw);
-  uint32_t* off = cnt + ncnt;
-  uint32_t* gbase = off + ncnt;
-  uint32_t* wsum = gbase + 1024;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);
-  const uint32_t cap = P.cap;
-  unsigned char* stg0 = smem_raw + (((size_t)(2 * ncnt + 1024 + 64) * 4 + 16 + 127) & ~(size_t)127);
-  const size_t SBY = stage_bytes<T, D>(cap);
-  uint32_t* ks = reinterpret_cast<uint32_t*>(stg0 + 2 * SBY);  // composites; then digit<<16|slot
-  uint32_t* tb = ks;
-  uint16_t* ord = reinterpret_cast<uint16_t*>(ks + cap);
-  uint16_t* inv = ord + cap;
-  const uint32_t xst = (uint32_t)((((size_t)(cap + 8) * sizeof(T) + 15) & ~(size_t)15) / sizeof(T));
-  const uint32_t m = (uint32_t)*P.step;
-  const uint32_t nb = P.nbuckets;
-  const uint32_t tid = threadIdx.x;
-  uint64_t pol = 0;
-  if (tid == 0) {
-    pol = l2_evict_first_policy();
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-  }
-  __syncthreads();
-  if (tid == 0 && blockIdx.x < nb) {
-    const uint32_t b = blockIdx.x, n = S[b + 1] - S[b];
-    stage_load<T, D>(src, b * scap, n, n <= cap, stg0, cap, &bar[0], pol);
-  }
-  uint32_t phase = 0;  // bit s = parity of stage s's next completion
-  const uint32_t shsb = 32u - P.B - P.SB;
-  const uint32_t lowmask = (P.lowbits >= 32u) ? 0xffffffffu : ((1u << P.lowbits) - 1u);
-  const uint32_t N = (uint32_t)P.n;
-  const uint32_t pend = (N & 1u) ? N - 3u : N;
-  const uint32_t osh = 32u - P.b1;
-  const uint32_t nout = 1u << P.b1;
-  uint32_t it = 0;
-  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x, ++it) {
-    const uint32_t s = it & 1u;
-    const uint32_t bn = b + gridDim.x;
-    if (tid == 0 && bn < nb) {  // prefetch the next bucket into the other stage
-      const uint32_t nn = S[bn + 1] - S[bn];
-      stage_load<T, D>(src, bn * scap, nn, nn <= cap, stg0 + (s ^ 1u) * SBY, cap, &bar[s ^ 1u], pol);
-    }
-    const uint32_t s0 = S[b], n = S[b + 1] - s0, sb = b * scap;
-    unsigned char* stg = stg0 + s * SBY;
-    uint32_t* id_l = reinterpret_cast<uint32_t*>(stg);
-    uint32_t* key_l = id_l + cap + 8;  // key_m by e; then key_{m+1} by e
-    uint32_t* ta = key_l;
-    const SX<T> xs{reinterpret_cast<T*>(key_l + cap + 8), xst};
-    mbar_wait(&bar[s], (phase >> s) & 1u);
-    phase ^= 1u << s;
-    if (n == 0) {  // keep thread 0 within one stage phase of the others
-      __syncthreads();
-      continue;
-    }
-    for (uint32_t i = tid; i < nsb; i += BLOCK) cnt[i] = 0;
-    if (n > cap) {
-      __syncthreads();
-      fused_big_path<T, D, KK, INTEG, BLOCK>(P, src, dst, cur_next, s0, sb, n, m, dcap, cnt, off, wsum);
-      __syncthreads();
-      continue;
-    }
-    __syncthreads();
-    // 1-3. exact (key, id) sort: counting sort on SB sub-digit bits + rank in sub-bucket
-    uint32_t rc[ITEMS], rs[ITEMS];
-#pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-      const uint32_t e = k * BLOCK + tid;
-      if (e < n) {
-        const uint32_t key = key_l[e];
-        const uint32_t sd = (key >> shsb) & (nsb - 1u);
-        rc[k] = ((key & lowmask) << P.idbits) | id_l[e];
-        rs[k] = (sd << 16) | atomicAdd(&cnt[sd], 1u);
-      }
-    }
-    __syncthreads();
-    for (uint32_t i = tid; i < nsb; i += BLOCK) off[i] = cnt[i];
-    __syncthreads();
-    block_excl_scan<BLOCK>(off, nsb, wsum);
-#pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-      const uint32_t e = k * BLOCK + tid;
-      if (e < n) ks[off[rs[k] >> 16] + (rs[k] & 0xffffu)] = rc[k];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-      const uint32_t e = k * BLOCK + tid;
-      if (e < n) {
-        const uint32_t sd = rs[k] >> 16;
-        const uint32_t a = off[sd], c = cnt[sd];
-        uint32_t r = a;
-        for (uint32_t i = a; i < a + c; ++i) r += (ks[i] < rc[k]) ? 1u : 0u;
-        ord[r] = (uint16_t)e;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {  // ks is dead: reuse as digit|slot (straddlers keep ~0)
-      const uint32_t e = k * BLOCK + tid;
-      if (e < n) tb[e] = 0xffffffffu;
-    }
-    for (uint32_t i = tid; i < nout; i += BLOCK) cnt[i] = 0;
-    if (P.dbg_order)
-      for (uint32_t q = tid; q < n; q += BLOCK) P.dbg_order[s0 + q] = id_l[ord[q]];
-    // interior pairs: even global starts in [s0, end), end excludes a final triple (N odd)
-    const uint32_t head = s0 & 1u;
-    const uint32_t lim = (min(s0 + n, pend) > s0) ? min(s0 + n, pend) - s0 : 0u;
-    const uint32_t npairs = (lim > head) ? (lim - head) / 2 : 0u;
-    const uint32_t covered = head + 2 * npairs;
-    const bool triple = (N & 1u) && (pend >= s0) && (N <= s0 + n);
-    __syncthreads();
-    // straddlers: unchanged, to their sorted places in the own gapped range
-    for (uint32_t q = tid; q < n; q += BLOCK) {
-      const bool in_triple = triple && (s0 + q >= pend);
-      if ((q < head || q >= covered) && !in_triple) {
-        const uint32_t e = ord[q];
-        src.id[sb + q] = id_l[e];
-#pragma unroll
-        for (int c = 0; c < D; ++c) src.x[c][sb + q] = xs.at(c, e);
-      }
-    }
-    // 4. one thread per pair
-    constexpr int PITEMS = (ITEMS + 1) / 2;
-#pragma unroll
-    for (int k = 0; k < PITEMS; ++k) {
-      const uint32_t j = k * BLOCK + tid;
-      if (j < npairs) {
-        const uint32_t q = head + 2 * j;
-        const uint32_t e0 = ord[q], e1 = ord[q + 1];
-        const uint32_t id0 = id_l[e0], id1 = id_l[e1];
-        T x0[D], x1[D], y0[D], y1[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) { x0[c] = xs.at(c, e0); x1[c] = xs.at(c, e1); }
-        pair_update<T, D, KK, INTEG>(P, m, x0, x1, id0, id1, y0, y1);
-        check_finite<T, D>(y0, P, id0, m);
-        check_finite<T, D>(y1, P, id1, m);
-        const uint32_t k0 = shuffle_key(P, id0, m + 1), k1 = shuffle_key(P, id1, m + 1);
-        ta[e0] = k0;
-        ta[e1] = k1;
-        tb[e0] = ((k0 >> osh) << 16) | atomicAdd(&cnt[k0 >> osh], 1u);
-        tb[e1] = ((k1 >> osh) << 16) | atomicAdd(&cnt[k1 >> osh], 1u);
-#pragma unroll
-        for (int c = 0; c < D; ++c) { xs.at(c, e0) = y0[c]; xs.at(c, e1) = y1[c]; }
-      }
-    }
-    if (triple && tid == 0)  // the remainder batch of size 3 (N odd), EM only
-      serial_batch<T, D, KK, INTEG>(P, m, pend - s0, n, ord, id_l, xs, ta, tb, cnt, osh);
-    __syncthreads();
-    fused_output<T, D, BLOCK>(P, dst, dcap, cur_next, n, id_l, ta, tb, xs, cnt, off, gbase, inv, wsum);
-    __syncthreads();  // stage s and the work arrays are free
   }
 }
 
@@ -2707,18 +1630,9 @@ template <typename T, int D>
 static __global__ void rbmr_pack_kernel(uint64_t n, State<T, D> st, T* __restrict__ xa) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
+    const Rec<T, D> r = ld_rec<T, D>(st.rec, (long long)i);  // id order: record i is id i
 #pragma unroll
-    for (int c = 0; c < 4; ++c) xa[i * 4 + c] = (c < D) ? st.x[c < D ? c : 0][i] : T(0);
-  }
-}
-
-template <typename T, int D>
-static __global__ void rbmr_unpack_kernel(uint64_t n, const T* __restrict__ xa, State<T, D> st) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    st.id[i] = (uint32_t)i;
-#pragma unroll
-    for (int c = 0; c < D; ++c) st.x[c][i] = xa[i * 4 + c];
+    for (int c = 0; c < 4; ++c) xa[i * 4 + c] = (c < D) ? r.x[c < D ? c : 0] : T(0);
   }
 }
 

@@ -132,7 +132,8 @@ def test_part_info_host_layout(R, G):
         info = PT.rbm_part_info_get(R.make_config(dict(cfg, world_size=G, rank=r)))
         st, ws = status_of(R, dict(cfg, world_size=G, rank=r))
         assert st == 0 and info.ws_bytes == ws
-        assert info.narrays == 2 + cfg["d"] and info.nseg % G == 0
+        # one exchanged array: the state records (id + d fp32 coordinates = 16 B)
+        assert info.narrays == 1 and info.elem_bytes[0] == 16 and info.nseg % G == 0
         regions = []
         for a in range(info.narrays):
             nb = G * info.chunk_elems * info.elem_bytes[a]
