@@ -50,9 +50,10 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="particles per GPU override")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
-                    help="partitioned mode: records stored into the peers' buffers over NVLink "
-                         "by the kernels (fused, CUDA IPC) or moved by NCCL all-to-all")
+    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl", "torch"],
+                    help="partitioned mode: the library's NCCL exchanges with records stored into the "
+                         "peers' buffers by the kernels (fused, CUDA IPC) or moved by an NCCL all-to-all "
+                         "(nccl); torch: the caller-exchange protocol over torch.distributed")
     ap.add_argument("--direct", action="store_true",
                     help="time the direct O(N^2) step (row f1) on the workload's model instead")
     ap.add_argument("--mode", default=None, choices=["partition", "ensemble"],
@@ -82,6 +83,12 @@ def elt(cfg):
     return 8 if cfg["dtype"] == "f64" else 4
 
 
+def rec_bytes(cfg):
+    """Bytes of one state record {id, [key,] x} (RecL in csrc/rbm_device.cuh)."""
+    raw = 4 + cfg["d"] * elt(cfg)
+    return 8 if raw <= 8 else (16 if raw <= 16 else 32)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -102,15 +109,18 @@ def alg_bytes(name: str, cfg: dict) -> float:
     return {"bucket_step": per, "rbmr_apply": per}.get(name, 0.0)
 
 
-def design_bytes(name: str, cfg: dict, prefix_bits: int) -> float:
-    """Bytes per launch THIS design must move: the
-    records it reads and writes once (id, carried key, d coordinates on the
-    gapped-bucket path).  Reported beside the algorithmic figure so that
-    traffic-inflating designs cannot hide (8(d) "useful GB/s")."""
+def design_bytes(name: str, cfg: dict, layout) -> float:
+    """Bytes per launch THIS design must move: one read
+    and one write of the RS-byte state record per particle, plus the 4-byte
+    side key pass 2 writes and the bucket step reads when the record has no
+    room for it (2-pass layouts).  Reported beside the algorithmic figure so
+    that traffic-inflating designs cannot hide (8(d) "useful GB/s")."""
     n = cfg["n"]
-    R = (8 if prefix_bits > 0 else 4) + cfg["d"] * elt(cfg)
+    R = rec_bytes(cfg)
+    keyed = 8 + cfg["d"] * elt(cfg) <= R
+    side = 4.0 if (not keyed and layout[1] == 2) else 0.0
     rbmr = n * (4 * elt(cfg) + 4 * elt(cfg) + 4 + 4 + 8)
-    return {"scatter_sub": 2.0 * R * n, "bucket_step": 2.0 * R * n,
+    return {"split": (2.0 * R + side) * n, "bucket_step": (2.0 * R + side) * n,
             "rbmr_batch": float(rbmr)}.get(name, 0.0)
 
 
@@ -271,24 +281,31 @@ def bench_direct(args, cfg, dev, local):
 
 def bench_partition(args, cfg, world, rank, local, dev, barrier, max_over_ranks):
     """One global system of world x n particles split by key range over the
-    ranks; exchanges over torch.distributed (NCCL/NVLink)."""
+    ranks.  Default: the library runs the whole step (kernels and
+    NCCL exchanges in rbm_run, CUDA-graph replayed; records stored into the
+    peers' buffers over NVLink when every rank could map them).
+    --exchange torch: the caller-exchange protocol over torch.distributed."""
     import torch
 
     from paper_1812_10575_b200 import partition as PT
     K = args.steps
     gcfg = dict(cfg, n=cfg["n"] * world, replica=0)
-    ps = PT.PartitionedRBM(gcfg, world, [rank], PT.DistExchange(), device=dev)
-    exchange = "nccl"
-    if args.exchange == "fused" and world <= 8:
-        if ps.enable_fused():  # collective; all ranks agree
-            exchange = "fused"
-        elif rank == 0:
-            print("fused exchange unavailable (peer mapping); using the NCCL all-to-all", file=sys.stderr)
-    stream = ps.systems[0].stream
+    if args.exchange == "torch":
+        ps = PT.PartitionedRBM(gcfg, world, [rank], PT.DistExchange(), device=dev)
+        exchange = "torch.distributed all-to-all (caller exchanges)"
+        if world <= 8 and ps.enable_fused():
+            exchange = "torch.distributed counts/halo, records stored into peer buffers by the kernels"
+        stream, launches = ps.systems[0].stream, ps.systems[0].launches_per_step
+    else:
+        ps = PT.CommPartitionedRBM(gcfg, world, rank, device=dev, fused=(args.exchange == "fused"))
+        exchange = ("library NCCL counts/halo, records stored into peer buffers by the kernels over NVLink"
+                    if ps.fused else "library NCCL all-to-all of the records")
+        stream, launches = ps.stream, ps.launches_per_step
     clk = Clocks(local)
     clk.start()
     time.sleep(0.3)
     ps.run(args.warmup)
+    ps.run(8)  # untimed: captures the CUDA graph of 8 steps the timed run replays
     ps.sync()
     barrier()
     torch.cuda.synchronize()
@@ -302,16 +319,21 @@ def bench_partition(args, cfg, world, rank, local, dev, barrier, max_over_ranks)
     ms = max_over_ranks(e0.elapsed_time(e1))
     ps.sync()
     value = gcfg["n"] * K / (ms / 1e3)
+    # NVLink bytes each rank sends per step: the records leaving it (R B each,
+    # (G-1)/G of its particles on average) + counts + halo
+    R = rec_bytes(cfg)
+    nvl = cfg["n"] * (world - 1) / world * R / (ms / K / 1e3) / 1e9
     line = {"metric": "particle-steps/s", "value": value, "unit": "particle-steps/s",
             "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": ms / K,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": cfg["dtype"], "data": "synthetic (Philox init from seed, BASELINE.json config)",
             "config": dict(config_dict(args, cfg, world), n_total=gcfg["n"],
-                           multi_gpu="partitioned single system (key-range split, halo; records "
-                                     + ("stored into peer buffers by the kernels over NVLink"
-                                        if exchange == "fused" else "moved by NCCL all-to-all") + ")"),
+                           multi_gpu="partitioned single system (key-range split, halo; " + exchange + ")"),
+            "nvlink": {"records_gbs_per_gpu": nvl, "record_bytes": R,
+                       "peak_gbs_per_direction": 770.0, "frac": nvl / 770.0,
+                       "note": "bytes leaving each GPU per step / step time; peak = measured peer copy per direction (B200_PROFILING.md)"},
             "roofline": None, "clocks": clocks,
-            "gpu_launches": ps.systems[0].launches_per_step * K, "e2e": None, "cpu_baseline": None,
+            "gpu_launches": launches * K, "e2e": None, "cpu_baseline": None,
             "note": "per-kernel roofline and e2e are reported by the 1-GPU run"}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -363,8 +385,9 @@ def main():
     clk.start()
     time.sleep(0.3)
     # warm-up right before the timed region (no idle gap: clocks stay up); it
-    # also captures the CUDA graphs rbm_run replays
     s.run(args.warmup)
+    if s.layout[0] > 0 and args.steps >= 8:
+        s.run(8)  # untimed: captures the CUDA graph of 8 steps the timed run replays
     s.sync()
     # timed region: K steps through rbm_run (the user API, graph-replayed)
     barrier()
@@ -399,7 +422,7 @@ def main():
     avg_ms = per_kernel[name] / max(nrec, 1)
     peak, peak_kind = peaks()
     nbytes = alg_bytes(name, cfg)
-    dbytes = design_bytes(name, cfg, lay[0])
+    dbytes = design_bytes(name, cfg, lay)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -420,7 +443,7 @@ def main():
                 "note": "one CTA (resident) or one launch per level: bounded by barrier and launch latency, not by HBM or ALU throughput"}
     step_ms = ms / K
     shares = {k: round(v / max(nrec, 1), 4) for k, v in per_kernel.items()}
-    R = 4 + cfg["d"] * elt(cfg)
+    R = rec_bytes(cfg)
     useful = value / world * 2 * cfg["d"] * elt(cfg) / 1e9
 
     # end-to-end through the public API with host buffers (pinned)
@@ -467,6 +490,7 @@ def main():
             "hbm": {"useful_gbs_per_gpu": useful, "useful_frac": useful / peak, "record_bytes": R,
                     "note": "useful = particle-steps/s x 2 d s (state read+write once), whole step"},
             "timing": {"headline": "rbm_run graph replays, CUDA events on the library stream",
+                       "graph_capture_steps": 8 if (s.layout[0] > 0 and args.steps >= 8) else 0,
                        "eager_ms_per_step": eager_ms / K,
                        "per_kernel": "second window of K eager steps with library events around each kernel"},
             "layout": {"prefix_bits": s.layout[0], "passes": s.layout[1], "bucket_cap": s.layout[2]},

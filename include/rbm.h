@@ -67,7 +67,7 @@ typedef enum {
   RBM_ERR_UNSUPPORTED = 3,    /* valid request this build does not implement */
   RBM_ERR_WORKSPACE = 4,      /* workspace NULL, too small or misaligned (256 B) */
   RBM_ERR_CUDA = 5,           /* a CUDA runtime call failed (message has the code) */
-  RBM_ERR_NCCL = 6,           /* reserved: multi-process partition mode */
+  RBM_ERR_NCCL = 6,           /* NCCL not loadable, or an NCCL call failed (partitioned system) */
   RBM_ERR_NONFINITE = 7,      /* a non-finite position was produced; message names step and id */
   RBM_ERR_STATE = 8,          /* call out of order (e.g. step before init) */
   RBM_ERR_CAPACITY = 9        /* an internal per-bucket capacity was exceeded */
@@ -152,6 +152,13 @@ typedef struct {
   uint32_t state_form;   /* RBM_INTEG_VERLET: 0 = (x, v) at step0, 1 = (x_n, x_{n-1}) */
 } rbm_config;
 
+/* Partitioned single system with the library's own NCCL communicator
+ * (SURVEY.md 8(b)): rank 0 calls this, the caller broadcasts the 128 bytes
+ * to every rank (e.g. torch.distributed), and each rank passes them to
+ * rbm_init().  libnccl.so.2 is opened at first use.
+ * Errors: RBM_ERR_NCCL (NCCL not loadable, or ncclGetUniqueId failed). */
+rbm_status rbm_get_nccl_unique_id(void* out128);
+
 /* Bytes of device workspace rbm_init() needs for this config.
  * Errors: RBM_ERR_INVALID_ARG / RBM_ERR_UNKNOWN_KERNEL (same validation as rbm_init). */
 rbm_status rbm_workspace_size(const rbm_config* cfg, size_t* bytes);
@@ -160,7 +167,12 @@ rbm_status rbm_workspace_size(const rbm_config* cfg, size_t* bytes);
  * above, 256-byte aligned, owned by the caller and untouched by it until
  * rbm_destroy), and enqueue the initial data on `cuda_stream` (a cudaStream_t;
  * NULL = legacy default stream).  For RBM_INIT_USER the state is undefined
- * until rbm_set_state().  nccl_unique_id must be NULL (world_size == 1).
+ * until rbm_set_state().  nccl_unique_id: NULL on one GPU, and for a
+ * partitioned context whose exchanges the caller performs (rbm_part_*);
+ * otherwise the 128-byte id of rbm_get_nccl_unique_id(), identical on every
+ * rank: rbm_init then creates the library's NCCL communicator (collective:
+ * every rank must call it; RBM_ERR_NCCL on failure), and rbm_step / rbm_run /
+ * rbm_gather on the partitioned context run the exchanges themselves.
  * On success *out receives the context; the step index is cfg->step0. */
 rbm_status rbm_init(const rbm_config* cfg, void* ws, size_t ws_bytes, void* cuda_stream,
                     const void* nccl_unique_id, rbm_ctx** out);
@@ -179,14 +191,28 @@ rbm_status rbm_set_state(rbm_ctx* ctx, const void* x, uint32_t where);
  * order by rounding only. */
 rbm_status rbm_step(rbm_ctx* ctx);
 
-/* Enqueue nsteps steps as CUDA-graph replays (async); no host work per step. */
+/* Enqueue nsteps steps as CUDA-graph replays (async); no host work per step.
+ * Partitioned context with a communicator: one step = phase 1, the halo
+ * exchange (NCCL send/recv), phase 2, the counts all-gather and the records
+ * all-to-all (none in the fused mode), all on the context's stream; the
+ * steps are captured into CUDA graphs with their NCCL calls (eager launches
+ * if the capture is refused). */
 rbm_status rbm_run(rbm_ctx* ctx, uint64_t nsteps);
 
 /* Write positions of ids [id_begin, id_end) in id order, (id_end-id_begin)*d
  * scalars, to x_out (host or device per `where`).  Synchronises the stream,
  * then reports RBM_ERR_NONFINITE / RBM_ERR_CAPACITY if the device flagged
- * one; the data are written in any case. */
+ * one; the data are written in any case.  Partitioned context with a
+ * communicator: collective (every rank calls it and receives the whole range;
+ * an NCCL all-reduce of the disjoint rows). */
 rbm_status rbm_gather(rbm_ctx* ctx, uint64_t id_begin, uint64_t id_end, void* x_out, uint32_t where);
+
+/* This rank's particles, unordered: ids_out (device, >= n_local u32) and
+ * x_out (device, >= n_local*d scalars, row-major) in storage order; *count
+ * (host) = n_local (all N on one GPU, written in id order).  Not collective;
+ * synchronises the stream.  Sizing: a rank holds at most its workspace's
+ * slot count; the caller may allocate N rows. */
+rbm_status rbm_gather_local(rbm_ctx* ctx, uint32_t* ids_out, void* x_out, uint64_t* count);
 
 /* Synchronise the stream and check the device flags (see rbm_gather). */
 rbm_status rbm_sync(rbm_ctx* ctx);
@@ -241,10 +267,12 @@ rbm_status rbm_timing_end(rbm_ctx* ctx, double* ms_per_kernel, uint32_t* steps_r
  * t_r = O_r - (start of that batch) <= p-1 records of rank r-1 (the "halo").
  * The result is bit-identical to the same config on one GPU (world_size 1).
  *
- * The library runs every computation; the caller performs the three
- * exchanges between the phases (plumbing: torch.distributed over NCCL on
- * NVLink in bench.py / paper_1812_10575_b200.partition), using byte offsets
- * into the caller-owned workspace from rbm_part_info_get():
+ * With an NCCL id given to rbm_init, the library runs the whole step,
+ * exchanges included (rbm_step / rbm_run above).  Without one, the library
+ * runs every computation and the caller performs the three exchanges between
+ * the phases (plumbing: torch.distributed, or the one-process loopback used
+ * to test the G > 1 kernels on one GPU), using byte offsets into the
+ * caller-owned workspace from rbm_part_info_get():
  *   H  halo:     rank r's halo_send (halo_bytes) -> rank r+1's halo_recv
  *   C  counts:   all-gather of every rank's counts_send (nseg u32) into
  *                counts_all (world_size * nseg u32, rank-major)
@@ -254,7 +282,8 @@ rbm_status rbm_timing_end(rbm_ctx* ctx, double* ms_per_kernel, uint32_t* steps_r
  *                recv_off[a]
  * Protocol: rbm_init; rbm_part_prologue; C; R; then per step
  *   rbm_part_phase1; H; rbm_part_phase2; C; R.
- * rbm_step / rbm_run return RBM_ERR_STATE on a partitioned context.
+ * rbm_step / rbm_run return RBM_ERR_STATE on a partitioned context without
+ * a communicator.
  * rbm_init draws (or rbm_set_state takes, n0 rows) the particles with ids
  * [id0, id0 + n0) = [floor(N r/G), floor(N (r+1)/G)); rbm_gather writes, into
  * a DEVICE buffer, the positions of the ids in the range that this rank holds
@@ -291,6 +320,14 @@ rbm_status rbm_part_info_get(const rbm_config* cfg, rbm_part_info* out);
  * Exchanges H and C stay (C, an all-gather, also orders the steps).  Call
  * before rbm_part_prologue; all ranks must use the same config. */
 rbm_status rbm_part_set_peers(rbm_ctx* ctx, const uint64_t* peer_ws, uint32_t count);
+
+/* Fused exchange set up by the library (communicator required; collective,
+ * before the first step): each rank's workspace allocation is exported with
+ * cudaIpcGetMemHandle, the handles are all-gathered over NCCL and opened on
+ * every rank (peer access over NVLink / NVSwitch), then as rbm_part_set_peers.
+ * All ranks switch or none does (RBM_ERR_UNSUPPORTED: the NCCL all-to-all
+ * stays in use).  The mappings are closed by rbm_destroy. */
+rbm_status rbm_part_map_peers(rbm_ctx* ctx);
 
 /* Enqueue the partition of the initial state (id order) into the send
  * buckets; follow with exchanges C and R.  Once per context. */

@@ -43,9 +43,77 @@ rbm_status check_flags(rbm_ctx* c) {
   return RBM_OK;
 }
 
+#define NC(call)                                                                             \
+  do {                                                                                       \
+    ncclResult_t r_ = (call);                                                                \
+    if (r_ != ncclSuccess)                                                                   \
+      return fail(c, RBM_ERR_NCCL, "%s failed: %s", #call, nccl().GetErrorString(r_));       \
+  } while (0)
+
+// Exchanges C (counts all-gather) and R (records all-to-all, equal chunks;
+// none when the kernels store into the peers' buffers) of the partitioned
+// step, on the stream, over the library's communicator (include/rbm.h).
+rbm_status part_exchange_cr(rbm_ctx* c, cudaStream_t s) {
+  NcclApi& N = nccl();
+  const int G = c->cfg.world_size;
+  NC(N.AllGather(c->counts_send, c->counts_all, c->L.nseg(), ncclUint32, c->comm, s));
+  if (!c->fused) {
+    const size_t chunk = (size_t)(c->L.nseg() >> c->L.g) * c->L.cap1 * rec_bytes(c->cfg);
+    NC(N.GroupStart());
+    for (int j = 0; j < G; ++j) {
+      NC(N.Send(c->recbuf[1] + (size_t)j * chunk, chunk, ncclUint8, j, c->comm, s));
+      NC(N.Recv(c->recbuf[2] + (size_t)j * chunk, chunk, ncclUint8, j, c->comm, s));
+    }
+    NC(N.GroupEnd());
+  }
+  return RBM_OK;
+}
+
+// Exchange H: rank r's halo_send -> rank r+1's halo_recv (the <= p-1 trailing
+// records of the batch crossing O_{r+1}, the regroup is the
+// step's only synchronisation point)
+rbm_status part_exchange_h(rbm_ctx* c, cudaStream_t s) {
+  NcclApi& N = nccl();
+  const int G = c->cfg.world_size, r = c->cfg.rank;
+  const size_t hb = 16 + (size_t)HALO_MAX * rec_bytes(c->cfg);
+  NC(N.GroupStart());
+  if (r + 1 < G) NC(N.Send(c->halo_send, hb, ncclUint8, r + 1, c->comm, s));
+  if (r > 0) NC(N.Recv(c->halo_recv, hb, ncclUint8, r - 1, c->comm, s));
+  NC(N.GroupEnd());
+  return RBM_OK;
+}
+
+// one step of the partitioned system with the library's exchanges
+rbm_status part_step(rbm_ctx* c, cudaStream_t s) {
+  c->P.verlet_start = c->verlet_start ? 1u : 0u;
+  if (!c->partitioned) {
+    c->eng->part_prologue(*c, s);
+    if (rbm_status e = part_exchange_cr(c, s)) return e;
+  }
+  c->eng->part_phase1(*c, s);
+  if (rbm_status e = part_exchange_h(c, s)) return e;
+  c->eng->part_phase2(*c, s);
+  if (rbm_status e = part_exchange_cr(c, s)) return e;
+  c->verlet_start = false;
+  c->P.verlet_start = 0u;
+  CU(cudaGetLastError());
+  return RBM_OK;
+}
+
 }  // namespace rbmhost
 
 extern "C" {
+
+rbm_status rbm_get_nccl_unique_id(void* out128) {
+  rbm_ctx* c = nullptr;
+  if (!out128) return fail(c, RBM_ERR_INVALID_ARG, "out is NULL");
+  NcclApi& N = nccl();
+  if (!N.ok) return fail(c, RBM_ERR_NCCL, "%s", N.err.c_str());
+  ncclUniqueId id;
+  NC(N.GetUniqueId(&id));
+  std::memcpy(out128, &id, sizeof id);
+  return RBM_OK;
+}
 
 rbm_status rbm_workspace_size(const rbm_config* cfg, size_t* bytes) {
   rbm_status s = validate(cfg);
@@ -160,8 +228,8 @@ rbm_status rbm_init(const rbm_config* cfg, void* wsp, size_t ws_bytes, void* cud
   if (s) return s;
   if (!out) return fail(nullptr, RBM_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
-  if (nccl_unique_id)
-    return fail(nullptr, RBM_ERR_UNSUPPORTED, "nccl_unique_id must be NULL: the partition exchanges are the caller's (torch.distributed over NCCL)");
+  if (nccl_unique_id && cfg->world_size == 1)
+    return fail(nullptr, RBM_ERR_INVALID_ARG, "nccl_unique_id given for world_size 1");
   size_t need = 0;
   rbm_workspace_size(cfg, &need);
   if (!wsp || ws_bytes < need || (reinterpret_cast<uintptr_t>(wsp) & 255))
@@ -171,6 +239,21 @@ rbm_status rbm_init(const rbm_config* cfg, void* wsp, size_t ws_bytes, void* cud
   c->L = choose_layout(*cfg);
   c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
   s = init_impl(c.get(), cfg, wsp, ws_bytes);
+  if (!s && nccl_unique_id) {  // library-owned communicator: the exchanges run inside rbm_step / rbm_run
+    NcclApi& N = nccl();
+    if (!N.ok) {
+      s = fail(c.get(), RBM_ERR_NCCL, "%s", N.err.c_str());
+    } else {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_unique_id, sizeof id);
+      const ncclResult_t r = N.CommInitRank(&c->comm, cfg->world_size, id, cfg->rank);
+      if (r != ncclSuccess) {
+        c->comm = nullptr;
+        s = fail(c.get(), RBM_ERR_NCCL, "ncclCommInitRank(world %d, rank %d): %s", cfg->world_size, cfg->rank,
+                 N.GetErrorString(r));
+      }
+    }
+  }
   if (s) {
     g_err = c->err;
     if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
@@ -200,8 +283,8 @@ rbm_status rbm_set_state(rbm_ctx* c, const void* x, uint32_t where) {
 }
 
 static rbm_status not_partitioned(rbm_ctx* c) {
-  if (is_partitioned(c->cfg))
-    return fail(c, RBM_ERR_STATE, "partitioned context (world_size %d): step with rbm_part_phase1/2 and the exchanges", c->cfg.world_size);
+  if (is_partitioned(c->cfg) && !c->comm)
+    return fail(c, RBM_ERR_STATE, "partitioned context (world_size %d) without a communicator: step with rbm_part_phase1/2 and the exchanges, or pass an NCCL id to rbm_init", c->cfg.world_size);
   return RBM_OK;
 }
 
@@ -209,6 +292,13 @@ rbm_status rbm_step(rbm_ctx* c) {
   if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
   if (rbm_status e = not_partitioned(c)) return e;
   if (c->step + 1 >= (1ull << 32)) return fail(c, RBM_ERR_INVALID_ARG, "step index would exceed 2^32");
+  if (is_partitioned(c->cfg)) {
+    rbm_status s = part_step(c, c->stream);
+    c->P.dbg_order = nullptr;
+    if (s) return s;
+    ++c->step;
+    return RBM_OK;
+  }
   rbm_status s = enqueue_steps(c, c->stream, 1);
   c->P.dbg_order = nullptr;
   if (s) return s;
@@ -225,6 +315,42 @@ rbm_status rbm_run(rbm_ctx* c, uint64_t nsteps) {
   const uint32_t per = 8;  // even: every layout returns to the same (cur, parity)
   c->graph_steps = per;
   uint64_t done = 0;
+  if (is_partitioned(c->cfg)) {  // the library's exchanges, captured with the kernels when possible
+    if (!c->partitioned && nsteps > 0) {
+      if (rbm_status e = part_step(c, c->stream)) return e;
+      ++c->step;
+      --nsteps;
+    }
+    if (nsteps >= per && !c->timing && !c->verlet_start) {
+      const int slot = (int)(c->step & 1);
+      if (!c->graph[slot] && !c->graph_failed) {
+        const uint64_t step0 = c->step;
+        bool ok = cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        for (uint32_t i = 0; ok && i < per; ++i) { ok = part_step(c, c->cap_stream) == RBM_OK; ++c->step; }
+        c->step = step0;
+        cudaGraph_t g = nullptr;
+        const bool ended = cudaStreamEndCapture(c->cap_stream, &g) == cudaSuccess && g;
+        ok = ok && ended && cudaGraphInstantiate(&c->graph[slot], g, 0) == cudaSuccess;
+        if (g) cudaGraphDestroy(g);
+        if (!ok) {  // NCCL or the driver refused capture: eager steps from now on
+          c->graph[slot] = nullptr;
+          c->graph_failed = true;
+          cudaGetLastError();
+        }
+      }
+      if (c->graph[slot]) {
+        const uint64_t reps = nsteps / per;
+        for (uint64_t r = 0; r < reps; ++r) CU(cudaGraphLaunch(c->graph[slot], c->stream));
+        done = reps * per;
+      }
+    }
+    c->step += done;
+    for (uint64_t i = done; i < nsteps; ++i) {
+      if (rbm_status e = part_step(c, c->stream)) return e;
+      ++c->step;
+    }
+    return RBM_OK;
+  }
   if (c->cfg.scheme == RBM_SCHEME_RBM1 && c->L.B == 0) {  // resident: chunks of <= 4096 steps per launch
     while (nsteps > 0) {
       const uint32_t k = (uint32_t)std::min<uint64_t>(nsteps, 4096);
@@ -278,8 +404,25 @@ rbm_status rbm_gather(rbm_ctx* c, uint64_t id_begin, uint64_t id_end, void* x_ou
   if (!x_out) return fail(c, RBM_ERR_INVALID_ARG, "x_out is NULL");
   if (id_begin > id_end || id_end > c->cfg.n) return fail(c, RBM_ERR_INVALID_ARG, "bad id range [%llu,%llu)", (unsigned long long)id_begin, (unsigned long long)id_end);
   const size_t bytes = (id_end - id_begin) * c->cfg.d * elt_size(c->cfg);
+  if (is_partitioned(c->cfg) && c->comm) {  // collective: every rank receives the whole id range
+    void* dev = x_out;
+    if (where == RBM_MEM_HOST) {
+      CU(cudaMallocAsync(&dev, bytes ? bytes : 4, c->stream));
+    }
+    if (bytes) CU(cudaMemsetAsync(dev, 0, bytes, c->stream));
+    c->eng->gather(*c, id_begin, id_end, dev, c->stream);
+    CU(cudaGetLastError());
+    // disjoint rows: every other rank contributes zero bits, so the integer sum is exact
+    if (bytes) NC(nccl().AllReduce(dev, dev, bytes / 4, ncclUint32, ncclSum, c->comm, c->stream));
+    if (where == RBM_MEM_HOST) {
+      if (bytes) CU(cudaMemcpyAsync(x_out, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+      CU(cudaFreeAsync(dev, c->stream));
+    }
+    CU(cudaStreamSynchronize(c->stream));
+    return check_flags(c);
+  }
   if (where == RBM_MEM_HOST && is_partitioned(c->cfg))
-    return fail(c, RBM_ERR_UNSUPPORTED, "partitioned context: gather to device memory (each rank writes the ids it holds), then combine across ranks");
+    return fail(c, RBM_ERR_UNSUPPORTED, "partitioned context without a communicator: gather to device memory (each rank writes the ids it holds), then combine across ranks");
   if (where == RBM_MEM_HOST) {
     void* scratch = c->recbuf[c->cur ^ 1];
     c->eng->gather(*c, id_begin, id_end, scratch, c->stream);
@@ -452,6 +595,75 @@ rbm_status rbm_part_set_peers(rbm_ctx* c, const uint64_t* peer_ws, uint32_t coun
   return RBM_OK;
 }
 
+rbm_status rbm_part_map_peers(rbm_ctx* c) {
+  if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
+  if (!c->comm) return fail(c, RBM_ERR_STATE, "no communicator: pass an NCCL id to rbm_init (or map the peers yourself and call rbm_part_set_peers)");
+  if (c->partitioned) return fail(c, RBM_ERR_STATE, "map the peers before the first step");
+  const int G = c->cfg.world_size, r = c->cfg.rank;
+  if (G > MAXG_FUSED) return fail(c, RBM_ERR_UNSUPPORTED, "fused exchange supports world_size <= %d (one NVSwitch node)", MAXG_FUSED);
+  NcclApi& N = nccl();
+  struct Entry { cudaIpcMemHandle_t h; unsigned long long off; int ok; int pad; };
+  static_assert(sizeof(Entry) <= 128, "IPC entry");
+  Entry mine{};
+  mine.ok = 0;
+  unsigned long long base = 0;
+  size_t sz = 0;
+  if (N.MemGetAddressRange && N.MemGetAddressRange(&base, &sz, (unsigned long long)c->ws_base) == 0 &&
+      cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void*>(base)) == cudaSuccess) {
+    mine.ok = 1;
+    mine.off = (unsigned long long)c->ws_base - base;
+  }
+  cudaGetLastError();
+  unsigned char* all = c->xchg;  // G entries of 128 B
+  CU(cudaMemcpyAsync(all + (size_t)r * 128, &mine, sizeof mine, cudaMemcpyHostToDevice, c->stream));
+  NC(N.AllGather(all + (size_t)r * 128, all, 128, ncclUint8, c->comm, c->stream));
+  std::vector<unsigned char> host((size_t)G * 128);
+  CU(cudaMemcpyAsync(host.data(), all, host.size(), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  int ok = 1;
+  void* opened[MAXG_FUSED] = {};
+  for (int j = 0; j < G; ++j) {
+    Entry e;
+    std::memcpy(&e, host.data() + (size_t)j * 128, sizeof e);
+    if (!e.ok) { ok = 0; continue; }
+    if (j == r) continue;
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, e.h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) { ok = 0; cudaGetLastError(); continue; }
+    opened[j] = p;
+    c->peer_base[j] = reinterpret_cast<unsigned char*>(p) + e.off;
+  }
+  // every rank switches, or none
+  int* flag = reinterpret_cast<int*>(all);
+  CU(cudaMemcpyAsync(flag, &ok, 4, cudaMemcpyHostToDevice, c->stream));
+  NC(N.AllReduce(flag, flag, 1, ncclInt32, ncclMin, c->comm, c->stream));
+  CU(cudaMemcpyAsync(&ok, flag, 4, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  if (!ok) {
+    for (int j = 0; j < G; ++j)
+      if (opened[j]) cudaIpcCloseMemHandle(opened[j]);
+    return fail(c, RBM_ERR_UNSUPPORTED, "CUDA IPC mapping of the peers' workspaces failed on some rank; the NCCL all-to-all stays in use");
+  }
+  c->peer_base[r] = c->ws_base;
+  for (int j = 0; j < G; ++j) c->ipc_open[j] = opened[j];
+  c->fused = true;
+  return RBM_OK;
+}
+
+rbm_status rbm_gather_local(rbm_ctx* c, uint32_t* ids_out, void* x_out, uint64_t* count) {
+  if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
+  if (!ids_out || !x_out || !count) return fail(c, RBM_ERR_INVALID_ARG, "NULL output");
+  if (!is_partitioned(c->cfg)) {  // one GPU holds every id: written in id order
+    c->eng->gather(*c, 0, c->cfg.n, x_out, c->stream);
+    iota_kernel<<<grid_for(c->cfg.n, 256), 256, 0, c->stream>>>(ids_out, c->cfg.n);
+    *count = c->cfg.n;
+  } else {
+    *count = c->eng->gather_local(*c, ids_out, x_out, c->stream);
+  }
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(c->stream));
+  return check_flags(c);
+}
+
 rbm_status rbm_part_prologue(rbm_ctx* c) { return part_call(c, 0); }
 rbm_status rbm_part_phase1(rbm_ctx* c) { return part_call(c, 1); }
 rbm_status rbm_part_phase2(rbm_ctx* c) { return part_call(c, 2); }
@@ -559,6 +771,9 @@ rbm_status rbm_destroy(rbm_ctx* c) {
   }
   for (int i = 0; i < 4; ++i)
     if (c->graph[i]) cudaGraphExecDestroy(c->graph[i]);
+  for (int j = 0; j < MAXG_FUSED; ++j)
+    if (c->ipc_open[j]) cudaIpcCloseMemHandle(c->ipc_open[j]);
+  if (c->comm) nccl().CommDestroy(c->comm);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   delete c;

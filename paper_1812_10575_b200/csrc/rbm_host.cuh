@@ -18,6 +18,7 @@
 
 #include "../../include/rbm.h"
 #include "rbm_kernels.cuh"
+#include "rbm_nccl.cuh"
 
 using namespace rbm;
 
@@ -83,6 +84,9 @@ struct rbm_ctx {
   bool fused = false;                          // G9: outputs stored into the peers' receive buffers
   unsigned char* peer_base[MAXG_FUSED] = {};   // every rank's workspace base (peer-mapped)
   uint32_t *counts_send = nullptr, *counts_all = nullptr;
+  ncclComm_t comm = nullptr;                   // library-owned communicator (id given to rbm_init)
+  void* ipc_open[MAXG_FUSED] = {};             // peer allocations opened by rbm_part_map_peers
+  unsigned char* xchg = nullptr;               // device scratch: IPC handles, local-gather offsets
   unsigned char *halo_send = nullptr, *halo_recv = nullptr;
   // gapped-bucket pipeline.  cur1[q]: counts (cursors) of the buckets the
   // state of step m (q = m & 1) is partitioned into -- pass-1 buckets (2-pass)
@@ -111,6 +115,7 @@ struct rbm_ctx {
   int tile = 4096;
   cudaGraphExec_t graph[4] = {nullptr, nullptr, nullptr, nullptr};  // by (cur, m & 1)
   uint32_t graph_steps = 1;
+  bool graph_failed = false;  // stream capture refused (partitioned steps fall back to eager launches)
   // optional per-kernel CUDA-event timing (rbm_timing_begin/end)
   bool timing = false;
   std::vector<cudaEvent_t> ev;
@@ -341,6 +346,7 @@ inline void carve(rbm_ctx& c, Workspace& ws) {
     c.counts_all = ws.take<uint32_t>((size_t)k.world_size * c.L.nseg());
     c.halo_send = ws.take<unsigned char>(16 + (size_t)HALO_MAX * 32);
     c.halo_recv = ws.take<unsigned char>(16 + (size_t)HALO_MAX * 32);
+    c.xchg = ws.take<unsigned char>(std::max<size_t>((size_t)MAXG_FUSED * 128, ((size_t)MAX_SEG_SPLIT + 2) * 4));
   }
   c.big_claim = ws.take<uint32_t>(NBIG);
   if (c.L.b2) c.cur2 = ws.take<uint32_t>((size_t)c.L.nbuckets * CUR2_STRIDE);
@@ -393,6 +399,8 @@ struct EngineBase {
   virtual void part_prologue(rbm_ctx& c, cudaStream_t s) = 0;
   virtual void part_phase1(rbm_ctx& c, cudaStream_t s) = 0;
   virtual void part_phase2(rbm_ctx& c, cudaStream_t s) = 0;
+  // this rank's records, unordered (ids and positions, row-major); returns the count (syncs)
+  virtual uint64_t gather_local(rbm_ctx& c, uint32_t* ids, void* x, cudaStream_t s) = 0;
 };
 
 template <typename T, int D, int KK, int INTEG>
@@ -676,6 +684,22 @@ struct Engine final : EngineBase {
     c.mark(s);
     advance_kernel<<<1, 1, 0, s>>>(c.step_dev);
     c.mark(s);
+  }
+
+  uint64_t gather_local(rbm_ctx& c, uint32_t* ids, void* x, cudaStream_t s) override {
+    if (!is_partitioned(c.cfg) || !c.partitioned) {  // records in id order (this rank's initial ids)
+      gather_local_kernel<T, D><<<grid_for(c.n0, 256), 256, 0, s>>>(c.n0, st(c, 0), ids, reinterpret_cast<T*>(x));
+      return c.n0;
+    }
+    uint32_t* off = reinterpret_cast<uint32_t*>(c.xchg);
+    seg_offsets_kernel<<<1, 1024, 0, s>>>(c.P, c.counts_all, (uint32_t)c.cfg.world_size, (uint32_t)c.cfg.rank, off);
+    gather_local_part_kernel<T, D><<<grid_for((uint64_t)c.L.nseg() * c.L.cap1, 256), 256, 0, s>>>(
+        c.P, st(c, recv_buf(c, c.step)), c.L.cap1, c.counts_all, (uint32_t)c.cfg.world_size, (uint32_t)c.cfg.rank,
+        off, ids, reinterpret_cast<T*>(x));
+    uint32_t total = 0;
+    cudaMemcpyAsync(&total, off + c.L.nseg(), 4, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    return total;
   }
 
   // Algorithm 2 as written (row f2): draws, per-particle slot chains, levels

@@ -300,6 +300,11 @@ static __global__ void philox_test_kernel(const uint32_t* __restrict__ in, uint3
 
 static __global__ void advance_kernel(uint64_t* step) { *step += 1; }
 
+static __global__ void iota_kernel(uint32_t* out, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = (uint32_t)i;
+}
+
 // ------------------------------------------------------------ gapped layout
 // nb buckets of fixed capacity cap; bucket u holds cnt[u*cstride] records at
 // physical slots [u*cap, u*cap + cnt).  Cursor padding spreads the run-
@@ -1562,6 +1567,58 @@ static __global__ void gather_part_kernel(const __grid_constant__ DevParams P, S
 #pragma unroll
       for (int c = 0; c < D; ++c) out[(id - i0) * D + c] = r.x[c];
     }
+  }
+}
+
+// this rank's records as (ids, rows) in storage order (rbm_gather_local):
+// records in id order (before the first step) ...
+template <typename T, int D>
+static __global__ void gather_local_kernel(uint64_t n, State<T, D> st, uint32_t* __restrict__ ids,
+                                           T* __restrict__ out) {
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const Rec<T, D> r = ld_rec<T, D>(st.rec, (long long)q);
+    ids[q] = r.id;
+#pragma unroll
+    for (int c = 0; c < D; ++c) out[q * D + c] = r.x[c];
+  }
+}
+
+// ... or in the received segments of a partitioned rank: off[v] = exclusive
+// prefix of the segment counts (off[nseg] = total), one block
+static __global__ void __launch_bounds__(1024) seg_offsets_kernel(const __grid_constant__ DevParams P,
+                                                                  const uint32_t* __restrict__ M, uint32_t G,
+                                                                  uint32_t rank, uint32_t* off) {
+  __shared__ uint32_t a[MAX_SEG_SPLIT + 1];
+  __shared__ uint32_t ws[33];
+  const uint32_t nseg = (1u << P.b1) << P.segk, nls = nseg / G;
+  for (uint32_t v = threadIdx.x; v < nseg; v += blockDim.x) {
+    const uint32_t s = v / nls, j = v - s * nls;
+    a[v] = M[(size_t)s * nseg + rank * nls + j];
+  }
+  __syncthreads();
+  const uint32_t total = block_excl_scan<1024>(a, nseg, ws);
+  for (uint32_t v = threadIdx.x; v < nseg; v += blockDim.x) off[v] = a[v];
+  if (threadIdx.x == 0) off[nseg] = total;
+}
+
+template <typename T, int D>
+static __global__ void gather_local_part_kernel(const __grid_constant__ DevParams P, State<T, D> st, uint32_t cap1,
+                                                const uint32_t* __restrict__ M, uint32_t G, uint32_t rank,
+                                                const uint32_t* __restrict__ off, uint32_t* __restrict__ ids,
+                                                T* __restrict__ out) {
+  const uint32_t nseg = (1u << P.b1) << P.segk, nls = nseg / G;
+  const uint64_t total = (uint64_t)nseg * cap1;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < total;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = (uint32_t)(q / cap1), e = (uint32_t)(q - (uint64_t)v * cap1);
+    const uint32_t s = v / nls, j = v - s * nls;
+    if (e >= M[(size_t)s * nseg + rank * nls + j]) continue;
+    const Rec<T, D> r = ld_rec<T, D>(st.rec, (long long)q);
+    const uint64_t o = (uint64_t)off[v] + e;
+    ids[o] = r.id;
+#pragma unroll
+    for (int c = 0; c < D; ++c) out[o * D + c] = r.x[c];
   }
 }
 

@@ -1,20 +1,26 @@
 """Partitioned single system over G ranks.
 
-librbm.so does every computation of the step (include/rbm.h, "Partitioned
-single system"); this module is the plumbing around its three exchanges:
+The production path is CommPartitionedRBM: rbm_init receives an NCCL id and
+librbm.so runs the whole step -- kernels and NCCL exchanges, captured into
+CUDA graphs -- on one process per GPU; torch.distributed only broadcasts the
+id.  The rest of this module drives the caller-exchange protocol of the same
+library (rbm_part_* phases), used to test the G > 1 kernels without several
+GPUs.  The step's three exchanges:
 
     H  halo     rank r's halo_send -> rank r+1's halo_recv (<= p-1 records)
     C  counts   all-gather of counts_send (2^b1 u32 per rank) -> counts_all
-    R  records  all-to-all, equal chunks, of the 2+d exchanged arrays
+    R  records  all-to-all, equal chunks, of the state records
 
 Protocol per context: rbm_init; prologue; C; R; then per step
 phase1; H; phase2; C; R.
 
-Two interchangeable exchanges move the bytes, both on byte views of the
+Interchangeable caller exchanges move the bytes, on byte views of the
 caller-owned workspaces (offsets from rbm_part_info_get):
 
   DistExchange      one rank per process, torch.distributed (NCCL over
                     NVLink on B200; gloo for the CPU tests of this plumbing)
+  HostDistExchange  the same with the collectives on host copies (gloo with
+                    device workspaces): several processes on ONE device
   LoopbackExchange  all G ranks in one process on one device: plain device
                     copies, run in stream order (no kernel waits on another
                     rank), used to test the G > 1 kernels on one GPU
@@ -185,6 +191,97 @@ class DistExchange:
                 q.wait()
 
 
+class HostDistExchange(DistExchange):
+    """DistExchange whose collectives run on host copies (gloo with device
+    workspaces): the counts and the halo are staged through CPU tensors, so
+    every exchange is preceded by a stream synchronisation of this rank.  Used
+    to run the fused path's cross-process CUDA-IPC stores with several ranks
+    on ONE device (tests): no kernel ever waits on another rank's kernel."""
+
+    def counts_records(self, ranks):
+        (me,) = ranks
+        d = self.dist
+        G = int(me.info.world_size)
+        cs = me.counts_send.cpu()
+        out = [self.torch.empty_like(cs) for _ in range(G)]
+        d.all_gather(out, cs, group=self.group)
+        me.counts_all.copy_(self.torch.cat(out).to(me.counts_all.device))
+        if self.fused:
+            return
+        for a in range(me.info.narrays):
+            cb = me.chunk_bytes[a]
+            send = me.send[a].cpu()
+            recv = [self.torch.empty(cb, dtype=send.dtype) for _ in range(G)]
+            d.all_to_all(recv, list(send.split(cb)), group=self.group)
+            me.recv[a].copy_(self.torch.cat(recv).to(me.recv[a].device))
+
+    def halo(self, ranks):
+        (me,) = ranks
+        d, r, G = self.dist, me.rank, int(me.info.world_size)
+        if r + 1 < G:
+            d.send(me.halo_send.cpu(), r + 1, group=self.group)
+        if r > 0:
+            buf = self.torch.empty(me.halo_recv.numel(), dtype=me.halo_recv.dtype)
+            d.recv(buf, r - 1, group=self.group)
+            me.halo_recv.copy_(buf.to(me.halo_recv.device))
+
+    @property
+    def torch(self):
+        import torch
+        return torch
+
+
+class CommPartitionedRBM:
+    """One rank of a global RBM-1 system whose whole step -- kernels and the
+    NCCL exchanges -- runs inside librbm.so (rbm_init with an NCCL id; rbm_run
+    replays CUDA graphs of steps with their NCCL calls).  torch.distributed
+    only broadcasts the 128-byte id (plumbing).  fused=True maps the peers'
+    workspaces over CUDA IPC in the library (rbm_part_map_peers) so the bucket
+    step stores the records straight into their destination ranks; the NCCL
+    all-to-all is used if any rank cannot map."""
+
+    def __init__(self, cfg: dict, world_size: int, rank: int, device=None, fused: bool = True, group=None):
+        import torch.distributed as dist
+        obj = [R.rbm_get_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        self.cfg = dict(cfg, world_size=int(world_size), rank=int(rank))
+        self.system = R.RBM(self.cfg, device=device, nccl_id=obj[0])
+        self.fused = False
+        if fused and world_size <= 8:
+            try:
+                R.rbm_part_map_peers(self.system.ctx)
+                self.fused = True
+            except R.RbmError:
+                self.fused = False
+
+    def run(self, nsteps: int):
+        self.system.run(nsteps)
+
+    def step(self):
+        self.system.step()
+
+    def sync(self):
+        self.system.sync()
+
+    def gather(self, host: bool = False):
+        """Whole state in id order on every rank (collective)."""
+        return self.system.gather(host=host)
+
+    def gather_local(self):
+        return self.system.gather_local()
+
+    @property
+    def stream(self):
+        return self.system.stream
+
+    @property
+    def launches_per_step(self) -> int:
+        return self.system.launches_per_step
+
+    def close(self):
+        self.system.close()
+
+
 class PartitionedRBM:
     """One global RBM-1 system split over `world_size` ranks.
 
@@ -223,7 +320,8 @@ class PartitionedRBM:
         except Exception:
             ok = 0
         if isinstance(self.exchange, DistExchange):
-            t = torch.tensor([ok], dtype=torch.int32, device=self.device)
+            cpu = isinstance(self.exchange, HostDistExchange)
+            t = torch.tensor([ok], dtype=torch.int32, device="cpu" if cpu else self.device)
             self.exchange.dist.all_reduce(t, op=self.exchange.dist.ReduceOp.MIN, group=self.exchange.group)
             ok = int(t.item())
         if ok:

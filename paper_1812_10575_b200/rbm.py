@@ -14,7 +14,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "librbm.so")
+# RBM_LIB: an alternative in-tree build of the same library (design experiments)
+LIB_PATH = os.environ.get("RBM_LIB") or os.path.join(PKG, "librbm.so")
 
 RBM_ABI_VERSION = 1
 STATUS = {0: "RBM_OK", 1: "RBM_ERR_INVALID_ARG", 2: "RBM_ERR_UNKNOWN_KERNEL",
@@ -30,7 +31,7 @@ EXPORTS = ["rbm_workspace_size", "rbm_init", "rbm_set_state", "rbm_step", "rbm_r
            "rbm_debug_permutation", "rbm_debug_slots", "rbm_debug_philox", "rbm_last_error",
            "rbm_destroy", "rbm_kernel_name", "rbm_timing_begin", "rbm_timing_end",
            "rbm_part_info_get", "rbm_part_prologue", "rbm_part_phase1", "rbm_part_phase2",
-           "rbm_part_set_peers",
+           "rbm_part_set_peers", "rbm_part_map_peers", "rbm_get_nccl_unique_id", "rbm_gather_local",
            "rbm_direct_workspace_size", "rbm_direct_reset", "rbm_direct_run", "rbm_direct_sync"]
 
 
@@ -83,6 +84,9 @@ def lib():
             "rbm_kernel_name": (C.c_char_p, [vp, u32]),
             "rbm_timing_begin": (st, [vp, u32]),
             "rbm_timing_end": (st, [vp, C.POINTER(C.c_double), C.POINTER(u32)]),
+            "rbm_get_nccl_unique_id": (st, [vp]),
+            "rbm_gather_local": (st, [vp, vp, vp, C.POINTER(u64)]),
+            "rbm_part_map_peers": (st, [vp]),
             "rbm_direct_workspace_size": (st, [cfgp, C.POINTER(C.c_size_t)]),
             "rbm_direct_reset": (st, [cfgp, vp, vp]),
             "rbm_direct_run": (st, [cfgp, vp, u64, u64, vp, C.c_size_t, vp]),
@@ -141,11 +145,28 @@ def rbm_workspace_size(cfg: RbmConfig) -> int:
     return n.value
 
 
-def rbm_init(cfg: RbmConfig, ws_ptr: int, ws_bytes: int, stream: int = 0):
+def rbm_get_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().rbm_get_nccl_unique_id(buf))
+    return buf.raw
+
+
+def rbm_init(cfg: RbmConfig, ws_ptr: int, ws_bytes: int, stream: int = 0, nccl_id: bytes | None = None):
     out = C.c_void_p()
-    _check(lib().rbm_init(C.byref(cfg), C.c_void_p(ws_ptr), ws_bytes, C.c_void_p(stream), None,
+    idbuf = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
+    _check(lib().rbm_init(C.byref(cfg), C.c_void_p(ws_ptr), ws_bytes, C.c_void_p(stream), idbuf,
                           C.byref(out)))
     return out
+
+
+def rbm_gather_local(ctx, ids_ptr: int, x_ptr: int) -> int:
+    n = C.c_uint64(0)
+    _check(lib().rbm_gather_local(ctx, C.c_void_p(ids_ptr), C.c_void_p(x_ptr), C.byref(n)), ctx)
+    return n.value
+
+
+def rbm_part_map_peers(ctx):
+    _check(lib().rbm_part_map_peers(ctx), ctx)
 
 
 def rbm_set_state(ctx, x_ptr: int, where: int):
@@ -220,7 +241,7 @@ def rbm_destroy(ctx):
 class RBM:
     """One RBM system on the current CUDA device (torch provides memory/stream)."""
 
-    def __init__(self, cfg: dict, x0=None, device=None):
+    def __init__(self, cfg: dict, x0=None, device=None, nccl_id: bytes | None = None):
         import torch
         self.torch = torch
         self.cfg = dict(cfg)
@@ -237,7 +258,7 @@ class RBM:
         self.ws_bytes = rbm_workspace_size(self.c)
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
         self.stream = torch.cuda.current_stream(self.device)
-        self.ctx = rbm_init(self.c, self.ws.data_ptr(), self.ws_bytes, self.stream.cuda_stream)
+        self.ctx = rbm_init(self.c, self.ws.data_ptr(), self.ws_bytes, self.stream.cuda_stream, nccl_id)
         if x0 is not None:
             self.set_state(x0)
 
@@ -274,6 +295,15 @@ class RBM:
         out = torch.empty((id_end - id_begin, self.d), dtype=self.dtype, device=self.device)
         rbm_gather(self.ctx, id_begin, id_end, out.data_ptr(), MEM_DEVICE)
         return out
+
+    def gather_local(self):
+        """(ids, x): the particles this context holds, unordered (device tensors)."""
+        torch = self.torch
+        cap = self.n  # a rank never holds more than the global N
+        ids = torch.empty(cap, dtype=torch.int32, device=self.device)
+        x = torch.empty((cap, self.d), dtype=self.dtype, device=self.device)
+        k = rbm_gather_local(self.ctx, ids.data_ptr(), x.data_ptr())
+        return ids[:k], x[:k]
 
     def step_permutation(self):
         """One rbm_step that also returns its permutation (sorted position -> id)."""
