@@ -234,8 +234,9 @@ rbm_status rbm_layout(const rbm_ctx* ctx, uint32_t* prefix_bits, uint32_t* passe
  * device pointer, stream-ordered.  rbm_run() ignores and clears it. */
 rbm_status rbm_debug_permutation(rbm_ctx* ctx, uint32_t* order_out);
 
-/* Test hook (RBM_SCHEME_RBMR / _SEQ only): the slot draws j_s of the next step,
- * ceil(N/p)*p uint32 values (device). */
+/* Test hook (RBM_SCHEME_RBMR / _SEQ only): the slot draws j_s of the last
+ * step, ceil(N/p)*p uint32 values (device); on a partitioned system the
+ * slots of this rank's batches only. */
 rbm_status rbm_debug_slots(rbm_ctx* ctx, uint32_t* slots_out);
 
 /* Test hook: Philox4x32-10 of `count` (ctr, key) pairs on the device:
@@ -304,7 +305,22 @@ typedef struct {
   uint64_t counts_all_off;  /* world_size * nseg u32, rank-major */
   uint64_t halo_send_off, halo_recv_off, halo_bytes;
   uint64_t id0, n0;         /* this rank's initial ids [id0, id0 + n0) */
+  uint64_t chunk_bytes[5];  /* bytes per destination chunk of exchange a (RBM-1: chunk_elems * elem_bytes[a]) */
+  uint32_t phases;          /* library phases per step: 2 (RBM-1) or 4 (RBM-r) */
+  uint32_t pad;
 } rbm_part_info;
+
+/* RBM-r on a partitioned system (scheme RBM_SCHEME_RBMR):
+ * rank r owns the ids [id0, id0+n0) and the batches [floor(nb r/G),
+ * floor(nb (r+1)/G)) of the sweep (nb = ceil(N/p)); the slot draws are the
+ * one-GPU ones, and the step is bit-identical to the one-GPU RBM-r step.  Its
+ * three exchanges are all-to-alls of equal chunks (chunk j of send_off[a] ->
+ * chunk r of rank j's recv_off[a], chunk_bytes[a] each), a = 0 requests
+ * (header: count; ids j_s), a = 1 responses (x_j, reverse direction at the
+ * requests' positions), a = 2 increments (slot s, Delta_s).  Caller protocol
+ * per step: rbm_part_phase(ctx, 1); exchange 0; phase 2; exchange 1; phase 3;
+ * exchange 2; phase 4 (m advances).  With a communicator, rbm_step / rbm_run
+ * do all of it. */
 
 /* Exchange layout for cfg (host-only computation, no device work; same
  * validation as rbm_init).  RBM_ERR_STATE if cfg->world_size == 1. */
@@ -344,6 +360,11 @@ rbm_status rbm_part_phase1(rbm_ctx* ctx);
  * one crossing O_r (with halo_recv), counts_send; m advances.  Follow with
  * exchanges C and R. */
 rbm_status rbm_part_phase2(rbm_ctx* ctx);
+
+/* Phase k of the step (1 <= k <= rbm_part_info.phases): RBM-1 k = 1, 2 are
+ * rbm_part_phase1 / rbm_part_phase2; RBM-r see above.  RBM_ERR_STATE out of
+ * order. */
+rbm_status rbm_part_phase(rbm_ctx* ctx, uint32_t k);
 
 /* ------------------------------------------------------------------------
  * Direct O(N^2) steps: the fully coupled forward

@@ -83,8 +83,33 @@ rbm_status part_exchange_h(rbm_ctx* c, cudaStream_t s) {
   return RBM_OK;
 }
 
+// RBM-r exchange a (0 requests, 1 responses, 2 increments): chunk j of the
+// send region to rank j, chunk j of the receive region from rank j
+rbm_status rbmr_exchange(rbm_ctx* c, cudaStream_t s, int a) {
+  NcclApi& N = nccl();
+  const RPart& R = c->rp;
+  const unsigned char* sr[3][2] = {{R.qs, R.qr}, {R.ps, R.pr}, {R.is, R.ir}};
+  const uint64_t cb[3] = {R.qchunk, R.pchunk, R.ichunk};
+  NC(N.GroupStart());
+  for (uint32_t j = 0; j < R.G; ++j) {
+    NC(N.Send(sr[a][0] + j * cb[a], cb[a], ncclUint8, (int)j, c->comm, s));
+    NC(N.Recv(const_cast<unsigned char*>(sr[a][1]) + j * cb[a], cb[a], ncclUint8, (int)j, c->comm, s));
+  }
+  NC(N.GroupEnd());
+  return RBM_OK;
+}
+
 // one step of the partitioned system with the library's exchanges
 rbm_status part_step(rbm_ctx* c, cudaStream_t s) {
+  if (c->cfg.scheme == RBM_SCHEME_RBMR) {
+    for (int k = 1; k <= 4; ++k) {
+      c->eng->rbmr_part_phase(*c, s, k);
+      if (k < 4)
+        if (rbm_status e = rbmr_exchange(c, s, k - 1)) return e;
+    }
+    CU(cudaGetLastError());
+    return RBM_OK;
+  }
   c->P.verlet_start = c->verlet_start ? 1u : 0u;
   if (!c->partitioned) {
     c->eng->part_prologue(*c, s);
@@ -316,7 +341,8 @@ rbm_status rbm_run(rbm_ctx* c, uint64_t nsteps) {
   c->graph_steps = per;
   uint64_t done = 0;
   if (is_partitioned(c->cfg)) {  // the library's exchanges, captured with the kernels when possible
-    if (!c->partitioned && nsteps > 0) {
+    const bool first = c->cfg.scheme == RBM_SCHEME_RBM1 ? !c->partitioned : !c->aos_valid;
+    if (first && nsteps > 0) {
       if (rbm_status e = part_step(c, c->stream)) return e;
       ++c->step;
       --nsteps;
@@ -511,7 +537,8 @@ rbm_status rbm_debug_slots(rbm_ctx* c, uint32_t* slots_out) {
   if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
   if (c->cfg.scheme == RBM_SCHEME_RBM1) return fail(c, RBM_ERR_STATE, "not an RBM-r context");
   if (!slots_out) return fail(c, RBM_ERR_INVALID_ARG, "slots_out is NULL");
-  CU(cudaMemcpyAsync(slots_out, c->js, c->nslots * 4, cudaMemcpyDeviceToDevice, c->stream));
+  const uint64_t ns = is_partitioned(c->cfg) ? (c->rp.bb1 - c->rp.bb0) * c->cfg.p : c->nslots;  // own batches' slots
+  CU(cudaMemcpyAsync(slots_out, c->js, ns * 4, cudaMemcpyDeviceToDevice, c->stream));
   return RBM_OK;
 }
 
@@ -555,12 +582,40 @@ rbm_status rbm_part_info_get(const rbm_config* cfg, rbm_part_info* out) {
   out->halo_bytes = 16 + (uint64_t)HALO_MAX * rec_bytes(*cfg);
   out->id0 = tmp.id0;
   out->n0 = tmp.n0;
+  out->phases = 2;
+  for (uint32_t a = 0; a < out->narrays; ++a) out->chunk_bytes[a] = out->chunk_elems * out->elem_bytes[a];
+  if (cfg->scheme == RBM_SCHEME_RBMR) {  // requests, responses, increments
+    const RPart& R = tmp.rp;
+    out->phases = 4;
+    out->nseg = 0;
+    out->narrays = 3;
+    out->chunk_elems = 0;
+    const unsigned char* sr[3][2] = {{R.qs, R.qr}, {R.ps, R.pr}, {R.is, R.ir}};
+    const uint64_t cb[3] = {R.qchunk, R.pchunk, R.ichunk};
+    for (int a = 0; a < 3; ++a) {
+      out->send_off[a] = off(sr[a][0]);
+      out->recv_off[a] = off(sr[a][1]);
+      out->elem_bytes[a] = 1;
+      out->chunk_bytes[a] = cb[a];
+    }
+    out->halo_bytes = 0;
+  }
+  return RBM_OK;
+}
+
+static rbm_status rbmr_part_call(rbm_ctx* c, int phase) {
+  if (phase < 1 || phase > 4) return fail(c, RBM_ERR_STATE, "RBM-r partitioned step: phases 1..4");
+  if (phase == 4 && c->step + 1 >= (1ull << 32)) return fail(c, RBM_ERR_INVALID_ARG, "step index would exceed 2^32");
+  c->eng->rbmr_part_phase(*c, c->stream, phase);
+  if (phase == 4) ++c->step;
+  CU(cudaGetLastError());
   return RBM_OK;
 }
 
 static rbm_status part_call(rbm_ctx* c, int phase) {
   if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
   if (!is_partitioned(c->cfg)) return fail(c, RBM_ERR_STATE, "not a partitioned context (world_size 1)");
+  if (c->cfg.scheme == RBM_SCHEME_RBMR) return rbmr_part_call(c, phase);
   if (phase == 0 && c->partitioned) return fail(c, RBM_ERR_STATE, "prologue already done (state is partitioned)");
   if (phase > 0 && !c->partitioned) return fail(c, RBM_ERR_STATE, "run rbm_part_prologue and its exchange first");
   if (phase == 2 && c->step + 1 >= (1ull << 32)) return fail(c, RBM_ERR_INVALID_ARG, "step index would exceed 2^32");
@@ -667,6 +722,11 @@ rbm_status rbm_gather_local(rbm_ctx* c, uint32_t* ids_out, void* x_out, uint64_t
 rbm_status rbm_part_prologue(rbm_ctx* c) { return part_call(c, 0); }
 rbm_status rbm_part_phase1(rbm_ctx* c) { return part_call(c, 1); }
 rbm_status rbm_part_phase2(rbm_ctx* c) { return part_call(c, 2); }
+rbm_status rbm_part_phase(rbm_ctx* c, uint32_t k) {
+  if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
+  if (k == 0) return fail(c, RBM_ERR_INVALID_ARG, "phases are numbered from 1");
+  return part_call(c, (int)k);
+}
 
 // --------------------------------------------- direct O(N^2) steps (f1)
 static rbm_status direct_validate(const rbm_config* cfg, size_t elt_bytes_out[2]) {

@@ -106,6 +106,8 @@ struct rbm_ctx {
   uint32_t *rprevb = nullptr, *rlevel = nullptr, *rorder = nullptr, *rlcnt = nullptr, *rloff = nullptr,
            *rlcur = nullptr, *rflags = nullptr;  // sequential RBM-r' (levels)
   bool aos_valid = false;  // RBM-r state currently in rxa
+  // RBM-r on a partitioned system (row e2): exchange regions and own batches
+  RPart rp{};
   bool verlet_start = false;  // the next step starts a Verlet run from (x_0, v_0)
   uint64_t nbatch = 0, nslots = 0;
   // state
@@ -301,8 +303,10 @@ inline rbm_status validate(const rbm_config* cfg) {
   if (k.rank < 0 || k.rank >= k.world_size)
     return fail(c, RBM_ERR_INVALID_ARG, "rank=%d not in [0, world_size=%d)", k.rank, k.world_size);
   if (is_partitioned(k)) {
-    if (k.scheme != RBM_SCHEME_RBM1)
-      return fail(c, RBM_ERR_UNSUPPORTED, "partitioned single system: RBM-1 only in this build");
+    if (k.scheme == RBM_SCHEME_RBMR_SEQ)
+      return fail(c, RBM_ERR_UNSUPPORTED, "partitioned single system: RBM-1 and RBM-r (the sequential RBM-r' is one GPU only)");
+    if (k.scheme == RBM_SCHEME_RBMR && k.integrator == RBM_INTEG_VERLET)
+      return fail(c, RBM_ERR_UNSUPPORTED, "partitioned RBM-r: Euler-Maruyama or split");
     if (k.p > HALO_MAX)
       return fail(c, RBM_ERR_INVALID_ARG, "partitioned single system needs p <= %u", HALO_MAX);
     if (k.n / (uint64_t)k.world_size < 1024 || k.n / (uint64_t)k.world_size < 16ull * k.p)
@@ -326,13 +330,14 @@ inline void carve(rbm_ctx& c, Workspace& ws) {
   const rbm_config& k = c.cfg;
   const size_t es = elt_size(k);
   const uint64_t n = k.n;
-  const uint64_t slots = (k.scheme == RBM_SCHEME_RBM1) ? c.L.slots : n;
   const bool part = is_partitioned(k);
+  const uint64_t slots = (k.scheme == RBM_SCHEME_RBM1) ? c.L.slots
+                         : (part ? (n + (uint64_t)k.world_size - 1) / (uint64_t)k.world_size : n);
   const size_t RS = rec_bytes(k);
   const bool side = k.scheme == RBM_SCHEME_RBM1 && !rec_keyed(k) && c.L.b2 > 0;
   initial_ids(k, c.id0, c.n0);
   c.xstride = (slots + 63) & ~63ull;  // 256-B aligned buffers (TMA)
-  for (int b = 0; b < (part ? 3 : 2); ++b) {
+  for (int b = 0; b < ((part && k.scheme == RBM_SCHEME_RBM1) ? 3 : 2); ++b) {
     c.recbuf[b] = ws.take<unsigned char>(c.xstride * RS);
     c.skey[b] = side ? ws.take<uint32_t>(c.xstride) : nullptr;
   }
@@ -354,7 +359,43 @@ inline void carve(rbm_ctx& c, Workspace& ws) {
   c.nonfinite = ws.take<unsigned long long>(1);
   c.capacity_err = ws.take<uint32_t>(1);
   c.big_scratch = ws.take<unsigned char>(NBIG * big_slot_bytes(RS));
-  if (k.scheme != RBM_SCHEME_RBM1) {
+  if (k.scheme != RBM_SCHEME_RBM1 && part) {
+    // RBM-r partitioned: own ids [id0, id0+n0) and batches [bb0, bb1); chunk
+    // capacity = mean requests per (source, destination) + 12 sigma + 64
+    const uint64_t G = (uint64_t)k.world_size;
+    c.nbatch = (n + k.p - 1) / k.p;
+    c.nslots = c.nbatch * k.p;
+    RPart& R = c.rp;
+    R.G = (uint32_t)G;
+    R.rank = (uint32_t)k.rank;
+    R.n = n;
+    R.id0 = c.id0;
+    R.n0 = c.n0;
+    R.bb0 = c.nbatch * (uint64_t)k.rank / G;
+    R.bb1 = c.nbatch * (uint64_t)(k.rank + 1) / G;
+    for (uint64_t q = 0; q <= G; ++q) R.idb[q] = n * q / G;
+    const double mu = (double)((c.nbatch + G - 1) / G * k.p) * (double)((n + G - 1) / G) / (double)n;
+    R.cap = (uint32_t)(((uint64_t)(mu + 12.0 * std::sqrt(mu) + 64.0) + 15) & ~15ull);
+    R.qchunk = 16 + (uint64_t)R.cap * 4;
+    R.pchunk = (uint64_t)R.cap * 4 * es;
+    R.ioff = (uint64_t)R.cap * 4;
+    R.ichunk = R.ioff + (uint64_t)R.cap * 4 * es;
+    R.qs = ws.take<unsigned char>(G * R.qchunk);
+    R.qr = ws.take<unsigned char>(G * R.qchunk);
+    R.ps = ws.take<unsigned char>(G * R.pchunk);
+    R.pr = ws.take<unsigned char>(G * R.pchunk);
+    R.is = ws.take<unsigned char>(G * R.ichunk);
+    R.ir = ws.take<unsigned char>(G * R.ichunk);
+    R.qcnt = ws.take<uint32_t>(G);
+    const uint64_t own = (R.bb1 - R.bb0) * k.p;
+    R.spos = ws.take<uint32_t>(own);
+    c.js = ws.take<uint32_t>(own);
+    c.rxa = ws.take<unsigned char>(c.n0 * 4 * es);
+    c.rmcnt = ws.take<uint32_t>(c.n0);
+    c.rmbox = ws.take<uint32_t>(c.n0 * MBOX);
+    c.rovf = ws.take<uint32_t>(2 * (size_t)OVF_CAP);
+    c.rnovf = ws.take<uint32_t>(1);
+  } else if (k.scheme != RBM_SCHEME_RBM1) {
     c.nbatch = (n + k.p - 1) / k.p;
     c.nslots = c.nbatch * k.p;
     c.js = ws.take<uint32_t>(c.nslots);
@@ -401,6 +442,8 @@ struct EngineBase {
   virtual void part_phase2(rbm_ctx& c, cudaStream_t s) = 0;
   // this rank's records, unordered (ids and positions, row-major); returns the count (syncs)
   virtual uint64_t gather_local(rbm_ctx& c, uint32_t* ids, void* x, cudaStream_t s) = 0;
+  // RBM-r on a partitioned system: phase k = 1..4 of the step (exchange k-1 follows phase k)
+  virtual void rbmr_part_phase(rbm_ctx& c, cudaStream_t s, int k) = 0;
 };
 
 template <typename T, int D, int KK, int INTEG>
@@ -504,6 +547,11 @@ struct Engine final : EngineBase {
   }
 
   void gather(rbm_ctx& c, uint64_t i0, uint64_t i1, void* out, cudaStream_t s) override {
+    if (is_partitioned(c.cfg) && c.cfg.scheme == RBM_SCHEME_RBMR && c.aos_valid) {
+      gather_aos_part_kernel<T, D><<<grid_for(c.n0, 256), 256, 0, s>>>(
+          reinterpret_cast<const T*>(c.rxa), c.id0, c.n0, i0, i1, reinterpret_cast<T*>(out), nullptr);
+      return;
+    }
     if (is_partitioned(c.cfg)) {
       if (c.partitioned) {
         gather_part_kernel<T, D><<<grid_for((uint64_t)c.L.nseg() * c.L.cap1, 256), 256, 0, s>>>(
@@ -686,7 +734,45 @@ struct Engine final : EngineBase {
     c.mark(s);
   }
 
+  void rbmr_part_phase(rbm_ctx& c, cudaStream_t s, int k) override {
+    const DevParams& P = c.P;
+    RPart& R = c.rp;
+    T* xa = reinterpret_cast<T*>(c.rxa);
+    const unsigned gb = grid_for(R.bb1 - R.bb0, 128, 148 * 64);
+    if (k == 1) {
+      if (!c.aos_valid) {  // records of the own ids (id order) -> AoS, once
+        rbmr_pack_local_kernel<T, D><<<grid_for(c.n0, 256), 256, 0, s>>>(c.n0, st(c, c.cur), xa);
+        c.aos_valid = true;
+      }
+      cudaMemsetAsync(R.qcnt, 0, (size_t)R.G * 4, s);
+      c.mark(s);
+      rbmr_req_kernel<<<gb, 128, 0, s>>>(P, R, c.js);
+      rbmr_req_counts_kernel<<<1, 64, 0, s>>>(R);
+    } else if (k == 2) {
+      c.mark(s);
+      rbmr_serve_kernel<T, D><<<grid_for((uint64_t)R.G * R.cap, 256), 256, 0, s>>>(R, xa);
+    } else if (k == 3) {
+      c.mark(s);
+      rbmr_delta_part_kernel<T, D, KK, INTEG><<<gb, 128, 0, s>>>(P, R);
+    } else {
+      cudaMemsetAsync(c.rmcnt, 0, c.n0 * 4, s);
+      cudaMemsetAsync(c.rnovf, 0, 4, s);
+      c.mark(s);
+      rbmr_register_part_kernel<<<grid_for((uint64_t)R.G * R.cap, 256), 256, 0, s>>>(P, R, c.rmcnt, c.rmbox,
+                                                                                   c.rovf, c.rnovf);
+      rbmr_apply_part_kernel<T, D><<<grid_for(c.n0, 256), 256, 0, s>>>(P, R, xa, c.rmcnt, c.rmbox, c.rovf,
+                                                                       c.rnovf);
+      advance_kernel<<<1, 1, 0, s>>>(c.step_dev);
+      c.mark(s);
+    }
+  }
+
   uint64_t gather_local(rbm_ctx& c, uint32_t* ids, void* x, cudaStream_t s) override {
+    if (c.cfg.scheme == RBM_SCHEME_RBMR && c.aos_valid) {
+      gather_aos_part_kernel<T, D><<<grid_for(c.n0, 256), 256, 0, s>>>(
+          reinterpret_cast<const T*>(c.rxa), c.id0, c.n0, 0, 0, reinterpret_cast<T*>(x), ids);
+      return c.n0;
+    }
     if (!is_partitioned(c.cfg) || !c.partitioned) {  // records in id order (this rank's initial ids)
       gather_local_kernel<T, D><<<grid_for(c.n0, 256), 256, 0, s>>>(c.n0, st(c, 0), ids, reinterpret_cast<T*>(x));
       return c.n0;
@@ -817,6 +903,8 @@ inline const char* const* kernel_names(const rbm_ctx& c, uint32_t* count) {
   static const char* const p2[] = {"tile_scan", "split", "final_scan", "bucket_step", "straddle", "advance"};
   static const char* const pt[] = {"part_scan", "split", "final_scan", "bucket_step",
                                    "halo_extract", "halo_place", "straddle", "pack_counts", "advance"};
+  static const char* const prr[] = {"rbmr_request", "rbmr_serve", "rbmr_delta", "rbmr_apply"};
+  if (is_partitioned(c.cfg) && c.cfg.scheme == RBM_SCHEME_RBMR) { *count = 4; return prr; }
   if (is_partitioned(c.cfg)) { *count = 9; return pt; }
   if (c.cfg.scheme == RBM_SCHEME_RBMR) { *count = 3; return r; }
   if (c.L.B == 0) { *count = 1; return b0; }

@@ -654,7 +654,7 @@ static __global__ void __launch_bounds__(BLOCK, 1) split_kernel(const __grid_con
 // copy one record (NW words) from src_rec to segment v, slot `slot` of dst
 template <typename T, int D>
 __device__ __forceinline__ void out_copy(const OutDst<T, D>& o, uint32_t v, uint32_t cap, uint32_t slot,
-                                         const unsigned char* src_rec, uint32_t key) {
+                                         const unsigned char* src_rec) {
   using L = RecL<T, D>;
   uint32_t w = 0;
   size_t g;
@@ -666,7 +666,6 @@ __device__ __forceinline__ void out_copy(const OutDst<T, D>& o, uint32_t v, uint
   }
   uint32_t wd[L::NW];
   ld_words<L::NW>(src_rec, wd);
-  if (L::KEYED) wd[1] = key;
   st_words<L::NW>(o.st[w].rec + g * L::RS, wd);
 }
 
@@ -720,11 +719,11 @@ __device__ __forceinline__ void interior_update(const DevParams& P, uint32_t m, 
 
 // One batch [l0, l1) handled by one thread (a remainder batch larger than the
 // lane group, or p > 32): every member from the old positions, then written
-// back in place; ta[e] = key_{m+1}, tb[e] = rank in its output digit.
+// back in place (keyed records carry key_{m+1}); tb[e] = output digit << 16 | rank in it.
 template <typename T, int D, int KK, int INTEG>
 __device__ __noinline__ void serial_batch(const DevParams& P, uint32_t m, uint32_t l0, uint32_t l1,
-                                          const uint16_t* ord, unsigned char* rs, uint32_t* ta,
-                                          uint16_t* tb, uint32_t* ocnt, uint32_t osh) {
+                                          const uint16_t* ord, unsigned char* rs,
+                                          uint32_t* tb, uint32_t* ocnt, uint32_t osh) {
   T xn[65][D];
   const RX<T, D> xs{rs};
   for (uint32_t q = l0; q < l1; ++q) {
@@ -742,8 +741,7 @@ __device__ __noinline__ void serial_batch(const DevParams& P, uint32_t m, uint32
     for (int c = 0; c < D; ++c) r.x[c] = xn[q - l0][c];
     r.key = kn;
     st_rec<T, D>(rs, e, r);
-    ta[e] = kn;
-    tb[e] = (uint16_t)atomicAdd(&ocnt[kn >> osh], 1u);
+    tb[e] = ((kn >> osh) << 16) | atomicAdd(&ocnt[kn >> osh], 1u);
   }
 }
 
@@ -949,10 +947,9 @@ static __global__ void __launch_bounds__(BUCKET_BLOCK, MINB) bucket_kernel(const
   }
   unsigned char* rs = reinterpret_cast<unsigned char*>(bar + 2);
   uint32_t* key_l = reinterpret_cast<uint32_t*>(rs + (size_t)(cap + 8) * L::RS);
-  uint32_t* ks = key_l + cap + 8;  // composites (sort); then tb | inv (u16 each)
-  uint16_t* tb = reinterpret_cast<uint16_t*>(ks);
-  uint16_t* inv = tb + cap;
-  uint32_t* ta = key_l;            // key_{m+1} by element
+  uint32_t* ks = key_l + cap + 8;  // composites (sort); then tb
+  uint32_t* tb = ks;               // output digit << 16 | rank in it, by element (~0: straddler)
+  uint32_t* inv = key_l;           // staged output slot -> element | digit << 16
   uint16_t* ord = reinterpret_cast<uint16_t*>(ks + cap);
   const bool side = !L::KEYED && P.side_key;
   if (threadIdx.x == 0) {
@@ -1045,9 +1042,11 @@ static __global__ void __launch_bounds__(BUCKET_BLOCK, MINB) bucket_kernel(const
     const uint32_t tri0 = triple ? pend - s0 : n;
     for (uint32_t t = threadIdx.x; t < head + (tri0 - tail); t += BLOCK) {
       const uint32_t q = t < head ? t : tail + (t - head);
+      const uint32_t e = ord[q];
       uint32_t wd[L::NW];
-      ld_words<L::NW>(rs + (size_t)ord[q] * L::RS, wd);
+      ld_words<L::NW>(rs + (size_t)e * L::RS, wd);
       st_words<L::NW>(src.rec + ((size_t)sb + q) * L::RS, wd);
+      tb[e] = 0xffffffffu;
     }
     RBM_PROF(P, 5);
     // one thread per pair: Eq. (2.2) + update in place; next keys and ranks
@@ -1070,14 +1069,12 @@ static __global__ void __launch_bounds__(BUCKET_BLOCK, MINB) bucket_kernel(const
         r1.key = kn1;
         st_rec<T, D>(rs, e0, r0);
         st_rec<T, D>(rs, e1, r1);
-        ta[e0] = kn0;
-        ta[e1] = kn1;
-        tb[e0] = (uint16_t)atomicAdd(&cnt[kn0 >> osh], 1u);
-        tb[e1] = (uint16_t)atomicAdd(&cnt[kn1 >> osh], 1u);
+        tb[e0] = ((kn0 >> osh) << 16) | atomicAdd(&cnt[kn0 >> osh], 1u);
+        tb[e1] = ((kn1 >> osh) << 16) | atomicAdd(&cnt[kn1 >> osh], 1u);
       }
     }
     // the size-3 remainder batch (N odd, EM): one thread, out of line
-    if (triple && threadIdx.x == 0) serial_batch<T, D, KK, INTEG>(P, m, tri0, n, ord, rs, ta, tb, cnt, osh);
+    if (triple && threadIdx.x == 0) serial_batch<T, D, KK, INTEG>(P, m, tri0, n, ord, rs, tb, cnt, osh);
     if (triple) tail = n;
   } else {
     // interior batches [kfirst, klast) of this bucket
@@ -1092,9 +1089,11 @@ static __global__ void __launch_bounds__(BUCKET_BLOCK, MINB) bucket_kernel(const
     tail = (kfirst < klast) ? batch_end(klast - 1, P) - s0 : n;
     for (uint32_t t = threadIdx.x; t < head + (n - tail); t += BLOCK) {
       const uint32_t q = t < head ? t : tail + (t - head);
+      const uint32_t e = ord[q];
       uint32_t wd[L::NW];
-      ld_words<L::NW>(rs + (size_t)ord[q] * L::RS, wd);
+      ld_words<L::NW>(rs + (size_t)e * L::RS, wd);
       st_words<L::NW>(src.rec + ((size_t)sb + q) * L::RS, wd);
+      tb[e] = 0xffffffffu;
     }
     RBM_PROF(P, 5);
     const uint32_t G = P.group;
@@ -1177,8 +1176,7 @@ static __global__ void __launch_bounds__(BUCKET_BLOCK, MINB) bucket_kernel(const
           for (int c = 0; c < D; ++c) ri.x[c] = xn[c];
           ri.key = kn;
           st_rec<T, D>(rs, e, ri);
-          ta[e] = kn;
-          tb[e] = (uint16_t)atomicAdd(&cnt[kn >> osh], 1u);
+          tb[e] = ((kn >> osh) << 16) | atomicAdd(&cnt[kn >> osh], 1u);
         }
       }
     }
@@ -1187,7 +1185,7 @@ static __global__ void __launch_bounds__(BUCKET_BLOCK, MINB) bucket_kernel(const
         (G == 0) ? kfirst
                  : ((klast > kfirst && batch_end(klast - 1, P) - (klast - 1) * P.p > G) ? klast - 1 : klast);
     for (uint32_t k = first_big + threadIdx.x; k < klast; k += BLOCK)
-      serial_batch<T, D, KK, INTEG>(P, m, k * P.p - s0, batch_end(k, P) - s0, ord, rs, ta, tb, cnt, osh);
+      serial_batch<T, D, KK, INTEG>(P, m, k * P.p - s0, batch_end(k, P) - s0, ord, rs, tb, cnt, osh);
   }
   __syncthreads();
   RBM_PROF(P, 6);
@@ -1201,9 +1199,9 @@ static __global__ void __launch_bounds__(BUCKET_BLOCK, MINB) bucket_kernel(const
     gres[r] = h ? atomicAdd(&cur_next[(size_t)out_seg(P, i, blockIdx.x) * CUR1_STRIDE], h) : 0u;
   }
   const uint32_t total = block_excl_scan4<BLOCK>(cnt, off, nout, wsum);
-  for (uint32_t q = head + threadIdx.x; q < tail; q += BLOCK) {
-    const uint32_t e = ord[q];
-    inv[off[ta[e] >> osh] + tb[e]] = (uint16_t)e;
+  for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {  // staging index (tb read in element order)
+    const uint32_t t = tb[e];
+    if (t != 0xffffffffu) inv[off[t >> 16] + (t & 0xffffu)] = e | (t & 0xffff0000u);
   }
 #pragma unroll
   for (int r = 0; r < NRES; ++r)  // gbase[d] - off[d]: output position j goes to slot gbase[dg] + j
@@ -1212,12 +1210,11 @@ static __global__ void __launch_bounds__(BUCKET_BLOCK, MINB) bucket_kernel(const
   RBM_PROF(P, 7);
   // staged slots -> coalesced runs of the step-(m+1) pass-1 buckets
   for (uint32_t j = threadIdx.x; j < total; j += BLOCK) {
-    const uint32_t e = inv[j];
-    const uint32_t kn = ta[e];
-    const uint32_t dg = kn >> osh;
+    const uint32_t v = inv[j];
+    const uint32_t e = v & 0xffffu, dg = v >> 16;
     const uint32_t slot = gbase[dg] + j;
     if (slot >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
-    out_copy<T, D>(dst, out_seg(P, dg, blockIdx.x), dcap, slot, rs + (size_t)e * L::RS, kn);
+    out_copy<T, D>(dst, out_seg(P, dg, blockIdx.x), dcap, slot, rs + (size_t)e * L::RS);
   }
   RBM_PROF(P, 8);
   if (P.prof && threadIdx.x == 0) atomicAdd(&P.prof[63], 1ull);
@@ -2063,6 +2060,261 @@ static __global__ void __launch_bounds__(128) rbmr_seq_apply_kernel(const __grid
       check_finite<T, D>(xnj, P, j, m);
 #pragma unroll
       for (int c = 0; c < D; ++c) { xa[(size_t)i * 4 + c] = xn[c]; xa[(size_t)j * 4 + c] = xnj[c]; }
+    }
+  }
+}
+
+// ------------------------ RBM-r on a partitioned global system (row e2)
+// Rank r owns the ids [id0, id0 + n0) (AoS state xa in local order) and the
+// batches [bb0, bb1) of the sweep (floor(nb r / G)).  One step (the Jacobi
+// sweep of reading D:8, SURVEY 8(e) "request, response, increment return"):
+//   A  draw j_s of the own slots (the G = 1 counters: bit-identical slots),
+//      request j_s from its owner: chunk dest of Q gets j_s at a cursor
+//   Q  all-to-all of the request chunks (header: count)
+//   B  serve: x[j] of every received request into the response chunk
+//   Pr all-to-all of the responses (reverse direction, same positions)
+//   C  Delta_s of every own batch from the responses (rbmr_deltas: the same
+//      arithmetic as the one-GPU kernel), increment record (s, Delta_s) at the
+//      request's position
+//   I  all-to-all of the increments
+//   D  the owner registers every received increment at its particle and adds
+//      them in ascending global s (the one-GPU order): bit-identical to G = 1.
+constexpr int RP_MAXG = 64;
+struct RPart {
+  uint32_t G, rank, cap;                 // ranks, this rank, records per (source, destination) chunk
+  uint64_t n, id0, n0, bb0, bb1;         // global N; own ids; own batches
+  uint64_t qchunk, pchunk, ichunk;       // bytes per chunk of the exchanges Q, Pr, I
+  uint64_t ioff;                         // byte offset of the Delta array inside an I chunk
+  unsigned char *qs, *qr, *ps, *pr, *is, *ir;  // send / receive regions (G chunks each)
+  uint32_t* qcnt;                        // G request cursors
+  uint32_t* spos;                        // own slot -> dest << 24 | pos
+  uint64_t idb[RP_MAXG + 1];             // first id of every rank; idb[G] = N
+};
+
+__device__ __forceinline__ uint32_t rp_owner(const RPart& R, uint32_t j) {
+  uint32_t a = 0, b = R.G;  // largest a with idb[a] <= j
+  while (b - a > 1) {
+    const uint32_t mid = (a + b) >> 1;
+    if (R.idb[mid] <= j) a = mid; else b = mid;
+  }
+  return a;
+}
+
+// draws of slot s0 + l (distinct within the batch, reading D:9): as rbmr_batch_kernel
+__device__ __forceinline__ uint32_t rbmr_draw(const DevParams& P, uint32_t m, uint64_t s, const uint32_t* prev,
+                                              uint32_t l) {
+  uint32_t t = 0, j;
+  for (;;) {
+    const uint4 w = block_at(P, (uint32_t)s, t, m, TAG_SLOT);
+    j = (uint32_t)__umul64hi(P.n, (((uint64_t)w.x) << 32) | w.y);
+    bool dup = false;
+    for (uint32_t l2 = 0; l2 < l; ++l2) dup |= (prev[l2] == j);
+    if (!dup) return j;
+    ++t;
+  }
+}
+
+// Delta_s of the p slots of batch s0/p from the members' positions x[l]
+// (the general path of rbmr_batch_kernel; for p = 2 the same arithmetic as
+// its pair path: the prefactor is exactly 1)
+template <typename T, int D, int KK, int INTEG>
+__device__ __forceinline__ void rbmr_deltas(const DevParams& P, uint32_t m, uint64_t s0, uint32_t p,
+                                            T (*x)[D], T (*dl)[D]) {
+  for (uint32_t l = 0; l < p; ++l) {
+    T z[D], xn[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) z[c] = T(0);
+    if (P.has_noise) Normals<T, D>::get(P, (uint32_t)(s0 + l), m, TAG_NOISE_SLOT, z);
+    if (INTEG == 0) {
+      T f[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) f[c] = T(0);
+      for (uint32_t l2 = 0; l2 < p; ++l2) {
+        if (l2 == l) continue;
+        add_interaction<T, D, KK>(x[l], x[l2], f, P);
+      }
+      const T inv = T(1) / T(p - 1);
+#pragma unroll
+      for (int c = 0; c < D; ++c) f[c] *= inv;
+      em_update<T, D>(x[l], f, z, xn, P, false);
+    } else {
+      T y[D];
+      pair_flow<T, D, KK>(x[0], x[1], l == 0, y, P);
+      split_finish<T, D>(y, z, xn, P, false);
+    }
+#pragma unroll
+    for (int c = 0; c < D; ++c) dl[l][c] = xn[c] - x[l][c];
+  }
+}
+
+// A: one thread per own batch
+static __global__ void __launch_bounds__(128) rbmr_req_kernel(const __grid_constant__ DevParams P,
+                                                              const __grid_constant__ RPart R, uint32_t* __restrict__ js) {
+  const uint32_t m = (uint32_t)*P.step;
+  const uint32_t p = P.p;
+  for (uint64_t b = R.bb0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < R.bb1;
+       b += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s0 = b * p, sl0 = (b - R.bb0) * p;
+    uint32_t jj[64];
+    for (uint32_t l = 0; l < p; ++l) {
+      const uint32_t j = rbmr_draw(P, m, s0 + l, jj, l);
+      jj[l] = j;
+      js[sl0 + l] = j;
+      const uint32_t dest = rp_owner(R, j);
+      const uint32_t pos = atomicAdd(&R.qcnt[dest], 1u);
+      if (pos >= R.cap) { atomicExch(P.capacity_err, 1u); R.spos[sl0 + l] = 0xffffffffu; continue; }
+      reinterpret_cast<uint32_t*>(R.qs + dest * R.qchunk + 16)[pos] = j;
+      R.spos[sl0 + l] = (dest << 24) | pos;
+    }
+  }
+}
+
+// request counts into the chunk headers
+static __global__ void rbmr_req_counts_kernel(const __grid_constant__ RPart R) {
+  for (uint32_t q = threadIdx.x; q < R.G; q += blockDim.x)
+    *reinterpret_cast<uint32_t*>(R.qs + q * R.qchunk) = min(R.qcnt[q], R.cap);
+}
+
+// B: serve the received requests (x of the own particles, 4 scalars each)
+template <typename T, int D>
+static __global__ void rbmr_serve_kernel(const __grid_constant__ RPart R, const T* __restrict__ xa) {
+  const uint64_t total = (uint64_t)R.G * R.cap;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t q = (uint32_t)(k / R.cap), e = (uint32_t)(k - (uint64_t)q * R.cap);
+    const unsigned char* qc = R.qr + q * R.qchunk;
+    if (e >= *reinterpret_cast<const uint32_t*>(qc)) continue;
+    const uint64_t jl = reinterpret_cast<const uint32_t*>(qc + 16)[e] - R.id0;
+    T* o = reinterpret_cast<T*>(R.ps + q * R.pchunk) + (size_t)e * 4;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) o[c] = xa[jl * 4 + c];
+  }
+}
+
+// C: Delta of every own batch from the responses -> increment records
+template <typename T, int D, int KK, int INTEG>
+static __global__ void __launch_bounds__(128) rbmr_delta_part_kernel(const __grid_constant__ DevParams P,
+                                                                     const __grid_constant__ RPart R) {
+  const uint32_t m = (uint32_t)*P.step;
+  const uint32_t p = P.p;
+  for (uint64_t b = R.bb0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < R.bb1;
+       b += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s0 = b * p, sl0 = (b - R.bb0) * p;
+    T x[64][D], dl[64][D];
+    bool ok = true;
+    for (uint32_t l = 0; l < p; ++l) {
+      const uint32_t sp = R.spos[sl0 + l];
+      if (sp == 0xffffffffu) { ok = false; break; }
+      const T* src = reinterpret_cast<const T*>(R.pr + (sp >> 24) * R.pchunk) + (size_t)(sp & 0xffffffu) * 4;
+#pragma unroll
+      for (int c = 0; c < D; ++c) x[l][c] = src[c];
+    }
+    if (!ok) continue;  // capacity overflow (flagged by the request kernel)
+    rbmr_deltas<T, D, KK, INTEG>(P, m, s0, p, x, dl);
+    for (uint32_t l = 0; l < p; ++l) {
+      const uint32_t sp = R.spos[sl0 + l], dest = sp >> 24, pos = sp & 0xffffffu;
+      unsigned char* ic = R.is + dest * R.ichunk;
+      reinterpret_cast<uint32_t*>(ic)[pos] = (uint32_t)(s0 + l);
+      T* o = reinterpret_cast<T*>(ic + R.ioff) + (size_t)pos * 4;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) o[c] = (c < D) ? dl[l][c < D ? c : 0] : T(0);
+    }
+  }
+}
+
+// D1: register every received increment (index q * cap + e) at its particle
+static __global__ void rbmr_register_part_kernel(const __grid_constant__ DevParams P, const __grid_constant__ RPart R,
+                                                 uint32_t* __restrict__ mcnt, uint32_t* __restrict__ mbox,
+                                                 uint32_t* __restrict__ ovf, uint32_t* __restrict__ novf) {
+  const uint64_t total = (uint64_t)R.G * R.cap;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t q = (uint32_t)(k / R.cap), e = (uint32_t)(k - (uint64_t)q * R.cap);
+    const unsigned char* qc = R.qr + q * R.qchunk;  // the requests this rank served, same positions
+    if (e >= *reinterpret_cast<const uint32_t*>(qc)) continue;
+    const uint32_t jl = (uint32_t)(reinterpret_cast<const uint32_t*>(qc + 16)[e] - R.id0);
+    const uint32_t idx = q * R.cap + e;
+    const uint32_t pos = atomicAdd(&mcnt[jl], 1u);
+    if (pos < MBOX) {
+      mbox[(size_t)jl * MBOX + pos] = idx;
+    } else {
+      const uint32_t o = atomicAdd(novf, 1u);
+      if (o < OVF_CAP) { ovf[2 * o] = jl; ovf[2 * o + 1] = idx; }
+      else atomicExch(P.capacity_err, 1u);
+    }
+  }
+}
+
+// D2: x_j += sum of its increments in ascending global slot s (reading D:8)
+template <typename T, int D>
+static __global__ void rbmr_apply_part_kernel(const __grid_constant__ DevParams P, const __grid_constant__ RPart R,
+                                              T* __restrict__ xa, const uint32_t* __restrict__ mcnt,
+                                              const uint32_t* __restrict__ mbox, const uint32_t* __restrict__ ovf,
+                                              const uint32_t* __restrict__ novf) {
+  const uint32_t m = (uint32_t)*P.step;
+  constexpr uint32_t MAXL = 32;
+  for (uint64_t jl = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; jl < R.n0;
+       jl += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = mcnt[jl];
+    if (c == 0) continue;
+    uint32_t ix[MAXL], sl[MAXL];
+    uint32_t k = 0;
+    const uint32_t cm = c < MBOX ? c : MBOX;
+    for (uint32_t q = 0; q < cm; ++q) ix[k++] = mbox[jl * MBOX + q];
+    if (c > MBOX) {
+      const uint32_t no = min(*novf, OVF_CAP);
+      for (uint32_t q = 0; q < no; ++q)
+        if (ovf[2 * q] == (uint32_t)jl) {
+          if (k < MAXL) ix[k++] = ovf[2 * q + 1];
+          else atomicExch(P.capacity_err, 1u);
+        }
+    }
+    for (uint32_t a = 0; a < k; ++a)
+      sl[a] = reinterpret_cast<const uint32_t*>(R.ir + (ix[a] / R.cap) * R.ichunk)[ix[a] % R.cap];
+    for (uint32_t a = 1; a < k; ++a) {  // insertion sort by global slot
+      const uint32_t v = sl[a], w0 = ix[a];
+      uint32_t w = a;
+      while (w > 0 && sl[w - 1] > v) { sl[w] = sl[w - 1]; ix[w] = ix[w - 1]; --w; }
+      sl[w] = v;
+      ix[w] = w0;
+    }
+    T x[D];
+    load4<T, D>(xa, (uint32_t)jl, x);
+    for (uint32_t a = 0; a < k; ++a) {
+      const T* dd = reinterpret_cast<const T*>(R.ir + (ix[a] / R.cap) * R.ichunk + R.ioff) + (size_t)(ix[a] % R.cap) * 4;
+#pragma unroll
+      for (int cc = 0; cc < D; ++cc) x[cc] += dd[cc];
+    }
+    if (P.constraint == 1) renormalise<T, D>(x);
+    check_finite<T, D>(x, P, (uint32_t)(R.id0 + jl), m);
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) xa[jl * 4 + cc] = x[cc];
+  }
+}
+
+// partitioned RBM-r: pack this rank's records (id order, ids [id0, id0+n0)) -> xa
+template <typename T, int D>
+static __global__ void rbmr_pack_local_kernel(uint64_t n0, State<T, D> st, T* __restrict__ xa) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n0;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const Rec<T, D> r = ld_rec<T, D>(st.rec, (long long)i);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) xa[i * 4 + c] = (c < D) ? r.x[c < D ? c : 0] : T(0);
+  }
+}
+
+// gather from a rank's AoS state (ids [id0, id0+n0)) for ids [i0, i1): rows of its own ids
+template <typename T, int D>
+static __global__ void gather_aos_part_kernel(const T* __restrict__ xa, uint64_t id0, uint64_t n0, uint64_t i0,
+                                              uint64_t i1, T* __restrict__ out, uint32_t* __restrict__ ids) {
+  for (uint64_t jl = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; jl < n0;
+       jl += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t id = id0 + jl;
+    if (ids) {  // local gather: (ids, rows) in local order
+      ids[jl] = (uint32_t)id;
+#pragma unroll
+      for (int c = 0; c < D; ++c) out[jl * D + c] = xa[jl * 4 + c];
+    } else if (id >= i0 && id < i1) {
+#pragma unroll
+      for (int c = 0; c < D; ++c) out[(id - i0) * D + c] = xa[jl * 4 + c];
     }
   }
 }

@@ -44,6 +44,7 @@ class RbmPartInfo(C.Structure):
         ("counts_send_off", C.c_uint64), ("counts_all_off", C.c_uint64),
         ("halo_send_off", C.c_uint64), ("halo_recv_off", C.c_uint64), ("halo_bytes", C.c_uint64),
         ("id0", C.c_uint64), ("n0", C.c_uint64),
+        ("chunk_bytes", C.c_uint64 * 5), ("phases", C.c_uint32), ("pad", C.c_uint32),
     ]
 
 
@@ -61,6 +62,8 @@ def _lib():
             f.restype, f.argtypes = C.c_int, [C.c_void_p]
         L.rbm_part_set_peers.restype = C.c_int
         L.rbm_part_set_peers.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.c_uint32]
+        L.rbm_part_phase.restype = C.c_int
+        L.rbm_part_phase.argtypes = [C.c_void_p, C.c_uint32]
         _sig_done = True
     return L
 
@@ -88,6 +91,10 @@ def rbm_part_phase2(ctx):
     R._check(_lib().rbm_part_phase2(ctx), ctx)
 
 
+def rbm_part_phase(ctx, k: int):
+    R._check(_lib().rbm_part_phase(ctx, int(k)), ctx)
+
+
 class RankBuffers:
     """Byte views of one rank's exchanged regions inside its workspace tensor."""
 
@@ -98,7 +105,7 @@ class RankBuffers:
         def v(off, nbytes):
             return ws[off:off + nbytes]
 
-        self.chunk_bytes = [info.chunk_elems * info.elem_bytes[a] for a in range(info.narrays)]
+        self.chunk_bytes = [int(info.chunk_bytes[a]) for a in range(info.narrays)]
         self.send = [v(info.send_off[a], G * self.chunk_bytes[a]) for a in range(info.narrays)]
         self.recv = [v(info.recv_off[a], G * self.chunk_bytes[a]) for a in range(info.narrays)]
         self.counts_send = v(info.counts_send_off, 4 * info.nseg)
@@ -141,6 +148,14 @@ class LoopbackExchange:
         for r in range(len(ranks) - 1):
             ranks[r + 1].halo_recv.copy_(ranks[r].halo_send)
 
+    def alltoall(self, ranks, a):
+        """All-to-all of equal chunks of exchanged array a (RBM-r exchanges)."""
+        G = len(ranks)
+        cb = ranks[0].chunk_bytes[a]
+        for r, src in enumerate(ranks):
+            for j in range(G):
+                ranks[j].recv[a][r * cb:(r + 1) * cb].copy_(src.send[a][j * cb:(j + 1) * cb])
+
 
 class DistExchange:
     """One rank per process over torch.distributed (NCCL on GPUs, gloo on CPU)."""
@@ -178,6 +193,10 @@ class DistExchange:
         for a in range(me.info.narrays):
             d.all_to_all_single(me.recv[a], me.send[a], group=self.group)
 
+    def alltoall(self, ranks, a):
+        (me,) = ranks
+        self.dist.all_to_all_single(me.recv[a], me.send[a], group=self.group)
+
     def halo(self, ranks):
         (me,) = ranks
         d, r, G = self.dist, me.rank, int(me.info.world_size)
@@ -208,12 +227,13 @@ class HostDistExchange(DistExchange):
         me.counts_all.copy_(self.torch.cat(out).to(me.counts_all.device))
         if self.fused:
             return
-        for a in range(me.info.narrays):
+        for a in range(me.info.narrays):  # gloo has no all-to-all: all-gather, keep chunk `rank`
             cb = me.chunk_bytes[a]
             send = me.send[a].cpu()
-            recv = [self.torch.empty(cb, dtype=send.dtype) for _ in range(G)]
-            d.all_to_all(recv, list(send.split(cb)), group=self.group)
-            me.recv[a].copy_(self.torch.cat(recv).to(me.recv[a].device))
+            allv = [self.torch.empty_like(send) for _ in range(G)]
+            d.all_gather(allv, send, group=self.group)
+            r = me.rank
+            me.recv[a].copy_(self.torch.cat([v[r * cb:(r + 1) * cb] for v in allv]).to(me.recv[a].device))
 
     def halo(self, ranks):
         (me,) = ranks
@@ -224,6 +244,14 @@ class HostDistExchange(DistExchange):
             buf = self.torch.empty(me.halo_recv.numel(), dtype=me.halo_recv.dtype)
             d.recv(buf, r - 1, group=self.group)
             me.halo_recv.copy_(buf.to(me.halo_recv.device))
+
+    def alltoall(self, ranks, a):  # gloo has no all-to-all: all-gather, keep chunk `rank`
+        (me,) = ranks
+        G, r, cb = int(me.info.world_size), me.rank, me.chunk_bytes[a]
+        send = me.send[a].cpu()
+        allv = [self.torch.empty_like(send) for _ in range(G)]
+        self.dist.all_gather(allv, send, group=self.group)
+        me.recv[a].copy_(self.torch.cat([v[r * cb:(r + 1) * cb] for v in allv]).to(me.recv[a].device))
 
     @property
     def torch(self):
@@ -344,6 +372,13 @@ class PartitionedRBM:
         self.started = True
 
     def step(self):
+        if self.bufs[0].info.phases == 4:  # RBM-r: request, response, increment exchanges
+            for k in range(1, 5):
+                for s in self.systems:
+                    rbm_part_phase(s.ctx, k)
+                if k < 4:
+                    self.exchange.alltoall(self.bufs, k - 1)
+            return
         if not self.started:
             self._start()
         for s in self.systems:

@@ -32,6 +32,7 @@ EXPORTS = ["rbm_workspace_size", "rbm_init", "rbm_set_state", "rbm_step", "rbm_r
            "rbm_destroy", "rbm_kernel_name", "rbm_timing_begin", "rbm_timing_end",
            "rbm_part_info_get", "rbm_part_prologue", "rbm_part_phase1", "rbm_part_phase2",
            "rbm_part_set_peers", "rbm_part_map_peers", "rbm_get_nccl_unique_id", "rbm_gather_local",
+           "rbm_part_phase",
            "rbm_direct_workspace_size", "rbm_direct_reset", "rbm_direct_run", "rbm_direct_sync"]
 
 
@@ -314,8 +315,11 @@ class RBM:
         return out.cpu().numpy().view("uint32")
 
     def slots(self):
+        """Slot draws j_s of the last step (partitioned: this rank's batches)."""
         nb = (self.n + self.c.p - 1) // self.c.p
-        out = self.torch.empty(nb * self.c.p, dtype=self.torch.int32, device=self.device)
+        G, r = int(self.c.world_size), int(self.c.rank)
+        nown = (nb * (r + 1) // G - nb * r // G) * self.c.p
+        out = self.torch.empty(nown, dtype=self.torch.int32, device=self.device)
         rbm_debug_slots(self.ctx, out.data_ptr())
         self.stream.synchronize()
         return out.cpu().numpy().view("uint32")

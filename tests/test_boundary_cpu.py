@@ -72,7 +72,8 @@ def status_of(R, cfg):
     (dict(p=1), 1), (dict(p=600), 1), (dict(d=4), 1), (dict(d=2), 1),  # dyson needs d=1
     (dict(sigma=-1.0), 1), (dict(dt=0.0), 1), (dict(kernel=99), 2), (dict(world_size=2), 1),
     (dict(world_size=3, n=100000), 1), (dict(world_size=2, rank=2, n=100000), 1),
-    (dict(world_size=2, n=100000, scheme="rbmr"), 3), (dict(world_size=2, n=100000, p=2), 0),
+    (dict(world_size=2, n=100000, scheme="rbmr"), 0), (dict(world_size=2, n=100000, scheme="rbmr_seq"), 3),
+    (dict(world_size=2, n=100000, p=2), 0),
     (dict(integrator="split", p=4), 1), (dict(n=501, integrator="split"), 1),
     (dict(n=1), 1), (dict(replica=1 << 24), 1), (dict(p=65, n=100000), 1),
 ])
