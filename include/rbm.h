@@ -100,7 +100,11 @@ typedef enum {
   RBM_K_GAUSS_ATTR_REP = 4,     /* z e^{-|z|^2/2} - z e^{-|z|^2/8}/4 (BASELINE.json C4)       */
   RBM_K_COULOMB_REG = 5,        /* z/(|z|^2+eps)^{3/2}, kparam={eps} (BASELINE.json C5)       */
   RBM_K_SMOOTH_TEST = 6,        /* z/(1+|z|^2)                             */
-  RBM_K_LINEAR = 7              /* -kappa z, kparam={kappa}: wealth trading phi=y^2/2 */
+  RBM_K_LINEAR = 7,             /* -kappa z, kparam={kappa}: wealth trading phi=y^2/2 */
+  RBM_K_ADJACENCY = 8           /* clustering (Sec. 5.3): the picked pair (i, j) follows
+                                   dX^i/dt = alpha (a_ij - beta)(X^j - X^i), a_ij from rbm_set_adjacency;
+                                   kparam={alpha, beta, edge_restricted}; RBM-r / RBM-r', p = 2, split
+                                   integrator (the exact update formula of P:1258-1264), one GPU */
 } rbm_kernel;
 
 /* Noise term of Eq. (1.2): additive sigma dB^i, or multiplicative sigma X^i dB^i
@@ -176,6 +180,16 @@ rbm_status rbm_workspace_size(const rbm_config* cfg, size_t* bytes);
  * On success *out receives the context; the step index is cfg->step0. */
 rbm_status rbm_init(const rbm_config* cfg, void* ws, size_t ws_bytes, void* cuda_stream,
                     const void* nccl_unique_id, rbm_ctx** out);
+
+/* Clustering model (RBM_K_ADJACENCY): the symmetric adjacency A = (a_ij) in
+ * CSR, device pointers owned by the caller and unchanged until rbm_destroy:
+ * row_ptr n+1 uint32, col_idx nnz uint32 (each row sorted ascending), val nnz
+ * doubles a_ij >= 0; entries off the pattern are 0.  With kparam[2] != 0 the
+ * RBM-r pairs are drawn uniformly among the nnz entries ("picked from
+ * those with nonzeros of a_ij only"; a diagonal entry is redrawn).  Must be
+ * called before the first step of such a context. */
+rbm_status rbm_set_adjacency(rbm_ctx* ctx, const uint32_t* row_ptr, const uint32_t* col_idx, const double* val,
+                             uint64_t nnz);
 
 /* Replace the state by X given in id order (N*d scalars of dtype, row-major);
  * `where` says whether x is a host or device pointer.  Host input is copied

@@ -21,7 +21,7 @@ SRC = os.path.join(HERE, "rbm_oracle.c")
 LIB = os.path.join(HERE, "librbm_oracle.so")
 
 KERNELS = {"zero": 0, "dyson": 1, "coulomb": 2, "bounded_confidence": 3,
-           "gauss_attr_rep": 4, "coulomb_reg": 5, "smooth": 6, "linear": 7}
+           "gauss_attr_rep": 4, "coulomb_reg": 5, "smooth": 6, "linear": 7, "adjacency": 8}
 INITS = {"user": 0, "normal": 1, "box": 2, "sphere": 3, "mixture": 4, "abs_normal": 5}
 
 
@@ -34,6 +34,7 @@ class OracleCfg(C.Structure):
         ("state_form", C.c_int32), ("pad1", C.c_int32),
         ("kparam", C.c_double * 4), ("vparam", C.c_double * 2), ("iparam", C.c_double * 8),
         ("sigma", C.c_double), ("dt", C.c_double), ("seed", C.c_uint64),
+        ("adj_rp", C.c_void_p), ("adj_ci", C.c_void_p), ("adj_v", C.c_void_p), ("adj_nnz", C.c_uint64),
     ]
 
 
@@ -78,6 +79,8 @@ def lib():
             "oracle_rbmr_seq_step": (C.c_int, [cfgp, C.c_uint64, f64p]),
             "oracle_run": (C.c_int, [cfgp, C.c_uint64, C.c_uint64, f64p]),
             "oracle_direct_run": (C.c_int, [cfgp, C.c_uint64, C.c_uint64, f64p]),
+            "oracle_adj_value": (C.c_double, [cfgp, C.c_uint32, C.c_uint32]),
+            "oracle_adj_pair_flow": (None, [cfgp, C.c_uint32, C.c_uint32, f64p, f64p, C.c_double, f64p, f64p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -112,6 +115,13 @@ def make_cfg(cfg: dict) -> OracleCfg:
     c.sigma = float(cfg.get("sigma", 0.0))
     c.dt = float(cfg["dt"])
     c.seed = int(cfg.get("seed", 0)) & 0xFFFFFFFFFFFFFFFF
+    adj = cfg.get("adjacency")
+    if adj is not None:  # (row_ptr u32, col u32, val f64) numpy arrays, kept alive by the dict
+        rp, ci, v = (np.ascontiguousarray(adj[0], dtype=np.uint32), np.ascontiguousarray(adj[1], dtype=np.uint32),
+                     np.ascontiguousarray(adj[2], dtype=np.float64))
+        cfg["_adj_keep"] = (rp, ci, v)
+        c.adj_rp, c.adj_ci, c.adj_v = rp.ctypes.data, ci.ctypes.data, v.ctypes.data
+        c.adj_nnz = len(ci)
     return c
 
 
@@ -252,6 +262,20 @@ def rbmr_slots(cfg: dict, m: int) -> np.ndarray:
     js = np.zeros(nb * c.p, dtype=np.uint32)
     lib().oracle_rbmr_slots(C.byref(c), int(m), _p(js, C.c_uint32))
     return js
+
+
+def adj_value(cfg: dict, i: int, j: int) -> float:
+    return float(lib().oracle_adj_value(C.byref(make_cfg(cfg)), int(i), int(j)))
+
+
+def adj_pair_flow(cfg: dict, i: int, j: int, xi, xj, tau: float):
+    c = make_cfg(cfg)
+    xi = np.ascontiguousarray(xi, dtype=np.float64).reshape(c.d)
+    xj = np.ascontiguousarray(xj, dtype=np.float64).reshape(c.d)
+    yi, yj = np.zeros(c.d), np.zeros(c.d)
+    lib().oracle_adj_pair_flow(C.byref(c), int(i), int(j), _p(xi, C.c_double), _p(xj, C.c_double), float(tau),
+                               _p(yi, C.c_double), _p(yj, C.c_double))
+    return yi, yj
 
 
 def batch_update(cfg: dict, m: int, ids, xb) -> np.ndarray:

@@ -51,10 +51,16 @@ typedef struct {
   double iparam[8];
   double sigma, dt;
   uint64_t seed;
+  /* clustering model (Sec. 5.3, K_ADJ): symmetric adjacency a_ij in CSR,
+   * rows sorted by column; kparam = {alpha, beta, edge_restricted} */
+  const uint32_t* adj_rp;  /* n+1 row starts */
+  const uint32_t* adj_ci;  /* nnz column indices */
+  const double* adj_v;     /* nnz values a_ij >= 0 */
+  uint64_t adj_nnz;
 } oracle_cfg;
 
 enum { K_ZERO = 0, K_DYSON = 1, K_COULOMB = 2, K_BOUNDED_CONF = 3,
-       K_GAUSS_AR = 4, K_COULOMB_REG = 5, K_SMOOTH = 6, K_LINEAR = 7 };
+       K_GAUSS_AR = 4, K_COULOMB_REG = 5, K_SMOOTH = 6, K_LINEAR = 7, K_ADJ = 8 };
 enum { TAG_KEY = 0, TAG_NOISE = 1, TAG_INIT = 2, TAG_INIT_AUX = 3,
        TAG_SLOT = 4, TAG_NOISE_SLOT = 5 };
 
@@ -400,6 +406,38 @@ void oracle_pair_flow(const oracle_cfg* c, const double* xi, const double* xj,
   for (uint32_t k = 0; k < d; ++k) { yi[k] = mid[k] + 0.5 * Dn[k]; yj[k] = mid[k] - 0.5 * Dn[k]; }
 }
 
+/* ------------------------------------------------------------------ */
+/* clustering through the interacting particle system (Sec. 5.3,        */
+/* P:1240-1264): dX^i/dt = alpha (a_{i theta} - beta)(X^theta - X^i)     */
+/* for the picked pair, solved exactly (the update formula of P:1258-    */
+/* 1264): D' = D exp(-2 alpha (a_ij - beta) tau), midpoint kept.         */
+/* ------------------------------------------------------------------ */
+double oracle_adj_value(const oracle_cfg* c, uint32_t i, uint32_t j) {
+  uint32_t lo = c->adj_rp[i], hi = c->adj_rp[i + 1];  /* binary search of row i */
+  while (lo < hi) {
+    uint32_t mid = lo + (hi - lo) / 2;
+    if (c->adj_ci[mid] < j) lo = mid + 1; else hi = mid;
+  }
+  return (lo < c->adj_rp[i + 1] && c->adj_ci[lo] == j) ? c->adj_v[lo] : 0.0;
+}
+
+void oracle_adj_pair_flow(const oracle_cfg* c, uint32_t i, uint32_t j, const double* xi,
+                          const double* xj, double tau, double* yi, double* yj) {
+  double e = exp(-2.0 * c->kparam[0] * (oracle_adj_value(c, i, j) - c->kparam[1]) * tau);
+  for (uint32_t k = 0; k < c->d; ++k) {
+    double D = xi[k] - xj[k], sum = xi[k] + xj[k];
+    yi[k] = 0.5 * (sum + D * e);
+    yj[k] = 0.5 * (sum - D * e);
+  }
+}
+
+/* the pair flow of the configured kernel for members (i, j) */
+static void pair_flow_ids(const oracle_cfg* c, uint32_t i, uint32_t j, const double* xi,
+                          const double* xj, double* yi, double* yj) {
+  if (c->kernel == K_ADJ) oracle_adj_pair_flow(c, i, j, xi, xj, c->dt, yi, yj);
+  else oracle_pair_flow(c, xi, xj, c->dt, yi, yj);
+}
+
 /* split step, second half: x' = y - tau grad V(y) + sigma sqrt(tau) z;
  * multiplicative noise ("solved by the splitting strategy" P:1175):
  * the exact geometric Brownian motion step x' = w exp(sigma sqrt(tau) z - sigma^2 tau/2),
@@ -561,10 +599,35 @@ uint32_t oracle_slot_draw(const oracle_cfg* c, uint64_t s, uint32_t t, uint64_t 
   return (uint32_t)(((unsigned __int128)c->n * u) >> 64);
 }
 
+/* edge-restricted pick ("the random batch can be picked from those
+ * with nonzeros of a_ij only"): edge e = floor(nnz U64 / 2^64) of the CSR,
+ * i = its row, j = its column; redrawn (t += 1) on a diagonal entry */
+static void edge_draw(const oracle_cfg* c, uint64_t s0, uint64_t m, uint32_t* i, uint32_t* j) {
+  for (uint32_t t = 0;; ++t) {
+    uint32_t w[4];
+    philox_block(c, (uint32_t)s0, t, m, TAG_SLOT, w);
+    uint64_t u = (((uint64_t)w[0]) << 32) | w[1];
+    uint64_t e = (uint64_t)(((unsigned __int128)c->adj_nnz * u) >> 64);
+    uint32_t lo = 0, hi = (uint32_t)c->n;  /* row: largest r with adj_rp[r] <= e */
+    while (hi - lo > 1) {
+      uint32_t mid = lo + (hi - lo) / 2;
+      if (c->adj_rp[mid] <= e) lo = mid; else hi = mid;
+    }
+    *i = lo;
+    *j = c->adj_ci[e];
+    if (*i != *j) return;
+  }
+}
+
 int oracle_rbmr_slots(const oracle_cfg* c, uint64_t m, uint32_t* js) {
   uint64_t n = c->n;
   uint32_t p = c->p;
   uint64_t nb = (n + p - 1) / p;
+  if (c->kernel == K_ADJ && c->kparam[2] != 0.0) {
+    if (p != 2) return 1;
+    for (uint64_t b = 0; b < nb; ++b) edge_draw(c, b * p, m, &js[b * p], &js[b * p + 1]);
+    return 0;
+  }
   for (uint64_t b = 0; b < nb; ++b) {
     for (uint32_t l = 0; l < p; ++l) {
       uint64_t s = b * p + l;
@@ -614,7 +677,7 @@ int oracle_rbmr_step(const oracle_cfg* c, uint64_t m, double* x) {
     } else {
       uint32_t i = js[s0], j = js[s0 + 1];
       double yi[3], yj[3], z[3], xn[3];
-      oracle_pair_flow(c, x + (uint64_t)i * d, x + (uint64_t)j * d, c->dt, yi, yj);
+      pair_flow_ids(c, i, j, x + (uint64_t)i * d, x + (uint64_t)j * d, yi, yj);
       normals(c, c->fp32, (uint32_t)s0, m, TAG_NOISE_SLOT, z);
       oracle_cfg c2 = *c; c2.constraint = 0;
       split_member(&c2, yi, z, xn);
@@ -674,7 +737,7 @@ int oracle_rbmr_seq_step(const oracle_cfg* c, uint64_t m, double* x) {
     } else {
       uint32_t i = js[s0], j = js[s0 + 1];
       double y[2][3], z[3];
-      oracle_pair_flow(c, x + (uint64_t)i * d, x + (uint64_t)j * d, c->dt, y[0], y[1]);
+      pair_flow_ids(c, i, j, x + (uint64_t)i * d, x + (uint64_t)j * d, y[0], y[1]);
       for (uint32_t l = 0; l < 2; ++l) {
         normals(c, c->fp32, (uint32_t)(s0 + l), m, TAG_NOISE_SLOT, z);
         split_member(c, y[l], z, xo + (uint64_t)l * d);

@@ -288,6 +288,22 @@ rbm_status rbm_init(const rbm_config* cfg, void* wsp, size_t ws_bytes, void* cud
   return RBM_OK;
 }
 
+rbm_status rbm_set_adjacency(rbm_ctx* c, const uint32_t* row_ptr, const uint32_t* col_idx, const double* val,
+                             uint64_t nnz) {
+  if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
+  if (c->cfg.kernel != RBM_K_ADJACENCY) return fail(c, RBM_ERR_STATE, "not an adjacency-kernel context");
+  if (!row_ptr || !col_idx || !val || nnz == 0 || nnz >= (1ull << 32))
+    return fail(c, RBM_ERR_INVALID_ARG, "adjacency: NULL array or nnz=%llu not in 1..2^32-1", (unsigned long long)nnz);
+  c->P.adj_rp = row_ptr;
+  c->P.adj_ci = col_idx;
+  c->P.adj_v = val;
+  c->P.adj_nnz = nnz;
+  c->P.adj_edges = c->cfg.kparam[2] != 0.0 ? 1u : 0u;
+  for (int i = 0; i < 4; ++i)  // kernel parameters changed: recapture
+    if (c->graph[i]) { cudaGraphExecDestroy(c->graph[i]); c->graph[i] = nullptr; }
+  return RBM_OK;
+}
+
 rbm_status rbm_set_state(rbm_ctx* c, const void* x, uint32_t where) {
   if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
   if (!x) return fail(c, RBM_ERR_INVALID_ARG, "x is NULL");
@@ -308,6 +324,8 @@ rbm_status rbm_set_state(rbm_ctx* c, const void* x, uint32_t where) {
 }
 
 static rbm_status not_partitioned(rbm_ctx* c) {
+  if (c->cfg.kernel == RBM_K_ADJACENCY && !c->P.adj_rp)
+    return fail(c, RBM_ERR_STATE, "adjacency kernel: call rbm_set_adjacency before stepping");
   if (is_partitioned(c->cfg) && !c->comm)
     return fail(c, RBM_ERR_STATE, "partitioned context (world_size %d) without a communicator: step with rbm_part_phase1/2 and the exchanges, or pass an NCCL id to rbm_init", c->cfg.world_size);
   return RBM_OK;

@@ -13,7 +13,7 @@ namespace rbm {
 enum : uint32_t { TAG_KEY = 0, TAG_NOISE = 1, TAG_INIT = 2, TAG_INIT_AUX = 3,
                   TAG_SLOT = 4, TAG_NOISE_SLOT = 5 };
 enum : int { KK_ZERO = 0, KK_DYSON = 1, KK_COULOMB = 2, KK_BOUNDED = 3,
-             KK_GAUSS_AR = 4, KK_COULOMB_REG = 5, KK_SMOOTH = 6, KK_LINEAR = 7 };
+             KK_GAUSS_AR = 4, KK_COULOMB_REG = 5, KK_SMOOTH = 6, KK_LINEAR = 7, KK_ADJ = 8 };
 
 // exact u32 division by a runtime-invariant divisor (Granlund-Montgomery):
 // q = n / d for every 32-bit n.
@@ -80,6 +80,13 @@ struct DevParams {
   // so that the run reservations of concurrent CTAs do not serialise on one
   // L2 atomic address per digit
   uint32_t segk, segmask;
+  // clustering model (Sec. 5.3, KK_ADJ): symmetric adjacency in CSR (caller-owned,
+  // device), kparam = {alpha, beta, edge_restricted}
+  const uint32_t* adj_rp;
+  const uint32_t* adj_ci;
+  const double* adj_v;
+  uint64_t adj_nnz;
+  uint32_t adj_edges;       // RBM-r pairs drawn among the edges only
   const uint64_t* step;     // device step counter m
   unsigned long long* nonfinite;  // atomicMin of (m<<32 | id); ~0 if clean
   uint32_t* capacity_err;         // set to 1 if a bucket overflowed every fallback
@@ -599,6 +606,47 @@ __device__ __forceinline__ void member_update(const T (&x)[D], const T (&f)[D], 
                                               const DevParams& P, bool vstart) {
   if (INTEG == 2) verlet_update<T, D>(x, f, xn, P, vstart);
   else em_update<T, D>(x, f, z, xn, P, true);
+}
+
+// ------------------------------------------- clustering model (KK_ADJ)
+// a_ij of the CSR adjacency (rows sorted by column; 0 off the pattern)
+__device__ __forceinline__ double adj_value(const DevParams& P, uint32_t i, uint32_t j) {
+  uint32_t lo = P.adj_rp[i], hi = P.adj_rp[i + 1];
+  const uint32_t end = hi;
+  while (lo < hi) {
+    const uint32_t mid = lo + (hi - lo) / 2;
+    if (P.adj_ci[mid] < j) lo = mid + 1; else hi = mid;
+  }
+  return (lo < end && P.adj_ci[lo] == j) ? P.adj_v[lo] : 0.0;
+}
+// exact flow of dX^i/dt = alpha (a_ij - beta)(X^j - X^i) over tau (the update
+// formula of PAPER.md:1258-1264): y = ((x_i + x_j) +- (x_i - x_j) e) / 2,
+// e = exp(-2 alpha (a_ij - beta) tau) evaluated in fp64
+template <typename T, int D>
+__device__ __forceinline__ void adj_flow(const DevParams& P, uint32_t i, uint32_t j, const T (&xi)[D],
+                                         const T (&xj)[D], bool first, T (&y)[D]) {
+  const T e = (T)exp(-2.0 * P.kp0 * (adj_value(P, i, j) - P.kp1) * P.dt);
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    const T Dv = xi[c] - xj[c], sum = xi[c] + xj[c];
+    y[c] = T(0.5) * (first ? sum + Dv * e : sum - Dv * e);
+  }
+}
+// edge-restricted pick: edge e = floor(nnz U64 / 2^64), its row and
+// column; redrawn on a diagonal entry
+__device__ __forceinline__ void adj_edge_draw(const DevParams& P, uint64_t s0, uint32_t m, uint32_t& i, uint32_t& j) {
+  for (uint32_t t = 0;; ++t) {
+    const uint4 w = block_at(P, (uint32_t)s0, t, m, TAG_SLOT);
+    const uint64_t e = __umul64hi(P.adj_nnz, (((uint64_t)w.x) << 32) | w.y);
+    uint32_t lo = 0, hi = (uint32_t)P.n;
+    while (hi - lo > 1) {
+      const uint32_t mid = lo + (hi - lo) / 2;
+      if (P.adj_rp[mid] <= e) lo = mid; else hi = mid;
+    }
+    i = lo;
+    j = P.adj_ci[e];
+    if (i != j) return;
+  }
 }
 
 template <typename T, int D>

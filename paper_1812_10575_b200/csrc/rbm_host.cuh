@@ -274,7 +274,13 @@ inline rbm_status validate(const rbm_config* cfg) {
       return fail(c, RBM_ERR_UNSUPPORTED, "Verlet: RBM-1 without constraint");
     if (k.state_form > 1) return fail(c, RBM_ERR_INVALID_ARG, "state_form %u", k.state_form);
   }
-  if (k.kernel > RBM_K_LINEAR) return fail(c, RBM_ERR_UNKNOWN_KERNEL, "kernel %u not in registry", k.kernel);
+  if (k.kernel > RBM_K_ADJACENCY) return fail(c, RBM_ERR_UNKNOWN_KERNEL, "kernel %u not in registry", k.kernel);
+  if (k.kernel == RBM_K_ADJACENCY) {
+    if (k.scheme == RBM_SCHEME_RBM1 || k.p != 2 || k.integrator != RBM_INTEG_SPLIT_EXACT_PAIR || k.world_size != 1)
+      return fail(c, RBM_ERR_UNSUPPORTED, "adjacency (clustering) kernel: RBM-r or RBM-r', p = 2, split integrator, one GPU");
+    if (!std::isfinite(k.kparam[0]) || !std::isfinite(k.kparam[1]))
+      return fail(c, RBM_ERR_INVALID_ARG, "adjacency kernel needs finite kparam = {alpha, beta}");
+  }
   if (k.noise > RBM_NOISE_GEOMETRIC) return fail(c, RBM_ERR_INVALID_ARG, "noise %u", k.noise);
   if (k.potential > RBM_V_HARMONIC) return fail(c, RBM_ERR_UNKNOWN_KERNEL, "potential %u not in registry", k.potential);
   if (k.constraint > RBM_CONSTRAINT_UNIT_SPHERE) return fail(c, RBM_ERR_INVALID_ARG, "constraint %u", k.constraint);
@@ -283,8 +289,9 @@ inline rbm_status validate(const rbm_config* cfg) {
   if (k.constraint == RBM_CONSTRAINT_UNIT_SPHERE && k.d != 3) return fail(c, RBM_ERR_INVALID_ARG, "sphere constraint needs d=3");
   if (k.integrator == RBM_INTEG_SPLIT_EXACT_PAIR) {
     if (k.p != 2) return fail(c, RBM_ERR_INVALID_ARG, "split integrator needs p=2");
-    if (k.kernel != RBM_K_DYSON && k.kernel != RBM_K_COULOMB && !(k.kernel == RBM_K_LINEAR && k.d == 1))
-      return fail(c, RBM_ERR_INVALID_ARG, "split integrator needs the Dyson, Coulomb or (d=1) linear kernel");
+    if (k.kernel != RBM_K_DYSON && k.kernel != RBM_K_COULOMB && !(k.kernel == RBM_K_LINEAR && k.d == 1) &&
+        k.kernel != RBM_K_ADJACENCY)
+      return fail(c, RBM_ERR_INVALID_ARG, "split integrator needs the Dyson, Coulomb, (d=1) linear or adjacency kernel");
     if (k.scheme == RBM_SCHEME_RBM1 && (k.n % 2))
       return fail(c, RBM_ERR_INVALID_ARG, "split integrator with RBM-1 needs even n");
   }
@@ -883,6 +890,7 @@ EngineBase* make_for_kernel(uint32_t kernel, uint32_t integ) {
     case RBM_K_COULOMB:
       if constexpr (D == 3) return integ ? (EngineBase*)new Engine<T, 3, KK_COULOMB, 1>() : new Engine<T, 3, KK_COULOMB, 0>();
       return nullptr;
+    case RBM_K_ADJACENCY: return integ == RBM_INTEG_SPLIT_EXACT_PAIR ? new Engine<T, D, KK_ADJ, 1>() : nullptr;
     case RBM_K_LINEAR:
       if constexpr (D == 1) {
         if (integ) return new Engine<T, 1, KK_LINEAR, 1>();

@@ -1711,14 +1711,18 @@ static __global__ void __launch_bounds__(128) rbmr_batch_kernel(const __grid_con
          b += (uint64_t)gridDim.x * blockDim.x) {
       const uint64_t s0 = 2 * b;
       uint32_t j0, j1;
-      {
-        const uint4 w = block_at(P, (uint32_t)s0, 0u, m, TAG_SLOT);
-        j0 = (uint32_t)__umul64hi(P.n, (((uint64_t)w.x) << 32) | w.y);
-      }
-      for (uint32_t t = 0;; ++t) {
-        const uint4 w = block_at(P, (uint32_t)(s0 + 1), t, m, TAG_SLOT);
-        j1 = (uint32_t)__umul64hi(P.n, (((uint64_t)w.x) << 32) | w.y);
-        if (j1 != j0) break;
+      if (KK == KK_ADJ && P.adj_edges) {
+        adj_edge_draw(P, s0, m, j0, j1);
+      } else {
+        {
+          const uint4 w = block_at(P, (uint32_t)s0, 0u, m, TAG_SLOT);
+          j0 = (uint32_t)__umul64hi(P.n, (((uint64_t)w.x) << 32) | w.y);
+        }
+        for (uint32_t t = 0;; ++t) {
+          const uint4 w = block_at(P, (uint32_t)(s0 + 1), t, m, TAG_SLOT);
+          j1 = (uint32_t)__umul64hi(P.n, (((uint64_t)w.x) << 32) | w.y);
+          if (j1 != j0) break;
+        }
       }
       T x0[D], x1[D];
       load4<T, D>(xa, j0, x0);
@@ -1745,8 +1749,13 @@ static __global__ void __launch_bounds__(128) rbmr_batch_kernel(const __grid_con
         em_update<T, D>(x1, f1, z1, y1, P, false);
       } else {
         T a[D], bb[D];
-        pair_flow<T, D, KK>(x0, x1, true, a, P);
-        pair_flow<T, D, KK>(x0, x1, false, bb, P);
+        if (KK == KK_ADJ) {
+          adj_flow<T, D>(P, j0, j1, x0, x1, true, a);
+          adj_flow<T, D>(P, j0, j1, x0, x1, false, bb);
+        } else {
+          pair_flow<T, D, KK>(x0, x1, true, a, P);
+          pair_flow<T, D, KK>(x0, x1, false, bb, P);
+        }
         split_finish<T, D>(a, z0, y0, P, false);
         split_finish<T, D>(bb, z1, y1, P, false);
       }
@@ -1892,10 +1901,13 @@ static __global__ void __launch_bounds__(128) rbmr_draw_reg_kernel(const __grid_
   for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nbatch;
        b += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t s0 = b * p;
+    uint32_t e0 = 0, e1 = 0;
+    if (P.adj_edges) adj_edge_draw(P, s0, m, e0, e1);  // clustering model, p = 2
     for (uint32_t l = 0; l < p; ++l) {
       const uint64_t s = s0 + l;
       uint32_t t = 0, j;
       for (;;) {
+        if (P.adj_edges) { j = l ? e1 : e0; break; }
         const uint4 w = block_at(P, (uint32_t)s, t, m, TAG_SLOT);
         j = (uint32_t)__umul64hi(P.n, (((uint64_t)w.x) << 32) | w.y);
         bool dup = false;
@@ -2047,14 +2059,16 @@ static __global__ void __launch_bounds__(128) rbmr_seq_apply_kernel(const __grid
       load4<T, D>(xa, j, xj);
 #pragma unroll
       for (int c = 0; c < D; ++c) z[c] = T(0);
-      pair_flow<T, D, KK>(xi, xj, true, y, P);
+      if (KK == KK_ADJ) adj_flow<T, D>(P, i, j, xi, xj, true, y);
+      else pair_flow<T, D, KK>(xi, xj, true, y, P);
       if (P.has_noise) Normals<T, D>::get(P, (uint32_t)s0, m, TAG_NOISE_SLOT, z);
       split_finish<T, D>(y, z, xn, P, true);
       check_finite<T, D>(xn, P, i, m);
       T yj[D], xnj[D];
 #pragma unroll
       for (int c = 0; c < D; ++c) z[c] = T(0);
-      pair_flow<T, D, KK>(xi, xj, false, yj, P);
+      if (KK == KK_ADJ) adj_flow<T, D>(P, i, j, xi, xj, false, yj);
+      else pair_flow<T, D, KK>(xi, xj, false, yj, P);
       if (P.has_noise) Normals<T, D>::get(P, (uint32_t)(s0 + 1), m, TAG_NOISE_SLOT, z);
       split_finish<T, D>(yj, z, xnj, P, true);
       check_finite<T, D>(xnj, P, j, m);

@@ -22,7 +22,7 @@ STATUS = {0: "RBM_OK", 1: "RBM_ERR_INVALID_ARG", 2: "RBM_ERR_UNKNOWN_KERNEL",
           3: "RBM_ERR_UNSUPPORTED", 4: "RBM_ERR_WORKSPACE", 5: "RBM_ERR_CUDA",
           6: "RBM_ERR_NCCL", 7: "RBM_ERR_NONFINITE", 8: "RBM_ERR_STATE", 9: "RBM_ERR_CAPACITY"}
 KERNELS = {"zero": 0, "dyson": 1, "coulomb": 2, "bounded_confidence": 3,
-           "gauss_attr_rep": 4, "coulomb_reg": 5, "smooth": 6, "linear": 7}
+           "gauss_attr_rep": 4, "coulomb_reg": 5, "smooth": 6, "linear": 7, "adjacency": 8}
 INITS = {"user": 0, "normal": 1, "box": 2, "sphere": 3, "mixture": 4, "abs_normal": 5}
 NOISES = {"additive": 0, "geometric": 1}
 MEM_DEVICE, MEM_HOST = 0, 1
@@ -32,7 +32,7 @@ EXPORTS = ["rbm_workspace_size", "rbm_init", "rbm_set_state", "rbm_step", "rbm_r
            "rbm_destroy", "rbm_kernel_name", "rbm_timing_begin", "rbm_timing_end",
            "rbm_part_info_get", "rbm_part_prologue", "rbm_part_phase1", "rbm_part_phase2",
            "rbm_part_set_peers", "rbm_part_map_peers", "rbm_get_nccl_unique_id", "rbm_gather_local",
-           "rbm_part_phase",
+           "rbm_part_phase", "rbm_set_adjacency",
            "rbm_direct_workspace_size", "rbm_direct_reset", "rbm_direct_run", "rbm_direct_sync"]
 
 
@@ -88,6 +88,7 @@ def lib():
             "rbm_get_nccl_unique_id": (st, [vp]),
             "rbm_gather_local": (st, [vp, vp, vp, C.POINTER(u64)]),
             "rbm_part_map_peers": (st, [vp]),
+            "rbm_set_adjacency": (st, [vp, vp, vp, vp, u64]),
             "rbm_direct_workspace_size": (st, [cfgp, C.POINTER(C.c_size_t)]),
             "rbm_direct_reset": (st, [cfgp, vp, vp]),
             "rbm_direct_run": (st, [cfgp, vp, u64, u64, vp, C.c_size_t, vp]),
@@ -260,6 +261,15 @@ class RBM:
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
         self.stream = torch.cuda.current_stream(self.device)
         self.ctx = rbm_init(self.c, self.ws.data_ptr(), self.ws_bytes, self.stream.cuda_stream, nccl_id)
+        adj = self.cfg.get("adjacency")
+        if adj is not None:  # clustering model: CSR adjacency uploaded once, kept by this object
+            rp, ci, v = adj[0], adj[1], adj[2]
+            self._adj = (torch.as_tensor(rp.astype("int64")).to(torch.int32).to(self.device),
+                         torch.as_tensor(ci.astype("int64")).to(torch.int32).to(self.device),
+                         torch.as_tensor(v, dtype=torch.float64).to(self.device))
+            _check(lib().rbm_set_adjacency(self.ctx, C.c_void_p(self._adj[0].data_ptr()),
+                                           C.c_void_p(self._adj[1].data_ptr()),
+                                           C.c_void_p(self._adj[2].data_ptr()), len(ci)), self.ctx)
         if x0 is not None:
             self.set_state(x0)
 

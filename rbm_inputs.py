@@ -97,6 +97,36 @@ def second_order(n: int = 2**24, p: int = 2, seed: int = 1, scheme: str = "rbm1"
                 dt=2.0 ** -7, seed=seed, init="normal", iparam=[0.0, 1.0], state_form="xv", steps=100)
 
 
+def sbm_adjacency(sizes=(200, 400, 600), p_in: float = 0.7, q_out: float = 0.3, seed: int = 1):
+    """Stochastic block model: symmetric 0/1 adjacency,
+    P(a_ij = 1) = p_in inside a block, q_out across, no self loops; CSR with
+    rows sorted by column: (row_ptr u32, col u32, val f64), plus the labels."""
+    rng = np.random.default_rng(seed)
+    n = int(sum(sizes))
+    lab = np.repeat(np.arange(len(sizes)), sizes)
+    prob = np.where(lab[:, None] == lab[None, :], p_in, q_out)
+    up = np.triu(rng.random((n, n)) < prob, 1)
+    a = up | up.T
+    rows, cols = np.nonzero(a)
+    rp = np.zeros(n + 1, dtype=np.uint32)
+    np.cumsum(np.bincount(rows, minlength=n), out=rp[1:])
+    return (rp, cols.astype(np.uint32), np.ones(len(cols))), lab
+
+
+def cluster_sbm(d: int = 2, seed: int = 1, graph_seed: int = 1, edge_restricted: bool = False,
+                scheme: str = "rbmr", dtype: str = "f64") -> dict:
+    """Clustering through the particle system (Sec. 5.3): SBM with
+    N = 1200 (200/400/600, p = 0.7, q = 0.3), alpha = 40, beta = 1/2,
+    tau = 1e-3, X_0 ~ U[0, 50]^d, RBM-r with p = 2 and the exact pair update
+    (P:1258-1264); one step = N/2 pair picks = tau.  d = 2 (reading
+    D:26): each coordinate follows the paper's dynamics with the same picks."""
+    adj, lab = sbm_adjacency(seed=graph_seed)
+    return dict(d=d, n=1200, p=2, dtype=dtype, scheme=scheme, integrator="split", kernel="adjacency",
+                kparam=[40.0, 0.5, 1.0 if edge_restricted else 0.0], potential="none", vparam=[1.0],
+                constraint="none", sigma=0.0, dt=1e-3, seed=seed, init="box", iparam=[0.0, 50.0],
+                adjacency=adj, labels=lab, steps=5000)
+
+
 ALL = {"C1": c1_dyson, "C2": c2_sphere, "C3": c3_opinion, "C4": c4_aggregation, "C5": c5_coulomb_reg,
        "verlet": second_order}
 

@@ -800,3 +800,123 @@ def test_bounded_confidence_closed_window(O):
         x = np.array([[0.0], [1.0]])
         y = O.rbm1_step(base, x, 0)
         assert np.allclose(y.ravel(), [0.4, 0.6], atol=1e-15)  # x -+ dt * 40 * 1
+
+
+# ------------------------- clustering through the particle system (Sec. 5.3)
+def _tiny_graph():
+    """n = 5, symmetric weighted adjacency (a_ij >= 0) in CSR and dense."""
+    dense = np.zeros((5, 5))
+    for i, j, a in [(0, 1, 1.0), (0, 2, 0.3), (1, 3, 2.0), (2, 4, 0.5), (3, 4, 1.0), (0, 4, 0.1)]:
+        dense[i, j] = dense[j, i] = a
+    rows, cols = np.nonzero(dense)
+    rp = np.zeros(6, dtype=np.uint32)
+    np.cumsum(np.bincount(rows, minlength=5), out=rp[1:])
+    return (rp, cols.astype(np.uint32), dense[rows, cols]), dense
+
+
+def _adj_cfg(**kw):
+    adj, _ = _tiny_graph()
+    c = dict(d=2, n=5, p=2, dtype="f64", scheme="rbmr", integrator="split", kernel="adjacency",
+             kparam=[40.0, 0.5, 0.0], potential="none", vparam=[1.0], constraint="none", sigma=0.0,
+             dt=1e-3, seed=5, init="box", iparam=[0.0, 50.0], adjacency=adj)
+    c.update(kw)
+    return c
+
+
+def test_adj_value_matches_dense(O):
+    _, dense = _tiny_graph()
+    c = _adj_cfg()
+    for i in range(5):
+        for j in range(5):
+            assert O.adj_value(c, i, j) == dense[i, j]
+
+
+@pytest.mark.parametrize("i,j", [(0, 1), (0, 2), (1, 3), (2, 4), (1, 2)])
+def test_adj_pair_flow_exact(O, i, j):
+    """P:1258-1264 is the exact flow of dX^i/dt = alpha (a_ij - beta)(X^j - X^i)
+    (P:1252): RK4 of the pair ODE agrees to 1e-10; the midpoint is kept; the
+    pair contracts for a_ij > beta and separates for a_ij < beta."""
+    _, dense = _tiny_graph()
+    c = _adj_cfg()
+    alpha, beta, tau = 40.0, 0.5, 1e-3
+    xi, xj = np.array([3.0, -1.0]), np.array([-2.0, 4.5])
+    yi, yj = O.adj_pair_flow(c, i, j, xi, xj, tau)
+    k = alpha * (dense[i, j] - beta)
+
+    def f(u):
+        a, b = u[:2], u[2:]
+        return np.concatenate([k * (b - a), k * (a - b)])
+    u, h = np.concatenate([xi, xj]), tau / 2000
+    for _ in range(2000):
+        k1 = f(u); k2 = f(u + h / 2 * k1); k3 = f(u + h / 2 * k2); k4 = f(u + h * k3)
+        u = u + h / 6 * (k1 + 2 * k2 + 2 * k3 + k4)
+    assert np.max(np.abs(np.concatenate([yi, yj]) - u)) < 1e-10
+    assert np.allclose(yi + yj, xi + xj, atol=1e-13)
+    d0, d1 = np.linalg.norm(xi - xj), np.linalg.norm(yi - yj)
+    if dense[i, j] == beta:
+        assert abs(d1 - d0) < 1e-12
+    else:
+        assert (d1 < d0) if dense[i, j] > beta else (d1 > d0)
+
+
+def test_adj_rbmr_step_conserves_sum(O):
+    """Every pair update keeps the pair's sum, so a Jacobi sweep keeps sum_i X^i."""
+    c = _adj_cfg()
+    x = O.init(c)
+    for m in range(20):
+        y = O.rbmr_step(c, x, m)
+        assert np.allclose(y.sum(0), x.sum(0), rtol=0, atol=1e-10)
+        x = y
+
+
+def test_adj_edge_restricted_slots(O):
+    """pairs picked among the nonzeros of A only, uniformly over the
+    nnz (directed) entries (chi^2)."""
+    adj, dense = _tiny_graph()
+    c = _adj_cfg(kparam=[40.0, 0.5, 1.0], n=5)
+    nnz = len(adj[1])
+    cnt = {}
+    for m in range(8000):
+        js = O.rbmr_slots(c, m)
+        for b in range(len(js) // 2):
+            i, j = int(js[2 * b]), int(js[2 * b + 1])
+            assert dense[i, j] > 0
+            cnt[(i, j)] = cnt.get((i, j), 0) + 1
+    obs = np.array(list(cnt.values()), dtype=float)
+    assert len(obs) == nnz
+    assert stats.chisquare(obs).pvalue > 1e-4
+
+
+def _mean_field_unstable(adj, n, alpha, beta, k=2):
+    """Top-k eigenvectors of the mean-field generator -alpha/(N-1) L_W,
+    W_ij = a_ij - beta (i != j): the modes the linear dynamics amplifies."""
+    rp, ci, v = adj
+    A = np.zeros((n, n))
+    A[np.repeat(np.arange(n), np.diff(rp.astype(np.int64))), ci.astype(np.int64)] = v
+    W = A - beta
+    np.fill_diagonal(W, 0.0)
+    L = np.diag(W.sum(1)) - W
+    ev, V = np.linalg.eigh(-alpha / (n - 1) * L)
+    return ev[-k:], V[:, -k:]
+
+
+def test_sbm_clusters_recovered_by_oracle(O):
+    """The paper's SBM experiment (N = 1200 in blocks 200/400/600,
+    p = 0.7, q = 0.3, alpha = 40, beta = 1/2, tau = 1e-3, X_0 ~ U[0, 50]) with
+    RBM-r p = 2 to T = 5: (i) each coordinate of the centred positions lies in
+    the dominant unstable subspace of the mean-field linear dynamics
+    (projection >= 0.85; two nearly degenerate unstable modes, both constant
+    on the blocks); (ii) 3-means of the whitened 2-D positions recovers the
+    blocks (ARI >= 0.95)."""
+    from sklearn.cluster import KMeans
+    from sklearn.metrics import adjusted_rand_score
+    c = RI.cluster_sbm(seed=3)
+    ev, V = _mean_field_unstable(c["adjacency"], 1200, 40.0, 0.5)
+    assert ev[0] > 0 and ev[1] > 0
+    x = O.run(c, O.init(c), 0, 5000)
+    z = x - x.mean(0)
+    for a in range(2):
+        assert np.linalg.norm(V.T @ z[:, a]) ** 2 / np.dot(z[:, a], z[:, a]) >= 0.85
+    w = np.linalg.cholesky(np.linalg.inv(np.cov(z.T)))
+    lab = KMeans(3, n_init=10, random_state=0).fit(z @ w).labels_
+    assert adjusted_rand_score(c["labels"], lab) >= 0.95

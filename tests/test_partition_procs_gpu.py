@@ -61,6 +61,11 @@ def _worker(rank, world, port, kind, fused, q):
         dist.all_gather_object(out, (ids.cpu().numpy(), x.cpu().numpy(), mapped))
         if rank == 0:
             q.put(out)
+        # release the peer mappings on every rank before any rank frees the
+        # workspace it exported (CUDA IPC producer/consumer order)
+        torch.cuda.synchronize()
+        ps.exchange._peer_tensors.clear()
+        dist.barrier()
         ps.close()
     except Exception as e:  # report instead of hanging the parent
         if rank == 0:
