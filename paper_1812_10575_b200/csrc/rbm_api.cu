@@ -54,6 +54,7 @@ rbm_status check_flags(rbm_ctx* c) {
 // none when the kernels store into the peers' buffers) of the partitioned
 // step, on the stream, over the library's communicator (include/rbm.h).
 rbm_status part_exchange_cr(rbm_ctx* c, cudaStream_t s) {
+  Nvtx range_("nccl_counts_records");
   NcclApi& N = nccl();
   const int G = c->cfg.world_size;
   NC(N.AllGather(c->counts_send, c->counts_all, c->L.nseg(), ncclUint32, c->comm, s));
@@ -73,6 +74,7 @@ rbm_status part_exchange_cr(rbm_ctx* c, cudaStream_t s) {
 // records of the batch crossing O_{r+1}, the regroup is the
 // step's only synchronisation point)
 rbm_status part_exchange_h(rbm_ctx* c, cudaStream_t s) {
+  Nvtx range_("nccl_halo");
   NcclApi& N = nccl();
   const int G = c->cfg.world_size, r = c->cfg.rank;
   const size_t hb = 16 + (size_t)HALO_MAX * rec_bytes(c->cfg);
@@ -86,6 +88,7 @@ rbm_status part_exchange_h(rbm_ctx* c, cudaStream_t s) {
 // RBM-r exchange a (0 requests, 1 responses, 2 increments): chunk j of the
 // send region to rank j, chunk j of the receive region from rank j
 rbm_status rbmr_exchange(rbm_ctx* c, cudaStream_t s, int a) {
+  Nvtx range_("nccl_rbmr_alltoall");
   NcclApi& N = nccl();
   const RPart& R = c->rp;
   const unsigned char* sr[3][2] = {{R.qs, R.qr}, {R.ps, R.pr}, {R.is, R.ir}};
@@ -351,6 +354,7 @@ rbm_status rbm_step(rbm_ctx* c) {
 
 rbm_status rbm_run(rbm_ctx* c, uint64_t nsteps) {
   if (!c) return fail(nullptr, RBM_ERR_INVALID_ARG, "ctx is NULL");
+  Nvtx range_("rbm_run");
   if (rbm_status e = not_partitioned(c)) return e;
   if (c->step + nsteps >= (1ull << 32)) return fail(c, RBM_ERR_INVALID_ARG, "step index would exceed 2^32");
   // steps per graph: even when a step flips the ping-pong buffers

@@ -16,6 +16,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/rbm.h"
 #include "rbm_kernels.cuh"
 #include "rbm_nccl.cuh"
@@ -25,6 +27,13 @@ using namespace rbm;
 namespace rbmhost {
 
 extern thread_local std::string g_err;  // failures without a context
+
+// NVTX range around a host-side sub-step (seen by Nsight Systems / ncu --nvtx;
+// a no-op unless a tool is attached)
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
 
 struct Workspace {
   unsigned char* base = nullptr;
@@ -592,6 +601,7 @@ struct Engine final : EngineBase {
 
   // pass 2: pass-1 buckets/segments (capacity cap1, counts cnt1 strided) -> final buckets
   void split2(rbm_ctx& c, cudaStream_t s, State<T, D> in, State<T, D> out, const uint32_t* cnt1) {
+    Nvtx r_("split");
     split_kernel<T, D, SPLIT_BLOCK><<<(unsigned)num_sms, SPLIT_BLOCK, sp_smem, s>>>(
         c.P, in, out, c.cur2, c.L.cap2, cnt1, c.tile_off, c.L.cap1);
   }
@@ -600,6 +610,7 @@ struct Engine final : EngineBase {
 
   void fused(rbm_ctx& c, cudaStream_t s, State<T, D> in, const OutDst<T, D>& out, uint32_t ocap,
              uint32_t* cur_next) {
+    Nvtx r_("bucket_step");
     if (pair_mode)
       bucket_kernel<T, D, KK, INTEG, MODE_PAIR, MINB>
           <<<c.L.nbuckets, BUCKET_BLOCK, bk_smem, s>>>(c.P, in, c.L.cap2, c.S, out, ocap, cur_next);
@@ -616,6 +627,7 @@ struct Engine final : EngineBase {
   }
 
   void step(rbm_ctx& c, cudaStream_t s) override {
+    Nvtx range_("rbm_step");
     if (c.cfg.scheme == RBM_SCHEME_RBMR) { step_rbmr(c, s); return; }
     if (c.cfg.scheme == RBM_SCHEME_RBMR_SEQ) { step_rbmr_seq(c, s); return; }
     const DevParams& P = c.P;
@@ -629,6 +641,7 @@ struct Engine final : EngineBase {
     // capacity of the buckets the state of a step lives in (pass-1 or final)
     const uint32_t pcap = L.b2 ? L.cap1 : L.cap2;
     if (!c.partitioned) {  // prologue: any storage order -> gapped buckets of step m
+      Nvtx r_("prologue");
       cudaMemsetAsync(c.cur1[q], 0, (size_t)L.nseg() * CUR1_STRIDE * 4, s);
       prologue(c, s, st(c, c.cur), od(st(c, c.cur ^ 1)), c.cur1[q], pcap, n);
       c.cur ^= 1;
@@ -699,6 +712,7 @@ struct Engine final : EngineBase {
   //                        all-to-all of B's records into C (equal chunks)
   //   phase1            -> halo_send of rank r to halo_recv of rank r+1
   void part_prologue(rbm_ctx& c, cudaStream_t s) override {
+    Nvtx range_("rbm_part_prologue");
     cudaMemsetAsync(c.cur1[0], 0, (size_t)c.L.nseg() * CUR1_STRIDE * 4, s);
     prologue(c, s, st(c, 0), part_dst(c, c.step), c.cur1[0], c.L.cap1, c.n0);
     pack_counts_kernel<<<1, 1024, 0, s>>>(c.cur1[0], c.L.nseg(), c.counts_send);
@@ -706,6 +720,7 @@ struct Engine final : EngineBase {
   }
 
   void part_phase1(rbm_ctx& c, cudaStream_t s) override {
+    Nvtx range_("rbm_part_phase1");
     const DevParams& P = c.P;
     const Layout& L = c.L;
     const uint32_t G = (uint32_t)c.cfg.world_size, rank = (uint32_t)c.cfg.rank;
@@ -726,6 +741,7 @@ struct Engine final : EngineBase {
   }
 
   void part_phase2(rbm_ctx& c, cudaStream_t s) override {
+    Nvtx range_("rbm_part_phase2");
     const DevParams& P = c.P;
     const Layout& L = c.L;
     c.mark(s);
@@ -742,6 +758,8 @@ struct Engine final : EngineBase {
   }
 
   void rbmr_part_phase(rbm_ctx& c, cudaStream_t s, int k) override {
+    static const char* const names[5] = {"", "rbmr_request", "rbmr_serve", "rbmr_delta", "rbmr_apply"};
+    Nvtx range_(names[k < 1 || k > 4 ? 0 : k]);
     const DevParams& P = c.P;
     RPart& R = c.rp;
     T* xa = reinterpret_cast<T*>(c.rxa);

@@ -11,6 +11,7 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs the CUDA path through the C ABI)")
     config.addinivalue_line("markers", "slow: long statistical run")
+    config.addinivalue_line("markers", "sanitizer: compute-sanitizer run of the kernels (RBM_SANITIZER=<tool>)")
 
 
 @pytest.fixture(scope="session")

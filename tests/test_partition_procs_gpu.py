@@ -97,7 +97,7 @@ def test_two_processes_bit_identical_to_one_gpu(R, kind, fused):
     for p in procs:
         p.join(timeout=120)
     assert not isinstance(got, str), got
-    assert all(p.exitcode == 0 for p in procs)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     assert all(m == fused for _, _, m in got)  # fused: both ranks mapped the peer over CUDA IPC
     ids = np.concatenate([g[0] for g in got]).view(np.uint32)
     xs = np.concatenate([g[1] for g in got])
