@@ -302,7 +302,7 @@ rbm_status rbm_set_adjacency(rbm_ctx* c, const uint32_t* row_ptr, const uint32_t
   c->P.adj_v = val;
   c->P.adj_nnz = nnz;
   c->P.adj_edges = c->cfg.kparam[2] != 0.0 ? 1u : 0u;
-  for (int i = 0; i < 4; ++i)  // kernel parameters changed: recapture
+  for (int i = 0; i < 6; ++i)  // kernel parameters changed: recapture
     if (c->graph[i]) { cudaGraphExecDestroy(c->graph[i]); c->graph[i] = nullptr; }
   return RBM_OK;
 }
@@ -851,7 +851,7 @@ rbm_status rbm_destroy(rbm_ctx* c) {
     }
     cudaFree(c->P.prof);
   }
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 6; ++i)
     if (c->graph[i]) cudaGraphExecDestroy(c->graph[i]);
   for (int j = 0; j < MAXG_FUSED; ++j)
     if (c->ipc_open[j]) cudaIpcCloseMemHandle(c->ipc_open[j]);

@@ -124,7 +124,7 @@ struct rbm_ctx {
   uint64_t step = 0;
   uint32_t launches = 0;
   int tile = 4096;
-  cudaGraphExec_t graph[4] = {nullptr, nullptr, nullptr, nullptr};  // by (cur, m & 1)
+  cudaGraphExec_t graph[6] = {};  // by (cur, m & 1)
   uint32_t graph_steps = 1;
   bool graph_failed = false;  // stream capture refused (partitioned steps fall back to eager launches)
   // optional per-kernel CUDA-event timing (rbm_timing_begin/end)
@@ -353,9 +353,12 @@ inline void carve(rbm_ctx& c, Workspace& ws) {
   const bool side = k.scheme == RBM_SCHEME_RBM1 && !rec_keyed(k) && c.L.b2 > 0;
   initial_ids(k, c.id0, c.n0);
   c.xstride = (slots + 63) & ~63ull;  // 256-B aligned buffers (TMA)
-  for (int b = 0; b < ((part && k.scheme == RBM_SCHEME_RBM1) ? 3 : 2); ++b) {
+  // partitioned: buffer 0 = final buckets (pass 2 writes the side keys),
+  // 1 = send, 2 = receive; one GPU: the state and the step's other buffer
+  const int nbuf = (k.scheme == RBM_SCHEME_RBM1 && part) ? 3 : 2;
+  for (int b = 0; b < nbuf; ++b) {
     c.recbuf[b] = ws.take<unsigned char>(c.xstride * RS);
-    c.skey[b] = side ? ws.take<uint32_t>(c.xstride) : nullptr;
+    c.skey[b] = (side && (!part || b == 0)) ? ws.take<uint32_t>(c.xstride) : nullptr;
   }
   for (int q = 0; q < 2; ++q) c.cur1[q] = ws.take<uint32_t>((size_t)MAX_SEG * CUR1_STRIDE);
   c.prefix1 = ws.take<uint32_t>(1025);
@@ -642,18 +645,19 @@ struct Engine final : EngineBase {
     const uint32_t pcap = L.b2 ? L.cap1 : L.cap2;
     if (!c.partitioned) {  // prologue: any storage order -> gapped buckets of step m
       Nvtx r_("prologue");
+      const int to = c.cur ^ 1;
       cudaMemsetAsync(c.cur1[q], 0, (size_t)L.nseg() * CUR1_STRIDE * 4, s);
-      prologue(c, s, st(c, c.cur), od(st(c, c.cur ^ 1)), c.cur1[q], pcap, n);
-      c.cur ^= 1;
+      prologue(c, s, st(c, c.cur), od(st(c, to)), c.cur1[q], pcap, n);
+      c.cur = to;
       c.partitioned = true;
     }
     cudaMemsetAsync(c.cur1[q ^ 1], 0, (size_t)L.nseg() * CUR1_STRIDE * 4, s);  // step-(m+1) cursors
     const unsigned straddle_grid = (unsigned)(((uint64_t)L.nbuckets * 32 + 255) / 256);
-    State<T, D> A = st(c, c.cur), Bf = st(c, c.cur ^ 1);
     c.mark(s);
     tile_scan_kernel<<<1, 1024, 0, s>>>(P, c.cur1[q], c.prefix1, c.tile_off, c.S, tile2());
     if (L.b2 == 0) {
       // A holds the final buckets of step m; the fused step writes m+1's into B
+      State<T, D> A = st(c, c.cur), Bf = st(c, c.cur ^ 1);
       c.mark(s);
       fused(c, s, A, od(Bf), L.cap2, c.cur1[q ^ 1]);
       c.mark(s);
@@ -661,7 +665,9 @@ struct Engine final : EngineBase {
                                                                      c.cur1[q ^ 1]);
       c.cur ^= 1;
     } else {
-      // A holds the pass-1 buckets of step m: split them by the next b2 bits into B
+      // A holds the pass-1 buckets of step m: split them by the next b2 bits
+      // into B, then the bucket step writes m+1's pass-1 buckets back into A
+      State<T, D> A = st(c, c.cur), Bf = st(c, c.cur ^ 1);
       cudaMemsetAsync(c.cur2, 0, (size_t)L.nbuckets * CUR2_STRIDE * 4, s);
       c.mark(s);
       split2(c, s, A, Bf, c.cur1[q]);
@@ -793,7 +799,7 @@ struct Engine final : EngineBase {
   }
 
   uint64_t gather_local(rbm_ctx& c, uint32_t* ids, void* x, cudaStream_t s) override {
-    if (c.cfg.scheme == RBM_SCHEME_RBMR && c.aos_valid) {
+    if (c.cfg.scheme == RBM_SCHEME_RBMR && c.aos_valid && is_partitioned(c.cfg)) {
       gather_aos_part_kernel<T, D><<<grid_for(c.n0, 256), 256, 0, s>>>(
           reinterpret_cast<const T*>(c.rxa), c.id0, c.n0, 0, 0, reinterpret_cast<T*>(x), ids);
       return c.n0;

@@ -914,19 +914,16 @@ template <typename T, int D> __host__ __device__ constexpr size_t bucket_smem_by
          + (((size_t)cap * 2 + 15) & ~(size_t)15);         // ord (u16)
 }
 
-template <typename T, int D, int KK, int INTEG, int MODE, int MINB>
-static __global__ void __launch_bounds__(BUCKET_BLOCK, MINB) bucket_kernel(const __grid_constant__ DevParams P, State<T, D> src,
-                                                                           uint32_t scap,
-                                                                           const uint32_t* __restrict__ S,
-                                                                           const __grid_constant__ OutDst<T, D> dst, uint32_t dcap,
-                                                                           uint32_t* __restrict__ cur_next) {
+// the bucket step of final bucket b (global start s0, n > 0 records at
+// physical slots [b scap, b scap + n) of src), in the CTA's shared memory smem_raw
+template <typename T, int D, int KK, int INTEG, int MODE>
+__device__ __forceinline__ void bucket_body(const DevParams& P, State<T, D> src, uint32_t scap, uint32_t b,
+                                            uint32_t s0, uint32_t n, const OutDst<T, D>& dst, uint32_t dcap,
+                                            uint32_t* __restrict__ cur_next, unsigned char* smem_raw) {
   using L = RecL<T, D>;
   constexpr int BLOCK = BUCKET_BLOCK, ITEMS = BUCKET_ITEMS;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
   RBM_PROF_BEGIN(P);
-  const uint32_t b = blockIdx.x;
-  const uint32_t s0 = S[b], n = S[b + 1] - s0, sb = b * scap;
-  if (n == 0) return;
+  const uint32_t sb = b * scap;
   const uint32_t nsb = 1u << P.SB;
   const uint32_t nout = 1u << P.b1;
   // sub-digit counts and offsets as packed u16 pairs (bucket sizes < 2^16);
@@ -953,6 +950,7 @@ static __global__ void __launch_bounds__(BUCKET_BLOCK, MINB) bucket_kernel(const
   uint16_t* ord = reinterpret_cast<uint16_t*>(ks + cap);
   const bool side = !L::KEYED && P.side_key;
   if (threadIdx.x == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem last touched by generic accesses
     const uint32_t bytes_r = (n * (uint32_t)L::RS + 15u) & ~15u;
     const uint32_t bytes_k = side ? ((n + 3u) & ~3u) * 4u : 0u;
     const uint64_t pol = l2_evict_first_policy();
@@ -1218,6 +1216,20 @@ static __global__ void __launch_bounds__(BUCKET_BLOCK, MINB) bucket_kernel(const
   }
   RBM_PROF(P, 8);
   if (P.prof && threadIdx.x == 0) atomicAdd(&P.prof[63], 1ull);
+}
+
+// one CTA per final bucket b of step m (S: exact global starts)
+template <typename T, int D, int KK, int INTEG, int MODE, int MINB>
+static __global__ void __launch_bounds__(BUCKET_BLOCK, MINB) bucket_kernel(const __grid_constant__ DevParams P, State<T, D> src,
+                                                                           uint32_t scap,
+                                                                           const uint32_t* __restrict__ S,
+                                                                           const __grid_constant__ OutDst<T, D> dst, uint32_t dcap,
+                                                                           uint32_t* __restrict__ cur_next) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const uint32_t b = blockIdx.x;
+  const uint32_t s0 = S[b], n = S[b + 1] - s0;
+  if (n == 0) return;
+  bucket_body<T, D, KK, INTEG, MODE>(P, src, scap, b, s0, n, dst, dcap, cur_next, smem_raw);
 }
 
 // ------------------------------------------ resident multi-step (N <= 2048)
