@@ -223,6 +223,7 @@ rbm_status init_impl(rbm_ctx* c, const rbm_config* cfg, void* wsp, size_t ws_byt
   P.segmask = (1u << c->L.segk) - 1u;
   P.halo = (is_partitioned(*cfg) && cfg->rank > 0) ? 1u : 0u;
   P.side_key = (cfg->scheme == RBM_SCHEME_RBM1 && !rec_keyed(*cfg) && c->L.b2 > 0) ? 1u : 0u;
+  P.jshift = 32u - c->L.idbits;
   if (std::getenv("RBM_PHASE_PROF")) {  // debug: per-phase cycles of the bucket kernel
     CU(cudaMalloc(&P.prof, 64 * 8));
     CU(cudaMemset(P.prof, 0, 64 * 8));

@@ -67,6 +67,7 @@ struct DevParams {
   uint32_t lowbits;    // key bits below prefix+sub-digit: 32 - B - SB (lowbits+idbits <= 32)
   uint32_t* dbg_order; // if set: sorted position -> id of this step (test hook)
   uint32_t side_key;   // the bucket step reads key_m from the side array pass 2 wrote (unkeyed records, 2-pass layouts)
+  uint32_t jshift;     // RBM-r increment partition: 32 - idbits (key = j << jshift)
   uint32_t group;      // lanes per batch in the fused step: pow2 >= p (<= 32), 0 = one thread per batch
   // partitioned single system (world_size G > 1): this rank
   // owns the key range whose top log2 G bits equal its rank.  The 2^b1 pass-1

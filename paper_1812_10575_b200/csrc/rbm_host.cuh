@@ -110,8 +110,8 @@ struct rbm_ctx {
   unsigned char* big_scratch = nullptr;
   // RBM-r
   uint32_t *js = nullptr, *rmcnt = nullptr, *rmbox = nullptr, *rovf = nullptr, *rnovf = nullptr;
-  void* rdelta = nullptr;  // Delta_s, 4 scalars per slot
   void* rxa = nullptr;     // AoS state (4 scalars per particle, id order)
+  unsigned char* rinc[2] = {nullptr, nullptr};  // RBM-r increment records: pass-1 and final buckets
   uint32_t *rprevb = nullptr, *rlevel = nullptr, *rorder = nullptr, *rlcnt = nullptr, *rloff = nullptr,
            *rlcur = nullptr, *rflags = nullptr;  // sequential RBM-r' (levels)
   bool aos_valid = false;  // RBM-r state currently in rxa
@@ -181,6 +181,31 @@ inline Layout choose_layout(const rbm_config& c) {
   const bool part = is_partitioned(c);
   L.idbits = ceil_log2((double)n);
   if (L.idbits < 1) L.idbits = 1;
+  // gapped capacities: mean + 12 sigma + 64 (overflow probability ~1e-33 per
+  // bucket; an overflow is flagged as RBM_ERR_CAPACITY), multiples of 64 so
+  // every bucket starts 256-B aligned (TMA)
+  auto gcap = [](double mu, uint32_t floor_) {
+    uint64_t v = (uint64_t)(mu + 12.0 * std::sqrt(mu) + 64.0);
+    if (v < floor_) v = floor_;
+    return (uint32_t)((v + 63) & ~63ull);
+  };
+  if (c.scheme == RBM_SCHEME_RBMR && !part) {
+    // RBM-r increments partitioned by particle index: final buckets of
+    // W = 2^(idbits-B) ids (~1024), one or two passes as for RBM-1
+    uint32_t B = ceil_log2((double)n / 1024.0);
+    if (B > L.idbits) B = L.idbits;
+    if (B > 20) B = 20;
+    L.B = B;
+    if (B <= 10) { L.b1 = B; L.b2 = 0; } else { L.b1 = B / 2; L.b2 = B - L.b1; }
+    L.nbuckets = 1u << B;
+    const double W = (double)(1ull << (L.idbits - B));
+    const double nslots = (double)(((n + c.p - 1) / c.p) * c.p);
+    L.cap2 = gcap(nslots * W / (double)n, 64);
+    L.cap1 = L.b2 ? gcap(nslots * W * (double)(1u << L.b2) / (double)n, 64) : L.cap2;
+    L.cap = L.cap2;
+    L.slots = std::max<uint64_t>((uint64_t)(1u << L.b1) * L.cap1, (uint64_t)L.nbuckets * L.cap2);
+    return L;
+  }
   if (part) L.g = ceil_log2((double)c.world_size);
   if (n <= 2048 && !part) {
     L.B = 0;  // one bucket: sorted-output kernel
@@ -223,14 +248,6 @@ inline Layout choose_layout(const rbm_config& c) {
     if (L.cap > FUSED_CAP_MAX) L.cap = FUSED_CAP_MAX;
   }
   if (c.debug_bucket_cap) L.cap = c.debug_bucket_cap;
-  // gapped capacities: mean + 12 sigma + 64 (overflow probability ~1e-33 per
-  // bucket; an overflow is flagged as RBM_ERR_CAPACITY), multiples of 64 so
-  // every bucket starts 256-B aligned (TMA)
-  auto gcap = [](double mu, uint32_t floor_) {
-    uint64_t v = (uint64_t)(mu + 12.0 * std::sqrt(mu) + 64.0);
-    if (v < floor_) v = floor_;
-    return (uint32_t)((v + 63) & ~63ull);
-  };
   L.slots = n;
   if (part) {
     // three buffers (final buckets A with a leading halo bucket, send B,
@@ -336,6 +353,8 @@ inline rbm_status validate(const rbm_config* cfg) {
   if (k.scheme == RBM_SCHEME_RBM1 && L.B == 0 &&
       (k.dtype == RBM_F64 ? resident_smem_bytes<double, 3>(L.cap) : resident_smem_bytes<float, 3>(L.cap)) > 227 * 1024)
     return fail(c, RBM_ERR_INVALID_ARG, "n=%llu too large for the resident kernel", (unsigned long long)k.n);
+  if (k.scheme == RBM_SCHEME_RBMR && !is_partitioned(k) && L.cap2 > 2048)
+    return fail(c, RBM_ERR_UNSUPPORTED, "RBM-r: %u slot records per id bucket exceed 2048", L.cap2);
   if (k.scheme == RBM_SCHEME_RBM1 && L.B > 0 && bucket_smem(k, L) > 227 * 1024)
     return fail(c, RBM_ERR_INVALID_ARG, "bucket capacity %u needs %zu B of shared memory", L.cap, bucket_smem(k, L));
   return RBM_OK;
@@ -417,14 +436,18 @@ inline void carve(rbm_ctx& c, Workspace& ws) {
   } else if (k.scheme != RBM_SCHEME_RBM1) {
     c.nbatch = (n + k.p - 1) / k.p;
     c.nslots = c.nbatch * k.p;
+    if (k.scheme == RBM_SCHEME_RBMR) {
+      const size_t irs = ((8 + k.d * es) + 15) / 16 * 16;
+      c.rinc[0] = ws.take<unsigned char>((size_t)(1u << c.L.b1) * c.L.cap1 * irs);
+      if (c.L.b2) c.rinc[1] = ws.take<unsigned char>((size_t)c.L.nbuckets * c.L.cap2 * irs);
+    }
     c.js = ws.take<uint32_t>(c.nslots);
-    c.rdelta = ws.take<unsigned char>(c.nslots * 4 * es);
     c.rxa = ws.take<unsigned char>(n * 4 * es);
-    c.rmcnt = ws.take<uint32_t>(n);
-    c.rmbox = ws.take<uint32_t>(n * MBOX);
-    c.rovf = ws.take<uint32_t>(2 * (size_t)OVF_CAP);
-    c.rnovf = ws.take<uint32_t>(1);
-    if (k.scheme == RBM_SCHEME_RBMR_SEQ) {
+    if (k.scheme == RBM_SCHEME_RBMR_SEQ) {  // per-particle slot mailboxes (levels of the sequential sweep)
+      c.rmcnt = ws.take<uint32_t>(n);
+      c.rmbox = ws.take<uint32_t>(n * MBOX);
+      c.rovf = ws.take<uint32_t>(2 * (size_t)OVF_CAP);
+      c.rnovf = ws.take<uint32_t>(1);
       c.rprevb = ws.take<uint32_t>(c.nslots);
       c.rlevel = ws.take<uint32_t>(c.nbatch);
       c.rorder = ws.take<uint32_t>(c.nbatch);
@@ -493,8 +516,18 @@ struct Engine final : EngineBase {
     rbm_status s;
     if ((s = chk(cudaFuncSetAttribute(prologue_kernel<T, D, PR_BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)pr_smem), "smem attr prologue"))) return s;
-    if ((s = chk(cudaFuncSetAttribute(split_kernel<T, D, SPLIT_BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((s = chk(cudaFuncSetAttribute(split_kernel<StateRT<T, D>, SPLIT_BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)sp_smem), "smem attr split"))) return s;
+    if (c.cfg.scheme == RBM_SCHEME_RBMR && !is_partitioned(c.cfg)) {
+      const uint32_t W = 1u << (c.L.idbits - c.L.B);
+      if ((s = chk(cudaFuncSetAttribute(rbmr_emit_kernel<T, D, KK, INTEG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)emit_smem_bytes<T, D>()), "smem attr rbmr emit"))) return s;
+      if ((s = chk(cudaFuncSetAttribute(split_kernel<IncRT<T, D>, SPLIT_BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)split_smem_bytes_rt<IncRT<T, D>>()), "smem attr rbmr split"))) return s;
+      if ((s = chk(cudaFuncSetAttribute(rbmr_bucket_apply_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)rapply_smem_bytes<T, D>(c.L.cap2, W)), "smem attr rbmr apply"))) return s;
+      return RBM_OK;
+    }
     if (c.L.B > 0) {
       if ((s = chk(pair_mode ? cudaFuncSetAttribute(bucket_kernel<T, D, KK, INTEG, MODE_PAIR, MINB>,
                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bk_smem)
@@ -605,8 +638,8 @@ struct Engine final : EngineBase {
   // pass 2: pass-1 buckets/segments (capacity cap1, counts cnt1 strided) -> final buckets
   void split2(rbm_ctx& c, cudaStream_t s, State<T, D> in, State<T, D> out, const uint32_t* cnt1) {
     Nvtx r_("split");
-    split_kernel<T, D, SPLIT_BLOCK><<<(unsigned)num_sms, SPLIT_BLOCK, sp_smem, s>>>(
-        c.P, in, out, c.cur2, c.L.cap2, cnt1, c.tile_off, c.L.cap1);
+    split_kernel<StateRT<T, D>, SPLIT_BLOCK><<<(unsigned)num_sms, SPLIT_BLOCK, sp_smem, s>>>(
+        c.P, in.rec, out.rec, out.key, c.cur2, c.L.cap2, cnt1, c.tile_off, c.L.cap1);
   }
 
   uint32_t tile2() const { return (uint32_t)split_tile<T, D>(); }
@@ -871,22 +904,40 @@ struct Engine final : EngineBase {
     c.mark(s);
   }
 
+  // RBM-r Jacobi sweep (reading D:8): increments routed to their particles
+  // through the partition by particle index (rbmr_emit -> split -> apply)
   void step_rbmr(rbm_ctx& c, cudaStream_t s) {
     const DevParams& P = c.P;
+    const Layout& L = c.L;
     const uint64_t n = c.cfg.n;
     T* xa = reinterpret_cast<T*>(c.rxa);
-    if (!c.aos_valid) {  // state set by init / set_state (SoA) -> AoS, once
+    if (!c.aos_valid) {  // state set by init / set_state (records) -> AoS, once
       rbmr_pack_kernel<T, D><<<grid_for(n, 256), 256, 0, s>>>(n, st(c, c.cur), xa);
       c.aos_valid = true;
     }
-    cudaMemsetAsync(c.rmcnt, 0, n * 4, s);
-    cudaMemsetAsync(c.rnovf, 0, 4, s);
+    using IL = IncL<T, D>;
+    const uint32_t W = 1u << (L.idbits - L.B);
+    const uint32_t bpc = EMIT_TS / c.cfg.p;
+    cudaMemsetAsync(c.cur1[0], 0, (size_t)(1u << L.b1) * CUR1_STRIDE * 4, s);
     c.mark(s);
-    rbmr_batch_kernel<T, D, KK, INTEG><<<grid_for(c.nbatch, 128, 148 * 64), 128, 0, s>>>(
-        P, c.nbatch, xa, c.js, reinterpret_cast<T*>(c.rdelta), c.rmcnt, c.rmbox, c.rovf, c.rnovf);
+    rbmr_emit_kernel<T, D, KK, INTEG><<<(unsigned)((c.nbatch + bpc - 1) / bpc), EMIT_BLOCK, emit_smem_bytes<T, D>(), s>>>(
+        P, c.nbatch, xa, c.js, c.rinc[0], c.cur1[0], L.cap1);
+    const unsigned char* fin = c.rinc[0];
+    const uint32_t* fcnt = c.cur1[0];
+    if (L.b2) {
+      c.mark(s);
+      tile_scan_kernel<<<1, 1024, 0, s>>>(P, c.cur1[0], c.prefix1, c.tile_off, c.S,
+                                          (uint32_t)split_tile_rt<IncRT<T, D>>());
+      cudaMemsetAsync(c.cur2, 0, (size_t)L.nbuckets * CUR2_STRIDE * 4, s);
+      c.mark(s);
+      split_kernel<IncRT<T, D>, SPLIT_BLOCK><<<(unsigned)num_sms, SPLIT_BLOCK, split_smem_bytes_rt<IncRT<T, D>>(), s>>>(
+          P, c.rinc[0], c.rinc[1], nullptr, c.cur2, L.cap2, c.cur1[0], c.tile_off, L.cap1);
+      fin = c.rinc[1];
+      fcnt = c.cur2;
+    }
     c.mark(s);
-    rbmr_apply_kernel<T, D><<<grid_for(n, 256), 256, 0, s>>>(P, n, xa, reinterpret_cast<const T*>(c.rdelta),
-                                                             c.rmcnt, c.rmbox, c.rovf, c.rnovf);
+    rbmr_bucket_apply_kernel<T, D><<<L.nbuckets, 256, rapply_smem_bytes<T, D>(L.cap2, W), s>>>(P, fin, L.cap2, fcnt, W, xa);
+    (void)sizeof(IL);
     c.mark(s);
     advance_kernel<<<1, 1, 0, s>>>(c.step_dev);
     c.mark(s);
@@ -927,7 +978,8 @@ EngineBase* make_for_kernel(uint32_t kernel, uint32_t integ) {
 }
 
 inline const char* const* kernel_names(const rbm_ctx& c, uint32_t* count) {
-  static const char* const r[] = {"rbmr_batch", "rbmr_apply", "advance"};
+  static const char* const r[] = {"rbmr_emit", "rbmr_apply", "advance"};
+  static const char* const r2[] = {"rbmr_emit", "tile_scan", "split", "rbmr_apply", "advance"};
   static const char* const rs[] = {"rbmr_draw", "rbmr_prev", "rbmr_levels", "rbmr_seq_apply", "advance"};
   if (c.cfg.scheme == RBM_SCHEME_RBMR_SEQ) { *count = 5; return rs; }
   static const char* const b0[] = {"resident_step"};
@@ -938,7 +990,11 @@ inline const char* const* kernel_names(const rbm_ctx& c, uint32_t* count) {
   static const char* const prr[] = {"rbmr_request", "rbmr_serve", "rbmr_delta", "rbmr_apply"};
   if (is_partitioned(c.cfg) && c.cfg.scheme == RBM_SCHEME_RBMR) { *count = 4; return prr; }
   if (is_partitioned(c.cfg)) { *count = 9; return pt; }
-  if (c.cfg.scheme == RBM_SCHEME_RBMR) { *count = 3; return r; }
+  if (c.cfg.scheme == RBM_SCHEME_RBMR) {
+    if (c.L.b2) { *count = 5; return r2; }
+    *count = 3;
+    return r;
+  }
   if (c.L.B == 0) { *count = 1; return b0; }
   if (c.L.b2 == 0) { *count = 4; return p1; }
   *count = 6;

@@ -519,25 +519,55 @@ static __global__ void __launch_bounds__(BLOCK) prologue_kernel(const __grid_con
 // store per record) into the reserved ranges of the final buckets.  Unkeyed
 // records: key_m is computed from the id here and written to the side key
 // array for the bucket step.
-template <typename T, int D> __host__ __device__ constexpr int split_tile() {
-  return (65536 / RecL<T, D>::RS) < 4096 ? (65536 / RecL<T, D>::RS) : 4096;  // <= 64 KB per stage
+// record traits of the splitter: the state records (key carried, or from
+// the id by Philox -> side key array), or the RBM-r increment records (the
+// partition key is the particle index j, left-aligned to 32 bits)
+template <typename T, int D> struct StateRT {
+  static constexpr int RS = RecL<T, D>::RS, NW = RecL<T, D>::NW;
+  static constexpr bool SIDE = !RecL<T, D>::KEYED;
+  __device__ __forceinline__ static uint32_t key(const DevParams& P, const unsigned char* r, uint32_t m) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(r);
+    return RecL<T, D>::KEYED ? w[1] : shuffle_key(P, w[0], m);
+  }
+};
+// RBM-r increment record {j, s, Delta_s[D]} (16 or 32 bytes)
+template <typename T, int D> struct IncL {
+  static constexpr int RS = ((8 + D * (int)sizeof(T)) + 15) / 16 * 16;
+  static constexpr int NW = RS / 4;
+};
+template <typename T, int D> struct IncRT {
+  static constexpr int RS = IncL<T, D>::RS, NW = IncL<T, D>::NW;
+  static constexpr bool SIDE = false;
+  __device__ __forceinline__ static uint32_t key(const DevParams& P, const unsigned char* r, uint32_t) {
+    return reinterpret_cast<const uint32_t*>(r)[0] << P.jshift;
+  }
+};
+
+template <class RT> __host__ __device__ constexpr int split_tile_rt() {
+  return (65536 / RT::RS) < 4096 ? (65536 / RT::RS) : 4096;  // <= 64 KB per stage
 }
+template <class RT> __host__ __device__ constexpr size_t split_smem_bytes_rt() {
+  return (3 * 1024 + 64) * 4 + 64 + 2 * (size_t)split_tile_rt<RT>() * RT::RS +
+         (size_t)split_tile_rt<RT>() * (4 + 4 + 2 + 2) + (size_t)(MAX_SEG_SPLIT + 1) * 4;
+}
+template <typename T, int D> __host__ __device__ constexpr int split_tile() { return split_tile_rt<StateRT<T, D>>(); }
 template <typename T, int D> __host__ __device__ constexpr size_t split_smem_bytes() {
-  return (3 * 1024 + 64) * 4 + 64 + 2 * (size_t)split_tile<T, D>() * RecL<T, D>::RS +
-         (size_t)split_tile<T, D>() * (4 + 4 + 2 + 2) + (size_t)(MAX_SEG_SPLIT + 1) * 4;
+  return split_smem_bytes_rt<StateRT<T, D>>();
 }
 
 struct TileInfo { uint32_t u, lo, hi, pad; };
 
-template <typename T, int D, int BLOCK>
+template <class RT, int BLOCK>
 static __global__ void __launch_bounds__(BLOCK, 1) split_kernel(const __grid_constant__ DevParams P,
-                                                                State<T, D> src, State<T, D> dst,
+                                                                const unsigned char* __restrict__ src_rec,
+                                                                unsigned char* __restrict__ dst_rec,
+                                                                uint32_t* __restrict__ dst_key,
                                                                 uint32_t* cur, uint32_t dcap,
                                                                 const uint32_t* __restrict__ cnt1,
                                                                 const uint32_t* __restrict__ tile_off,
                                                                 uint32_t scap) {
-  using L = RecL<T, D>;
-  constexpr int TILE = split_tile<T, D>();
+  using L = RT;
+  constexpr int TILE = split_tile_rt<RT>();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   RBM_PROF_BEGIN(P);
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw);  // 1024
@@ -569,7 +599,7 @@ static __global__ void __launch_bounds__(BLOCK, 1) split_kernel(const __grid_con
     const uint32_t bytes = (cnt * (uint32_t)L::RS + 15u) & ~15u;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(&bar[st], bytes);
-    if (cnt) bulk_g2s_stream(stg0 + st * SBY, src.rec + ((size_t)ti.u * scap + ti.lo) * L::RS, bytes, &bar[st], pol);
+    if (cnt) bulk_g2s_stream(stg0 + st * SBY, src_rec + ((size_t)ti.u * scap + ti.lo) * L::RS, bytes, &bar[st], pol);
   };
   if (tid == 0) {
     pol = l2_evict_first_policy();
@@ -593,13 +623,8 @@ static __global__ void __launch_bounds__(BLOCK, 1) split_kernel(const __grid_con
     const unsigned char* stg = stg0 + s * SBY;
     __syncthreads();
     for (uint32_t e = tid; e < cnt; e += BLOCK) {
-      uint32_t key;
-      if (L::KEYED) {
-        key = reinterpret_cast<const uint32_t*>(stg + (size_t)e * L::RS)[1];
-      } else {
-        key = shuffle_key(P, ld_id<T, D>(stg, e), m);
-        kl[e] = key;
-      }
+      const uint32_t key = RT::key(P, stg + (size_t)e * L::RS, m);
+      if (RT::SIDE) kl[e] = key;
       const uint32_t dg = (key >> sh) & mask;
       rk[e] = (dg << 16) | atomicAdd(&hist[dg], 1u);
     }
@@ -642,8 +667,8 @@ static __global__ void __launch_bounds__(BLOCK, 1) split_kernel(const __grid_con
       const size_t g = (size_t)(dbase0 + dg) * dcap + slot;
       uint32_t w[L::NW];
       ld_words<L::NW>(stg + (size_t)e * L::RS, w);
-      st_words<L::NW>(dst.rec + g * L::RS, w);
-      if (!L::KEYED) dst.key[g] = kl[e];
+      st_words<L::NW>(dst_rec + g * L::RS, w);
+      if (RT::SIDE) dst_key[g] = kl[e];
     }
     __syncthreads();  // stage s, rk, inv free
     RBM_PROF(P, 21);
@@ -1686,9 +1711,12 @@ static __global__ void __launch_bounds__(TB) direct_kernel(const __grid_constant
 // One sweep of ceil(N/p) with-replacement batches (Alg. 2/3),
 // Jacobi-additive reading D:8: every batch evaluated from X_m, then
 // x_j <- x_j + sum over the slots s with j_s = j of Delta_s, in ascending s.
-// State in id order as AoS (4 scalars per particle, one sector per gather);
-// slots are registered in per-particle mailboxes (MBOX entries, overflow list
-// for the ~1e-6 of particles drawn more often), sorted by s when applied.
+// State in id order as AoS (4 scalars per particle, one sector per gather).
+// One GPU: the increments go through a partition by particle index (the
+// rbmr_emit / split / rbmr_bucket_apply kernels below).  The sequential
+// RBM-r' and the partitioned system register slots in per-particle mailboxes
+// (MBOX entries, overflow list for the ~1e-6 of particles drawn more often),
+// sorted by s when applied.
 constexpr uint32_t MBOX = 8;
 constexpr uint32_t OVF_CAP = 1u << 20;
 
@@ -1708,192 +1736,6 @@ __device__ __forceinline__ void load4(const T* __restrict__ xa, uint32_t j, T (&
   for (int c = 0; c < D; ++c) x[c] = xa[(size_t)j * 4 + c];
 }
 
-// one thread per batch b: draws j_s (s = b p + l, distinct in the batch, D:9),
-// the increments Delta_s from X_m, and the mailbox registration of each slot
-template <typename T, int D, int KK, int INTEG>
-static __global__ void __launch_bounds__(128) rbmr_batch_kernel(const __grid_constant__ DevParams P, uint64_t nbatch,
-                                                                const T* __restrict__ xa, uint32_t* __restrict__ js,
-                                                                T* __restrict__ delta, uint32_t* __restrict__ mcnt,
-                                                                uint32_t* __restrict__ mbox, uint32_t* __restrict__ ovf,
-                                                                uint32_t* __restrict__ novf) {
-  const uint32_t m = (uint32_t)*P.step;
-  const uint32_t p = P.p;
-  if (p == 2) {  // pairs: every memory access of a batch issued before its first use
-    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nbatch;
-         b += (uint64_t)gridDim.x * blockDim.x) {
-      const uint64_t s0 = 2 * b;
-      uint32_t j0, j1;
-      if (KK == KK_ADJ && P.adj_edges) {
-        adj_edge_draw(P, s0, m, j0, j1);
-      } else {
-        {
-          const uint4 w = block_at(P, (uint32_t)s0, 0u, m, TAG_SLOT);
-          j0 = (uint32_t)__umul64hi(P.n, (((uint64_t)w.x) << 32) | w.y);
-        }
-        for (uint32_t t = 0;; ++t) {
-          const uint4 w = block_at(P, (uint32_t)(s0 + 1), t, m, TAG_SLOT);
-          j1 = (uint32_t)__umul64hi(P.n, (((uint64_t)w.x) << 32) | w.y);
-          if (j1 != j0) break;
-        }
-      }
-      T x0[D], x1[D];
-      load4<T, D>(xa, j0, x0);
-      load4<T, D>(xa, j1, x1);
-      const uint32_t pos0 = atomicAdd(&mcnt[j0], 1u);
-      const uint32_t pos1 = atomicAdd(&mcnt[j1], 1u);
-      js[s0] = j0;
-      js[s0 + 1] = j1;
-      T z0[D], z1[D], y0[D], y1[D];
-#pragma unroll
-      for (int c = 0; c < D; ++c) { z0[c] = T(0); z1[c] = T(0); }
-      if (P.has_noise) {
-        Normals<T, D>::get(P, (uint32_t)s0, m, TAG_NOISE_SLOT, z0);
-        Normals<T, D>::get(P, (uint32_t)(s0 + 1), m, TAG_NOISE_SLOT, z1);
-      }
-      if (INTEG == 0) {
-        T f0[D], f1[D], zz[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) { f0[c] = T(0); f1[c] = T(0); }
-        add_interaction<T, D, KK>(x0, x1, f0, P);  // 1/(p-1) = 1
-        add_interaction<T, D, KK>(x1, x0, f1, P);
-        (void)zz;
-        em_update<T, D>(x0, f0, z0, y0, P, false);
-        em_update<T, D>(x1, f1, z1, y1, P, false);
-      } else {
-        T a[D], bb[D];
-        if (KK == KK_ADJ) {
-          adj_flow<T, D>(P, j0, j1, x0, x1, true, a);
-          adj_flow<T, D>(P, j0, j1, x0, x1, false, bb);
-        } else {
-          pair_flow<T, D, KK>(x0, x1, true, a, P);
-          pair_flow<T, D, KK>(x0, x1, false, bb, P);
-        }
-        split_finish<T, D>(a, z0, y0, P, false);
-        split_finish<T, D>(bb, z1, y1, P, false);
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        delta[s0 * 4 + c] = (c < D) ? y0[c < D ? c : 0] - x0[c < D ? c : 0] : T(0);
-        delta[(s0 + 1) * 4 + c] = (c < D) ? y1[c < D ? c : 0] - x1[c < D ? c : 0] : T(0);
-      }
-      const uint32_t jj[2] = {j0, j1}, pp[2] = {pos0, pos1};
-#pragma unroll
-      for (int l = 0; l < 2; ++l) {
-        if (pp[l] < MBOX) {
-          mbox[(size_t)jj[l] * MBOX + pp[l]] = (uint32_t)(s0 + l);
-        } else {
-          const uint32_t q = atomicAdd(novf, 1u);
-          if (q < OVF_CAP) { ovf[2 * q] = jj[l]; ovf[2 * q + 1] = (uint32_t)(s0 + l); }
-          else atomicExch(P.capacity_err, 1u);
-        }
-      }
-    }
-    return;
-  }
-  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nbatch;
-       b += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t s0 = b * p;
-    for (uint32_t l = 0; l < p; ++l) {
-      const uint64_t s = s0 + l;
-      uint32_t t = 0, j;
-      for (;;) {
-        const uint4 w = block_at(P, (uint32_t)s, t, m, TAG_SLOT);
-        const uint64_t u = (((uint64_t)w.x) << 32) | w.y;
-        j = (uint32_t)__umul64hi(P.n, u);
-        bool dup = false;
-        for (uint32_t l2 = 0; l2 < l; ++l2) dup |= (js[s0 + l2] == j);
-        if (!dup) break;
-        ++t;
-      }
-      js[s] = j;
-    }
-    for (uint32_t l = 0; l < p; ++l) {
-      const uint64_t s = s0 + l;
-      const uint32_t j = js[s];
-      T xi[D], z[D], xn[D];
-      load4<T, D>(xa, j, xi);
-#pragma unroll
-      for (int c = 0; c < D; ++c) z[c] = T(0);
-      if (P.has_noise) Normals<T, D>::get(P, (uint32_t)s, m, TAG_NOISE_SLOT, z);
-      if (INTEG == 0) {
-        T f[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) f[c] = T(0);
-        for (uint32_t l2 = 0; l2 < p; ++l2) {  // ascending lane, self skipped
-          if (l2 == l) continue;
-          T xj[D];
-          load4<T, D>(xa, js[s0 + l2], xj);
-          add_interaction<T, D, KK>(xi, xj, f, P);
-        }
-        const T inv = T(1) / T(p - 1);
-#pragma unroll
-        for (int c = 0; c < D; ++c) f[c] *= inv;
-        em_update<T, D>(xi, f, z, xn, P, false);
-      } else {
-        T xa0[D], xb0[D], y[D];
-        load4<T, D>(xa, js[s0], xa0);
-        load4<T, D>(xa, js[s0 + 1], xb0);
-        pair_flow<T, D, KK>(xa0, xb0, l == 0, y, P);
-        split_finish<T, D>(y, z, xn, P, false);
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) delta[s * 4 + c] = (c < D) ? xn[c < D ? c : 0] - xi[c < D ? c : 0] : T(0);
-      const uint32_t pos = atomicAdd(&mcnt[j], 1u);
-      if (pos < MBOX) {
-        mbox[(size_t)j * MBOX + pos] = (uint32_t)s;
-      } else {
-        const uint32_t q = atomicAdd(novf, 1u);
-        if (q < OVF_CAP) { ovf[2 * q] = j; ovf[2 * q + 1] = (uint32_t)s; }
-        else atomicExch(P.capacity_err, 1u);
-      }
-    }
-  }
-}
-
-// x_j += Delta_s over j's slots in ascending s (reading D:8); sphere: renormalise
-template <typename T, int D>
-static __global__ void rbmr_apply_kernel(const __grid_constant__ DevParams P, uint64_t n, T* __restrict__ xa,
-                                         const T* __restrict__ delta, const uint32_t* __restrict__ mcnt,
-                                         const uint32_t* __restrict__ mbox, const uint32_t* __restrict__ ovf,
-                                         const uint32_t* __restrict__ novf) {
-  const uint32_t m = (uint32_t)*P.step;
-  constexpr uint32_t MAXL = 32;
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
-       j += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t c = mcnt[j];
-    if (c == 0) continue;
-    uint32_t sl[MAXL];
-    uint32_t k = 0;
-    const uint32_t cm = c < MBOX ? c : MBOX;
-    for (uint32_t q = 0; q < cm; ++q) sl[k++] = mbox[j * MBOX + q];
-    if (c > MBOX) {  // rare: the rest of j's slots are in the overflow list
-      const uint32_t no = min(*novf, OVF_CAP);
-      for (uint32_t q = 0; q < no; ++q)
-        if (ovf[2 * q] == (uint32_t)j) {
-          if (k < MAXL) sl[k++] = ovf[2 * q + 1];
-          else atomicExch(P.capacity_err, 1u);
-        }
-    }
-    for (uint32_t a = 1; a < k; ++a) {  // insertion sort of the (short) slot list
-      const uint32_t v = sl[a];
-      uint32_t w = a;
-      while (w > 0 && sl[w - 1] > v) { sl[w] = sl[w - 1]; --w; }
-      sl[w] = v;
-    }
-    T x[D];
-    load4<T, D>(xa, (uint32_t)j, x);
-    for (uint32_t a = 0; a < k; ++a) {
-      const uint64_t s = sl[a];
-#pragma unroll
-      for (int cc = 0; cc < D; ++cc) x[cc] += delta[s * 4 + cc];
-    }
-    if (P.constraint == 1) renormalise<T, D>(x);
-    check_finite<T, D>(x, P, (uint32_t)j, m);
-#pragma unroll
-    for (int cc = 0; cc < D; ++cc) xa[j * 4 + cc] = x[cc];
-  }
-}
-
 // ----------------------- exact sequential RBM-r' (Alg. 2, row f2)
 // Batches of one sweep are applied in draw order from the current positions.
 // Batch b depends on the earlier batches that share a member; its level is
@@ -1903,7 +1745,7 @@ static __global__ void rbmr_apply_kernel(const __grid_constant__ DevParams P, ui
 constexpr uint32_t NO_BATCH = 0xffffffffu;
 constexpr uint32_t MAX_LEVELS = 4096;
 
-// draws j_s of batch b (as rbmr_batch_kernel) and mailbox registration only
+// draws j_s of batch b (as the oracle, reading D:9) and mailbox registration only
 static __global__ void __launch_bounds__(128) rbmr_draw_reg_kernel(const __grid_constant__ DevParams P, uint64_t nbatch,
                                                                    uint32_t* __restrict__ js, uint32_t* __restrict__ mcnt,
                                                                    uint32_t* __restrict__ mbox, uint32_t* __restrict__ ovf,
@@ -2126,7 +1968,7 @@ __device__ __forceinline__ uint32_t rp_owner(const RPart& R, uint32_t j) {
   return a;
 }
 
-// draws of slot s0 + l (distinct within the batch, reading D:9): as rbmr_batch_kernel
+// draws of slot s0 + l (distinct within the batch, reading D:9)
 __device__ __forceinline__ uint32_t rbmr_draw(const DevParams& P, uint32_t m, uint64_t s, const uint32_t* prev,
                                               uint32_t l) {
   uint32_t t = 0, j;
@@ -2141,11 +1983,11 @@ __device__ __forceinline__ uint32_t rbmr_draw(const DevParams& P, uint32_t m, ui
 }
 
 // Delta_s of the p slots of batch s0/p from the members' positions x[l]
-// (the general path of rbmr_batch_kernel; for p = 2 the same arithmetic as
-// its pair path: the prefactor is exactly 1)
+// (Eq. 2.2 over the batch in ascending lane order, prefactor 1/(p-1), exactly
+// 1 for pairs; or the exact pair flow)
 template <typename T, int D, int KK, int INTEG>
 __device__ __forceinline__ void rbmr_deltas(const DevParams& P, uint32_t m, uint64_t s0, uint32_t p,
-                                            T (*x)[D], T (*dl)[D]) {
+                                            const uint32_t* jj, T (*x)[D], T (*dl)[D]) {
   for (uint32_t l = 0; l < p; ++l) {
     T z[D], xn[D];
 #pragma unroll
@@ -2165,7 +2007,8 @@ __device__ __forceinline__ void rbmr_deltas(const DevParams& P, uint32_t m, uint
       em_update<T, D>(x[l], f, z, xn, P, false);
     } else {
       T y[D];
-      pair_flow<T, D, KK>(x[0], x[1], l == 0, y, P);
+      if (KK == KK_ADJ) adj_flow<T, D>(P, jj[0], jj[1], x[0], x[1], l == 0, y);
+      else pair_flow<T, D, KK>(x[0], x[1], l == 0, y, P);
       split_finish<T, D>(y, z, xn, P, false);
     }
 #pragma unroll
@@ -2235,7 +2078,7 @@ static __global__ void __launch_bounds__(128) rbmr_delta_part_kernel(const __gri
       for (int c = 0; c < D; ++c) x[l][c] = src[c];
     }
     if (!ok) continue;  // capacity overflow (flagged by the request kernel)
-    rbmr_deltas<T, D, KK, INTEG>(P, m, s0, p, x, dl);
+    rbmr_deltas<T, D, KK, INTEG>(P, m, s0, p, R.spos + sl0, x, dl);
     for (uint32_t l = 0; l < p; ++l) {
       const uint32_t sp = R.spos[sl0 + l], dest = sp >> 24, pos = sp & 0xffffffu;
       unsigned char* ic = R.is + dest * R.ichunk;
@@ -2342,6 +2185,193 @@ static __global__ void gather_aos_part_kernel(const T* __restrict__ xa, uint64_t
 #pragma unroll
       for (int c = 0; c < D; ++c) out[(id - i0) * D + c] = xa[jl * 4 + c];
     }
+  }
+}
+
+// ------------------------------------------- RBM-r Jacobi sweep, one GPU
+// The increments Delta_s are routed to their particles through the same
+// MSD partition as the RBM-1 records, keyed by j_s (no random mailboxes):
+//   emit     one thread per batch: draws j_s (as the oracle, reading D:9),
+//            gathers x_{j_s}, computes Delta_s (rbmr_deltas), and the CTA's
+//            records {j_s, s, Delta_s} are staged by the top b1 bits of j_s
+//            and written as coalesced runs into the pass-1 buckets
+//   split    pass-1 -> final buckets of 2^(idbits-B) particle ids (split_kernel<IncRT>)
+//   apply    one CTA per final bucket: the records are ordered by (j, s) in
+//            shared memory and every particle of the id range adds its
+//            increments in ascending s to its own position (reading D:8)
+constexpr int EMIT_BLOCK = 256;
+constexpr uint32_t EMIT_TS = 2048;  // slots per emit CTA
+
+template <typename T, int D> __host__ __device__ constexpr size_t emit_smem_bytes() {
+  return (size_t)EMIT_TS * IncL<T, D>::RS + (size_t)EMIT_TS * (4 + 2) + (3 * 1024 + 64) * 4;
+}
+
+template <typename T, int D, int KK, int INTEG>
+static __global__ void __launch_bounds__(EMIT_BLOCK) rbmr_emit_kernel(const __grid_constant__ DevParams P, uint64_t nbatch,
+                                                                      const T* __restrict__ xa, uint32_t* __restrict__ js,
+                                                                      unsigned char* __restrict__ dst, uint32_t* cur,
+                                                                      uint32_t dcap) {
+  using IL = IncL<T, D>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char* stg = smem_raw;                                            // EMIT_TS records
+  uint32_t* rk = reinterpret_cast<uint32_t*>(stg + (size_t)EMIT_TS * IL::RS);  // digit << 16 | rank
+  uint16_t* inv = reinterpret_cast<uint16_t*>(rk + EMIT_TS);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(inv + EMIT_TS);             // 1024
+  uint32_t* gbase = hist + 1024;                                           // 1024
+  uint32_t* off = gbase + 1024;                                            // 1024
+  uint32_t* wsum = off + 1024;                                             // 64
+  const uint32_t m = (uint32_t)*P.step;
+  const uint32_t p = P.p;
+  const uint32_t bpc = EMIT_TS / p;  // batches per CTA
+  const uint64_t b0 = (uint64_t)blockIdx.x * bpc;
+  if (b0 >= nbatch) return;
+  const uint32_t nb = (uint32_t)min((uint64_t)bpc, nbatch - b0), cnt = nb * p;
+  const uint32_t nbins = 1u << P.b1, sh = 32u - P.b1;
+  for (uint32_t i = threadIdx.x; i < nbins; i += EMIT_BLOCK) hist[i] = 0;
+  __syncthreads();
+  for (uint32_t lb = threadIdx.x; lb < nb; lb += EMIT_BLOCK) {
+    const uint64_t b = b0 + lb, s0 = b * p;
+    uint32_t jj[64];
+    if (KK == KK_ADJ && P.adj_edges) {
+      adj_edge_draw(P, s0, m, jj[0], jj[1]);
+    } else {
+      for (uint32_t l = 0; l < p; ++l) jj[l] = rbmr_draw(P, m, s0 + l, jj, l);
+    }
+    T x[64][D], dl[64][D];
+    for (uint32_t l = 0; l < p; ++l) load4<T, D>(xa, jj[l], x[l]);
+    rbmr_deltas<T, D, KK, INTEG>(P, m, s0, p, jj, x, dl);
+    for (uint32_t l = 0; l < p; ++l) {
+      const uint32_t e = lb * p + l;
+      js[s0 + l] = jj[l];
+      uint32_t w[IL::NW];
+#pragma unroll
+      for (int k = 0; k < IL::NW; ++k) w[k] = 0u;
+      w[0] = jj[l];
+      w[1] = (uint32_t)(s0 + l);
+#pragma unroll
+      for (int c = 0; c < D; ++c) to_w(dl[l][c], w + 2 + c * (int)(sizeof(T) / 4));
+      st_words<IL::NW>(stg + (size_t)e * IL::RS, w);
+      const uint32_t dg = (jj[l] << P.jshift) >> sh;
+      rk[e] = (dg << 16) | atomicAdd(&hist[dg], 1u);
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < nbins; i += EMIT_BLOCK) {
+    const uint32_t h = hist[i];
+    off[i] = h;
+    gbase[i] = h ? atomicAdd(&cur[(size_t)i * CUR1_STRIDE], h) : 0u;
+  }
+  __syncthreads();
+  block_excl_scan<EMIT_BLOCK>(off, nbins, wsum);
+  for (uint32_t e = threadIdx.x; e < cnt; e += EMIT_BLOCK) {
+    const uint32_t v = rk[e];
+    inv[off[v >> 16] + (v & 0xffffu)] = (uint16_t)e;
+  }
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < cnt; j += EMIT_BLOCK) {
+    const uint32_t e = inv[j];
+    const uint32_t dg = rk[e] >> 16;
+    const uint32_t slot = gbase[dg] + (j - off[dg]);
+    if (slot >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
+    uint32_t w[IL::NW];
+    ld_words<IL::NW>(stg + (size_t)e * IL::RS, w);
+    st_words<IL::NW>(dst + ((size_t)dg * dcap + slot) * IL::RS, w);
+  }
+}
+
+template <typename T, int D> __host__ __device__ constexpr size_t rapply_smem_bytes(uint32_t cap, uint32_t W) {
+  return (size_t)(cap + 8) * IncL<T, D>::RS + (size_t)cap * 4 + (size_t)W * 8 + 64 * 4 + 16;
+}
+
+// apply: final bucket b = the particle ids [b W, (b+1) W); n = cnt[b] records
+template <typename T, int D>
+static __global__ void __launch_bounds__(256) rbmr_bucket_apply_kernel(const __grid_constant__ DevParams P,
+                                                                       const unsigned char* __restrict__ fin, uint32_t cap,
+                                                                       const uint32_t* __restrict__ cnt, uint32_t W,
+                                                                       T* __restrict__ xa) {
+  using IL = IncL<T, D>;
+  constexpr int BLOCK = 256;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const uint32_t b = blockIdx.x;
+  const uint32_t n = cnt[(size_t)b * CUR2_STRIDE];
+  const uint64_t j0 = (uint64_t)b * W;
+  if (j0 >= P.n) return;
+  const uint32_t nid = (uint32_t)min((uint64_t)W, P.n - j0);
+  const uint32_t m = (uint32_t)*P.step;
+  unsigned char* rs = smem_raw;
+  uint32_t* pos = reinterpret_cast<uint32_t*>(rs + (size_t)(cap + 8) * IL::RS);  // element -> rank within its particle
+  uint32_t* pc = pos + cap;        // per particle: count
+  uint32_t* po = pc + W;           // per particle: first index in ix (after the scan)
+  uint32_t* wsum = po + W;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);
+  uint16_t* ix = reinterpret_cast<uint16_t*>(pos);  // reused after the placement: sorted element indices
+  if (threadIdx.x == 0 && n) {
+    mbar_init(bar, 1);
+    const uint32_t bytes = (n * (uint32_t)IL::RS + 15u) & ~15u;
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s_stream(rs, fin + (size_t)b * cap * IL::RS, bytes, bar, l2_evict_first_policy());
+  }
+  for (uint32_t i = threadIdx.x; i < W; i += BLOCK) pc[i] = 0;
+  __syncthreads();
+  if (n > cap) {  // cannot happen at the layout's 12-sigma capacity: flagged
+    if (threadIdx.x == 0) atomicExch(P.capacity_err, 1u);
+    return;
+  }
+  if (n) mbar_wait(bar, 0);
+  for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
+    const uint32_t jl = (uint32_t)(reinterpret_cast<const uint32_t*>(rs + (size_t)e * IL::RS)[0] - j0);
+    pos[e] = atomicAdd(&pc[jl], 1u);
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < W; i += BLOCK) po[i] = pc[i];
+  __syncthreads();
+  block_excl_scan<BLOCK>(po, (int)W, wsum);
+  uint32_t myjl[8], myr[8];
+  uint32_t k = 0;
+  for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
+    myjl[k] = (uint32_t)(reinterpret_cast<const uint32_t*>(rs + (size_t)e * IL::RS)[0] - j0);
+    myr[k] = pos[e];
+    ++k;
+  }
+  __syncthreads();  // pos is dead: its space becomes ix
+  k = 0;
+  for (uint32_t e = threadIdx.x; e < n; e += BLOCK, ++k) ix[po[myjl[k]] + myr[k]] = (uint16_t)e;
+  __syncthreads();
+  // every particle of the range with increments: ascending slot order (D:8)
+  for (uint32_t jl = threadIdx.x; jl < nid; jl += BLOCK) {
+    const uint32_t c = pc[jl];
+    if (c == 0) continue;
+    constexpr uint32_t MAXL = 32;
+    uint32_t ee[MAXL], ss[MAXL];
+    const uint32_t kk = c < MAXL ? c : MAXL;
+    if (c > MAXL) atomicExch(P.capacity_err, 1u);
+    for (uint32_t a = 0; a < kk; ++a) {
+      ee[a] = ix[po[jl] + a];
+      ss[a] = reinterpret_cast<const uint32_t*>(rs + (size_t)ee[a] * IL::RS)[1];
+    }
+    for (uint32_t a = 1; a < kk; ++a) {  // insertion sort by global slot
+      const uint32_t v = ss[a], w0 = ee[a];
+      uint32_t w = a;
+      while (w > 0 && ss[w - 1] > v) { ss[w] = ss[w - 1]; ee[w] = ee[w - 1]; --w; }
+      ss[w] = v;
+      ee[w] = w0;
+    }
+    const uint64_t j = j0 + jl;
+    T x[D];
+    load4<T, D>(xa, (uint32_t)j, x);
+    for (uint32_t a = 0; a < kk; ++a) {
+      const uint32_t* wd = reinterpret_cast<const uint32_t*>(rs + (size_t)ee[a] * IL::RS) + 2;
+#pragma unroll
+      for (int cc = 0; cc < D; ++cc) {
+        T dv;
+        from_w(dv, wd + cc * (int)(sizeof(T) / 4));
+        x[cc] += dv;
+      }
+    }
+    if (P.constraint == 1) renormalise<T, D>(x);
+    check_finite<T, D>(x, P, (uint32_t)j, m);
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) xa[j * 4 + cc] = x[cc];
   }
 }
 
