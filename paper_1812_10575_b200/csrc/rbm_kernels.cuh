@@ -19,6 +19,8 @@
 // The state is an array of RS-byte records (RecL in rbm_device.cuh): every
 // move of a particle is one 8/16/32-byte vector access.
 #pragma once
+#include <type_traits>
+
 #include "rbm_device.cuh"
 
 namespace rbm {
@@ -1985,10 +1987,11 @@ __device__ __forceinline__ uint32_t rbmr_draw(const DevParams& P, uint32_t m, ui
 // Delta_s of the p slots of batch s0/p from the members' positions x[l]
 // (Eq. 2.2 over the batch in ascending lane order, prefactor 1/(p-1), exactly
 // 1 for pairs; or the exact pair flow)
-template <typename T, int D, int KK, int INTEG>
+template <typename T, int D, int KK, int INTEG, int PMAX = 64>
 __device__ __forceinline__ void rbmr_deltas(const DevParams& P, uint32_t m, uint64_t s0, uint32_t p,
                                             const uint32_t* jj, T (*x)[D], T (*dl)[D]) {
-  for (uint32_t l = 0; l < p; ++l) {
+  for (uint32_t l = 0; l < (uint32_t)PMAX; ++l) {
+    if (l >= p) break;
     T z[D], xn[D];
 #pragma unroll
     for (int c = 0; c < D; ++c) z[c] = T(0);
@@ -1997,7 +2000,8 @@ __device__ __forceinline__ void rbmr_deltas(const DevParams& P, uint32_t m, uint
       T f[D];
 #pragma unroll
       for (int c = 0; c < D; ++c) f[c] = T(0);
-      for (uint32_t l2 = 0; l2 < p; ++l2) {
+      for (uint32_t l2 = 0; l2 < (uint32_t)PMAX; ++l2) {
+        if (l2 >= p) break;
         if (l2 == l) continue;
         add_interaction<T, D, KK>(x[l], x[l2], f, P);
       }
@@ -2229,32 +2233,44 @@ static __global__ void __launch_bounds__(EMIT_BLOCK) rbmr_emit_kernel(const __gr
   const uint32_t nbins = 1u << P.b1, sh = 32u - P.b1;
   for (uint32_t i = threadIdx.x; i < nbins; i += EMIT_BLOCK) hist[i] = 0;
   __syncthreads();
-  for (uint32_t lb = threadIdx.x; lb < nb; lb += EMIT_BLOCK) {
-    const uint64_t b = b0 + lb, s0 = b * p;
-    uint32_t jj[64];
-    if (KK == KK_ADJ && P.adj_edges) {
-      adj_edge_draw(P, s0, m, jj[0], jj[1]);
-    } else {
-      for (uint32_t l = 0; l < p; ++l) jj[l] = rbmr_draw(P, m, s0 + l, jj, l);
-    }
-    T x[64][D], dl[64][D];
-    for (uint32_t l = 0; l < p; ++l) load4<T, D>(xa, jj[l], x[l]);
-    rbmr_deltas<T, D, KK, INTEG>(P, m, s0, p, jj, x, dl);
-    for (uint32_t l = 0; l < p; ++l) {
-      const uint32_t e = lb * p + l;
-      js[s0 + l] = jj[l];
-      uint32_t w[IL::NW];
+  auto batches = [&](auto pm) {
+    constexpr int PM = decltype(pm)::value;  // array bound: 2 (registers) or 64
+    for (uint32_t lb = threadIdx.x; lb < nb; lb += EMIT_BLOCK) {
+      const uint64_t b = b0 + lb, s0 = b * p;
+      uint32_t jj[PM];
+      if (KK == KK_ADJ && P.adj_edges) {
+        adj_edge_draw(P, s0, m, jj[0], jj[PM > 1 ? 1 : 0]);
+      } else {
+        for (uint32_t l = 0; l < (uint32_t)PM; ++l) {
+          if (l >= p) break;
+          jj[l] = rbmr_draw(P, m, s0 + l, jj, l);
+        }
+      }
+      T x[PM][D], dl[PM][D];
+      for (uint32_t l = 0; l < (uint32_t)PM; ++l) {
+        if (l >= p) break;
+        load4<T, D>(xa, jj[l], x[l]);
+      }
+      rbmr_deltas<T, D, KK, INTEG, PM>(P, m, s0, p, jj, x, dl);
+      for (uint32_t l = 0; l < (uint32_t)PM; ++l) {
+        if (l >= p) break;
+        const uint32_t e = lb * p + l;
+        js[s0 + l] = jj[l];
+        uint32_t w[IL::NW];
 #pragma unroll
-      for (int k = 0; k < IL::NW; ++k) w[k] = 0u;
-      w[0] = jj[l];
-      w[1] = (uint32_t)(s0 + l);
+        for (int k = 0; k < IL::NW; ++k) w[k] = 0u;
+        w[0] = jj[l];
+        w[1] = (uint32_t)(s0 + l);
 #pragma unroll
-      for (int c = 0; c < D; ++c) to_w(dl[l][c], w + 2 + c * (int)(sizeof(T) / 4));
-      st_words<IL::NW>(stg + (size_t)e * IL::RS, w);
-      const uint32_t dg = (jj[l] << P.jshift) >> sh;
-      rk[e] = (dg << 16) | atomicAdd(&hist[dg], 1u);
+        for (int c = 0; c < D; ++c) to_w(dl[l][c], w + 2 + c * (int)(sizeof(T) / 4));
+        st_words<IL::NW>(stg + (size_t)e * IL::RS, w);
+        const uint32_t dg = (jj[l] << P.jshift) >> sh;
+        rk[e] = (dg << 16) | atomicAdd(&hist[dg], 1u);
+      }
     }
-  }
+  };
+  if (p == 2) batches(std::integral_constant<int, 2>{});
+  else batches(std::integral_constant<int, 64>{});
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < nbins; i += EMIT_BLOCK) {
     const uint32_t h = hist[i];
@@ -2280,7 +2296,7 @@ static __global__ void __launch_bounds__(EMIT_BLOCK) rbmr_emit_kernel(const __gr
 }
 
 template <typename T, int D> __host__ __device__ constexpr size_t rapply_smem_bytes(uint32_t cap, uint32_t W) {
-  return (size_t)(cap + 8) * IncL<T, D>::RS + (size_t)cap * 4 + (size_t)W * 8 + 64 * 4 + 16;
+  return (size_t)(cap + 8) * IncL<T, D>::RS + (size_t)W * 4 * sizeof(T) + (size_t)cap * 4 + (size_t)W * 8 + 64 * 4 + 16;
 }
 
 // apply: final bucket b = the particle ids [b W, (b+1) W); n = cnt[b] records
@@ -2299,7 +2315,8 @@ static __global__ void __launch_bounds__(256) rbmr_bucket_apply_kernel(const __g
   const uint32_t nid = (uint32_t)min((uint64_t)W, P.n - j0);
   const uint32_t m = (uint32_t)*P.step;
   unsigned char* rs = smem_raw;
-  uint32_t* pos = reinterpret_cast<uint32_t*>(rs + (size_t)(cap + 8) * IL::RS);  // element -> rank within its particle
+  T* xs = reinterpret_cast<T*>(rs + (size_t)(cap + 8) * IL::RS);   // the id range's positions (4 scalars each)
+  uint32_t* pos = reinterpret_cast<uint32_t*>(xs + (size_t)W * 4);  // element -> rank within its particle
   uint32_t* pc = pos + cap;        // per particle: count
   uint32_t* po = pc + W;           // per particle: first index in ix (after the scan)
   uint32_t* wsum = po + W;
@@ -2308,8 +2325,11 @@ static __global__ void __launch_bounds__(256) rbmr_bucket_apply_kernel(const __g
   if (threadIdx.x == 0 && n) {
     mbar_init(bar, 1);
     const uint32_t bytes = (n * (uint32_t)IL::RS + 15u) & ~15u;
-    mbar_expect_tx(bar, bytes);
-    bulk_g2s_stream(rs, fin + (size_t)b * cap * IL::RS, bytes, bar, l2_evict_first_policy());
+    const uint32_t xbytes = nid * 4u * (uint32_t)sizeof(T);
+    const uint64_t pol = l2_evict_first_policy();
+    mbar_expect_tx(bar, bytes + xbytes);
+    bulk_g2s_stream(rs, fin + (size_t)b * cap * IL::RS, bytes, bar, pol);
+    bulk_g2s_stream(xs, xa + j0 * 4, xbytes, bar, pol);
   }
   for (uint32_t i = threadIdx.x; i < W; i += BLOCK) pc[i] = 0;
   __syncthreads();
@@ -2358,7 +2378,8 @@ static __global__ void __launch_bounds__(256) rbmr_bucket_apply_kernel(const __g
     }
     const uint64_t j = j0 + jl;
     T x[D];
-    load4<T, D>(xa, (uint32_t)j, x);
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) x[cc] = xs[(size_t)jl * 4 + cc];
     for (uint32_t a = 0; a < kk; ++a) {
       const uint32_t* wd = reinterpret_cast<const uint32_t*>(rs + (size_t)ee[a] * IL::RS) + 2;
 #pragma unroll
