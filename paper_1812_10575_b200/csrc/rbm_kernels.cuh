@@ -2296,7 +2296,7 @@ static __global__ void __launch_bounds__(EMIT_BLOCK) rbmr_emit_kernel(const __gr
 }
 
 template <typename T, int D> __host__ __device__ constexpr size_t rapply_smem_bytes(uint32_t cap, uint32_t W) {
-  return (size_t)(cap + 8) * IncL<T, D>::RS + (size_t)W * 4 * sizeof(T) + (size_t)cap * 4 + (size_t)W * 8 + 64 * 4 + 16;
+  return (size_t)(cap + 8) * IncL<T, D>::RS + (size_t)cap * 4 + (size_t)W * 8 + 64 * 4 + 16;
 }
 
 // apply: final bucket b = the particle ids [b W, (b+1) W); n = cnt[b] records
@@ -2315,8 +2315,7 @@ static __global__ void __launch_bounds__(256) rbmr_bucket_apply_kernel(const __g
   const uint32_t nid = (uint32_t)min((uint64_t)W, P.n - j0);
   const uint32_t m = (uint32_t)*P.step;
   unsigned char* rs = smem_raw;
-  T* xs = reinterpret_cast<T*>(rs + (size_t)(cap + 8) * IL::RS);   // the id range's positions (4 scalars each)
-  uint32_t* pos = reinterpret_cast<uint32_t*>(xs + (size_t)W * 4);  // element -> rank within its particle
+  uint32_t* pos = reinterpret_cast<uint32_t*>(rs + (size_t)(cap + 8) * IL::RS);  // element -> rank within its particle
   uint32_t* pc = pos + cap;        // per particle: count
   uint32_t* po = pc + W;           // per particle: first index in ix (after the scan)
   uint32_t* wsum = po + W;
@@ -2325,11 +2324,8 @@ static __global__ void __launch_bounds__(256) rbmr_bucket_apply_kernel(const __g
   if (threadIdx.x == 0 && n) {
     mbar_init(bar, 1);
     const uint32_t bytes = (n * (uint32_t)IL::RS + 15u) & ~15u;
-    const uint32_t xbytes = nid * 4u * (uint32_t)sizeof(T);
-    const uint64_t pol = l2_evict_first_policy();
-    mbar_expect_tx(bar, bytes + xbytes);
-    bulk_g2s_stream(rs, fin + (size_t)b * cap * IL::RS, bytes, bar, pol);
-    bulk_g2s_stream(xs, xa + j0 * 4, xbytes, bar, pol);
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s_stream(rs, fin + (size_t)b * cap * IL::RS, bytes, bar, l2_evict_first_policy());
   }
   for (uint32_t i = threadIdx.x; i < W; i += BLOCK) pc[i] = 0;
   __syncthreads();
@@ -2378,8 +2374,7 @@ static __global__ void __launch_bounds__(256) rbmr_bucket_apply_kernel(const __g
     }
     const uint64_t j = j0 + jl;
     T x[D];
-#pragma unroll
-    for (int cc = 0; cc < D; ++cc) x[cc] = xs[(size_t)jl * 4 + cc];
+    load4<T, D>(xa, (uint32_t)j, x);
     for (uint32_t a = 0; a < kk; ++a) {
       const uint32_t* wd = reinterpret_cast<const uint32_t*>(rs + (size_t)ee[a] * IL::RS) + 2;
 #pragma unroll
