@@ -930,7 +930,11 @@ __device__ __noinline__ void big_bucket(const DevParams& P, State<T, D> src, con
 // Members of batches that straddle the bucket's ends are written unchanged to
 // their sorted places in the own gapped range (the straddle kernel steps them).
 constexpr int MODE_PAIR = 0, MODE_GROUP = 1;
-constexpr int BUCKET_BLOCK = 320, BUCKET_ITEMS = 8;  // 10 warps, capacity <= 2560 in registers
+#ifndef RBM_BUCKET_BLOCK  // design-experiment builds override these (build.py -D...)
+#define RBM_BUCKET_BLOCK 320
+#define RBM_BUCKET_ITEMS 8
+#endif
+constexpr int BUCKET_BLOCK = RBM_BUCKET_BLOCK, BUCKET_ITEMS = RBM_BUCKET_ITEMS;  // 10 warps, capacity <= 2560 in registers
 
 template <typename T, int D> __host__ __device__ constexpr size_t bucket_smem_bytes(uint32_t cap, uint32_t SB,
                                                                                    uint32_t b1) {
