@@ -86,7 +86,11 @@ def elt(cfg):
 def rec_bytes(cfg):
     """Bytes of one state record {id, [key,] x} (RecL in csrc/rbm_device.cuh)."""
     raw = 4 + cfg["d"] * elt(cfg)
-    return 8 if raw <= 8 else (16 if raw <= 16 else 32)
+    if raw <= 8:
+        return 8
+    if raw <= 16:
+        return 16
+    return 24 if (elt(cfg) == 8 and raw + 4 <= 24) else 32
 
 
 def peaks():

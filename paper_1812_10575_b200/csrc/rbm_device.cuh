@@ -119,14 +119,14 @@ __host__ __device__ constexpr size_t big_slot_bytes(size_t rec_x_bytes) {
 // The state is an array of fixed-size records (AoS) so that every move of a
 // particle is one vector access: word 0 = id, then (if it fits) word 1 = the
 // carried shuffle key of the step the record is partitioned for, then the d
-// coordinates.  RS = 8, 16 or 32 bytes:
+// coordinates.  RS = 8, 16, 24 or 32 bytes:
 //   f32 d=1 {id, x} 8 B        f32 d=2 {id, key, x, y} 16 B   f32 d=3 {id, x, y, z} 16 B
-//   f64 d=1 {id, key, x} 16 B  f64 d=2 {id, key, x, y} 32 B   f64 d=3 {id, key, x, y, z} 32 B
+//   f64 d=1 {id, key, x} 16 B  f64 d=2 {id, key, x, y} 24 B   f64 d=3 {id, key, x, y, z} 32 B
 // Unkeyed layouts recompute key_m from the id (Philox) where it is needed;
 // pass 2 hands it to the bucket step in a side array.
 template <typename T, int D> struct RecL {
   static constexpr int XB = D * (int)sizeof(T);
-  static constexpr int RS = (4 + XB <= 8) ? 8 : ((4 + XB <= 16) ? 16 : 32);
+  static constexpr int RS = (4 + XB <= 8) ? 8 : ((4 + XB <= 16) ? 16 : ((sizeof(T) == 8 && 8 + XB <= 24) ? 24 : 32));
   static constexpr bool KEYED = 8 + XB <= RS;
   static constexpr int XW = KEYED ? 2 : (sizeof(T) == 8 ? 2 : 1);  // word offset of x[0]
   static constexpr int NW = RS / 4;
@@ -144,9 +144,12 @@ __device__ __forceinline__ void to_w(double x, uint32_t* w) {
 }
 template <int NW>
 __device__ __forceinline__ void ld_words(const unsigned char* p, uint32_t (&w)[NW]) {
-  if (NW == 2) {
-    const uint2 v = *reinterpret_cast<const uint2*>(p);
-    w[0] = v.x; w[NW > 1 ? 1 : 0] = v.y;
+  if (NW % 4 != 0) {  // 8- and 24-byte records: 8-byte accesses
+#pragma unroll
+    for (int h = 0; h < NW / 2; ++h) {
+      const uint2 v = reinterpret_cast<const uint2*>(p)[h];
+      w[2 * h] = v.x; w[2 * h + 1] = v.y;
+    }
   } else {
 #pragma unroll
     for (int h = 0; h < NW / 4; ++h) {
@@ -157,8 +160,9 @@ __device__ __forceinline__ void ld_words(const unsigned char* p, uint32_t (&w)[N
 }
 template <int NW>
 __device__ __forceinline__ void st_words(unsigned char* p, const uint32_t (&w)[NW]) {
-  if (NW == 2) {
-    *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[NW > 1 ? 1 : 0]);
+  if (NW % 4 != 0) {
+#pragma unroll
+    for (int h = 0; h < NW / 2; ++h) reinterpret_cast<uint2*>(p)[h] = make_uint2(w[2 * h], w[2 * h + 1]);
   } else {
 #pragma unroll
     for (int h = 0; h < NW / 4; ++h)

@@ -63,7 +63,7 @@ constexpr uint32_t FUSED_CAP_MAX = 4096;  // largest per-bucket smem capacity (u
 // bytes of one state record and whether it carries the shuffle key (RecL)
 inline uint32_t rec_bytes(const rbm_config& c) {
   const uint32_t xb = c.d * (c.dtype == RBM_F64 ? 8u : 4u);
-  return (4 + xb <= 8) ? 8u : ((4 + xb <= 16) ? 16u : 32u);
+  return (4 + xb <= 8) ? 8u : ((4 + xb <= 16) ? 16u : ((c.dtype == RBM_F64 && 8 + xb <= 24) ? 24u : 32u));
 }
 inline bool rec_keyed(const rbm_config& c) {
   return 8 + c.d * (c.dtype == RBM_F64 ? 8u : 4u) <= rec_bytes(c);

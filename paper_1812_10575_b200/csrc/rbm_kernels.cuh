@@ -439,8 +439,8 @@ __device__ __forceinline__ bool gapped_tile(const uint32_t* __restrict__ tile_of
 // keyed records).  Records are staged in shared memory by digit so that each
 // reserved run is written coalesced.  Order inside a bucket is irrelevant:
 // the bucket step sorts exactly.
-template <typename T, int D> __host__ __device__ constexpr int prologue_tile() {
-  return (65536 / RecL<T, D>::RS) < 4096 ? (65536 / RecL<T, D>::RS) : 4096;  // <= 64 KB of staged records
+template <typename T, int D> __host__ __device__ constexpr int prologue_tile() {  // <= 64 KB of staged records
+  return ((65536 / RecL<T, D>::RS) < 4096 ? (65536 / RecL<T, D>::RS) : 4096) / 256 * 256;
 }
 template <typename T, int D, int BLOCK> __host__ __device__ constexpr size_t prologue_smem_bytes() {
   return (1024 + 1024 + 64) * 4 + (size_t)prologue_tile<T, D>() * (RecL<T, D>::RS + 2);
