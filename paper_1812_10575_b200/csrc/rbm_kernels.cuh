@@ -624,11 +624,25 @@ static __global__ void __launch_bounds__(BLOCK, 1) split_kernel(const __grid_con
     const uint32_t dbase0 = ((ti.u >> P.segk) & P.nb1_loc_mask) << P.b2;
     const unsigned char* stg = stg0 + s * SBY;
     __syncthreads();
-    for (uint32_t e = tid; e < cnt; e += BLOCK) {
-      const uint32_t key = RT::key(P, stg + (size_t)e * L::RS, m);
-      if (RT::SIDE) kl[e] = key;
-      const uint32_t dg = (key >> sh) & mask;
-      rk[e] = (dg << 16) | atomicAdd(&hist[dg], 1u);
+    // PER <= 4 records per thread: their keys (independent Philox chains for
+    // unkeyed records) are computed together, then ranked in their digits
+    constexpr int PER = (TILE + BLOCK - 1) / BLOCK;
+    {
+      uint32_t kk[PER];
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const uint32_t e = min(tid + k * BLOCK, cnt ? cnt - 1 : 0u);
+        kk[k] = RT::key(P, stg + (size_t)e * L::RS, m);
+      }
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const uint32_t e = tid + k * BLOCK;
+        if (e < cnt) {
+          if (RT::SIDE) kl[e] = kk[k];
+          const uint32_t dg = (kk[k] >> sh) & mask;
+          rk[e] = (dg << 16) | atomicAdd(&hist[dg], 1u);
+        }
+      }
     }
     __syncthreads();
     RBM_PROF(P, 18);
