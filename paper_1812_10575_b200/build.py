@@ -67,6 +67,18 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
     return lib
 
 
+CHECKED = os.path.join(PKG, "librbm_checked.so")
+
+
+def build_checked(force: bool = False) -> str:
+    """librbm_checked.so: the same library with index bounds asserted in the
+    kernels (-DRBM_CHECKED=1; the memory-safety tier, tests/test_checked_gpu.py)."""
+    if not force and os.path.exists(CHECKED) and os.path.getmtime(CHECKED) >= max(
+            os.path.getmtime(p) for p in _sources()):
+        return CHECKED
+    return build(force=True, out=CHECKED, defines=["RBM_CHECKED=1"])
+
+
 if __name__ == "__main__":
     # python -m paper_1812_10575_b200.build [--force] [-DNAME=V ... -o out.so]
     defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]

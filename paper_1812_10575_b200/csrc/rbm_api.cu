@@ -36,6 +36,7 @@ rbm_status check_flags(rbm_ctx* c) {
   CU(cudaMemcpy(&nf, c->nonfinite, sizeof nf, cudaMemcpyDeviceToHost));
   CU(cudaMemcpy(&cap, c->capacity_err, sizeof cap, cudaMemcpyDeviceToHost));
   if (cap == 2) return fail(c, RBM_ERR_CAPACITY, "a rank of the partitioned system held fewer than p particles; results are invalid");
+  if (cap == 3) return fail(c, RBM_ERR_CAPACITY, "bounds check failed in a kernel (checked build); results are invalid");
   if (cap) return fail(c, RBM_ERR_CAPACITY, "a bucket exceeded every capacity fallback; results of that step are invalid");
   if (nf != ~0ull)
     return fail(c, RBM_ERR_NONFINITE, "non-finite position at step %llu, particle id %llu",

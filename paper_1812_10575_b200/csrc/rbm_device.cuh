@@ -108,6 +108,21 @@ struct DevParams {
     }                                                                   \
   } while (0)
 
+// Checked build (librbm_checked.so, -DRBM_CHECKED=1): index bounds asserted
+// in the kernels; a violation sets capacity_err = 3, reported by rbm_sync /
+// rbm_gather as RBM_ERR_CAPACITY ("bounds check").  compute-sanitizer is not
+// available on the GPU pool, so this build is the memory-safety tier.
+#ifdef RBM_CHECKED
+#define RBM_CHECK(P, cond)                                     \
+  do {                                                         \
+    if (!(cond)) atomicExch((P).capacity_err, 3u);             \
+  } while (0)
+#else
+#define RBM_CHECK(P, cond) \
+  do {                     \
+  } while (0)
+#endif
+
 constexpr int NBIG = 2;             // concurrent oversized buckets handled per step
 constexpr uint32_t BIG_CAP = 65535; // u16 indices
 // bytes of one oversized-bucket scratch slot (256-B aligned stride)

@@ -496,6 +496,7 @@ static __global__ void __launch_bounds__(BLOCK) prologue_kernel(const __grid_con
     if (e < cnt) {
       const uint32_t dg = rds[k] >> 16;
       const uint32_t s = hist[dg] + (rds[k] & 0xffffu);
+      RBM_CHECK(P, s < cnt);
       st_rec<T, D>(stg, s, rr[k]);
       st_dig[s] = (uint16_t)dg;
     }
@@ -663,6 +664,7 @@ static __global__ void __launch_bounds__(BLOCK, 1) split_kernel(const __grid_con
     for (uint32_t e = tid; e < cnt; e += BLOCK) {
       const uint32_t v = rk[e];
       const uint32_t pos = off[v >> 16] + (v & 0xffffu);
+      RBM_CHECK(P, pos < cnt);
       inv[pos] = (uint16_t)e;
       idg[pos] = (uint16_t)(v >> 16);
     }
@@ -675,6 +677,7 @@ static __global__ void __launch_bounds__(BLOCK, 1) split_kernel(const __grid_con
     RBM_PROF(P, 20);
     for (uint32_t j = tid; j < cnt; j += BLOCK) {
       const uint32_t e = inv[j], dg = idg[j];
+      RBM_CHECK(P, e < cnt && dg < nbins);
       const uint32_t slot = gbase[dg] + j;
       if (slot >= dcap) {  // bucket capacity exceeded (probability ~1e-30): fail loudly
         atomicExch(P.capacity_err, 1u);
@@ -1039,6 +1042,7 @@ __device__ __forceinline__ void bucket_body(const DevParams& P, State<T, D> src,
     if (e < n) {
       const uint32_t sd = rsd[k] >> 16, sh16 = (sd & 1u) << 4;
       const uint32_t a = (off[sd >> 1] >> sh16) & 0xffffu, c = (cnt[sd >> 1] >> sh16) & 0xffffu;
+      RBM_CHECK(P, a + (rsd[k] & 0xffffu) < n && a + c <= n);
       ks[a + (rsd[k] & 0xffffu)] = rc[k];
       rsd[k] = (a << 16) | c;  // sub-bucket start and size, for the rank below
     }
@@ -1060,6 +1064,7 @@ __device__ __forceinline__ void bucket_body(const DevParams& P, State<T, D> src,
 #pragma unroll 1
         for (uint32_t i = 6; i < c; ++i) r += (ks[a + i] < rc[k]) ? 1u : 0u;
       }
+      RBM_CHECK(P, r < n);
       ord[r] = (uint16_t)e;
     }
   }
@@ -1099,7 +1104,9 @@ __device__ __forceinline__ void bucket_body(const DevParams& P, State<T, D> src,
       const uint32_t j = k * BLOCK + threadIdx.x;
       if (j < npairs) {
         const uint32_t q = head + 2 * j;
+        RBM_CHECK(P, q + 1 < n);
         const uint32_t e0 = ord[q], e1 = ord[q + 1];
+        RBM_CHECK(P, e0 < n && e1 < n);
         Rec<T, D> r0 = ld_rec<T, D>(rs, e0), r1 = ld_rec<T, D>(rs, e1);
         const uint32_t kn0 = shuffle_key(P, r0.id, m + 1), kn1 = shuffle_key(P, r1.id, m + 1);
         T y0[D], y1[D];
@@ -1244,7 +1251,11 @@ __device__ __forceinline__ void bucket_body(const DevParams& P, State<T, D> src,
   const uint32_t total = block_excl_scan4<BLOCK>(cnt, off, nout, wsum);
   for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {  // staging index (tb read in element order)
     const uint32_t t = tb[e];
-    if (t != 0xffffffffu) inv[off[t >> 16] + (t & 0xffffu)] = e | (t & 0xffff0000u);
+    RBM_CHECK(P, t == 0xffffffffu || (t >> 16) < nout);
+    if (t != 0xffffffffu) {
+      RBM_CHECK(P, off[t >> 16] + (t & 0xffffu) < total);
+      inv[off[t >> 16] + (t & 0xffffu)] = e | (t & 0xffff0000u);
+    }
   }
 #pragma unroll
   for (int r = 0; r < NRES; ++r)  // gbase[d] - off[d]: output position j goes to slot gbase[dg] + j
@@ -1255,6 +1266,7 @@ __device__ __forceinline__ void bucket_body(const DevParams& P, State<T, D> src,
   for (uint32_t j = threadIdx.x; j < total; j += BLOCK) {
     const uint32_t v = inv[j];
     const uint32_t e = v & 0xffffu, dg = v >> 16;
+    RBM_CHECK(P, e < n && dg < nout);
     const uint32_t slot = gbase[dg] + j;
     if (slot >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
     out_copy<T, D>(dst, out_seg(P, dg, blockIdx.x), dcap, slot, rs + (size_t)e * L::RS);
@@ -1423,6 +1435,7 @@ static __global__ void __launch_bounds__(256) straddle_kernel(const __grid_const
     for (uint32_t q = 0; q < sz; ++q) {
       const uint32_t Pq = b0 + q;
       while (Pq >= S[bb + 1]) ++bb;
+      RBM_CHECK(P, Pq - S[bb] < cap && sz <= 96);
       if ((q & 31u) == (uint32_t)lane) phys[k++] = (long long)bb * cap + (Pq - S[bb]);
     }
   }
@@ -2299,6 +2312,7 @@ static __global__ void __launch_bounds__(EMIT_BLOCK) rbmr_emit_kernel(const __gr
   block_excl_scan<EMIT_BLOCK>(off, nbins, wsum);
   for (uint32_t e = threadIdx.x; e < cnt; e += EMIT_BLOCK) {
     const uint32_t v = rk[e];
+    RBM_CHECK(P, off[v >> 16] + (v & 0xffffu) < cnt);
     inv[off[v >> 16] + (v & 0xffffu)] = (uint16_t)e;
   }
   __syncthreads();
@@ -2354,6 +2368,7 @@ static __global__ void __launch_bounds__(256) rbmr_bucket_apply_kernel(const __g
   if (n) mbar_wait(bar, 0);
   for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
     const uint32_t jl = (uint32_t)(reinterpret_cast<const uint32_t*>(rs + (size_t)e * IL::RS)[0] - j0);
+    RBM_CHECK(P, jl < nid);
     pos[e] = atomicAdd(&pc[jl], 1u);
   }
   __syncthreads();
@@ -2369,7 +2384,10 @@ static __global__ void __launch_bounds__(256) rbmr_bucket_apply_kernel(const __g
   }
   __syncthreads();  // pos is dead: its space becomes ix
   k = 0;
-  for (uint32_t e = threadIdx.x; e < n; e += BLOCK, ++k) ix[po[myjl[k]] + myr[k]] = (uint16_t)e;
+  for (uint32_t e = threadIdx.x; e < n; e += BLOCK, ++k) {
+    RBM_CHECK(P, k < 8 && po[myjl[k]] + myr[k] < n);
+    ix[po[myjl[k]] + myr[k]] = (uint16_t)e;
+  }
   __syncthreads();
   // every particle of the range with increments: ascending slot order (D:8)
   for (uint32_t jl = threadIdx.x; jl < nid; jl += BLOCK) {
