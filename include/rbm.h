@@ -77,9 +77,9 @@ typedef enum { RBM_F32 = 0, RBM_F64 = 1 } rbm_dtype;
 /* RBM_SCHEME_RBMR_SEQ: Algorithm 2 (RBM-r') exactly as
  * written: the ceil(N/p) batches of a sweep (the same slot draws as RBMR) are
  * applied in draw order, each from the positions left by the earlier ones.
- * Run level by level on the GPU (a batch's level = the longest chain of
- * earlier batches sharing a member); each rbm_step synchronises the stream
- * once per sweep to size the levels (no CUDA graph). */
+ * On the GPU each batch waits only for the earlier batches that last touched
+ * its members (dependency flags), so independent batches run in parallel; no
+ * host synchronisation, CUDA-graph replayed like the other schemes. */
 typedef enum { RBM_SCHEME_RBM1 = 0, RBM_SCHEME_RBMR = 1, RBM_SCHEME_RBMR_SEQ = 2 } rbm_scheme;
 /* RBM_INTEG_VERLET (row f3): the second-order (Hamiltonian) system of
  * PAPER.md:848-870, X' = V, V' = -grad V(X) + mean K, for 1-D particles

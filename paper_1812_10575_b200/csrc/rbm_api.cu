@@ -422,7 +422,7 @@ rbm_status rbm_run(rbm_ctx* c, uint64_t nsteps) {
     ++c->step;
     --nsteps;
   }
-  if (nsteps >= per && !c->timing && c->cfg.scheme != RBM_SCHEME_RBMR_SEQ) {  // (the sequential sweep syncs per step)
+  if (nsteps >= per && !c->timing) {
     const int slot = (c->cur << 1) | (int)(c->step & 1);
     if (!c->graph[slot]) {
       const int cur0 = c->cur;

@@ -112,8 +112,7 @@ struct rbm_ctx {
   uint32_t *js = nullptr, *rmcnt = nullptr, *rmbox = nullptr, *rovf = nullptr, *rnovf = nullptr;
   void* rxa = nullptr;     // AoS state (4 scalars per particle, id order)
   unsigned char* rinc[2] = {nullptr, nullptr};  // RBM-r increment records: pass-1 and final buckets
-  uint32_t *rprevb = nullptr, *rlevel = nullptr, *rorder = nullptr, *rlcnt = nullptr, *rloff = nullptr,
-           *rlcur = nullptr, *rflags = nullptr;  // sequential RBM-r' (levels)
+  uint32_t *rprevb = nullptr, *rdone = nullptr, *rticket = nullptr;  // sequential RBM-r': slot chains, batch flags
   bool aos_valid = false;  // RBM-r state currently in rxa
   // RBM-r on a partitioned system (row e2): exchange regions and own batches
   RPart rp{};
@@ -449,12 +448,8 @@ inline void carve(rbm_ctx& c, Workspace& ws) {
       c.rovf = ws.take<uint32_t>(2 * (size_t)OVF_CAP);
       c.rnovf = ws.take<uint32_t>(1);
       c.rprevb = ws.take<uint32_t>(c.nslots);
-      c.rlevel = ws.take<uint32_t>(c.nbatch);
-      c.rorder = ws.take<uint32_t>(c.nbatch);
-      c.rlcnt = ws.take<uint32_t>(MAX_LEVELS + 1);
-      c.rloff = ws.take<uint32_t>(MAX_LEVELS + 1);
-      c.rlcur = ws.take<uint32_t>(MAX_LEVELS + 1);
-      c.rflags = ws.take<uint32_t>(2);
+      c.rdone = ws.take<uint32_t>(c.nbatch);
+      c.rticket = ws.take<uint32_t>(4);
     }
   }
   ws.used = (ws.used + 255) & ~size_t(255);
@@ -852,53 +847,28 @@ struct Engine final : EngineBase {
     return total;
   }
 
-  // Algorithm 2 as written (row f2): draws, per-particle slot chains, levels
-  // by relaxation (host-checked convergence), counting sort of the batches by
-  // level, then one launch per level
+  // Algorithm 2 as written (row f2): draws + per-particle slot chains, then
+  // the dependency-driven sweep (no host synchronisation: graph-capturable)
   void step_rbmr_seq(rbm_ctx& c, cudaStream_t s) {
     const DevParams& P = c.P;
     const uint64_t n = c.cfg.n;
     T* xa = reinterpret_cast<T*>(c.rxa);
     if (!c.aos_valid) {
       rbmr_pack_kernel<T, D><<<grid_for(n, 256), 256, 0, s>>>(n, st(c, c.cur), xa);
+      cudaMemsetAsync(c.rdone, 0, c.nbatch * 4, s);  // flags carry the step stamp m + 1
       c.aos_valid = true;
     }
     cudaMemsetAsync(c.rmcnt, 0, n * 4, s);
     cudaMemsetAsync(c.rnovf, 0, 4, s);
-    cudaMemsetAsync(c.rlcnt, 0, (MAX_LEVELS + 1) * 4, s);
-    cudaMemsetAsync(c.rflags, 0, 8, s);
+    cudaMemsetAsync(c.rticket, 0, 4, s);
     const unsigned gb = grid_for(c.nbatch, 128, 148 * 64);
     c.mark(s);
-    rbmr_draw_reg_kernel<<<gb, 128, 0, s>>>(P, c.nbatch, c.js, c.rmcnt, c.rmbox, c.rovf, c.rnovf, c.rlevel);
+    rbmr_draw_reg_kernel<<<gb, 128, 0, s>>>(P, c.nbatch, c.js, c.rmcnt, c.rmbox, c.rovf, c.rnovf);
     c.mark(s);
     rbmr_prev_kernel<<<grid_for(n, 256), 256, 0, s>>>(P, n, c.rmcnt, c.rmbox, c.rovf, c.rnovf, c.rprevb);
     c.mark(s);
-    for (uint32_t it = 0; it < MAX_LEVELS; it += 4) {
-      cudaMemsetAsync(c.rflags, 0, 4, s);
-      for (int k = 0; k < 4; ++k)
-        rbmr_level_kernel<<<grid_for(c.nbatch, 256), 256, 0, s>>>(P, c.nbatch, c.rprevb, c.rlevel, c.rflags);
-      uint32_t changed = 1;
-      cudaMemcpyAsync(&changed, c.rflags, 4, cudaMemcpyDeviceToHost, s);
-      cudaStreamSynchronize(s);
-      if (!changed) break;
-    }
-    rbmr_level_hist_kernel<<<grid_for(c.nbatch, 256), 256, 0, s>>>(c.nbatch, c.rlevel, c.rlcnt, c.rflags + 1);
-    rbmr_level_scan_kernel<<<1, 1024, 0, s>>>(c.rlcnt, c.rloff, c.rlcur);
-    rbmr_level_scatter_kernel<<<grid_for(c.nbatch, 256), 256, 0, s>>>(c.nbatch, c.rlevel, c.rlcur, c.rorder);
-    std::vector<uint32_t> loff(MAX_LEVELS + 1);
-    uint32_t lerr = 0;
-    cudaMemcpyAsync(loff.data(), c.rloff, (MAX_LEVELS + 1) * 4, cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(&lerr, c.rflags + 1, 4, cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    if (lerr) cudaMemsetAsync(c.capacity_err, 1, 1, s);  // deeper than MAX_LEVELS: flagged
-    c.mark(s);
-    for (uint32_t lv = 0; lv < MAX_LEVELS; ++lv) {
-      const uint32_t o0 = loff[lv], o1 = loff[lv + 1];
-      if (o1 > o0)
-        rbmr_seq_apply_kernel<T, D, KK, INTEG><<<grid_for(o1 - o0, 128), 128, 0, s>>>(P, c.rorder, o0, o1,
-                                                                                      c.js, xa);
-      if (o1 == loff[MAX_LEVELS]) break;
-    }
+    rbmr_seq_dep_kernel<T, D, KK, INTEG><<<(unsigned)num_sms * 16, 128, 0, s>>>(P, c.nbatch, c.js, c.rprevb, xa,
+                                                                              c.rdone, c.rticket);
     c.mark(s);
     advance_kernel<<<1, 1, 0, s>>>(c.step_dev);
     c.mark(s);
@@ -980,8 +950,8 @@ EngineBase* make_for_kernel(uint32_t kernel, uint32_t integ) {
 inline const char* const* kernel_names(const rbm_ctx& c, uint32_t* count) {
   static const char* const r[] = {"rbmr_emit", "rbmr_apply", "advance"};
   static const char* const r2[] = {"rbmr_emit", "tile_scan", "split", "rbmr_apply", "advance"};
-  static const char* const rs[] = {"rbmr_draw", "rbmr_prev", "rbmr_levels", "rbmr_seq_apply", "advance"};
-  if (c.cfg.scheme == RBM_SCHEME_RBMR_SEQ) { *count = 5; return rs; }
+  static const char* const rs[] = {"rbmr_draw", "rbmr_prev", "rbmr_seq_sweep", "advance"};
+  if (c.cfg.scheme == RBM_SCHEME_RBMR_SEQ) { *count = 4; return rs; }
   static const char* const b0[] = {"resident_step"};
   static const char* const p1[] = {"tile_scan", "bucket_step", "straddle", "advance"};
   static const char* const p2[] = {"tile_scan", "split", "final_scan", "bucket_step", "straddle", "advance"};

@@ -1771,18 +1771,21 @@ __device__ __forceinline__ void load4(const T* __restrict__ xa, uint32_t j, T (&
 
 // ----------------------- exact sequential RBM-r' (Alg. 2, row f2)
 // Batches of one sweep are applied in draw order from the current positions.
-// Batch b depends on the earlier batches that share a member; its level is
-// the longest such chain.  Batches of one level have disjoint members, so the
-// sweep runs level by level with every batch of a level in parallel, and each
-// batch sees exactly the positions the sequential loop would give it.
+// Batch b depends only on the earlier batches that last touched one of its
+// members (prevb).  One dependency-driven kernel applies them: warps take
+// consecutive groups of 32 batches in ticket order, and a batch starts once
+// the flags of its prevb batches carry this step's stamp; it then reads the
+// current positions and publishes its own flag.  Every batch waits only on
+// lower-numbered batches, which were taken earlier by running warps, so the
+// sweep always drains; each batch sees exactly the positions the sequential
+// loop would give it.  No levels, no host synchronisation.
 constexpr uint32_t NO_BATCH = 0xffffffffu;
-constexpr uint32_t MAX_LEVELS = 4096;
 
 // draws j_s of batch b (as the oracle, reading D:9) and mailbox registration only
 static __global__ void __launch_bounds__(128) rbmr_draw_reg_kernel(const __grid_constant__ DevParams P, uint64_t nbatch,
                                                                    uint32_t* __restrict__ js, uint32_t* __restrict__ mcnt,
                                                                    uint32_t* __restrict__ mbox, uint32_t* __restrict__ ovf,
-                                                                   uint32_t* __restrict__ novf, uint32_t* __restrict__ level) {
+                                                                   uint32_t* __restrict__ novf) {
   const uint32_t m = (uint32_t)*P.step;
   const uint32_t p = P.p;
   for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nbatch;
@@ -1812,7 +1815,6 @@ static __global__ void __launch_bounds__(128) rbmr_draw_reg_kernel(const __grid_
         else atomicExch(P.capacity_err, 1u);
       }
     }
-    level[b] = 0;
   }
 }
 
@@ -1850,118 +1852,97 @@ static __global__ void rbmr_prev_kernel(const __grid_constant__ DevParams P, uin
   }
 }
 
-// one relaxation sweep of level[b] = max over members (level[prevb] + 1);
-// monotone, reaches the longest-chain levels after (depth + 1) sweeps
-static __global__ void rbmr_level_kernel(const __grid_constant__ DevParams P, uint64_t nbatch,
-                                         const uint32_t* __restrict__ prevb, uint32_t* level,
-                                         uint32_t* changed) {
-  const uint32_t p = P.p;
-  uint32_t ch = 0;
-  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nbatch;
-       b += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t lv = 0;
-    for (uint32_t l = 0; l < p; ++l) {
-      const uint32_t pb = prevb[b * p + l];
-      if (pb != NO_BATCH) lv = max(lv, level[pb] + 1u);
-    }
-    if (lv > level[b]) {
-      level[b] = lv;
-      ch = 1;
-    }
-  }
-  if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) atomicExch(changed, 1u);
-}
-
-// batches grouped by level: histogram, then order[] by level (counting sort)
-static __global__ void rbmr_level_hist_kernel(uint64_t nbatch, const uint32_t* __restrict__ level,
-                                              uint32_t* lcnt, uint32_t* err) {
-  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nbatch;
-       b += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t lv = level[b];
-    if (lv < MAX_LEVELS) atomicAdd(&lcnt[lv], 1u);
-    else atomicExch(err, 1u);
-  }
-}
-
-static __global__ void __launch_bounds__(1024) rbmr_level_scan_kernel(const uint32_t* __restrict__ lcnt,
-                                                                      uint32_t* loff, uint32_t* lcur) {
-  __shared__ uint32_t a[MAX_LEVELS];
-  __shared__ uint32_t ws[33];
-  for (uint32_t i = threadIdx.x; i < MAX_LEVELS; i += blockDim.x) a[i] = lcnt[i];
-  __syncthreads();
-  const uint32_t total = block_excl_scan<1024>(a, MAX_LEVELS, ws);
-  for (uint32_t i = threadIdx.x; i < MAX_LEVELS; i += blockDim.x) { loff[i] = a[i]; lcur[i] = a[i]; }
-  if (threadIdx.x == 0) loff[MAX_LEVELS] = total;
-}
-
-static __global__ void rbmr_level_scatter_kernel(uint64_t nbatch, const uint32_t* __restrict__ level,
-                                                 uint32_t* lcur, uint32_t* order) {
-  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nbatch;
-       b += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t lv = level[b];
-    if (lv < MAX_LEVELS) order[atomicAdd(&lcur[lv], 1u)] = (uint32_t)b;
-  }
-}
-
-// the batches order[o0 .. o1) of one level: Eq. (2.2) + update from the
-// current positions, written in place (members are disjoint within a level)
+// one batch of the sequential sweep from the current positions (members
+// distinct): Eq. (2.2) + EM, or the exact pair flow; positions read through L2
+// (other SMs wrote them) and written in place
 template <typename T, int D, int KK, int INTEG>
-static __global__ void __launch_bounds__(128) rbmr_seq_apply_kernel(const __grid_constant__ DevParams P,
-                                                                    const uint32_t* __restrict__ order, uint32_t o0,
-                                                                    uint32_t o1, const uint32_t* __restrict__ js,
-                                                                    T* __restrict__ xa) {
-  const uint32_t m = (uint32_t)*P.step;
+__device__ __forceinline__ void seq_batch(const DevParams& P, uint32_t m, uint64_t b, const uint32_t* __restrict__ js,
+                                          T* xa) {
   const uint32_t p = P.p;
-  for (uint32_t o = o0 + blockIdx.x * blockDim.x + threadIdx.x; o < o1; o += gridDim.x * blockDim.x) {
-    const uint64_t b = order[o], s0 = b * p;
-    if (INTEG == 0) {
-      T xn[64][D];  // p <= 64; new positions of all members before any is written
-      for (uint32_t l = 0; l < p; ++l) {
-        T xi[D], f[D], z[D];
-        load4<T, D>(xa, js[s0 + l], xi);
+  const uint64_t s0 = b * p;
+  auto ld = [&](uint32_t j, T (&x)[D]) {
 #pragma unroll
-        for (int c = 0; c < D; ++c) { f[c] = T(0); z[c] = T(0); }
-        for (uint32_t l2 = 0; l2 < p; ++l2) {
-          if (l2 == l) continue;
-          T xj[D];
-          load4<T, D>(xa, js[s0 + l2], xj);
-          add_interaction<T, D, KK>(xi, xj, f, P);
-        }
-        const T inv = T(1) / T(p - 1);
+    for (int c = 0; c < D; ++c) x[c] = __ldcg(xa + (size_t)j * 4 + c);
+  };
+  if (INTEG == 0) {
+    T xn[64][D];  // p <= 64; new positions of all members before any is written
+    for (uint32_t l = 0; l < p; ++l) {
+      T xi[D], f[D], z[D];
+      ld(js[s0 + l], xi);
 #pragma unroll
-        for (int c = 0; c < D; ++c) f[c] *= inv;
-        if (P.has_noise) Normals<T, D>::get(P, (uint32_t)(s0 + l), m, TAG_NOISE_SLOT, z);
-        em_update<T, D>(xi, f, z, xn[l], P, true);
-        check_finite<T, D>(xn[l], P, js[s0 + l], m);
+      for (int c = 0; c < D; ++c) { f[c] = T(0); z[c] = T(0); }
+      for (uint32_t l2 = 0; l2 < p; ++l2) {
+        if (l2 == l) continue;
+        T xj[D];
+        ld(js[s0 + l2], xj);
+        add_interaction<T, D, KK>(xi, xj, f, P);
       }
-      for (uint32_t l = 0; l < p; ++l) {
-        const uint32_t j = js[s0 + l];
+      const T inv = T(1) / T(p - 1);
 #pragma unroll
-        for (int c = 0; c < D; ++c) xa[(size_t)j * 4 + c] = xn[l][c];
-      }
-    } else {
-      const uint32_t i = js[s0], j = js[s0 + 1];
-      T xi[D], xj[D], y[D], z[D], xn[D];
-      load4<T, D>(xa, i, xi);
-      load4<T, D>(xa, j, xj);
-#pragma unroll
-      for (int c = 0; c < D; ++c) z[c] = T(0);
-      if (KK == KK_ADJ) adj_flow<T, D>(P, i, j, xi, xj, true, y);
-      else pair_flow<T, D, KK>(xi, xj, true, y, P);
-      if (P.has_noise) Normals<T, D>::get(P, (uint32_t)s0, m, TAG_NOISE_SLOT, z);
-      split_finish<T, D>(y, z, xn, P, true);
-      check_finite<T, D>(xn, P, i, m);
-      T yj[D], xnj[D];
-#pragma unroll
-      for (int c = 0; c < D; ++c) z[c] = T(0);
-      if (KK == KK_ADJ) adj_flow<T, D>(P, i, j, xi, xj, false, yj);
-      else pair_flow<T, D, KK>(xi, xj, false, yj, P);
-      if (P.has_noise) Normals<T, D>::get(P, (uint32_t)(s0 + 1), m, TAG_NOISE_SLOT, z);
-      split_finish<T, D>(yj, z, xnj, P, true);
-      check_finite<T, D>(xnj, P, j, m);
-#pragma unroll
-      for (int c = 0; c < D; ++c) { xa[(size_t)i * 4 + c] = xn[c]; xa[(size_t)j * 4 + c] = xnj[c]; }
+      for (int c = 0; c < D; ++c) f[c] *= inv;
+      if (P.has_noise) Normals<T, D>::get(P, (uint32_t)(s0 + l), m, TAG_NOISE_SLOT, z);
+      em_update<T, D>(xi, f, z, xn[l], P, true);
+      check_finite<T, D>(xn[l], P, js[s0 + l], m);
     }
+    for (uint32_t l = 0; l < p; ++l) {
+      const uint32_t j = js[s0 + l];
+#pragma unroll
+      for (int c = 0; c < D; ++c) xa[(size_t)j * 4 + c] = xn[l][c];
+    }
+  } else {
+    const uint32_t i = js[s0], j = js[s0 + 1];
+    T xi[D], xj[D], y[D], z[D], xn[D];
+    ld(i, xi);
+    ld(j, xj);
+#pragma unroll
+    for (int c = 0; c < D; ++c) z[c] = T(0);
+    if (KK == KK_ADJ) adj_flow<T, D>(P, i, j, xi, xj, true, y);
+    else pair_flow<T, D, KK>(xi, xj, true, y, P);
+    if (P.has_noise) Normals<T, D>::get(P, (uint32_t)s0, m, TAG_NOISE_SLOT, z);
+    split_finish<T, D>(y, z, xn, P, true);
+    check_finite<T, D>(xn, P, i, m);
+    T yj[D], xnj[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) z[c] = T(0);
+    if (KK == KK_ADJ) adj_flow<T, D>(P, i, j, xi, xj, false, yj);
+    else pair_flow<T, D, KK>(xi, xj, false, yj, P);
+    if (P.has_noise) Normals<T, D>::get(P, (uint32_t)(s0 + 1), m, TAG_NOISE_SLOT, z);
+    split_finish<T, D>(yj, z, xnj, P, true);
+    check_finite<T, D>(xnj, P, j, m);
+#pragma unroll
+    for (int c = 0; c < D; ++c) { xa[(size_t)i * 4 + c] = xn[c]; xa[(size_t)j * 4 + c] = xnj[c]; }
+  }
+}
+
+// the sweep, dependency-driven: done[b] = m + 1 once batch b of step m is applied
+template <typename T, int D, int KK, int INTEG>
+static __global__ void __launch_bounds__(128) rbmr_seq_dep_kernel(const __grid_constant__ DevParams P, uint64_t nbatch,
+                                                                  const uint32_t* __restrict__ js,
+                                                                  const uint32_t* __restrict__ prevb, T* xa,
+                                                                  uint32_t* done, uint32_t* ticket) {
+  const uint32_t m = (uint32_t)*P.step;
+  const uint32_t stamp = m + 1u;
+  const uint32_t p = P.p;
+  const uint32_t lane = threadIdx.x & 31u;
+  for (;;) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(ticket, 32u);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if ((uint64_t)base >= nbatch) break;
+    const uint64_t b = (uint64_t)base + lane;
+    if (b < nbatch) {
+      for (uint32_t l = 0; l < p; ++l) {
+        const uint32_t pb = prevb[b * p + l];
+        if (pb == NO_BATCH) continue;
+        RBM_CHECK(P, pb < b);
+        while (atomicAdd(&done[pb], 0u) != stamp) __nanosleep(32);
+      }
+      __threadfence();
+      seq_batch<T, D, KK, INTEG>(P, m, b, js, xa);
+      __threadfence();
+      atomicExch(&done[b], stamp);
+    }
+    __syncwarp();
   }
 }
 
