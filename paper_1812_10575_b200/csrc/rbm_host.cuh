@@ -112,7 +112,7 @@ struct rbm_ctx {
   uint32_t *js = nullptr, *rmcnt = nullptr, *rmbox = nullptr, *rovf = nullptr, *rnovf = nullptr;
   void* rxa = nullptr;     // AoS state (4 scalars per particle, id order)
   unsigned char* rinc[2] = {nullptr, nullptr};  // RBM-r increment records: pass-1 and final buckets
-  uint32_t *rprevb = nullptr, *rdone = nullptr, *rticket = nullptr;  // sequential RBM-r': slot chains, batch flags
+  uint32_t *rexpect = nullptr, *rticket = nullptr;  // sequential RBM-r': per-slot expected tags, ticket
   bool aos_valid = false;  // RBM-r state currently in rxa
   // RBM-r on a partitioned system (row e2): exchange regions and own batches
   RPart rp{};
@@ -188,8 +188,8 @@ inline Layout choose_layout(const rbm_config& c) {
     if (v < floor_) v = floor_;
     return (uint32_t)((v + 63) & ~63ull);
   };
-  if (c.scheme == RBM_SCHEME_RBMR && !part) {
-    // RBM-r increments partitioned by particle index: final buckets of
+  if ((c.scheme == RBM_SCHEME_RBMR || c.scheme == RBM_SCHEME_RBMR_SEQ) && !part) {
+    // RBM-r increments (RBM-r' link records) partitioned by particle index: final buckets of
     // W = 2^(idbits-B) ids (~1024), one or two passes as for RBM-1
     uint32_t B = ceil_log2((double)n / 1024.0);
     if (B > L.idbits) B = L.idbits;
@@ -352,7 +352,7 @@ inline rbm_status validate(const rbm_config* cfg) {
   if (k.scheme == RBM_SCHEME_RBM1 && L.B == 0 &&
       (k.dtype == RBM_F64 ? resident_smem_bytes<double, 3>(L.cap) : resident_smem_bytes<float, 3>(L.cap)) > 227 * 1024)
     return fail(c, RBM_ERR_INVALID_ARG, "n=%llu too large for the resident kernel", (unsigned long long)k.n);
-  if (k.scheme == RBM_SCHEME_RBMR && !is_partitioned(k) && L.cap2 > 2048)
+  if ((k.scheme == RBM_SCHEME_RBMR || k.scheme == RBM_SCHEME_RBMR_SEQ) && !is_partitioned(k) && L.cap2 > 2048)
     return fail(c, RBM_ERR_UNSUPPORTED, "RBM-r: %u slot records per id bucket exceed 2048", L.cap2);
   if (k.scheme == RBM_SCHEME_RBM1 && L.B > 0 && bucket_smem(k, L) > 227 * 1024)
     return fail(c, RBM_ERR_INVALID_ARG, "bucket capacity %u needs %zu B of shared memory", L.cap, bucket_smem(k, L));
@@ -435,20 +435,15 @@ inline void carve(rbm_ctx& c, Workspace& ws) {
   } else if (k.scheme != RBM_SCHEME_RBM1) {
     c.nbatch = (n + k.p - 1) / k.p;
     c.nslots = c.nbatch * k.p;
-    if (k.scheme == RBM_SCHEME_RBMR) {
-      const size_t irs = ((8 + k.d * es) + 15) / 16 * 16;
+    {  // RBM-r increment records, or the 8-byte link records of RBM-r'
+      const size_t irs = k.scheme == RBM_SCHEME_RBMR_SEQ ? 8 : ((8 + k.d * es) + 15) / 16 * 16;
       c.rinc[0] = ws.take<unsigned char>((size_t)(1u << c.L.b1) * c.L.cap1 * irs);
       if (c.L.b2) c.rinc[1] = ws.take<unsigned char>((size_t)c.L.nbuckets * c.L.cap2 * irs);
     }
     c.js = ws.take<uint32_t>(c.nslots);
     c.rxa = ws.take<unsigned char>(n * 4 * es);
-    if (k.scheme == RBM_SCHEME_RBMR_SEQ) {  // per-particle slot mailboxes (levels of the sequential sweep)
-      c.rmcnt = ws.take<uint32_t>(n);
-      c.rmbox = ws.take<uint32_t>(n * MBOX);
-      c.rovf = ws.take<uint32_t>(2 * (size_t)OVF_CAP);
-      c.rnovf = ws.take<uint32_t>(1);
-      c.rprevb = ws.take<uint32_t>(c.nslots);
-      c.rdone = ws.take<uint32_t>(c.nbatch);
+    if (k.scheme == RBM_SCHEME_RBMR_SEQ) {  // slot chains and flags of the sequential sweep
+      c.rexpect = ws.take<uint32_t>(c.nslots);
       c.rticket = ws.take<uint32_t>(4);
     }
   }
@@ -487,13 +482,25 @@ template <typename T, int D, int KK, int INTEG>
 struct Engine final : EngineBase {
   using RL = RecL<T, D>;
   static constexpr int PR_BLOCK = 256;
-  static constexpr int SPLIT_BLOCK = 1024;
   static constexpr int MINB = (RL::RS <= 16) ? 3 : 2;  // CTAs per SM the bucket kernel is register-budgeted for
   size_t pr_smem = 0, sp_smem = 0, bk_smem = 0, rs_smem = 0;
   bool pair_mode = false;
   int num_sms = 148;
 
   State<T, D> st(rbm_ctx& c, int b) { return State<T, D>{c.recbuf[b], c.skey[b]}; }
+
+  template <bool LINK, class RT> rbm_status setup_rbmr(rbm_ctx& c) {
+    const uint32_t W = 1u << (c.L.idbits - c.L.B);
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(rbmr_emit_kernel<T, D, KK, INTEG, LINK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)emit_smem_bytes<T, D, LINK>())) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(split_kernel<RT, SPLIT_BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)split_smem_bytes_rt<RT>())) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(rbmr_bucket_apply_kernel<T, D, LINK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)rapply_smem_bytes<T, D, LINK>(c.L.cap2, W))) != cudaSuccess)
+      return fail(&c, RBM_ERR_CUDA, "smem attr rbmr: %s", cudaGetErrorString(e));
+    return RBM_OK;
+  }
 
   rbm_status setup(rbm_ctx& c) override {
     c.tile = split_tile<T, D>();
@@ -513,16 +520,8 @@ struct Engine final : EngineBase {
                                       (int)pr_smem), "smem attr prologue"))) return s;
     if ((s = chk(cudaFuncSetAttribute(split_kernel<StateRT<T, D>, SPLIT_BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)sp_smem), "smem attr split"))) return s;
-    if (c.cfg.scheme == RBM_SCHEME_RBMR && !is_partitioned(c.cfg)) {
-      const uint32_t W = 1u << (c.L.idbits - c.L.B);
-      if ((s = chk(cudaFuncSetAttribute(rbmr_emit_kernel<T, D, KK, INTEG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)emit_smem_bytes<T, D>()), "smem attr rbmr emit"))) return s;
-      if ((s = chk(cudaFuncSetAttribute(split_kernel<IncRT<T, D>, SPLIT_BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)split_smem_bytes_rt<IncRT<T, D>>()), "smem attr rbmr split"))) return s;
-      if ((s = chk(cudaFuncSetAttribute(rbmr_bucket_apply_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)rapply_smem_bytes<T, D>(c.L.cap2, W)), "smem attr rbmr apply"))) return s;
-      return RBM_OK;
-    }
+    if (c.cfg.scheme == RBM_SCHEME_RBMR && !is_partitioned(c.cfg)) return setup_rbmr<false, IncRT<T, D>>(c);
+    if (c.cfg.scheme == RBM_SCHEME_RBMR_SEQ) return setup_rbmr<true, LinkRT>(c);
     if (c.L.B > 0) {
       if ((s = chk(pair_mode ? cudaFuncSetAttribute(bucket_kernel<T, D, KK, INTEG, MODE_PAIR, MINB>,
                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bk_smem)
@@ -633,7 +632,7 @@ struct Engine final : EngineBase {
   // pass 2: pass-1 buckets/segments (capacity cap1, counts cnt1 strided) -> final buckets
   void split2(rbm_ctx& c, cudaStream_t s, State<T, D> in, State<T, D> out, const uint32_t* cnt1) {
     Nvtx r_("split");
-    split_kernel<StateRT<T, D>, SPLIT_BLOCK><<<(unsigned)num_sms, SPLIT_BLOCK, sp_smem, s>>>(
+    split_kernel<StateRT<T, D>, SPLIT_BLOCK><<<(unsigned)num_sms * SPLIT_MINB, SPLIT_BLOCK, sp_smem, s>>>(
         c.P, in.rec, out.rec, out.key, c.cur2, c.L.cap2, cnt1, c.tile_off, c.L.cap1);
   }
 
@@ -847,67 +846,65 @@ struct Engine final : EngineBase {
     return total;
   }
 
-  // Algorithm 2 as written (row f2): draws + per-particle slot chains, then
-  // the dependency-driven sweep (no host synchronisation: graph-capturable)
+  // Algorithm 2 as written (row f2): draws + slot chains through the
+  // partition by particle index (link records), then the dependency-driven
+  // sweep (no host synchronisation: graph-capturable)
   void step_rbmr_seq(rbm_ctx& c, cudaStream_t s) {
-    const DevParams& P = c.P;
-    const uint64_t n = c.cfg.n;
     T* xa = reinterpret_cast<T*>(c.rxa);
     if (!c.aos_valid) {
-      rbmr_pack_kernel<T, D><<<grid_for(n, 256), 256, 0, s>>>(n, st(c, c.cur), xa);
-      cudaMemsetAsync(c.rdone, 0, c.nbatch * 4, s);  // flags carry the step stamp m + 1
+      rbmr_pack_kernel<T, D><<<grid_for(c.cfg.n, 256), 256, 0, s>>>(c.cfg.n, st(c, c.cur), xa);
       c.aos_valid = true;
     }
-    cudaMemsetAsync(c.rmcnt, 0, n * 4, s);
-    cudaMemsetAsync(c.rnovf, 0, 4, s);
     cudaMemsetAsync(c.rticket, 0, 4, s);
-    const unsigned gb = grid_for(c.nbatch, 128, 148 * 64);
+    cudaMemsetAsync(c.rexpect, 0xff, c.nslots * 4, s);  // SEQ_FREE: a particle's first slot waits for nobody
+    partition_slots<true, LinkRT>(c, s, c.rexpect);
     c.mark(s);
-    rbmr_draw_reg_kernel<<<gb, 128, 0, s>>>(P, c.nbatch, c.js, c.rmcnt, c.rmbox, c.rovf, c.rnovf);
-    c.mark(s);
-    rbmr_prev_kernel<<<grid_for(n, 256), 256, 0, s>>>(P, n, c.rmcnt, c.rmbox, c.rovf, c.rnovf, c.rprevb);
-    c.mark(s);
-    rbmr_seq_dep_kernel<T, D, KK, INTEG><<<(unsigned)num_sms * 16, 128, 0, s>>>(P, c.nbatch, c.js, c.rprevb, xa,
-                                                                              c.rdone, c.rticket);
+    rbmr_seq_dep_kernel<T, D, KK, INTEG><<<(unsigned)num_sms * 16, 128, 0, s>>>(c.P, c.nbatch, c.js, c.rexpect, xa,
+                                                                              c.rticket);
     c.mark(s);
     advance_kernel<<<1, 1, 0, s>>>(c.step_dev);
     c.mark(s);
   }
 
-  // RBM-r Jacobi sweep (reading D:8): increments routed to their particles
-  // through the partition by particle index (rbmr_emit -> split -> apply)
-  void step_rbmr(rbm_ctx& c, cudaStream_t s) {
+  // slot records {j_s, s[, Delta_s]} -> partition by particle index -> per id
+  // bucket: increments added in ascending s (RBM-r), or expected tags (RBM-r', LINK)
+  template <bool LINK, class RT> void partition_slots(rbm_ctx& c, cudaStream_t s, uint32_t* expect) {
     const DevParams& P = c.P;
     const Layout& L = c.L;
-    const uint64_t n = c.cfg.n;
     T* xa = reinterpret_cast<T*>(c.rxa);
-    if (!c.aos_valid) {  // state set by init / set_state (records) -> AoS, once
-      rbmr_pack_kernel<T, D><<<grid_for(n, 256), 256, 0, s>>>(n, st(c, c.cur), xa);
-      c.aos_valid = true;
-    }
-    using IL = IncL<T, D>;
     const uint32_t W = 1u << (L.idbits - L.B);
     const uint32_t bpc = EMIT_TS / c.cfg.p;
     cudaMemsetAsync(c.cur1[0], 0, (size_t)(1u << L.b1) * CUR1_STRIDE * 4, s);
     c.mark(s);
-    rbmr_emit_kernel<T, D, KK, INTEG><<<(unsigned)((c.nbatch + bpc - 1) / bpc), EMIT_BLOCK, emit_smem_bytes<T, D>(), s>>>(
-        P, c.nbatch, xa, c.js, c.rinc[0], c.cur1[0], L.cap1);
+    rbmr_emit_kernel<T, D, KK, INTEG, LINK>
+        <<<(unsigned)((c.nbatch + bpc - 1) / bpc), EMIT_BLOCK, emit_smem_bytes<T, D, LINK>(), s>>>(
+            P, c.nbatch, xa, c.js, c.rinc[0], c.cur1[0], L.cap1);
     const unsigned char* fin = c.rinc[0];
     const uint32_t* fcnt = c.cur1[0];
     if (L.b2) {
       c.mark(s);
-      tile_scan_kernel<<<1, 1024, 0, s>>>(P, c.cur1[0], c.prefix1, c.tile_off, c.S,
-                                          (uint32_t)split_tile_rt<IncRT<T, D>>());
+      tile_scan_kernel<<<1, 1024, 0, s>>>(P, c.cur1[0], c.prefix1, c.tile_off, c.S, (uint32_t)split_tile_rt<RT>());
       cudaMemsetAsync(c.cur2, 0, (size_t)L.nbuckets * CUR2_STRIDE * 4, s);
       c.mark(s);
-      split_kernel<IncRT<T, D>, SPLIT_BLOCK><<<(unsigned)num_sms, SPLIT_BLOCK, split_smem_bytes_rt<IncRT<T, D>>(), s>>>(
+      split_kernel<RT, SPLIT_BLOCK><<<(unsigned)num_sms * SPLIT_MINB, SPLIT_BLOCK, split_smem_bytes_rt<RT>(), s>>>(
           P, c.rinc[0], c.rinc[1], nullptr, c.cur2, L.cap2, c.cur1[0], c.tile_off, L.cap1);
       fin = c.rinc[1];
       fcnt = c.cur2;
     }
     c.mark(s);
-    rbmr_bucket_apply_kernel<T, D><<<L.nbuckets, 256, rapply_smem_bytes<T, D>(L.cap2, W), s>>>(P, fin, L.cap2, fcnt, W, xa);
-    (void)sizeof(IL);
+    rbmr_bucket_apply_kernel<T, D, LINK><<<L.nbuckets, 256, rapply_smem_bytes<T, D, LINK>(L.cap2, W), s>>>(
+        P, fin, L.cap2, fcnt, W, xa, expect);
+  }
+
+  // RBM-r Jacobi sweep (reading D:8): increments routed to their particles
+  // through the partition by particle index (rbmr_emit -> split -> apply)
+  void step_rbmr(rbm_ctx& c, cudaStream_t s) {
+    T* xa = reinterpret_cast<T*>(c.rxa);
+    if (!c.aos_valid) {  // state set by init / set_state (records) -> AoS, once
+      rbmr_pack_kernel<T, D><<<grid_for(c.cfg.n, 256), 256, 0, s>>>(c.cfg.n, st(c, c.cur), xa);
+      c.aos_valid = true;
+    }
+    partition_slots<false, IncRT<T, D>>(c, s, nullptr);
     c.mark(s);
     advance_kernel<<<1, 1, 0, s>>>(c.step_dev);
     c.mark(s);
@@ -950,8 +947,13 @@ EngineBase* make_for_kernel(uint32_t kernel, uint32_t integ) {
 inline const char* const* kernel_names(const rbm_ctx& c, uint32_t* count) {
   static const char* const r[] = {"rbmr_emit", "rbmr_apply", "advance"};
   static const char* const r2[] = {"rbmr_emit", "tile_scan", "split", "rbmr_apply", "advance"};
-  static const char* const rs[] = {"rbmr_draw", "rbmr_prev", "rbmr_seq_sweep", "advance"};
-  if (c.cfg.scheme == RBM_SCHEME_RBMR_SEQ) { *count = 4; return rs; }
+  static const char* const rs[] = {"rbmr_draw", "rbmr_link", "rbmr_seq_sweep", "advance"};
+  static const char* const rs2[] = {"rbmr_draw", "tile_scan", "split", "rbmr_link", "rbmr_seq_sweep", "advance"};
+  if (c.cfg.scheme == RBM_SCHEME_RBMR_SEQ) {
+    if (c.L.b2) { *count = 6; return rs2; }
+    *count = 4;
+    return rs;
+  }
   static const char* const b0[] = {"resident_step"};
   static const char* const p1[] = {"tile_scan", "bucket_step", "straddle", "advance"};
   static const char* const p2[] = {"tile_scan", "split", "final_scan", "bucket_step", "straddle", "advance"};

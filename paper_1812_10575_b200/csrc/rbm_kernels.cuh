@@ -546,8 +546,27 @@ template <typename T, int D> struct IncRT {
   }
 };
 
+#ifndef RBM_SPLIT_STAGE  // design-experiment builds override these (build.py -D...)
+#define RBM_SPLIT_STAGE 65536
+#define RBM_SPLIT_BLOCK 1024
+#define RBM_SPLIT_MINB 1
+#endif
+constexpr int SPLIT_BLOCK = RBM_SPLIT_BLOCK, SPLIT_MINB = RBM_SPLIT_MINB;  // CTAs of SPLIT_BLOCK threads per SM
+// RBM-r' link record {j, s} (8 bytes)
+struct LinkL {
+  static constexpr int RS = 8, NW = 2;
+};
+struct LinkRT {
+  static constexpr int RS = LinkL::RS, NW = LinkL::NW;
+  static constexpr bool SIDE = false;
+  __device__ __forceinline__ static uint32_t key(const DevParams& P, const unsigned char* r, uint32_t) {
+    return reinterpret_cast<const uint32_t*>(r)[0] << P.jshift;
+  }
+};
+template <typename T, int D, bool LINK> using IncOrLink = std::conditional_t<LINK, LinkL, IncL<T, D>>;
+
 template <class RT> __host__ __device__ constexpr int split_tile_rt() {
-  return (65536 / RT::RS) < 4096 ? (65536 / RT::RS) : 4096;  // <= 64 KB per stage
+  return (RBM_SPLIT_STAGE / RT::RS) < 4096 ? (RBM_SPLIT_STAGE / RT::RS) : 4096;  // <= one stage of records
 }
 template <class RT> __host__ __device__ constexpr size_t split_smem_bytes_rt() {
   return (3 * 1024 + 64) * 4 + 64 + 2 * (size_t)split_tile_rt<RT>() * RT::RS +
@@ -561,7 +580,7 @@ template <typename T, int D> __host__ __device__ constexpr size_t split_smem_byt
 struct TileInfo { uint32_t u, lo, hi, pad; };
 
 template <class RT, int BLOCK>
-static __global__ void __launch_bounds__(BLOCK, 1) split_kernel(const __grid_constant__ DevParams P,
+static __global__ void __launch_bounds__(BLOCK, SPLIT_MINB) split_kernel(const __grid_constant__ DevParams P,
                                                                 const unsigned char* __restrict__ src_rec,
                                                                 unsigned char* __restrict__ dst_rec,
                                                                 uint32_t* __restrict__ dst_key,
@@ -1746,10 +1765,11 @@ static __global__ void __launch_bounds__(TB) direct_kernel(const __grid_constant
 // x_j <- x_j + sum over the slots s with j_s = j of Delta_s, in ascending s.
 // State in id order as AoS (4 scalars per particle, one sector per gather).
 // One GPU: the increments go through a partition by particle index (the
-// rbmr_emit / split / rbmr_bucket_apply kernels below).  The sequential
-// RBM-r' and the partitioned system register slots in per-particle mailboxes
-// (MBOX entries, overflow list for the ~1e-6 of particles drawn more often),
-// sorted by s when applied.
+// rbmr_emit / split / rbmr_bucket_apply kernels below); the sequential RBM-r'
+// finds each slot's predecessor through the same partition (link records).
+// The partitioned system registers slots in per-particle mailboxes (MBOX
+// entries, overflow list for the ~1e-6 of particles drawn more often), sorted
+// by s when applied.
 constexpr uint32_t MBOX = 8;
 constexpr uint32_t OVF_CAP = 1u << 20;
 
@@ -1771,86 +1791,21 @@ __device__ __forceinline__ void load4(const T* __restrict__ xa, uint32_t j, T (&
 
 // ----------------------- exact sequential RBM-r' (Alg. 2, row f2)
 // Batches of one sweep are applied in draw order from the current positions.
-// Batch b depends only on the earlier batches that last touched one of its
-// members (prevb).  One dependency-driven kernel applies them: warps take
-// consecutive groups of 32 batches in ticket order, and a batch starts once
-// the flags of its prevb batches carry this step's stamp; it then reads the
-// current positions and publishes its own flag.  Every batch waits only on
-// lower-numbered batches, which were taken earlier by running warps, so the
-// sweep always drains; each batch sees exactly the positions the sequential
-// loop would give it.  No levels, no host synchronisation.
-constexpr uint32_t NO_BATCH = 0xffffffffu;
+// Batch b depends only on the earlier batches that touched its members.  Each
+// particle's AoS record carries, in its padding word, a write counter (tag).
+// The link pass routes records {j_s, s} through the partition by particle
+// index (rbmr_emit_kernel<LINK> -> split -> rbmr_bucket_apply_kernel<LINK>):
+// per particle j with slots s_0 < s_1 < ... in this sweep, expect[s_a] =
+// tag_j + a (a > 0; the first slot waits for nobody).  The dependency-driven
+// kernel then applies the batches: warps take consecutive groups of 32
+// batches in ticket order; a batch waits until the tag of each member reaches
+// its expect value (all earlier writers of that particle are done), reads the
+// positions, writes the new ones and bumps the tags: fp32 records are 16
+// bytes, read and written as single 128-bit accesses carrying position and
+// tag together; wider records store the tag after a release fence.  Every batch waits only on lower-numbered batches,
+// which were taken earlier by running warps, so the sweep always drains; each
+// batch sees exactly the positions the sequential loop would give it.
 
-// draws j_s of batch b (as the oracle, reading D:9) and mailbox registration only
-static __global__ void __launch_bounds__(128) rbmr_draw_reg_kernel(const __grid_constant__ DevParams P, uint64_t nbatch,
-                                                                   uint32_t* __restrict__ js, uint32_t* __restrict__ mcnt,
-                                                                   uint32_t* __restrict__ mbox, uint32_t* __restrict__ ovf,
-                                                                   uint32_t* __restrict__ novf) {
-  const uint32_t m = (uint32_t)*P.step;
-  const uint32_t p = P.p;
-  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nbatch;
-       b += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t s0 = b * p;
-    uint32_t e0 = 0, e1 = 0;
-    if (P.adj_edges) adj_edge_draw(P, s0, m, e0, e1);  // clustering model, p = 2
-    for (uint32_t l = 0; l < p; ++l) {
-      const uint64_t s = s0 + l;
-      uint32_t t = 0, j;
-      for (;;) {
-        if (P.adj_edges) { j = l ? e1 : e0; break; }
-        const uint4 w = block_at(P, (uint32_t)s, t, m, TAG_SLOT);
-        j = (uint32_t)__umul64hi(P.n, (((uint64_t)w.x) << 32) | w.y);
-        bool dup = false;
-        for (uint32_t l2 = 0; l2 < l; ++l2) dup |= (js[s0 + l2] == j);
-        if (!dup) break;
-        ++t;
-      }
-      js[s] = j;
-      const uint32_t pos = atomicAdd(&mcnt[j], 1u);
-      if (pos < MBOX) {
-        mbox[(size_t)j * MBOX + pos] = (uint32_t)s;
-      } else {
-        const uint32_t q = atomicAdd(novf, 1u);
-        if (q < OVF_CAP) { ovf[2 * q] = j; ovf[2 * q + 1] = (uint32_t)s; }
-        else atomicExch(P.capacity_err, 1u);
-      }
-    }
-  }
-}
-
-// per particle: its slots in ascending order; prevb[s] = batch of the slot of
-// the same particle drawn just before s (NO_BATCH for the first)
-static __global__ void rbmr_prev_kernel(const __grid_constant__ DevParams P, uint64_t n,
-                                        const uint32_t* __restrict__ mcnt, const uint32_t* __restrict__ mbox,
-                                        const uint32_t* __restrict__ ovf, const uint32_t* __restrict__ novf,
-                                        uint32_t* __restrict__ prevb) {
-  constexpr uint32_t MAXL = 32;
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
-       j += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t c = mcnt[j];
-    if (c == 0) continue;
-    uint32_t sl[MAXL];
-    uint32_t k = 0;
-    const uint32_t cm = c < MBOX ? c : MBOX;
-    for (uint32_t q = 0; q < cm; ++q) sl[k++] = mbox[j * MBOX + q];
-    if (c > MBOX) {
-      const uint32_t no = min(*novf, OVF_CAP);
-      for (uint32_t q = 0; q < no; ++q)
-        if (ovf[2 * q] == (uint32_t)j) {
-          if (k < MAXL) sl[k++] = ovf[2 * q + 1];
-          else atomicExch(P.capacity_err, 1u);
-        }
-    }
-    for (uint32_t a = 1; a < k; ++a) {
-      const uint32_t v = sl[a];
-      uint32_t w = a;
-      while (w > 0 && sl[w - 1] > v) { sl[w] = sl[w - 1]; --w; }
-      sl[w] = v;
-    }
-    prevb[sl[0]] = NO_BATCH;
-    for (uint32_t a = 1; a < k; ++a) prevb[sl[a]] = sl[a - 1] / P.p;
-  }
-}
 
 // one batch of the sequential sweep from the current positions (members
 // distinct): Eq. (2.2) + EM, or the exact pair flow; positions read through L2
@@ -1914,14 +1869,94 @@ __device__ __forceinline__ void seq_batch(const DevParams& P, uint32_t m, uint64
   }
 }
 
-// the sweep, dependency-driven: done[b] = m + 1 once batch b of step m is applied
+// p = 2: the new positions of both members, computed exactly as seq_batch
+// does (same operations, same order)
+template <typename T, int D, int KK, int INTEG>
+__device__ __forceinline__ void seq_pair(const DevParams& P, uint32_t m, uint64_t s0, uint32_t i, uint32_t j,
+                                         const T (&xi)[D], const T (&xj)[D], T (&xni)[D], T (&xnj)[D]) {
+  T z[D];
+  if (INTEG == 0) {
+    T f[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) { f[c] = T(0); z[c] = T(0); }
+    add_interaction<T, D, KK>(xi, xj, f, P);
+#pragma unroll
+    for (int c = 0; c < D; ++c) f[c] *= T(1);
+    if (P.has_noise) Normals<T, D>::get(P, (uint32_t)s0, m, TAG_NOISE_SLOT, z);
+    em_update<T, D>(xi, f, z, xni, P, true);
+#pragma unroll
+    for (int c = 0; c < D; ++c) { f[c] = T(0); z[c] = T(0); }
+    add_interaction<T, D, KK>(xj, xi, f, P);
+#pragma unroll
+    for (int c = 0; c < D; ++c) f[c] *= T(1);
+    if (P.has_noise) Normals<T, D>::get(P, (uint32_t)(s0 + 1), m, TAG_NOISE_SLOT, z);
+    em_update<T, D>(xj, f, z, xnj, P, true);
+  } else {
+    T y[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) z[c] = T(0);
+    if (KK == KK_ADJ) adj_flow<T, D>(P, i, j, xi, xj, true, y);
+    else pair_flow<T, D, KK>(xi, xj, true, y, P);
+    if (P.has_noise) Normals<T, D>::get(P, (uint32_t)s0, m, TAG_NOISE_SLOT, z);
+    split_finish<T, D>(y, z, xni, P, true);
+#pragma unroll
+    for (int c = 0; c < D; ++c) z[c] = T(0);
+    if (KK == KK_ADJ) adj_flow<T, D>(P, i, j, xi, xj, false, y);
+    else pair_flow<T, D, KK>(xi, xj, false, y, P);
+    if (P.has_noise) Normals<T, D>::get(P, (uint32_t)(s0 + 1), m, TAG_NOISE_SLOT, z);
+    split_finish<T, D>(y, z, xnj, P, true);
+  }
+  check_finite<T, D>(xni, P, i, m);
+  check_finite<T, D>(xnj, P, j, m);
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* a) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* a) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu(uint32_t* a, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// one 16-byte record, read and written whole at L2 (the position and its tag
+// together, as one aligned 128-bit access)
+__device__ __forceinline__ uint4 ld_cg_v4(const void* a) {
+  uint4 v;
+  asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_cg_v4(void* a, uint4 v) {
+  asm volatile("st.global.cg.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+// expect value of a particle's first slot in the sweep: no earlier writer
+constexpr uint32_t SEQ_FREE = 0xffffffffu;
+// the write counter of particle j: the padding word of its AoS record (D <= 3)
+template <typename T> __device__ __forceinline__ uint32_t* seq_tag(T* xa, uint32_t j) {
+  return reinterpret_cast<uint32_t*>(xa + (size_t)j * 4 + 3);
+}
+// wait until the earlier writers of the particle are done (tag >= e, mod 2^32)
+template <typename T> __device__ __forceinline__ void wait_tag(T* xa, uint32_t j, uint32_t e) {
+  if (e == SEQ_FREE) return;
+  while ((int32_t)(ld_acquire_gpu(seq_tag(xa, j)) - e) < 0) __nanosleep(32);
+}
+template <typename T> __device__ __forceinline__ uint32_t next_tag(T* xa, uint32_t j, uint32_t e) {
+  return (e == SEQ_FREE ? ld_relaxed_gpu(seq_tag(xa, j)) : e) + 1u;
+}
+
 template <typename T, int D, int KK, int INTEG>
 static __global__ void __launch_bounds__(128) rbmr_seq_dep_kernel(const __grid_constant__ DevParams P, uint64_t nbatch,
                                                                   const uint32_t* __restrict__ js,
-                                                                  const uint32_t* __restrict__ prevb, T* xa,
-                                                                  uint32_t* done, uint32_t* ticket) {
+                                                                  const uint32_t* __restrict__ expect, T* xa,
+                                                                  uint32_t* ticket) {
   const uint32_t m = (uint32_t)*P.step;
-  const uint32_t stamp = m + 1u;
   const uint32_t p = P.p;
   const uint32_t lane = threadIdx.x & 31u;
   for (;;) {
@@ -1931,16 +1966,50 @@ static __global__ void __launch_bounds__(128) rbmr_seq_dep_kernel(const __grid_c
     if ((uint64_t)base >= nbatch) break;
     const uint64_t b = (uint64_t)base + lane;
     if (b < nbatch) {
-      for (uint32_t l = 0; l < p; ++l) {
-        const uint32_t pb = prevb[b * p + l];
-        if (pb == NO_BATCH) continue;
-        RBM_CHECK(P, pb < b);
-        while (atomicAdd(&done[pb], 0u) != stamp) __nanosleep(32);
+      if (p == 2) {
+        const uint2 jj = reinterpret_cast<const uint2*>(js)[b];
+        const uint2 ex = reinterpret_cast<const uint2*>(expect)[b];
+        T xi[D], xj[D], xni[D], xnj[D];
+        if constexpr (sizeof(T) == 4) {
+          // 16-byte records {x, tag}: the tag is polled in the same 128-bit
+          // load that returns the position, and the new position goes out
+          // with the bumped tag in one 128-bit store (no fence)
+          uint4 ri = ld_cg_v4(xa + (size_t)jj.x * 4), rj = ld_cg_v4(xa + (size_t)jj.y * 4);
+          while (ex.x != SEQ_FREE && (int32_t)(ri.w - ex.x) < 0) { __nanosleep(32); ri = ld_cg_v4(xa + (size_t)jj.x * 4); }
+          while (ex.y != SEQ_FREE && (int32_t)(rj.w - ex.y) < 0) { __nanosleep(32); rj = ld_cg_v4(xa + (size_t)jj.y * 4); }
+          const uint32_t wi[3] = {ri.x, ri.y, ri.z}, wj[3] = {rj.x, rj.y, rj.z};
+#pragma unroll
+          for (int c = 0; c < D; ++c) { xi[c] = __uint_as_float(wi[c]); xj[c] = __uint_as_float(wj[c]); }
+          seq_pair<T, D, KK, INTEG>(P, m, b * 2, jj.x, jj.y, xi, xj, xni, xnj);
+          uint32_t oi[3] = {0u, 0u, 0u}, oj[3] = {0u, 0u, 0u};
+#pragma unroll
+          for (int c = 0; c < D; ++c) { oi[c] = __float_as_uint((float)xni[c]); oj[c] = __float_as_uint((float)xnj[c]); }
+          st_cg_v4(xa + (size_t)jj.x * 4, make_uint4(oi[0], oi[1], oi[2], ri.w + 1u));
+          st_cg_v4(xa + (size_t)jj.y * 4, make_uint4(oj[0], oj[1], oj[2], rj.w + 1u));
+        } else {
+          wait_tag(xa, jj.x, ex.x);
+          wait_tag(xa, jj.y, ex.y);
+#pragma unroll
+          for (int c = 0; c < D; ++c) { xi[c] = __ldcg(xa + (size_t)jj.x * 4 + c); xj[c] = __ldcg(xa + (size_t)jj.y * 4 + c); }
+          seq_pair<T, D, KK, INTEG>(P, m, b * 2, jj.x, jj.y, xi, xj, xni, xnj);
+          const uint32_t ti = next_tag(xa, jj.x, ex.x), tj = next_tag(xa, jj.y, ex.y);
+#pragma unroll
+          for (int c = 0; c < D; ++c) { xa[(size_t)jj.x * 4 + c] = xni[c]; xa[(size_t)jj.y * 4 + c] = xnj[c]; }
+          fence_acq_rel_gpu();  // positions before the tags (release pattern)
+          st_relaxed_gpu(seq_tag(xa, jj.x), ti);
+          st_relaxed_gpu(seq_tag(xa, jj.y), tj);
+        }
+      } else {
+        const uint64_t s0 = b * p;
+        for (uint32_t l = 0; l < p; ++l) wait_tag(xa, js[s0 + l], expect[s0 + l]);
+        seq_batch<T, D, KK, INTEG>(P, m, b, js, xa);
+        fence_acq_rel_gpu();
+        for (uint32_t l = 0; l < p; ++l) {
+          const uint32_t j = js[s0 + l], e = expect[s0 + l];
+          // a first slot's tag is stable until this batch bumps it
+          st_relaxed_gpu(seq_tag(xa, j), e == SEQ_FREE ? ld_relaxed_gpu(seq_tag(xa, j)) + 1u : e + 1u);
+        }
       }
-      __threadfence();
-      seq_batch<T, D, KK, INTEG>(P, m, b, js, xa);
-      __threadfence();
-      atomicExch(&done[b], stamp);
     }
     __syncwarp();
   }
@@ -2218,16 +2287,17 @@ static __global__ void gather_aos_part_kernel(const T* __restrict__ xa, uint64_t
 constexpr int EMIT_BLOCK = 256;
 constexpr uint32_t EMIT_TS = 2048;  // slots per emit CTA
 
-template <typename T, int D> __host__ __device__ constexpr size_t emit_smem_bytes() {
-  return (size_t)EMIT_TS * IncL<T, D>::RS + (size_t)EMIT_TS * (4 + 2) + (3 * 1024 + 64) * 4;
+template <typename T, int D, bool LINK> __host__ __device__ constexpr size_t emit_smem_bytes() {
+  return (size_t)EMIT_TS * IncOrLink<T, D, LINK>::RS + (size_t)EMIT_TS * (4 + 2) + (3 * 1024 + 64) * 4;
 }
 
-template <typename T, int D, int KK, int INTEG>
+// LINK (the sequential RBM-r'): the records are {j_s, s} only (no gathers)
+template <typename T, int D, int KK, int INTEG, bool LINK>
 static __global__ void __launch_bounds__(EMIT_BLOCK) rbmr_emit_kernel(const __grid_constant__ DevParams P, uint64_t nbatch,
                                                                       const T* __restrict__ xa, uint32_t* __restrict__ js,
                                                                       unsigned char* __restrict__ dst, uint32_t* cur,
                                                                       uint32_t dcap) {
-  using IL = IncL<T, D>;
+  using IL = IncOrLink<T, D, LINK>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned char* stg = smem_raw;                                            // EMIT_TS records
   uint32_t* rk = reinterpret_cast<uint32_t*>(stg + (size_t)EMIT_TS * IL::RS);  // digit << 16 | rank
@@ -2258,12 +2328,15 @@ static __global__ void __launch_bounds__(EMIT_BLOCK) rbmr_emit_kernel(const __gr
           jj[l] = rbmr_draw(P, m, s0 + l, jj, l);
         }
       }
-      T x[PM][D], dl[PM][D];
-      for (uint32_t l = 0; l < (uint32_t)PM; ++l) {
-        if (l >= p) break;
-        load4<T, D>(xa, jj[l], x[l]);
+      T dl[LINK ? 1 : PM][D];
+      if constexpr (!LINK) {
+        T x[PM][D];
+        for (uint32_t l = 0; l < (uint32_t)PM; ++l) {
+          if (l >= p) break;
+          load4<T, D>(xa, jj[l], x[l]);
+        }
+        rbmr_deltas<T, D, KK, INTEG, PM>(P, m, s0, p, jj, x, dl);
       }
-      rbmr_deltas<T, D, KK, INTEG, PM>(P, m, s0, p, jj, x, dl);
       for (uint32_t l = 0; l < (uint32_t)PM; ++l) {
         if (l >= p) break;
         const uint32_t e = lb * p + l;
@@ -2273,8 +2346,10 @@ static __global__ void __launch_bounds__(EMIT_BLOCK) rbmr_emit_kernel(const __gr
         for (int k = 0; k < IL::NW; ++k) w[k] = 0u;
         w[0] = jj[l];
         w[1] = (uint32_t)(s0 + l);
+        if constexpr (!LINK) {
 #pragma unroll
-        for (int c = 0; c < D; ++c) to_w(dl[l][c], w + 2 + c * (int)(sizeof(T) / 4));
+          for (int c = 0; c < D; ++c) to_w(dl[l][c], w + 2 + c * (int)(sizeof(T) / 4));
+        }
         st_words<IL::NW>(stg + (size_t)e * IL::RS, w);
         const uint32_t dg = (jj[l] << P.jshift) >> sh;
         rk[e] = (dg << 16) | atomicAdd(&hist[dg], 1u);
@@ -2308,17 +2383,20 @@ static __global__ void __launch_bounds__(EMIT_BLOCK) rbmr_emit_kernel(const __gr
   }
 }
 
-template <typename T, int D> __host__ __device__ constexpr size_t rapply_smem_bytes(uint32_t cap, uint32_t W) {
-  return (size_t)(cap + 8) * IncL<T, D>::RS + (size_t)cap * 4 + (size_t)W * 8 + 64 * 4 + 16;
+template <typename T, int D, bool LINK> __host__ __device__ constexpr size_t rapply_smem_bytes(uint32_t cap, uint32_t W) {
+  return (size_t)(cap + 8) * IncOrLink<T, D, LINK>::RS + (size_t)cap * 4 + (size_t)W * 8 + 64 * 4 + 16;
 }
 
-// apply: final bucket b = the particle ids [b W, (b+1) W); n = cnt[b] records
-template <typename T, int D>
+// apply: final bucket b = the particle ids [b W, (b+1) W); n = cnt[b] records.
+// LINK (the sequential RBM-r'): instead of adding increments, the a-th slot
+// s_a of particle j (ascending) gets expect[s_a] = tag_j + a for a > 0 (the
+// caller presets expect[] to SEQ_FREE, the first slot's value)
+template <typename T, int D, bool LINK>
 static __global__ void __launch_bounds__(256) rbmr_bucket_apply_kernel(const __grid_constant__ DevParams P,
                                                                        const unsigned char* __restrict__ fin, uint32_t cap,
                                                                        const uint32_t* __restrict__ cnt, uint32_t W,
-                                                                       T* __restrict__ xa) {
-  using IL = IncL<T, D>;
+                                                                       T* __restrict__ xa, uint32_t* __restrict__ expect) {
+  using IL = IncOrLink<T, D, LINK>;
   constexpr int BLOCK = 256;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t b = blockIdx.x;
@@ -2377,7 +2455,10 @@ static __global__ void __launch_bounds__(256) rbmr_bucket_apply_kernel(const __g
     constexpr uint32_t MAXL = 32;
     uint32_t ee[MAXL], ss[MAXL];
     const uint32_t kk = c < MAXL ? c : MAXL;
-    if (c > MAXL) atomicExch(P.capacity_err, 1u);
+    if (c > MAXL) {
+      atomicExch(P.capacity_err, 1u);
+      if constexpr (LINK) continue;  // flagged; no slot of the particle waits (the sweep cannot hang)
+    }
     for (uint32_t a = 0; a < kk; ++a) {
       ee[a] = ix[po[jl] + a];
       ss[a] = reinterpret_cast<const uint32_t*>(rs + (size_t)ee[a] * IL::RS)[1];
@@ -2388,6 +2469,13 @@ static __global__ void __launch_bounds__(256) rbmr_bucket_apply_kernel(const __g
       while (w > 0 && ss[w - 1] > v) { ss[w] = ss[w - 1]; ee[w] = ee[w - 1]; --w; }
       ss[w] = v;
       ee[w] = w0;
+    }
+    if constexpr (LINK) {
+      if (kk > 1) {  // expect[] was preset to SEQ_FREE: only the later slots are written
+        const uint32_t t0 = *seq_tag(xa, (uint32_t)(j0 + jl));
+        for (uint32_t a = 1; a < kk; ++a) expect[ss[a]] = t0 + a;
+      }
+      continue;
     }
     const uint64_t j = j0 + jl;
     T x[D];

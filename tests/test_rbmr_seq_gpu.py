@@ -1,6 +1,7 @@
 """Exact sequential RBM-r' (Algorithm 2)
-on the GPU, -m gpu: the level-by-level sweep equals the oracle's sequential
-loop over the batches (same slot draws, bit-exact; states within the
+on the GPU, -m gpu: the dependency-driven sweep (each batch waits for the
+earlier batches that share a member) equals the oracle's sequential loop over
+the batches (same slot draws, bit-exact; states within the
 BASELINE.json tolerances)."""
 import numpy as np
 import pytest
@@ -80,3 +81,25 @@ def test_seq_many_steps_and_fp32(R, O):
     s.step()
     assert E(s.gather(host=True), O.rbmr_seq_step(c32, x0, 0)) <= 1e-4
     s.close()
+
+
+def test_seq_step_run_and_set_state(R, O):
+    """rbm_step x k == rbm_run(k) (graph path) bit-exactly, and a set_state
+    between runs (the AoS state and its write counters are rebuilt) continues
+    the oracle's trajectory; p = 2 (pair path) and p = 3 (general path)."""
+    for p in (2, 3):
+        c = model("coulomb_reg", 3, 40_009, p, seed=5)
+        a = R.RBM(c)
+        b = R.RBM(c)
+        x0 = a.gather(host=True)
+        for _ in range(6):
+            a.step()
+        b.run(6)
+        ga, gb = a.gather(host=True), b.gather(host=True)
+        assert np.array_equal(ga, gb)
+        assert E(ga, O.run(c, x0, 0, 6)) <= 1e-10
+        b.set_state(gb)
+        b.run(4)
+        assert E(b.gather(host=True), O.run(c, x0, 0, 10)) <= 1e-9
+        a.close()
+        b.close()
