@@ -110,7 +110,11 @@ def alg_bytes(name: str, cfg: dict) -> float:
     shuffle keys and the permutation moves are the overhead of realising a
     random division on a bandwidth machine (8(d) "Algorithmic bytes")."""
     per = 2.0 * cfg["d"] * elt(cfg) * cfg["n"]
-    return {"bucket_step": per, "rbmr_apply": per}.get(name, 0.0)
+    # RBM-r: the emit kernel reads x_{j_s} once per slot (d s per particle-step,
+    # random sectors), the apply kernel reads and writes each position;
+    # RBM-r': the sweep reads and writes the members' positions (random)
+    return {"bucket_step": per, "rbmr_apply": per, "rbmr_emit": per / 2,
+            "rbmr_seq_sweep": per}.get(name, 0.0)
 
 
 def design_bytes(name: str, cfg: dict, layout) -> float:
@@ -441,10 +445,13 @@ def main():
                 "algorithmic": "2 d s bytes per particle-step (SURVEY 8(d)) x N particles per launch",
                 "design_bytes_per_launch": dbytes,
                 "design_frac": (dbytes / (avg_ms / 1e3) / 1e9) / peak if dbytes else None}
-    else:  # resident multi-step kernel (N <= 2048) / RBM-r' levels: latency-bound, no byte roofline
+        if name in ("rbmr_emit", "rbmr_seq_sweep"):
+            roof["access"] = "random 32-byte sectors (x_{j_s} of randomly drawn particles): far below the streaming peak by nature"
+
+    else:  # resident multi-step kernel (N <= 2048): latency-bound, no byte roofline
         roof = {"bound": "latency", "kernel": name, "achieved": None, "peak": None, "unit": "GB/s",
                 "frac": None, "traffic": traffic, "avg_launch_ms": avg_ms,
-                "note": "one CTA (resident) or one launch per level: bounded by barrier and launch latency, not by HBM or ALU throughput"}
+                "note": "one CTA keeps the system in shared memory for many steps: bounded by barrier latency, not by HBM or ALU throughput"}
     step_ms = ms / K
     shares = {k: round(v / max(nrec, 1), 4) for k, v in per_kernel.items()}
     R = rec_bytes(cfg)

@@ -103,3 +103,22 @@ def test_seq_step_run_and_set_state(R, O):
         assert E(b.gather(host=True), O.run(c, x0, 0, 10)) <= 1e-9
         a.close()
         b.close()
+
+
+def test_seq_fp32_pair_path_large(R, O):
+    """fp32, p = 2: the sweep's 128-bit record path (position and write
+    counter in one access) at N = 2^21 under full occupancy: two runs are
+    bit-identical (no ordering race changes a result) and match the oracle's
+    sequential loop within the fp32 bound."""
+    c = model("coulomb_reg", 3, 1 << 21, 2, dtype="f32", seed=9)
+    a = R.RBM(c)
+    x0 = a.gather(host=True).astype(np.float64)
+    a.run(5)
+    g1 = a.gather(host=True)
+    a.close()
+    b = R.RBM(c)
+    b.run(5)
+    g2 = b.gather(host=True)
+    b.close()
+    assert np.array_equal(g1, g2)
+    assert E(g1, O.run(c, x0, 0, 5)) <= 1e-4
