@@ -507,6 +507,10 @@ struct Engine final : EngineBase {
     pr_smem = prologue_smem_bytes<T, D, PR_BLOCK>();
     sp_smem = split_smem_bytes<T, D>();
     bk_smem = bucket_smem_bytes<T, D>(c.L.cap, c.L.SB, c.L.b1);
+    if (const char* e = std::getenv("RBM_BUCKET_SMEM_MIN")) {  // experiment knob: fewer CTAs per SM
+      const size_t v = (size_t)std::atoll(e);
+      if (v > bk_smem && v <= 227 * 1024) bk_smem = v;
+    }
     rs_smem = resident_smem_bytes<T, D>(c.L.cap);
     pair_mode = c.cfg.p == 2;
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, c.device);
