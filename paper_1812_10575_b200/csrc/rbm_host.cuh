@@ -131,9 +131,16 @@ struct rbm_ctx {
   std::vector<cudaEvent_t> ev;
   size_t ev_used = 0;
   std::string err;
+  int debug_sync = -1;  // RBM_DEBUG_SYNC: synchronise and check after every sub-step (debugging)
   void mark(cudaStream_t s) {
     if (timing && ev_used < ev.size()) cudaEventRecord(ev[ev_used++], s);
+    if (debug_sync < 0) debug_sync = std::getenv("RBM_DEBUG_SYNC") ? 1 : 0;
+    if (debug_sync) {
+      const cudaError_t e = cudaStreamSynchronize(s);
+      std::fprintf(stderr, "[rbm debug] mark %u: %s\n", ev_dbg++, cudaGetErrorString(e));
+    }
   }
+  unsigned ev_dbg = 0;
 };
 
 namespace rbmhost {
@@ -191,7 +198,10 @@ inline Layout choose_layout(const rbm_config& c) {
   if ((c.scheme == RBM_SCHEME_RBMR || c.scheme == RBM_SCHEME_RBMR_SEQ) && !part) {
     // RBM-r increments (RBM-r' link records) partitioned by particle index: final buckets of
     // W = 2^(idbits-B) ids (~1024), one or two passes as for RBM-1
-    uint32_t B = ceil_log2((double)n / 1024.0);
+    double w = 1024.0;  // ids per final bucket (experiment knob RBM_RBMR_W)
+    if (const char* e = std::getenv("RBM_RBMR_W")) w = std::atof(e);
+    if (!(w >= 128.0 && w <= 1024.0)) w = 1024.0;
+    uint32_t B = ceil_log2((double)n / w);
     if (B > L.idbits) B = L.idbits;
     if (B > 20) B = 20;
     L.B = B;

@@ -570,7 +570,8 @@ template <class RT> __host__ __device__ constexpr int split_tile_rt() {
   return (RBM_SPLIT_STAGE / RT::RS) < 4096 ? (RBM_SPLIT_STAGE / RT::RS) : 4096;  // <= one stage of records
 }
 template <class RT> __host__ __device__ constexpr size_t split_smem_bytes_rt() {
-  return (3 * 1024 + 64) * 4 + 64 + 2 * (size_t)split_tile_rt<RT>() * RT::RS +
+  // header (counters, scratch, barriers) padded to 128 B as the kernel lays it out
+  return (((3 * 1024 + 64) * 4 + 64 + 127) & ~(size_t)127) + 2 * (size_t)split_tile_rt<RT>() * RT::RS +
          (size_t)split_tile_rt<RT>() * (4 + 4 + 2 + 2) + (size_t)(MAX_SEG_SPLIT + 1) * 4;
 }
 template <typename T, int D> __host__ __device__ constexpr int split_tile() { return split_tile_rt<StateRT<T, D>>(); }

@@ -122,3 +122,28 @@ def test_seq_fp32_pair_path_large(R, O):
     b.close()
     assert np.array_equal(g1, g2)
     assert E(g1, O.run(c, x0, 0, 5)) <= 1e-4
+
+
+@pytest.mark.parametrize("scheme", ["rbmr", "rbmr_seq"])
+def test_rbmr_widest_partition_layout(R, scheme, monkeypatch):
+    """The slot partition at its widest layout (B = 20: 2^10 pass-1 buckets,
+    2^10 final buckets each; reached by N >= 2^29 at the default 1024 ids per
+    bucket, here by N = 2^27 at 128 ids per bucket) gives results
+    bit-identical to the default layout (B = 17): the per-particle order of the
+    slots, and so every sum, does not depend on the layout.  (Regression: the
+    pass-2 splitter's shared-memory size missed its 128-byte header padding,
+    which only the 2^10-segment tile table reached.)"""
+    import rbm_inputs as RI
+    c = dict(RI.c5_coulomb_reg(n=1 << 27, scheme=scheme), seed=4)
+    out = []
+    for w in (None, "128"):
+        if w:
+            monkeypatch.setenv("RBM_RBMR_W", w)
+        s = R.RBM(c)
+        if w:
+            assert s.layout[0] == 20
+        s.run(2)
+        out.append(s.gather())  # device tensor
+        s.sync()
+        s.close()
+    assert torch.equal(out[0], out[1])
