@@ -226,7 +226,7 @@ inline Layout choose_layout(const rbm_config& c) {
     L.B = ceil_log2((double)n / target);
     if (L.B < 2) L.B = 2;
     if (part && L.B < L.g + 2) L.B = L.g + 2;  // >= 4 final buckets per rank, two passes
-    if (L.B > (part ? 20u : 18u)) L.B = part ? 20u : 18u;
+    if (L.B > 20u) L.B = 20u;  // 2^10 x 2^10 digits; mean bucket 2048 up to N = 2^31
   }
   if (L.B <= 10 && !part) { L.b1 = L.B; L.b2 = 0; }
   else {

@@ -381,7 +381,7 @@ def test_c2_configured_size(R, O):
 
 
 # ----------------------------------------------- full-size sampled checks
-@pytest.mark.parametrize("which", ["C4", "C5p8", "C5p2"])
+@pytest.mark.parametrize("which", ["C4", "C5p8", "C5p2", "C5max"])
 def test_full_size_sampled(R, O, which):
     """BASELINE.json sizes in the bench launch configuration: the whole
     permutation is checked by properties (partition + (key,id) order with the
@@ -390,6 +390,8 @@ def test_full_size_sampled(R, O, which):
     bench times: pass-2 split of the carried partition, then the bucket step)."""
     if which == "C4":
         c = RI.c4_aggregation()
+    elif which == "C5max":  # N = 2^30: the widest one-GPU layout in use (B = 19, 2^19 final buckets)
+        c = RI.c5_coulomb_reg(n=1 << 30)
     else:
         c = RI.c5_coulomb_reg(p=8 if which == "C5p8" else 2)
     s = R.RBM(c)
