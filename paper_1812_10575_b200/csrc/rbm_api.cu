@@ -187,6 +187,11 @@ void fill_params(const rbm_config& k, DevParams& P) {
   P.dtf = (float)P.dt; P.sqf = (float)P.sq;
   P.invp = 1.0 / (double)(k.p - 1);
   P.invpf = (float)P.invp;
+  P.invp1 = 1.0 / (double)k.p;  // size p + 1
+  P.invp1f = 1.0f / (float)k.p;
+  const uint32_t r = (uint32_t)(k.n % k.p);
+  P.invr = r >= 2 ? 1.0 / (double)(r - 1) : 0.0;
+  P.invrf = r >= 2 ? 1.0f / (float)(r - 1) : 0.0f;
   P.geo_noise = k.noise == RBM_NOISE_GEOMETRIC ? 1u : 0u;
   P.closed_window = (k.kernel == RBM_K_BOUNDED_CONFIDENCE && k.kparam[2] != 0.0) ? 1u : 0u;
   P.verlet_start = (k.integrator == RBM_INTEG_VERLET && k.state_form == 0) ? 1u : 0u;

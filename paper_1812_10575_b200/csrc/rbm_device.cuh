@@ -52,6 +52,8 @@ struct DevParams {
   float kp0f, kp1f, betaf, dtf, sqf;
   double invp;         // 1/(p-1): prefactor of a regular batch (Eq. 2.2)
   float invpf;
+  double invr, invp1;  // 1/(r-1) (remainder batch of size r = N mod p >= 2) and 1/p (size p+1, D:7)
+  float invrf, invp1f;
   uint32_t geo_noise;  // multiplicative noise sigma x dB (wealth model)
   uint32_t verlet_start;  // Verlet (row f3): this step starts from (x_0, v_0), not (x_n, x_{n-1})
   uint32_t closed_window; // bounded confidence: closed window |z| <= r (the paper's chi_[0,1])
@@ -380,6 +382,8 @@ template <> struct Prm<float> {
   __device__ __forceinline__ static float dt(const DevParams& P) { return P.dtf; }
   __device__ __forceinline__ static float sq(const DevParams& P) { return P.sqf; }
   __device__ __forceinline__ static float invp(const DevParams& P) { return P.invpf; }
+  __device__ __forceinline__ static float invr(const DevParams& P) { return P.invrf; }
+  __device__ __forceinline__ static float invp1(const DevParams& P) { return P.invp1f; }
   __device__ __forceinline__ static float half_s2dt(const DevParams& P) { return P.half_s2dtf; }
   __device__ __forceinline__ static float lin_decay(const DevParams& P) { return P.lin_decayf; }
 };
@@ -390,11 +394,17 @@ template <> struct Prm<double> {
   __device__ __forceinline__ static double dt(const DevParams& P) { return P.dt; }
   __device__ __forceinline__ static double sq(const DevParams& P) { return P.sq; }
   __device__ __forceinline__ static double invp(const DevParams& P) { return P.invp; }
+  __device__ __forceinline__ static double invr(const DevParams& P) { return P.invr; }
+  __device__ __forceinline__ static double invp1(const DevParams& P) { return P.invp1; }
   __device__ __forceinline__ static double half_s2dt(const DevParams& P) { return P.half_s2dt; }
   __device__ __forceinline__ static double lin_decay(const DevParams& P) { return P.lin_decay; }
 };
 
 __device__ __forceinline__ float inv_cube_sqrt(float q) { const float r = rsqrtf(q); return r * r * r; }
+// s(r^2) of the attractive-repulsive Gaussian kernel (C4): fp32 through the
+// MUFU exp2 (__expf, ~2 ulp, as rsqrtf above and Box-Muller's MUFU maps, D:13)
+__device__ __forceinline__ float gauss_ar(float r2) { return __expf(-0.5f * r2) - 0.25f * __expf(-0.125f * r2); }
+__device__ __forceinline__ double gauss_ar(double r2) { return exp(-0.5 * r2) - 0.25 * exp(-0.125 * r2); }
 __device__ __forceinline__ double inv_cube_sqrt(double q) { return 1.0 / (q * sqrt(q)); }
 
 // K(z) = s(z) z for every registry entry (Eq. 1.2)
@@ -411,7 +421,7 @@ __device__ __forceinline__ T kernel_scale(const T (&z)[D], const DevParams& P) {
     const bool inside = P.closed_window ? (az <= rad) : (az < rad);
     return inside ? -Prm<T>::kp0(P) : T(0);
   }
-  if (KK == KK_GAUSS_AR) return exp(T(-0.5) * r2) - T(0.25) * exp(T(-0.125) * r2);
+  if (KK == KK_GAUSS_AR) return gauss_ar(r2);
   if (KK == KK_COULOMB_REG) return inv_cube_sqrt(r2 + Prm<T>::kp0(P));
   if (KK == KK_SMOOTH) return T(1) / (T(1) + r2);
   if (KK == KK_LINEAR) return -Prm<T>::kp0(P);                                // -kappa z

@@ -735,8 +735,11 @@ __device__ __forceinline__ void out_copy(const OutDst<T, D>& o, uint32_t v, uint
 }
 
 // ------------------------------------------------------- bucket step pieces
+// 1/(|B|-1) for the three batch sizes the division produces (D:7): p, p + 1
+// (N mod p = 1) and r = N mod p >= 2; host-computed, no division here
 template <typename T> __device__ __forceinline__ T batch_inv(const DevParams& P, uint32_t sz) {
-  return (sz == P.p) ? Prm<T>::invp(P) : T(1) / T(sz - 1);
+  RBM_CHECK(P, sz == P.p || sz == P.p + 1 || (sz == P.rem && sz >= 2));
+  return (sz == P.p) ? Prm<T>::invp(P) : (sz == P.p + 1 ? Prm<T>::invp1(P) : Prm<T>::invr(P));
 }
 
 // coordinates of record e in a shared-memory (or scratch) record array
