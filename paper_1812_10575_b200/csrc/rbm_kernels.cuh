@@ -516,12 +516,19 @@ static __global__ void __launch_bounds__(BLOCK) prologue_kernel(const __grid_con
 // ------------------------------------------- persistent pass-2 splitter
 // Tiles of the pass-1 buckets (segments) -> final buckets by the next b2 key
 // bits.  One 1024-thread CTA per SM loops over tiles with a two-stage TMA
-// ring (one bulk copy of TILE records per stage, L2 evict-first); each record
-// is ranked in its digit with a shared-memory atomic, the tile's output order
-// goes through a u16 index, and the runs are written coalesced (one vector
-// store per record) into the reserved ranges of the final buckets.  Unkeyed
-// records: key_m is computed from the id here and written to the side key
-// array for the bucket step.
+// ring (one bulk copy of TILE records per stage, L2 evict-first), split into
+// two warp groups that work on different tiles at once:
+//   rank group (warps 0..15): key of every record (Philox for unkeyed
+//     records), its rank in its digit (shared-memory atomics), one run
+//     reservation per digit, the digit offsets, and the tile's output order
+//     (staging index + the keys in output order) for stage s;
+//   write group (warps 16..31): the coalesced runs of stage s (one vector
+//     store per record, + the side key), then the TMA load of the tile after
+//     next into the freed stage.
+// So the stores of tile t overlap the key / rank work of tile t+1 (before:
+// the phases of one tile ran one after the other in the whole CTA).
+// Stage handshakes are mbarriers: tma[s] (bytes landed), full[s] (staging
+// index of stage s ready); every per-stage array is double-buffered.
 // record traits of the splitter: the state records (key carried, or from
 // the id by Philox -> side key array), or the RBM-r increment records (the
 // partition key is the particle index j, left-aligned to 32 bits)
@@ -549,10 +556,9 @@ template <typename T, int D> struct IncRT {
 
 #ifndef RBM_SPLIT_STAGE  // design-experiment builds override these (build.py -D...)
 #define RBM_SPLIT_STAGE 65536
-#define RBM_SPLIT_BLOCK 1024
-#define RBM_SPLIT_MINB 1
 #endif
-constexpr int SPLIT_BLOCK = RBM_SPLIT_BLOCK, SPLIT_MINB = RBM_SPLIT_MINB;  // CTAs of SPLIT_BLOCK threads per SM
+constexpr int SPLIT_BLOCK = 1024, SPLIT_MINB = 1;  // one CTA of 2 x 512 threads per SM
+constexpr int SPLIT_GRP = SPLIT_BLOCK / 2;          // threads per warp group
 // RBM-r' link record {j, s} (8 bytes)
 struct LinkL {
   static constexpr int RS = 8, NW = 2;
@@ -569,10 +575,13 @@ template <typename T, int D, bool LINK> using IncOrLink = std::conditional_t<LIN
 template <class RT> __host__ __device__ constexpr int split_tile_rt() {
   return (RBM_SPLIT_STAGE / RT::RS) < 4096 ? (RBM_SPLIT_STAGE / RT::RS) : 4096;  // <= one stage of records
 }
+// header: hist, off (1024 each), wsum (64), 4 mbarriers, 2 tile infos, gbase[2][1024]
+constexpr size_t SPLIT_HDR = (((2 * 1024 + 64) * 4 + 4 * 8 + 2 * 16 + 2 * 1024 * 4) + 127) & ~(size_t)127;
 template <class RT> __host__ __device__ constexpr size_t split_smem_bytes_rt() {
-  // header (counters, scratch, barriers) padded to 128 B as the kernel lays it out
-  return (((3 * 1024 + 64) * 4 + 64 + 127) & ~(size_t)127) + 2 * (size_t)split_tile_rt<RT>() * RT::RS +
-         (size_t)split_tile_rt<RT>() * (4 + 4 + 2 + 2) + (size_t)(MAX_SEG_SPLIT + 1) * 4;
+  return SPLIT_HDR + 2 * (size_t)split_tile_rt<RT>() * RT::RS                 // stages
+         + 2 * (size_t)split_tile_rt<RT>() * 4                                // staging index per stage
+         + (RT::SIDE ? 2 * (size_t)split_tile_rt<RT>() * 4 : 0)               // keys in output order per stage
+         + (size_t)(MAX_SEG_SPLIT + 1) * 4 + (size_t)MAX_SEG_SPLIT * 4;       // tile table, segment counts
 }
 template <typename T, int D> __host__ __device__ constexpr int split_tile() { return split_tile_rt<StateRT<T, D>>(); }
 template <typename T, int D> __host__ __device__ constexpr size_t split_smem_bytes() {
@@ -580,6 +589,36 @@ template <typename T, int D> __host__ __device__ constexpr size_t split_smem_byt
 }
 
 struct TileInfo { uint32_t u, lo, hi, pad; };
+
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// exclusive scan of a[0..n) (n <= 2 GRP) by the GRP threads of a warp group
+// (local index lt, named barrier bid); returns with a[] scanned, group synced
+template <int GRP>
+__device__ __forceinline__ void group_excl_scan(uint32_t* a, uint32_t n, uint32_t* wsum, uint32_t lt, int bid) {
+  const uint32_t per = (n + GRP - 1) / GRP;
+  const uint32_t b0 = min(n, lt * per), b1 = min(n, b0 + per);
+  uint32_t s = 0;
+  for (uint32_t i = b0; i < b1; ++i) s += a[i];
+  const uint32_t inc = warp_incl_scan(s);
+  const uint32_t lane = lt & 31, w = lt >> 5;
+  if (lane == 31) wsum[w] = inc;
+  named_bar(bid, GRP);
+  if (w == 0) {
+    const uint32_t v = (lane < GRP / 32) ? wsum[lane] : 0u;
+    const uint32_t vi = warp_incl_scan(v);
+    if (lane < GRP / 32) wsum[lane] = vi - v;
+  }
+  named_bar(bid, GRP);
+  uint32_t run = wsum[w] + inc - s;
+  for (uint32_t i = b0; i < b1; ++i) { const uint32_t v = a[i]; a[i] = run; run += v; }
+  named_bar(bid, GRP);
+}
 
 template <class RT, int BLOCK>
 static __global__ void __launch_bounds__(BLOCK, SPLIT_MINB) split_kernel(const __grid_constant__ DevParams P,
@@ -592,127 +631,161 @@ static __global__ void __launch_bounds__(BLOCK, SPLIT_MINB) split_kernel(const _
                                                                 uint32_t scap) {
   using L = RT;
   constexpr int TILE = split_tile_rt<RT>();
+  constexpr int GRP = BLOCK / 2;
+  static_assert(GRP == SPLIT_GRP && GRP % 32 == 0, "two equal warp groups");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   RBM_PROF_BEGIN(P);
-  uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw);  // 1024
-  uint32_t* off = hist + 1024;                             // 1024
-  uint32_t* gbase = off + 1024;                            // 1024
-  uint32_t* wsum = gbase + 1024;                           // 64
-  uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);  // 2
-  TileInfo* tinfo = reinterpret_cast<TileInfo*>(bar + 2);  // 2
-  unsigned char* stg0 = smem_raw + (((3 * 1024 + 64) * 4 + 64 + 127) & ~127);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw);  // 1024 (rank group)
+  uint32_t* off = hist + 1024;                             // 1024 (rank group)
+  uint32_t* wsum = off + 1024;                             // 64
+  uint64_t* tma = reinterpret_cast<uint64_t*>(wsum + 64);  // 2: stage s landed
+  uint64_t* full = tma + 2;                                // 2: staging index of stage s ready
+  TileInfo* tinfo = reinterpret_cast<TileInfo*>(full + 2); // 2
+  uint32_t* gbase2 = reinterpret_cast<uint32_t*>(tinfo + 2);  // [2][1024]
+  unsigned char* stg0 = smem_raw + SPLIT_HDR;
   constexpr size_t SBY = (size_t)TILE * L::RS;
-  uint32_t* rk = reinterpret_cast<uint32_t*>(stg0 + 2 * SBY);  // digit<<16 | rank, by element
-  uint32_t* kl = rk + TILE;                                    // key_m by element (unkeyed records)
-  uint16_t* inv = reinterpret_cast<uint16_t*>(kl + TILE);      // output slot -> element
-  uint16_t* idg = inv + TILE;                                  // output slot -> digit
-  uint32_t* toff = reinterpret_cast<uint32_t*>(idg + TILE);    // copy of tile_off (binary search in smem)
+  uint32_t* invd2 = reinterpret_cast<uint32_t*>(stg0 + 2 * SBY);  // [2][TILE]: element | digit << 16, by output slot
+  uint32_t* kls2 = invd2 + 2 * TILE;                               // [2][TILE]: key_m by output slot (unkeyed)
+  uint32_t* toff = kls2 + (L::SIDE ? 2 * TILE : 0);                // copy of tile_off (binary search in smem)
+  uint32_t* cnts = toff + MAX_SEG_SPLIT + 1;                       // segment counts
   const uint32_t nseg = (1u << P.b1) << P.segk;
   const uint32_t ntiles = tile_off[nseg];
   const uint32_t bits = P.b2, sh = 32u - P.b1 - P.b2, nbins = 1u << bits, mask = nbins - 1u;
   const uint32_t tid = threadIdx.x;
   const uint32_t m = (uint32_t)*P.step;
-  uint64_t pol = 0;
   for (uint32_t i = tid; i <= nseg; i += BLOCK) toff[i] = tile_off[i];
-  __syncthreads();
-  auto issue = [&](uint32_t t, uint32_t st) {  // thread 0
+  for (uint32_t i = tid; i < nseg; i += BLOCK) cnts[i] = cnt1[(size_t)i * CUR1_STRIDE];
+  // tile t into stage st (one thread): its info, then one bulk copy
+  auto issue = [&](uint32_t t, uint32_t st, uint64_t pol) {
     TileInfo ti{0u, 0u, 0u, 0u};
-    if (t < ntiles) gapped_tile(toff, cnt1, nseg, t, TILE, ti.u, ti.lo, ti.hi);
+    const uint32_t tt = min(t, ntiles - 1u);
+    uint32_t a = 0, b = nseg;  // largest u with toff[u] <= tt
+    while (b - a > 1) {
+      const uint32_t mid = (a + b) >> 1;
+      if (toff[mid] <= tt) a = mid; else b = mid;
+    }
+    ti.u = a;
+    ti.lo = (tt - toff[a]) * TILE;
+    ti.hi = min(ti.lo + TILE, cnts[a]);
     tinfo[st] = ti;
     const uint32_t cnt = ti.hi - ti.lo;
     const uint32_t bytes = (cnt * (uint32_t)L::RS + 15u) & ~15u;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(&bar[st], bytes);
-    if (cnt) bulk_g2s_stream(stg0 + st * SBY, src_rec + ((size_t)ti.u * scap + ti.lo) * L::RS, bytes, &bar[st], pol);
+    mbar_expect_tx(&tma[st], bytes);
+    if (cnt) bulk_g2s_stream(stg0 + st * SBY, src_rec + ((size_t)ti.u * scap + ti.lo) * L::RS, bytes, &tma[st], pol);
   };
+  __syncthreads();  // toff, cnts
   if (tid == 0) {
-    pol = l2_evict_first_policy();
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    mbar_init(&tma[0], 1);
+    mbar_init(&tma[1], 1);
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    const uint64_t pol = l2_evict_first_policy();
+    if (blockIdx.x < ntiles) issue(blockIdx.x, 0, pol);
+    if (blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1, pol);
   }
   __syncthreads();
-  uint32_t phase = 0, it = 0;
-  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-    const uint32_t s = it & 1u;
-    if (tid == 0 && t + gridDim.x < ntiles) issue(t + gridDim.x, s ^ 1u);  // prefetch into the free stage
-    for (uint32_t i = tid; i < nbins; i += BLOCK) hist[i] = 0;
-    RBM_PROF(P, 16);
-    mbar_wait(&bar[s], (phase >> s) & 1u);
-    phase ^= 1u << s;
-    RBM_PROF(P, 17);
-    const TileInfo ti = tinfo[s];
-    const uint32_t cnt = ti.hi - ti.lo;
-    const uint32_t dbase0 = ((ti.u >> P.segk) & P.nb1_loc_mask) << P.b2;
-    const unsigned char* stg = stg0 + s * SBY;
-    __syncthreads();
-    // PER <= 4 records per thread: their keys (independent Philox chains for
-    // unkeyed records) are computed together, then ranked in their digits
-    constexpr int PER = (TILE + BLOCK - 1) / BLOCK;
-    {
-      uint32_t kk[PER];
+  if (tid < GRP) {
+    // ---------------------------------------------------------- rank group
+    const uint32_t lt = tid;
+    constexpr int PER = (TILE + GRP - 1) / GRP;
+    uint32_t it = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const uint32_t s = it & 1u, ph = (it >> 1) & 1u;
+      for (uint32_t i = lt; i < nbins; i += GRP) hist[i] = 0;
+      mbar_wait(&tma[s], ph);
+      named_bar(1, GRP);  // hist zeroed (and off / wsum of the previous tile consumed)
+      RBM_PROF(P, 16);
+      const TileInfo ti = tinfo[s];
+      const uint32_t cnt = ti.hi - ti.lo;
+      const unsigned char* stg = stg0 + s * SBY;
+      uint32_t* invd = invd2 + s * TILE;
+      uint32_t* kls = kls2 + s * TILE;
+      uint32_t* gbase = gbase2 + s * 1024;
+      const uint32_t dbase0 = ((ti.u >> P.segk) & P.nb1_loc_mask) << P.b2;
+      // PER records per thread: keys computed together (independent Philox
+      // chains for unkeyed records), then ranked in their digits
+      uint32_t kk[PER], rk[PER];
 #pragma unroll
       for (int k = 0; k < PER; ++k) {
-        const uint32_t e = min(tid + k * BLOCK, cnt ? cnt - 1 : 0u);
+        const uint32_t e = min(lt + k * GRP, cnt ? cnt - 1 : 0u);
         kk[k] = RT::key(P, stg + (size_t)e * L::RS, m);
       }
 #pragma unroll
       for (int k = 0; k < PER; ++k) {
-        const uint32_t e = tid + k * BLOCK;
+        const uint32_t e = lt + k * GRP;
         if (e < cnt) {
-          if (RT::SIDE) kl[e] = kk[k];
           const uint32_t dg = (kk[k] >> sh) & mask;
-          rk[e] = (dg << 16) | atomicAdd(&hist[dg], 1u);
+          rk[k] = (dg << 16) | atomicAdd(&hist[dg], 1u);
         }
       }
-    }
-    __syncthreads();
-    RBM_PROF(P, 18);
-    // run reservations issued now and consumed after the staging index
-    // (their L2 round trip overlaps the scan and the placement)
-    constexpr int NRES = (1024 + BLOCK - 1) / BLOCK;
-    uint32_t gres[NRES];
+      named_bar(1, GRP);
+      RBM_PROF(P, 17);
+      // run reservations issued now and consumed after the offsets scan
+      constexpr int NRES = (1024 + GRP - 1) / GRP;
+      uint32_t gres[NRES];
 #pragma unroll
-    for (int r = 0; r < NRES; ++r) {
-      const uint32_t i = tid + r * BLOCK;
-      const uint32_t h = i < nbins ? hist[i] : 0u;
-      if (i < nbins) off[i] = h;
-      gres[r] = h ? atomicAdd(&cur[(size_t)(dbase0 + i) * CUR2_STRIDE], h) : 0u;
-    }
-    __syncthreads();
-    block_excl_scan<BLOCK>(off, nbins, wsum);
-    RBM_PROF(P, 19);
-    for (uint32_t e = tid; e < cnt; e += BLOCK) {
-      const uint32_t v = rk[e];
-      const uint32_t pos = off[v >> 16] + (v & 0xffffu);
-      RBM_CHECK(P, pos < cnt);
-      inv[pos] = (uint16_t)e;
-      idg[pos] = (uint16_t)(v >> 16);
-    }
-    // gbase[d] - off[d]: the global slot of output position j is gbase[dg] + j
-#pragma unroll
-    for (int r = 0; r < NRES; ++r)
-      if (tid + r * BLOCK < nbins) gbase[tid + r * BLOCK] = gres[r] - off[tid + r * BLOCK];
-    __syncthreads();
-
-    RBM_PROF(P, 20);
-    for (uint32_t j = tid; j < cnt; j += BLOCK) {
-      const uint32_t e = inv[j], dg = idg[j];
-      RBM_CHECK(P, e < cnt && dg < nbins);
-      const uint32_t slot = gbase[dg] + j;
-      if (slot >= dcap) {  // bucket capacity exceeded (probability ~1e-30): fail loudly
-        atomicExch(P.capacity_err, 1u);
-        continue;
+      for (int r = 0; r < NRES; ++r) {
+        const uint32_t i = lt + r * GRP;
+        const uint32_t h = i < nbins ? hist[i] : 0u;
+        if (i < nbins) off[i] = h;
+        gres[r] = h ? atomicAdd(&cur[(size_t)(dbase0 + i) * CUR2_STRIDE], h) : 0u;
       }
-      const size_t g = (size_t)(dbase0 + dg) * dcap + slot;
-      uint32_t w[L::NW];
-      ld_words<L::NW>(stg + (size_t)e * L::RS, w);
-      st_words<L::NW>(dst_rec + g * L::RS, w);
-      if (RT::SIDE) dst_key[g] = kl[e];
+      named_bar(1, GRP);
+      group_excl_scan<GRP>(off, nbins, wsum, lt, 1);
+      RBM_PROF(P, 18);
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const uint32_t e = lt + k * GRP;
+        if (e < cnt) {
+          const uint32_t pos = off[rk[k] >> 16] + (rk[k] & 0xffffu);
+          RBM_CHECK(P, pos < cnt);
+          invd[pos] = e | (rk[k] & 0xffff0000u);
+          if (L::SIDE) kls[pos] = kk[k];
+        }
+      }
+      // gbase[d] - off[d]: the global slot of output position j is gbase[dg] + j
+#pragma unroll
+      for (int r = 0; r < NRES; ++r)
+        if (lt + r * GRP < nbins) gbase[lt + r * GRP] = gres[r] - off[lt + r * GRP];
+      named_bar(1, GRP);
+      if (lt == 0) mbar_arrive(&full[s]);  // release: the write group may take stage s
+      RBM_PROF(P, 19);
     }
-    __syncthreads();  // stage s, rk, inv free
-    RBM_PROF(P, 21);
-    if (P.prof && threadIdx.x == 0) atomicAdd(&P.prof[62], 1ull);
+  } else {
+    // --------------------------------------------------------- write group
+    const uint32_t lt = tid - GRP;
+    const uint64_t pol = (lt == 0) ? l2_evict_first_policy() : 0ull;
+    uint32_t it = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const uint32_t s = it & 1u, ph = (it >> 1) & 1u;
+      mbar_wait(&full[s], ph);
+      const TileInfo ti = tinfo[s];
+      const uint32_t cnt = ti.hi - ti.lo;
+      const unsigned char* stg = stg0 + s * SBY;
+      const uint32_t* invd = invd2 + s * TILE;
+      const uint32_t* kls = kls2 + s * TILE;
+      const uint32_t* gbase = gbase2 + s * 1024;
+      const uint32_t dbase0 = ((ti.u >> P.segk) & P.nb1_loc_mask) << P.b2;
+      for (uint32_t j = lt; j < cnt; j += GRP) {
+        const uint32_t v = invd[j];
+        const uint32_t e = v & 0xffffu, dg = v >> 16;
+        RBM_CHECK(P, e < cnt && dg < nbins);
+        const uint32_t slot = gbase[dg] + j;
+        if (slot >= dcap) {  // bucket capacity exceeded (probability ~1e-30): fail loudly
+          atomicExch(P.capacity_err, 1u);
+          continue;
+        }
+        const size_t g = (size_t)(dbase0 + dg) * dcap + slot;
+        uint32_t w[L::NW];
+        ld_words<L::NW>(stg + (size_t)e * L::RS, w);
+        st_words<L::NW>(dst_rec + g * L::RS, w);
+        if (L::SIDE) dst_key[g] = kls[j];
+      }
+      named_bar(2, GRP);  // stage s, its staging index and tile info consumed
+      if (lt == 0 && t + 2 * gridDim.x < ntiles) issue(t + 2 * gridDim.x, s, pol);
+      if (lt == 0 && P.prof) atomicAdd(&P.prof[62], 1ull);
+    }
   }
 }
 
