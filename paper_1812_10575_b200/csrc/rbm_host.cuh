@@ -253,7 +253,7 @@ inline Layout choose_layout(const rbm_config& c) {
   } else {
     const double mu = (double)n / L.nbuckets;
     L.cap = (uint32_t)(mu + 6.0 * std::sqrt(mu) + 32.0);
-    L.cap = (L.cap + 31) & ~31u;
+    L.cap = (L.cap + 15) & ~15u;  // C5: 2352 records, so four bucket CTAs fit an SM
     if (L.cap > FUSED_CAP_MAX) L.cap = FUSED_CAP_MAX;
   }
   if (c.debug_bucket_cap) L.cap = c.debug_bucket_cap;
@@ -281,9 +281,8 @@ inline Layout choose_layout(const rbm_config& c) {
 
 // shared memory of the bucket kernel (bucket_smem_bytes in rbm_kernels.cuh)
 inline size_t bucket_smem(const rbm_config& c, const Layout& L) {
-  const size_t ncw = std::max<size_t>((1u << L.SB) / 2, 1u << L.b1);
-  return (2 * ncw + (1u << L.b1) + 64) * 4 + 16 + (size_t)(L.cap + 8) * rec_bytes(c) + (size_t)(L.cap + 8) * 4 +
-         (size_t)L.cap * 4 + (((size_t)L.cap * 2 + 15) & ~(size_t)15);
+  return ((size_t)bucket_ncw(L.SB, L.b1) + (1u << L.b1) + 64) * 4 + 16 + (size_t)(L.cap + 8) * rec_bytes(c) +
+         (size_t)(L.cap + 8) * 4 + (((size_t)L.cap * 2 + 15) & ~(size_t)15);
 }
 
 inline rbm_status validate(const rbm_config* cfg) {
@@ -492,7 +491,7 @@ template <typename T, int D, int KK, int INTEG>
 struct Engine final : EngineBase {
   using RL = RecL<T, D>;
   static constexpr int PR_BLOCK = 256;
-  static constexpr int MINB = (RL::RS <= 16) ? 3 : 2;  // CTAs per SM the bucket kernel is register-budgeted for
+  static constexpr int MINB = (RL::RS <= 16) ? 4 : 2;  // CTAs per SM the bucket kernel is register-budgeted for
   size_t pr_smem = 0, sp_smem = 0, bk_smem = 0, rs_smem = 0;
   bool pair_mode = false;
   int num_sms = 148;

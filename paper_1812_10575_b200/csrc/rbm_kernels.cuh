@@ -1045,18 +1045,26 @@ __device__ __noinline__ void big_bucket(const DevParams& P, State<T, D> src, con
 // their sorted places in the own gapped range (the straddle kernel steps them).
 constexpr int MODE_PAIR = 0, MODE_GROUP = 1;
 #ifndef RBM_BUCKET_BLOCK  // design-experiment builds override these (build.py -D...)
-#define RBM_BUCKET_BLOCK 320
-#define RBM_BUCKET_ITEMS 8
+#define RBM_BUCKET_BLOCK 256
+#define RBM_BUCKET_ITEMS 10
 #endif
-constexpr int BUCKET_BLOCK = RBM_BUCKET_BLOCK, BUCKET_ITEMS = RBM_BUCKET_ITEMS;  // 10 warps, capacity <= 2560 in registers
+// 8 warps, capacity <= 2560 in registers; at <= 56 KB of shared memory four
+// CTAs (buckets) share an SM (C5: 2352-record capacity, 57.3 KB)
+constexpr int BUCKET_BLOCK = RBM_BUCKET_BLOCK, BUCKET_ITEMS = RBM_BUCKET_ITEMS;
 
+// counter words: the packed u16 sub-digit counts (scanned in place), later the
+// output digit counts; >= 512 for the oversized-bucket path's two 256 arrays
+__host__ __device__ constexpr uint32_t bucket_ncw(uint32_t SB, uint32_t b1) {
+  return ((1u << SB) / 2 > (1u << b1) ? (1u << SB) / 2 : (1u << b1)) > 512u
+             ? ((1u << SB) / 2 > (1u << b1) ? (1u << SB) / 2 : (1u << b1))
+             : 512u;
+}
 template <typename T, int D> __host__ __device__ constexpr size_t bucket_smem_bytes(uint32_t cap, uint32_t SB,
                                                                                    uint32_t b1) {
-  return (size_t)(2 * (((1u << SB) / 2 > (1u << b1)) ? (1u << SB) / 2 : (1u << b1)) + (1u << b1) + 64) * 4 + 16
+  return (size_t)(bucket_ncw(SB, b1) + (1u << b1) + 64) * 4 + 16  // counters, gbase, wsum, mbarrier
          + (size_t)(cap + 8) * RecL<T, D>::RS              // records (TMA window, updated in place)
-         + (size_t)(cap + 8) * 4                           // side keys (TMA window) -> key_{m+1}
-         + (size_t)cap * 4                                 // composites -> tb | inv (u16 each)
-         + (((size_t)cap * 2 + 15) & ~(size_t)15);         // ord (u16)
+         + (size_t)(cap + 8) * 4                           // side keys (TMA window) -> composites -> tb
+         + (((size_t)cap * 2 + 15) & ~(size_t)15);         // ord (u16) -> staging index (u16)
 }
 
 // the bucket step of final bucket b (global start s0, n > 0 records at
@@ -1071,12 +1079,13 @@ __device__ __forceinline__ void bucket_body(const DevParams& P, State<T, D> src,
   const uint32_t sb = b * scap;
   const uint32_t nsb = 1u << P.SB;
   const uint32_t nout = 1u << P.b1;
-  // sub-digit counts and offsets as packed u16 pairs (bucket sizes < 2^16);
-  // the same words later hold the <= 1024 output digit counts / offsets
-  const uint32_t ncw = (nsb / 2 > nout) ? nsb / 2 : nout;
+  // sub-digit counts as packed u16 pairs (bucket sizes < 2^16), scanned in
+  // place into offsets; the same words later hold the <= 1024 output digit
+  // counts, again scanned in place
+  const uint32_t ncw = bucket_ncw(P.SB, P.b1);
   uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw);
-  uint32_t* off = cnt + ncw;
-  uint32_t* gbase = off + ncw;
+  uint32_t* off = cnt;
+  uint32_t* gbase = cnt + ncw;
   uint32_t* wsum = gbase + nout;
   uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + 64);
   const uint32_t cap = P.cap;
@@ -1084,15 +1093,15 @@ __device__ __forceinline__ void bucket_body(const DevParams& P, State<T, D> src,
   for (uint32_t i = threadIdx.x; i < ncw / 4; i += BLOCK) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
   if (n > cap || n > (uint32_t)(BLOCK * ITEMS)) {  // oversized bucket: global scratch
     __syncthreads();
-    big_bucket<T, D, KK, INTEG, BLOCK>(P, src, dst, cur_next, s0, sb, n, m, dcap, cnt, off, wsum);
+    big_bucket<T, D, KK, INTEG, BLOCK>(P, src, dst, cur_next, s0, sb, n, m, dcap, cnt, cnt + 256, wsum);
     return;
   }
   unsigned char* rs = reinterpret_cast<unsigned char*>(bar + 2);
   uint32_t* key_l = reinterpret_cast<uint32_t*>(rs + (size_t)(cap + 8) * L::RS);
-  uint32_t* ks = key_l + cap + 8;  // composites (sort); then tb
-  uint32_t* tb = ks;               // output digit << 16 | rank in it, by element (~0: straddler)
-  uint32_t* inv = key_l;           // staged output slot -> element | digit << 16
-  uint16_t* ord = reinterpret_cast<uint16_t*>(ks + cap);
+  uint32_t* ks = key_l;             // composites (sort), once the side keys are consumed
+  uint32_t* tb = ks;                // then: output digit << 16 | rank in it, by element (~0: straddler)
+  uint16_t* ord = reinterpret_cast<uint16_t*>(key_l + cap + 8);
+  uint16_t* inv = ord;              // after the batch update: staged output slot -> element
   const bool side = !L::KEYED && P.side_key;
   if (threadIdx.x == 0) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem last touched by generic accesses
@@ -1131,14 +1140,17 @@ __device__ __forceinline__ void bucket_body(const DevParams& P, State<T, D> src,
   }
   __syncthreads();
   RBM_PROF(P, 1);
-  block_excl_scan_u16x2<BLOCK>(cnt, off, nsb / 2, wsum);
+  block_excl_scan_u16x2<BLOCK>(cnt, off, nsb / 2, wsum);  // in place
   RBM_PROF(P, 2);
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t e = k * BLOCK + threadIdx.x;
     if (e < n) {
       const uint32_t sd = rsd[k] >> 16, sh16 = (sd & 1u) << 4;
-      const uint32_t a = (off[sd >> 1] >> sh16) & 0xffffu, c = (cnt[sd >> 1] >> sh16) & 0xffffu;
+      const uint32_t a = (off[sd >> 1] >> sh16) & 0xffffu;
+      // sub-bucket size = next offset - own offset (the last ends at n)
+      const uint32_t a1 = (sd + 1u < nsb) ? ((off[(sd + 1u) >> 1] >> (((sd + 1u) & 1u) << 4)) & 0xffffu) : n;
+      const uint32_t c = a1 - a;
       RBM_CHECK(P, a + (rsd[k] & 0xffffu) < n && a + c <= n);
       ks[a + (rsd[k] & 0xffffu)] = rc[k];
       rsd[k] = (a << 16) | c;  // sub-bucket start and size, for the rank below
@@ -1345,13 +1357,13 @@ __device__ __forceinline__ void bucket_body(const DevParams& P, State<T, D> src,
     const uint32_t h = i < nout ? cnt[i] : 0u;
     gres[r] = h ? atomicAdd(&cur_next[(size_t)out_seg(P, i, blockIdx.x) * CUR1_STRIDE], h) : 0u;
   }
-  const uint32_t total = block_excl_scan4<BLOCK>(cnt, off, nout, wsum);
+  const uint32_t total = block_excl_scan4<BLOCK>(cnt, off, nout, wsum);  // in place
   for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {  // staging index (tb read in element order)
     const uint32_t t = tb[e];
     RBM_CHECK(P, t == 0xffffffffu || (t >> 16) < nout);
     if (t != 0xffffffffu) {
       RBM_CHECK(P, off[t >> 16] + (t & 0xffffu) < total);
-      inv[off[t >> 16] + (t & 0xffffu)] = e | (t & 0xffff0000u);
+      inv[off[t >> 16] + (t & 0xffffu)] = (uint16_t)e;
     }
   }
 #pragma unroll
@@ -1361,9 +1373,10 @@ __device__ __forceinline__ void bucket_body(const DevParams& P, State<T, D> src,
   RBM_PROF(P, 7);
   // staged slots -> coalesced runs of the step-(m+1) pass-1 buckets
   for (uint32_t j = threadIdx.x; j < total; j += BLOCK) {
-    const uint32_t v = inv[j];
-    const uint32_t e = v & 0xffffu, dg = v >> 16;
-    RBM_CHECK(P, e < n && dg < nout);
+    const uint32_t e = inv[j];
+    RBM_CHECK(P, e < n);
+    const uint32_t dg = tb[e] >> 16;
+    RBM_CHECK(P, dg < nout);
     const uint32_t slot = gbase[dg] + j;
     if (slot >= dcap) { atomicExch(P.capacity_err, 1u); continue; }
     out_copy<T, D>(dst, out_seg(P, dg, blockIdx.x), dcap, slot, rs + (size_t)e * L::RS);
