@@ -1146,10 +1146,13 @@ __device__ __forceinline__ void bucket_body(const DevParams& P, State<T, D> src,
   for (int k = 0; k < ITEMS; ++k) {
     const uint32_t e = k * BLOCK + threadIdx.x;
     if (e < n) {
-      const uint32_t sd = rsd[k] >> 16, sh16 = (sd & 1u) << 4;
-      const uint32_t a = (off[sd >> 1] >> sh16) & 0xffffu;
-      // sub-bucket size = next offset - own offset (the last ends at n)
-      const uint32_t a1 = (sd + 1u < nsb) ? ((off[(sd + 1u) >> 1] >> (((sd + 1u) & 1u) << 4)) & 0xffffu) : n;
+      const uint32_t sd = rsd[k] >> 16;
+      // sub-bucket size = next offset - own offset (the last ends at n); for
+      // an even sub-digit the next offset is the high half of the same word
+      const uint32_t w0 = off[sd >> 1];
+      const uint32_t a = (sd & 1u) ? (w0 >> 16) : (w0 & 0xffffu);
+      uint32_t a1 = w0 >> 16;
+      if (sd & 1u) a1 = (sd + 1u < nsb) ? (off[(sd + 1u) >> 1] & 0xffffu) : n;
       const uint32_t c = a1 - a;
       RBM_CHECK(P, a + (rsd[k] & 0xffffu) < n && a + c <= n);
       ks[a + (rsd[k] & 0xffffu)] = rc[k];
@@ -1164,10 +1167,17 @@ __device__ __forceinline__ void bucket_body(const DevParams& P, State<T, D> src,
     if (e < n) {
       const uint32_t a = rsd[k] >> 16, c = rsd[k] & 0xffffu;
       uint32_t r = a;
-      if (c > 1) {  // sub-buckets hold ~1 element: a short predicated scan
+      if (c > 1) {  // sub-buckets hold ~1 element: a short predicated count
+        // six independent loads (a + 5 < cap + 8: inside the array; entries
+        // past the sub-bucket are masked by i < c)
+        const uint32_t x = rc[k];
+        uint32_t v[6];
 #pragma unroll
-        for (uint32_t i = 0; i < 6; ++i)
-          if (i < c) r += (ks[a + i] < rc[k]) ? 1u : 0u;
+        for (int i = 0; i < 6; ++i) v[i] = ks[a + i];
+        uint32_t t = (uint32_t)(v[0] < x) + (uint32_t)(v[1] < x);
+#pragma unroll
+        for (uint32_t i = 2; i < 6; ++i) t += (uint32_t)(i < c && v[i] < x);
+        r += t;
         // more than 6 (probability ~6e-4 per element): a plain loop, not
         // unrolled, so warps that never take it pay no loop prologue
 #pragma unroll 1
