@@ -880,7 +880,7 @@ struct Engine final : EngineBase {
   }
 
   // slot records {j_s, s[, Delta_s]} -> partition by particle index -> per id
-  // bucket: increments added in ascending s (RBM-r), or expected tags (RBM-r', LINK)
+  // bucket: increments added in the canonical order (RBM-r), or expected tags (RBM-r', LINK)
   template <bool LINK, class RT> void partition_slots(rbm_ctx& c, cudaStream_t s, uint32_t* expect) {
     const DevParams& P = c.P;
     const Layout& L = c.L;

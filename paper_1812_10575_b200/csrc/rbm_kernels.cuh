@@ -540,11 +540,59 @@ template <typename T, int D> struct StateRT {
     return RecL<T, D>::KEYED ? w[1] : shuffle_key(P, w[0], m);
   }
 };
-// RBM-r increment record {j, s, Delta_s[D]} (16 or 32 bytes; 24-byte records
-// for fp32 d=3 measured slower: 24.9 vs 21.3 ms per C5 step)
+// RBM-r increment record {j, [pad,] Delta_s[D]}: fp32 d=1 8 B, fp32 d=2/3 and
+// fp64 d=1 16 B, fp64 d=2/3 32 B.  The slot index s is not carried: a
+// particle's increments are summed order-independently (Fx below, reading D:8)
 template <typename T, int D> struct IncL {
-  static constexpr int RS = ((8 + D * (int)sizeof(T)) + 15) / 16 * 16;
+  static constexpr int XW = (int)(sizeof(T) / 4);  // word offset of Delta[0] (fp64: 8-byte aligned)
+  static constexpr int RS0 = 4 * XW + D * (int)sizeof(T);
+  static constexpr int RS = RS0 <= 8 ? 8 : (RS0 + 15) / 16 * 16;
   static constexpr int NW = RS / 4;
+};
+// Order-independent sum of a particle's increments (reading D:8): for each
+// coordinate, every increment is converted exactly to a fixed-point integer at
+// the scale of the largest exponent among them (G guard bits below that
+// increment's ulp; bits further down are truncated), the integers are summed
+// exactly in int64 (so the order of the increments does not matter), and the
+// sum is added to x with one rounding.  One GPU (shared-memory atomics) and
+// the partitioned path (per-particle loop) compute the same integers.
+template <typename T> struct Fx;
+template <> struct Fx<float> {
+  static constexpr int G = 28;  // |acc| <= c 2^52: int64 for c < 2^11 increments
+  __device__ __forceinline__ static uint32_t ex(float v) {
+    const uint32_t e = (__float_as_uint(v) >> 23) & 0xffu;
+    return e ? e : 1u;
+  }
+  __device__ __forceinline__ static long long q(float v, uint32_t E) {
+    const uint32_t u = __float_as_uint(v), e = (u >> 23) & 0xffu;
+    const unsigned long long mant = (unsigned long long)((u & 0x7fffffu) | (e ? 0x800000u : 0u)) << G;
+    const uint32_t sh = E - (e ? e : 1u);
+    const long long mag = sh >= 64u ? 0ll : (long long)(mant >> sh);
+    return (u >> 31) ? -mag : mag;
+  }
+  __device__ __forceinline__ static float add(float x, long long acc, uint32_t E) {
+    if (E >= 255u) return __int_as_float(0x7fc00000);  // a non-finite increment: flagged downstream
+    return (float)((double)x + ldexp((double)acc, (int)E - 150 - G));
+  }
+};
+template <> struct Fx<double> {
+  static constexpr int G = 4;  // |acc| <= c 2^57: int64 for c < 64 increments
+  __device__ __forceinline__ static uint32_t ex(double v) {
+    const uint32_t e = (uint32_t)(((unsigned long long)__double_as_longlong(v) >> 52) & 0x7ffu);
+    return e ? e : 1u;
+  }
+  __device__ __forceinline__ static long long q(double v, uint32_t E) {
+    const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+    const uint32_t e = (uint32_t)((u >> 52) & 0x7ffu);
+    const unsigned long long mant = ((u & 0xfffffffffffffull) | (e ? 0x10000000000000ull : 0ull)) << G;
+    const uint32_t sh = E - (e ? e : 1u);
+    const long long mag = sh >= 64u ? 0ll : (long long)(mant >> sh);
+    return (u >> 63) ? -mag : mag;
+  }
+  __device__ __forceinline__ static double add(double x, long long acc, uint32_t E) {
+    if (E >= 2047u) return __longlong_as_double(0x7ff8000000000000ll);
+    return x + ldexp((double)acc, (int)E - 1075 - G);
+  }
 };
 template <typename T, int D> struct IncRT {
   static constexpr int RS = IncL<T, D>::RS, NW = IncL<T, D>::NW;
@@ -1863,7 +1911,8 @@ static __global__ void __launch_bounds__(TB) direct_kernel(const __grid_constant
 // ------------------------------------------------------------------ RBM-r
 // One sweep of ceil(N/p) with-replacement batches (Alg. 2/3),
 // Jacobi-additive reading D:8: every batch evaluated from X_m, then
-// x_j <- x_j + sum over the slots s with j_s = j of Delta_s, in ascending s.
+// x_j <- x_j + sum over the slots s with j_s = j of Delta_s, summed
+// order-independently in fixed point (Fx).
 // State in id order as AoS (4 scalars per particle, one sector per gather).
 // One GPU: the increments go through a partition by particle index (the
 // rbmr_emit / split / rbmr_bucket_apply kernels below); the sequential RBM-r'
@@ -1886,8 +1935,34 @@ static __global__ void rbmr_pack_kernel(uint64_t n, State<T, D> st, T* __restric
 
 template <typename T, int D>
 __device__ __forceinline__ void load4(const T* __restrict__ xa, uint32_t j, T (&x)[D]) {
+  if constexpr (sizeof(T) == 4) {  // one 16-byte access
+    const float4 v = reinterpret_cast<const float4*>(xa)[j];
+    const float w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-  for (int c = 0; c < D; ++c) x[c] = xa[(size_t)j * 4 + c];
+    for (int c = 0; c < D; ++c) x[c] = (T)w[c];
+  } else {
+    const double2 v0 = reinterpret_cast<const double2*>(xa)[2 * (size_t)j];
+    const double2 v1 = reinterpret_cast<const double2*>(xa)[2 * (size_t)j + 1];
+    const double w[4] = {v0.x, v0.y, v1.x, v1.y};
+#pragma unroll
+    for (int c = 0; c < D; ++c) x[c] = (T)w[c];
+  }
+}
+
+// the D coordinates of particle j into its 4-wide AoS slot, padding zero (as
+// rbmr_pack_kernel writes it; only the Jacobi RBM-r state is stored this way):
+// one 16-byte store for fp32, two for fp64, no read
+template <typename T, int D>
+__device__ __forceinline__ void store4(T* __restrict__ xa, uint32_t j, const T (&x)[D]) {
+  T w[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) w[c] = (c < D) ? x[c < D ? c : 0] : T(0);
+  if constexpr (sizeof(T) == 4) {
+    reinterpret_cast<float4*>(xa)[j] = make_float4((float)w[0], (float)w[1], (float)w[2], (float)w[3]);
+  } else {
+    reinterpret_cast<double2*>(xa)[2 * (size_t)j] = make_double2((double)w[0], (double)w[1]);
+    reinterpret_cast<double2*>(xa)[2 * (size_t)j + 1] = make_double2((double)w[2], (double)w[3]);
+  }
 }
 
 // ----------------------- exact sequential RBM-r' (Alg. 2, row f2)
@@ -2130,7 +2205,7 @@ static __global__ void __launch_bounds__(128) rbmr_seq_dep_kernel(const __grid_c
 //      request's position
 //   I  all-to-all of the increments
 //   D  the owner registers every received increment at its particle and adds
-//      them in ascending global s (the one-GPU order): bit-identical to G = 1.
+//      them order-independently (Fx, as on one GPU): bit-identical to G = 1.
 constexpr int RP_MAXG = 64;
 struct RPart {
   uint32_t G, rank, cap;                 // ranks, this rank, records per (source, destination) chunk
@@ -2298,7 +2373,7 @@ static __global__ void rbmr_register_part_kernel(const __grid_constant__ DevPara
   }
 }
 
-// D2: x_j += sum of its increments in ascending global slot s (reading D:8)
+// D2: x_j += the order-independent sum of its increments (Fx, reading D:8)
 template <typename T, int D>
 static __global__ void rbmr_apply_part_kernel(const __grid_constant__ DevParams P, const __grid_constant__ RPart R,
                                               T* __restrict__ xa, const uint32_t* __restrict__ mcnt,
@@ -2310,7 +2385,7 @@ static __global__ void rbmr_apply_part_kernel(const __grid_constant__ DevParams 
        jl += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t c = mcnt[jl];
     if (c == 0) continue;
-    uint32_t ix[MAXL], sl[MAXL];
+    uint32_t ix[MAXL];
     uint32_t k = 0;
     const uint32_t cm = c < MBOX ? c : MBOX;
     for (uint32_t q = 0; q < cm; ++q) ix[k++] = mbox[jl * MBOX + q];
@@ -2322,21 +2397,18 @@ static __global__ void rbmr_apply_part_kernel(const __grid_constant__ DevParams 
           else atomicExch(P.capacity_err, 1u);
         }
     }
-    for (uint32_t a = 0; a < k; ++a)
-      sl[a] = reinterpret_cast<const uint32_t*>(R.ir + (ix[a] / R.cap) * R.ichunk)[ix[a] % R.cap];
-    for (uint32_t a = 1; a < k; ++a) {  // insertion sort by global slot
-      const uint32_t v = sl[a], w0 = ix[a];
-      uint32_t w = a;
-      while (w > 0 && sl[w - 1] > v) { sl[w] = sl[w - 1]; ix[w] = ix[w - 1]; --w; }
-      sl[w] = v;
-      ix[w] = w0;
-    }
+    auto dd = [&](uint32_t idx) {
+      return reinterpret_cast<const T*>(R.ir + (idx / R.cap) * R.ichunk + R.ioff) + (size_t)(idx % R.cap) * 4;
+    };
     T x[D];
     load4<T, D>(xa, (uint32_t)jl, x);
-    for (uint32_t a = 0; a < k; ++a) {
-      const T* dd = reinterpret_cast<const T*>(R.ir + (ix[a] / R.cap) * R.ichunk + R.ioff) + (size_t)(ix[a] % R.cap) * 4;
 #pragma unroll
-      for (int cc = 0; cc < D; ++cc) x[cc] += dd[cc];
+    for (int cc = 0; cc < D; ++cc) {  // order-independent fixed-point sum (Fx, D:8), as on one GPU
+      uint32_t E = 0;
+      for (uint32_t a = 0; a < k; ++a) E = max(E, Fx<T>::ex(dd(ix[a])[cc]));
+      long long acc = 0;
+      for (uint32_t a = 0; a < k; ++a) acc += Fx<T>::q(dd(ix[a])[cc], E);
+      x[cc] = Fx<T>::add(x[cc], acc, E);
     }
     if (P.constraint == 1) renormalise<T, D>(x);
     check_finite<T, D>(x, P, (uint32_t)(R.id0 + jl), m);
@@ -2379,12 +2451,13 @@ static __global__ void gather_aos_part_kernel(const T* __restrict__ xa, uint64_t
 // MSD partition as the RBM-1 records, keyed by j_s (no random mailboxes):
 //   emit     one thread per batch: draws j_s (as the oracle, reading D:9),
 //            gathers x_{j_s}, computes Delta_s (rbmr_deltas), and the CTA's
-//            records {j_s, s, Delta_s} are staged by the top b1 bits of j_s
+//            records {j_s, Delta_s} are staged by the top b1 bits of j_s
 //            and written as coalesced runs into the pass-1 buckets
 //   split    pass-1 -> final buckets of 2^(idbits-B) particle ids (split_kernel<IncRT>)
-//   apply    one CTA per final bucket: the records are ordered by (j, s) in
-//            shared memory and every particle of the id range adds its
-//            increments in ascending s to its own position (reading D:8)
+//   apply    one CTA per final bucket of W ids: per coordinate, the largest
+//            increment exponent of each particle (shared-memory atomicMax),
+//            then the exact fixed-point sum of its increments (64-bit
+//            shared-memory atomics, any order), added once (Fx, reading D:8)
 constexpr int EMIT_BLOCK = 256;
 constexpr uint32_t EMIT_TS = 2048;  // slots per emit CTA
 
@@ -2446,10 +2519,11 @@ static __global__ void __launch_bounds__(EMIT_BLOCK) rbmr_emit_kernel(const __gr
 #pragma unroll
         for (int k = 0; k < IL::NW; ++k) w[k] = 0u;
         w[0] = jj[l];
-        w[1] = (uint32_t)(s0 + l);
-        if constexpr (!LINK) {
+        if constexpr (LINK) {
+          w[1] = (uint32_t)(s0 + l);
+        } else {
 #pragma unroll
-          for (int c = 0; c < D; ++c) to_w(dl[l][c], w + 2 + c * (int)(sizeof(T) / 4));
+          for (int c = 0; c < D; ++c) to_w(dl[l][c], w + IncL<T, D>::XW + c * (int)(sizeof(T) / 4));
         }
         st_words<IL::NW>(stg + (size_t)e * IL::RS, w);
         const uint32_t dg = (jj[l] << P.jshift) >> sh;
@@ -2485,7 +2559,8 @@ static __global__ void __launch_bounds__(EMIT_BLOCK) rbmr_emit_kernel(const __gr
 }
 
 template <typename T, int D, bool LINK> __host__ __device__ constexpr size_t rapply_smem_bytes(uint32_t cap, uint32_t W) {
-  return (size_t)(cap + 8) * IncOrLink<T, D, LINK>::RS + (size_t)cap * 4 + (size_t)W * 8 + 64 * 4 + 16;
+  return LINK ? (size_t)(cap + 8) * IncOrLink<T, D, LINK>::RS + (size_t)cap * 4 + (size_t)W * 8 + 64 * 4 + 16
+              : (size_t)W * D * (8 + 4) + 16;  // Jacobi: acc (int64) and emax (u32) per particle and coordinate
 }
 
 // apply: final bucket b = the particle ids [b W, (b+1) W); n = cnt[b] records.
@@ -2493,7 +2568,7 @@ template <typename T, int D, bool LINK> __host__ __device__ constexpr size_t rap
 // s_a of particle j (ascending) gets expect[s_a] = tag_j + a for a > 0 (the
 // caller presets expect[] to SEQ_FREE, the first slot's value)
 template <typename T, int D, bool LINK>
-static __global__ void __launch_bounds__(256) rbmr_bucket_apply_kernel(const __grid_constant__ DevParams P,
+static __global__ void __launch_bounds__(256, 4) rbmr_bucket_apply_kernel(const __grid_constant__ DevParams P,
                                                                        const unsigned char* __restrict__ fin, uint32_t cap,
                                                                        const uint32_t* __restrict__ cnt, uint32_t W,
                                                                        T* __restrict__ xa, uint32_t* __restrict__ expect) {
@@ -2506,6 +2581,75 @@ static __global__ void __launch_bounds__(256) rbmr_bucket_apply_kernel(const __g
   if (j0 >= P.n) return;
   const uint32_t nid = (uint32_t)min((uint64_t)W, P.n - j0);
   const uint32_t m = (uint32_t)*P.step;
+  constexpr int RMAX = 4;  // W <= 1024 particles in registers (larger W: loaded in the loop)
+  if constexpr (!LINK) {
+    // ---- Jacobi RBM-r: order-independent fixed-point sums (Fx, reading D:8)
+    long long* acc = reinterpret_cast<long long*>(smem_raw);              // [W][D]
+    uint32_t* emax = reinterpret_cast<uint32_t*>(acc + (size_t)W * D);    // [W][D]; 0: no increment
+    T xv[RMAX][D];
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) {  // the id range's positions, loaded before the increments
+      const uint32_t jl = threadIdx.x + r * BLOCK;
+      if (jl < nid) load4<T, D>(xa, (uint32_t)(j0 + jl), xv[r]);
+    }
+    for (uint32_t i = threadIdx.x; i < W * D; i += BLOCK) { acc[i] = 0; emax[i] = 0; }
+    if (n > cap || cap > 8u * BLOCK) {  // cannot happen at the layout's 12-sigma capacity (<= 2048): flagged
+      if (threadIdx.x == 0) atomicExch(P.capacity_err, 1u);
+      return;
+    }
+    constexpr int AI = 8;
+    uint32_t jl_k[AI];
+    T dv[AI][D];
+#pragma unroll
+    for (int k = 0; k < AI; ++k) {
+      const uint32_t e = k * BLOCK + threadIdx.x;
+      if (e < n) {
+        uint32_t w[IL::NW];
+        ld_words<IL::NW>(fin + ((size_t)b * cap + e) * IL::RS, w);
+        jl_k[k] = w[0] - (uint32_t)j0;
+        RBM_CHECK(P, jl_k[k] < nid);
+#pragma unroll
+        for (int cc = 0; cc < D; ++cc) from_w(dv[k][cc], w + IncL<T, D>::XW + cc * (int)(sizeof(T) / 4));
+      }
+    }
+    __syncthreads();  // acc / emax zeroed
+#pragma unroll
+    for (int k = 0; k < AI; ++k)
+      if (k * BLOCK + threadIdx.x < n)
+#pragma unroll
+        for (int cc = 0; cc < D; ++cc) atomicMax(&emax[jl_k[k] * D + cc], Fx<T>::ex(dv[k][cc]));
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < AI; ++k)
+      if (k * BLOCK + threadIdx.x < n)
+#pragma unroll
+        for (int cc = 0; cc < D; ++cc) {
+          const uint32_t i = jl_k[k] * D + cc;
+          atomicAdd(reinterpret_cast<unsigned long long*>(&acc[i]),
+                    (unsigned long long)Fx<T>::q(dv[k][cc], emax[i]));
+        }
+    __syncthreads();
+    auto particle = [&](uint32_t jl, T (&x)[D]) {
+      if (emax[jl * D] == 0u) return;  // no increment
+#pragma unroll
+      for (int cc = 0; cc < D; ++cc) x[cc] = Fx<T>::add(x[cc], acc[jl * D + cc], emax[jl * D + cc]);
+      if (P.constraint == 1) renormalise<T, D>(x);
+      check_finite<T, D>(x, P, (uint32_t)(j0 + jl), m);
+      store4<T, D>(xa, (uint32_t)(j0 + jl), x);
+    };
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) {
+      const uint32_t jl = threadIdx.x + r * BLOCK;
+      if (jl < nid) particle(jl, xv[r]);
+    }
+    for (uint32_t jl = threadIdx.x + RMAX * BLOCK; jl < nid; jl += BLOCK) {
+      T x[D];
+      load4<T, D>(xa, (uint32_t)(j0 + jl), x);
+      particle(jl, x);
+    }
+    return;
+  }
+  // ---- RBM-r' link pass: records grouped by particle, each particle's slots in ascending s
   unsigned char* rs = smem_raw;
   uint32_t* pos = reinterpret_cast<uint32_t*>(rs + (size_t)(cap + 8) * IL::RS);  // element -> rank within its particle
   uint32_t* pc = pos + cap;        // per particle: count
@@ -2521,79 +2665,64 @@ static __global__ void __launch_bounds__(256) rbmr_bucket_apply_kernel(const __g
   }
   for (uint32_t i = threadIdx.x; i < W; i += BLOCK) pc[i] = 0;
   __syncthreads();
-  if (n > cap) {  // cannot happen at the layout's 12-sigma capacity: flagged
+  if (n > cap || cap > 8u * BLOCK) {  // cannot happen at the layout's 12-sigma capacity (<= 2048): flagged
     if (threadIdx.x == 0) atomicExch(P.capacity_err, 1u);
     return;
   }
   if (n) mbar_wait(bar, 0);
-  for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
-    const uint32_t jl = (uint32_t)(reinterpret_cast<const uint32_t*>(rs + (size_t)e * IL::RS)[0] - j0);
-    RBM_CHECK(P, jl < nid);
-    pos[e] = atomicAdd(&pc[jl], 1u);
+  // each record's particle and its arrival rank there (registers), counts per particle
+  constexpr int AI = 8;
+  uint32_t myjl[AI], myr[AI];
+#pragma unroll
+  for (int k = 0; k < AI; ++k) {
+    const uint32_t e = k * BLOCK + threadIdx.x;
+    if (e < n) {
+      myjl[k] = (uint32_t)(reinterpret_cast<const uint32_t*>(rs + (size_t)e * IL::RS)[0] - j0);
+      RBM_CHECK(P, myjl[k] < nid);
+      myr[k] = atomicAdd(&pc[myjl[k]], 1u);
+    }
   }
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < W; i += BLOCK) po[i] = pc[i];
   __syncthreads();
   block_excl_scan<BLOCK>(po, (int)W, wsum);
-  uint32_t myjl[8], myr[8];
-  uint32_t k = 0;
-  for (uint32_t e = threadIdx.x; e < n; e += BLOCK) {
-    myjl[k] = (uint32_t)(reinterpret_cast<const uint32_t*>(rs + (size_t)e * IL::RS)[0] - j0);
-    myr[k] = pos[e];
-    ++k;
-  }
-  __syncthreads();  // pos is dead: its space becomes ix
-  k = 0;
-  for (uint32_t e = threadIdx.x; e < n; e += BLOCK, ++k) {
-    RBM_CHECK(P, k < 8 && po[myjl[k]] + myr[k] < n);
-    ix[po[myjl[k]] + myr[k]] = (uint16_t)e;
+#pragma unroll
+  for (int k = 0; k < AI; ++k) {
+    const uint32_t e = k * BLOCK + threadIdx.x;
+    if (e < n) {
+      RBM_CHECK(P, po[myjl[k]] + myr[k] < n);
+      ix[po[myjl[k]] + myr[k]] = (uint16_t)e;
+    }
   }
   __syncthreads();
-  // every particle of the range with increments: ascending slot order (D:8)
-  for (uint32_t jl = threadIdx.x; jl < nid; jl += BLOCK) {
-    const uint32_t c = pc[jl];
-    if (c == 0) continue;
-    constexpr uint32_t MAXL = 32;
-    uint32_t ee[MAXL], ss[MAXL];
-    const uint32_t kk = c < MAXL ? c : MAXL;
-    if (c > MAXL) {
-      atomicExch(P.capacity_err, 1u);
-      if constexpr (LINK) continue;  // flagged; no slot of the particle waits (the sweep cannot hang)
-    }
-    for (uint32_t a = 0; a < kk; ++a) {
-      ee[a] = ix[po[jl] + a];
-      ss[a] = reinterpret_cast<const uint32_t*>(rs + (size_t)ee[a] * IL::RS)[1];
-    }
-    for (uint32_t a = 1; a < kk; ++a) {  // insertion sort by global slot
-      const uint32_t v = ss[a], w0 = ee[a];
-      uint32_t w = a;
-      while (w > 0 && ss[w - 1] > v) { ss[w] = ss[w - 1]; ee[w] = ee[w - 1]; --w; }
-      ss[w] = v;
-      ee[w] = w0;
-    }
-    if constexpr (LINK) {
+  {
+    // every particle of the range with slots: ascending slot order
+    for (uint32_t jl = threadIdx.x; jl < nid; jl += BLOCK) {
+      const uint32_t c = pc[jl];
+      if (c == 0) continue;
+      constexpr uint32_t MAXL = 32;
+      uint32_t ee[MAXL], ss[MAXL];
+      const uint32_t kk = c < MAXL ? c : MAXL;
+      if (c > MAXL) {
+        atomicExch(P.capacity_err, 1u);
+        continue;  // flagged; no slot of the particle waits (the sweep cannot hang)
+      }
+      for (uint32_t a = 0; a < kk; ++a) {
+        ee[a] = ix[po[jl] + a];
+        ss[a] = reinterpret_cast<const uint32_t*>(rs + (size_t)ee[a] * IL::RS)[1];
+      }
+      for (uint32_t a = 1; a < kk; ++a) {  // insertion sort by global slot
+        const uint32_t v = ss[a], w0 = ee[a];
+        uint32_t w = a;
+        while (w > 0 && ss[w - 1] > v) { ss[w] = ss[w - 1]; ee[w] = ee[w - 1]; --w; }
+        ss[w] = v;
+        ee[w] = w0;
+      }
       if (kk > 1) {  // expect[] was preset to SEQ_FREE: only the later slots are written
         const uint32_t t0 = *seq_tag(xa, (uint32_t)(j0 + jl));
         for (uint32_t a = 1; a < kk; ++a) expect[ss[a]] = t0 + a;
       }
-      continue;
     }
-    const uint64_t j = j0 + jl;
-    T x[D];
-    load4<T, D>(xa, (uint32_t)j, x);
-    for (uint32_t a = 0; a < kk; ++a) {
-      const uint32_t* wd = reinterpret_cast<const uint32_t*>(rs + (size_t)ee[a] * IL::RS) + 2;
-#pragma unroll
-      for (int cc = 0; cc < D; ++cc) {
-        T dv;
-        from_w(dv, wd + cc * (int)(sizeof(T) / 4));
-        x[cc] += dv;
-      }
-    }
-    if (P.constraint == 1) renormalise<T, D>(x);
-    check_finite<T, D>(x, P, (uint32_t)j, m);
-#pragma unroll
-    for (int cc = 0; cc < D; ++cc) xa[j * 4 + cc] = x[cc];
   }
 }
 
