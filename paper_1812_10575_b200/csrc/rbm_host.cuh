@@ -502,7 +502,7 @@ struct Engine final : EngineBase {
     const uint32_t W = 1u << (c.L.idbits - c.L.B);
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(rbmr_emit_kernel<T, D, KK, INTEG, LINK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)emit_smem_bytes<T, D, LINK>())) != cudaSuccess ||
+                                  200 * 1024)) != cudaSuccess ||
         (e = cudaFuncSetAttribute(split_kernel<RT, SPLIT_BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)split_smem_bytes_rt<RT>())) != cudaSuccess ||
         (e = cudaFuncSetAttribute(rbmr_bucket_apply_kernel<T, D, LINK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -889,8 +889,15 @@ struct Engine final : EngineBase {
     const uint32_t bpc = EMIT_TS / c.cfg.p;
     cudaMemsetAsync(c.cur1[0], 0, (size_t)(1u << L.b1) * CUR1_STRIDE * 4, s);
     c.mark(s);
+    // sized for 2^10 digits whatever b1: three CTAs per SM at C5.  Measured
+    // (gpu_r3em.sh, C5 RBM-r emit): 4 CTAs/SM 10.5 ms, 3 CTAs 7.36, 2 CTAs
+    // 7.47, 1 CTA 10.9 -- more concurrent random gathers than three CTAs'
+    // worth slow the gathers down
+    size_t esm = emit_smem_bytes<T, D, LINK>();
+    if (const char* e = std::getenv("RBM_EMIT_SMEM"))  // experiment knob: pad to limit CTAs per SM
+      esm = std::max<size_t>(esm, std::min<size_t>((size_t)std::atol(e), 200 * 1024));
     rbmr_emit_kernel<T, D, KK, INTEG, LINK>
-        <<<(unsigned)((c.nbatch + bpc - 1) / bpc), EMIT_BLOCK, emit_smem_bytes<T, D, LINK>(), s>>>(
+        <<<(unsigned)((c.nbatch + bpc - 1) / bpc), EMIT_BLOCK, esm, s>>>(
             P, c.nbatch, xa, c.js, c.rinc[0], c.cur1[0], L.cap1);
     const unsigned char* fin = c.rinc[0];
     const uint32_t* fcnt = c.cur1[0];

@@ -2461,8 +2461,10 @@ static __global__ void gather_aos_part_kernel(const T* __restrict__ xa, uint64_t
 constexpr int EMIT_BLOCK = 256;
 constexpr uint32_t EMIT_TS = 2048;  // slots per emit CTA
 
-template <typename T, int D, bool LINK> __host__ __device__ constexpr size_t emit_smem_bytes() {
-  return (size_t)EMIT_TS * IncOrLink<T, D, LINK>::RS + (size_t)EMIT_TS * (4 + 2) + (3 * 1024 + 64) * 4;
+// staged records, ranks, staging index, and hist / gbase / off over the 2^b1
+// output digits (sized by b1: four CTAs per SM at C5)
+template <typename T, int D, bool LINK> __host__ __device__ constexpr size_t emit_smem_bytes(uint32_t b1 = 10) {
+  return (size_t)EMIT_TS * IncOrLink<T, D, LINK>::RS + (size_t)EMIT_TS * (4 + 2) + (3 * (1u << b1) + 64) * 4;
 }
 
 // LINK (the sequential RBM-r'): the records are {j_s, s} only (no gathers)
@@ -2476,10 +2478,10 @@ static __global__ void __launch_bounds__(EMIT_BLOCK) rbmr_emit_kernel(const __gr
   unsigned char* stg = smem_raw;                                            // EMIT_TS records
   uint32_t* rk = reinterpret_cast<uint32_t*>(stg + (size_t)EMIT_TS * IL::RS);  // digit << 16 | rank
   uint16_t* inv = reinterpret_cast<uint16_t*>(rk + EMIT_TS);
-  uint32_t* hist = reinterpret_cast<uint32_t*>(inv + EMIT_TS);             // 1024
-  uint32_t* gbase = hist + 1024;                                           // 1024
-  uint32_t* off = gbase + 1024;                                            // 1024
-  uint32_t* wsum = off + 1024;                                             // 64
+  uint32_t* hist = reinterpret_cast<uint32_t*>(inv + EMIT_TS);             // 2^b1
+  uint32_t* gbase = hist + (1u << P.b1);                                   // 2^b1
+  uint32_t* off = gbase + (1u << P.b1);                                    // 2^b1
+  uint32_t* wsum = off + (1u << P.b1);                                     // 64
   const uint32_t m = (uint32_t)*P.step;
   const uint32_t p = P.p;
   const uint32_t bpc = EMIT_TS / p;  // batches per CTA
