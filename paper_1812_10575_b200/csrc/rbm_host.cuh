@@ -872,8 +872,13 @@ struct Engine final : EngineBase {
     cudaMemsetAsync(c.rexpect, 0xff, c.nslots * 4, s);  // SEQ_FREE: a particle's first slot waits for nobody
     partition_slots<true, LinkRT>(c, s, c.rexpect);
     c.mark(s);
-    rbmr_seq_dep_kernel<T, D, KK, INTEG><<<(unsigned)num_sms * 16, 128, 0, s>>>(c.P, c.nbatch, c.js, c.rexpect, xa,
-                                                                              c.rticket);
+    // CTAs of 4 warps per SM (experiment knob RBM_SEQ_CTAS).  Measured at C5
+    // (gpu_r3sq.sh): 16/12/8/6/4/2 CTAs per SM = 14.12/14.12/13.49/13.23/
+    // 13.06/13.79 ms -- fewer random sector accesses in flight go faster
+    unsigned per_sm = 4;
+    if (const char* e = std::getenv("RBM_SEQ_CTAS")) per_sm = (unsigned)std::max(1, std::min(16, std::atoi(e)));
+    rbmr_seq_dep_kernel<T, D, KK, INTEG><<<(unsigned)num_sms * per_sm, 128, 0, s>>>(c.P, c.nbatch, c.js, c.rexpect, xa,
+                                                                                  c.rticket);
     c.mark(s);
     advance_kernel<<<1, 1, 0, s>>>(c.step_dev);
     c.mark(s);
