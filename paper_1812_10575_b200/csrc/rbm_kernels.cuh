@@ -2698,32 +2698,26 @@ static __global__ void __launch_bounds__(256, 4) rbmr_bucket_apply_kernel(const 
   }
   __syncthreads();
   {
-    // every particle of the range with slots: ascending slot order
-    for (uint32_t jl = threadIdx.x; jl < nid; jl += BLOCK) {
-      const uint32_t c = pc[jl];
-      if (c == 0) continue;
-      constexpr uint32_t MAXL = 32;
-      uint32_t ee[MAXL], ss[MAXL];
-      const uint32_t kk = c < MAXL ? c : MAXL;
-      if (c > MAXL) {
-        atomicExch(P.capacity_err, 1u);
-        continue;  // flagged; no slot of the particle waits (the sweep cannot hang)
+    // each slot record ranks itself among its particle's slots by global slot
+    // index (the group's records sit at ix[po[j] .. po[j] + c) in arrival
+    // order); the a-th slot, a >= 1, gets expect[s] = tag_j + a.  expect[] was
+    // preset to SEQ_FREE, which the first slot keeps
+    constexpr uint32_t MAXL = 32;
+    auto slot_of = [&](uint32_t e) { return reinterpret_cast<const uint32_t*>(rs + (size_t)e * IL::RS)[1]; };
+#pragma unroll
+    for (int k = 0; k < AI; ++k) {
+      const uint32_t e = k * BLOCK + threadIdx.x;
+      if (e >= n) continue;
+      const uint32_t jl = myjl[k], c = pc[jl];
+      if (c < 2) continue;
+      if (c > MAXL) {  // flagged; no slot of the particle waits (the sweep cannot hang)
+        if (myr[k] == 0) atomicExch(P.capacity_err, 1u);
+        continue;
       }
-      for (uint32_t a = 0; a < kk; ++a) {
-        ee[a] = ix[po[jl] + a];
-        ss[a] = reinterpret_cast<const uint32_t*>(rs + (size_t)ee[a] * IL::RS)[1];
-      }
-      for (uint32_t a = 1; a < kk; ++a) {  // insertion sort by global slot
-        const uint32_t v = ss[a], w0 = ee[a];
-        uint32_t w = a;
-        while (w > 0 && ss[w - 1] > v) { ss[w] = ss[w - 1]; ee[w] = ee[w - 1]; --w; }
-        ss[w] = v;
-        ee[w] = w0;
-      }
-      if (kk > 1) {  // expect[] was preset to SEQ_FREE: only the later slots are written
-        const uint32_t t0 = *seq_tag(xa, (uint32_t)(j0 + jl));
-        for (uint32_t a = 1; a < kk; ++a) expect[ss[a]] = t0 + a;
-      }
+      const uint32_t se = slot_of(e), base = po[jl];
+      uint32_t r = 0;
+      for (uint32_t q = 0; q < c; ++q) r += (slot_of(ix[base + q]) < se) ? 1u : 0u;
+      if (r > 0) expect[se] = *seq_tag(xa, (uint32_t)(j0 + jl)) + r;
     }
   }
 }
