@@ -494,6 +494,7 @@ struct Engine final : EngineBase {
   static constexpr int MINB = (RL::RS <= 16) ? 4 : 2;  // CTAs per SM the bucket kernel is register-budgeted for
   size_t pr_smem = 0, sp_smem = 0, bk_smem = 0, rs_smem = 0;
   bool pair_mode = false;
+  int bmode = MODE_GROUP;  // bucket kernel MODE: pair, runtime group, or a compile-time group size (fp32)
   int num_sms = 148;
 
   State<T, D> st(rbm_ctx& c, int b) { return State<T, D>{c.recbuf[b], c.skey[b]}; }
@@ -522,6 +523,12 @@ struct Engine final : EngineBase {
     }
     rs_smem = resident_smem_bytes<T, D>(c.L.cap);
     pair_mode = c.cfg.p == 2;
+    {
+      uint32_t g = 0;
+      if (c.cfg.p <= 32) { g = 1; while (g < c.cfg.p) g <<= 1; }
+      bmode = pair_mode ? MODE_PAIR : MODE_GROUP;
+      if (std::is_same<T, float>::value && !pair_mode && (g == 4 || g == 8 || g == 32)) bmode = (int)g;
+    }
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, c.device);
     if (num_sms <= 0) num_sms = 148;
     auto chk = [&](cudaError_t e, const char* what) -> rbm_status {
@@ -536,11 +543,7 @@ struct Engine final : EngineBase {
     if (c.cfg.scheme == RBM_SCHEME_RBMR && !is_partitioned(c.cfg)) return setup_rbmr<false, IncRT<T, D>>(c);
     if (c.cfg.scheme == RBM_SCHEME_RBMR_SEQ) return setup_rbmr<true, LinkRT>(c);
     if (c.L.B > 0) {
-      if ((s = chk(pair_mode ? cudaFuncSetAttribute(bucket_kernel<T, D, KK, INTEG, MODE_PAIR, MINB>,
-                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bk_smem)
-                             : cudaFuncSetAttribute(bucket_kernel<T, D, KK, INTEG, MODE_GROUP, MINB>,
-                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bk_smem),
-                   "smem attr bucket"))) return s;
+      if ((s = chk(bucket_attr(), "smem attr bucket"))) return s;
     } else if (rs_smem <= 227 * 1024) {
       if ((s = chk(cudaFuncSetAttribute(resident_kernel<T, D, KK, INTEG, 256>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem),
@@ -654,12 +657,31 @@ struct Engine final : EngineBase {
   void fused(rbm_ctx& c, cudaStream_t s, State<T, D> in, const OutDst<T, D>& out, uint32_t ocap,
              uint32_t* cur_next) {
     Nvtx r_("bucket_step");
-    if (pair_mode)
-      bucket_kernel<T, D, KK, INTEG, MODE_PAIR, MINB>
+    auto go = [&](auto mode) {
+      bucket_kernel<T, D, KK, INTEG, decltype(mode)::value, MINB>
           <<<c.L.nbuckets, BUCKET_BLOCK, bk_smem, s>>>(c.P, in, c.L.cap2, c.S, out, ocap, cur_next);
-    else
-      bucket_kernel<T, D, KK, INTEG, MODE_GROUP, MINB>
-          <<<c.L.nbuckets, BUCKET_BLOCK, bk_smem, s>>>(c.P, in, c.L.cap2, c.S, out, ocap, cur_next);
+    };
+    if (bmode == MODE_PAIR) { go(std::integral_constant<int, MODE_PAIR>{}); return; }
+    if constexpr (std::is_same<T, float>::value) {
+      if (bmode == 4) { go(std::integral_constant<int, 4>{}); return; }
+      if (bmode == 8) { go(std::integral_constant<int, 8>{}); return; }
+      if (bmode == 32) { go(std::integral_constant<int, 32>{}); return; }
+    }
+    go(std::integral_constant<int, MODE_GROUP>{});
+  }
+
+  cudaError_t bucket_attr() {
+    auto at = [&](auto mode) {
+      return cudaFuncSetAttribute(bucket_kernel<T, D, KK, INTEG, decltype(mode)::value, MINB>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bk_smem);
+    };
+    if (bmode == MODE_PAIR) return at(std::integral_constant<int, MODE_PAIR>{});
+    if constexpr (std::is_same<T, float>::value) {
+      if (bmode == 4) return at(std::integral_constant<int, 4>{});
+      if (bmode == 8) return at(std::integral_constant<int, 8>{});
+      if (bmode == 32) return at(std::integral_constant<int, 32>{});
+    }
+    return at(std::integral_constant<int, MODE_GROUP>{});
   }
 
   void prologue(rbm_ctx& c, cudaStream_t s, State<T, D> src, const OutDst<T, D>& dst, uint32_t* cur,

@@ -1091,6 +1091,9 @@ __device__ __noinline__ void big_bucket(const DevParams& P, State<T, D> src, con
 //       index, written coalesced (one vector store per record).
 // Members of batches that straddle the bucket's ends are written unchanged to
 // their sorted places in the own gapped range (the straddle kernel steps them).
+// MODE_PAIR (p = 2), MODE_GROUP (lane groups of the runtime size P.group), or
+// a compile-time lane-group size MODE in {4, 8, 32} (the fp32 group kernels:
+// the partner loop unrolled, shuffle widths and lane arithmetic constant)
 constexpr int MODE_PAIR = 0, MODE_GROUP = 1;
 #ifndef RBM_BUCKET_BLOCK  // design-experiment builds override these (build.py -D...)
 #define RBM_BUCKET_BLOCK 256
@@ -1313,7 +1316,7 @@ __device__ __forceinline__ void bucket_body(const DevParams& P, State<T, D> src,
       tb[e] = 0xffffffffu;
     }
     RBM_PROF(P, 5);
-    const uint32_t G = P.group;
+    const uint32_t G = (MODE > MODE_GROUP) ? (uint32_t)MODE : P.group;
     if (G != 0) {
       // lane groups: batches with sz <= G; each pair evaluated once in the
       // canonical rotation order (batch_force), the partner's term by shuffle
@@ -1338,6 +1341,7 @@ __device__ __forceinline__ void bucket_body(const DevParams& P, State<T, D> src,
           T f[D];
 #pragma unroll
           for (int c = 0; c < D; ++c) f[c] = T(0);
+#pragma unroll
           for (uint32_t o = 1; o <= G / 2; ++o) {
             const uint32_t jp = (li + o) & (G - 1), jm = (li - o) & (G - 1);
             T xj[D], t[D];
