@@ -549,16 +549,20 @@ template <typename T, int D> struct IncL {
   static constexpr int RS = RS0 <= 8 ? 8 : (RS0 + 15) / 16 * 16;
   static constexpr int NW = RS / 4;
 };
-// Order-independent sum of a particle's increments (reading D:8): for each
-// coordinate, every increment is converted exactly to a fixed-point integer at
-// the scale of the largest exponent among them (G guard bits below that
-// increment's ulp; bits further down are truncated), the integers are summed
-// exactly in int64 (so the order of the increments does not matter), and the
-// sum is added to x with one rounding.  One GPU (shared-memory atomics) and
-// the partitioned path (per-particle loop) compute the same integers.
+// Order-independent sum of a particle's increments (reading D:8): every
+// increment coordinate is converted exactly to a fixed-point integer at the
+// scale of the particle's largest increment exponent E (over all its
+// increments and coordinates; G guard bits below the ulp of that scale, bits
+// further down truncated), the integers are summed exactly (so the order of
+// the increments does not matter), and each coordinate's sum is added to x
+// with one rounding.  On one GPU the sum is formed by 32-bit shared-memory
+// atomics on NCH chunks of CB bits of q + BIAS (64-bit shared atomics are CAS
+// loops on sm_100a); the partitioned path sums the same integers in int64.
 template <typename T> struct Fx;
 template <> struct Fx<float> {
-  static constexpr int G = 28;  // |acc| <= c 2^52: int64 for c < 2^11 increments
+  static constexpr int G = 16;                     // |q| < 2^40
+  static constexpr int NCH = 2, CB = 21;           // q + 2^40 in two chunks: u32 sums of < 2^11 increments
+  static constexpr long long BIAS = 1ll << 40;
   __device__ __forceinline__ static uint32_t ex(float v) {
     const uint32_t e = (__float_as_uint(v) >> 23) & 0xffu;
     return e ? e : 1u;
@@ -572,11 +576,15 @@ template <> struct Fx<float> {
   }
   __device__ __forceinline__ static float add(float x, long long acc, uint32_t E) {
     if (E >= 255u) return __int_as_float(0x7fc00000);  // a non-finite increment: flagged downstream
-    return (float)((double)x + ldexp((double)acc, (int)E - 150 - G));
+    // 2^(E - 150 - G) is a normal double for every E in [1, 254]: exact scaling
+    const double sc = __longlong_as_double((long long)(E - 150 - G + 1023) << 52);
+    return (float)((double)x + (double)acc * sc);
   }
 };
 template <> struct Fx<double> {
-  static constexpr int G = 4;  // |acc| <= c 2^57: int64 for c < 64 increments
+  static constexpr int G = 4;                      // |q| < 2^57: int64 sums of < 64 increments
+  static constexpr int NCH = 3, CB = 20;           // q + 2^57 in three chunks: u32 sums of < 2^12 increments
+  static constexpr long long BIAS = 1ll << 57;
   __device__ __forceinline__ static uint32_t ex(double v) {
     const uint32_t e = (uint32_t)(((unsigned long long)__double_as_longlong(v) >> 52) & 0x7ffu);
     return e ? e : 1u;
@@ -591,7 +599,9 @@ template <> struct Fx<double> {
   }
   __device__ __forceinline__ static double add(double x, long long acc, uint32_t E) {
     if (E >= 2047u) return __longlong_as_double(0x7ff8000000000000ll);
-    return x + ldexp((double)acc, (int)E - 1075 - G);
+    const int ex2 = (int)E - 1075 - G;  // >= -1078: below the normal range for the smallest E
+    return x + (ex2 >= -1022 ? (double)acc * __longlong_as_double((long long)(ex2 + 1023) << 52)
+                             : ldexp((double)acc, ex2));
   }
 };
 template <typename T, int D> struct IncRT {
@@ -2406,10 +2416,12 @@ static __global__ void rbmr_apply_part_kernel(const __grid_constant__ DevParams 
     };
     T x[D];
     load4<T, D>(xa, (uint32_t)jl, x);
+    uint32_t E = 0;  // order-independent fixed-point sums (Fx, D:8), as on one GPU
+    for (uint32_t a = 0; a < k; ++a)
 #pragma unroll
-    for (int cc = 0; cc < D; ++cc) {  // order-independent fixed-point sum (Fx, D:8), as on one GPU
-      uint32_t E = 0;
-      for (uint32_t a = 0; a < k; ++a) E = max(E, Fx<T>::ex(dd(ix[a])[cc]));
+      for (int cc = 0; cc < D; ++cc) E = max(E, Fx<T>::ex(dd(ix[a])[cc]));
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) {
       long long acc = 0;
       for (uint32_t a = 0; a < k; ++a) acc += Fx<T>::q(dd(ix[a])[cc], E);
       x[cc] = Fx<T>::add(x[cc], acc, E);
@@ -2566,7 +2578,7 @@ static __global__ void __launch_bounds__(EMIT_BLOCK) rbmr_emit_kernel(const __gr
 
 template <typename T, int D, bool LINK> __host__ __device__ constexpr size_t rapply_smem_bytes(uint32_t cap, uint32_t W) {
   return LINK ? (size_t)(cap + 8) * IncOrLink<T, D, LINK>::RS + (size_t)cap * 4 + (size_t)W * 8 + 64 * 4 + 16
-              : (size_t)W * D * (8 + 4) + 16;  // Jacobi: acc (int64) and emax (u32) per particle and coordinate
+              : (size_t)W * (2 + Fx<T>::NCH * D) * 4 + 16;  // Jacobi: exponent, count, chunk sums per particle
 }
 
 // apply: final bucket b = the particle ids [b W, (b+1) W); n = cnt[b] records.
@@ -2590,15 +2602,17 @@ static __global__ void __launch_bounds__(256, 4) rbmr_bucket_apply_kernel(const 
   constexpr int RMAX = 4;  // W <= 1024 particles in registers (larger W: loaded in the loop)
   if constexpr (!LINK) {
     // ---- Jacobi RBM-r: order-independent fixed-point sums (Fx, reading D:8)
-    long long* acc = reinterpret_cast<long long*>(smem_raw);              // [W][D]
-    uint32_t* emax = reinterpret_cast<uint32_t*>(acc + (size_t)W * D);    // [W][D]; 0: no increment
+    using F = Fx<T>;
+    uint32_t* emax = reinterpret_cast<uint32_t*>(smem_raw);  // [W]: common exponent; 0: no increment
+    uint32_t* cntp = emax + W;                               // [W]: increments per particle
+    uint32_t* ch = cntp + W;                                 // [NCH][W][D]: chunk sums of q + BIAS
     T xv[RMAX][D];
 #pragma unroll
     for (int r = 0; r < RMAX; ++r) {  // the id range's positions, loaded before the increments
       const uint32_t jl = threadIdx.x + r * BLOCK;
       if (jl < nid) load4<T, D>(xa, (uint32_t)(j0 + jl), xv[r]);
     }
-    for (uint32_t i = threadIdx.x; i < W * D; i += BLOCK) { acc[i] = 0; emax[i] = 0; }
+    for (uint32_t i = threadIdx.x; i < W * (2 + F::NCH * D); i += BLOCK) emax[i] = 0;
     if (n > cap || cap > 8u * BLOCK) {  // cannot happen at the layout's 12-sigma capacity (<= 2048): flagged
       if (threadIdx.x == 0) atomicExch(P.capacity_err, 1u);
       return;
@@ -2618,27 +2632,42 @@ static __global__ void __launch_bounds__(256, 4) rbmr_bucket_apply_kernel(const 
         for (int cc = 0; cc < D; ++cc) from_w(dv[k][cc], w + IncL<T, D>::XW + cc * (int)(sizeof(T) / 4));
       }
     }
-    __syncthreads();  // acc / emax zeroed
+    __syncthreads();  // counters zeroed
 #pragma unroll
     for (int k = 0; k < AI; ++k)
-      if (k * BLOCK + threadIdx.x < n)
+      if (k * BLOCK + threadIdx.x < n) {
+        uint32_t e = 0;
 #pragma unroll
-        for (int cc = 0; cc < D; ++cc) atomicMax(&emax[jl_k[k] * D + cc], Fx<T>::ex(dv[k][cc]));
+        for (int cc = 0; cc < D; ++cc) e = max(e, F::ex(dv[k][cc]));
+        atomicMax(&emax[jl_k[k]], e);
+        atomicAdd(&cntp[jl_k[k]], 1u);
+      }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < AI; ++k)
-      if (k * BLOCK + threadIdx.x < n)
+      if (k * BLOCK + threadIdx.x < n) {
+        const uint32_t E = emax[jl_k[k]];
 #pragma unroll
         for (int cc = 0; cc < D; ++cc) {
-          const uint32_t i = jl_k[k] * D + cc;
-          atomicAdd(reinterpret_cast<unsigned long long*>(&acc[i]),
-                    (unsigned long long)Fx<T>::q(dv[k][cc], emax[i]));
+          const unsigned long long qb = (unsigned long long)(F::q(dv[k][cc], E) + F::BIAS);
+#pragma unroll
+          for (int h = 0; h < F::NCH; ++h)
+            atomicAdd(&ch[((size_t)h * W + jl_k[k]) * D + cc],
+                      (uint32_t)((qb >> (F::CB * h)) & ((h + 1 < F::NCH) ? ((1ull << F::CB) - 1ull) : ~0ull)));
         }
+      }
     __syncthreads();
     auto particle = [&](uint32_t jl, T (&x)[D]) {
-      if (emax[jl * D] == 0u) return;  // no increment
+      const uint32_t c = cntp[jl];
+      if (c == 0u) return;  // no increment
+      const uint32_t E = emax[jl];
 #pragma unroll
-      for (int cc = 0; cc < D; ++cc) x[cc] = Fx<T>::add(x[cc], acc[jl * D + cc], emax[jl * D + cc]);
+      for (int cc = 0; cc < D; ++cc) {
+        long long acc = -(long long)c * F::BIAS;
+#pragma unroll
+        for (int h = 0; h < F::NCH; ++h) acc += (long long)ch[((size_t)h * W + jl) * D + cc] << (F::CB * h);
+        x[cc] = F::add(x[cc], acc, E);
+      }
       if (P.constraint == 1) renormalise<T, D>(x);
       check_finite<T, D>(x, P, (uint32_t)(j0 + jl), m);
       store4<T, D>(xa, (uint32_t)(j0 + jl), x);
