@@ -567,6 +567,13 @@ rbm_status rbm_debug_slots(rbm_ctx* c, uint32_t* slots_out) {
   if (c->cfg.scheme == RBM_SCHEME_RBM1) return fail(c, RBM_ERR_STATE, "not an RBM-r context");
   if (!slots_out) return fail(c, RBM_ERR_INVALID_ARG, "slots_out is NULL");
   const uint64_t ns = is_partitioned(c->cfg) ? (c->rp.bb1 - c->rp.bb0) * c->cfg.p : c->nslots;  // own batches' slots
+  if (c->cfg.scheme == RBM_SCHEME_RBMR && !is_partitioned(c->cfg)) {
+    // the one-GPU Jacobi sweep does not store its draws: recompute those of the last step
+    if (c->step == c->cfg.step0) return fail(c, RBM_ERR_STATE, "no step has run yet");
+    c->eng->rbmr_slots(*c, (uint32_t)(c->step - 1), slots_out, c->stream);
+    CU(cudaGetLastError());
+    return RBM_OK;
+  }
   CU(cudaMemcpyAsync(slots_out, c->js, ns * 4, cudaMemcpyDeviceToDevice, c->stream));
   return RBM_OK;
 }

@@ -449,7 +449,7 @@ inline void carve(rbm_ctx& c, Workspace& ws) {
       c.rinc[0] = ws.take<unsigned char>((size_t)(1u << c.L.b1) * c.L.cap1 * irs);
       if (c.L.b2) c.rinc[1] = ws.take<unsigned char>((size_t)c.L.nbuckets * c.L.cap2 * irs);
     }
-    c.js = ws.take<uint32_t>(c.nslots);
+    if (k.scheme == RBM_SCHEME_RBMR_SEQ) c.js = ws.take<uint32_t>(c.nslots);  // the Jacobi sweep keeps no draws
     c.rxa = ws.take<unsigned char>(n * 4 * es);
     if (k.scheme == RBM_SCHEME_RBMR_SEQ) {  // slot chains and flags of the sequential sweep
       c.rexpect = ws.take<uint32_t>(c.nslots);
@@ -485,6 +485,8 @@ struct EngineBase {
   virtual uint64_t gather_local(rbm_ctx& c, uint32_t* ids, void* x, cudaStream_t s) = 0;
   // RBM-r on a partitioned system: phase k = 1..4 of the step (exchange k-1 follows phase k)
   virtual void rbmr_part_phase(rbm_ctx& c, cudaStream_t s, int k) = 0;
+  // the slot draws of step m of the one-GPU Jacobi sweep, recomputed (test hook)
+  virtual void rbmr_slots(rbm_ctx& c, uint32_t m, uint32_t* out, cudaStream_t s) = 0;
 };
 
 template <typename T, int D, int KK, int INTEG>
@@ -925,7 +927,7 @@ struct Engine final : EngineBase {
       esm = std::max<size_t>(esm, std::min<size_t>((size_t)std::atol(e), 200 * 1024));
     rbmr_emit_kernel<T, D, KK, INTEG, LINK>
         <<<(unsigned)((c.nbatch + bpc - 1) / bpc), EMIT_BLOCK, esm, s>>>(
-            P, c.nbatch, xa, c.js, c.rinc[0], c.cur1[0], L.cap1);
+            P, c.nbatch, xa, LINK ? c.js : nullptr, c.rinc[0], c.cur1[0], L.cap1);
     const unsigned char* fin = c.rinc[0];
     const uint32_t* fcnt = c.cur1[0];
     if (L.b2) {
@@ -941,6 +943,10 @@ struct Engine final : EngineBase {
     c.mark(s);
     rbmr_bucket_apply_kernel<T, D, LINK><<<L.nbuckets, 256, rapply_smem_bytes<T, D, LINK>(L.cap2, W), s>>>(
         P, fin, L.cap2, fcnt, W, xa, expect);
+  }
+
+  void rbmr_slots(rbm_ctx& c, uint32_t m, uint32_t* out, cudaStream_t s) override {
+    rbmr_slots_kernel<KK><<<grid_for(c.nbatch, 128), 128, 0, s>>>(c.P, c.nbatch, m, out);
   }
 
   // RBM-r Jacobi sweep (reading D:8): increments routed to their particles

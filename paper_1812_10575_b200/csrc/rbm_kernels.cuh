@@ -2532,7 +2532,7 @@ static __global__ void __launch_bounds__(EMIT_BLOCK) rbmr_emit_kernel(const __gr
       for (uint32_t l = 0; l < (uint32_t)PM; ++l) {
         if (l >= p) break;
         const uint32_t e = lb * p + l;
-        js[s0 + l] = jj[l];
+        if (js) js[s0 + l] = jj[l];  // RBM-r' only (its sweep reads them); the Jacobi sweep recomputes on demand
         uint32_t w[IL::NW];
 #pragma unroll
         for (int k = 0; k < IL::NW; ++k) w[k] = 0u;
@@ -2573,6 +2573,26 @@ static __global__ void __launch_bounds__(EMIT_BLOCK) rbmr_emit_kernel(const __gr
     uint32_t w[IL::NW];
     ld_words<IL::NW>(stg + (size_t)e * IL::RS, w);
     st_words<IL::NW>(dst + ((size_t)dg * dcap + slot) * IL::RS, w);
+  }
+}
+
+// the slot draws j_s of step m (test hook rbm_debug_slots of the one-GPU
+// Jacobi sweep, whose emit kernel does not store them): the emit's draws, one
+// thread per batch
+template <int KK>
+static __global__ void rbmr_slots_kernel(const __grid_constant__ DevParams P, uint64_t nbatch, uint32_t m,
+                                         uint32_t* __restrict__ js) {
+  const uint32_t p = P.p;
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nbatch;
+       b += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s0 = b * p;
+    uint32_t jj[64];
+    if (KK == KK_ADJ && P.adj_edges) {
+      adj_edge_draw(P, s0, m, jj[0], jj[1]);
+    } else {
+      for (uint32_t l = 0; l < p; ++l) jj[l] = rbmr_draw(P, m, s0 + l, jj, l);
+    }
+    for (uint32_t l = 0; l < p; ++l) js[s0 + l] = jj[l];
   }
 }
 
