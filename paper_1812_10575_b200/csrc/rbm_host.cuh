@@ -493,7 +493,7 @@ template <typename T, int D, int KK, int INTEG>
 struct Engine final : EngineBase {
   using RL = RecL<T, D>;
   static constexpr int PR_BLOCK = 256;
-  static constexpr int MINB = (RL::RS <= 16) ? 4 : 2;  // CTAs per SM the bucket kernel is register-budgeted for
+  static constexpr int MINB = ((RL::RS <= 16) ? 4 : 2) * (BUCKET_BLOCK < 256 ? 256 / BUCKET_BLOCK : 1);  // CTAs per SM the bucket kernel is register-budgeted for
   size_t pr_smem = 0, sp_smem = 0, bk_smem = 0, rs_smem = 0;
   bool pair_mode = false;
   int bmode = MODE_GROUP;  // bucket kernel MODE: pair, runtime group, or a compile-time group size (fp32)
