@@ -58,7 +58,10 @@ struct Layout {
   uint32_t cap2 = 0;     // gapped capacity of a final bucket
   uint64_t slots = 0;    // elements per state buffer: max(N, 2^b1 cap1, 2^B cap2)
 };
-constexpr uint32_t FUSED_CAP_MAX = 4096;  // largest per-bucket smem capacity (u16 indices)
+#ifndef RBM_FUSED_CAP_MAX  // design-experiment builds override this (build.py -D...)
+#define RBM_FUSED_CAP_MAX 4096
+#endif
+constexpr uint32_t FUSED_CAP_MAX = RBM_FUSED_CAP_MAX;  // largest per-bucket smem capacity (u16 indices)
 
 // bytes of one state record and whether it carries the shuffle key (RecL)
 inline uint32_t rec_bytes(const rbm_config& c) {
@@ -222,7 +225,7 @@ inline Layout choose_layout(const rbm_config& c) {
     // target mean bucket size (tuning knob RBM_BUCKET_TARGET, default 2048)
     double target = 2048.0;
     if (const char* e = std::getenv("RBM_BUCKET_TARGET")) target = std::atof(e);
-    if (!(target >= 64.0 && target <= 2048.0)) target = 2048.0;
+    if (!(target >= 64.0 && target <= (double)(FUSED_CAP_MAX / 2))) target = 2048.0;
     L.B = ceil_log2((double)n / target);
     if (L.B < 2) L.B = 2;
     if (part && L.B < L.g + 2) L.B = L.g + 2;  // >= 4 final buckets per rank, two passes
@@ -493,7 +496,8 @@ template <typename T, int D, int KK, int INTEG>
 struct Engine final : EngineBase {
   using RL = RecL<T, D>;
   static constexpr int PR_BLOCK = 256;
-  static constexpr int MINB = ((RL::RS <= 16) ? 4 : 2) * (BUCKET_BLOCK < 256 ? 256 / BUCKET_BLOCK : 1);  // CTAs per SM the bucket kernel is register-budgeted for
+  // CTAs per SM the bucket kernel is register-budgeted for (1024 / 512 threads per SM)
+  static constexpr int MINB = (((RL::RS <= 16) ? 4 : 2) * 256 / BUCKET_BLOCK) > 0 ? ((RL::RS <= 16) ? 4 : 2) * 256 / BUCKET_BLOCK : 1;
   size_t pr_smem = 0, sp_smem = 0, bk_smem = 0, rs_smem = 0;
   bool pair_mode = false;
   int bmode = MODE_GROUP;  // bucket kernel MODE: pair, runtime group, or a compile-time group size (fp32)

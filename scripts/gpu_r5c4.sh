@@ -16,5 +16,5 @@ cap() {  # name, kernel regex, skip, count, bench args...
 cap c4 "split_kernel|bucket_kernel" 4 2 --workload C4
 cap c5p8 "bucket_kernel" 2 1 --p 8 --n 33554432
 cap rbmr "rbmr_emit_kernel|rbmr_bucket_apply_kernel" 4 2 --scheme rbmr --n 33554432
-rm -f $O/*.ncu-rep.tmp
+rm -f $O/*.ncu-rep $O/*.ncu-rep.tmp
 echo done
