@@ -385,7 +385,7 @@ def test_c2_configured_size(R, O):
 def test_full_size_sampled(R, O, which):
     """BASELINE.json sizes in the bench launch configuration: the whole
     permutation is checked by properties (partition + (key,id) order with the
-    oracle's keys), and 50,000 sampled batches (~25 of them straddling a final
+    oracle's keys), and 200,000 sampled batches (~100 of them straddling a final
     bucket's end at C5) plus the first and last against the oracle's batch update,
     at step 0 (first-step prologue) and step 1 (the steady-state path the
     bench times: pass-2 split of the carried partition, then the bucket step)."""
@@ -407,7 +407,7 @@ def test_full_size_sampled(R, O, which):
         k = keys[order].astype(np.uint64) << np.uint64(32) | order.astype(np.uint64)
         assert np.all(k[1:] > k[:-1])
         del k, keys
-        picks = np.concatenate([rng.choice(n // p, 50_000, replace=False), [0, n // p - 1]])
+        picks = np.concatenate([rng.choice(n // p, 200_000, replace=False), [0, n // p - 1]])
         for b in picks:
             ids = order[b * p:(b + 1) * p]
             want = O.batch_update(c, m, ids, x0[ids])

@@ -147,3 +147,25 @@ def test_rbmr_widest_partition_layout(R, scheme, monkeypatch):
         s.sync()
         s.close()
     assert torch.equal(out[0], out[1])
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("scheme", ["rbmr", "rbmr_seq"])
+def test_rbmr_two_pass_layout_full_state(R, O, scheme, dtype):
+    """C5 physics at N = 4,194,319: the slot partition by particle index takes
+    two passes (B = 13 > 10: pass-2 split of the increment / link records, then
+    the per-bucket apply / the sweep's chains) -- the layout the C5 RBM-r and
+    RBM-r' bench lines time.  Slot draws bit-exact and every particle against
+    the oracle (Alg. 2; Jacobi form D:8) at two consecutive
+    steps."""
+    c = dict(RI.c5_coulomb_reg(n=4_194_319, scheme=scheme), dtype=dtype, seed=9)
+    s = R.RBM(c)
+    assert s.layout[0] > 10 and s.layout[1] == 2
+    step = O.rbmr_step if scheme == "rbmr" else O.rbmr_seq_step
+    tol = 1e-12 if dtype == "f64" else 1e-4
+    for m in (0, 1):
+        x0 = s.gather(host=True).astype(np.float64)
+        s.step()
+        assert np.array_equal(s.slots(), O.rbmr_slots(c, m))
+        assert E(s.gather(host=True), step(c, x0, m)) <= tol
+    s.close()
