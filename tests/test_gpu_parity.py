@@ -349,6 +349,26 @@ def test_two_pass_full_state_one_step(R, O, dtype, p):
     s.close()
 
 
+@pytest.mark.parametrize("which", ["C5p2", "C5p8", "C4"])
+def test_two_pass_full_state_large(R, O, which):
+    """Every particle against the oracle at one eighth of the bench size, fp32,
+    in the layout family the bench times: C5 physics at N = 33,554,399
+    (B = 14, two passes of 7 bits; p = 2 and 8) and C4 at N = 12,500,003
+    (B = 13), at the prologue step and the steady-state step after it."""
+    if which == "C4":
+        c = RI.c4_aggregation(n=12_500_003)
+    else:
+        c = RI.c5_coulomb_reg(n=33_554_399, p=8 if which == "C5p8" else 2)
+    s = R.RBM(c)
+    assert s.layout[:2] == ((13, 2) if which == "C4" else (14, 2))
+    for m in (0, 1):
+        x0 = s.gather(host=True).astype(np.float64)
+        s.step()
+        g = s.gather(host=True)
+        assert E(g, O.rbm1_step(c, x0, m)) <= 1e-4, m
+    s.close()
+
+
 def test_two_pass_100_steps_fp64(R, O):
     """100 steps in fp64 on the 2-pass layout (N = 2,200,013: B = 11), regularised
     Coulomb (C5 physics), p = 2, against the oracle's 100-step run."""

@@ -169,3 +169,20 @@ def test_rbmr_two_pass_layout_full_state(R, O, scheme, dtype):
         assert np.array_equal(s.slots(), O.rbmr_slots(c, m))
         assert E(s.gather(host=True), step(c, x0, m)) <= tol
     s.close()
+
+
+@pytest.mark.parametrize("scheme", ["rbmr", "rbmr_seq"])
+def test_rbmr_full_state_large(R, O, scheme):
+    """Every particle against the oracle at one eighth of the bench size
+    (C5 physics, N = 33,554,399, fp32; slot partition B = 15, two passes):
+    slot draws bit-exact, states within the fp32 bar, at two consecutive steps."""
+    c = dict(RI.c5_coulomb_reg(n=33_554_399, scheme=scheme), seed=5)
+    s = R.RBM(c)
+    assert s.layout[0] == 15 and s.layout[1] == 2
+    step = O.rbmr_step if scheme == "rbmr" else O.rbmr_seq_step
+    for m in (0, 1):
+        x0 = s.gather(host=True).astype(np.float64)
+        s.step()
+        assert np.array_equal(s.slots(), O.rbmr_slots(c, m))
+        assert E(s.gather(host=True), step(c, x0, m)) <= 1e-4
+    s.close()
