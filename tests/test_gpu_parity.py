@@ -9,6 +9,7 @@ The oracle always starts from the GPU's own X_m (gathered), so one-step
 comparisons isolate one step.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -366,6 +367,30 @@ def test_two_pass_full_state_large(R, O, which):
         s.step()
         g = s.gather(host=True)
         assert E(g, O.rbm1_step(c, x0, m)) <= 1e-4, m
+    s.close()
+
+
+@pytest.mark.skipif(not os.environ.get("RBM_FULL_ORACLE"),
+                    reason="opt-in (RBM_FULL_ORACLE=1): ~5 min of single-threaded oracle at N = 2^28")
+def test_full_size_every_particle(R, O):
+    """The bench's own workload and launch configuration (C5: N = 2^28, p = 2,
+    fp32, B = 17): EVERY particle against the oracle's full step, at the
+    prologue step and at the steady-state step the bench times.  Opt-in because
+    the single-threaded oracle needs minutes at this size; the result of the
+    last run is recorded in profiles/r2d_summary.md."""
+    c = RI.c5_coulomb_reg()
+    s = R.RBM(c)
+    assert s.layout[:2] == (17, 2)
+    for m in (0, 1):
+        x0 = s.gather(host=True).astype(np.float64)
+        s.step()
+        g = s.gather(host=True)
+        o = O.rbm1_step(c, x0, m)
+        del x0
+        err = np.abs(g - o).max() / max(1.0, float(np.abs(o).max()))
+        print(f"full-size step {m}: E = {err:.3e}")
+        assert err <= 1e-4, m
+        del g, o
     s.close()
 
 
