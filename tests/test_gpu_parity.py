@@ -372,23 +372,31 @@ def test_two_pass_full_state_large(R, O, which):
 
 @pytest.mark.skipif(not os.environ.get("RBM_FULL_ORACLE"),
                     reason="opt-in (RBM_FULL_ORACLE=1): ~5 min of single-threaded oracle at N = 2^28")
-def test_full_size_every_particle(R, O):
-    """The bench's own workload and launch configuration (C5: N = 2^28, p = 2,
-    fp32, B = 17): EVERY particle against the oracle's full step, at the
-    prologue step and at the steady-state step the bench times.  Opt-in because
-    the single-threaded oracle needs minutes at this size; the result of the
-    last run is recorded in profiles/r2d_summary.md."""
-    c = RI.c5_coulomb_reg()
+@pytest.mark.parametrize("which", ["C5", "C4", "C5rbmr"])
+def test_full_size_every_particle(R, O, which):
+    """The bench's own workloads and launch configurations (C5: N = 2^28,
+    p = 2, fp32, B = 17; C4: N = 10^8, p = 4, fp32, B = 16; the C5 RBM-r Jacobi
+    sweep, slot partition B = 18): EVERY particle
+    against the oracle's full step, at the prologue step and at the
+    steady-state step the bench times.  Opt-in because the single-threaded
+    oracle needs minutes at these sizes; the result of the last run is
+    recorded in profiles/r2d_summary.md."""
+    c = {"C5": RI.c5_coulomb_reg, "C4": RI.c4_aggregation,
+         "C5rbmr": lambda: RI.c5_coulomb_reg(scheme="rbmr")}[which]()
     s = R.RBM(c)
-    assert s.layout[:2] == (17, 2)
+    assert s.layout[:2] == {"C5": (17, 2), "C4": (16, 2), "C5rbmr": (18, 2)}[which]
     for m in (0, 1):
         x0 = s.gather(host=True).astype(np.float64)
         s.step()
         g = s.gather(host=True)
-        o = O.rbm1_step(c, x0, m)
+        if which == "C5rbmr":  # RBM-r (Jacobi sweep): slot draws bit-exact, then the states
+            assert np.array_equal(s.slots(), O.rbmr_slots(c, m))
+            o = O.rbmr_step(c, x0, m)
+        else:
+            o = O.rbm1_step(c, x0, m)
         del x0
         err = np.abs(g - o).max() / max(1.0, float(np.abs(o).max()))
-        print(f"full-size step {m}: E = {err:.3e}")
+        print(f"full-size {which} step {m}: E = {err:.3e}")
         assert err <= 1e-4, m
         del g, o
     s.close()
